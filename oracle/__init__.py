@@ -1,0 +1,291 @@
+"""Scalar CPU oracle for the differentiable optimizer step (ctypes wrapper).
+
+TEST INFRASTRUCTURE ONLY. Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s CPU-baseline legs (``cpu_baseline`` and ``--impl reference``)
+may import this package. The product package ``paper_2211_06934_b200`` never
+imports it and shares no code with it (see ``oracle/oracle.hpp`` header for
+the formulas and their citations into PAPER.md / SPEC.md).
+
+Every function takes numpy arrays holding the exact fp32 inputs the GPU path
+sees (bf16 state as uint16 bit patterns) and returns float64 arrays.
+``prec=1`` evaluates in x87 long double.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liboracle.so")
+SOURCES = [os.path.join(_HERE, "oracle.cpp"), os.path.join(_HERE, "oracle.hpp")]
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with g++ (-O2, no fast-math, OpenMP)."""
+    newest = max(os.path.getmtime(s) for s in SOURCES)
+    if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
+        return LIB_PATH
+    cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-fopenmp",
+           "-fno-fast-math", "-o", LIB_PATH, SOURCES[0]]
+    subprocess.check_call(cmd)
+    return LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.c_void_p
+        i64 = ctypes.c_int64
+        I = ctypes.c_int
+        L.oracle_set_num_threads.argtypes = [I]
+        L.oracle_set_num_threads.restype = I
+        L.oracle_has_openmp.restype = I
+        L.oracle_adam_fwd.argtypes = [i64, i64, P, I, I, P, P, P, P, P, P]
+        L.oracle_adam_vjp.argtypes = [i64, i64, P, I, I, P, P, P, P, P, P, P, P, P, P, P, i64, P, P]
+        L.oracle_rmsprop_fwd.argtypes = [i64, P, I, I, P, P, P, P]
+        L.oracle_rmsprop_vjp.argtypes = [i64, P, I, I, P, P, P, P, P, P, P, P, i64, P, P]
+        L.oracle_sgd_fwd.argtypes = [i64, P, I, I, P, P, P, P]
+        L.oracle_sgd_vjp.argtypes = [i64, P, I, I, P, P, P, P, P, P, P, P, i64, P, P]
+        L.oracle_bf16_rne.argtypes = [i64, P, P]
+        L.oracle_sweep_quadratic.argtypes = [I, i64, i64, P, I, P, P, P, P, P, P, P, P, P]
+        L.oracle_adam_fwd_cplx.argtypes = [i64, i64] + [P] * 14
+        L.oracle_rmsprop_fwd_cplx.argtypes = [i64] + [P] * 10
+        L.oracle_sgd_fwd_cplx.argtypes = [i64, P, P, I] + [P] * 8
+        L.oracle_sweep_forward_cplx.argtypes = [I, i64, i64, P, P, I, P, P, P, P, P, P, P]
+        _lib = L
+    return _lib
+
+
+def set_num_threads(n: int) -> int:
+    """Threads for the chunked loops (0 = all cores). Returns the count used."""
+    return lib().oracle_set_num_threads(int(n))
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def _f32(a):
+    if a is None:
+        return None
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _state(a, bf16):
+    if a is None:
+        return None
+    if bf16:
+        a = np.ascontiguousarray(a)
+        assert a.dtype == np.uint16, "bf16 state is passed as uint16 bit patterns"
+        return a
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _out(n, want=True):
+    return np.empty(n, dtype=np.float64) if want else None
+
+
+def _hp(vals):
+    return np.ascontiguousarray(vals, dtype=np.float64)
+
+
+def _offsets(offsets):
+    if offsets is None:
+        return 0, None
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    return len(off) - 1, off
+
+
+# ------------------------------------------------------------------ Adam
+def adam_fwd(g, m, v, t, lr, b1, b2, eps, eps_root=0.0, state_bf16=False, prec=0):
+    """(u, m', v') of one Adam step. m/v None = zero state."""
+    g = _f32(g)
+    n = g.size
+    m, v = _state(m, state_bf16), _state(v, state_bf16)
+    hp = _hp([lr, b1, b2, eps, eps_root])
+    u, m1, v1 = _out(n), _out(n), _out(n)
+    lib().oracle_adam_fwd(n, int(t), _p(hp), int(state_bf16), int(prec), _p(g), _p(m), _p(v),
+                          _p(u), _p(m1), _p(v1))
+    return u, m1, v1
+
+
+def adam_vjp(g, m, v, du, dm1, dv1, t, lr, b1, b2, eps, eps_root=0.0, state_bf16=False,
+             prec=0, offsets=None):
+    """VJP of the Adam step. Returns dict with dg, dm, dv (arrays), dhp (4:
+    lr, b1, b2, eps), dhp_abs (Sigma|term|), and dhp_leaf (n_leaves x 4) if
+    offsets is given."""
+    g = _f32(g)
+    n = g.size
+    m, v = _state(m, state_bf16), _state(v, state_bf16)
+    du, dm1, dv1 = _f32(du), _f32(dm1), _f32(dv1)
+    hp = _hp([lr, b1, b2, eps, eps_root])
+    dg, dm, dv = _out(n), _out(n), _out(n)
+    dhp, dhp_abs = np.zeros(4), np.zeros(4)
+    nl, off = _offsets(offsets)
+    leaf = np.zeros((nl, 4)) if off is not None else None
+    lib().oracle_adam_vjp(n, int(t), _p(hp), int(state_bf16), int(prec), _p(g), _p(m), _p(v),
+                          _p(du), _p(dm1), _p(dv1), _p(dg), _p(dm), _p(dv), _p(dhp),
+                          _p(dhp_abs), nl, _p(off), _p(leaf))
+    return dict(dg=dg, dm=dm, dv=dv, dhp=dhp, dhp_abs=dhp_abs, dhp_leaf=leaf)
+
+
+# --------------------------------------------------------------- RMSProp
+def rmsprop_fwd(g, v, lr, alpha, eps, state_bf16=False, prec=0):
+    """(u, v') of one RMSProp step."""
+    g = _f32(g)
+    n = g.size
+    v = _state(v, state_bf16)
+    hp = _hp([lr, alpha, eps])
+    u, v1 = _out(n), _out(n)
+    lib().oracle_rmsprop_fwd(n, _p(hp), int(state_bf16), int(prec), _p(g), _p(v), _p(u), _p(v1))
+    return u, v1
+
+
+def rmsprop_vjp(g, v, du, dv1, lr, alpha, eps, state_bf16=False, prec=0, offsets=None):
+    """VJP of the RMSProp step; dhp = (lr, alpha, eps)."""
+    g = _f32(g)
+    n = g.size
+    v = _state(v, state_bf16)
+    du, dv1 = _f32(du), _f32(dv1)
+    hp = _hp([lr, alpha, eps])
+    dg, dv = _out(n), _out(n)
+    dhp, dhp_abs = np.zeros(3), np.zeros(3)
+    nl, off = _offsets(offsets)
+    leaf = np.zeros((nl, 3)) if off is not None else None
+    lib().oracle_rmsprop_vjp(n, _p(hp), int(state_bf16), int(prec), _p(g), _p(v), _p(du),
+                             _p(dv1), _p(dg), _p(dv), _p(dhp), _p(dhp_abs), nl, _p(off),
+                             _p(leaf))
+    return dict(dg=dg, dv=dv, dhp=dhp, dhp_abs=dhp_abs, dhp_leaf=leaf)
+
+
+# ------------------------------------------------------------------- SGD
+def sgd_fwd(g, b, lr, momentum, nesterov=False, state_bf16=False, prec=0):
+    """(u, b') of one SGD(-momentum) step."""
+    g = _f32(g)
+    n = g.size
+    b = _state(b, state_bf16)
+    hp = _hp([lr, momentum, 1.0 if nesterov else 0.0])
+    u, b1 = _out(n), _out(n)
+    lib().oracle_sgd_fwd(n, _p(hp), int(state_bf16), int(prec), _p(g), _p(b), _p(u), _p(b1))
+    return u, b1
+
+
+def sgd_vjp(g, b, du, db1, lr, momentum, nesterov=False, state_bf16=False, prec=0,
+            offsets=None):
+    """VJP of the SGD step; dhp = (lr, momentum)."""
+    g = _f32(g)
+    n = g.size
+    b = _state(b, state_bf16)
+    du, db1 = _f32(du), _f32(db1)
+    hp = _hp([lr, momentum, 1.0 if nesterov else 0.0])
+    dg, db = _out(n), _out(n)
+    dhp, dhp_abs = np.zeros(2), np.zeros(2)
+    nl, off = _offsets(offsets)
+    leaf = np.zeros((nl, 2)) if off is not None else None
+    lib().oracle_sgd_vjp(n, _p(hp), int(state_bf16), int(prec), _p(g), _p(b), _p(du), _p(db1),
+                         _p(dg), _p(db), _p(dhp), _p(dhp_abs), nl, _p(off), _p(leaf))
+    return dict(dg=dg, db=db, dhp=dhp, dhp_abs=dhp_abs, dhp_leaf=leaf)
+
+
+def bf16_rne(x):
+    """Round-to-nearest-even of float64 values to bf16 bit patterns (Z9)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty(x.size, dtype=np.uint16)
+    lib().oracle_bf16_rne(x.size, _p(x), _p(out))
+    return out
+
+
+def bf16_to_f64(bits):
+    """Exact value of bf16 bit patterns."""
+    bits = np.ascontiguousarray(bits, dtype=np.uint16)
+    return (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+# ------------------------------------------------------ K-step sweep (a9)
+KIND = {"adam": 0, "rmsprop": 1, "sgd": 2}
+
+
+def sweep_quadratic(kind, a, theta0, phi, y, K, hp, prec=0):
+    """Row a9: K unrolled steps on L_in = 1/2 sum a (theta-phi)^2 and the
+    reverse sweep of L_out = 1/2 ||theta_K - y||^2. ``hp`` is the optimizer's
+    hyper-parameter list (adam: lr,b1,b2,eps,eps_root; rmsprop: lr,alpha,eps;
+    sgd: lr,momentum,nesterov). Returns dict phi_bar, theta0_bar, hyper_bar(4),
+    loss, thetaK."""
+    a, theta0, phi, y = _f32(a), _f32(theta0), _f32(phi), _f32(y)
+    n = a.size
+    hp = _hp(list(hp) + [0.0] * (5 - len(hp)))
+    pb, tb, tk = _out(n), _out(n), _out(n)
+    hyp = np.zeros(4)
+    loss = np.zeros(1)
+    lib().oracle_sweep_quadratic(KIND[kind], n, int(K), _p(hp), int(prec), _p(a), _p(theta0),
+                                 _p(phi), _p(y), _p(pb), _p(tb), _p(hyp), _p(loss), _p(tk))
+    return dict(phi_bar=pb, theta0_bar=tb, hyper_bar=hyp, loss=float(loss[0]), thetaK=tk)
+
+
+# --------------------------------------------------- complex-step helpers
+def _cparts(x, n):
+    if x is None:
+        return None, None
+    x = np.broadcast_to(np.asarray(x, dtype=np.complex128), (n,))
+    return np.ascontiguousarray(x.real), np.ascontiguousarray(x.imag)
+
+
+def adam_fwd_complex(g, m, v, t, hp):
+    """Forward Adam map in complex128 (hp: 5 complex). Returns (u, m', v')."""
+    g = np.asarray(g, dtype=np.complex128)
+    n = g.size
+    hr, hi = _cparts(hp, 5)
+    gr, gi = _cparts(g, n)
+    mr, mi = _cparts(m, n)
+    vr, vi = _cparts(v, n)
+    outs = [np.empty(n) for _ in range(6)]
+    lib().oracle_adam_fwd_cplx(n, int(t), _p(hr), _p(hi), _p(gr), _p(gi), _p(mr), _p(mi),
+                               _p(vr), _p(vi), *[_p(o) for o in outs])
+    return tuple(outs[2 * k] + 1j * outs[2 * k + 1] for k in range(3))
+
+
+def rmsprop_fwd_complex(g, v, hp):
+    g = np.asarray(g, dtype=np.complex128)
+    n = g.size
+    hr, hi = _cparts(hp, 3)
+    gr, gi = _cparts(g, n)
+    vr, vi = _cparts(v, n)
+    outs = [np.empty(n) for _ in range(4)]
+    lib().oracle_rmsprop_fwd_cplx(n, _p(hr), _p(hi), _p(gr), _p(gi), _p(vr), _p(vi),
+                                  *[_p(o) for o in outs])
+    return tuple(outs[2 * k] + 1j * outs[2 * k + 1] for k in range(2))
+
+
+def sgd_fwd_complex(g, b, hp, nesterov=False):
+    g = np.asarray(g, dtype=np.complex128)
+    n = g.size
+    hr, hi = _cparts(hp, 2)
+    gr, gi = _cparts(g, n)
+    br, bi = _cparts(b, n)
+    outs = [np.empty(n) for _ in range(4)]
+    lib().oracle_sgd_fwd_cplx(n, _p(hr), _p(hi), int(nesterov), _p(gr), _p(gi), _p(br), _p(bi),
+                              *[_p(o) for o in outs])
+    return tuple(outs[2 * k] + 1j * outs[2 * k + 1] for k in range(2))
+
+
+def sweep_forward_complex(kind, a, theta0, phi, K, hp, nesterov=False):
+    """theta_K of the K-step map in complex128 (per element)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    n = a.size
+    nhp = 5 if kind == "adam" else 3
+    hp = list(hp) + [0.0] * (nhp - len(hp))
+    hr, hi = _cparts(hp, nhp)
+    tr, ti = _cparts(theta0, n)
+    pr, pi = _cparts(phi, n)
+    o_r, o_i = np.empty(n), np.empty(n)
+    lib().oracle_sweep_forward_cplx(KIND[kind], n, int(K), _p(hr), _p(hi), int(nesterov), _p(a),
+                                    _p(tr), _p(ti), _p(pr), _p(pi), _p(o_r), _p(o_i))
+    return o_r + 1j * o_i

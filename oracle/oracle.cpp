@@ -1,0 +1,549 @@
+// oracle/oracle.cpp -- array entry points of the scalar oracle (C ABI, ctypes).
+//
+// TEST INFRASTRUCTURE ONLY (see oracle.hpp): callable from tests/,
+// __graft_entry__.smoke() and bench.py's CPU-baseline legs, never from the
+// product package. Shares no code with paper_2211_06934_b200/.
+//
+// Conventions of this file (not of the product ABI):
+//   * inputs are the exact fp32 values the GPU sees (or bf16 bit patterns for
+//     state when state_bf16 = 1, promoted exactly: bits << 16);
+//   * a NULL state input means the zero state (opt.init); a NULL
+//     cotangent means a zero cotangent; a NULL output is skipped;
+//   * outputs are double; prec = 0 evaluates in double, prec = 1 in long
+//     double (x87 80-bit) -- SURVEY Z11: the textbook chain rule has relative
+//     error ~1e-16 |g|/eps in dg, long double removes that from parity checks;
+//   * hyper-gradient sums ("Sigma-reduced", north star) are summed per fixed
+//     4096-element chunk (S:250 chunking), then over chunks in index order, in
+//     long double; the result does not depend on the thread count;
+//   * dhp_abs (optional) receives Sigma |term| per hyper-gradient, the scale
+//     a tolerance on a sum of signed terms must use (reading Z10).
+#include "oracle.hpp"
+
+#include <cstdint>
+#include <cstring>
+#include <vector>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+using oracle::AdamHP;
+using oracle::RmsHP;
+using oracle::SgdHP;
+typedef std::complex<double> cd;
+
+namespace {
+
+int g_threads = 1;
+const int64_t kChunk = 4096;
+
+inline float bf16_to_f32(uint16_t b) {
+  uint32_t u = (uint32_t)b << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+// Input element i of a state array (NULL -> 0).
+inline double state_in(const void* p, int bf16, int64_t i) {
+  if (!p) return 0.0;
+  if (bf16) return (double)bf16_to_f32(((const uint16_t*)p)[i]);
+  return (double)((const float*)p)[i];
+}
+inline double f32_in(const float* p, int64_t i) { return p ? (double)p[i] : 0.0; }
+inline void put(double* p, int64_t i, double x) {
+  if (p) p[i] = x;
+}
+
+// Run body(i, acc[]) for every element; acc has `nh` hyper-gradient slots.
+// Per-chunk partials, then an index-ordered sum over chunks.
+template <class Body>
+void for_chunks(int64_t n, int nh, double* sums, double* abs_sums, Body body) {
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  std::vector<long double> part((size_t)nchunks * nh * 2, 0.0L);
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+#endif
+  for (int64_t c = 0; c < nchunks; ++c) {
+    long double* acc = &part[(size_t)c * nh * 2];
+    const int64_t lo = c * kChunk, hi = (lo + kChunk < n) ? lo + kChunk : n;
+    for (int64_t i = lo; i < hi; ++i) body(i, acc);
+  }
+  for (int k = 0; k < nh; ++k) {
+    long double s = 0.0L, a = 0.0L;
+    for (int64_t c = 0; c < nchunks; ++c) {
+      s += part[(size_t)c * nh * 2 + k];
+      a += part[(size_t)c * nh * 2 + nh + k];
+    }
+    if (sums) sums[k] = (double)s;
+    if (abs_sums) abs_sums[k] = (double)a;
+  }
+}
+
+inline void acc_term(long double* acc, int nh, int k, long double x) {
+  acc[k] += x;
+  acc[nh + k] += (x < 0 ? -x : x);
+}
+
+// Per-leaf sums: plain loop over leaves (P:87/S:120 flatten -> offsets).
+template <class Term>
+void leaf_sums(int64_t n_leaves, const int64_t* off, int nh, double* out, Term term) {
+  for (int64_t l = 0; l < n_leaves; ++l) {
+    std::vector<long double> s(nh, 0.0L);
+    for (int64_t i = off[l]; i < off[l + 1]; ++i) term(i, s.data());
+    for (int k = 0; k < nh; ++k) out[l * nh + k] = (double)s[k];
+  }
+}
+
+template <class T>
+AdamHP<T> adam_hp(const double* hp) {
+  return {T(hp[0]), T(hp[1]), T(hp[2]), T(hp[3]), T(hp[4])};
+}
+template <class T>
+RmsHP<T> rms_hp(const double* hp) {
+  return {T(hp[0]), T(hp[1]), T(hp[2])};
+}
+template <class T>
+SgdHP<T> sgd_hp(const double* hp) {
+  return {T(hp[0]), T(hp[1]), hp[2] != 0.0 ? 1 : 0};
+}
+
+// ---------------------------------------------------------------- adam
+template <class T>
+void adam_fwd_arr(int64_t n, int64_t t, const double* hp, int bf, const float* g,
+                  const void* m, const void* v, double* u, double* m1, double* v1) {
+  const AdamHP<T> h = adam_hp<T>(hp);
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+#endif
+  for (int64_t i = 0; i < n; ++i) {
+    auto r = oracle::adam_fwd<T>(T(f32_in(g, i)), T(state_in(m, bf, i)),
+                                 T(state_in(v, bf, i)), h, t);
+    put(u, i, (double)r.u);
+    put(m1, i, (double)r.m1);
+    put(v1, i, (double)r.v1);
+  }
+}
+
+template <class T>
+void adam_vjp_arr(int64_t n, int64_t t, const double* hp, int bf, const float* g,
+                  const void* m, const void* v, const float* du, const float* dm1,
+                  const float* dv1, double* dg, double* dm, double* dv, double* dhp,
+                  double* dhp_abs, int64_t n_leaves, const int64_t* off,
+                  double* dhp_leaf) {
+  const AdamHP<T> h = adam_hp<T>(hp);
+  auto elem = [&](int64_t i) {
+    return oracle::adam_vjp<T>(T(f32_in(g, i)), T(state_in(m, bf, i)),
+                               T(state_in(v, bf, i)), T(f32_in(du, i)),
+                               T(f32_in(dm1, i)), T(f32_in(dv1, i)), h, t);
+  };
+  for_chunks(n, 4, dhp, dhp_abs, [&](int64_t i, long double* acc) {
+    auto r = elem(i);
+    put(dg, i, (double)r.dg);
+    put(dm, i, (double)r.dm);
+    put(dv, i, (double)r.dv);
+    acc_term(acc, 4, 0, (long double)r.dlr);
+    acc_term(acc, 4, 1, (long double)r.db1);
+    acc_term(acc, 4, 2, (long double)r.db2);
+    acc_term(acc, 4, 3, (long double)r.deps);
+  });
+  if (dhp_leaf && off)
+    leaf_sums(n_leaves, off, 4, dhp_leaf, [&](int64_t i, long double* s) {
+      auto r = elem(i);
+      s[0] += (long double)r.dlr;
+      s[1] += (long double)r.db1;
+      s[2] += (long double)r.db2;
+      s[3] += (long double)r.deps;
+    });
+}
+
+// ------------------------------------------------------------- rmsprop
+template <class T>
+void rms_fwd_arr(int64_t n, const double* hp, int bf, const float* g, const void* v,
+                 double* u, double* v1) {
+  const RmsHP<T> h = rms_hp<T>(hp);
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+#endif
+  for (int64_t i = 0; i < n; ++i) {
+    auto r = oracle::rmsprop_fwd<T>(T(f32_in(g, i)), T(state_in(v, bf, i)), h);
+    put(u, i, (double)r.u);
+    put(v1, i, (double)r.v1);
+  }
+}
+
+template <class T>
+void rms_vjp_arr(int64_t n, const double* hp, int bf, const float* g, const void* v,
+                 const float* du, const float* dv1, double* dg, double* dv,
+                 double* dhp, double* dhp_abs, int64_t n_leaves, const int64_t* off,
+                 double* dhp_leaf) {
+  const RmsHP<T> h = rms_hp<T>(hp);
+  auto elem = [&](int64_t i) {
+    return oracle::rmsprop_vjp<T>(T(f32_in(g, i)), T(state_in(v, bf, i)),
+                                  T(f32_in(du, i)), T(f32_in(dv1, i)), h);
+  };
+  for_chunks(n, 3, dhp, dhp_abs, [&](int64_t i, long double* acc) {
+    auto r = elem(i);
+    put(dg, i, (double)r.dg);
+    put(dv, i, (double)r.dv);
+    acc_term(acc, 3, 0, (long double)r.dlr);
+    acc_term(acc, 3, 1, (long double)r.dalpha);
+    acc_term(acc, 3, 2, (long double)r.deps);
+  });
+  if (dhp_leaf && off)
+    leaf_sums(n_leaves, off, 3, dhp_leaf, [&](int64_t i, long double* s) {
+      auto r = elem(i);
+      s[0] += (long double)r.dlr;
+      s[1] += (long double)r.dalpha;
+      s[2] += (long double)r.deps;
+    });
+}
+
+// ----------------------------------------------------------------- sgd
+template <class T>
+void sgd_fwd_arr(int64_t n, const double* hp, int bf, const float* g, const void* b,
+                 double* u, double* b1) {
+  const SgdHP<T> h = sgd_hp<T>(hp);
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+#endif
+  for (int64_t i = 0; i < n; ++i) {
+    auto r = oracle::sgd_fwd<T>(T(f32_in(g, i)), T(state_in(b, bf, i)), h);
+    put(u, i, (double)r.u);
+    put(b1, i, (double)r.b1);
+  }
+}
+
+template <class T>
+void sgd_vjp_arr(int64_t n, const double* hp, int bf, const float* g, const void* b,
+                 const float* du, const float* db1, double* dg, double* db,
+                 double* dhp, double* dhp_abs, int64_t n_leaves, const int64_t* off,
+                 double* dhp_leaf) {
+  const SgdHP<T> h = sgd_hp<T>(hp);
+  auto elem = [&](int64_t i) {
+    return oracle::sgd_vjp<T>(T(f32_in(g, i)), T(state_in(b, bf, i)), T(f32_in(du, i)),
+                              T(f32_in(db1, i)), h);
+  };
+  for_chunks(n, 2, dhp, dhp_abs, [&](int64_t i, long double* acc) {
+    auto r = elem(i);
+    put(dg, i, (double)r.dg);
+    put(db, i, (double)r.db);
+    acc_term(acc, 2, 0, (long double)r.dlr);
+    acc_term(acc, 2, 1, (long double)r.dmu);
+  });
+  if (dhp_leaf && off)
+    leaf_sums(n_leaves, off, 2, dhp_leaf, [&](int64_t i, long double* s) {
+      auto r = elem(i);
+      s[0] += (long double)r.dlr;
+      s[1] += (long double)r.dmu;
+    });
+}
+
+// ----------------------------------------------- K-step unrolled sweep
+// SURVEY §8(a) row a9 (EG over unrolled optimisation, Listing 1
+// P:124-132): synthetic inner loss L_in = 1/2 sum a_i (theta_i - phi_i)^2, so
+// g = a (theta - phi), H = diag(a), dg/dphi = -diag(a); outer loss
+// L_out = 1/2 ||theta_K - y||^2 (reading Z17). Forward k = 0..K-1 with step
+// count t = k+1, theta_{k+1} = theta_k + u_k (apply_updates). Reverse:
+// the VJP of each step in reverse order, theta_bar_k = theta_bar_{k+1} + H g_bar_k,
+// phi_bar -= a g_bar_k, hyper_bar += this step's hyper cotangents.
+// Every element is independent except for the shared hyper-parameters.
+// kind: 0 adam (hp[5]), 1 rmsprop (hp[3]), 2 sgd (hp[3]: lr, mu, nesterov).
+template <class T>
+struct StepRes {
+  T u, s1, s2;  // update and the new state(s)
+};
+
+template <class T>
+StepRes<T> step_fwd(int kind, T g, T s1, T s2, const double* hp, int64_t t) {
+  if (kind == 0) {
+    auto r = oracle::adam_fwd<T>(g, s1, s2, adam_hp<T>(hp), t);
+    return {r.u, r.m1, r.v1};
+  } else if (kind == 1) {
+    auto r = oracle::rmsprop_fwd<T>(g, s1, rms_hp<T>(hp));
+    return {r.u, r.v1, T(0)};
+  }
+  auto r = oracle::sgd_fwd<T>(g, s1, sgd_hp<T>(hp));
+  return {r.u, r.b1, T(0)};
+}
+
+template <class T>
+void sweep_elem(int kind, int64_t K, const double* hp, T a, T th0, T phi, T y,
+                T* phi_bar, T* th0_bar, T* hyper, T* loss, T* thK) {
+  std::vector<T> gk(K), s1k(K + 1), s2k(K + 1);
+  T th = th0;
+  s1k[0] = T(0);
+  s2k[0] = T(0);
+  for (int64_t k = 0; k < K; ++k) {
+    gk[k] = a * (th - phi);
+    auto r = step_fwd<T>(kind, gk[k], s1k[k], s2k[k], hp, k + 1);
+    s1k[k + 1] = r.s1;
+    s2k[k + 1] = r.s2;
+    th = th + r.u;
+  }
+  *thK = th;
+  *loss = T(0.5) * (th - y) * (th - y);
+  T thb = th - y, s1b = T(0), s2b = T(0), phib = T(0);
+  for (int k = 0; k < 4; ++k) hyper[k] = T(0);
+  for (int64_t k = K - 1; k >= 0; --k) {
+    T gb;
+    if (kind == 0) {
+      auto r = oracle::adam_vjp<T>(gk[k], s1k[k], s2k[k], thb, s1b, s2b, adam_hp<T>(hp), k + 1);
+      gb = r.dg; s1b = r.dm; s2b = r.dv;
+      hyper[0] = hyper[0] + r.dlr; hyper[1] = hyper[1] + r.db1;
+      hyper[2] = hyper[2] + r.db2; hyper[3] = hyper[3] + r.deps;
+    } else if (kind == 1) {
+      auto r = oracle::rmsprop_vjp<T>(gk[k], s1k[k], thb, s1b, rms_hp<T>(hp));
+      gb = r.dg; s1b = r.dv;
+      hyper[0] = hyper[0] + r.dlr; hyper[1] = hyper[1] + r.dalpha;
+      hyper[2] = hyper[2] + r.deps;
+    } else {
+      auto r = oracle::sgd_vjp<T>(gk[k], s1k[k], thb, s1b, sgd_hp<T>(hp));
+      gb = r.dg; s1b = r.db;
+      hyper[0] = hyper[0] + r.dlr; hyper[1] = hyper[1] + r.dmu;
+    }
+    // theta_{k+1} = theta_k + u_k  -> identity on theta_bar, plus g_k = a (theta_k - phi)
+    thb = thb + a * gb;
+    phib = phib - a * gb;
+  }
+  *phi_bar = phib;
+  *th0_bar = thb;
+}
+
+}  // namespace
+
+extern "C" {
+
+int oracle_set_num_threads(int n) {
+#ifdef _OPENMP
+  g_threads = n > 0 ? n : omp_get_max_threads();
+#else
+  g_threads = 1;
+  (void)n;
+#endif
+  return g_threads;
+}
+
+int oracle_has_openmp(void) {
+#ifdef _OPENMP
+  return 1;
+#else
+  return 0;
+#endif
+}
+
+void oracle_adam_fwd(int64_t n, int64_t t, const double* hp, int state_bf16, int prec,
+                     const float* g, const void* m, const void* v, double* u,
+                     double* m1, double* v1) {
+  if (prec)
+    adam_fwd_arr<long double>(n, t, hp, state_bf16, g, m, v, u, m1, v1);
+  else
+    adam_fwd_arr<double>(n, t, hp, state_bf16, g, m, v, u, m1, v1);
+}
+
+void oracle_adam_vjp(int64_t n, int64_t t, const double* hp, int state_bf16, int prec,
+                     const float* g, const void* m, const void* v, const float* du,
+                     const float* dm1, const float* dv1, double* dg, double* dm,
+                     double* dv, double* dhp, double* dhp_abs, int64_t n_leaves,
+                     const int64_t* offsets, double* dhp_leaf) {
+  if (prec)
+    adam_vjp_arr<long double>(n, t, hp, state_bf16, g, m, v, du, dm1, dv1, dg, dm, dv,
+                              dhp, dhp_abs, n_leaves, offsets, dhp_leaf);
+  else
+    adam_vjp_arr<double>(n, t, hp, state_bf16, g, m, v, du, dm1, dv1, dg, dm, dv, dhp,
+                         dhp_abs, n_leaves, offsets, dhp_leaf);
+}
+
+void oracle_rmsprop_fwd(int64_t n, const double* hp, int state_bf16, int prec,
+                        const float* g, const void* v, double* u, double* v1) {
+  if (prec)
+    rms_fwd_arr<long double>(n, hp, state_bf16, g, v, u, v1);
+  else
+    rms_fwd_arr<double>(n, hp, state_bf16, g, v, u, v1);
+}
+
+void oracle_rmsprop_vjp(int64_t n, const double* hp, int state_bf16, int prec,
+                        const float* g, const void* v, const float* du, const float* dv1,
+                        double* dg, double* dv, double* dhp, double* dhp_abs,
+                        int64_t n_leaves, const int64_t* offsets, double* dhp_leaf) {
+  if (prec)
+    rms_vjp_arr<long double>(n, hp, state_bf16, g, v, du, dv1, dg, dv, dhp, dhp_abs,
+                             n_leaves, offsets, dhp_leaf);
+  else
+    rms_vjp_arr<double>(n, hp, state_bf16, g, v, du, dv1, dg, dv, dhp, dhp_abs, n_leaves,
+                        offsets, dhp_leaf);
+}
+
+void oracle_sgd_fwd(int64_t n, const double* hp, int state_bf16, int prec, const float* g,
+                    const void* b, double* u, double* b1) {
+  if (prec)
+    sgd_fwd_arr<long double>(n, hp, state_bf16, g, b, u, b1);
+  else
+    sgd_fwd_arr<double>(n, hp, state_bf16, g, b, u, b1);
+}
+
+void oracle_sgd_vjp(int64_t n, const double* hp, int state_bf16, int prec, const float* g,
+                    const void* b, const float* du, const float* db1, double* dg,
+                    double* db, double* dhp, double* dhp_abs, int64_t n_leaves,
+                    const int64_t* offsets, double* dhp_leaf) {
+  if (prec)
+    sgd_vjp_arr<long double>(n, hp, state_bf16, g, b, du, db1, dg, db, dhp, dhp_abs,
+                             n_leaves, offsets, dhp_leaf);
+  else
+    sgd_vjp_arr<double>(n, hp, state_bf16, g, b, du, db1, dg, db, dhp, dhp_abs, n_leaves,
+                        offsets, dhp_leaf);
+}
+
+// Round-to-nearest-even of a double to bf16 (reading Z9: stored bf16 state
+// is RNE of the exact value). Independent bit-level implementation on the
+// IEEE double: keep sign, exponent and the top 7 mantissa bits.
+void oracle_bf16_rne(int64_t n, const double* x, uint16_t* out) {
+  for (int64_t i = 0; i < n; ++i) {
+    // exact double -> the nearest bf16 via the float grid: bf16 values are
+    // floats whose low 16 bits are zero; find neighbours on that grid.
+    double d = x[i];
+    if (d != d) {  // NaN
+      out[i] = 0x7FC0;
+      continue;
+    }
+    float f = (float)d;  // nearest float (RNE); refine against d below
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    uint32_t lo = u & 0xFFFF0000u;          // truncation toward zero on the bf16 grid
+    uint32_t hi = lo + 0x00010000u;         // next bf16 away from zero
+    float flo, fhi;
+    std::memcpy(&flo, &lo, 4);
+    std::memcpy(&fhi, &hi, 4);
+    double elo = d - (double)flo, ehi = (double)fhi - d;
+    if (elo < 0) elo = -elo;
+    if (ehi < 0) ehi = -ehi;
+    uint32_t pick;
+    if (elo < ehi) pick = lo;
+    else if (ehi < elo) pick = hi;
+    else pick = ((lo >> 16) & 1u) ? hi : lo;  // tie -> even
+    out[i] = (uint16_t)(pick >> 16);
+  }
+}
+
+// K-step sweep in double / long double. prec as above.
+void oracle_sweep_quadratic(int kind, int64_t n, int64_t K, const double* hp, int prec,
+                            const float* a, const float* theta0, const float* phi,
+                            const float* y, double* phi_bar, double* theta0_bar,
+                            double* hyper_bar, double* loss, double* thetaK) {
+  std::vector<long double> hyp_part((size_t)((n + kChunk - 1) / kChunk + 1) * 5, 0.0L);
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+#endif
+  for (int64_t c = 0; c < nchunks; ++c) {
+    long double* acc = &hyp_part[(size_t)c * 5];
+    const int64_t lo = c * kChunk, hi = (lo + kChunk < n) ? lo + kChunk : n;
+    for (int64_t i = lo; i < hi; ++i) {
+      if (prec) {
+        long double pb, tb, h[4], l, tk;
+        sweep_elem<long double>(kind, K, hp, a[i], theta0[i], phi[i], y[i], &pb, &tb, h, &l, &tk);
+        put(phi_bar, i, (double)pb);
+        put(theta0_bar, i, (double)tb);
+        put(thetaK, i, (double)tk);
+        for (int k = 0; k < 4; ++k) acc[k] += h[k];
+        acc[4] += l;
+      } else {
+        double pb, tb, h[4], l, tk;
+        sweep_elem<double>(kind, K, hp, a[i], theta0[i], phi[i], y[i], &pb, &tb, h, &l, &tk);
+        put(phi_bar, i, pb);
+        put(theta0_bar, i, tb);
+        put(thetaK, i, tk);
+        for (int k = 0; k < 4; ++k) acc[k] += h[k];
+        acc[4] += l;
+      }
+    }
+  }
+  long double s[5] = {0, 0, 0, 0, 0};
+  for (int64_t c = 0; c < nchunks; ++c)
+    for (int k = 0; k < 5; ++k) s[k] += hyp_part[(size_t)c * 5 + k];
+  for (int k = 0; k < 4; ++k)
+    if (hyper_bar) hyper_bar[k] = (double)s[k];
+  if (loss) *loss = (double)s[4];
+}
+
+// ------------------------------------------------ complex-step entry points
+// Forward maps in std::complex<double>. Each array is given as
+// separate real and imaginary parts; a NULL imaginary part means 0.
+static inline cd cin(const double* re_, const double* im_, int64_t i) {
+  return cd(re_ ? re_[i] : 0.0, im_ ? im_[i] : 0.0);
+}
+static inline void cout_(double* re_, double* im_, int64_t i, cd x) {
+  if (re_) re_[i] = x.real();
+  if (im_) im_[i] = x.imag();
+}
+
+void oracle_adam_fwd_cplx(int64_t n, int64_t t, const double* hp_re, const double* hp_im,
+                          const double* g_re, const double* g_im, const double* m_re,
+                          const double* m_im, const double* v_re, const double* v_im,
+                          double* u_re, double* u_im, double* m1_re, double* m1_im,
+                          double* v1_re, double* v1_im) {
+  AdamHP<cd> h{cin(hp_re, hp_im, 0), cin(hp_re, hp_im, 1), cin(hp_re, hp_im, 2),
+               cin(hp_re, hp_im, 3), cin(hp_re, hp_im, 4)};
+  for (int64_t i = 0; i < n; ++i) {
+    auto r = oracle::adam_fwd<cd>(cin(g_re, g_im, i), cin(m_re, m_im, i), cin(v_re, v_im, i), h, t);
+    cout_(u_re, u_im, i, r.u);
+    cout_(m1_re, m1_im, i, r.m1);
+    cout_(v1_re, v1_im, i, r.v1);
+  }
+}
+
+void oracle_rmsprop_fwd_cplx(int64_t n, const double* hp_re, const double* hp_im,
+                             const double* g_re, const double* g_im, const double* v_re,
+                             const double* v_im, double* u_re, double* u_im, double* v1_re,
+                             double* v1_im) {
+  RmsHP<cd> h{cin(hp_re, hp_im, 0), cin(hp_re, hp_im, 1), cin(hp_re, hp_im, 2)};
+  for (int64_t i = 0; i < n; ++i) {
+    auto r = oracle::rmsprop_fwd<cd>(cin(g_re, g_im, i), cin(v_re, v_im, i), h);
+    cout_(u_re, u_im, i, r.u);
+    cout_(v1_re, v1_im, i, r.v1);
+  }
+}
+
+void oracle_sgd_fwd_cplx(int64_t n, const double* hp_re, const double* hp_im, int nesterov,
+                         const double* g_re, const double* g_im, const double* b_re,
+                         const double* b_im, double* u_re, double* u_im, double* b1_re,
+                         double* b1_im) {
+  SgdHP<cd> h{cin(hp_re, hp_im, 0), cin(hp_re, hp_im, 1), nesterov};
+  for (int64_t i = 0; i < n; ++i) {
+    auto r = oracle::sgd_fwd<cd>(cin(g_re, g_im, i), cin(b_re, b_im, i), h);
+    cout_(u_re, u_im, i, r.u);
+    cout_(b1_re, b1_im, i, r.b1);
+  }
+}
+
+// Complex forward of the K-step map: theta_K per element (row a9 forward).
+void oracle_sweep_forward_cplx(int kind, int64_t n, int64_t K, const double* hp_re,
+                               const double* hp_im, int nesterov, const double* a,
+                               const double* th0_re, const double* th0_im,
+                               const double* phi_re, const double* phi_im,
+                               double* thK_re, double* thK_im) {
+  const int nhp = kind == 0 ? 5 : 3;
+  cd hpc[5];
+  for (int k = 0; k < nhp; ++k) hpc[k] = cin(hp_re, hp_im, k);
+  for (int64_t i = 0; i < n; ++i) {
+    cd th = cin(th0_re, th0_im, i), phi = cin(phi_re, phi_im, i);
+    cd s1(0), s2(0);
+    for (int64_t k = 0; k < K; ++k) {
+      cd g = cd(a[i]) * (th - phi);
+      cd u;
+      if (kind == 0) {
+        auto r = oracle::adam_fwd<cd>(g, s1, s2, AdamHP<cd>{hpc[0], hpc[1], hpc[2], hpc[3], hpc[4]}, k + 1);
+        u = r.u; s1 = r.m1; s2 = r.v1;
+      } else if (kind == 1) {
+        auto r = oracle::rmsprop_fwd<cd>(g, s1, RmsHP<cd>{hpc[0], hpc[1], hpc[2]});
+        u = r.u; s1 = r.v1;
+      } else {
+        auto r = oracle::sgd_fwd<cd>(g, s1, SgdHP<cd>{hpc[0], hpc[1], nesterov});
+        u = r.u; s1 = r.b1;
+      }
+      th = th + u;
+    }
+    cout_(thK_re, thK_im, i, th);
+  }
+}
+
+}  // extern "C"

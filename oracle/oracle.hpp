@@ -1,0 +1,240 @@
+// oracle/oracle.hpp -- scalar reference for the differentiable optimizer step.
+//
+// TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and
+// bench.py's cpu_baseline / --impl reference legs may load, call or link
+// anything under oracle/. The product path (paper_2211_06934_b200/) never
+// does, and shares no code, header, table or constant with this file.
+//
+// What this computes (PAPER.md = P:, SPEC.md = S:, SURVEY.md §8(c) readings Z*):
+//   * The paper names the accelerated, differentiable optimizers "SGD, RMSProp,
+//     Adam" (§1 contribution (2)(i)) and says their forward and backward
+//     are written by hand (§2.3 "CPU/GPU-accelerated optimizers"). It
+//     prints no formula; the recurrences are the standard ones quoted by
+//     S:188 (adam), S:196-204 (sgd), S:206 (rmsprop) -- reading Z1.
+//   * The backward is the vector-Jacobian product of the step map
+//         (g, state, hyper) -> (u, state')
+//     written here as plain reverse-mode: one adjoint per intermediate of the
+//     forward, in reverse order. No symbolic reduction is applied on purpose,
+//     so that this file and the CUDA kernels are two independent derivations.
+//   * 0/0 handling ("explicitly canceling some 0/0 cases"): reading Z6 --
+//     if s = sqrt(.) == 0 the adjoint through the sqrt is 0; reading Z7 -- if
+//     d = s + eps == 0 the update is 0 and every adjoint through 1/d is 0.
+//
+// Everything is templated on the scalar T so that the same text runs in
+// double (the oracle), long double (x87 80-bit, for parity on inputs where
+// the textbook chain rule loses digits) and std::complex<double>
+// (complex-step pins of the VJP against the forward).
+#pragma once
+#include <cmath>
+#include <complex>
+#include <cstdint>
+
+namespace oracle {
+
+// Real part, for the branch tests at the singular points.
+inline double re(double x) { return x; }
+inline double re(long double x) { return (double)x; }
+inline double re(const std::complex<double>& x) { return x.real(); }
+
+// b^t by repeated multiplication: exact integer powers, S:251 (DESIGN
+// DECISIONS: "bias-correction uses exact powers b1^t, b2^t").
+template <class T>
+T ipow(T b, int64_t t) {
+  T r = T(1);
+  for (int64_t i = 0; i < t; ++i) r = r * b;
+  return r;
+}
+
+template <class T>
+T tsqrt(const T& x) {
+  using std::sqrt;
+  return sqrt(x);
+}
+
+// ---------------------------------------------------------------- Adam ----
+// m <- b1 m + (1-b1) g ; v <- b2 v + (1-b2) g^2 ;
+//        mhat = m/(1-b1^t) ; vhat = v/(1-b2^t) ; u = -lr mhat/(sqrt(vhat)+eps)
+// eps_root (reading Z4) is added under the sqrt; default 0 reproduces S:188.
+// t is the 1-based step count (reading Z3; S:193 uses t=1 on the first step).
+template <class T>
+struct AdamHP {
+  T lr, b1, b2, eps, eps_root;
+};
+
+template <class T>
+struct AdamFwd {
+  T u, m1, v1;
+};
+
+template <class T>
+AdamFwd<T> adam_fwd(T g, T m, T v, const AdamHP<T>& h, int64_t t) {
+  const T one(1);
+  T m1 = h.b1 * m + (one - h.b1) * g;         // S:188 first moment
+  T v1 = h.b2 * v + (one - h.b2) * g * g;     // S:188 second moment
+  T bc1 = one - ipow(h.b1, t);                // S:188 bias corrections
+  T bc2 = one - ipow(h.b2, t);
+  T mhat = m1 / bc1;
+  T vhat = v1 / bc2;
+  T s = tsqrt(vhat + h.eps_root);
+  T d = s + h.eps;
+  T u = (re(d) == 0.0) ? T(0) : -h.lr * mhat / d;  // Z7: d == 0 -> u := 0
+  return {u, m1, v1};
+}
+
+template <class T>
+struct AdamVjp {
+  T dg, dm, dv;              // cotangents of the inputs g, m, v
+  T dlr, db1, db2, deps;     // hyper-parameter cotangents (this element's term)
+};
+
+// Reverse mode over the forward graph above. Inputs du, dm1, dv1 are the
+// cotangents of the outputs u, m1, v1. ("manually writing the forward
+// and backward functions"; reading Z5 for which cotangents are produced.)
+template <class T>
+AdamVjp<T> adam_vjp(T g, T m, T v, T du, T dm1_out, T dv1_out,
+                    const AdamHP<T>& h, int64_t t) {
+  const T one(1), two(2);
+  // ---- forward, keeping every intermediate
+  T m1 = h.b1 * m + (one - h.b1) * g;
+  T v1 = h.b2 * v + (one - h.b2) * g * g;
+  T p1 = ipow(h.b1, t), p2 = ipow(h.b2, t);
+  T bc1 = one - p1, bc2 = one - p2;
+  T mhat = m1 / bc1;
+  T vhat = v1 / bc2;
+  T s = tsqrt(vhat + h.eps_root);
+  T d = s + h.eps;
+  const bool d_zero = re(d) == 0.0;   // Z7
+  const bool s_zero = re(s) == 0.0;   // Z6
+  // ---- reverse: u = -lr * mhat / d
+  T dlr = d_zero ? T(0) : du * (-mhat / d);
+  T dmhat = d_zero ? T(0) : du * (-h.lr / d);
+  T dd = d_zero ? T(0) : du * (h.lr * mhat / (d * d));
+  // d = s + eps
+  T deps = dd;
+  T ds = dd;
+  // s = sqrt(vhat + eps_root)   (Z6: adjoint through sqrt at 0 is 0)
+  T dvhat = s_zero ? T(0) : ds / (two * s);
+  // mhat = m1 / bc1 ; vhat = v1 / bc2
+  T dm1 = dm1_out + dmhat / bc1;
+  T dbc1 = -dmhat * m1 / (bc1 * bc1);
+  T dv1 = dv1_out + dvhat / bc2;
+  T dbc2 = -dvhat * v1 / (bc2 * bc2);
+  // bc = 1 - b^t  ->  d(bc)/db = -t b^(t-1)
+  T tt = T((double)t);
+  T db1 = -dbc1 * tt * ipow(h.b1, t - 1);
+  T db2 = -dbc2 * tt * ipow(h.b2, t - 1);
+  // m1 = b1 m + (1-b1) g ; v1 = b2 v + (1-b2) g^2
+  db1 = db1 + dm1 * (m - g);
+  db2 = db2 + dv1 * (v - g * g);
+  T dm = dm1 * h.b1;
+  T dv = dv1 * h.b2;
+  T dg = dm1 * (one - h.b1) + dv1 * (one - h.b2) * two * g;
+  return {dg, dm, dv, dlr, db1, db2, deps};
+}
+
+// ------------------------------------------------------------- RMSProp ----
+// nu <- alpha nu + (1-alpha) g^2 ; u = -lr g/(sqrt(nu)+eps)
+// (eps outside the sqrt, not centred, no momentum -- reading Z1).
+template <class T>
+struct RmsHP {
+  T lr, alpha, eps;
+};
+
+template <class T>
+struct RmsFwd {
+  T u, v1;
+};
+
+template <class T>
+RmsFwd<T> rmsprop_fwd(T g, T v, const RmsHP<T>& h) {
+  const T one(1);
+  T v1 = h.alpha * v + (one - h.alpha) * g * g;
+  T s = tsqrt(v1);
+  T d = s + h.eps;
+  T u = (re(d) == 0.0) ? T(0) : -h.lr * g / d;  // Z7
+  return {u, v1};
+}
+
+template <class T>
+struct RmsVjp {
+  T dg, dv;
+  T dlr, dalpha, deps;
+};
+
+template <class T>
+RmsVjp<T> rmsprop_vjp(T g, T v, T du, T dv1_out, const RmsHP<T>& h) {
+  const T one(1), two(2);
+  T v1 = h.alpha * v + (one - h.alpha) * g * g;
+  T s = tsqrt(v1);
+  T d = s + h.eps;
+  const bool d_zero = re(d) == 0.0;
+  const bool s_zero = re(s) == 0.0;
+  // u = -lr * g / d
+  T dlr = d_zero ? T(0) : du * (-g / d);
+  T dg = d_zero ? T(0) : du * (-h.lr / d);
+  T dd = d_zero ? T(0) : du * (h.lr * g / (d * d));
+  T deps = dd;
+  T ds = dd;
+  T dv1 = dv1_out + (s_zero ? T(0) : ds / (two * s));  // Z6
+  // v1 = alpha v + (1-alpha) g^2
+  T dalpha = dv1 * (v - g * g);
+  T dv = dv1 * h.alpha;
+  dg = dg + dv1 * (one - h.alpha) * two * g;
+  return {dg, dv, dlr, dalpha, deps};
+}
+
+// ------------------------------------------------------- SGD-momentum ----
+// momentum = 0 -> u = -lr g ; else b <- mu b + g (no dampening,
+// pinned by S:203: buffers 1 then 1.9) and u = -lr b ; Nesterov (Z14):
+// u = -lr (g + mu b').
+template <class T>
+struct SgdHP {
+  T lr, mu;
+  int nesterov;
+};
+
+template <class T>
+struct SgdFwd {
+  T u, b1;
+};
+
+template <class T>
+SgdFwd<T> sgd_fwd(T g, T b, const SgdHP<T>& h) {
+  T b1 = h.mu * b + g;
+  T u = h.nesterov ? -h.lr * (g + h.mu * b1) : -h.lr * b1;
+  return {u, b1};
+}
+
+template <class T>
+struct SgdVjp {
+  T dg, db;
+  T dlr, dmu;
+};
+
+template <class T>
+SgdVjp<T> sgd_vjp(T g, T b, T du, T db1_out, const SgdHP<T>& h) {
+  T b1 = h.mu * b + g;
+  T dlr, dmu, dg, db1;
+  if (h.nesterov) {
+    // u = -lr * (g + mu * b1)
+    T w = g + h.mu * b1;
+    dlr = du * (-w);
+    T dw = du * (-h.lr);
+    dg = dw;
+    dmu = dw * b1;
+    db1 = db1_out + dw * h.mu;
+  } else {
+    // u = -lr * b1
+    dlr = du * (-b1);
+    dg = T(0);
+    dmu = T(0);
+    db1 = db1_out + du * (-h.lr);
+  }
+  // b1 = mu * b + g
+  dmu = dmu + db1 * b;
+  T db = db1 * h.mu;
+  dg = dg + db1;
+  return {dg, db, dlr, dmu};
+}
+
+}  // namespace oracle

@@ -1,0 +1,474 @@
+"""Pins of the CPU oracle against things other than itself (no GPU).
+
+Each test names what fixes the expected value: a worked example printed in
+SPEC.md (tests/golden/spec_examples.json), a closed form derived by hand, a
+library routine (torch.optim in float64), the complex-step derivative of the
+oracle's own *forward* (which is pinned separately), central finite
+differences, or an algebraic property of a VJP. A plausible slip in the
+oracle's VJP (dropped term, wrong sign, wrong power of bc, transposed
+operand) changes at least one of these.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+H = 1e-30  # complex-step size
+
+
+def rel_err(x, ref):
+    x, ref = np.asarray(x, np.float64), np.asarray(ref, np.float64)
+    return np.max(np.abs(x - ref) / np.maximum(np.abs(ref), 1e-300))
+
+
+# ------------------------------------------------ worked examples (SPEC)
+def test_spec_adam_first_step(orc):
+    e = GOLD["adam_first_step"]
+    u, m1, v1 = orc.adam_fwd([e["g"]], None, None, e["t"], e["lr"], e["b1"], e["b2"], e["eps"])
+    assert m1[0] == pytest.approx(e["m1"], rel=1e-15)
+    assert v1[0] == pytest.approx(e["v1"], rel=1e-12)
+    assert u[0] == pytest.approx(e["delta"], rel=1e-15)
+    assert e["theta"] + u[0] == pytest.approx(e["theta1"], rel=1e-7)
+
+
+def test_spec_adam_zero_grad_exact(orc):
+    e = GOLD["adam_zero_grad"]
+    u, m1, v1 = orc.adam_fwd([e["g"]], None, None, 1, e["lr"], e["b1"], e["b2"], e["eps"])
+    assert u[0] == 0.0 and m1[0] == 0.0 and v1[0] == 0.0
+
+
+def test_spec_sgd_examples(orc):
+    e = GOLD["sgd_plain"]
+    u, _ = orc.sgd_fwd([e["g"]], None, e["lr"], e["momentum"])
+    assert u[0] == e["delta"]
+    e = GOLD["sgd_momentum_two_steps"]
+    b = None
+    for k in range(2):
+        u, b1 = orc.sgd_fwd([e["g"][k]], b, e["lr"], e["momentum"])
+        assert b1[0] == pytest.approx(e["buffers"][k], rel=1e-15)
+        assert u[0] == pytest.approx(e["deltas"][k], rel=1e-15)
+        b = b1.astype(np.float32)
+    e = GOLD["sgd_zero_grad"]
+    u, _ = orc.sgd_fwd([e["g"]], np.zeros(1, np.float32), e["lr"], e["momentum"])
+    assert u[0] == 0.0
+
+
+def test_spec_rmsprop_first_step(orc):
+    e = GOLD["rmsprop_first_step"]
+    u, v1 = orc.rmsprop_fwd([e["g"]], None, e["lr"], e["alpha"], e["eps"])
+    assert v1[0] == pytest.approx(e["nu"], rel=1e-14)
+    assert u[0] == pytest.approx(e["delta"], rel=1e-13)
+
+
+# ------------------------------------------------------- closed forms
+def test_adam_t1_closed_form_forward_and_vjp(orc):
+    """SURVEY P1 / north star: at t=1 from zero state, u = -lr g/(|g|+eps),
+    du/dg = -lr eps/(|g|+eps)^2, du/dlr = -g/(|g|+eps),
+    du/deps = lr g/(|g|+eps)^2, du/db1 = du/db2 = 0; with zero m', v'
+    cotangents dm = -b1 lr/((1-b1)(|g|+eps)), dv = b2 lr sgn(g)/(2(1-b2)(|g|+eps)^2)."""
+    rng = np.random.default_rng(1)
+    g = (rng.standard_normal(64) * 10.0 ** rng.uniform(-3, 0, 64)).astype(np.float32)
+    lr, b1, b2, eps = 0.3, 0.9, 0.999, 1e-8
+    gd = g.astype(np.float64)
+    a = np.abs(gd) + eps
+    u, m1, v1 = orc.adam_fwd(g, None, None, 1, lr, b1, b2, eps)
+    assert rel_err(u, -lr * gd / a) < 1e-14
+    assert rel_err(m1, (1 - b1) * gd) < 1e-15
+    assert rel_err(v1, (1 - b2) * gd * gd) < 1e-14
+    for prec, tol in ((0, 1e-6), (1, 1e-10)):
+        for i in range(g.size):  # per element: hyper-gradients of one element
+            r = orc.adam_vjp(g[i:i + 1], None, None, np.ones(1), None, None, 1, lr, b1, b2, eps,
+                             prec=prec)
+            ai = a[i]
+            assert r["dg"][0] == pytest.approx(-lr * eps / ai ** 2, rel=tol)
+            assert r["dhp"][0] == pytest.approx(-gd[i] / ai, rel=1e-13)
+            assert r["dhp"][3] == pytest.approx(lr * gd[i] / ai ** 2, rel=1e-13)
+            assert abs(r["dhp"][1]) <= 1e-12 * lr / ai
+            assert abs(r["dhp"][2]) <= 1e-12 * lr / ai
+            assert r["dm"][0] == pytest.approx(-b1 * lr / ((1 - b1) * ai), rel=1e-13)
+            assert r["dv"][0] == pytest.approx(b2 * lr * np.sign(gd[i]) / (2 * (1 - b2) * ai ** 2),
+                                               rel=1e-12)
+
+
+def test_adam_zero_point_conventions(orc):
+    """SURVEY P3 / readings Z6, Z7: g = m = v = 0 gives u = 0 exactly and finite
+    cotangents; dg = (1-b1) dm1 - lr A du/eps with A = (1-b1)/bc1,
+    dm = b1 (dm1 - du lr/(bc1 eps)), dv = b2 dv1."""
+    lr, b1, b2, eps = 0.5, 0.9, 0.999, 1e-8
+    du = np.array([1.0, -2.0, 0.5], np.float32)
+    dm1 = np.array([0.3, 0.0, -1.0], np.float32)
+    dv1 = np.array([2.0, 1.0, 0.0], np.float32)
+    z = np.zeros(3, np.float32)
+    dud, dm1d = du.astype(np.float64), dm1.astype(np.float64)
+    for t in (1, 3, 50):
+        u, m1, v1 = orc.adam_fwd(z, z, z, t, lr, b1, b2, eps)
+        assert np.all(u == 0) and np.all(m1 == 0) and np.all(v1 == 0)
+        r = orc.adam_vjp(z, z, z, du, dm1, dv1, t, lr, b1, b2, eps)
+        bc1 = 1 - b1 ** t
+        A = (1 - b1) / bc1
+        for k in ("dg", "dm", "dv"):
+            assert np.all(np.isfinite(r[k]))
+        np.testing.assert_allclose(r["dg"], (1 - b1) * dm1d - lr * A * dud / eps, rtol=1e-12)
+        np.testing.assert_allclose(r["dm"], b1 * (dm1d - dud * lr / (bc1 * eps)), rtol=1e-12)
+        np.testing.assert_allclose(r["dv"], b2 * dv1.astype(np.float64), rtol=1e-15)
+
+
+def test_adam_constant_gradient_invariant(orc):
+    """a constant g from zero state keeps mhat = g, vhat = g^2, so
+    u_t = -lr g/(|g|+eps) at every step t (bias correction exactness)."""
+    g = np.array([0.7, -1e-3, 2.5, 1e-6], np.float32)
+    lr, b1, b2, eps = 1e-2, 0.9, 0.999, 1e-8
+    gd = g.astype(np.float64)
+    m = v = None
+    for t in range(1, 31):
+        u, m1, v1 = orc.adam_fwd(g, m, v, t, lr, b1, b2, eps)
+        assert rel_err(u, -lr * gd / (np.abs(gd) + eps)) < 1e-6  # fp32 state storage
+        m, v = m1.astype(np.float32), v1.astype(np.float32)
+
+
+def test_rmsprop_zero_point(orc):
+    """Reading Z6 for RMSProp: g = v = 0 gives dg = -lr du/eps, dv = alpha dv1."""
+    du = np.array([1.0, -3.0], np.float32)
+    dv1 = np.array([0.5, 2.0], np.float32)
+    z = np.zeros(2, np.float32)
+    r = orc.rmsprop_vjp(z, z, du, dv1, 0.1, 0.99, 1e-8)
+    np.testing.assert_allclose(r["dg"], -0.1 * du.astype(np.float64) / 1e-8, rtol=1e-12)
+    np.testing.assert_allclose(r["dv"], 0.99 * dv1.astype(np.float64), rtol=1e-15)
+
+
+def test_eps_zero_convention(orc):
+    """Reading Z7: eps = 0 and g = v = 0 -> u := 0 and finite backward."""
+    z = np.zeros(1, np.float32)
+    u, v1 = orc.rmsprop_fwd(z, z, 1.0, 0.99, 0.0)
+    assert u[0] == 0.0
+    r = orc.rmsprop_vjp(z, z, np.ones(1), np.ones(1), 1.0, 0.99, 0.0)
+    assert np.all(np.isfinite(r["dg"])) and r["dg"][0] == 0.0
+
+
+# ----------------------------------------- library routine: torch.optim
+def _torch_steps(opt_cls, kwargs, grads):
+    p = torch.zeros(grads[0].shape, dtype=torch.float64, requires_grad=True)
+    opt = opt_cls([p], **kwargs)
+    ups = []
+    for g in grads:
+        before = p.detach().clone()
+        p.grad = torch.as_tensor(g, dtype=torch.float64)
+        opt.step()
+        ups.append((p.detach() - before).numpy())
+    return ups, opt.state[p]
+
+
+def test_forward_matches_torch_optim_float64(orc):
+    """torch.optim.Adam / RMSprop / SGD (float64, CPU) are an
+    independent implementation of the same recurrences (eps outside the
+    sqrt, bias correction, dampening 0). Compared over 12 steps; the oracle
+    state is kept in float64 by exact float32 grads and fp64 chaining via
+    prec=0 outputs fed back through float32 only where exact."""
+    rng = np.random.default_rng(7)
+    grads = [(rng.standard_normal(257) * 10.0 ** rng.uniform(-4, 0, 257)).astype(np.float32)
+             for _ in range(12)]
+    # Adam: chain the oracle with float64 state by calling the complex forward
+    # (real inputs) which accepts float64 state exactly.
+    ups, _ = _torch_steps(torch.optim.Adam, dict(lr=1e-2, betas=(0.9, 0.999), eps=1e-8), grads)
+    m = v = np.zeros(257)
+    for t, g in enumerate(grads, 1):
+        u, m, v = (x.real for x in orc.adam_fwd_complex(g.astype(np.float64), m, v, t,
+                                                         [1e-2, 0.9, 0.999, 1e-8, 0.0]))
+        np.testing.assert_allclose(u, ups[t - 1], rtol=1e-9, atol=1e-300)
+    ups, _ = _torch_steps(torch.optim.RMSprop, dict(lr=1e-2, alpha=0.99, eps=1e-8), grads)
+    v = np.zeros(257)
+    for t, g in enumerate(grads, 1):
+        u, v = (x.real for x in orc.rmsprop_fwd_complex(g.astype(np.float64), v, [1e-2, 0.99, 1e-8]))
+        np.testing.assert_allclose(u, ups[t - 1], rtol=1e-9, atol=1e-300)
+    for nest in (False, True):
+        ups, _ = _torch_steps(torch.optim.SGD, dict(lr=0.1, momentum=0.9, nesterov=nest), grads)
+        b = np.zeros(257)
+        for t, g in enumerate(grads, 1):
+            u, b = (x.real for x in orc.sgd_fwd_complex(g.astype(np.float64), b, [0.1, 0.9], nest))
+            np.testing.assert_allclose(u, ups[t - 1], rtol=1e-9, atol=1e-300)
+
+
+def test_real_and_complex_forward_agree(orc):
+    """The float64 entry points and the complex128 entry points evaluate the
+    same template; on real inputs they must agree to rounding."""
+    x = synth.state_tree(3, [1000, 24])
+    u, m1, v1 = orc.adam_fwd(x["g"], x["m"], x["v"], 4, 1e-3, 0.9, 0.999, 1e-8)
+    uc, mc, vc = orc.adam_fwd_complex(x["g"], x["m"], x["v"], 4, [1e-3, 0.9, 0.999, 1e-8, 0])
+    np.testing.assert_array_equal(u, uc.real)
+    np.testing.assert_array_equal(m1, mc.real)
+
+
+# ---------------------------------------------- complex-step VJP pins
+def _state_inputs(seed, n, t_warm=True):
+    x = synth.state_tree(seed, [n // 2, n - n // 2], warm=t_warm, zero_frac=0.0)
+    return x
+
+
+@pytest.mark.parametrize("t", [1, 2, 7, 100])
+@pytest.mark.parametrize("eps_root", [0.0, 1e-10])
+def test_adam_vjp_vs_complex_step(orc, t, eps_root):
+    """every VJP output, including the four hyper-gradient sums,
+    equals the complex-step Jacobian of the (separately pinned) forward
+    contracted with the cotangents."""
+    x = _state_inputs(11 + t, 200, t_warm=(t > 1))
+    g, m, v, du, dm1, dv1 = (x[k] for k in ("g", "m", "v", "du", "dm1", "dv1"))
+    hp = np.array([0.05, 0.9, 0.999, 1e-8, eps_root])
+    gd = g.astype(np.float64)
+    md = np.zeros_like(gd) if m is None else m.astype(np.float64)
+    vd = np.zeros_like(gd) if v is None else v.astype(np.float64)
+    cot = (du.astype(np.float64), dm1.astype(np.float64), dv1.astype(np.float64))
+
+    def contract(outs):
+        return sum(c * o.imag / H for c, o in zip(cot, outs))
+
+    r = orc.adam_vjp(g, m, v, du, dm1, dv1, t, *hp, prec=1)
+    cs_g = contract(orc.adam_fwd_complex(gd + 1j * H, md, vd, t, hp))
+    cs_m = contract(orc.adam_fwd_complex(gd, md + 1j * H, vd, t, hp))
+    cs_v = contract(orc.adam_fwd_complex(gd, md, vd + 1j * H, t, hp))
+    scale = lambda a: np.abs(a) + 1e-12 * np.max(np.abs(a))
+    assert np.max(np.abs(r["dg"] - cs_g) / scale(cs_g)) < 1e-8
+    assert np.max(np.abs(r["dm"] - cs_m) / scale(cs_m)) < 1e-8
+    assert np.max(np.abs(r["dv"] - cs_v) / scale(cs_v)) < 1e-8
+    for k in range(4):  # lr, b1, b2, eps
+        hpc = hp.astype(np.complex128)
+        hpc[k] += 1j * H
+        cs = contract(orc.adam_fwd_complex(gd, md, vd, t, hpc)).sum()
+        assert r["dhp"][k] == pytest.approx(cs, rel=1e-8, abs=1e-10 * r["dhp_abs"][k] + 1e-300)
+
+
+def test_rmsprop_vjp_vs_complex_step(orc):
+    x = _state_inputs(5, 300)
+    g, v, du, dv1 = x["g"], x["v"], x["du"], x["dv1"]
+    hp = np.array([0.01, 0.95, 1e-8])
+    gd, vd = g.astype(np.float64), v.astype(np.float64)
+    cot = (du.astype(np.float64), dv1.astype(np.float64))
+    contract = lambda outs: sum(c * o.imag / H for c, o in zip(cot, outs))
+    r = orc.rmsprop_vjp(g, v, du, dv1, *hp, prec=1)
+    np.testing.assert_allclose(r["dg"], contract(orc.rmsprop_fwd_complex(gd + 1j * H, vd, hp)),
+                               rtol=1e-8)
+    np.testing.assert_allclose(r["dv"], contract(orc.rmsprop_fwd_complex(gd, vd + 1j * H, hp)),
+                               rtol=1e-8)
+    for k in range(3):
+        hpc = hp.astype(np.complex128)
+        hpc[k] += 1j * H
+        cs = contract(orc.rmsprop_fwd_complex(gd, vd, hpc)).sum()
+        assert r["dhp"][k] == pytest.approx(cs, rel=1e-8)
+
+
+@pytest.mark.parametrize("nesterov", [False, True])
+def test_sgd_vjp_vs_complex_step(orc, nesterov):
+    x = _state_inputs(9, 300)
+    g, b, du, db1 = x["g"], x["m"], x["du"], x["dm1"]
+    hp = np.array([0.1, 0.9])
+    gd, bd = g.astype(np.float64), b.astype(np.float64)
+    cot = (du.astype(np.float64), db1.astype(np.float64))
+    contract = lambda outs: sum(c * o.imag / H for c, o in zip(cot, outs))
+    r = orc.sgd_vjp(g, b, du, db1, *hp, nesterov=nesterov, prec=1)
+    np.testing.assert_allclose(r["dg"], contract(orc.sgd_fwd_complex(gd + 1j * H, bd, hp, nesterov)),
+                               rtol=1e-12)
+    np.testing.assert_allclose(r["db"], contract(orc.sgd_fwd_complex(gd, bd + 1j * H, hp, nesterov)),
+                               rtol=1e-12)
+    for k in range(2):
+        hpc = hp.astype(np.complex128)
+        hpc[k] += 1j * H
+        cs = contract(orc.sgd_fwd_complex(gd, bd, hpc, nesterov)).sum()
+        assert r["dhp"][k] == pytest.approx(cs, rel=1e-10)
+
+
+# ------------------------------------------------ finite differences
+def test_adam_vjp_vs_central_fd(orc):
+    """central differences in double on a few elements (an
+    independent numerical derivative, not reusing complex arithmetic)."""
+    x = _state_inputs(21, 8)
+    g, m, v = (x[k].astype(np.float64) for k in ("g", "m", "v"))
+    du = x["du"].astype(np.float64)
+    hp = [0.05, 0.9, 0.999, 1e-8, 0.0]
+    t = 5
+
+    def U(gg, mm, vv, h=hp):
+        return orc.adam_fwd_complex(gg, mm, vv, t, h)[0].real
+
+    r = orc.adam_vjp(x["g"], x["m"], x["v"], x["du"], None, None, t, *hp, prec=1)
+    for i in range(8):
+        e = np.zeros(8)
+        hstep = 1e-6 * max(abs(g[i]), 1e-6)
+        e[i] = hstep
+        fd = (U(g + e, m, v) - U(g - e, m, v))[i] / (2 * hstep) * du[i]
+        assert r["dg"][i] == pytest.approx(fd, rel=2e-5, abs=1e-9 * abs(du[i]))
+    hstep = 1e-7
+    for k, hk in ((0, 1e-7), (1, 1e-7), (2, 1e-7)):
+        hpp, hpm = list(hp), list(hp)
+        hpp[k] += hk
+        hpm[k] -= hk
+        fd = np.sum((U(g, m, v, hpp) - U(g, m, v, hpm)) / (2 * hk) * du)
+        assert r["dhp"][k] == pytest.approx(fd, rel=1e-5, abs=1e-6 * r["dhp_abs"][k])
+
+
+# ------------------------------------------------ algebraic properties
+def test_vjp_linear_in_cotangents_and_null_is_zero(orc):
+    """the VJP is linear in (du, dm1, dv1); a NULL cotangent is
+    bitwise the zero cotangent."""
+    x = synth.state_tree(31, [500, 12])
+    g, m, v, du, dm1, dv1 = (x[k] for k in ("g", "m", "v", "du", "dm1", "dv1"))
+    hp = (1e-3, 0.9, 0.999, 1e-8)
+    r_all = orc.adam_vjp(g, m, v, du, dm1, dv1, 10, *hp)
+    r_u = orc.adam_vjp(g, m, v, du, None, None, 10, *hp)
+    r_u0 = orc.adam_vjp(g, m, v, du, np.zeros_like(du), np.zeros_like(du), 10, *hp)
+    r_m = orc.adam_vjp(g, m, v, None, dm1, None, 10, *hp)
+    r_v = orc.adam_vjp(g, m, v, None, None, dv1, 10, *hp)
+    for k in ("dg", "dm", "dv"):
+        np.testing.assert_array_equal(r_u[k], r_u0[k])
+        s = r_u[k] + r_m[k] + r_v[k]
+        np.testing.assert_allclose(r_all[k], s, rtol=1e-9, atol=1e-9 * np.max(np.abs(s)))
+    np.testing.assert_allclose(r_all["dhp"], r_u["dhp"] + r_m["dhp"] + r_v["dhp"], rtol=1e-9,
+                               atol=1e-12 * np.max(r_all["dhp_abs"]))
+
+
+def test_per_leaf_sums_add_to_global(orc):
+    leaves = [5, 4096, 1, 300, 9000]
+    x = synth.state_tree(41, leaves)
+    off = synth.offsets_of(leaves)
+    r = orc.adam_vjp(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], 3, 1e-3, 0.9, 0.999,
+                     1e-8, offsets=off)
+    np.testing.assert_allclose(r["dhp_leaf"].sum(0), r["dhp"], rtol=1e-12,
+                               atol=1e-14 * r["dhp_abs"].max())
+    # each leaf's sum equals the global sum over that leaf alone
+    l = 3
+    sl = slice(off[l], off[l + 1])
+    r3 = orc.adam_vjp(x["g"][sl], x["m"][sl], x["v"][sl], x["du"][sl], x["dm1"][sl],
+                      x["dv1"][sl], 3, 1e-3, 0.9, 0.999, 1e-8)
+    np.testing.assert_allclose(r["dhp_leaf"][l], r3["dhp"], rtol=1e-13)
+
+
+def test_thread_count_independent(orc):
+    x = synth.state_tree(51, [70000])
+    args = (x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], 4, 1e-3, 0.9, 0.999, 1e-8)
+    orc.set_num_threads(1)
+    r1 = orc.adam_vjp(*args)
+    orc.set_num_threads(0)
+    r2 = orc.adam_vjp(*args)
+    orc.set_num_threads(1)
+    np.testing.assert_array_equal(r1["dhp"], r2["dhp"])
+    np.testing.assert_array_equal(r1["dg"], r2["dg"])
+
+
+# ---------------------------------------------------------- bf16 state
+def test_bf16_rne_against_hand_cases_and_torch(orc):
+    """Reading Z9: RNE to bf16. Hand cases: exact ties go to even; values
+    just above a tie go up. Float32-representable values must match torch's
+    float32 -> bfloat16 conversion (RNE)."""
+    one = 1.0
+    cases = {one + 2 ** -8: 0x3F80, one + 3 * 2 ** -8: 0x3F82, one + 2 ** -8 + 2 ** -30: 0x3F81,
+             -(one + 2 ** -8): 0xBF80, 0.0: 0x0000}
+    bits = orc.bf16_rne(np.array(list(cases.keys())))
+    assert [int(b) for b in bits] == list(cases.values())
+    rng = np.random.default_rng(0)
+    f = (rng.standard_normal(10000) * 10.0 ** rng.uniform(-20, 20, 10000)).astype(np.float32)
+    tb = torch.from_numpy(f).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    np.testing.assert_array_equal(orc.bf16_rne(f.astype(np.float64)), tb)
+
+
+def test_bf16_state_inputs_are_promoted_exactly(orc):
+    x = synth.state_tree(61, [1000])
+    mb, vb = synth.to_bf16_bits(x["m"]), synth.to_bf16_bits(x["v"])
+    u_b, m_b, v_b = orc.adam_fwd(x["g"], mb, vb, 10, 1e-3, 0.9, 0.999, 1e-8, state_bf16=True)
+    mf = orc.bf16_to_f64(mb).astype(np.float32)
+    vf = orc.bf16_to_f64(vb).astype(np.float32)
+    u_f, m_f, v_f = orc.adam_fwd(x["g"], mf, vf, 10, 1e-3, 0.9, 0.999, 1e-8)
+    np.testing.assert_array_equal(u_b, u_f)
+    np.testing.assert_array_equal(m_b, m_f)
+
+
+# ----------------------------------------------- K-step sweep (row a9)
+def _quad(seed, n):
+    return synth.quadratic_problem(seed, n)
+
+
+@pytest.mark.parametrize("K", [1, 3, 5, 10])
+def test_sweep_sgd_closed_form(orc, K):
+    """SURVEY P6 / S:281: plain SGD on 1/2 a (theta-phi)^2 gives
+    theta_K = phi + (1 - lr a)^K (theta0 - phi); so
+    phi_bar = (theta_K - y)(1 - (1-lr a)^K), theta0_bar = (theta_K - y)(1-lr a)^K,
+    lr_bar = sum (theta_K - y) * (-K a (1-lr a)^(K-1) (theta0 - phi))."""
+    q = _quad(3, 64)
+    a, th0, phi, y = (q[k].astype(np.float64) for k in ("a", "theta0", "phi", "y"))
+    for lr in (0.1, 0.5):
+        r = orc.sweep_quadratic("sgd", q["a"], q["theta0"], q["phi"], q["y"], K, [lr, 0.0, 0.0])
+        c = (1 - lr * a) ** K
+        thK = phi + c * (th0 - phi)
+        np.testing.assert_allclose(r["thetaK"], thK, rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(r["phi_bar"], (thK - y) * (1 - c), rtol=1e-10, atol=1e-13)
+        np.testing.assert_allclose(r["theta0_bar"], (thK - y) * c, rtol=1e-10, atol=1e-13)
+        lr_bar = np.sum((thK - y) * (-K * a * (1 - lr * a) ** (K - 1) * (th0 - phi)))
+        assert r["hyper_bar"][0] == pytest.approx(lr_bar, rel=1e-10)
+        assert r["loss"] == pytest.approx(0.5 * np.sum((thK - y) ** 2), rel=1e-12)
+
+
+@pytest.mark.parametrize("nesterov", [False, True])
+def test_sweep_momentum_closed_form(orc, nesterov):
+    """with momentum, [theta-phi; b] evolves by T = [[1-lr a, -lr mu],
+    [a, mu]] (Nesterov: [[1-lr a(1+mu), -lr mu^2], [a, mu]]); b_0 = 0 so
+    dtheta_K/dtheta0 = (T^K)_00 and dtheta_K/dphi = 1 - (T^K)_00."""
+    q = _quad(4, 32)
+    a, th0, phi, y = (q[k].astype(np.float64) for k in ("a", "theta0", "phi", "y"))
+    lr, mu, K = 0.2, 0.9, 5
+    r = orc.sweep_quadratic("sgd", q["a"], q["theta0"], q["phi"], q["y"], K,
+                            [lr, mu, 1.0 if nesterov else 0.0])
+    for i in range(32):
+        if nesterov:
+            T = np.array([[1 - lr * a[i] * (1 + mu), -lr * mu * mu], [a[i], mu]])
+        else:
+            T = np.array([[1 - lr * a[i], -lr * mu], [a[i], mu]])
+        c = np.linalg.matrix_power(T, K)[0, 0]
+        thK = phi[i] + c * (th0[i] - phi[i])
+        assert r["thetaK"][i] == pytest.approx(thK, rel=1e-12, abs=1e-14)
+        assert r["theta0_bar"][i] == pytest.approx((thK - y[i]) * c, rel=1e-10, abs=1e-13)
+        assert r["phi_bar"][i] == pytest.approx((thK - y[i]) * (1 - c), rel=1e-10, abs=1e-13)
+
+
+@pytest.mark.parametrize("kind,hp", [("adam", [1e-2, 0.9, 0.999, 1e-8, 0.0]),
+                                     ("rmsprop", [1e-2, 0.99, 1e-8]),
+                                     ("sgd", [0.1, 0.9, 0.0]), ("sgd", [0.1, 0.9, 1.0])])
+def test_sweep_vs_complex_step(orc, kind, hp):
+    """The reverse sweep (VJP of every step, in reverse, plus the quadratic's
+    Hessian) equals the complex-step derivative of the K-step forward map."""
+    K = 5
+    q = _quad(5, 40)
+    a, th0, phi, y = (q[k].astype(np.float64) for k in ("a", "theta0", "phi", "y"))
+    r = orc.sweep_quadratic(kind, q["a"], q["theta0"], q["phi"], q["y"], K, hp, prec=1)
+    nest = bool(hp[2]) if kind == "sgd" else False
+    hpf = hp[:2] if kind == "sgd" else hp
+    thK = orc.sweep_forward_complex(kind, a, th0, phi, K, hpf, nest).real
+    res = thK - y
+    d_phi = orc.sweep_forward_complex(kind, a, th0, phi + 1j * H, K, hpf, nest).imag / H
+    d_th0 = orc.sweep_forward_complex(kind, a, th0 + 1j * H, phi, K, hpf, nest).imag / H
+    np.testing.assert_allclose(r["phi_bar"], res * d_phi, rtol=1e-7, atol=1e-12)
+    np.testing.assert_allclose(r["theta0_bar"], res * d_th0, rtol=1e-7, atol=1e-12)
+    nh = {"adam": 4, "rmsprop": 3, "sgd": 2}[kind]
+    for k in range(nh):
+        hpc = np.array(hpf, dtype=np.complex128)
+        hpc[k] += 1j * H
+        cs = np.sum(res * orc.sweep_forward_complex(kind, a, th0, phi, K, hpc, nest).imag / H)
+        assert r["hyper_bar"][k] == pytest.approx(cs, rel=1e-7, abs=1e-9)
+
+
+def test_sweep_adam_vs_central_fd(orc):
+    """meta-gradient of a 5-step Adam inner loop matches central
+    finite differences over phi (rel <= 1e-4)."""
+    q = _quad(6, 6)
+    a, th0, phi, y = (q[k].astype(np.float64) for k in ("a", "theta0", "phi", "y"))
+    hp = [1e-2, 0.9, 0.999, 1e-8, 0.0]
+    r = orc.sweep_quadratic("adam", q["a"], q["theta0"], q["phi"], q["y"], 5, hp, prec=1)
+
+    def L(ph):
+        thK = orc.sweep_forward_complex("adam", a, th0, ph, 5, hp).real
+        return 0.5 * (thK - y) ** 2
+
+    h = 1e-6
+    fd = (L(phi + h) - L(phi - h)) / (2 * h)
+    np.testing.assert_allclose(r["phi_bar"], fd, rtol=1e-4, atol=1e-9)
