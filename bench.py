@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""Benchmark of the fused differentiable optimizer step (BASELINE.json metric
+"diff-Adam fwd+bwd GB/s & % HBM peak").
+
+Default workload (configs[1], C2): differentiable Adam forward + backward over
+a ResNet-18-shaped tree (62 leaves, 11,689,512 fp32 elements) in one
+multi-tensor launch each, warm state at t = 10, all cotangents supplied and
+the four hyper-gradient sums produced. One "step" = opt_adam_fwd +
+opt_adam_bwd through the C ABI. value = algorithmic bytes (60 B/elem:
+24 forward + 36 backward) / device time, summed over
+ranks (each rank runs its own tree: weak scaling, no data-path collective).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--compute default|f32|f64] [--workload c2|c1|c5] [--sizes ...]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+HBM_FALLBACK = 6650.0
+NOMINAL_HBM = 8000.0
+BYTES_FWD = 24   # g, m, v -> u, m', v'   (fp32)
+BYTES_BWD = 36   # g, m, v, du, dm', dv' -> dg, dm, dv
+HP = (1e-3, 0.9, 0.999, 1e-8, 0.0)
+STEP_T = 10
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the GPU works."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for nm, val in zip(names, r[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------- workloads
+def c2_inputs():
+    leaves = synth.RESNET18_LEAVES
+    return synth.state_tree(0xC2, leaves), synth.offsets_of(leaves), "C2 resnet18-tree"
+
+
+def c1_inputs():
+    x = synth.c1_inputs()
+    return x, np.array([0, x["g"].size], np.int64), "C1 flat-4096"
+
+
+def c5_inputs(n):
+    return synth.state_tree(0xC5, None, n=n), np.array([0, n], np.int64), f"C5 flat-{n}"
+
+
+class AdamWorkload:
+    """Device buffers for R rotating sets of one fwd+bwd step."""
+
+    def __init__(self, L, x, offsets, dev, sets, compute, bf16=False):
+        import torch
+
+        self.L, self.torch, self.dev, self.compute = L, torch, dev, compute
+        self.tree = L.Tree(offsets=offsets, device=dev)
+        self.n = self.tree.numel
+        self.sd = 1 if bf16 else 0
+        t = torch
+
+        def up(a, state=False):
+            if a is None:
+                return None
+            if state and bf16:
+                bits = synth.to_bf16_bits(a)
+                return t.from_numpy(bits.view(np.int16)).to(dev).view(t.bfloat16)
+            return t.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+        sdt = t.bfloat16 if bf16 else t.float32
+        self.sets = []
+        for _ in range(sets):
+            s = dict(g=up(x["g"]), m=up(x["m"], True), v=up(x["v"], True), du=up(x["du"]),
+                     dm1=up(x["dm1"]), dv1=up(x["dv1"]))
+            s.update(u=t.empty(self.n, device=dev), m1=t.empty(self.n, dtype=sdt, device=dev),
+                     v1=t.empty(self.n, dtype=sdt, device=dev), dg=t.empty(self.n, device=dev),
+                     dm=t.empty(self.n, device=dev), dv=t.empty(self.n, device=dev),
+                     dhp=t.empty(4, dtype=t.float64, device=dev))
+            self.sets.append(s)
+        self.ws = self.tree.workspace(dev)
+        bpe_state = 2 if bf16 else 4
+        self.bytes_fwd = self.n * (4 + 2 * bpe_state + 4 + 2 * bpe_state)
+        self.bytes_bwd = self.n * (4 + 2 * bpe_state + 12 + 12)
+
+    def fwd(self, s):
+        self.L.opt_adam_fwd(self.tree, STEP_T, HP, self.sd, self.compute, s["g"], s["m"], s["v"],
+                            s["u"], s["m1"], s["v1"])
+
+    def bwd(self, s):
+        self.L.opt_adam_bwd(self.tree, STEP_T, HP, self.sd, self.compute, s["g"], s["m"], s["v"],
+                            s["du"], s["dm1"], s["dv1"], s["dg"], s["dm"], s["dv"], s["dhp"],
+                            None, self.ws)
+
+
+def time_ours(args, workload_inputs, dev, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2211_06934_b200 import _lib as L
+
+    x, offsets, wname = workload_inputs
+    compute = {"default": 0, "f32": 1, "f64": 2}[args.compute]
+    n = int(offsets[-1])
+    # rotate buffer sets so no step re-reads what the previous one left in L2
+    bytes_per_set = n * 4 * 12
+    sets = max(2, min(8, int(np.ceil(3 * 126e6 / max(bytes_per_set, 1))) + 1))
+    W = AdamWorkload(L, x, offsets, dev, sets, compute, bf16=args.bf16)
+    stream = torch.cuda.current_stream()
+    sampler = ClockSampler(torch.cuda.current_device())
+
+    def step(i):
+        s = W.sets[i % sets]
+        W.fwd(s)
+        W.bwd(s)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    sampler.start()
+    # clock soak: keep the GPU busy ~0.5 s (untimed) so the sampler sees load
+    t_end = time.time() + 0.5
+    i = 0
+    while time.time() < t_end:
+        for _ in range(50):
+            step(i)
+            i += 1
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = L.opt_launch_count()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev[0].record(stream)
+    for k in range(args.steps):
+        s = W.sets[k % sets]
+        kev[k][0].record(stream)
+        W.fwd(s)
+        kev[k][1].record(stream)
+        W.bwd(s)
+        kev[k][2].record(stream)
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    launches = L.opt_launch_count() - launches0
+    ms = ev[0].elapsed_time(ev[1])
+    fwd_ms = [a.elapsed_time(b) for a, b, _ in kev]
+    bwd_ms = [b.elapsed_time(c) for _, b, c in kev]
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+
+    # end-to-end through the C ABI with host buffers (pinned), copies timed
+    e2e = time_e2e(args, W, dev)
+    return dict(ms=ms, fwd_ms=fwd_ms, bwd_ms=bwd_ms, clocks=clocks, launches=launches, W=W,
+                e2e=e2e, wname=wname, sets=sets)
+
+
+def time_e2e(args, W, dev):
+    import torch
+
+    t = torch
+    s0 = W.sets[0]
+    ins = ["g", "m", "v", "du", "dm1", "dv1"]
+    outs = ["u", "m1", "v1", "dg", "dm", "dv", "dhp"]
+    h_in = {k: s0[k].cpu().pin_memory() for k in ins}
+    h_out = {k: t.empty_like(s0[k], device="cpu").pin_memory() for k in outs}
+    stream = t.cuda.current_stream()
+    steps = max(3, min(args.steps, 20))
+
+    def one():
+        for k in ins:
+            s0[k].copy_(h_in[k], non_blocking=True)
+        W.fwd(s0)
+        W.bwd(s0)
+        for k in outs:
+            h_out[k].copy_(s0[k], non_blocking=True)
+
+    for _ in range(2):
+        one()
+    t.cuda.synchronize()
+    a, b = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        one()
+    b.record(stream)
+    t.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    h2d = sum(h_in[k].numel() * h_in[k].element_size() for k in ins)
+    d2h = sum(h_out[k].numel() * h_out[k].element_size() for k in outs)
+    return {"value": (W.bytes_fwd + W.bytes_bwd) / (ms * 1e-3) / 1e9, "unit": "GB/s",
+            "ms_per_step": ms, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "how": "C-ABI opt_adam_fwd/bwd on device buffers staged from pinned host memory; "
+                   "H2D of the 6 inputs and D2H of the 6 outputs + d_hp inside the timed region"}
+
+
+# --------------------------------------------------- CPU oracle timing
+def time_oracle(x, offsets, max_elems=None, threads=0):
+    """Oracle (as it stands, fp64) fwd + VJP on a bounded sample: whole
+    leaves of the same workload up to max_elems elements."""
+    import oracle
+
+    n = int(offsets[-1])
+    if max_elems is not None and max_elems < n:
+        n = max_elems
+    sl = slice(0, n)
+    xs = {k: (None if x[k] is None else x[k][sl]) for k in x}
+    used = oracle.set_num_threads(threads)
+    t0 = time.perf_counter()
+    oracle.adam_fwd(xs["g"], xs["m"], xs["v"], STEP_T, *HP)
+    oracle.adam_vjp(xs["g"], xs["m"], xs["v"], xs["du"], xs["dm1"], xs["dv1"], STEP_T, *HP)
+    dt = time.perf_counter() - t0
+    oracle.set_num_threads(1)
+    gbs = n * (BYTES_FWD + BYTES_BWD) / dt / 1e9
+    return dict(value=gbs, unit="GB/s", cores=used, kind="oracle", seconds=dt,
+                sample=f"first {n} of {int(offsets[-1])} elements of the same tree "
+                       f"(fwd + VJP, fp64, {used} threads)")
+
+
+def workload(args):
+    if args.workload == "c1":
+        return c1_inputs()
+    if args.workload == "c5":
+        return c5_inputs(args.size)
+    return c2_inputs()
+
+
+def traffic_from_profiles(wname, compute):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(f"{wname}|{compute}|bwd")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--compute", default="default", choices=["default", "f32", "f64"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c1", "c5"])
+    ap.add_argument("--size", type=int, default=1 << 24)
+    ap.add_argument("--bf16", action="store_true", help="bf16 optimizer state")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    wl = workload(args)
+    r = time_ours(args, wl, dev, rank, world)
+    W = r["W"]
+    ms_step = r["ms"] / args.steps
+    per_rank_bytes = W.bytes_fwd + W.bytes_bwd
+    value = world * per_rank_bytes * args.steps / (r["ms"] * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    bwd_avg = statistics.mean(r["bwd_ms"])
+    fwd_avg = statistics.mean(r["fwd_ms"])
+    achieved = W.bytes_bwd / (bwd_avg * 1e-3) / 1e9
+    compute_name = {"default": "f32", "f32": "f32", "f64": "f64"}[args.compute]
+    from paper_2211_06934_b200 import _lib as L
+    out = {
+        "metric": "diff-Adam fwd+bwd GB/s",
+        "value": round(value, 2),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": compute_name,
+        "data": "synthetic (seeded SplitMix64/Box-Muller; DESIGN.md input recipe)",
+        "config": {"workload": r["wname"] + " adam fwd+bwd", "numel": W.n,
+                   "n_leaves": W.tree.n_leaves, "state": "bf16" if args.bf16 else "f32",
+                   "compute": compute_name, "step_t": STEP_T,
+                   "l2": f"{r['sets']} rotating buffer sets of {W.n * 48 / 1e6:.0f} MB (> 126 MB L2)",
+                   "parallelism": f"replicas x{world} (no data-path collective)",
+                   "alg_bytes_per_step": per_rank_bytes},
+        "frac_of_measured_hbm": round(value / world / peak, 4),
+        "frac_of_nominal_8tbs": round(value / world / NOMINAL_HBM, 4),
+        "fwd_ms": round(fwd_avg, 5), "bwd_ms": round(bwd_avg, 5),
+        "fwd_gbs": round(W.bytes_fwd / (fwd_avg * 1e-3) / 1e9, 1),
+        "clocks": r["clocks"],
+        "e2e": r["e2e"],
+        "gpu_launches": r["launches"],
+        "roofline": {"bound": "hbm", "kernel": "step_uniform<AdamBwd> (opt_adam_bwd)",
+                     "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic_from_profiles(r["wname"], compute_name),
+                     "alg_bytes_per_launch": W.bytes_bwd},
+        "libdiffopt_abi": L.opt_abi_version(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        x, offsets, _ = wl
+        out["cpu_baseline"] = {k: v for k, v in time_oracle(x, offsets).items() if k != "seconds"}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def run_reference(args, world, rank):
+    """Reference arm: the oracle (CPU, fp64, all host cores) on a bounded
+    sample of the same workload, timed per step; rank 0 only."""
+    if rank != 0:
+        return
+    x, offsets, wname = workload(args)
+    n = int(offsets[-1])
+    sample = min(n, 1 << 21)
+    for _ in range(min(args.warmup, 1)):
+        time_oracle(x, offsets, sample)
+    times = []
+    info = None
+    for _ in range(args.steps if args.steps <= 5 else 5):
+        info = time_oracle(x, offsets, sample)
+        times.append(info["seconds"])
+    sec = statistics.median(times)
+    value = sample * (BYTES_FWD + BYTES_BWD) / sec / 1e9
+    out = {"metric": "diff-Adam fwd+bwd GB/s", "value": round(value, 3), "unit": "GB/s",
+           "impl": "reference", "n_gpus": world, "steps": len(times), "warmup": args.warmup,
+           "ms_per_step": round(sec * 1e3 * n / sample, 3), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": wname + " adam fwd+bwd", "numel": n},
+           "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": info["cores"],
+                            "kind": "oracle", "sample": info["sample"]},
+           "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,192 @@
+/* include/diffopt.h -- C ABI of the B200 fused differentiable optimizer step.
+ *
+ * What the library computes (PAPER.md = P:, SPEC.md = S:, SURVEY.md = SV):
+ *   The paper's "CPU/GPU-accelerated optimizers" take "the optimizer as a
+ *   whole instead of separating it into several basic operators", with the
+ *   forward and backward written by hand, "symbolic reduction" and explicit
+ *   0/0 cancellation (§2.3; contribution (2)(i), P:36 names SGD,
+ *   RMSProp and Adam). This library is that operator for sm_100a: one fused
+ *   pass over HBM for the update (forward) and one for its vector-Jacobian
+ *   product (backward) with respect to the gradient, the optimizer state and
+ *   the hyper-parameters. The update formulas are the standard ones quoted in
+ *   S:188 (Adam), S:196-204 (SGD-momentum), S:206 (RMSProp); every reading
+ *   of a point the paper leaves open is listed in DESIGN.md ("Readings").
+ *
+ * Data layout (SV §8(b), P:87 / P:248 tensor trees):
+ *   A tensor tree is flattened once on the host into ONE contiguous buffer
+ *   per role (gradient, each state slot, update, each cotangent). Leaves are
+ *   contiguous segments [offsets[l], offsets[l+1]) in depth-first leaf order
+ *   (S:123). All element arrays are indexed by the same flat index.
+ *   fp32 arrays are `float`; state arrays (mu, nu, momentum buffer) are
+ *   `float` when state_dtype == OPT_F32 and bf16 (`uint16_t` bit patterns)
+ *   when state_dtype == OPT_BF16 (reading Z9: only persistent state is
+ *   bf16; gradients, updates and all cotangents stay fp32).
+ *
+ * Conventions shared by every entry point:
+ *   - All array pointers are DEVICE pointers (cudaMalloc'd, or mapped host
+ *     memory) and must be 16-byte aligned (else OPT_EALIGN).
+ *   - A NULL state input means the zero state (opt.init); a NULL
+ *     cotangent means a zero cotangent (bitwise identical result); a NULL
+ *     output is not written.
+ *   - Exact aliasing of an output with the input it replaces is allowed
+ *     (mu_out == mu, nu_out == nu, updates == g, d_g == d_updates,
+ *     d_mu == d_mu_out, d_nu == d_nu_out, params_out == params); every element
+ *     is read before it is written. Any other overlap is undefined.
+ *   - The caller owns every buffer. The library allocates nothing, keeps no
+ *     per-call state, never synchronises the device and enqueues all work on
+ *     `stream` (a cudaStream_t; NULL = legacy default stream).
+ *   - Host-side validation runs before anything is enqueued; on error nothing
+ *     is launched and the thread-local message is set (opt_last_error).
+ *     Device-side NaN/Inf inputs propagate; they are not checked.
+ *   - numel == 0 is valid: nothing is launched except zeroing d_hp/d_hp_leaf
+ *     (cudaMemsetAsync on `stream`).
+ *   - Hyper-gradient outputs d_hp / d_hp_leaf are device double arrays that
+ *     are WRITTEN (not accumulated). Their reduction order is fixed, so they
+ *     are bitwise reproducible run to run on one device (reading Z12).
+ *   - Thread-safe and re-entrant; concurrent calls must not share a
+ *     workspace.
+ */
+#ifndef DIFFOPT_H
+#define DIFFOPT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DIFFOPT_ABI_VERSION 1
+
+typedef enum {
+  OPT_OK = 0,
+  OPT_EINVAL = 1,      /* invalid argument (hyper-parameter range, sizes, offsets) */
+  OPT_EALIGN = 2,      /* an array pointer is not 16-byte aligned */
+  OPT_ECUDA = 3,       /* a CUDA call or launch failed (message in opt_last_error) */
+  OPT_EWORKSPACE = 4   /* workspace missing or smaller than opt_workspace_bytes() */
+} opt_status;
+
+typedef enum { OPT_F32 = 0, OPT_BF16 = 1 } opt_state_dtype;
+
+/* Arithmetic precision inside the kernel. Storage is unchanged (fp32 arrays,
+ * state per opt_state_dtype); only the per-element arithmetic differs.
+ * OPT_COMPUTE_DEFAULT picks the library default. */
+typedef enum { OPT_COMPUTE_DEFAULT = 0, OPT_COMPUTE_F32 = 1, OPT_COMPUTE_F64 = 2 } opt_compute;
+
+/* The flattened tree (SV §8(a) row a1). offsets has n_leaves + 1 int64
+ * entries, offsets[0] = 0, non-decreasing, offsets[n_leaves] = numel.
+ * h_offsets (host) is always required when n_leaves > 0; d_offsets (device
+ * copy of the same values) is required only when per-leaf outputs are
+ * requested. n_leaves == 0 means "one leaf of numel elements". Caller-owned. */
+typedef struct {
+  int64_t numel;
+  int64_t n_leaves;
+  const int64_t* h_offsets;
+  const int64_t* d_offsets;
+} opt_tree;
+
+/* Adam: m' = b1 m + (1-b1) g ; v' = b2 v + (1-b2) g^2 ;
+ *   u = -lr (m'/(1-b1^t)) / (sqrt(v'/(1-b2^t) + eps_root) + eps).
+ * Valid: lr finite, 0 <= b1 < 1, 0 <= b2 < 1, eps >= 0, eps_root >= 0. */
+typedef struct { double lr, b1, b2, eps, eps_root; } opt_adam_hp;
+/* RMSProp: v' = alpha v + (1-alpha) g^2 ; u = -lr g/(sqrt(v') + eps).
+ * Valid: lr finite, 0 <= alpha < 1, eps >= 0. */
+typedef struct { double lr, alpha, eps; } opt_rmsprop_hp;
+/* SGD: b' = momentum b + g ; u = -lr b' (nesterov: -lr (g + momentum b')).
+ * Valid: lr finite, 0 <= momentum < 1. */
+typedef struct { double lr, momentum; int nesterov; } opt_sgd_hp;
+
+/* Bytes of device workspace a backward call needs (per_leaf != 0 when
+ * d_hp_leaf will be requested). The workspace must be zero-filled once
+ * when allocated; every call leaves it zero-filled again. Returns 0 and
+ * sets opt_last_error on an invalid tree. */
+size_t opt_workspace_bytes(const opt_tree* tree, int per_leaf);
+
+/* ------------------------------------------------------------------ Adam
+ * Forward (SV §8(a) row a3). Reads g, mu, nu (+ params); writes updates,
+ * mu_out, nu_out and, when params and params_out are both non-NULL,
+ * params_out = params + updates (apply_updates fused; updates may then
+ * be NULL). step = t >= 1 (reading Z3).
+ * Returns OPT_OK / OPT_EINVAL / OPT_EALIGN / OPT_ECUDA. */
+int opt_adam_fwd(const opt_tree* tree, int64_t step, const opt_adam_hp* hp,
+                 int state_dtype, int compute,
+                 const float* g, const void* mu, const void* nu,
+                 float* updates, void* mu_out, void* nu_out,
+                 const float* params, float* params_out, void* stream);
+
+/* Backward (VJP; SV §8(a) rows a4, a5). Given the forward's inputs g, mu, nu
+ * and the cotangents d_updates, d_mu_out, d_nu_out of its outputs, writes
+ * d_g, d_mu, d_nu (fp32) and, if non-NULL, d_hp[4] = (lr, b1, b2, eps)
+ * hyper-gradients summed over all elements, and d_hp_leaf[n_leaves][4] the
+ * same sums per leaf (needs tree->d_offsets; at most 4096 leaves). eps_root
+ * is not differentiated. workspace: see opt_workspace_bytes. */
+int opt_adam_bwd(const opt_tree* tree, int64_t step, const opt_adam_hp* hp,
+                 int state_dtype, int compute,
+                 const float* g, const void* mu, const void* nu,
+                 const float* d_updates, const float* d_mu_out, const float* d_nu_out,
+                 float* d_g, float* d_mu, float* d_nu,
+                 double* d_hp, double* d_hp_leaf,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* --------------------------------------------------------------- RMSProp
+ * As Adam with one state array nu; d_hp[3] = (lr, alpha, eps). */
+int opt_rmsprop_fwd(const opt_tree* tree, const opt_rmsprop_hp* hp,
+                    int state_dtype, int compute,
+                    const float* g, const void* nu,
+                    float* updates, void* nu_out,
+                    const float* params, float* params_out, void* stream);
+
+int opt_rmsprop_bwd(const opt_tree* tree, const opt_rmsprop_hp* hp,
+                    int state_dtype, int compute,
+                    const float* g, const void* nu,
+                    const float* d_updates, const float* d_nu_out,
+                    float* d_g, float* d_nu,
+                    double* d_hp, double* d_hp_leaf,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------- SGD
+ * State = momentum buffer (may be NULL on input = zero buffer; mom_out may
+ * be NULL when momentum == 0). d_hp[2] = (lr, momentum). */
+int opt_sgd_fwd(const opt_tree* tree, const opt_sgd_hp* hp,
+                int state_dtype, int compute,
+                const float* g, const void* mom,
+                float* updates, void* mom_out,
+                const float* params, float* params_out, void* stream);
+
+int opt_sgd_bwd(const opt_tree* tree, const opt_sgd_hp* hp,
+                int state_dtype, int compute,
+                const float* g, const void* mom,
+                const float* d_updates, const float* d_mom_out,
+                float* d_g, float* d_mom,
+                double* d_hp, double* d_hp_leaf,
+                void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------- apply_updates (row a8)
+ * out = params + updates (out may alias params). Its VJP is the identity. */
+int opt_apply_updates(int64_t numel, const float* params, const float* updates,
+                      float* out, void* stream);
+
+/* ------------------------------------- unrolled-sweep workload (row a9)
+ * The synthetic inner loss of DESIGN.md "Input recipe" (C3), L_in =
+ * 1/2 sum a_i (theta_i - phi_i)^2, whose gradient and Hessian-vector
+ * product a real model would get from autograd:
+ *   opt_quadratic_grad: g = a (theta - phi)
+ *   opt_quadratic_rev:  theta_bar += a g_bar ; phi_bar -= a g_bar   (in place) */
+int opt_quadratic_grad(int64_t numel, const float* a, const float* theta,
+                       const float* phi, float* g, void* stream);
+int opt_quadratic_rev(int64_t numel, const float* a, const float* g_bar,
+                      float* theta_bar, float* phi_bar, void* stream);
+
+/* -------------------------------------------------------------- misc */
+const char* opt_status_string(int status);
+/* Message of the last failing call on this host thread ("" if none). */
+const char* opt_last_error(void);
+int opt_abi_version(void);
+/* Kernel launches this library has enqueued in this process (all threads);
+ * used by bench.py to report gpu_launches. */
+int64_t opt_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DIFFOPT_H */

@@ -1,0 +1,230 @@
+"""Thin ctypes binding of include/diffopt.h (argument marshalling only).
+
+Every function here has the name of the C entry point it calls and forwards
+device pointers (``tensor.data_ptr()``), sizes, hyper-parameters and the
+current CUDA stream. All arithmetic happens in libdiffopt.so. There is no CPU
+fallback: if the library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdiffopt.so")
+
+OPT_OK, OPT_EINVAL, OPT_EALIGN, OPT_ECUDA, OPT_EWORKSPACE = 0, 1, 2, 3, 4
+OPT_F32, OPT_BF16 = 0, 1
+OPT_COMPUTE_DEFAULT, OPT_COMPUTE_F32, OPT_COMPUTE_F64 = 0, 1, 2
+
+EXPORTS = [
+    "opt_workspace_bytes", "opt_adam_fwd", "opt_adam_bwd", "opt_rmsprop_fwd", "opt_rmsprop_bwd",
+    "opt_sgd_fwd", "opt_sgd_bwd", "opt_apply_updates", "opt_quadratic_grad", "opt_quadratic_rev",
+    "opt_status_string", "opt_last_error", "opt_abi_version", "opt_launch_count",
+]
+
+
+class opt_tree(ctypes.Structure):
+    _fields_ = [("numel", ctypes.c_int64), ("n_leaves", ctypes.c_int64),
+                ("h_offsets", ctypes.c_void_p), ("d_offsets", ctypes.c_void_p)]
+
+
+class opt_adam_hp(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_double) for k in ("lr", "b1", "b2", "eps", "eps_root")]
+
+
+class opt_rmsprop_hp(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_double) for k in ("lr", "alpha", "eps")]
+
+
+class opt_sgd_hp(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_double), ("momentum", ctypes.c_double), ("nesterov", ctypes.c_int)]
+
+
+class DiffoptError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_status_name(code)}: {msg}")
+        self.code = code
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2211_06934_b200.build` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    P, i64, I, sz, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t, ctypes.c_double
+    T = ctypes.POINTER(opt_tree)
+    L.opt_workspace_bytes.argtypes = [T, I]
+    L.opt_workspace_bytes.restype = sz
+    L.opt_adam_fwd.argtypes = [T, i64, ctypes.POINTER(opt_adam_hp), I, I] + [P] * 9
+    L.opt_adam_bwd.argtypes = [T, i64, ctypes.POINTER(opt_adam_hp), I, I] + [P] * 12 + [sz, P]
+    L.opt_rmsprop_fwd.argtypes = [T, ctypes.POINTER(opt_rmsprop_hp), I, I] + [P] * 7
+    L.opt_rmsprop_bwd.argtypes = [T, ctypes.POINTER(opt_rmsprop_hp), I, I] + [P] * 9 + [sz, P]
+    L.opt_sgd_fwd.argtypes = [T, ctypes.POINTER(opt_sgd_hp), I, I] + [P] * 7
+    L.opt_sgd_bwd.argtypes = [T, ctypes.POINTER(opt_sgd_hp), I, I] + [P] * 9 + [sz, P]
+    L.opt_apply_updates.argtypes = [i64, P, P, P, P]
+    L.opt_quadratic_grad.argtypes = [i64, P, P, P, P, P]
+    L.opt_quadratic_rev.argtypes = [i64, P, P, P, P, P]
+    L.opt_status_string.argtypes = [I]
+    L.opt_status_string.restype = ctypes.c_char_p
+    L.opt_last_error.restype = ctypes.c_char_p
+    L.opt_abi_version.restype = I
+    L.opt_launch_count.restype = i64
+    for name in ("opt_adam_fwd", "opt_adam_bwd", "opt_rmsprop_fwd", "opt_rmsprop_bwd",
+                 "opt_sgd_fwd", "opt_sgd_bwd", "opt_apply_updates", "opt_quadratic_grad",
+                 "opt_quadratic_rev"):
+        getattr(L, name).restype = I
+    return L
+
+
+lib = _load()
+
+
+def _status_name(code):
+    return lib.opt_status_string(int(code)).decode()
+
+
+def _check(rc):
+    if rc != OPT_OK:
+        raise DiffoptError(rc, lib.opt_last_error().decode())
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class Tree:
+    """A flattened tensor tree: numel and leaf offsets (host + device copy).
+
+    ``offsets`` is [0, n_0, n_0+n_1, ..., numel]."""
+
+    def __init__(self, numel=None, offsets=None, device=None):
+        if offsets is None:
+            offsets = [0, int(numel)]
+        self.h_offsets = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+        self.numel = int(self.h_offsets[-1])
+        self.n_leaves = len(self.h_offsets) - 1
+        self.sizes = np.diff(self.h_offsets).tolist()
+        self.d_offsets = None
+        if device is not None and torch.device(device).type == "cuda":
+            self.d_offsets = torch.from_numpy(self.h_offsets).to(device)
+        self.c = opt_tree(self.numel, self.n_leaves, self.h_offsets.ctypes.data,
+                          _ptr(self.d_offsets))
+
+    @classmethod
+    def from_sizes(cls, sizes, device=None):
+        off = np.zeros(len(sizes) + 1, dtype=np.int64)
+        off[1:] = np.cumsum(np.asarray(sizes, dtype=np.int64))
+        return cls(offsets=off, device=device)
+
+    def workspace_bytes(self, per_leaf=False):
+        n = lib.opt_workspace_bytes(ctypes.byref(self.c), int(bool(per_leaf)))
+        if n == 0:
+            raise DiffoptError(OPT_EINVAL, lib.opt_last_error().decode())
+        return int(n)
+
+    def workspace(self, device, per_leaf=False):
+        """Zero-filled workspace (diffopt.h: zero once; calls leave it zero)."""
+        nbytes = self.workspace_bytes(per_leaf)
+        return torch.zeros((nbytes + 7) // 8, dtype=torch.float64, device=device)
+
+
+def _ws(ws):
+    if ws is None:
+        return None, 0
+    return ws.data_ptr(), ws.numel() * ws.element_size()
+
+
+# ------------------------------------------------------------- entry points
+def opt_adam_fwd(tree, step, hp, state_dtype, compute, g, mu, nu, updates, mu_out, nu_out,
+                 params=None, params_out=None, stream=None):
+    h = opt_adam_hp(*hp) if not isinstance(hp, opt_adam_hp) else hp
+    _check(lib.opt_adam_fwd(ctypes.byref(tree.c), int(step), ctypes.byref(h), int(state_dtype),
+                            int(compute), _ptr(g), _ptr(mu), _ptr(nu), _ptr(updates),
+                            _ptr(mu_out), _ptr(nu_out), _ptr(params), _ptr(params_out),
+                            _stream(stream)))
+
+
+def opt_adam_bwd(tree, step, hp, state_dtype, compute, g, mu, nu, d_updates, d_mu_out,
+                 d_nu_out, d_g, d_mu, d_nu, d_hp=None, d_hp_leaf=None, workspace=None,
+                 stream=None):
+    h = opt_adam_hp(*hp) if not isinstance(hp, opt_adam_hp) else hp
+    wp, wb = _ws(workspace)
+    _check(lib.opt_adam_bwd(ctypes.byref(tree.c), int(step), ctypes.byref(h), int(state_dtype),
+                            int(compute), _ptr(g), _ptr(mu), _ptr(nu), _ptr(d_updates),
+                            _ptr(d_mu_out), _ptr(d_nu_out), _ptr(d_g), _ptr(d_mu), _ptr(d_nu),
+                            _ptr(d_hp), _ptr(d_hp_leaf), wp, wb, _stream(stream)))
+
+
+def opt_rmsprop_fwd(tree, hp, state_dtype, compute, g, nu, updates, nu_out, params=None,
+                    params_out=None, stream=None):
+    h = opt_rmsprop_hp(*hp) if not isinstance(hp, opt_rmsprop_hp) else hp
+    _check(lib.opt_rmsprop_fwd(ctypes.byref(tree.c), ctypes.byref(h), int(state_dtype),
+                               int(compute), _ptr(g), _ptr(nu), _ptr(updates), _ptr(nu_out),
+                               _ptr(params), _ptr(params_out), _stream(stream)))
+
+
+def opt_rmsprop_bwd(tree, hp, state_dtype, compute, g, nu, d_updates, d_nu_out, d_g, d_nu,
+                    d_hp=None, d_hp_leaf=None, workspace=None, stream=None):
+    h = opt_rmsprop_hp(*hp) if not isinstance(hp, opt_rmsprop_hp) else hp
+    wp, wb = _ws(workspace)
+    _check(lib.opt_rmsprop_bwd(ctypes.byref(tree.c), ctypes.byref(h), int(state_dtype),
+                               int(compute), _ptr(g), _ptr(nu), _ptr(d_updates), _ptr(d_nu_out),
+                               _ptr(d_g), _ptr(d_nu), _ptr(d_hp), _ptr(d_hp_leaf), wp, wb,
+                               _stream(stream)))
+
+
+def opt_sgd_fwd(tree, hp, state_dtype, compute, g, mom, updates, mom_out, params=None,
+                params_out=None, stream=None):
+    h = opt_sgd_hp(hp[0], hp[1], int(bool(hp[2]))) if not isinstance(hp, opt_sgd_hp) else hp
+    _check(lib.opt_sgd_fwd(ctypes.byref(tree.c), ctypes.byref(h), int(state_dtype), int(compute),
+                           _ptr(g), _ptr(mom), _ptr(updates), _ptr(mom_out), _ptr(params),
+                           _ptr(params_out), _stream(stream)))
+
+
+def opt_sgd_bwd(tree, hp, state_dtype, compute, g, mom, d_updates, d_mom_out, d_g, d_mom,
+                d_hp=None, d_hp_leaf=None, workspace=None, stream=None):
+    h = opt_sgd_hp(hp[0], hp[1], int(bool(hp[2]))) if not isinstance(hp, opt_sgd_hp) else hp
+    wp, wb = _ws(workspace)
+    _check(lib.opt_sgd_bwd(ctypes.byref(tree.c), ctypes.byref(h), int(state_dtype), int(compute),
+                           _ptr(g), _ptr(mom), _ptr(d_updates), _ptr(d_mom_out), _ptr(d_g),
+                           _ptr(d_mom), _ptr(d_hp), _ptr(d_hp_leaf), wp, wb, _stream(stream)))
+
+
+def opt_apply_updates(numel, params, updates, out, stream=None):
+    _check(lib.opt_apply_updates(int(numel), _ptr(params), _ptr(updates), _ptr(out),
+                                 _stream(stream)))
+
+
+def opt_quadratic_grad(numel, a, theta, phi, g, stream=None):
+    _check(lib.opt_quadratic_grad(int(numel), _ptr(a), _ptr(theta), _ptr(phi), _ptr(g),
+                                  _stream(stream)))
+
+
+def opt_quadratic_rev(numel, a, g_bar, theta_bar, phi_bar, stream=None):
+    _check(lib.opt_quadratic_rev(int(numel), _ptr(a), _ptr(g_bar), _ptr(theta_bar),
+                                 _ptr(phi_bar), _stream(stream)))
+
+
+def opt_launch_count():
+    return int(lib.opt_launch_count())
+
+
+def opt_abi_version():
+    return int(lib.opt_abi_version())

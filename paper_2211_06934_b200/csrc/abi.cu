@@ -1,0 +1,598 @@
+// abi.cu -- host side of the C ABI declared in include/diffopt.h.
+//
+// Validation, per-step scalar precompute in double,
+// kernel selection (op x state dtype x compute precision x reduction mode)
+// and launch on the caller's stream. No allocation, no synchronisation.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "diffopt.h"
+#include "step_kernel.cuh"
+
+using namespace dopt;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+constexpr int64_t kMaxGrid = 4096;       // upper bound on blocks of any launch
+constexpr size_t kCounterBytes = 256;    // workspace head (ticket counter)
+constexpr int kNhMax = 4;
+constexpr int kDefaultCompute = OPT_COMPUTE_F32;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+bool misaligned(const void* p) { return p && (reinterpret_cast<uintptr_t>(p) & 15u); }
+
+int check_align(std::initializer_list<const void*> ps) {
+  int k = 0;
+  for (const void* p : ps) {
+    if (misaligned(p)) return fail(OPT_EALIGN, "array argument #%d (%p) is not 16-byte aligned", k, p);
+    ++k;
+  }
+  return OPT_OK;
+}
+
+// Tree validation (row a1): offsets monotone, [0] = 0, [n] = numel.
+int check_tree(const opt_tree* t) {
+  if (!t) return fail(OPT_EINVAL, "tree is NULL");
+  if (t->numel < 0) return fail(OPT_EINVAL, "numel < 0");
+  if (t->n_leaves < 0) return fail(OPT_EINVAL, "n_leaves < 0");
+  if (t->n_leaves > 0) {
+    if (!t->h_offsets) return fail(OPT_EINVAL, "h_offsets is NULL with n_leaves > 0");
+    if (t->h_offsets[0] != 0) return fail(OPT_EINVAL, "offsets[0] != 0");
+    for (int64_t l = 0; l < t->n_leaves; ++l)
+      if (t->h_offsets[l + 1] < t->h_offsets[l])
+        return fail(OPT_EINVAL, "offsets decrease at leaf %lld", (long long)l);
+    if (t->h_offsets[t->n_leaves] != t->numel)
+      return fail(OPT_EINVAL, "offsets[n_leaves] = %lld != numel = %lld",
+                  (long long)t->h_offsets[t->n_leaves], (long long)t->numel);
+  }
+  return OPT_OK;
+}
+
+int64_t count_tiles(const opt_tree* t) {
+  int64_t n = 0;
+  for (int64_t l = 0; l < t->n_leaves; ++l)
+    n += (t->h_offsets[l + 1] - t->h_offsets[l] + kTile - 1) / kTile;
+  return n;
+}
+
+bool finite(double x) { return std::isfinite(x); }
+bool unit(double b) { return finite(b) && b >= 0.0 && b < 1.0; }
+
+int resolve_compute(int compute, int* ct) {
+  if (compute == OPT_COMPUTE_DEFAULT) compute = kDefaultCompute;
+  if (compute != OPT_COMPUTE_F32 && compute != OPT_COMPUTE_F64)
+    return fail(OPT_EINVAL, "compute = %d is not an opt_compute", compute);
+  *ct = compute;
+  return OPT_OK;
+}
+
+int check_state_dtype(int sd) {
+  if (sd != OPT_F32 && sd != OPT_BF16)
+    return fail(OPT_EINVAL, "state_dtype = %d is not an opt_state_dtype", sd);
+  return OPT_OK;
+}
+
+// Persistent grid: SMs x resident blocks of this kernel, capped by work.
+template <class K>
+int grid_for(K kernel, int64_t work_blocks, size_t smem, int* grid) {
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, smem);
+  if (e != cudaSuccess) return fail(OPT_ECUDA, "device query failed: %s", cudaGetErrorString(e));
+  int64_t g = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  if (g > kMaxGrid) g = kMaxGrid;
+  if (work_blocks < g) g = work_blocks;
+  *grid = (int)(g > 0 ? g : 1);
+  return OPT_OK;
+}
+
+int launched(cudaStream_t) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(OPT_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return OPT_OK;
+}
+
+// Workspace and reduction plumbing shared by the three backward ops.
+struct Reduce {
+  double* d_hp;
+  double* d_hp_leaf;
+  bool leaf;
+  int64_t n_tiles;
+  double* partials;
+  unsigned int* counter;
+};
+
+int setup_reduce(const opt_tree* t, int nh, double* d_hp, double* d_hp_leaf, void* ws,
+                 size_t ws_bytes, Reduce* r) {
+  r->d_hp = d_hp;
+  r->d_hp_leaf = d_hp_leaf;
+  r->leaf = d_hp_leaf != nullptr;
+  r->n_tiles = 0;
+  r->partials = nullptr;
+  r->counter = nullptr;
+  if (!d_hp && !d_hp_leaf) return OPT_OK;
+  if (r->leaf) {
+    if (t->n_leaves < 1) return fail(OPT_EINVAL, "d_hp_leaf needs n_leaves >= 1");
+    if (t->n_leaves > kMaxLeafSmem)
+      return fail(OPT_EINVAL, "d_hp_leaf supports at most %d leaves (got %lld)", kMaxLeafSmem,
+                  (long long)t->n_leaves);
+    if (!t->d_offsets) return fail(OPT_EINVAL, "d_hp_leaf needs tree->d_offsets");
+    r->n_tiles = count_tiles(t);
+  }
+  size_t need = opt_workspace_bytes(t, r->leaf ? 1 : 0);
+  if (!ws || ws_bytes < need)
+    return fail(OPT_EWORKSPACE, "workspace %p of %zu bytes; need %zu", ws, ws_bytes, need);
+  if (reinterpret_cast<uintptr_t>(ws) & 15u) return fail(OPT_EALIGN, "workspace not 16-byte aligned");
+  (void)nh;
+  r->counter = static_cast<unsigned int*>(ws);
+  r->partials = reinterpret_cast<double*>(static_cast<char*>(ws) + kCounterBytes);
+  return OPT_OK;
+}
+
+int zero_outputs(const opt_tree* t, int nh, double* d_hp, double* d_hp_leaf, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
+  if (d_hp) e = cudaMemsetAsync(d_hp, 0, sizeof(double) * nh, s);
+  if (e == cudaSuccess && d_hp_leaf && t->n_leaves > 0)
+    e = cudaMemsetAsync(d_hp_leaf, 0, sizeof(double) * nh * t->n_leaves, s);
+  if (e != cudaSuccess) return fail(OPT_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(e));
+  return OPT_OK;
+}
+
+// Launch an op (forward: no reduction) with state type ST.
+template <class Op, class ST, int U>
+int launch_fwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, cudaStream_t s) {
+  auto k = step_uniform<Op, ST, U>;
+  int grid = 0;
+  int64_t work = ((a.numel >> 2) + kBlock - 1) / kBlock + 1;
+  int rc = grid_for(k, work, 0, &grid);
+  if (rc) return rc;
+  k<<<grid, kBlock, 0, s>>>(op, a);
+  return launched(s);
+}
+
+template <class Op, class ST, int U>
+int launch_bwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r,
+               const opt_tree* t, cudaStream_t s) {
+  a.d_hp = r.d_hp;
+  a.d_hp_leaf = r.d_hp_leaf;
+  a.partials = r.partials;
+  a.counter = r.counter;
+  a.want_hp = (r.d_hp || r.d_hp_leaf) ? 1 : 0;
+  if (r.leaf) {
+    a.offsets = t->d_offsets;
+    a.n_leaves = t->n_leaves;
+    a.n_tiles = r.n_tiles;
+    auto k = step_leaf<Op, ST, U>;
+    size_t smem = sizeof(int64_t) * 2 * (size_t)(t->n_leaves + 1);
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return fail(OPT_ECUDA, "smem attribute: %s", cudaGetErrorString(e));
+    }
+    int grid = 0;
+    int rc = grid_for(k, r.n_tiles, smem, &grid);
+    if (rc) return rc;
+    k<<<grid, kBlock, smem, s>>>(op, a);
+    return launched(s);
+  }
+  auto k = step_uniform<Op, ST, U>;
+  int grid = 0;
+  int64_t work = ((a.numel >> 2) + kBlock - 1) / kBlock + 1;
+  int rc = grid_for(k, work, 0, &grid);
+  if (rc) return rc;
+  k<<<grid, kBlock, 0, s>>>(op, a);
+  return launched(s);
+}
+
+// Dispatch on (state dtype, compute precision).
+template <template <class> class OpT, bool kBwd, class Fill>
+int dispatch(int state_dtype, int ct, StepArgs<OpT<float>::NIN, OpT<float>::NOUT>& a,
+             const Reduce* r, const opt_tree* t, cudaStream_t s, Fill fill) {
+  constexpr int U = 2;
+  if (ct == OPT_COMPUTE_F64) {
+    OpT<double> op;
+    fill(op);
+    if (state_dtype == OPT_BF16) {
+      if constexpr (kBwd) return launch_bwd<OpT<double>, bf16, U>(op, a, *r, t, s);
+      else return launch_fwd<OpT<double>, bf16, U>(op, a, s);
+    }
+    if constexpr (kBwd) return launch_bwd<OpT<double>, float, U>(op, a, *r, t, s);
+    else return launch_fwd<OpT<double>, float, U>(op, a, s);
+  }
+  OpT<float> op;
+  fill(op);
+  if (state_dtype == OPT_BF16) {
+    if constexpr (kBwd) return launch_bwd<OpT<float>, bf16, U>(op, a, *r, t, s);
+    else return launch_fwd<OpT<float>, bf16, U>(op, a, s);
+  }
+  if constexpr (kBwd) return launch_bwd<OpT<float>, float, U>(op, a, *r, t, s);
+  else return launch_fwd<OpT<float>, float, U>(op, a, s);
+}
+
+// b^t by repeated squaring in double (exact integer power).
+double ipow(double b, int64_t t) {
+  double r = 1.0, x = b;
+  while (t > 0) {
+    if (t & 1) r *= x;
+    x *= x;
+    t >>= 1;
+  }
+  return r;
+}
+
+int check_adam(int64_t step, const opt_adam_hp* hp) {
+  if (!hp) return fail(OPT_EINVAL, "hp is NULL");
+  if (step < 1) return fail(OPT_EINVAL, "step = %lld < 1", (long long)step);
+  if (!finite(hp->lr)) return fail(OPT_EINVAL, "lr is not finite");
+  if (!unit(hp->b1)) return fail(OPT_EINVAL, "b1 = %g outside [0, 1)", hp->b1);
+  if (!unit(hp->b2)) return fail(OPT_EINVAL, "b2 = %g outside [0, 1)", hp->b2);
+  if (!(finite(hp->eps) && hp->eps >= 0)) return fail(OPT_EINVAL, "eps = %g < 0", hp->eps);
+  if (!(finite(hp->eps_root) && hp->eps_root >= 0))
+    return fail(OPT_EINVAL, "eps_root = %g < 0", hp->eps_root);
+  return OPT_OK;
+}
+
+int check_rms(const opt_rmsprop_hp* hp) {
+  if (!hp) return fail(OPT_EINVAL, "hp is NULL");
+  if (!finite(hp->lr)) return fail(OPT_EINVAL, "lr is not finite");
+  if (!unit(hp->alpha)) return fail(OPT_EINVAL, "alpha = %g outside [0, 1)", hp->alpha);
+  if (!(finite(hp->eps) && hp->eps >= 0)) return fail(OPT_EINVAL, "eps = %g < 0", hp->eps);
+  return OPT_OK;
+}
+
+int check_sgd(const opt_sgd_hp* hp) {
+  if (!hp) return fail(OPT_EINVAL, "hp is NULL");
+  if (!finite(hp->lr)) return fail(OPT_EINVAL, "lr is not finite");
+  if (!unit(hp->momentum)) return fail(OPT_EINVAL, "momentum = %g outside [0, 1)", hp->momentum);
+  return OPT_OK;
+}
+
+#define TRY(x)                \
+  do {                        \
+    int rc_ = (x);            \
+    if (rc_) return rc_;      \
+  } while (0)
+
+}  // namespace
+
+extern "C" {
+
+size_t opt_workspace_bytes(const opt_tree* tree, int per_leaf) {
+  if (check_tree(tree)) return 0;
+  int64_t slots = kMaxGrid;
+  if (per_leaf) {
+    int64_t nt = count_tiles(tree);
+    if (nt > slots) slots = nt;
+  }
+  return kCounterBytes + sizeof(double) * kNhMax * (size_t)slots;
+}
+
+// ------------------------------------------------------------------ Adam
+int opt_adam_fwd(const opt_tree* tree, int64_t step, const opt_adam_hp* hp, int state_dtype,
+                 int compute, const float* g, const void* mu, const void* nu, float* updates,
+                 void* mu_out, void* nu_out, const float* params, float* params_out,
+                 void* stream) {
+  g_err.clear();
+  int ct = 0;
+  TRY(check_tree(tree));
+  TRY(check_adam(step, hp));
+  TRY(check_state_dtype(state_dtype));
+  TRY(resolve_compute(compute, &ct));
+  TRY(check_align({g, mu, nu, updates, mu_out, nu_out, params, params_out}));
+  if (tree->numel == 0) return OPT_OK;
+  if (!g) return fail(OPT_EINVAL, "g is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const double b1 = hp->b1, b2 = hp->b2;
+  const double bc1 = 1.0 - ipow(b1, step), bc2 = 1.0 - ipow(b2, step);
+  StepArgs<4, 4> a{};
+  a.in[0] = g; a.in[1] = mu; a.in[2] = nu; a.in[3] = (params && params_out) ? params : nullptr;
+  a.out[0] = updates; a.out[1] = mu_out; a.out[2] = nu_out;
+  a.out[3] = (params && params_out) ? params_out : nullptr;
+  a.numel = tree->numel;
+  return dispatch<AdamFwd, false>(state_dtype, ct, a, nullptr, tree, s, [&](auto& op) {
+    typedef typename std::remove_reference<decltype(op)>::type::CT CT;
+    op.b1 = (CT)b1; op.om1 = (CT)(1.0 - b1); op.b2 = (CT)b2; op.om2 = (CT)(1.0 - b2);
+    op.ibc1 = (CT)(1.0 / bc1); op.ibc2 = (CT)(1.0 / bc2); op.lr = (CT)hp->lr;
+    op.eps = (CT)hp->eps; op.eps_root = (CT)hp->eps_root;
+  });
+}
+
+int opt_adam_bwd(const opt_tree* tree, int64_t step, const opt_adam_hp* hp, int state_dtype,
+                 int compute, const float* g, const void* mu, const void* nu,
+                 const float* d_updates, const float* d_mu_out, const float* d_nu_out,
+                 float* d_g, float* d_mu, float* d_nu, double* d_hp, double* d_hp_leaf,
+                 void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  int ct = 0;
+  TRY(check_tree(tree));
+  TRY(check_adam(step, hp));
+  TRY(check_state_dtype(state_dtype));
+  TRY(resolve_compute(compute, &ct));
+  TRY(check_align({g, mu, nu, d_updates, d_mu_out, d_nu_out, d_g, d_mu, d_nu}));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (tree->numel == 0) return zero_outputs(tree, 4, d_hp, d_hp_leaf, s);
+  if (!g) return fail(OPT_EINVAL, "g is NULL");
+  Reduce r;
+  TRY(setup_reduce(tree, 4, d_hp, d_hp_leaf, workspace, workspace_bytes, &r));
+  // Per-step constants in double (row a2), rounded once to the compute type.
+  const double b1 = hp->b1, b2 = hp->b2, t = (double)step;
+  const double p1 = ipow(b1, step), p2 = ipow(b2, step);
+  const double p1m = ipow(b1, step - 1), p2m = ipow(b2, step - 1);
+  const double bc1 = 1.0 - p1, bc2 = 1.0 - p2;
+  // d mhat/d b1 = m K1 - g K2 ; d vhat/d b2 = v K3 - g^2 K4
+  const double K1 = (1.0 - p1 + t * p1) / (bc1 * bc1);
+  const double K2 = (1.0 - p1 - t * p1m * (1.0 - b1)) / (bc1 * bc1);
+  const double K3 = (1.0 - p2 + t * p2) / (bc2 * bc2);
+  const double K4 = (1.0 - p2 - t * p2m * (1.0 - b2)) / (bc2 * bc2);
+  StepArgs<6, 3> a{};
+  a.in[0] = g; a.in[1] = mu; a.in[2] = nu; a.in[3] = d_updates; a.in[4] = d_mu_out;
+  a.in[5] = d_nu_out;
+  a.out[0] = d_g; a.out[1] = d_mu; a.out[2] = d_nu;
+  a.numel = tree->numel;
+  return dispatch<AdamBwd, true>(state_dtype, ct, a, &r, tree, s, [&](auto& op) {
+    typedef typename std::remove_reference<decltype(op)>::type::CT CT;
+    op.b1 = (CT)b1; op.om1 = (CT)(1.0 - b1); op.b2 = (CT)b2; op.two_om2 = (CT)(2.0 * (1.0 - b2));
+    op.A = (CT)((1.0 - b1) / bc1); op.C = (CT)((1.0 - b2) / bc2);
+    op.ibc1 = (CT)(1.0 / bc1); op.ibc2 = (CT)(1.0 / bc2);
+    op.b1ibc1 = (CT)(b1 / bc1); op.b2ibc2 = (CT)(b2 / bc2);
+    op.eps_root = (CT)hp->eps_root; op.lr = (CT)hp->lr; op.eps = (CT)hp->eps;
+    op.K1 = (CT)K1; op.K2 = (CT)K2; op.K3 = (CT)K3; op.K4 = (CT)K4;
+  });
+}
+
+// --------------------------------------------------------------- RMSProp
+int opt_rmsprop_fwd(const opt_tree* tree, const opt_rmsprop_hp* hp, int state_dtype,
+                    int compute, const float* g, const void* nu, float* updates, void* nu_out,
+                    const float* params, float* params_out, void* stream) {
+  g_err.clear();
+  int ct = 0;
+  TRY(check_tree(tree));
+  TRY(check_rms(hp));
+  TRY(check_state_dtype(state_dtype));
+  TRY(resolve_compute(compute, &ct));
+  TRY(check_align({g, nu, updates, nu_out, params, params_out}));
+  if (tree->numel == 0) return OPT_OK;
+  if (!g) return fail(OPT_EINVAL, "g is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  StepArgs<3, 3> a{};
+  a.in[0] = g; a.in[1] = nu; a.in[2] = (params && params_out) ? params : nullptr;
+  a.out[0] = updates; a.out[1] = nu_out; a.out[2] = (params && params_out) ? params_out : nullptr;
+  a.numel = tree->numel;
+  return dispatch<RmsFwd, false>(state_dtype, ct, a, nullptr, tree, s, [&](auto& op) {
+    typedef typename std::remove_reference<decltype(op)>::type::CT CT;
+    op.alpha = (CT)hp->alpha; op.oma = (CT)(1.0 - hp->alpha); op.lr = (CT)hp->lr;
+    op.eps = (CT)hp->eps;
+  });
+}
+
+int opt_rmsprop_bwd(const opt_tree* tree, const opt_rmsprop_hp* hp, int state_dtype,
+                    int compute, const float* g, const void* nu, const float* d_updates,
+                    const float* d_nu_out, float* d_g, float* d_nu, double* d_hp,
+                    double* d_hp_leaf, void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  int ct = 0;
+  TRY(check_tree(tree));
+  TRY(check_rms(hp));
+  TRY(check_state_dtype(state_dtype));
+  TRY(resolve_compute(compute, &ct));
+  TRY(check_align({g, nu, d_updates, d_nu_out, d_g, d_nu}));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (tree->numel == 0) return zero_outputs(tree, 3, d_hp, d_hp_leaf, s);
+  if (!g) return fail(OPT_EINVAL, "g is NULL");
+  Reduce r;
+  TRY(setup_reduce(tree, 3, d_hp, d_hp_leaf, workspace, workspace_bytes, &r));
+  StepArgs<4, 2> a{};
+  a.in[0] = g; a.in[1] = nu; a.in[2] = d_updates; a.in[3] = d_nu_out;
+  a.out[0] = d_g; a.out[1] = d_nu;
+  a.numel = tree->numel;
+  return dispatch<RmsBwd, true>(state_dtype, ct, a, &r, tree, s, [&](auto& op) {
+    typedef typename std::remove_reference<decltype(op)>::type::CT CT;
+    op.alpha = (CT)hp->alpha; op.oma = (CT)(1.0 - hp->alpha);
+    op.two_oma = (CT)(2.0 * (1.0 - hp->alpha)); op.lr = (CT)hp->lr; op.eps = (CT)hp->eps;
+  });
+}
+
+// ------------------------------------------------------------------- SGD
+int opt_sgd_fwd(const opt_tree* tree, const opt_sgd_hp* hp, int state_dtype, int compute,
+                const float* g, const void* mom, float* updates, void* mom_out,
+                const float* params, float* params_out, void* stream) {
+  g_err.clear();
+  int ct = 0;
+  TRY(check_tree(tree));
+  TRY(check_sgd(hp));
+  TRY(check_state_dtype(state_dtype));
+  TRY(resolve_compute(compute, &ct));
+  TRY(check_align({g, mom, updates, mom_out, params, params_out}));
+  if (tree->numel == 0) return OPT_OK;
+  if (!g) return fail(OPT_EINVAL, "g is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  StepArgs<3, 3> a{};
+  a.in[0] = g; a.in[1] = mom; a.in[2] = (params && params_out) ? params : nullptr;
+  a.out[0] = updates; a.out[1] = mom_out; a.out[2] = (params && params_out) ? params_out : nullptr;
+  a.numel = tree->numel;
+  return dispatch<SgdFwd, false>(state_dtype, ct, a, nullptr, tree, s, [&](auto& op) {
+    typedef typename std::remove_reference<decltype(op)>::type::CT CT;
+    op.lr = (CT)hp->lr; op.mu = (CT)hp->momentum; op.nesterov = hp->nesterov ? 1 : 0;
+  });
+}
+
+int opt_sgd_bwd(const opt_tree* tree, const opt_sgd_hp* hp, int state_dtype, int compute,
+                const float* g, const void* mom, const float* d_updates, const float* d_mom_out,
+                float* d_g, float* d_mom, double* d_hp, double* d_hp_leaf, void* workspace,
+                size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  int ct = 0;
+  TRY(check_tree(tree));
+  TRY(check_sgd(hp));
+  TRY(check_state_dtype(state_dtype));
+  TRY(resolve_compute(compute, &ct));
+  TRY(check_align({g, mom, d_updates, d_mom_out, d_g, d_mom}));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (tree->numel == 0) return zero_outputs(tree, 2, d_hp, d_hp_leaf, s);
+  if (!g) return fail(OPT_EINVAL, "g is NULL");
+  Reduce r;
+  TRY(setup_reduce(tree, 2, d_hp, d_hp_leaf, workspace, workspace_bytes, &r));
+  StepArgs<4, 2> a{};
+  a.in[0] = g; a.in[1] = mom; a.in[2] = d_updates; a.in[3] = d_mom_out;
+  a.out[0] = d_g; a.out[1] = d_mom;
+  a.numel = tree->numel;
+  return dispatch<SgdBwd, true>(state_dtype, ct, a, &r, tree, s, [&](auto& op) {
+    typedef typename std::remove_reference<decltype(op)>::type::CT CT;
+    op.lr = (CT)hp->lr; op.mu = (CT)hp->momentum; op.nesterov = hp->nesterov ? 1 : 0;
+  });
+}
+
+// -------------------------------------------------------- misc / glue
+const char* opt_status_string(int status) {
+  switch (status) {
+    case OPT_OK: return "OPT_OK";
+    case OPT_EINVAL: return "OPT_EINVAL: invalid argument";
+    case OPT_EALIGN: return "OPT_EALIGN: pointer not 16-byte aligned";
+    case OPT_ECUDA: return "OPT_ECUDA: CUDA error";
+    case OPT_EWORKSPACE: return "OPT_EWORKSPACE: workspace too small";
+    default: return "unknown opt_status";
+  }
+}
+
+const char* opt_last_error(void) { return g_err.c_str(); }
+int opt_abi_version(void) { return DIFFOPT_ABI_VERSION; }
+int64_t opt_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"
+
+// ------------------------------------------------------ glue kernels
+// apply_updates (row a8) and the synthetic quadratic inner loss of row a9.
+namespace {
+
+__global__ void __launch_bounds__(kBlock) apply_kernel(int64_t n, const float* __restrict__ p,
+                                                       const float* __restrict__ u,
+                                                       float* out) {
+  const int64_t nvec = n >> 2, stride = (int64_t)gridDim.x * kBlock;
+  for (int64_t v = (int64_t)blockIdx.x * kBlock + threadIdx.x; v < nvec; v += stride) {
+    float a[4], b[4];
+    load4(p, v, a);
+    load4(u, v, b);
+    const float o[4] = {a[0] + b[0], a[1] + b[1], a[2] + b[2], a[3] + b[3]};
+    store4(out, v, o);
+  }
+  const int64_t i = (nvec << 2) + threadIdx.x;
+  if (blockIdx.x == gridDim.x - 1 && i < n) out[i] = p[i] + u[i];
+}
+
+__global__ void __launch_bounds__(kBlock) quad_grad_kernel(int64_t n, const float* __restrict__ a,
+                                                           const float* __restrict__ th,
+                                                           const float* __restrict__ phi,
+                                                           float* g) {
+  const int64_t nvec = n >> 2, stride = (int64_t)gridDim.x * kBlock;
+  for (int64_t v = (int64_t)blockIdx.x * kBlock + threadIdx.x; v < nvec; v += stride) {
+    float x[4], t[4], p[4];
+    load4(a, v, x);
+    load4(th, v, t);
+    load4(phi, v, p);
+    const float o[4] = {x[0] * (t[0] - p[0]), x[1] * (t[1] - p[1]), x[2] * (t[2] - p[2]),
+                        x[3] * (t[3] - p[3])};
+    store4(g, v, o);
+  }
+  const int64_t i = (nvec << 2) + threadIdx.x;
+  if (blockIdx.x == gridDim.x - 1 && i < n) g[i] = a[i] * (th[i] - phi[i]);
+}
+
+__global__ void __launch_bounds__(kBlock) quad_rev_kernel(int64_t n, const float* __restrict__ a,
+                                                          const float* __restrict__ gb,
+                                                          float* thb, float* phib) {
+  const int64_t nvec = n >> 2, stride = (int64_t)gridDim.x * kBlock;
+  for (int64_t v = (int64_t)blockIdx.x * kBlock + threadIdx.x; v < nvec; v += stride) {
+    float x[4], g[4], t[4], p[4];
+    load4(a, v, x);
+    load4(gb, v, g);
+    load4(thb, v, t);
+    load4(phib, v, p);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float ag = x[e] * g[e];
+      t[e] += ag;
+      p[e] -= ag;
+    }
+    store4(thb, v, t);
+    store4(phib, v, p);
+  }
+  const int64_t i = (nvec << 2) + threadIdx.x;
+  if (blockIdx.x == gridDim.x - 1 && i < n) {
+    const float ag = a[i] * gb[i];
+    thb[i] += ag;
+    phib[i] -= ag;
+  }
+}
+
+template <class K>
+int glue_launch(K kernel, int64_t n, cudaStream_t s, int* grid) {
+  return grid_for(kernel, ((n >> 2) + kBlock - 1) / kBlock + 1, 0, grid);
+}
+
+}  // namespace
+
+extern "C" {
+
+int opt_apply_updates(int64_t numel, const float* params, const float* updates, float* out,
+                      void* stream) {
+  g_err.clear();
+  if (numel < 0) return fail(OPT_EINVAL, "numel < 0");
+  TRY(check_align({params, updates, out}));
+  if (numel == 0) return OPT_OK;
+  if (!params || !updates || !out) return fail(OPT_EINVAL, "NULL array");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int grid = 0;
+  TRY(glue_launch(apply_kernel, numel, s, &grid));
+  apply_kernel<<<grid, kBlock, 0, s>>>(numel, params, updates, out);
+  return launched(s);
+}
+
+int opt_quadratic_grad(int64_t numel, const float* a, const float* theta, const float* phi,
+                       float* g, void* stream) {
+  g_err.clear();
+  if (numel < 0) return fail(OPT_EINVAL, "numel < 0");
+  TRY(check_align({a, theta, phi, g}));
+  if (numel == 0) return OPT_OK;
+  if (!a || !theta || !phi || !g) return fail(OPT_EINVAL, "NULL array");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int grid = 0;
+  TRY(glue_launch(quad_grad_kernel, numel, s, &grid));
+  quad_grad_kernel<<<grid, kBlock, 0, s>>>(numel, a, theta, phi, g);
+  return launched(s);
+}
+
+int opt_quadratic_rev(int64_t numel, const float* a, const float* g_bar, float* theta_bar,
+                      float* phi_bar, void* stream) {
+  g_err.clear();
+  if (numel < 0) return fail(OPT_EINVAL, "numel < 0");
+  TRY(check_align({a, g_bar, theta_bar, phi_bar}));
+  if (numel == 0) return OPT_OK;
+  if (!a || !g_bar || !theta_bar || !phi_bar) return fail(OPT_EINVAL, "NULL array");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int grid = 0;
+  TRY(glue_launch(quad_rev_kernel, numel, s, &grid));
+  quad_rev_kernel<<<grid, kBlock, 0, s>>>(numel, a, g_bar, theta_bar, phi_bar);
+  return launched(s);
+}
+
+}  // extern "C"

@@ -1,0 +1,354 @@
+"""Differentiable optimizer steps as torch.autograd.Functions over flat buffers,
+and the functional API of PAPER.md Listing 1:
+
+    opt = adam(lr=1e-3)
+    state = opt.init(params)
+    updates, state = opt.update(grads, state, inplace=False)
+    params = apply_updates(params, updates)
+
+Every forward and backward is one call into libdiffopt.so (the C ABI); this
+module only allocates outputs (torch caching allocator), picks the current
+stream and wires autograd ("we define the forward and backward
+behavior using torch.autograd.Function"). Hyper-parameters may be Python
+floats or CPU scalar tensors; a tensor that requires grad receives the
+kernel's hyper-gradient sum.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+from torch.autograd.function import once_differentiable
+
+from . import _lib as L
+
+_WS = {}
+
+
+def _workspace(tree: L.Tree, device, per_leaf=False):
+    """Per (device, stream, tree size) zeroed workspace, reused across calls
+    (the library leaves it zero-filled)."""
+    stream = torch.cuda.current_stream(device).cuda_stream
+    nbytes = tree.workspace_bytes(per_leaf)
+    key = (str(device), stream, nbytes)
+    ws = _WS.get(key)
+    if ws is None:
+        ws = tree.workspace(device, per_leaf)
+        _WS[key] = ws
+    return ws
+
+
+def _f(x):
+    return float(x.detach().item()) if isinstance(x, torch.Tensor) else float(x)
+
+
+def _needs(x):
+    return isinstance(x, torch.Tensor) and x.requires_grad
+
+
+def _hp_grad(x, val):
+    if not _needs(x):
+        return None
+    return val.to(device=x.device, dtype=x.dtype).reshape(x.shape)
+
+
+def _state_dtype(t):
+    if t is None:
+        return None
+    if t.dtype == torch.bfloat16:
+        return L.OPT_BF16
+    if t.dtype == torch.float32:
+        return L.OPT_F32
+    raise TypeError(f"state must be float32 or bfloat16, got {t.dtype}")
+
+
+def _sd(*states, default=L.OPT_F32):
+    for s in states:
+        if s is not None:
+            return _state_dtype(s)
+    return default
+
+
+def _empty_state(like, sd):
+    return torch.empty_like(like, dtype=torch.bfloat16 if sd == L.OPT_BF16 else torch.float32)
+
+
+def _contig(t):
+    return None if t is None else t.contiguous()
+
+
+@dataclass
+class StepConfig:
+    tree: L.Tree
+    compute: int = L.OPT_COMPUTE_DEFAULT
+    state_dtype: Optional[int] = None   # None: follow the input state (fp32 if none)
+
+
+# ------------------------------------------------------------------ Adam
+class AdamStep(torch.autograd.Function):
+    """(g, mu, nu[, params]) -> (updates or params + updates, mu', nu')."""
+
+    @staticmethod
+    def forward(ctx, g, mu, nu, params, lr, b1, b2, eps, step, eps_root, cfg):
+        g, mu, nu, params = _contig(g), _contig(mu), _contig(nu), _contig(params)
+        sd = cfg.state_dtype if cfg.state_dtype is not None else _sd(mu, nu)
+        hp = (_f(lr), _f(b1), _f(b2), _f(eps), float(eps_root))
+        out = torch.empty_like(g)
+        mu1, nu1 = _empty_state(g, sd), _empty_state(g, sd)
+        fused = params is not None
+        L.opt_adam_fwd(cfg.tree, step, hp, sd, cfg.compute, g, mu, nu,
+                       None if fused else out, mu1, nu1,
+                       params if fused else None, out if fused else None)
+        ctx.save_for_backward(g, mu, nu)
+        ctx.meta = (hp, step, sd, cfg, fused, (lr, b1, b2, eps), mu is None, nu is None)
+        return out, mu1, nu1
+
+    @staticmethod
+    @once_differentiable
+    def backward(ctx, d_out, d_mu1, d_nu1):
+        g, mu, nu = ctx.saved_tensors
+        hp, step, sd, cfg, fused, hps, mu_none, nu_none = ctx.meta
+        want_hp = any(_needs(x) for x in hps)
+        d_g = torch.empty_like(g)
+        d_mu = None if mu_none or not ctx.needs_input_grad[1] else torch.empty_like(g)
+        d_nu = None if nu_none or not ctx.needs_input_grad[2] else torch.empty_like(g)
+        d_hp = torch.empty(4, dtype=torch.float64, device=g.device) if want_hp else None
+        ws = _workspace(cfg.tree, g.device) if want_hp else None
+        L.opt_adam_bwd(cfg.tree, step, hp, sd, cfg.compute, g, mu, nu, _contig(d_out),
+                       _contig(d_mu1), _contig(d_nu1), d_g, d_mu, d_nu, d_hp, None, ws)
+        d_params = d_out if fused else None
+        hg = [None] * 4 if d_hp is None else [_hp_grad(x, d_hp[k]) for k, x in enumerate(hps)]
+        return (d_g, d_mu, d_nu, d_params, *hg, None, None, None)
+
+
+# --------------------------------------------------------------- RMSProp
+class RmsPropStep(torch.autograd.Function):
+    """(g, nu[, params]) -> (updates or params + updates, nu')."""
+
+    @staticmethod
+    def forward(ctx, g, nu, params, lr, alpha, eps, cfg):
+        g, nu, params = _contig(g), _contig(nu), _contig(params)
+        sd = cfg.state_dtype if cfg.state_dtype is not None else _sd(nu)
+        hp = (_f(lr), _f(alpha), _f(eps))
+        out = torch.empty_like(g)
+        nu1 = _empty_state(g, sd)
+        fused = params is not None
+        L.opt_rmsprop_fwd(cfg.tree, hp, sd, cfg.compute, g, nu, None if fused else out, nu1,
+                          params if fused else None, out if fused else None)
+        ctx.save_for_backward(g, nu)
+        ctx.meta = (hp, sd, cfg, fused, (lr, alpha, eps), nu is None)
+        return out, nu1
+
+    @staticmethod
+    @once_differentiable
+    def backward(ctx, d_out, d_nu1):
+        g, nu = ctx.saved_tensors
+        hp, sd, cfg, fused, hps, nu_none = ctx.meta
+        want_hp = any(_needs(x) for x in hps)
+        d_g = torch.empty_like(g)
+        d_nu = None if nu_none or not ctx.needs_input_grad[1] else torch.empty_like(g)
+        d_hp = torch.empty(3, dtype=torch.float64, device=g.device) if want_hp else None
+        ws = _workspace(cfg.tree, g.device) if want_hp else None
+        L.opt_rmsprop_bwd(cfg.tree, hp, sd, cfg.compute, g, nu, _contig(d_out), _contig(d_nu1),
+                          d_g, d_nu, d_hp, None, ws)
+        hg = [None] * 3 if d_hp is None else [_hp_grad(x, d_hp[k]) for k, x in enumerate(hps)]
+        return (d_g, d_nu, d_out if fused else None, *hg, None)
+
+
+# ------------------------------------------------------------------- SGD
+class SgdStep(torch.autograd.Function):
+    """(g, mom[, params]) -> (updates or params + updates, mom')."""
+
+    @staticmethod
+    def forward(ctx, g, mom, params, lr, momentum, nesterov, cfg):
+        g, mom, params = _contig(g), _contig(mom), _contig(params)
+        sd = cfg.state_dtype if cfg.state_dtype is not None else _sd(mom)
+        hp = (_f(lr), _f(momentum), bool(nesterov))
+        out = torch.empty_like(g)
+        has_state = hp[1] != 0.0
+        mom1 = _empty_state(g, sd) if has_state else None
+        fused = params is not None
+        L.opt_sgd_fwd(cfg.tree, hp, sd, cfg.compute, g, mom, None if fused else out, mom1,
+                      params if fused else None, out if fused else None)
+        ctx.save_for_backward(g, mom)
+        ctx.meta = (hp, sd, cfg, fused, (lr, momentum), mom is None)
+        if mom1 is None:
+            mom1 = g.new_zeros(0)
+        return out, mom1
+
+    @staticmethod
+    @once_differentiable
+    def backward(ctx, d_out, d_mom1):
+        g, mom = ctx.saved_tensors
+        hp, sd, cfg, fused, hps, mom_none = ctx.meta
+        want_hp = any(_needs(x) for x in hps)
+        if d_mom1 is not None and d_mom1.numel() == 0:
+            d_mom1 = None
+        d_g = torch.empty_like(g)
+        d_mom = None if mom_none or not ctx.needs_input_grad[1] else torch.empty_like(g)
+        d_hp = torch.empty(2, dtype=torch.float64, device=g.device) if want_hp else None
+        ws = _workspace(cfg.tree, g.device) if want_hp else None
+        L.opt_sgd_bwd(cfg.tree, hp, sd, cfg.compute, g, mom, _contig(d_out), _contig(d_mom1),
+                      d_g, d_mom, d_hp, None, ws)
+        hg = [None] * 2 if d_hp is None else [_hp_grad(x, d_hp[k]) for k, x in enumerate(hps)]
+        return (d_g, d_mom, d_out if fused else None, *hg, None, None)
+
+
+class ApplyUpdates(torch.autograd.Function):
+    """params + updates (row a8); backward is the identity for both."""
+
+    @staticmethod
+    def forward(ctx, params, updates):
+        p, u = params.contiguous(), updates.contiguous()
+        out = torch.empty_like(p)
+        L.opt_apply_updates(p.numel(), p, u, out)
+        return out
+
+    @staticmethod
+    @once_differentiable
+    def backward(ctx, d):
+        return d, d
+
+
+# ------------------------------------------------ functional (Listing 1)
+class FlatTree:
+    """Host description of a tensor tree flattened to one buffer per role
+    (leaves in depth-first order). ``views(flat)`` returns the leaf
+    views of a flat buffer via one ``split`` whose autograd backward is a
+    single concatenation (no per-leaf scatter)."""
+
+    def __init__(self, shapes, device):
+        self.shapes = [tuple(s) for s in shapes]
+        self.sizes = [int(torch.Size(s).numel()) for s in self.shapes]
+        self.tree = L.Tree.from_sizes(self.sizes, device=device)
+        self.device = device
+
+    @classmethod
+    def of(cls, tensors):
+        tensors = list(tensors)
+        return cls([t.shape for t in tensors], tensors[0].device)
+
+    def flatten(self, tensors):
+        return torch.cat([t.reshape(-1) for t in tensors])
+
+    def views(self, flat):
+        return [p.view(s) for p, s in zip(torch.split(flat, self.sizes), self.shapes)]
+
+
+@dataclass
+class OptState:
+    step: int
+    slots: tuple          # flat state buffers (or None = zero state)
+    layout: FlatTree
+
+
+class GradientTransformation:
+    """init/update pair. ``update`` accepts a flat gradient
+    buffer or a sequence of leaf gradients (flattened once into one buffer)."""
+
+    def __init__(self, kind, hp, n_slots, compute=L.OPT_COMPUTE_DEFAULT, state_dtype=L.OPT_F32):
+        self.kind, self.hp, self.n_slots = kind, hp, n_slots
+        self.compute, self.state_dtype = compute, state_dtype
+
+    def init(self, params):
+        """Zero state. Slots are None until the first update: the
+        kernel reads a NULL state as zeros (no HBM read)."""
+        if isinstance(params, torch.Tensor):
+            layout = FlatTree([params.shape], params.device)
+        else:
+            layout = FlatTree.of(params)
+        return OptState(0, (None,) * self.n_slots, layout)
+
+    def update(self, grads, state: OptState, inplace: bool = False, params=None):
+        differentiable = torch.is_grad_enabled()
+        if inplace and differentiable and _any_requires_grad(grads, state):
+            # in-place update would destroy the state the VJP needs
+            raise RuntimeError("inplace=True is not allowed with a differentiable update")
+        layout = state.layout
+        flat = grads if isinstance(grads, torch.Tensor) and grads.dim() == 1 \
+            and len(layout.sizes) == 1 else layout.flatten(grads)
+        cfg = StepConfig(layout.tree, self.compute, self.state_dtype)
+        t = state.step + 1
+        flat_p = None
+        if params is not None:
+            flat_p = params if isinstance(params, torch.Tensor) else layout.flatten(params)
+        if self.kind == "adam":
+            lr, b1, b2, eps, eps_root = self.hp
+            out, m1, v1 = AdamStep.apply(flat, state.slots[0], state.slots[1], flat_p, lr, b1,
+                                         b2, eps, t, eps_root, cfg)
+            slots = (m1, v1)
+        elif self.kind == "rmsprop":
+            lr, alpha, eps = self.hp
+            out, v1 = RmsPropStep.apply(flat, state.slots[0], flat_p, lr, alpha, eps, cfg)
+            slots = (v1,)
+        else:
+            lr, mom, nest = self.hp
+            out, b1 = SgdStep.apply(flat, state.slots[0] if state.slots else None, flat_p, lr,
+                                    mom, nest, cfg)
+            slots = (b1 if _f(mom) != 0.0 else None,)
+        if inplace and not differentiable:
+            for old, new in zip(state.slots, slots):
+                if old is not None and new is not None:
+                    old.copy_(new)
+        return out, OptState(t, slots, layout)
+
+
+def _any_requires_grad(grads, state):
+    ts = [grads] if isinstance(grads, torch.Tensor) else list(grads)
+    ts += [s for s in state.slots if s is not None]
+    return any(t.requires_grad for t in ts)
+
+
+def _check_unit(name, x):
+    v = _f(x)
+    if not (0.0 <= v < 1.0):
+        raise ValueError(f"{name} must be in [0, 1), got {v}")
+
+
+def _check_lr(lr):
+    if not _f(lr) > 0.0:
+        raise ValueError(f"lr must be > 0, got {_f(lr)}")
+
+
+def adam(lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, eps_root=0.0, compute=L.OPT_COMPUTE_DEFAULT,
+         state_dtype=L.OPT_F32):
+    """Adam (defaults; validation S:189)."""
+    _check_lr(lr)
+    _check_unit("b1", b1)
+    _check_unit("b2", b2)
+    if not _f(eps) > 0.0:
+        raise ValueError("eps must be > 0")
+    return GradientTransformation("adam", (lr, b1, b2, eps, eps_root), 2, compute, state_dtype)
+
+
+def rmsprop(lr=1e-2, alpha=0.99, eps=1e-8, compute=L.OPT_COMPUTE_DEFAULT, state_dtype=L.OPT_F32):
+    """RMSProp."""
+    _check_lr(lr)
+    _check_unit("alpha", alpha)
+    if not _f(eps) >= 0.0:
+        raise ValueError("eps must be >= 0")
+    return GradientTransformation("rmsprop", (lr, alpha, eps), 1, compute, state_dtype)
+
+
+def sgd(lr, momentum=0.0, nesterov=False, compute=L.OPT_COMPUTE_DEFAULT, state_dtype=L.OPT_F32):
+    """SGD with optional (Nesterov) momentum."""
+    _check_lr(lr)
+    _check_unit("momentum", momentum)
+    return GradientTransformation("sgd", (lr, momentum, nesterov), 1, compute, state_dtype)
+
+
+def apply_updates(params, updates):
+    """params + updates, leafwise or on flat buffers."""
+    if isinstance(params, torch.Tensor):
+        if params.shape != updates.shape:
+            raise ValueError("params and updates differ in shape")
+        return ApplyUpdates.apply(params, updates)
+    params = list(params)
+    if isinstance(updates, torch.Tensor):  # flat updates for a leaf tuple
+        layout = FlatTree.of(params)
+        return layout.views(ApplyUpdates.apply(layout.flatten(params), updates))
+    updates = list(updates)
+    if len(params) != len(updates):
+        raise ValueError("TreeDef mismatch between params and updates")
+    return [ApplyUpdates.apply(p, u) for p, u in zip(params, updates)]

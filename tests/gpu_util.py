@@ -1,0 +1,61 @@
+"""Helpers for the GPU parity tests: run one op through the C ABI on seeded
+inputs and compare with the oracle element by element."""
+import numpy as np
+import torch
+
+import synth
+
+DEV = "cuda:0"
+HP_NAMES = {"adam": 4, "rmsprop": 3, "sgd": 2}
+
+
+def dev_f32(x):
+    return None if x is None else torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(DEV)
+
+
+def dev_state(x, bf16):
+    if x is None:
+        return None
+    if bf16:
+        bits = synth.to_bf16_bits(x) if x.dtype != np.uint16 else x
+        return torch.from_numpy(bits.view(np.int16)).to(DEV).view(torch.bfloat16)
+    return dev_f32(x)
+
+
+def host(t):
+    if t is None:
+        return None
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.cpu().numpy()
+
+
+def state_host_bits(x, bf16):
+    """The state values the oracle must see (bf16 bit patterns when bf16)."""
+    if x is None:
+        return None
+    return synth.to_bf16_bits(x) if bf16 else x
+
+
+def tol_fail(x, ref, rtol=1e-5, atol=1e-6):
+    """Boolean mask of elements outside |x - ref| <= atol + rtol |ref|."""
+    x = np.asarray(x, np.float64)
+    ref = np.asarray(ref, np.float64)
+    return ~(np.abs(x - ref) <= atol + rtol * np.abs(ref))
+
+
+def assert_close(name, x, ref, rtol=1e-5, atol=1e-6):
+    bad = tol_fail(x, ref, rtol, atol)
+    if bad.any():
+        i = np.flatnonzero(bad)[:5]
+        raise AssertionError(f"{name}: {bad.sum()}/{bad.size} outside tol (rtol={rtol}, atol={atol});"
+                             f" idx {i.tolist()} got {np.asarray(x)[i].tolist()} "
+                             f"want {np.asarray(ref)[i].tolist()}")
+
+
+def assert_sum_close(name, x, ref, ref_abs, rtol=1e-5, atol=1e-6):
+    """Hyper-gradient sums: error scaled by Sigma |term| (reading Z10)."""
+    x, ref, ref_abs = (np.asarray(a, np.float64) for a in (x, ref, ref_abs))
+    ok = np.abs(x - ref) <= atol + rtol * ref_abs
+    if not ok.all():
+        raise AssertionError(f"{name}: got {x.tolist()} want {ref.tolist()} (Sigma|t| {ref_abs.tolist()})")

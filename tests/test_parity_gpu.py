@@ -1,0 +1,277 @@
+"""GPU parity: every CUDA op, called through the C ABI, against the oracle on
+the same seeded inputs (bar: |x - ref| <= 1e-6 + 1e-5 |ref| for fp32 outputs,
+1e-2 relative for bf16-stored state, hyper-gradient sums scaled by
+Sigma|term|)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import (DEV, assert_close, assert_sum_close, dev_f32, dev_state, host,
+                      state_host_bits)
+
+pytestmark = pytest.mark.gpu
+
+LEAVES_RAGGED = [5, 4096, 1, 300, 9000, 3, 1027, 64]   # 14,560 elements: tiles + ragged tails
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2211_06934_b200 import _lib
+
+    return _lib
+
+
+def _inputs(case):
+    if case == "c1":
+        x = synth.c1_inputs()
+        return x, None, 1
+    x = synth.state_tree(0xA1, LEAVES_RAGGED)
+    return x, synth.offsets_of(LEAVES_RAGGED), 10
+
+
+COMPUTES = [1, 2]  # OPT_COMPUTE_F32, OPT_COMPUTE_F64
+
+
+def _tols(ct):
+    return dict(rtol=1e-5, atol=1e-6)
+
+
+# ------------------------------------------------------------------ Adam
+@pytest.mark.parametrize("case", ["c1", "ragged"])
+@pytest.mark.parametrize("lr", [1e-3, 1.0])
+@pytest.mark.parametrize("bf16", [False, True])
+@pytest.mark.parametrize("ct", COMPUTES)
+def test_adam_fwd_bwd(L, case, lr, bf16, ct):
+    x, off, t = _inputs(case)
+    hp = (lr, 0.9, 0.999, 1e-8, 0.0)
+    n = x["g"].size
+    tree = L.Tree(offsets=off if off is not None else [0, n], device=DEV)
+    m_h, v_h = state_host_bits(x["m"], bf16), state_host_bits(x["v"], bf16)
+    g, m, v = dev_f32(x["g"]), dev_state(x["m"], bf16), dev_state(x["v"], bf16)
+    sd = 1 if bf16 else 0
+    u = torch.empty_like(g)
+    sdt = torch.bfloat16 if bf16 else torch.float32
+    m1, v1 = torch.empty(n, dtype=sdt, device=DEV), torch.empty(n, dtype=sdt, device=DEV)
+    L.opt_adam_fwd(tree, t, hp, sd, ct, g, m, v, u, m1, v1)
+    ru, rm1, rv1 = oracle.adam_fwd(x["g"], m_h, v_h, t, *hp, state_bf16=bf16, prec=1)
+    assert_close("u", host(u), ru, **_tols(ct))
+    if bf16:
+        assert_close("m1", oracle.bf16_to_f64(host(m1)), rm1, rtol=1e-2, atol=0)
+        assert_close("v1", oracle.bf16_to_f64(host(v1)), rv1, rtol=1e-2, atol=0)
+    else:
+        assert_close("m1", host(m1), rm1, **_tols(ct))
+        assert_close("v1", host(v1), rv1, **_tols(ct))
+    # backward with all cotangents + global and per-leaf hyper-gradients
+    du, dm1, dv1 = dev_f32(x["du"]), dev_f32(x["dm1"]), dev_f32(x["dv1"])
+    dg, dm, dv = torch.empty_like(g), torch.empty_like(g), torch.empty_like(g)
+    dhp = torch.empty(4, dtype=torch.float64, device=DEV)
+    dhl = torch.empty(tree.n_leaves * 4, dtype=torch.float64, device=DEV)
+    ws = tree.workspace(DEV, per_leaf=True)
+    L.opt_adam_bwd(tree, t, hp, sd, ct, g, m, v, du, dm1, dv1, dg, dm, dv, dhp, dhl, ws)
+    r = oracle.adam_vjp(x["g"], m_h, v_h, x["du"], x["dm1"], x["dv1"], t, *hp, state_bf16=bf16,
+                        prec=1, offsets=tree.h_offsets)
+    assert_close("dg", host(dg), r["dg"], **_tols(ct))
+    assert_close("dm", host(dm), r["dm"], **_tols(ct))
+    assert_close("dv", host(dv), r["dv"], **_tols(ct))
+    assert_sum_close("dhp", host(dhp), r["dhp"], r["dhp_abs"])
+    assert np.allclose(host(dhl).reshape(-1, 4).sum(0), host(dhp), rtol=1e-12,
+                       atol=1e-12 * r["dhp_abs"].max())
+    # global-only reduction path gives the same sums
+    dhp2 = torch.empty(4, dtype=torch.float64, device=DEV)
+    L.opt_adam_bwd(tree, t, hp, sd, ct, g, m, v, du, dm1, dv1, None, None, None, dhp2, None, ws)
+    assert_sum_close("dhp(uniform)", host(dhp2), r["dhp"], r["dhp_abs"])
+
+
+@pytest.mark.parametrize("bf16", [False, True])
+@pytest.mark.parametrize("ct", COMPUTES)
+def test_rmsprop_fwd_bwd(L, bf16, ct):
+    x, off, t = _inputs("ragged")
+    hp = (1e-2, 0.99, 1e-8)
+    n = x["g"].size
+    tree = L.Tree(offsets=off, device=DEV)
+    v_h = state_host_bits(x["v"], bf16)
+    g, v = dev_f32(x["g"]), dev_state(x["v"], bf16)
+    sd = 1 if bf16 else 0
+    u = torch.empty_like(g)
+    v1 = torch.empty(n, dtype=torch.bfloat16 if bf16 else torch.float32, device=DEV)
+    L.opt_rmsprop_fwd(tree, hp, sd, ct, g, v, u, v1)
+    ru, rv1 = oracle.rmsprop_fwd(x["g"], v_h, *hp, state_bf16=bf16, prec=1)
+    assert_close("u", host(u), ru)
+    if bf16:
+        assert_close("v1", oracle.bf16_to_f64(host(v1)), rv1, rtol=1e-2, atol=0)
+    else:
+        assert_close("v1", host(v1), rv1)
+    du, dv1 = dev_f32(x["du"]), dev_f32(x["dv1"])
+    dg, dv = torch.empty_like(g), torch.empty_like(g)
+    dhp = torch.empty(3, dtype=torch.float64, device=DEV)
+    dhl = torch.empty(tree.n_leaves * 3, dtype=torch.float64, device=DEV)
+    ws = tree.workspace(DEV, per_leaf=True)
+    L.opt_rmsprop_bwd(tree, hp, sd, ct, g, v, du, dv1, dg, dv, dhp, dhl, ws)
+    r = oracle.rmsprop_vjp(x["g"], v_h, x["du"], x["dv1"], *hp, state_bf16=bf16, prec=1,
+                           offsets=tree.h_offsets)
+    assert_close("dg", host(dg), r["dg"])
+    assert_close("dv", host(dv), r["dv"])
+    assert_sum_close("dhp", host(dhp), r["dhp"], r["dhp_abs"])
+    np.testing.assert_allclose(host(dhl).reshape(-1, 3), r["dhp_leaf"], rtol=1e-5,
+                               atol=1e-6 + 1e-5 * r["dhp_abs"].max())
+
+
+@pytest.mark.parametrize("nesterov", [False, True])
+@pytest.mark.parametrize("bf16", [False, True])
+@pytest.mark.parametrize("ct", COMPUTES)
+def test_sgd_fwd_bwd(L, nesterov, bf16, ct):
+    x, off, t = _inputs("ragged")
+    hp = (0.1, 0.9, nesterov)
+    n = x["g"].size
+    tree = L.Tree(offsets=off, device=DEV)
+    b_h = state_host_bits(x["m"], bf16)
+    g, b = dev_f32(x["g"]), dev_state(x["m"], bf16)
+    sd = 1 if bf16 else 0
+    u = torch.empty_like(g)
+    b1 = torch.empty(n, dtype=torch.bfloat16 if bf16 else torch.float32, device=DEV)
+    L.opt_sgd_fwd(tree, hp, sd, ct, g, b, u, b1)
+    ru, rb1 = oracle.sgd_fwd(x["g"], b_h, *hp, state_bf16=bf16, prec=1)
+    assert_close("u", host(u), ru)
+    if bf16:
+        assert_close("b1", oracle.bf16_to_f64(host(b1)), rb1, rtol=1e-2, atol=0)
+    else:
+        assert_close("b1", host(b1), rb1)
+    du, db1 = dev_f32(x["du"]), dev_f32(x["dm1"])
+    dg, db = torch.empty_like(g), torch.empty_like(g)
+    dhp = torch.empty(2, dtype=torch.float64, device=DEV)
+    ws = tree.workspace(DEV)
+    L.opt_sgd_bwd(tree, hp, sd, ct, g, b, du, db1, dg, db, dhp, None, ws)
+    r = oracle.sgd_vjp(x["g"], b_h, x["du"], x["dm1"], *hp, state_bf16=bf16, prec=1)
+    assert_close("dg", host(dg), r["dg"])
+    assert_close("db", host(db), r["db"])
+    assert_sum_close("dhp", host(dhp), r["dhp"], r["dhp_abs"])
+
+
+# --------------------------------------------------- ABI conventions
+def test_null_cotangent_is_zero_bitwise(L):
+    x, off, t = _inputs("ragged")
+    hp = (1e-3, 0.9, 0.999, 1e-8, 0.0)
+    tree = L.Tree(offsets=off, device=DEV)
+    g, m, v, du = dev_f32(x["g"]), dev_f32(x["m"]), dev_f32(x["v"]), dev_f32(x["du"])
+    z = torch.zeros_like(g)
+    outs = []
+    for dm1, dv1 in ((None, None), (z, z)):
+        dg, dm, dv = torch.empty_like(g), torch.empty_like(g), torch.empty_like(g)
+        dhp = torch.empty(4, dtype=torch.float64, device=DEV)
+        L.opt_adam_bwd(tree, t, hp, 0, 0, g, m, v, du, dm1, dv1, dg, dm, dv, dhp, None,
+                       tree.workspace(DEV))
+        outs.append([host(a) for a in (dg, dm, dv, dhp)])
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_inplace_aliasing_matches_out_of_place(L):
+    x, off, t = _inputs("ragged")
+    hp = (1e-3, 0.9, 0.999, 1e-8, 0.0)
+    tree = L.Tree(offsets=off, device=DEV)
+    g, m, v = dev_f32(x["g"]), dev_f32(x["m"]), dev_f32(x["v"])
+    u, m1, v1 = torch.empty_like(g), torch.empty_like(g), torch.empty_like(g)
+    L.opt_adam_fwd(tree, t, hp, 0, 0, g, m, v, u, m1, v1)
+    g2, m2, v2 = g.clone(), m.clone(), v.clone()
+    L.opt_adam_fwd(tree, t, hp, 0, 0, g2, m2, v2, g2, m2, v2)  # updates == g, mu_out == mu ...
+    for a, b in ((u, g2), (m1, m2), (v1, v2)):
+        assert torch.equal(a, b)
+
+
+def test_fused_apply_equals_params_plus_update(L):
+    x, off, t = _inputs("ragged")
+    hp = (1e-2, 0.9, 0.999, 1e-8, 0.0)
+    tree = L.Tree(offsets=off, device=DEV)
+    g, m, v = dev_f32(x["g"]), dev_f32(x["m"]), dev_f32(x["v"])
+    p = dev_f32(x["du"])
+    u, m1, v1 = torch.empty_like(g), torch.empty_like(g), torch.empty_like(g)
+    p_out = torch.empty_like(g)
+    L.opt_adam_fwd(tree, t, hp, 0, 2, g, m, v, u, m1, v1, p, p_out)
+    ru, _, _ = oracle.adam_fwd(x["g"], x["m"], x["v"], t, *hp, prec=1)
+    assert_close("params_out", host(p_out), x["du"].astype(np.float64) + ru)
+    out2 = torch.empty_like(g)
+    L.opt_apply_updates(g.numel(), p, u, out2)
+    np.testing.assert_allclose(host(out2), x["du"].astype(np.float64) + host(u).astype(np.float64),
+                               rtol=1e-7, atol=1e-7)
+
+
+def test_hyper_gradients_deterministic(L):
+    x = synth.state_tree(0xD, [1 << 20, 3333])
+    tree = L.Tree(offsets=synth.offsets_of([1 << 20, 3333]), device=DEV)
+    hp = (1e-3, 0.9, 0.999, 1e-8, 0.0)
+    args = [dev_f32(x[k]) for k in ("g", "m", "v", "du", "dm1", "dv1")]
+    ws = tree.workspace(DEV, per_leaf=True)
+    res = []
+    for _ in range(3):
+        dhp = torch.empty(4, dtype=torch.float64, device=DEV)
+        dhl = torch.empty(8, dtype=torch.float64, device=DEV)
+        L.opt_adam_bwd(tree, 7, hp, 0, 0, *args, None, None, None, dhp, dhl, ws)
+        res.append((host(dhp), host(dhl)))
+    for a, b in res[1:]:
+        np.testing.assert_array_equal(a, res[0][0])
+        np.testing.assert_array_equal(b, res[0][1])
+
+
+def test_empty_tree_zeroes_hyper_gradients(L):
+    tree = L.Tree(offsets=[0, 0, 0], device=DEV)
+    dhp = torch.full((4,), 7.0, dtype=torch.float64, device=DEV)
+    dhl = torch.full((8,), 7.0, dtype=torch.float64, device=DEV)
+    L.opt_adam_bwd(tree, 1, (1e-3, 0.9, 0.999, 1e-8, 0.0), 0, 0, None, None, None, None, None,
+                   None, None, None, None, dhp, dhl, None)
+    assert torch.all(dhp == 0) and torch.all(dhl == 0)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 255, 1023, 4097])
+def test_tiny_and_ragged_sizes(L, n):
+    x = synth.state_tree(n, None, n=n)
+    tree = L.Tree(numel=n, device=DEV)
+    hp = (1e-2, 0.9, 0.999, 1e-8, 0.0)
+    g, m, v = dev_f32(x["g"]), dev_f32(x["m"]), dev_f32(x["v"])
+    u, m1, v1 = torch.empty_like(g), torch.empty_like(g), torch.empty_like(g)
+    L.opt_adam_fwd(tree, 3, hp, 0, 0, g, m, v, u, m1, v1)
+    ru, rm1, rv1 = oracle.adam_fwd(x["g"], x["m"], x["v"], 3, *hp, prec=1)
+    assert_close("u", host(u), ru)
+    dg = torch.empty_like(g)
+    dhp = torch.empty(4, dtype=torch.float64, device=DEV)
+    L.opt_adam_bwd(tree, 3, hp, 0, 0, g, m, v, dev_f32(x["du"]), None, None, dg, None, None, dhp,
+                   None, tree.workspace(DEV))
+    r = oracle.adam_vjp(x["g"], x["m"], x["v"], x["du"], None, None, 3, *hp, prec=1)
+    assert_close("dg", host(dg), r["dg"])
+    assert_sum_close("dhp", host(dhp), r["dhp"], r["dhp_abs"])
+
+
+# ------------------------------------------ full-size C2, sampled check
+@pytest.mark.slow
+@pytest.mark.parametrize("ct", COMPUTES)
+def test_c2_resnet18_full_size_sampled(L, ct):
+    """Config C2 at full size (11,689,512 elements, 62 leaves) in the launch
+    configuration bench.py times; 2^16 sampled elements against the oracle
+    (elementwise independence makes the sample exact) and the hyper-gradient
+    sums against the full oracle sum."""
+    leaves = synth.RESNET18_LEAVES
+    x = synth.state_tree(0xC2, leaves)
+    tree = L.Tree(offsets=synth.offsets_of(leaves), device=DEV)
+    hp = (1e-3, 0.9, 0.999, 1e-8, 0.0)
+    t = 10
+    g, m, v, du, dm1, dv1 = (dev_f32(x[k]) for k in ("g", "m", "v", "du", "dm1", "dv1"))
+    u, m1, v1 = torch.empty_like(g), torch.empty_like(g), torch.empty_like(g)
+    L.opt_adam_fwd(tree, t, hp, 0, ct, g, m, v, u, m1, v1)
+    dg, dm, dv = torch.empty_like(g), torch.empty_like(g), torch.empty_like(g)
+    dhp = torch.empty(4, dtype=torch.float64, device=DEV)
+    L.opt_adam_bwd(tree, t, hp, 0, ct, g, m, v, du, dm1, dv1, dg, dm, dv, dhp, None,
+                   tree.workspace(DEV))
+    idx = np.sort(np.random.default_rng(0).choice(tree.numel, 1 << 16, replace=False))
+    xs = {k: x[k][idx] for k in x}
+    ru, rm1, rv1 = oracle.adam_fwd(xs["g"], xs["m"], xs["v"], t, *hp, prec=1)
+    r = oracle.adam_vjp(xs["g"], xs["m"], xs["v"], xs["du"], xs["dm1"], xs["dv1"], t, *hp, prec=1)
+    for name, got, ref in (("u", u, ru), ("m1", m1, rm1), ("v1", v1, rv1), ("dg", dg, r["dg"]),
+                           ("dm", dm, r["dm"]), ("dv", dv, r["dv"])):
+        assert_close(name, host(got)[idx], ref)
+    oracle.set_num_threads(0)
+    full = oracle.adam_vjp(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], t, *hp)
+    oracle.set_num_threads(1)
+    assert_sum_close("dhp", host(dhp), full["dhp"], full["dhp_abs"])
