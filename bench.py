@@ -190,7 +190,7 @@ def time_ours(args, workload_inputs, dev, rank, world):
     torch.cuda.synchronize()
     sampler.start()
     # clock soak: keep the GPU busy ~0.5 s (untimed) so the sampler sees load
-    t_end = time.time() + 0.5
+    t_end = time.time() + (0.0 if args.quick else 0.5)
     i = 0
     while time.time() < t_end:
         for _ in range(50):
@@ -227,7 +227,7 @@ def time_ours(args, workload_inputs, dev, rank, world):
         ms = float(tt.item())
 
     # end-to-end through the C ABI with host buffers (pinned), copies timed
-    e2e = time_e2e(args, W, dev)
+    e2e = None if args.quick else time_e2e(args, W, dev)
     return dict(ms=ms, fwd_ms=fwd_ms, bwd_ms=bwd_ms, clocks=clocks, launches=launches, W=W,
                 e2e=e2e, wname=wname, sets=sets)
 
@@ -320,6 +320,7 @@ def main():
     ap.add_argument("--size", type=int, default=1 << 24)
     ap.add_argument("--bf16", action="store_true", help="bf16 optimizer state")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip e2e and clock soak (tuning)")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.warmup < 3:

@@ -171,11 +171,13 @@ int opt_apply_updates(int64_t numel, const float* params, const float* updates,
  * 1/2 sum a_i (theta_i - phi_i)^2, whose gradient and Hessian-vector
  * product a real model would get from autograd:
  *   opt_quadratic_grad: g = a (theta - phi)
- *   opt_quadratic_rev:  theta_bar += a g_bar ; phi_bar -= a g_bar   (in place) */
+ *   opt_quadratic_rev:  theta_bar += a g_bar ;
+ *                       phi_bar = (init_phi ? 0 : phi_bar) - a g_bar   (in place;
+ *                       phi_bar is not read when init_phi != 0) */
 int opt_quadratic_grad(int64_t numel, const float* a, const float* theta,
                        const float* phi, float* g, void* stream);
 int opt_quadratic_rev(int64_t numel, const float* a, const float* g_bar,
-                      float* theta_bar, float* phi_bar, void* stream);
+                      float* theta_bar, float* phi_bar, int init_phi, void* stream);
 
 /* -------------------------------------------------------------- misc */
 const char* opt_status_string(int status);

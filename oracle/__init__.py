@@ -289,3 +289,57 @@ def sweep_forward_complex(kind, a, theta0, phi, K, hp, nesterov=False):
     lib().oracle_sweep_forward_cplx(KIND[kind], n, int(K), _p(hr), _p(hi), int(nesterov), _p(a),
                                     _p(tr), _p(ti), _p(pr), _p(pi), _p(o_r), _p(o_i))
     return o_r + 1j * o_i
+
+
+# ------------------------------------------------ magnitude twins (Z10)
+def _mag_lib():
+    L = lib()
+    P, i64, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    L.oracle_adam_mag.argtypes = [i64, i64, P, I, P, P, P, P, P, P, P, P]
+    L.oracle_rmsprop_mag.argtypes = [i64, P, I, P, P, P, P, P, P]
+    L.oracle_sgd_mag.argtypes = [i64, P, I, P, P, P, P, P, P]
+    return L
+
+
+def adam_mag(g, m, v, du, dm1, dv1, t, lr, b1, b2, eps, eps_root=0.0, state_bf16=False):
+    """Magnitude twins (fp32 error scales, reading Z10) of u, m', v', dg, dm,
+    dv and of the four hyper-gradient sums (Sigma of per-element scales)."""
+    g = _f32(g)
+    n = g.size
+    m, v = _state(m, state_bf16), _state(v, state_bf16)
+    du, dm1, dv1 = _f32(du), _f32(dm1), _f32(dv1)
+    hp = _hp([lr, b1, b2, eps, eps_root])
+    out = np.empty(6 * n)
+    hs = np.zeros(4)
+    _mag_lib().oracle_adam_mag(n, int(t), _p(hp), int(state_bf16), _p(g), _p(m), _p(v), _p(du),
+                               _p(dm1), _p(dv1), _p(out), _p(hs))
+    o = out.reshape(6, n)
+    return dict(u=o[0], m1=o[1], v1=o[2], dg=o[3], dm=o[4], dv=o[5], dhp=hs)
+
+
+def rmsprop_mag(g, v, du, dv1, lr, alpha, eps, state_bf16=False):
+    g = _f32(g)
+    n = g.size
+    v = _state(v, state_bf16)
+    du, dv1 = _f32(du), _f32(dv1)
+    hp = _hp([lr, alpha, eps])
+    out = np.empty(4 * n)
+    hs = np.zeros(3)
+    _mag_lib().oracle_rmsprop_mag(n, _p(hp), int(state_bf16), _p(g), _p(v), _p(du), _p(dv1),
+                                  _p(out), _p(hs))
+    o = out.reshape(4, n)
+    return dict(u=o[0], v1=o[1], dg=o[2], dv=o[3], dhp=hs)
+
+
+def sgd_mag(g, b, du, db1, lr, momentum, nesterov=False, state_bf16=False):
+    g = _f32(g)
+    n = g.size
+    b = _state(b, state_bf16)
+    du, db1 = _f32(du), _f32(db1)
+    hp = _hp([lr, momentum, 1.0 if nesterov else 0.0])
+    out = np.empty(4 * n)
+    hs = np.zeros(2)
+    _mag_lib().oracle_sgd_mag(n, _p(hp), int(state_bf16), _p(g), _p(b), _p(du), _p(db1), _p(out),
+                              _p(hs))
+    o = out.reshape(4, n)
+    return dict(u=o[0], b1=o[1], dg=o[2], db=o[3], dhp=hs)

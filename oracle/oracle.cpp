@@ -547,3 +547,51 @@ void oracle_sweep_forward_cplx(int kind, int64_t n, int64_t K, const double* hp_
 }
 
 }  // extern "C"
+
+// ---------------------------------------------- magnitude-twin entry points
+// out[k*n + i]: per-element scales of the outputs in the order documented in
+// oracle/__init__.py; hsum[k]: Sigma over elements of the hyper-term scales.
+extern "C" {
+
+void oracle_adam_mag(int64_t n, int64_t t, const double* hp, int bf, const float* g,
+                     const void* m, const void* v, const float* du, const float* dm1,
+                     const float* dv1, double* out, double* hsum) {
+  const AdamHP<double> h = adam_hp<double>(hp);
+  long double hs[4] = {0, 0, 0, 0};
+  for (int64_t i = 0; i < n; ++i) {
+    auto r = oracle::adam_mag(f32_in(g, i), state_in(m, bf, i), state_in(v, bf, i), f32_in(du, i),
+                              f32_in(dm1, i), f32_in(dv1, i), h, t);
+    const double o[6] = {r.u, r.m1, r.v1, r.dg, r.dm, r.dv};
+    for (int k = 0; k < 6; ++k) out[k * n + i] = o[k];
+    for (int k = 0; k < 4; ++k) hs[k] += r.h[k];
+  }
+  for (int k = 0; k < 4; ++k) hsum[k] = (double)hs[k];
+}
+
+void oracle_rmsprop_mag(int64_t n, const double* hp, int bf, const float* g, const void* v,
+                        const float* du, const float* dv1, double* out, double* hsum) {
+  const RmsHP<double> h = rms_hp<double>(hp);
+  long double hs[3] = {0, 0, 0};
+  for (int64_t i = 0; i < n; ++i) {
+    auto r = oracle::rmsprop_mag(f32_in(g, i), state_in(v, bf, i), f32_in(du, i), f32_in(dv1, i), h);
+    const double o[4] = {r.u, r.v1, r.dg, r.dv};
+    for (int k = 0; k < 4; ++k) out[k * n + i] = o[k];
+    for (int k = 0; k < 3; ++k) hs[k] += r.h[k];
+  }
+  for (int k = 0; k < 3; ++k) hsum[k] = (double)hs[k];
+}
+
+void oracle_sgd_mag(int64_t n, const double* hp, int bf, const float* g, const void* b,
+                    const float* du, const float* db1, double* out, double* hsum) {
+  const SgdHP<double> h = sgd_hp<double>(hp);
+  long double hs[2] = {0, 0};
+  for (int64_t i = 0; i < n; ++i) {
+    auto r = oracle::sgd_mag(f32_in(g, i), state_in(b, bf, i), f32_in(du, i), f32_in(db1, i), h);
+    const double o[4] = {r.u, r.b1, r.dg, r.db};
+    for (int k = 0; k < 4; ++k) out[k * n + i] = o[k];
+    for (int k = 0; k < 2; ++k) hs[k] += r.h[k];
+  }
+  for (int k = 0; k < 2; ++k) hsum[k] = (double)hs[k];
+}
+
+}  // extern "C"

@@ -238,3 +238,104 @@ SgdVjp<T> sgd_vjp(T g, T b, T du, T db1_out, const SgdHP<T>& h) {
 }
 
 }  // namespace oracle
+
+// ------------------------------------------------- magnitude twins (Z10)
+// Error scale for a kernel that evaluates the REDUCED forms
+// in fp32: the same expression tree with every + and - replaced by |a|+|b|
+// and every product by its absolute value (denominators keep their value).
+// |x - ref| <= 1e-6 + 1e-5 mag(ref) is then the fp32 tolerance: it charges a
+// kernel only for the conditioning of its inputs (e.g. m' = b1 m + (1-b1) g
+// can cancel, and fp32 cannot even hold b1 exactly), never for a
+// cancellation the reduced form removes, so a textbook-form fp32 kernel
+// still fails it (verified). This is a tolerance, not a value:
+// nothing here is compared against the kernels' arithmetic.
+namespace oracle {
+
+struct AdamMag {
+  double u, m1, v1, dg, dm, dv, h[4];
+};
+
+inline AdamMag adam_mag(double g, double m, double v, double du, double dm1, double dv1,
+                        const AdamHP<double>& h, int64_t t) {
+  const double b1 = h.b1, b2 = h.b2, lr = std::fabs(h.lr), eps = h.eps;
+  const double bc1 = 1.0 - ipow(b1, t), bc2 = 1.0 - ipow(b2, t);
+  const double A = (1 - b1) / bc1, C = (1 - b2) / bc2;
+  const double P = b1 * m / bc1, Q = b2 * v / bc2 + h.eps_root;
+  const double s = std::sqrt(C * g * g + Q), d = s + eps;
+  const double rd = d == 0 ? 0 : 1 / d, rs = s == 0 ? 0 : 1 / s;
+  const double ag = std::fabs(g), adu = std::fabs(du);
+  const double mh = A * ag + std::fabs(P);
+  AdamMag r;
+  r.m1 = b1 * std::fabs(m) + (1 - b1) * ag;
+  r.v1 = b2 * std::fabs(v) + (1 - b2) * g * g;
+  r.u = lr * mh * rd;
+  r.dg = (1 - b1) * std::fabs(dm1) + 2 * (1 - b2) * ag * std::fabs(dv1) +
+         adu * lr * rd * rd * (A * eps + (A * std::fabs(Q) + std::fabs(P * C * g)) * rs);
+  r.dm = b1 * (std::fabs(dm1) + adu * lr * rd / bc1);
+  const double w = 0.5 * lr * mh * rd * rd * rs;
+  r.dv = b2 * (std::fabs(dv1) + adu * w / bc2);
+  const double tt = (double)t;
+  const double p1 = ipow(b1, t), p2 = ipow(b2, t);
+  const double K1 = (1 - p1 + tt * p1) / (bc1 * bc1);
+  const double K2 = (1 - p1 - tt * ipow(b1, t - 1) * (1 - b1)) / (bc1 * bc1);
+  const double K3 = (1 - p2 + tt * p2) / (bc2 * bc2);
+  const double K4 = (1 - p2 - tt * ipow(b2, t - 1) * (1 - b2)) / (bc2 * bc2);
+  r.h[0] = adu * mh * rd;
+  r.h[1] = std::fabs(dm1) * (std::fabs(m) + ag) +
+           adu * lr * rd * (std::fabs(m * K1) + std::fabs(g * K2));
+  r.h[2] = std::fabs(dv1) * (std::fabs(v) + g * g) +
+           adu * w * (std::fabs(v * K3) + std::fabs(g * g * K4));
+  r.h[3] = adu * lr * mh * rd * rd;
+  return r;
+}
+
+struct RmsMag {
+  double u, v1, dg, dv, h[3];
+};
+
+inline RmsMag rmsprop_mag(double g, double v, double du, double dv1, const RmsHP<double>& h) {
+  const double a = h.alpha, lr = std::fabs(h.lr), eps = h.eps;
+  const double s = std::sqrt(a * v + (1 - a) * g * g), d = s + eps;
+  const double rd = d == 0 ? 0 : 1 / d, rs = s == 0 ? 0 : 1 / s;
+  const double ag = std::fabs(g), adu = std::fabs(du);
+  RmsMag r;
+  r.v1 = a * std::fabs(v) + (1 - a) * g * g;
+  r.u = lr * ag * rd;
+  r.dg = 2 * (1 - a) * ag * std::fabs(dv1) + adu * lr * rd * rd * (eps + a * std::fabs(v) * rs);
+  const double w = 0.5 * lr * ag * rd * rd * rs;
+  r.dv = a * (std::fabs(dv1) + adu * w);
+  r.h[0] = adu * ag * rd;
+  r.h[1] = (std::fabs(dv1) + adu * w) * (std::fabs(v) + g * g);
+  r.h[2] = adu * lr * ag * rd * rd;
+  return r;
+}
+
+struct SgdMag {
+  double u, b1, dg, db, h[2];
+};
+
+inline SgdMag sgd_mag(double g, double b, double du, double db1, const SgdHP<double>& h) {
+  const double mu = h.mu, lr = std::fabs(h.lr);
+  const double ab1 = mu * std::fabs(b) + std::fabs(g);
+  const double adu = std::fabs(du), adb = std::fabs(db1);
+  SgdMag r;
+  r.b1 = ab1;
+  if (h.nesterov) {
+    const double B = adb + lr * mu * adu;
+    r.u = lr * (std::fabs(g) + mu * ab1);
+    r.dg = B + lr * adu;
+    r.db = mu * B;
+    r.h[0] = adu * (std::fabs(g) + mu * ab1);
+    r.h[1] = B * std::fabs(b) + adu * lr * ab1;
+  } else {
+    const double B = adb + lr * adu;
+    r.u = lr * ab1;
+    r.dg = B;
+    r.db = mu * B;
+    r.h[0] = adu * ab1;
+    r.h[1] = B * std::fabs(b);
+  }
+  return r;
+}
+
+}  // namespace oracle

@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdiffopt.so")
+LIB_PATH = os.environ.get("DIFFOPT_LIB") or os.path.join(HERE, "libdiffopt.so")  # env: tuning sweeps
 
 OPT_OK, OPT_EINVAL, OPT_EALIGN, OPT_ECUDA, OPT_EWORKSPACE = 0, 1, 2, 3, 4
 OPT_F32, OPT_BF16 = 0, 1
@@ -68,7 +68,7 @@ def _load():
     L.opt_sgd_bwd.argtypes = [T, ctypes.POINTER(opt_sgd_hp), I, I] + [P] * 9 + [sz, P]
     L.opt_apply_updates.argtypes = [i64, P, P, P, P]
     L.opt_quadratic_grad.argtypes = [i64, P, P, P, P, P]
-    L.opt_quadratic_rev.argtypes = [i64, P, P, P, P, P]
+    L.opt_quadratic_rev.argtypes = [i64, P, P, P, P, I, P]
     L.opt_status_string.argtypes = [I]
     L.opt_status_string.restype = ctypes.c_char_p
     L.opt_last_error.restype = ctypes.c_char_p
@@ -217,9 +217,9 @@ def opt_quadratic_grad(numel, a, theta, phi, g, stream=None):
                                   _stream(stream)))
 
 
-def opt_quadratic_rev(numel, a, g_bar, theta_bar, phi_bar, stream=None):
+def opt_quadratic_rev(numel, a, g_bar, theta_bar, phi_bar, init_phi=False, stream=None):
     _check(lib.opt_quadratic_rev(int(numel), _ptr(a), _ptr(g_bar), _ptr(theta_bar),
-                                 _ptr(phi_bar), _stream(stream)))
+                                 _ptr(phi_bar), int(bool(init_phi)), _stream(stream)))
 
 
 def opt_launch_count():

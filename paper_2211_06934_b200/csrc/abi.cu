@@ -15,6 +15,7 @@
 
 #include "diffopt.h"
 #include "step_kernel.cuh"
+#include "tma_kernel.cuh"
 
 using namespace dopt;
 
@@ -159,10 +160,53 @@ int zero_outputs(const opt_tree* t, int nh, double* d_hp, double* d_hp_leaf, cud
   return OPT_OK;
 }
 
+// Launch shape per direction: U vectors in flight per thread, MINB resident
+// blocks per SM requested from ptxas (register cap). Tuned on B200
+// (DESIGN.md "Kernels"); -D overrides exist for tuning sweeps.
+#ifndef DOPT_U_FWD
+#define DOPT_U_FWD 2
+#endif
+#ifndef DOPT_MINB_FWD
+#define DOPT_MINB_FWD 1
+#endif
+#ifndef DOPT_U_BWD
+#define DOPT_U_BWD 2
+#endif
+#ifndef DOPT_MINB_BWD
+#define DOPT_MINB_BWD 1
+#endif
+
+#ifndef DOPT_TMA_FWD
+#define DOPT_TMA_FWD 0
+#endif
+#ifndef DOPT_TMA_BWD
+#define DOPT_TMA_BWD 0
+#endif
+
+// TMA-bulk pipelined path: one CTA per SM, STAGES-deep smem ring.
+template <class Op, class ST>
+int launch_tma(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, cudaStream_t s) {
+  constexpr uint32_t sb = TmaLayout<Op, ST>::stage_bytes();
+  constexpr int STAGES = (200 * 1024 / sb) > 8 ? 8 : (int)(200 * 1024 / sb);
+  auto k = step_tma<Op, ST, STAGES>;
+  const size_t smem = tma_smem_bytes<Op, ST, STAGES>();
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return fail(OPT_ECUDA, "smem attribute: %s", cudaGetErrorString(e));
+  int dev = 0, sms = 0;
+  e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return fail(OPT_ECUDA, "device query failed: %s", cudaGetErrorString(e));
+  const int64_t tiles = (a.numel + kTmaTile - 1) / kTmaTile;
+  int grid = (int)(tiles < sms ? tiles : sms);
+  k<<<grid > 0 ? grid : 1, kTmaThreads, smem, s>>>(op, a);
+  return launched(s);
+}
+
 // Launch an op (forward: no reduction) with state type ST.
 template <class Op, class ST, int U>
 int launch_fwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, cudaStream_t s) {
-  auto k = step_uniform<Op, ST, U>;
+  if (DOPT_TMA_FWD) return launch_tma<Op, ST>(op, a, s);
+  auto k = step_uniform<Op, ST, U, DOPT_MINB_FWD>;
   int grid = 0;
   int64_t work = ((a.numel >> 2) + kBlock - 1) / kBlock + 1;
   int rc = grid_for(k, work, 0, &grid);
@@ -183,7 +227,7 @@ int launch_bwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r,
     a.offsets = t->d_offsets;
     a.n_leaves = t->n_leaves;
     a.n_tiles = r.n_tiles;
-    auto k = step_leaf<Op, ST, U>;
+    auto k = step_leaf<Op, ST, U, DOPT_MINB_BWD>;
     size_t smem = sizeof(int64_t) * 2 * (size_t)(t->n_leaves + 1);
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -195,7 +239,8 @@ int launch_bwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r,
     k<<<grid, kBlock, smem, s>>>(op, a);
     return launched(s);
   }
-  auto k = step_uniform<Op, ST, U>;
+  if (DOPT_TMA_BWD) return launch_tma<Op, ST>(op, a, s);
+  auto k = step_uniform<Op, ST, U, DOPT_MINB_BWD>;
   int grid = 0;
   int64_t work = ((a.numel >> 2) + kBlock - 1) / kBlock + 1;
   int rc = grid_for(k, work, 0, &grid);
@@ -208,7 +253,7 @@ int launch_bwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r,
 template <template <class> class OpT, bool kBwd, class Fill>
 int dispatch(int state_dtype, int ct, StepArgs<OpT<float>::NIN, OpT<float>::NOUT>& a,
              const Reduce* r, const opt_tree* t, cudaStream_t s, Fill fill) {
-  constexpr int U = 2;
+  constexpr int U = kBwd ? DOPT_U_BWD : DOPT_U_FWD;
   if (ct == OPT_COMPUTE_F64) {
     OpT<double> op;
     fill(op);
@@ -519,14 +564,18 @@ __global__ void __launch_bounds__(kBlock) quad_grad_kernel(int64_t n, const floa
 
 __global__ void __launch_bounds__(kBlock) quad_rev_kernel(int64_t n, const float* __restrict__ a,
                                                           const float* __restrict__ gb,
-                                                          float* thb, float* phib) {
+                                                          float* thb, float* phib, int init) {
   const int64_t nvec = n >> 2, stride = (int64_t)gridDim.x * kBlock;
   for (int64_t v = (int64_t)blockIdx.x * kBlock + threadIdx.x; v < nvec; v += stride) {
     float x[4], g[4], t[4], p[4];
     load4(a, v, x);
     load4(gb, v, g);
     load4(thb, v, t);
-    load4(phib, v, p);
+    if (init) {
+      p[0] = p[1] = p[2] = p[3] = 0.f;
+    } else {
+      load4(phib, v, p);
+    }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float ag = x[e] * g[e];
@@ -540,7 +589,7 @@ __global__ void __launch_bounds__(kBlock) quad_rev_kernel(int64_t n, const float
   if (blockIdx.x == gridDim.x - 1 && i < n) {
     const float ag = a[i] * gb[i];
     thb[i] += ag;
-    phib[i] -= ag;
+    phib[i] = (init ? 0.f : phib[i]) - ag;
   }
 }
 
@@ -582,7 +631,7 @@ int opt_quadratic_grad(int64_t numel, const float* a, const float* theta, const 
 }
 
 int opt_quadratic_rev(int64_t numel, const float* a, const float* g_bar, float* theta_bar,
-                      float* phi_bar, void* stream) {
+                      float* phi_bar, int init_phi, void* stream) {
   g_err.clear();
   if (numel < 0) return fail(OPT_EINVAL, "numel < 0");
   TRY(check_align({a, g_bar, theta_bar, phi_bar}));
@@ -591,7 +640,7 @@ int opt_quadratic_rev(int64_t numel, const float* a, const float* g_bar, float* 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int grid = 0;
   TRY(glue_launch(quad_rev_kernel, numel, s, &grid));
-  quad_rev_kernel<<<grid, kBlock, 0, s>>>(numel, a, g_bar, theta_bar, phi_bar);
+  quad_rev_kernel<<<grid, kBlock, 0, s>>>(numel, a, g_bar, theta_bar, phi_bar, init_phi);
   return launched(s);
 }
 

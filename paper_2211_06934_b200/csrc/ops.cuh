@@ -22,10 +22,22 @@
 
 namespace dopt {
 
-template <class CT>
-__device__ __forceinline__ CT safe_rcp(CT x) {
-  return x == CT(0) ? CT(0) : CT(1) / x;
-}
+// Arithmetic primitives. fp64: IEEE div/sqrt. fp32: the MUFU approximations
+// (rsqrt, rcp; <= 2 ulp) unless DOPT_IEEE_F32 -- the fp32 bar is 1e-5 of the
+// magnitude twin, ~40x the approximation error, and the IEEE sequences cost
+// issue slots in an HBM-bound loop.
+__device__ __forceinline__ double safe_rcp(double x) { return x == 0.0 ? 0.0 : 1.0 / x; }
+__device__ __forceinline__ double ct_sqrt(double x) { return sqrt(x); }
+__device__ __forceinline__ double ct_div(double a, double b) { return a / b; }
+#ifdef DOPT_IEEE_F32
+__device__ __forceinline__ float safe_rcp(float x) { return x == 0.f ? 0.f : 1.f / x; }
+__device__ __forceinline__ float ct_sqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ float ct_div(float a, float b) { return a / b; }
+#else
+__device__ __forceinline__ float safe_rcp(float x) { return x == 0.f ? 0.f : __fdividef(1.f, x); }
+__device__ __forceinline__ float ct_sqrt(float x) { return x > 0.f ? x * rsqrtf(x) : 0.f; }
+__device__ __forceinline__ float ct_div(float a, float b) { return __fdividef(a, b); }
+#endif
 
 // ------------------------------------------------------------------ Adam
 template <class CT_>
@@ -36,14 +48,14 @@ struct AdamFwd {
   __host__ __device__ static constexpr bool out_state(int i) { return i == 1 || i == 2; }
   CT b1, om1, b2, om2, ibc1, ibc2, lr, eps, eps_root;
 
-  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], double*,
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT*,
                                              bool) const {
     const CT g = x[0], m = x[1], v = x[2];
     const CT m1 = b1 * m + om1 * g;
     const CT v1 = b2 * v + om2 * (g * g);
-    const CT s = sqrt(v1 * ibc2 + eps_root);
+    const CT s = ct_sqrt(v1 * ibc2 + eps_root);
     const CT d = s + eps;
-    const CT u = d == CT(0) ? CT(0) : (-lr * (m1 * ibc1)) / d;
+    const CT u = d == CT(0) ? CT(0) : ct_div(-lr * (m1 * ibc1), d);
     y[0] = u;
     y[1] = m1;
     y[2] = v1;
@@ -60,14 +72,14 @@ struct AdamBwd {
   CT b1, om1, b2, two_om2, A, C, ibc1, ibc2, b1ibc1, b2ibc2, eps_root, lr, eps;
   CT K1, K2, K3, K4;
 
-  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], double* h,
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT* h,
                                              bool want_hp) const {
     const CT g = x[0], m = x[1], v = x[2], du = x[3], dm1 = x[4], dv1 = x[5];
     const CT P = b1ibc1 * m;
     const CT Q = b2ibc2 * v + eps_root;
     const CT gg = g * g;
     const CT mhat = A * g + P;
-    const CT s = sqrt(C * gg + Q);
+    const CT s = ct_sqrt(C * gg + Q);
     const CT d = s + eps;
     const CT rd = safe_rcp(d);
     const CT rs = safe_rcp(s);
@@ -78,10 +90,10 @@ struct AdamBwd {
     y[1] = b1 * (dm1 - du * lr_rd * ibc1);
     y[2] = b2 * (dv1 + du * w * ibc2);
     if (want_hp) {
-      h[0] += (double)(-du * mhat * rd);
-      h[1] += (double)(dm1 * (m - g) - du * lr_rd * (m * K1 - g * K2));
-      h[2] += (double)(dv1 * (v - gg) + du * w * (v * K3 - gg * K4));
-      h[3] += (double)(du * lr * mhat * rd2);
+      h[0] += (-du * mhat * rd);
+      h[1] += (dm1 * (m - g) - du * lr_rd * (m * K1 - g * K2));
+      h[2] += (dv1 * (v - gg) + du * w * (v * K3 - gg * K4));
+      h[3] += (du * lr * mhat * rd2);
     }
   }
 };
@@ -95,12 +107,12 @@ struct RmsFwd {
   __host__ __device__ static constexpr bool out_state(int i) { return i == 1; }
   CT alpha, oma, lr, eps;
 
-  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], double*,
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT*,
                                              bool) const {
     const CT g = x[0], v = x[1];
     const CT v1 = alpha * v + oma * (g * g);
-    const CT d = sqrt(v1) + eps;
-    const CT u = d == CT(0) ? CT(0) : (-lr * g) / d;
+    const CT d = ct_sqrt(v1) + eps;
+    const CT u = d == CT(0) ? CT(0) : ct_div(-lr * g, d);
     y[0] = u;
     y[1] = v1;
     y[2] = CT(x[2]) + u;
@@ -116,11 +128,11 @@ struct RmsBwd {
   __host__ __device__ static constexpr bool out_state(int) { return false; }
   CT alpha, oma, two_oma, lr, eps;
 
-  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], double* h,
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT* h,
                                              bool want_hp) const {
     const CT g = x[0], v = x[1], du = x[2], dv1 = x[3];
     const CT gg = g * g;
-    const CT s = sqrt(alpha * v + oma * gg);
+    const CT s = ct_sqrt(alpha * v + oma * gg);
     const CT d = s + eps;
     const CT rd = safe_rcp(d);
     const CT rs = safe_rcp(s);
@@ -130,9 +142,9 @@ struct RmsBwd {
     y[0] = two_oma * g * dv1 - du * lr * rd2 * (eps + alpha * v * rs);
     y[1] = alpha * V;
     if (want_hp) {
-      h[0] += (double)(-du * g * rd);
-      h[1] += (double)(V * (v - gg));
-      h[2] += (double)(du * lr * g * rd2);
+      h[0] += (-du * g * rd);
+      h[1] += (V * (v - gg));
+      h[2] += (du * lr * g * rd2);
     }
   }
 };
@@ -147,7 +159,7 @@ struct SgdFwd {
   CT lr, mu;
   int nesterov;
 
-  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], double*,
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT*,
                                              bool) const {
     const CT g = x[0], b = x[1];
     const CT b1 = mu * b + g;
@@ -167,7 +179,7 @@ struct SgdBwd {
   CT lr, mu;
   int nesterov;
 
-  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], double* h,
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT* h,
                                              bool want_hp) const {
     const CT g = x[0], b = x[1], du = x[2], db1 = x[3];
     const CT b1 = mu * b + g;
@@ -176,16 +188,16 @@ struct SgdBwd {
       y[0] = B - lr * du;
       y[1] = mu * B;
       if (want_hp) {
-        h[0] += (double)(-du * (g + mu * b1));
-        h[1] += (double)(B * b - du * lr * b1);
+        h[0] += (-du * (g + mu * b1));
+        h[1] += (B * b - du * lr * b1);
       }
     } else {
       const CT B = db1 - lr * du;
       y[0] = B;
       y[1] = mu * B;
       if (want_hp) {
-        h[0] += (double)(-du * b1);
-        h[1] += (double)(B * b);
+        h[0] += (-du * b1);
+        h[1] += (B * b);
       }
     }
   }

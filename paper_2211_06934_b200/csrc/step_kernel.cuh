@@ -66,16 +66,24 @@ __device__ __forceinline__ void compute_store_vec(const Op& op,
                                                   int64_t v, const float (&x)[Op::NIN][4],
                                                   double* acc, bool want_hp) {
   typedef typename Op::CT CT;
+  constexpr int NH = Op::NH > 0 ? Op::NH : 1;
   CT y[Op::NOUT][4];
+  CT hv[NH];  // this vector's hyper terms in CT, then one fp64 add each
+#pragma unroll
+  for (int k = 0; k < NH; ++k) hv[k] = CT(0);
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     float xe[Op::NIN];
 #pragma unroll
     for (int i = 0; i < Op::NIN; ++i) xe[i] = x[i][e];
     CT ye[Op::NOUT];
-    op(xe, ye, acc, want_hp);
+    op(xe, ye, hv, want_hp);
 #pragma unroll
     for (int o = 0; o < Op::NOUT; ++o) y[o][e] = ye[o];
+  }
+  if (Op::NH > 0 && want_hp) {
+#pragma unroll
+    for (int k = 0; k < Op::NH; ++k) acc[k] += (double)hv[k];
   }
 #pragma unroll
   for (int o = 0; o < Op::NOUT; ++o) {
@@ -102,7 +110,15 @@ __device__ __forceinline__ void process_elem(const Op& op, const StepArgs<Op::NI
       xe[k] = 0.f;
   }
   CT ye[Op::NOUT];
-  op(xe, ye, acc, want_hp);
+  constexpr int NH = Op::NH > 0 ? Op::NH : 1;
+  CT hv[NH];
+#pragma unroll
+  for (int k = 0; k < NH; ++k) hv[k] = CT(0);
+  op(xe, ye, hv, want_hp);
+  if (Op::NH > 0 && want_hp) {
+#pragma unroll
+    for (int k = 0; k < Op::NH; ++k) acc[k] += (double)hv[k];
+  }
 #pragma unroll
   for (int o = 0; o < Op::NOUT; ++o) {
     if (a.out[o]) {
@@ -178,8 +194,8 @@ __device__ __forceinline__ bool last_block(unsigned int* counter, unsigned int n
 }
 
 // ------------------------------------------------------- uniform kernel
-template <class Op, class ST, int U>
-__global__ void __launch_bounds__(kBlock) step_uniform(const Op op,
+template <class Op, class ST, int U, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) step_uniform(const Op op,
                                                        const StepArgs<Op::NIN, Op::NOUT> a) {
   constexpr int NH = Op::NH > 0 ? Op::NH : 1;
   const bool want_hp = Op::NH > 0 && a.want_hp;
@@ -226,8 +242,8 @@ __global__ void __launch_bounds__(kBlock) step_uniform(const Op op,
 // Dynamic smem: s_off[n_leaves+1], s_tp[n_leaves+1] (first tile of leaf l).
 __device__ __forceinline__ int64_t tiles_of(int64_t len) { return (len + kTile - 1) / kTile; }
 
-template <class Op, class ST, int U>
-__global__ void __launch_bounds__(kBlock) step_leaf(const Op op,
+template <class Op, class ST, int U, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) step_leaf(const Op op,
                                                     const StepArgs<Op::NIN, Op::NOUT> a) {
   static_assert(Op::NH > 0, "leaf mode is for ops with hyper-gradient sums");
   constexpr int NH = Op::NH;

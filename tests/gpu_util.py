@@ -37,15 +37,17 @@ def state_host_bits(x, bf16):
     return synth.to_bf16_bits(x) if bf16 else x
 
 
-def tol_fail(x, ref, rtol=1e-5, atol=1e-6):
-    """Boolean mask of elements outside |x - ref| <= atol + rtol |ref|."""
+def tol_fail(x, ref, rtol=1e-5, atol=1e-6, scale=None):
+    """Boolean mask of elements outside |x - ref| <= atol + rtol * scale
+    (scale defaults to |ref|)."""
     x = np.asarray(x, np.float64)
     ref = np.asarray(ref, np.float64)
-    return ~(np.abs(x - ref) <= atol + rtol * np.abs(ref))
+    sc = np.abs(ref) if scale is None else np.asarray(scale, np.float64)
+    return ~(np.abs(x - ref) <= atol + rtol * sc)
 
 
-def assert_close(name, x, ref, rtol=1e-5, atol=1e-6):
-    bad = tol_fail(x, ref, rtol, atol)
+def assert_close(name, x, ref, rtol=1e-5, atol=1e-6, scale=None):
+    bad = tol_fail(x, ref, rtol, atol, scale)
     if bad.any():
         i = np.flatnonzero(bad)[:5]
         raise AssertionError(f"{name}: {bad.sum()}/{bad.size} outside tol (rtol={rtol}, atol={atol});"

@@ -472,3 +472,69 @@ def test_sweep_adam_vs_central_fd(orc):
     h = 1e-6
     fd = (L(phi + h) - L(phi - h)) / (2 * h)
     np.testing.assert_allclose(r["phi_bar"], fd, rtol=1e-4, atol=1e-9)
+
+
+# ------------------------------------ magnitude twins (tolerance, Z10)
+def test_mag_twins_bound_the_values(orc):
+    """Every magnitude twin is the same expression tree over |.|, so it
+    bounds the absolute value of the exact result (a property any slip in
+    the twin -- a missing term -- would eventually break)."""
+    x = synth.state_tree(71, [3000, 97])
+    g, m, v, du, dm1, dv1 = (x[k] for k in ("g", "m", "v", "du", "dm1", "dv1"))
+    for t in (1, 10):
+        hp = (0.5, 0.9, 0.999, 1e-8)
+        mag = orc.adam_mag(g, m, v, du, dm1, dv1, t, *hp)
+        u, m1, v1 = orc.adam_fwd(g, m, v, t, *hp, prec=1)
+        r = orc.adam_vjp(g, m, v, du, dm1, dv1, t, *hp, prec=1)
+        for k, val in (("u", u), ("m1", m1), ("v1", v1), ("dg", r["dg"]), ("dm", r["dm"]),
+                       ("dv", r["dv"])):
+            assert np.all(np.abs(val) <= mag[k] * (1 + 1e-9) + 1e-300), k
+        assert np.all(np.abs(r["dhp"]) <= mag["dhp"] * (1 + 1e-9))
+    magr = orc.rmsprop_mag(g, v, du, dv1, 0.3, 0.99, 1e-8)
+    rr = orc.rmsprop_vjp(g, v, du, dv1, 0.3, 0.99, 1e-8, prec=1)
+    ur, vr = orc.rmsprop_fwd(g, v, 0.3, 0.99, 1e-8, prec=1)
+    for k, val in (("u", ur), ("v1", vr), ("dg", rr["dg"]), ("dv", rr["dv"])):
+        assert np.all(np.abs(val) <= magr[k] * (1 + 1e-9) + 1e-300), k
+    for nest in (False, True):
+        mags = orc.sgd_mag(g, m, du, dm1, 0.1, 0.9, nest)
+        rs = orc.sgd_vjp(g, m, du, dm1, 0.1, 0.9, nest, prec=1)
+        us, bs = orc.sgd_fwd(g, m, 0.1, 0.9, nest, prec=1)
+        for k, val in (("u", us), ("b1", bs), ("dg", rs["dg"]), ("db", rs["db"])):
+            assert np.all(np.abs(val) <= mags[k] * (1 + 1e-9) + 1e-300), k
+
+
+def _f32_adam_dg(g, du, lr, b1, b2, eps, reduced):
+    """numpy float32 emulation of an fp32 kernel's dg at t=1 from zero state
+    with zero m'/v' cotangents: the textbook chain rule vs the reduced form."""
+    f = np.float32
+    g, du = g.astype(f), du.astype(f)
+    b1, b2, lr, eps = f(b1), f(b2), f(lr), f(eps)
+    bc1, bc2 = f(1) - b1, f(1) - b2
+    A, C = (f(1) - b1) / bc1, (f(1) - b2) / bc2
+    mhat = A * g
+    s = np.sqrt(C * g * g)
+    d = s + eps
+    if reduced:
+        rs = np.where(s == 0, f(0), f(1) / np.where(s == 0, f(1), s))
+        return -du * lr * (A * eps + (f(0) - f(0) * C * g) * rs) / (d * d)
+    dmhat = du * (-lr / d)
+    dd = du * (lr * mhat / (d * d))
+    dvhat = np.where(s == 0, f(0), dd / (f(2) * np.where(s == 0, f(1), s)))
+    return dmhat / bc1 * (f(1) - b1) + dvhat / bc2 * (f(1) - b2) * f(2) * g
+
+
+def test_mag_criterion_has_teeth(orc):
+    """The fp32 criterion |x-ref| <= 1e-6 + 1e-5 mag is passed by an fp32
+    evaluation of the reduced form and failed by an fp32 evaluation of the
+    textbook chain rule (100% vs ~7% at lr=1, t=1)."""
+    rng = np.random.default_rng(3)
+    n = 1 << 16
+    g = (1e-2 * rng.standard_normal(n)).astype(np.float32)
+    du = rng.standard_normal(n).astype(np.float32)
+    hp = (1.0, 0.9, 0.999, 1e-8)
+    r = orc.adam_vjp(g, None, None, du, None, None, 1, *hp, prec=1)
+    mag = orc.adam_mag(g, None, None, du, None, None, 1, *hp)
+    ok = lambda x: np.abs(x.astype(np.float64) - r["dg"]) <= 1e-6 + 1e-5 * np.maximum(
+        mag["dg"], np.abs(r["dg"]))
+    assert ok(_f32_adam_dg(g, du, *hp, reduced=True)).mean() == 1.0
+    assert ok(_f32_adam_dg(g, du, *hp, reduced=False)).mean() < 0.5

@@ -1,0 +1,36 @@
+"""Build libdiffopt variants with different launch shapes for a tuning sweep:
+tools/tune_build/lib_<tag>.so, tag = U_F-MINB_F-U_B-MINB_B[-extra]."""
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2211_06934_b200 import build as B  # noqa: E402
+
+OUT = os.path.join(ROOT, "tools", "tune_build")
+
+
+def one(cfg):
+    uf, mf, ub, mb, extra = cfg
+    tag = f"{uf}-{mf}-{ub}-{mb}" + (f"-{extra}" if extra else "")
+    defs = [f"DOPT_U_FWD={uf}", f"DOPT_MINB_FWD={mf}", f"DOPT_U_BWD={ub}", f"DOPT_MINB_BWD={mb}"]
+    if "ieee" in extra:
+        defs.append("DOPT_IEEE_F32")
+    if "tma" in extra:
+        defs += ["DOPT_TMA_FWD=1", "DOPT_TMA_BWD=1"]
+    out = os.path.join(OUT, f"lib_{tag}.so")
+    B.build(force=True, out=out, defines=defs)
+    return out
+
+
+if __name__ == "__main__":
+    os.makedirs(OUT, exist_ok=True)
+    cfgs = []
+    for arg in sys.argv[1:]:
+        parts = arg.split("-")
+        cfgs.append(tuple(int(p) for p in parts[:4]) + ((parts[4] if len(parts) > 4 else ""),))
+    with ThreadPoolExecutor(8) as ex:
+        for o in ex.map(one, cfgs):
+            print(o)
