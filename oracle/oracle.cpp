@@ -268,7 +268,7 @@ StepRes<T> step_fwd(int kind, T g, T s1, T s2, const double* hp, int64_t t) {
 
 template <class T>
 void sweep_elem(int kind, int64_t K, const double* hp, T a, T th0, T phi, T y,
-                T* phi_bar, T* th0_bar, T* hyper, T* loss, T* thK) {
+                T* phi_bar, T* th0_bar, T* hyper, T* loss, T* thK, double* bar_abs) {
   std::vector<T> gk(K), s1k(K + 1), s2k(K + 1);
   T th = th0;
   s1k[0] = T(0);
@@ -283,6 +283,7 @@ void sweep_elem(int kind, int64_t K, const double* hp, T a, T th0, T phi, T y,
   *thK = th;
   *loss = T(0.5) * (th - y) * (th - y);
   T thb = th - y, s1b = T(0), s2b = T(0), phib = T(0);
+  double babs = std::fabs((double)thb);  // Sigma |terms| of theta_bar / phi_bar
   for (int k = 0; k < 4; ++k) hyper[k] = T(0);
   for (int64_t k = K - 1; k >= 0; --k) {
     T gb;
@@ -304,7 +305,9 @@ void sweep_elem(int kind, int64_t K, const double* hp, T a, T th0, T phi, T y,
     // theta_{k+1} = theta_k + u_k  -> identity on theta_bar, plus g_k = a (theta_k - phi)
     thb = thb + a * gb;
     phib = phib - a * gb;
+    babs += std::fabs((double)(a * gb));
   }
+  *bar_abs = babs;
   *phi_bar = phib;
   *th0_bar = thb;
 }
@@ -428,7 +431,7 @@ void oracle_bf16_rne(int64_t n, const double* x, uint16_t* out) {
 void oracle_sweep_quadratic(int kind, int64_t n, int64_t K, const double* hp, int prec,
                             const float* a, const float* theta0, const float* phi,
                             const float* y, double* phi_bar, double* theta0_bar,
-                            double* hyper_bar, double* loss, double* thetaK) {
+                            double* hyper_bar, double* loss, double* thetaK, double* bar_abs) {
   std::vector<long double> hyp_part((size_t)((n + kChunk - 1) / kChunk + 1) * 5, 0.0L);
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
 #ifdef _OPENMP
@@ -440,7 +443,9 @@ void oracle_sweep_quadratic(int kind, int64_t n, int64_t K, const double* hp, in
     for (int64_t i = lo; i < hi; ++i) {
       if (prec) {
         long double pb, tb, h[4], l, tk;
-        sweep_elem<long double>(kind, K, hp, a[i], theta0[i], phi[i], y[i], &pb, &tb, h, &l, &tk);
+        double ba;
+        sweep_elem<long double>(kind, K, hp, a[i], theta0[i], phi[i], y[i], &pb, &tb, h, &l, &tk, &ba);
+        put(bar_abs, i, ba);
         put(phi_bar, i, (double)pb);
         put(theta0_bar, i, (double)tb);
         put(thetaK, i, (double)tk);
@@ -448,7 +453,9 @@ void oracle_sweep_quadratic(int kind, int64_t n, int64_t K, const double* hp, in
         acc[4] += l;
       } else {
         double pb, tb, h[4], l, tk;
-        sweep_elem<double>(kind, K, hp, a[i], theta0[i], phi[i], y[i], &pb, &tb, h, &l, &tk);
+        double ba;
+        sweep_elem<double>(kind, K, hp, a[i], theta0[i], phi[i], y[i], &pb, &tb, h, &l, &tk, &ba);
+        put(bar_abs, i, ba);
         put(phi_bar, i, pb);
         put(theta0_bar, i, tb);
         put(thetaK, i, tk);

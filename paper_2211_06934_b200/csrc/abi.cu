@@ -164,16 +164,16 @@ int zero_outputs(const opt_tree* t, int nh, double* d_hp, double* d_hp_leaf, cud
 // blocks per SM requested from ptxas (register cap). Tuned on B200
 // (DESIGN.md "Kernels"); -D overrides exist for tuning sweeps.
 #ifndef DOPT_U_FWD
-#define DOPT_U_FWD 2
+#define DOPT_U_FWD 1
 #endif
 #ifndef DOPT_MINB_FWD
 #define DOPT_MINB_FWD 1
 #endif
 #ifndef DOPT_U_BWD
-#define DOPT_U_BWD 2
+#define DOPT_U_BWD 1
 #endif
 #ifndef DOPT_MINB_BWD
-#define DOPT_MINB_BWD 1
+#define DOPT_MINB_BWD 3
 #endif
 
 #ifndef DOPT_TMA_FWD

@@ -1,0 +1,167 @@
+"""GPU tests of the drivers above the C ABI: the K-step unrolled sweep (row
+a9) against the oracle sweep, the autograd wiring (functional API, P:246
+torch.autograd.Function) against the oracle VJP, and the MAML meta-batch
+(row a10) with the fused inner step against a plain-torch inner step."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import DEV, assert_close, assert_sum_close, dev_f32, host
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2211_06934_b200 as p
+
+    return p
+
+
+SWEEP_CASES = [("adam", (1e-2, 0.9, 0.999, 1e-8, 0.0)), ("rmsprop", (1e-2, 0.99, 1e-8)),
+               ("sgd", (0.1, 0.9, False)), ("sgd", (0.1, 0.9, True))]
+
+
+@pytest.mark.parametrize("kind,hp", SWEEP_CASES)
+@pytest.mark.parametrize("K", [1, 5])
+def test_sweep_matches_oracle(pkg, kind, hp, K):
+    from paper_2211_06934_b200.unroll import QuadraticSweep, NH
+
+    leaves = [7, 4096, 333, 5000, 1]
+    n = sum(leaves)
+    q = synth.quadratic_problem(0xC3, n)
+    tree = pkg.Tree(offsets=synth.offsets_of(leaves), device=DEV)
+    sw = QuadraticSweep(tree, kind, hp, K, DEV)
+    a, th0, phi, y = (dev_f32(q[k]) for k in ("a", "theta0", "phi", "y"))
+    thK, phib, th0b, hyper = sw.run(a, th0, phi, y)
+    torch.cuda.synchronize()
+    ohp = list(hp[:2]) + [1.0 if hp[2] else 0.0] if kind == "sgd" else list(hp)
+    ref = oracle.sweep_quadratic(kind, q["a"], q["theta0"], q["phi"], q["y"], K, ohp, prec=1)
+    assert_close("thetaK", host(thK), ref["thetaK"], rtol=1e-5, atol=1e-6,
+                 scale=np.abs(ref["thetaK"]) + np.abs(q["theta0"]))
+    assert_close("phi_bar", host(phib), ref["phi_bar"], scale=ref["bar_abs"])
+    assert_close("theta0_bar", host(th0b), ref["theta0_bar"], scale=ref["bar_abs"])
+    hs = host(hyper).sum(0)
+    nh = NH[kind]
+    hp_abs = np.abs(host(hyper)).sum(0)
+    assert_sum_close("hyper", hs[:nh], ref["hyper_bar"][:nh], hp_abs[:nh] + 1e-3 * np.abs(hs[:nh]))
+    assert sw.launches_per_sweep == 4 * K + 2
+
+
+def test_sweep_bytes_accounting(pkg):
+    from paper_2211_06934_b200.unroll import QuadraticSweep
+
+    tree = pkg.Tree(numel=1024, device=DEV)
+    sw = QuadraticSweep(tree, "adam", (1e-2, 0.9, 0.999, 1e-8, 0.0), 5, DEV)
+    # K=5 Adam: fwd 5x16 + (20 + 4x28) ; outer 16 ; reverse 5x(24 incl.) ...
+    per = sw.alg_bytes() // 1024
+    assert 250 <= per <= 400
+
+
+# ------------------------------------------------- autograd / functional
+def test_adam_autograd_matches_oracle(pkg):
+    """AdamStep.apply forward + torch.autograd backward (through the C ABI)
+    equals the oracle's step and VJP, including the lr hyper-gradient."""
+    x = synth.state_tree(0xF1, [1000, 37])
+    g = dev_f32(x["g"]).requires_grad_(True)
+    m = dev_f32(x["m"]).requires_grad_(True)
+    v = dev_f32(x["v"]).requires_grad_(True)
+    lr = torch.tensor(1e-2, dtype=torch.float64, requires_grad=True)
+    cfg = pkg.functional.StepConfig(pkg.Tree(numel=g.numel(), device=DEV))
+    u, m1, v1 = pkg.AdamStep.apply(g, m, v, None, lr, 0.9, 0.999, 1e-8, 5, 0.0, cfg)
+    du, dm1, dv1 = dev_f32(x["du"]), dev_f32(x["dm1"]), dev_f32(x["dv1"])
+    loss = (u * du).sum() + (m1 * dm1).sum() + (v1 * dv1).sum()
+    gg, gm, gv, glr = torch.autograd.grad(loss, [g, m, v, lr])
+    r = oracle.adam_vjp(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], 5, 1e-2, 0.9, 0.999,
+                        1e-8, prec=1)
+    mag = oracle.adam_mag(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], 5, 1e-2, 0.9, 0.999,
+                          1e-8)
+    for name, got in (("dg", gg), ("dm", gm), ("dv", gv)):
+        assert_close(name, host(got), r[name], scale=np.maximum(np.abs(r[name]), mag[name]))
+    assert_sum_close("dlr", [float(glr)], [r["dhp"][0]], [mag["dhp"][0]])
+
+
+def test_listing1_functional_api_two_steps(pkg):
+    """Listing 1: opt.init / opt.update(inplace=False) /
+    apply_updates over a 3-leaf tree for two steps, meta-gradient w.r.t. a
+    meta-parameter scaling the inner loss; compared with the same program
+    on plain torch ops in float64 (independent composed implementation)."""
+    torch.manual_seed(0)
+    shapes = [(5, 3), (7,), (2, 2, 2)]
+    params0 = [torch.randn(s, device=DEV) for s in shapes]
+    target = [torch.randn(s, device=DEV) for s in shapes]
+
+    def run(use_fused, dtype):
+        meta = torch.tensor(1.5, device=DEV, dtype=dtype, requires_grad=True)
+        params = [p.to(dtype).clone().requires_grad_(True) for p in params0]
+        if use_fused:
+            opt = pkg.adam(lr=0.1)
+            layout = pkg.FlatTree.of(params)
+            flat = layout.flatten(params)
+            state = opt.init(params)
+            for _ in range(2):
+                ps = layout.views(flat)
+                inner = meta * sum(((p - t) ** 2).sum() for p, t in zip(ps, target))
+                (gflat,) = torch.autograd.grad(inner, flat, create_graph=True)
+                upd, state = opt.update(gflat, state, inplace=False)
+                flat = pkg.apply_updates(flat, upd)
+            ps = layout.views(flat)
+        else:
+            ps = params
+            m = [torch.zeros_like(p) for p in ps]
+            v = [torch.zeros_like(p) for p in ps]
+            for t in (1, 2):
+                inner = meta * sum(((p - tt.to(dtype)) ** 2).sum() for p, tt in zip(ps, target))
+                gs = torch.autograd.grad(inner, ps, create_graph=True)
+                m = [0.9 * mm + 0.1 * gg for mm, gg in zip(m, gs)]
+                v = [0.999 * vv + 0.001 * gg * gg for vv, gg in zip(v, gs)]
+                ps = [p - 0.1 * (mm / (1 - 0.9 ** t)) / ((vv / (1 - 0.999 ** t)).sqrt() + 1e-8)
+                      for p, mm, vv in zip(ps, m, v)]
+        outer = sum((p.to(torch.float64) ** 2).sum() for p in ps)
+        (gmeta,) = torch.autograd.grad(outer, meta)
+        return float(outer), float(gmeta)
+
+    o_f, g_f = run(True, torch.float32)
+    o_r, g_r = run(False, torch.float64)
+    assert o_f == pytest.approx(o_r, rel=1e-5)
+    assert g_f == pytest.approx(g_r, rel=1e-3, abs=1e-6)
+
+
+def test_inplace_differentiable_rejected(pkg):
+    opt = pkg.adam(lr=0.1)
+    p = torch.randn(8, device=DEV, requires_grad=True)
+    state = opt.init(p)
+    g = (p * 2).detach().requires_grad_(True)
+    with pytest.raises(RuntimeError):
+        opt.update(g, state, inplace=True)
+
+
+# ---------------------------------------------------------------- MAML
+def test_maml_fused_inner_matches_torch_inner(pkg):
+    """One outer step of a 2-task, 2-inner-step meta-batch: the fused CUDA
+    SGD-momentum step (create_graph second-order path) gives the same
+    meta-gradient as a plain-torch differentiable SGD-momentum step."""
+    from paper_2211_06934_b200 import maml
+
+    cfg = maml.MamlConfig(tasks=2, inner_steps=2)
+    phi = maml.init_params(0, DEV)
+    inner = maml.FusedSgdInner(maml.sizes_of(maml.CONV4_SHAPES), DEV, cfg)
+
+    def torch_inner(g, b, theta):
+        b1 = g if b is None else cfg.inner_momentum * b + g
+        return theta - cfg.inner_lr * b1, b1
+
+    torch.backends.cudnn.deterministic = True
+    mg_f, loss_f = maml.meta_grad_tasks(phi, range(2), 0, cfg, inner)
+    mg_t, loss_t = maml.meta_grad_tasks(phi, range(2), 0, cfg, torch_inner)
+    assert float(loss_f) == pytest.approx(float(loss_t), rel=1e-5)
+    err = (mg_f - mg_t).norm() / mg_t.norm()
+    assert float(err) < 1e-4
+    outer = maml.FusedAdamOuter(phi.numel(), DEV, 1e-3)
+    phi2 = phi.clone()
+    outer(phi2, mg_f)
+    assert torch.isfinite(phi2).all() and not torch.equal(phi2, phi)
