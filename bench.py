@@ -233,7 +233,14 @@ def time_ours(args, workload_inputs, dev, rank, world):
 
 
 def time_e2e(args, W, dev):
+    """End-to-end through the public API with HOST buffers: the inputs live
+    in pinned host memory and the outputs land there. Primary: the streamed
+    path (offload.HostStreamedAdam: chunked H2D / fused kernels / D2H on
+    three streams); also reported: plain serial staging (all H2D, the two
+    C-ABI calls, all D2H)."""
     import torch
+
+    from paper_2211_06934_b200.offload import HostStreamedAdam, IN_KEYS, OUT_KEYS
 
     t = torch
     s0 = W.sets[0]
@@ -244,7 +251,19 @@ def time_e2e(args, W, dev):
     stream = t.cuda.current_stream()
     steps = max(3, min(args.steps, 20))
 
-    def one():
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        t.cuda.synchronize()
+        a, b = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            fn()
+        b.record(stream)
+        t.cuda.synchronize()
+        return a.elapsed_time(b) / steps
+
+    def serial():
         for k in ins:
             s0[k].copy_(h_in[k], non_blocking=True)
         W.fwd(s0)
@@ -252,22 +271,26 @@ def time_e2e(args, W, dev):
         for k in outs:
             h_out[k].copy_(s0[k], non_blocking=True)
 
-    for _ in range(2):
-        one()
-    t.cuda.synchronize()
-    a, b = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for _ in range(steps):
-        one()
-    b.record(stream)
-    t.cuda.synchronize()
-    ms = a.elapsed_time(b) / steps
-    h2d = sum(h_in[k].numel() * h_in[k].element_size() for k in ins)
-    d2h = sum(h_out[k].numel() * h_out[k].element_size() for k in outs)
-    return {"value": (W.bytes_fwd + W.bytes_bwd) / (ms * 1e-3) / 1e9, "unit": "GB/s",
-            "ms_per_step": ms, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "how": "C-ABI opt_adam_fwd/bwd on device buffers staged from pinned host memory; "
-                   "H2D of the 6 inputs and D2H of the 6 outputs + d_hp inside the timed region"}
+    ms_serial = timed(serial)
+    out = {"serial_ms_per_step": round(ms_serial, 4)}
+    if W.sd == 0 and W.n >= 1 << 16:
+        hs = HostStreamedAdam(W.n, dev, chunks=16, compute=W.compute)
+        hin = {k: h_in[k] for k in IN_KEYS}
+        hout = {k: h_out[k] for k in OUT_KEYS}
+        ms = timed(lambda: hs.run(hin, hout, STEP_T, HP))
+        h2d, d2h = hs.bytes_h2d(), hs.bytes_d2h()
+        how = ("paper_2211_06934_b200.offload.HostStreamedAdam: pinned host inputs/outputs, "
+               "16 chunks, H2D / opt_adam_fwd+bwd / D2H overlapped on 3 streams; all copies "
+               "inside the timed region")
+    else:
+        ms = ms_serial
+        h2d = sum(h_in[k].numel() * h_in[k].element_size() for k in ins)
+        d2h = sum(h_out[k].numel() * h_out[k].element_size() for k in outs)
+        how = "serial staging: H2D of the inputs, opt_adam_fwd/bwd, D2H of the outputs"
+    out.update({"value": round((W.bytes_fwd + W.bytes_bwd) / (ms * 1e-3) / 1e9, 2),
+                "unit": "GB/s", "ms_per_step": round(ms, 4), "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "how": how})
+    return out
 
 
 # --------------------------------------------------- CPU oracle timing

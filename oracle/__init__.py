@@ -55,7 +55,7 @@ def lib():
         L.oracle_sgd_fwd.argtypes = [i64, P, I, I, P, P, P, P]
         L.oracle_sgd_vjp.argtypes = [i64, P, I, I, P, P, P, P, P, P, P, P, i64, P, P]
         L.oracle_bf16_rne.argtypes = [i64, P, P]
-        L.oracle_sweep_quadratic.argtypes = [I, i64, i64, P, I, P, P, P, P, P, P, P, P, P, P]
+        L.oracle_sweep_quadratic.argtypes = [I, i64, i64, P, I, P, P, P, P, P, P, P, P, P, P, P]
         L.oracle_adam_fwd_cplx.argtypes = [i64, i64] + [P] * 14
         L.oracle_rmsprop_fwd_cplx.argtypes = [i64] + [P] * 10
         L.oracle_sgd_fwd_cplx.argtypes = [i64, P, P, I] + [P] * 8
@@ -223,12 +223,13 @@ def sweep_quadratic(kind, a, theta0, phi, y, K, hp, prec=0):
     n = a.size
     hp = _hp(list(hp) + [0.0] * (5 - len(hp)))
     pb, tb, tk, ba = _out(n), _out(n), _out(n), _out(n)
-    hyp = np.zeros(4)
+    hyp, habs = np.zeros(4), np.zeros(4)
     loss = np.zeros(1)
     lib().oracle_sweep_quadratic(KIND[kind], n, int(K), _p(hp), int(prec), _p(a), _p(theta0),
-                                 _p(phi), _p(y), _p(pb), _p(tb), _p(hyp), _p(loss), _p(tk), _p(ba))
+                                 _p(phi), _p(y), _p(pb), _p(tb), _p(hyp), _p(loss), _p(tk), _p(ba),
+                                 _p(habs))
     return dict(phi_bar=pb, theta0_bar=tb, hyper_bar=hyp, loss=float(loss[0]), thetaK=tk,
-                bar_abs=ba)
+                bar_abs=ba, hyper_abs=habs)
 
 
 # --------------------------------------------------- complex-step helpers

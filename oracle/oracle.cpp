@@ -268,7 +268,8 @@ StepRes<T> step_fwd(int kind, T g, T s1, T s2, const double* hp, int64_t t) {
 
 template <class T>
 void sweep_elem(int kind, int64_t K, const double* hp, T a, T th0, T phi, T y,
-                T* phi_bar, T* th0_bar, T* hyper, T* loss, T* thK, double* bar_abs) {
+                T* phi_bar, T* th0_bar, T* hyper, T* loss, T* thK, double* bar_abs,
+                double* hyper_abs) {
   std::vector<T> gk(K), s1k(K + 1), s2k(K + 1);
   T th = th0;
   s1k[0] = T(0);
@@ -284,7 +285,10 @@ void sweep_elem(int kind, int64_t K, const double* hp, T a, T th0, T phi, T y,
   *loss = T(0.5) * (th - y) * (th - y);
   T thb = th - y, s1b = T(0), s2b = T(0), phib = T(0);
   double babs = std::fabs((double)thb);  // Sigma |terms| of theta_bar / phi_bar
-  for (int k = 0; k < 4; ++k) hyper[k] = T(0);
+  for (int k = 0; k < 4; ++k) {
+    hyper[k] = T(0);
+    hyper_abs[k] = 0.0;
+  }
   for (int64_t k = K - 1; k >= 0; --k) {
     T gb;
     if (kind == 0) {
@@ -292,15 +296,20 @@ void sweep_elem(int kind, int64_t K, const double* hp, T a, T th0, T phi, T y,
       gb = r.dg; s1b = r.dm; s2b = r.dv;
       hyper[0] = hyper[0] + r.dlr; hyper[1] = hyper[1] + r.db1;
       hyper[2] = hyper[2] + r.db2; hyper[3] = hyper[3] + r.deps;
+      hyper_abs[0] += std::fabs((double)r.dlr); hyper_abs[1] += std::fabs((double)r.db1);
+      hyper_abs[2] += std::fabs((double)r.db2); hyper_abs[3] += std::fabs((double)r.deps);
     } else if (kind == 1) {
       auto r = oracle::rmsprop_vjp<T>(gk[k], s1k[k], thb, s1b, rms_hp<T>(hp));
       gb = r.dg; s1b = r.dv;
       hyper[0] = hyper[0] + r.dlr; hyper[1] = hyper[1] + r.dalpha;
       hyper[2] = hyper[2] + r.deps;
+      hyper_abs[0] += std::fabs((double)r.dlr); hyper_abs[1] += std::fabs((double)r.dalpha);
+      hyper_abs[2] += std::fabs((double)r.deps);
     } else {
       auto r = oracle::sgd_vjp<T>(gk[k], s1k[k], thb, s1b, sgd_hp<T>(hp));
       gb = r.dg; s1b = r.db;
       hyper[0] = hyper[0] + r.dlr; hyper[1] = hyper[1] + r.dmu;
+      hyper_abs[0] += std::fabs((double)r.dlr); hyper_abs[1] += std::fabs((double)r.dmu);
     }
     // theta_{k+1} = theta_k + u_k  -> identity on theta_bar, plus g_k = a (theta_k - phi)
     thb = thb + a * gb;
@@ -431,21 +440,24 @@ void oracle_bf16_rne(int64_t n, const double* x, uint16_t* out) {
 void oracle_sweep_quadratic(int kind, int64_t n, int64_t K, const double* hp, int prec,
                             const float* a, const float* theta0, const float* phi,
                             const float* y, double* phi_bar, double* theta0_bar,
-                            double* hyper_bar, double* loss, double* thetaK, double* bar_abs) {
-  std::vector<long double> hyp_part((size_t)((n + kChunk - 1) / kChunk + 1) * 5, 0.0L);
+                            double* hyper_bar, double* loss, double* thetaK, double* bar_abs,
+                            double* hyper_abs) {
+  std::vector<long double> hyp_part((size_t)((n + kChunk - 1) / kChunk + 1) * 9, 0.0L);
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
 #ifdef _OPENMP
 #pragma omp parallel for schedule(static) num_threads(g_threads)
 #endif
   for (int64_t c = 0; c < nchunks; ++c) {
-    long double* acc = &hyp_part[(size_t)c * 5];
+    long double* acc = &hyp_part[(size_t)c * 9];
     const int64_t lo = c * kChunk, hi = (lo + kChunk < n) ? lo + kChunk : n;
     for (int64_t i = lo; i < hi; ++i) {
       if (prec) {
         long double pb, tb, h[4], l, tk;
-        double ba;
-        sweep_elem<long double>(kind, K, hp, a[i], theta0[i], phi[i], y[i], &pb, &tb, h, &l, &tk, &ba);
+        double ba, habs[4];
+        sweep_elem<long double>(kind, K, hp, a[i], theta0[i], phi[i], y[i], &pb, &tb, h, &l, &tk, &ba,
+                                habs);
         put(bar_abs, i, ba);
+        for (int k = 0; k < 4; ++k) acc[5 + k] += habs[k];
         put(phi_bar, i, (double)pb);
         put(theta0_bar, i, (double)tb);
         put(thetaK, i, (double)tk);
@@ -453,9 +465,11 @@ void oracle_sweep_quadratic(int kind, int64_t n, int64_t K, const double* hp, in
         acc[4] += l;
       } else {
         double pb, tb, h[4], l, tk;
-        double ba;
-        sweep_elem<double>(kind, K, hp, a[i], theta0[i], phi[i], y[i], &pb, &tb, h, &l, &tk, &ba);
+        double ba, habs[4];
+        sweep_elem<double>(kind, K, hp, a[i], theta0[i], phi[i], y[i], &pb, &tb, h, &l, &tk, &ba,
+                           habs);
         put(bar_abs, i, ba);
+        for (int k = 0; k < 4; ++k) acc[5 + k] += habs[k];
         put(phi_bar, i, pb);
         put(theta0_bar, i, tb);
         put(thetaK, i, tk);
@@ -464,11 +478,13 @@ void oracle_sweep_quadratic(int kind, int64_t n, int64_t K, const double* hp, in
       }
     }
   }
-  long double s[5] = {0, 0, 0, 0, 0};
+  long double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int64_t c = 0; c < nchunks; ++c)
-    for (int k = 0; k < 5; ++k) s[k] += hyp_part[(size_t)c * 5 + k];
-  for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < 9; ++k) s[k] += hyp_part[(size_t)c * 9 + k];
+  for (int k = 0; k < 4; ++k) {
     if (hyper_bar) hyper_bar[k] = (double)s[k];
+    if (hyper_abs) hyper_abs[k] = (double)s[5 + k];
+  }
   if (loss) *loss = (double)s[4];
 }
 

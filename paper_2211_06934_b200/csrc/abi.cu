@@ -184,12 +184,22 @@ int zero_outputs(const opt_tree* t, int nh, double* d_hp, double* d_hp_leaf, cud
 #endif
 
 // TMA-bulk pipelined path: one CTA per SM, STAGES-deep smem ring.
+#ifndef DOPT_TMA_NCONS
+#define DOPT_TMA_NCONS 256
+#endif
+#ifndef DOPT_TMA_CTAS
+#define DOPT_TMA_CTAS 1
+#endif
 template <class Op, class ST>
 int launch_tma(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, cudaStream_t s) {
-  constexpr uint32_t sb = TmaLayout<Op, ST>::stage_bytes();
-  constexpr int STAGES = (200 * 1024 / sb) > 8 ? 8 : (int)(200 * 1024 / sb);
-  auto k = step_tma<Op, ST, STAGES>;
-  const size_t smem = tma_smem_bytes<Op, ST, STAGES>();
+  constexpr int NCONS = DOPT_TMA_NCONS, CTAS = DOPT_TMA_CTAS;
+  constexpr uint32_t sb = TmaLayout<Op, ST, NCONS>::stage_bytes();
+  constexpr uint32_t budget = 200 * 1024 / CTAS;
+  constexpr int STAGES = (budget / sb) > 8 ? 8 : (int)(budget / sb);
+  static_assert(STAGES >= 2, "TMA ring needs >= 2 stages");
+  constexpr int kTmaTile = 4 * NCONS;
+  auto k = step_tma<Op, ST, STAGES, NCONS, CTAS>;
+  const size_t smem = tma_smem_bytes<Op, ST, STAGES, NCONS>();
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(OPT_ECUDA, "smem attribute: %s", cudaGetErrorString(e));
   int dev = 0, sms = 0;
@@ -197,8 +207,8 @@ int launch_tma(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, cudaStream_t s) {
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return fail(OPT_ECUDA, "device query failed: %s", cudaGetErrorString(e));
   const int64_t tiles = (a.numel + kTmaTile - 1) / kTmaTile;
-  int grid = (int)(tiles < sms ? tiles : sms);
-  k<<<grid > 0 ? grid : 1, kTmaThreads, smem, s>>>(op, a);
+  int grid = (int)(tiles < (int64_t)sms * CTAS ? tiles : (int64_t)sms * CTAS);
+  k<<<grid > 0 ? grid : 1, NCONS + 32, smem, s>>>(op, a);
   return launched(s);
 }
 

@@ -17,9 +17,8 @@
 
 namespace dopt {
 
-constexpr int kTmaConsumers = 256;            // 8 warps
-constexpr int kTmaThreads = kTmaConsumers + 32;
-constexpr int kTmaTile = 4 * kTmaConsumers;   // 1024 elements per stage
+// Consumer threads per CTA (NCONS) and tile = 4 * NCONS elements are
+// template parameters; the producer is one extra warp.
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -60,11 +59,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-template <class Op, class ST>
+template <class Op, class ST, int NCONS>
 struct TmaLayout {
+  static constexpr int kTile = 4 * NCONS;
   // bytes of one tile of input array i in shared memory
   static __host__ __device__ constexpr uint32_t in_bytes(int i) {
-    return (uint32_t)kTmaTile * (Op::in_state(i) ? (uint32_t)sizeof(ST) : 4u);
+    return (uint32_t)kTile * (Op::in_state(i) ? (uint32_t)sizeof(ST) : 4u);
   }
   static __host__ __device__ constexpr uint32_t stage_bytes() {
     uint32_t b = 0;
@@ -73,9 +73,9 @@ struct TmaLayout {
   }
 };
 
-template <class Op, class ST, int STAGES>
+template <class Op, class ST, int STAGES, int NCONS>
 __host__ __device__ constexpr size_t tma_smem_bytes() {
-  return (size_t)STAGES * TmaLayout<Op, ST>::stage_bytes() + 2 * STAGES * sizeof(uint64_t) + 128;
+  return (size_t)STAGES * TmaLayout<Op, ST, NCONS>::stage_bytes() + 2 * STAGES * sizeof(uint64_t) + 128;
 }
 
 // smem vector of 4 elements (fp32 16 B, bf16 8 B) -> float[4]
@@ -91,10 +91,13 @@ __device__ __forceinline__ void lds4(const bf16* p, float (&o)[4]) {
   o[3] = __uint_as_float(t.y & 0xFFFF0000u);
 }
 
-template <class Op, class ST, int STAGES>
-__global__ void __launch_bounds__(kTmaThreads, 1)
+template <class Op, class ST, int STAGES, int NCONS, int MINB>
+__global__ void __launch_bounds__(NCONS + 32, MINB)
     step_tma(const Op op, const StepArgs<Op::NIN, Op::NOUT> a) {
-  typedef TmaLayout<Op, ST> Lay;
+  typedef TmaLayout<Op, ST, NCONS> Lay;
+  constexpr int kTmaConsumers = NCONS;
+  constexpr int kTmaThreads = NCONS + 32;
+  constexpr int kTmaTile = Lay::kTile;
   constexpr int NH = Op::NH > 0 ? Op::NH : 1;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * Lay::stage_bytes());

@@ -20,6 +20,11 @@ def one(cfg):
         defs.append("DOPT_IEEE_F32")
     if "tma" in extra:
         defs += ["DOPT_TMA_FWD=1", "DOPT_TMA_BWD=1"]
+        # extra like tma512x1 : consumers x CTAs per SM
+        spec = extra.split("tma")[1]
+        if spec:
+            nc, ctas = spec.split("x")
+            defs += [f"DOPT_TMA_NCONS={nc}", f"DOPT_TMA_CTAS={ctas}"]
     out = os.path.join(OUT, f"lib_{tag}.so")
     B.build(force=True, out=out, defines=defs)
     return out
