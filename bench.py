@@ -341,6 +341,7 @@ def main():
     ap.add_argument("--compute", default="default", choices=["default", "f32", "f64"])
     ap.add_argument("--workload", default="c2", choices=["c2", "c1", "c5", "c3", "maml"])
     ap.add_argument("--tasks", type=int, default=32, help="MAML meta-batch (C4)")
+    ap.add_argument("--no-graph", action="store_true", help="MAML without CUDA-graph capture")
     ap.add_argument("--size", type=int, default=1 << 24)
     ap.add_argument("--bf16", action="store_true", help="bf16 optimizer state")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -496,9 +497,15 @@ def run_maml(args, dev, rank, world):
     outer = maml.FusedAdamOuter(phi.numel(), dev, cfg.outer_lr)
     state = {"phi": phi}
     torch.backends.cudnn.benchmark = True
+    torch.backends.cudnn.allow_tf32 = False   # fp32 convolutions (dtype f32)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    shard = None
+    if not args.no_graph:
+        shard = maml.GraphedShard(maml.task_range(world, rank, cfg.tasks), cfg, inner, dev)
 
     def step(i):
-        state["phi"], loss, _ = maml.outer_step(state["phi"], i, cfg, inner, outer, world, rank)
+        state["phi"], loss, _ = maml.outer_step(state["phi"], i, cfg, inner, outer, world, rank,
+                                                shard=shard)
 
     steps = max(1, min(args.steps, 20))
     l0 = L.opt_launch_count()
@@ -510,7 +517,8 @@ def run_maml(args, dev, rank, world):
            "ms_per_step": round(ms / steps, 3), "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded 5-way tasks)",
            "config": {"workload": "C4 MAML 4-conv64, 5-way 5-shot 15-query, 5 inner SGD-mom steps",
-                      "tasks": cfg.tasks, "parallelism": f"task-sharded x{world}, NCCL all-reduce"},
+                      "tasks": cfg.tasks, "parallelism": f"task-sharded x{world}, NCCL all-reduce",
+                      "cuda_graph": shard is not None},
            "gpu_launches": launches}
     if rank == 0:
         print(json.dumps(out), flush=True)

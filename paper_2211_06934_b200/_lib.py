@@ -101,6 +101,26 @@ def _ptr(t):
     return t.data_ptr()
 
 
+_HP_CACHE = {}
+
+
+def _hp(cls, hp):
+    """ctypes struct for a hyper-parameter tuple, cached by value."""
+    if isinstance(hp, cls):
+        return hp
+    key = (cls, tuple(hp))
+    h = _HP_CACHE.get(key)
+    if h is None:
+        if cls is opt_sgd_hp:
+            h = cls(float(hp[0]), float(hp[1]), int(bool(hp[2])))
+        else:
+            h = cls(*[float(x) for x in hp])
+        if len(_HP_CACHE) > 4096:
+            _HP_CACHE.clear()
+        _HP_CACHE[key] = h
+    return h
+
+
 def _stream(stream):
     if stream is None:
         return torch.cuda.current_stream().cuda_stream
@@ -154,7 +174,7 @@ def _ws(ws):
 # ------------------------------------------------------------- entry points
 def opt_adam_fwd(tree, step, hp, state_dtype, compute, g, mu, nu, updates, mu_out, nu_out,
                  params=None, params_out=None, stream=None):
-    h = opt_adam_hp(*hp) if not isinstance(hp, opt_adam_hp) else hp
+    h = _hp(opt_adam_hp, hp)
     _check(lib.opt_adam_fwd(ctypes.byref(tree.c), int(step), ctypes.byref(h), int(state_dtype),
                             int(compute), _ptr(g), _ptr(mu), _ptr(nu), _ptr(updates),
                             _ptr(mu_out), _ptr(nu_out), _ptr(params), _ptr(params_out),
@@ -164,7 +184,7 @@ def opt_adam_fwd(tree, step, hp, state_dtype, compute, g, mu, nu, updates, mu_ou
 def opt_adam_bwd(tree, step, hp, state_dtype, compute, g, mu, nu, d_updates, d_mu_out,
                  d_nu_out, d_g, d_mu, d_nu, d_hp=None, d_hp_leaf=None, workspace=None,
                  stream=None):
-    h = opt_adam_hp(*hp) if not isinstance(hp, opt_adam_hp) else hp
+    h = _hp(opt_adam_hp, hp)
     wp, wb = _ws(workspace)
     _check(lib.opt_adam_bwd(ctypes.byref(tree.c), int(step), ctypes.byref(h), int(state_dtype),
                             int(compute), _ptr(g), _ptr(mu), _ptr(nu), _ptr(d_updates),
@@ -174,7 +194,7 @@ def opt_adam_bwd(tree, step, hp, state_dtype, compute, g, mu, nu, d_updates, d_m
 
 def opt_rmsprop_fwd(tree, hp, state_dtype, compute, g, nu, updates, nu_out, params=None,
                     params_out=None, stream=None):
-    h = opt_rmsprop_hp(*hp) if not isinstance(hp, opt_rmsprop_hp) else hp
+    h = _hp(opt_rmsprop_hp, hp)
     _check(lib.opt_rmsprop_fwd(ctypes.byref(tree.c), ctypes.byref(h), int(state_dtype),
                                int(compute), _ptr(g), _ptr(nu), _ptr(updates), _ptr(nu_out),
                                _ptr(params), _ptr(params_out), _stream(stream)))
@@ -182,7 +202,7 @@ def opt_rmsprop_fwd(tree, hp, state_dtype, compute, g, nu, updates, nu_out, para
 
 def opt_rmsprop_bwd(tree, hp, state_dtype, compute, g, nu, d_updates, d_nu_out, d_g, d_nu,
                     d_hp=None, d_hp_leaf=None, workspace=None, stream=None):
-    h = opt_rmsprop_hp(*hp) if not isinstance(hp, opt_rmsprop_hp) else hp
+    h = _hp(opt_rmsprop_hp, hp)
     wp, wb = _ws(workspace)
     _check(lib.opt_rmsprop_bwd(ctypes.byref(tree.c), ctypes.byref(h), int(state_dtype),
                                int(compute), _ptr(g), _ptr(nu), _ptr(d_updates), _ptr(d_nu_out),
@@ -192,7 +212,7 @@ def opt_rmsprop_bwd(tree, hp, state_dtype, compute, g, nu, d_updates, d_nu_out, 
 
 def opt_sgd_fwd(tree, hp, state_dtype, compute, g, mom, updates, mom_out, params=None,
                 params_out=None, stream=None):
-    h = opt_sgd_hp(hp[0], hp[1], int(bool(hp[2]))) if not isinstance(hp, opt_sgd_hp) else hp
+    h = _hp(opt_sgd_hp, hp)
     _check(lib.opt_sgd_fwd(ctypes.byref(tree.c), ctypes.byref(h), int(state_dtype), int(compute),
                            _ptr(g), _ptr(mom), _ptr(updates), _ptr(mom_out), _ptr(params),
                            _ptr(params_out), _stream(stream)))
@@ -200,7 +220,7 @@ def opt_sgd_fwd(tree, hp, state_dtype, compute, g, mom, updates, mom_out, params
 
 def opt_sgd_bwd(tree, hp, state_dtype, compute, g, mom, d_updates, d_mom_out, d_g, d_mom,
                 d_hp=None, d_hp_leaf=None, workspace=None, stream=None):
-    h = opt_sgd_hp(hp[0], hp[1], int(bool(hp[2]))) if not isinstance(hp, opt_sgd_hp) else hp
+    h = _hp(opt_sgd_hp, hp)
     wp, wb = _ws(workspace)
     _check(lib.opt_sgd_bwd(ctypes.byref(tree.c), ctypes.byref(h), int(state_dtype), int(compute),
                            _ptr(g), _ptr(mom), _ptr(d_updates), _ptr(d_mom_out), _ptr(d_g),

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "diffopt.h"
 #include "step_kernel.cuh"
@@ -92,15 +93,53 @@ int check_state_dtype(int sd) {
   return OPT_OK;
 }
 
+// Per-device SM count and per-(kernel, smem) occupancy, queried once: the
+// host path of a call is on the critical path of launch-bound workloads
+// (small trees, MAML inner loops).
+std::mutex g_cache_mu;
+std::unordered_map<uint64_t, int> g_occ_cache;
+std::atomic<int> g_sms[64];
+
+int sm_count(int* sms) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(OPT_ECUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+  if (dev < 64) {
+    int c = g_sms[dev].load(std::memory_order_relaxed);
+    if (c > 0) {
+      *sms = c;
+      return OPT_OK;
+    }
+  }
+  int c = 0;
+  e = cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return fail(OPT_ECUDA, "device query failed: %s", cudaGetErrorString(e));
+  if (dev < 64) g_sms[dev].store(c, std::memory_order_relaxed);
+  *sms = c;
+  return OPT_OK;
+}
+
 // Persistent grid: SMs x resident blocks of this kernel, capped by work.
 template <class K>
 int grid_for(K kernel, int64_t work_blocks, size_t smem, int* grid) {
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, smem);
-  if (e != cudaSuccess) return fail(OPT_ECUDA, "device query failed: %s", cudaGetErrorString(e));
-  int64_t g = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  int sms = 0, per_sm = 0;
+  int rc = sm_count(&sms);
+  if (rc) return rc;
+  const uint64_t key = reinterpret_cast<uint64_t>(reinterpret_cast<const void*>(kernel)) ^
+                       ((uint64_t)smem << 48);
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_occ_cache.find(key);
+    if (it != g_occ_cache.end()) per_sm = it->second;
+  }
+  if (per_sm == 0) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, smem);
+    if (e != cudaSuccess) return fail(OPT_ECUDA, "occupancy query: %s", cudaGetErrorString(e));
+    if (per_sm < 1) per_sm = 1;
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_occ_cache[key] = per_sm;
+  }
+  int64_t g = (int64_t)sms * per_sm;
   if (g > kMaxGrid) g = kMaxGrid;
   if (work_blocks < g) g = work_blocks;
   *grid = (int)(g > 0 ? g : 1);
@@ -200,12 +239,12 @@ int launch_tma(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, cudaStream_t s) {
   constexpr int kTmaTile = 4 * NCONS;
   auto k = step_tma<Op, ST, STAGES, NCONS, CTAS>;
   const size_t smem = tma_smem_bytes<Op, ST, STAGES, NCONS>();
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return fail(OPT_ECUDA, "smem attribute: %s", cudaGetErrorString(e));
-  int dev = 0, sms = 0;
-  e = cudaGetDevice(&dev);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e != cudaSuccess) return fail(OPT_ECUDA, "device query failed: %s", cudaGetErrorString(e));
+  static const cudaError_t attr =  // once per instantiation (thread-safe static init)
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (attr != cudaSuccess) return fail(OPT_ECUDA, "smem attribute: %s", cudaGetErrorString(attr));
+  int sms = 0;
+  int rc = sm_count(&sms);
+  if (rc) return rc;
   const int64_t tiles = (a.numel + kTmaTile - 1) / kTmaTile;
   int grid = (int)(tiles < (int64_t)sms * CTAS ? tiles : (int64_t)sms * CTAS);
   k<<<grid > 0 ? grid : 1, NCONS + 32, smem, s>>>(op, a);
@@ -239,10 +278,9 @@ int launch_bwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r,
     a.n_tiles = r.n_tiles;
     auto k = step_leaf<Op, ST, U, DOPT_MINB_BWD>;
     size_t smem = sizeof(int64_t) * 2 * (size_t)(t->n_leaves + 1);
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return fail(OPT_ECUDA, "smem attribute: %s", cudaGetErrorString(e));
-    }
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(int64_t) * 2 * (kMaxLeafSmem + 1)));
+    if (attr != cudaSuccess) return fail(OPT_ECUDA, "smem attribute: %s", cudaGetErrorString(attr));
     int grid = 0;
     int rc = grid_for(k, r.n_tiles, smem, &grid);
     if (rc) return rc;

@@ -61,19 +61,23 @@ def init_params(seed, device):
     return torch.cat([p.reshape(-1) for p in out]).to(device)
 
 
+def task_seed(outer_step, task_id, seed=0):
+    return ((seed * 1_000_003 + outer_step) * 1_000_033 + task_id) & 0x7FFFFFFFFFFFFFFF
+
+
 def task_data(outer_step, task_id, device, seed=0):
-    """Seeded synthetic 5-way task; depends only on (seed, step, task)."""
-    gen = torch.Generator().manual_seed(((seed * 1_000_003 + outer_step) * 1_000_033 + task_id)
-                                        & 0x7FFFFFFFFFFFFFFF)
-    xs = torch.randn(WAYS * SHOTS, 1, HW, HW, generator=gen)
-    xq = torch.randn(WAYS * QUERIES, 1, HW, HW, generator=gen)
+    """Seeded synthetic 5-way task, generated on `device` by a generator
+    keyed on (seed, step, task) only -- never on the rank layout. (CPU and
+    CUDA generators draw different streams; each is reproducible.)"""
+    device = torch.device(device)
+    gen = torch.Generator(device=device).manual_seed(task_seed(outer_step, task_id, seed))
+    xs = torch.randn(WAYS * SHOTS, 1, HW, HW, generator=gen, device=device)
+    xq = torch.randn(WAYS * QUERIES, 1, HW, HW, generator=gen, device=device)
     # class-dependent mean shift so the task is learnable
-    proto = torch.randn(WAYS, 1, HW, HW, generator=gen)
-    ys = torch.arange(WAYS).repeat_interleave(SHOTS)
-    yq = torch.arange(WAYS).repeat_interleave(QUERIES)
-    xs = xs + proto[ys]
-    xq = xq + proto[yq]
-    return xs.to(device), ys.to(device), xq.to(device), yq.to(device)
+    proto = torch.randn(WAYS, 1, HW, HW, generator=gen, device=device)
+    ys = torch.arange(WAYS, device=device).repeat_interleave(SHOTS)
+    yq = torch.arange(WAYS, device=device).repeat_interleave(QUERIES)
+    return xs + proto[ys], ys, xq + proto[yq], yq
 
 
 @dataclass
@@ -136,12 +140,17 @@ def sizes_of(shapes):
 def meta_grad_tasks(phi, task_ids, outer_step, cfg: MamlConfig, inner):
     """Sum over task_ids (in order) of d L_query(theta_K(phi)) / d phi, and
     the summed query loss. phi: flat leaf tensor (no grad needed on entry)."""
+    data = [task_data(outer_step, tid, phi.device, cfg.seed) for tid in task_ids]
+    return meta_grad_data(phi, data, cfg, inner)
+
+
+def meta_grad_data(phi, data, cfg: MamlConfig, inner):
+    """meta_grad_tasks on pre-generated task data [(xs, ys, xq, yq), ...]."""
     sizes = sizes_of(CONV4_SHAPES)
     phi_v = phi.detach().requires_grad_(True)
     total = torch.zeros_like(phi)
     loss_sum = torch.zeros((), device=phi.device)
-    for tid in task_ids:
-        xs, ys, xq, yq = task_data(outer_step, tid, phi.device, cfg.seed)
+    for xs, ys, xq, yq in data:
         theta, b = phi_v, None
         for _ in range(cfg.inner_steps):
             params = [p.view(s) for p, s in zip(torch.split(theta, sizes), CONV4_SHAPES)]
@@ -156,12 +165,47 @@ def meta_grad_tasks(phi, task_ids, outer_step, cfg: MamlConfig, inner):
     return total, loss_sum
 
 
-def outer_step(phi, outer_step_idx, cfg: MamlConfig, inner, outer, world=1, rank=0, group=None):
-    """One synchronous meta-update over the cfg.tasks-task meta-batch."""
+class GraphedShard:
+    """One rank's share of the meta-batch captured as a single CUDA graph
+    (all inner loops, query losses, second-order backward and the local
+    meta-gradient sum): per outer step only the task data and phi are
+    copied into static buffers and the graph is replayed, removing the
+    per-kernel launch cost that dominates these tiny convolutions.
+    Call it like meta_grad_tasks."""
+
+    def __init__(self, task_ids, cfg: MamlConfig, inner, device, warmup=2):
+        self.ids, self.cfg, self.inner = list(task_ids), cfg, inner
+        self.phi = torch.zeros(sum(sizes_of(CONV4_SHAPES)), device=device)
+        self.data = [task_data(0, t, device, cfg.seed) for t in self.ids]
+        side = torch.cuda.Stream(device)
+        side.wait_stream(torch.cuda.current_stream(device))
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                meta_grad_data(self.phi, self.data, cfg, inner)
+        torch.cuda.current_stream(device).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.mg, self.loss = meta_grad_data(self.phi, self.data, cfg, inner)
+
+    def __call__(self, phi, task_ids, outer_step, cfg, inner):
+        assert list(task_ids) == self.ids
+        self.phi.copy_(phi)
+        for tid, bufs in zip(self.ids, self.data):
+            for dst, src in zip(bufs, task_data(outer_step, tid, phi.device, cfg.seed)):
+                dst.copy_(src)
+        self.graph.replay()
+        return self.mg, self.loss
+
+
+def outer_step(phi, outer_step_idx, cfg: MamlConfig, inner, outer, world=1, rank=0, group=None,
+               shard=None):
+    """One synchronous meta-update over the cfg.tasks-task meta-batch.
+    ``shard`` (optional) replaces meta_grad_tasks, e.g. a GraphedShard."""
     import torch.distributed as dist
 
     ids = task_range(world, rank, cfg.tasks)
-    mg, loss = meta_grad_tasks(phi, ids, outer_step_idx, cfg, inner)
+    run = shard if shard is not None else meta_grad_tasks
+    mg, loss = run(phi, ids, outer_step_idx, cfg, inner)
     buf = torch.cat([mg, loss.reshape(1)])
     if world > 1:
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)  # the one exchange step
