@@ -146,6 +146,33 @@ int grid_for(K kernel, int64_t work_blocks, size_t smem, int* grid) {
   return OPT_OK;
 }
 
+#ifndef DOPT_PDL
+#define DOPT_PDL 0
+#endif
+// Launch with programmatic dependent launch (PDL): the grid may be scheduled
+// while the previous kernel on the stream drains; every step kernel starts
+// with griddepcontrol.wait, so it still observes all prior work.
+template <class Op, class K>
+cudaError_t launch_k(K kernel, int grid, int block, size_t smem, cudaStream_t s, const Op& op,
+                     const StepArgs<Op::NIN, Op::NOUT>& a) {
+#if DOPT_PDL
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, op, a);
+#else
+  kernel<<<grid, block, smem, s>>>(op, a);
+  return cudaSuccess;
+#endif
+}
+
 int launched(cudaStream_t) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(OPT_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
@@ -247,7 +274,8 @@ int launch_tma(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, cudaStream_t s) {
   if (rc) return rc;
   const int64_t tiles = (a.numel + kTmaTile - 1) / kTmaTile;
   int grid = (int)(tiles < (int64_t)sms * CTAS ? tiles : (int64_t)sms * CTAS);
-  k<<<grid > 0 ? grid : 1, NCONS + 32, smem, s>>>(op, a);
+  cudaError_t le = launch_k(k, grid > 0 ? grid : 1, NCONS + 32, smem, s, op, a);
+  if (le != cudaSuccess) return fail(OPT_ECUDA, "launch: %s", cudaGetErrorString(le));
   return launched(s);
 }
 
@@ -260,7 +288,8 @@ int launch_fwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, cudaStream_t s) {
   int64_t work = ((a.numel >> 2) + kBlock - 1) / kBlock + 1;
   int rc = grid_for(k, work, 0, &grid);
   if (rc) return rc;
-  k<<<grid, kBlock, 0, s>>>(op, a);
+  cudaError_t le = launch_k(k, grid, kBlock, 0, s, op, a);
+  if (le != cudaSuccess) return fail(OPT_ECUDA, "launch: %s", cudaGetErrorString(le));
   return launched(s);
 }
 
@@ -284,7 +313,8 @@ int launch_bwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r,
     int grid = 0;
     int rc = grid_for(k, r.n_tiles, smem, &grid);
     if (rc) return rc;
-    k<<<grid, kBlock, smem, s>>>(op, a);
+    cudaError_t le = launch_k(k, grid, kBlock, smem, s, op, a);
+    if (le != cudaSuccess) return fail(OPT_ECUDA, "launch: %s", cudaGetErrorString(le));
     return launched(s);
   }
   if (DOPT_TMA_BWD) return launch_tma<Op, ST>(op, a, s);
@@ -293,7 +323,8 @@ int launch_bwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r,
   int64_t work = ((a.numel >> 2) + kBlock - 1) / kBlock + 1;
   int rc = grid_for(k, work, 0, &grid);
   if (rc) return rc;
-  k<<<grid, kBlock, 0, s>>>(op, a);
+  cudaError_t le = launch_k(k, grid, kBlock, 0, s, op, a);
+  if (le != cudaSuccess) return fail(OPT_ECUDA, "launch: %s", cudaGetErrorString(le));
   return launched(s);
 }
 

@@ -193,6 +193,14 @@ __device__ __forceinline__ bool last_block(unsigned int* counter, unsigned int n
   return s_last;
 }
 
+// PDL hooks (no-ops unless the launch used programmatic serialization).
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------------------------------- uniform kernel
 template <class Op, class ST, int U, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) step_uniform(const Op op,
@@ -206,7 +214,9 @@ __global__ void __launch_bounds__(kBlock, MINB) step_uniform(const Op op,
   const int64_t nvec = a.numel >> 2;
   const int64_t nthreads = (int64_t)gridDim.x * kBlock;
   const int64_t tid = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+  pdl_wait();
   process_vectors<Op, ST, U>(op, a, 0, nvec, tid, nthreads, acc, want_hp);
+  pdl_trigger();
   // ragged tail (numel % 4 elements) -> the last block
   const int64_t tail0 = nvec << 2;
   if (blockIdx.x == gridDim.x - 1 && tail0 + threadIdx.x < a.numel)
@@ -254,6 +264,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_leaf(const Op op,
   __shared__ int64_t s_scan[kBlock];
 
   const int64_t nl = a.n_leaves;
+  pdl_wait();
   // stage offsets; per-thread contiguous chunk for the scan
   for (int64_t l = threadIdx.x; l <= nl; l += kBlock) s_off[l] = a.offsets[l];
   __syncthreads();

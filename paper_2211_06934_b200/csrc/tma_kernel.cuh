@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(NCONS + 32, MINB)
   const int64_t n_tiles = (numel + kTmaTile - 1) / kTmaTile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+  pdl_wait();
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);

@@ -16,6 +16,8 @@ def one(cfg):
     uf, mf, ub, mb, extra = cfg
     tag = f"{uf}-{mf}-{ub}-{mb}" + (f"-{extra}" if extra else "")
     defs = [f"DOPT_U_FWD={uf}", f"DOPT_MINB_FWD={mf}", f"DOPT_U_BWD={ub}", f"DOPT_MINB_BWD={mb}"]
+    if "pdl" in extra:
+        defs.append("DOPT_PDL=1")
     if "ieee" in extra:
         defs.append("DOPT_IEEE_F32")
     if "tma" in extra:
