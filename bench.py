@@ -252,7 +252,7 @@ def time_e2e(args, W, dev):
 
     t = torch
     s0 = W.sets[0]
-    ins = ["g", "m", "v", "du", "dm1", "dv1"]
+    ins = [k for k in ("g", "m", "v", "du", "dm1", "dv1") if s0[k] is not None]
     outs = ["u", "m1", "v1", "dg", "dm", "dv", "dhp"]
     h_in = {k: s0[k].cpu().pin_memory() for k in ins}
     h_out = {k: t.empty_like(s0[k], device="cpu").pin_memory() for k in outs}
@@ -281,7 +281,7 @@ def time_e2e(args, W, dev):
 
     ms_serial = timed(serial)
     out = {"serial_ms_per_step": round(ms_serial, 4)}
-    if W.sd == 0 and W.n >= 1 << 16:
+    if W.sd == 0 and W.n >= 1 << 16 and len(ins) == 6:
         hs = HostStreamedAdam(W.n, dev, chunks=16, compute=W.compute)
         hin = {k: h_in[k] for k in IN_KEYS}
         hout = {k: h_out[k] for k in OUT_KEYS}
@@ -519,6 +519,8 @@ def run_maml(args, dev, rank, world):
     l0 = L.opt_launch_count()
     ms = _timed(step, steps, args.warmup, world)
     launches = (L.opt_launch_count() - l0) * steps // (steps + args.warmup)
+    if shard is not None:  # library launches replayed inside the CUDA graph
+        launches += shard.launches_per_replay * steps
     value = cfg.tasks * steps / (ms * 1e-3)
     out = {"metric": "MAML meta-batch tasks/s", "value": round(value, 2), "unit": "tasks/s",
            "n_gpus": world, "steps": steps, "warmup": args.warmup,

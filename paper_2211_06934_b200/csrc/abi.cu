@@ -147,7 +147,7 @@ int grid_for(K kernel, int64_t work_blocks, size_t smem, int* grid) {
 }
 
 #ifndef DOPT_PDL
-#define DOPT_PDL 0
+#define DOPT_PDL 1
 #endif
 // Launch with programmatic dependent launch (PDL): the grid may be scheduled
 // while the previous kernel on the stream drains; every step kernel starts
@@ -477,9 +477,11 @@ int opt_adam_bwd(const opt_tree* tree, int64_t step, const opt_adam_hp* hp, int 
     typedef typename std::remove_reference<decltype(op)>::type::CT CT;
     op.b1 = (CT)b1; op.om1 = (CT)(1.0 - b1); op.b2 = (CT)b2; op.two_om2 = (CT)(2.0 * (1.0 - b2));
     op.A = (CT)((1.0 - b1) / bc1); op.C = (CT)((1.0 - b2) / bc2);
-    op.ibc1 = (CT)(1.0 / bc1); op.ibc2 = (CT)(1.0 / bc2);
     op.b1ibc1 = (CT)(b1 / bc1); op.b2ibc2 = (CT)(b2 / bc2);
     op.eps_root = (CT)hp->eps_root; op.lr = (CT)hp->lr; op.eps = (CT)hp->eps;
+    op.Aeps = (CT)((1.0 - b1) / bc1 * hp->eps);
+    op.kM = (CT)(b1 * hp->lr / bc1); op.kV = (CT)(0.5 * b2 * hp->lr / bc2);
+    op.hlr = (CT)(0.5 * hp->lr);
     op.K1 = (CT)K1; op.K2 = (CT)K2; op.K3 = (CT)K3; op.K4 = (CT)K4;
   });
 }
@@ -533,6 +535,7 @@ int opt_rmsprop_bwd(const opt_tree* tree, const opt_rmsprop_hp* hp, int state_dt
     typedef typename std::remove_reference<decltype(op)>::type::CT CT;
     op.alpha = (CT)hp->alpha; op.oma = (CT)(1.0 - hp->alpha);
     op.two_oma = (CT)(2.0 * (1.0 - hp->alpha)); op.lr = (CT)hp->lr; op.eps = (CT)hp->eps;
+    op.hlr = (CT)(0.5 * hp->lr);
   });
 }
 

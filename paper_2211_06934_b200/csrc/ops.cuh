@@ -29,14 +29,17 @@ namespace dopt {
 __device__ __forceinline__ double safe_rcp(double x) { return x == 0.0 ? 0.0 : 1.0 / x; }
 __device__ __forceinline__ double ct_sqrt(double x) { return sqrt(x); }
 __device__ __forceinline__ double ct_div(double a, double b) { return a / b; }
+__device__ __forceinline__ double rsqrt_or_zero(double x) { return x > 0.0 ? 1.0 / sqrt(x) : 0.0; }
 #ifdef DOPT_IEEE_F32
 __device__ __forceinline__ float safe_rcp(float x) { return x == 0.f ? 0.f : 1.f / x; }
 __device__ __forceinline__ float ct_sqrt(float x) { return sqrtf(x); }
 __device__ __forceinline__ float ct_div(float a, float b) { return a / b; }
+__device__ __forceinline__ float rsqrt_or_zero(float x) { return x > 0.f ? 1.f / sqrtf(x) : 0.f; }
 #else
 __device__ __forceinline__ float safe_rcp(float x) { return x == 0.f ? 0.f : __fdividef(1.f, x); }
 __device__ __forceinline__ float ct_sqrt(float x) { return x > 0.f ? x * rsqrtf(x) : 0.f; }
 __device__ __forceinline__ float ct_div(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ float rsqrt_or_zero(float x) { return x > 0.f ? rsqrtf(x) : 0.f; }
 #endif
 
 // ------------------------------------------------------------------ Adam
@@ -69,31 +72,34 @@ struct AdamBwd {
   static constexpr int NIN = 6, NOUT = 3, NH = 4;  // in: g m v du dm1 dv1 ; out: dg dm dv
   __host__ __device__ static constexpr bool in_state(int i) { return i == 1 || i == 2; }
   __host__ __device__ static constexpr bool out_state(int) { return false; }
-  CT b1, om1, b2, two_om2, A, C, ibc1, ibc2, b1ibc1, b2ibc2, eps_root, lr, eps;
+  // host-precomputed (abi.cu): A=(1-b1)/bc1, C=(1-b2)/bc2, b1ibc1=b1/bc1,
+  // b2ibc2=b2/bc2, Aeps=A*eps, kM=b1*lr/bc1, kV=b2*lr/(2*bc2), hlr=lr/2
+  CT b1, om1, b2, two_om2, A, C, b1ibc1, b2ibc2, eps_root, lr, eps, Aeps, kM, kV, hlr;
   CT K1, K2, K3, K4;
 
   __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT* h,
                                              bool want_hp) const {
     const CT g = x[0], m = x[1], v = x[2], du = x[3], dm1 = x[4], dv1 = x[5];
-    const CT P = b1ibc1 * m;
-    const CT Q = b2ibc2 * v + eps_root;
+    const CT P = b1ibc1 * m;                 // mhat = A g + P
+    const CT Q = b2ibc2 * v + eps_root;      // s^2  = C g^2 + Q
     const CT gg = g * g;
     const CT mhat = A * g + P;
-    const CT s = ct_sqrt(C * gg + Q);
-    const CT d = s + eps;
-    const CT rd = safe_rcp(d);
-    const CT rs = safe_rcp(s);
-    const CT rd2 = rd * rd;
-    const CT lr_rd = lr * rd;
-    const CT w = CT(0.5) * lr * mhat * rd2 * rs;  // du/dvhat = lr mhat / (2 s d^2)
-    y[0] = om1 * dm1 + two_om2 * g * dv1 - du * lr * rd2 * (A * eps + (A * Q - P * C * g) * rs);
-    y[1] = b1 * (dm1 - du * lr_rd * ibc1);
-    y[2] = b2 * (dv1 + du * w * ibc2);
+    const CT s2 = C * gg + Q;
+    const CT rs = rsqrt_or_zero(s2);         // 1/s  (Z6: 0 at s = 0)
+    const CT d = s2 * rs + eps;              // d = s + eps
+    const CT rd = safe_rcp(d);               // 1/d  (Z7: 0 at d = 0)
+    const CT R = du * rd;                    // du/d
+    const CT T = R * rd;                     // du/d^2
+    const CT U = mhat * T * rs;              // du mhat/(s d^2)
+    // dg = (1-b1) dm1 + 2(1-b2) g dv1 - lr du [A eps + (A Q - P C g)/s]/d^2
+    y[0] = om1 * dm1 + two_om2 * g * dv1 - (lr * T) * (Aeps + (A * Q - P * C * g) * rs);
+    y[1] = b1 * dm1 - kM * R;                // b1 (dm1 - du lr/(bc1 d))
+    y[2] = b2 * dv1 + kV * U;                // b2 (dv1 + du lr mhat/(2 s bc2 d^2))
     if (want_hp) {
-      h[0] += (-du * mhat * rd);
-      h[1] += (dm1 * (m - g) - du * lr_rd * (m * K1 - g * K2));
-      h[2] += (dv1 * (v - gg) + du * w * (v * K3 - gg * K4));
-      h[3] += (du * lr * mhat * rd2);
+      h[0] -= mhat * R;                                       // lr
+      h[1] += dm1 * (m - g) - (lr * R) * (m * K1 - g * K2);   // b1
+      h[2] += dv1 * (v - gg) + (hlr * U) * (v * K3 - gg * K4);  // b2
+      h[3] += lr * (mhat * T);                                // eps
     }
   }
 };
@@ -126,25 +132,25 @@ struct RmsBwd {
   static constexpr int NIN = 4, NOUT = 2, NH = 3;  // in: g v du dv1 ; out: dg dv
   __host__ __device__ static constexpr bool in_state(int i) { return i == 1; }
   __host__ __device__ static constexpr bool out_state(int) { return false; }
-  CT alpha, oma, two_oma, lr, eps;
+  CT alpha, oma, two_oma, lr, eps, hlr;  // hlr = lr/2
 
   __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT* h,
                                              bool want_hp) const {
     const CT g = x[0], v = x[1], du = x[2], dv1 = x[3];
     const CT gg = g * g;
-    const CT s = ct_sqrt(alpha * v + oma * gg);
-    const CT d = s + eps;
+    const CT s2 = alpha * v + oma * gg;
+    const CT rs = rsqrt_or_zero(s2);
+    const CT d = s2 * rs + eps;
     const CT rd = safe_rcp(d);
-    const CT rs = safe_rcp(s);
-    const CT rd2 = rd * rd;
-    const CT w = CT(0.5) * lr * g * rd2 * rs;  // du/dv' = lr g / (2 s d^2)
-    const CT V = dv1 + du * w;
-    y[0] = two_oma * g * dv1 - du * lr * rd2 * (eps + alpha * v * rs);
+    const CT R = du * rd;                   // du/d
+    const CT T = R * rd;                    // du/d^2
+    const CT V = dv1 + hlr * (g * T) * rs;  // dv1 + du lr g/(2 s d^2)
+    y[0] = two_oma * g * dv1 - (lr * T) * (eps + alpha * v * rs);
     y[1] = alpha * V;
     if (want_hp) {
-      h[0] += (-du * g * rd);
-      h[1] += (V * (v - gg));
-      h[2] += (du * lr * g * rd2);
+      h[0] -= g * R;
+      h[1] += V * (v - gg);
+      h[2] += lr * (g * T);
     }
   }
 };

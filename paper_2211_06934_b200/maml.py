@@ -183,9 +183,13 @@ class GraphedShard:
             for _ in range(warmup):
                 meta_grad_data(self.phi, self.data, cfg, inner)
         torch.cuda.current_stream(device).wait_stream(side)
+        from . import _lib as L
+
         self.graph = torch.cuda.CUDAGraph()
+        n0 = L.opt_launch_count()
         with torch.cuda.graph(self.graph):
             self.mg, self.loss = meta_grad_data(self.phi, self.data, cfg, inner)
+        self.launches_per_replay = L.opt_launch_count() - n0  # captured library kernels
 
     def __call__(self, phi, task_ids, outer_step, cfg, inner):
         assert list(task_ids) == self.ids
