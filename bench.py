@@ -213,22 +213,22 @@ def time_ours(args, workload_inputs, dev, rank, world):
         dist.barrier()
     launches = L.opt_launch_count() - launches0
     ms = ev[0].elapsed_time(ev[1])
-    # per-kernel durations for the roofline: the same K steps again with an
-    # event around every launch (kept out of the step timing above, where
-    # events between launches would perturb back-to-back scheduling)
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    for k in range(args.steps):
-        s = W.sets[k % sets]
-        kev[k][0].record(stream)
-        W.fwd(s)
-        kev[k][1].record(stream)
-        W.bwd(s)
-        kev[k][2].record(stream)
-    torch.cuda.synchronize()
+    # per-kernel average launch durations for the roofline: K back-to-back
+    # launches of each kernel alone (same rotating buffer sets), bracketed by
+    # CUDA events on the launching stream; an event between every launch
+    # would itself perturb the back-to-back scheduling being measured.
+    def loop_ms(fn):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for k in range(args.steps):
+            fn(W.sets[k % sets])
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / args.steps
+
+    fwd_ms = [loop_ms(W.fwd)]
+    bwd_ms = [loop_ms(W.bwd)]
     clocks = sampler.stop()
-    fwd_ms = [a.elapsed_time(b) for a, b, _ in kev]
-    bwd_ms = [b.elapsed_time(c) for _, b, c in kev]
     if world > 1:
         tt = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -416,7 +416,10 @@ def main():
                      "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic_from_profiles(r["wname"], compute_name),
-                     "alg_bytes_per_launch": W.bytes_bwd},
+                     "alg_bytes_per_launch": W.bytes_bwd,
+                     "share_of_step": round(bwd_avg / (fwd_avg + bwd_avg), 3),
+                     "how": "avg duration of K back-to-back opt_adam_bwd launches (CUDA "
+                            "events on the launching stream around the loop)"},
         "libdiffopt_abi": L.opt_abi_version(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
