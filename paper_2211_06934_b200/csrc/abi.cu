@@ -279,6 +279,13 @@ int launch_tma(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, cudaStream_t s) {
   return launched(s);
 }
 
+// fp64 arithmetic needs more registers: cap at 2 blocks/SM (128 regs) there
+// instead of spilling under the fp32 cap.
+template <class Op>
+constexpr int minb_bwd() {
+  return sizeof(typename Op::CT) == 8 ? (DOPT_MINB_BWD < 2 ? DOPT_MINB_BWD : 2) : DOPT_MINB_BWD;
+}
+
 // Launch an op (forward: no reduction) with state type ST.
 template <class Op, class ST, int U>
 int launch_fwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, cudaStream_t s) {
@@ -305,7 +312,7 @@ int launch_bwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r,
     a.offsets = t->d_offsets;
     a.n_leaves = t->n_leaves;
     a.n_tiles = r.n_tiles;
-    auto k = step_leaf<Op, ST, U, DOPT_MINB_BWD>;
+    auto k = step_leaf<Op, ST, U, minb_bwd<Op>()>;
     size_t smem = sizeof(int64_t) * 2 * (size_t)(t->n_leaves + 1);
     static const cudaError_t attr = cudaFuncSetAttribute(
         k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(int64_t) * 2 * (kMaxLeafSmem + 1)));
@@ -318,7 +325,7 @@ int launch_bwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r,
     return launched(s);
   }
   if (DOPT_TMA_BWD) return launch_tma<Op, ST>(op, a, s);
-  auto k = step_uniform<Op, ST, U, DOPT_MINB_BWD>;
+  auto k = step_uniform<Op, ST, U, minb_bwd<Op>()>;
   int grid = 0;
   int64_t work = ((a.numel >> 2) + kBlock - 1) / kBlock + 1;
   int rc = grid_for(k, work, 0, &grid);

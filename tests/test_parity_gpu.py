@@ -293,3 +293,159 @@ def test_c2_resnet18_full_size_sampled(L, ct):
     oracle.set_num_threads(1)
     fmag = oracle.adam_mag(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], t, *hp)
     assert_sum_close("dhp", host(dhp), full["dhp"], np.maximum(full["dhp_abs"], fmag["dhp"]))
+
+
+# ----------------------------------------------- more structural cases
+def test_many_leaves_per_leaf_sums(L):
+    """4096 leaves of ragged sizes (the shared-memory leaf table at its
+    limit): per-leaf hyper-gradient sums equal the oracle's; 4097 leaves
+    are rejected with OPT_EINVAL before any launch."""
+    rng = np.random.default_rng(5)
+    leaves = rng.integers(0, 600, 4096).tolist()
+    leaves[7] = 0  # an empty leaf
+    x = synth.state_tree(0xB5, leaves)
+    off = synth.offsets_of(leaves)
+    tree = L.Tree(offsets=off, device=DEV)
+    hp = (1e-2, 0.9, 0.999, 1e-8, 0.0)
+    g, m, v, du, dm1, dv1 = (dev_f32(x[k]) for k in ("g", "m", "v", "du", "dm1", "dv1"))
+    dg = torch.empty_like(g)
+    dhp = torch.empty(4, dtype=torch.float64, device=DEV)
+    dhl = torch.empty(4096 * 4, dtype=torch.float64, device=DEV)
+    L.opt_adam_bwd(tree, 4, hp, 0, 0, g, m, v, du, dm1, dv1, dg, None, None, dhp, dhl,
+                   tree.workspace(DEV, per_leaf=True))
+    r = oracle.adam_vjp(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], 4, *hp, prec=1,
+                        offsets=off)
+    mag = oracle.adam_mag(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], 4, *hp)
+    check("dg", host(dg), r["dg"], mag["dg"], 1)
+    got = host(dhl).reshape(-1, 4)
+    hs = np.maximum(r["dhp_abs"], mag["dhp"])
+    np.testing.assert_allclose(got, r["dhp_leaf"], rtol=1e-5, atol=1e-6 + 1e-5 * hs.max())
+    assert np.all(got[7] == 0)
+    big = L.Tree(offsets=synth.offsets_of([1] * 4097), device=DEV)
+    z = torch.zeros(4097, device=DEV)
+    with pytest.raises(L.DiffoptError) as e:
+        L.opt_adam_bwd(big, 1, hp, 0, 0, z, None, None, z, None, None, z, None, None,
+                       torch.empty(4, dtype=torch.float64, device=DEV),
+                       torch.empty(4097 * 4, dtype=torch.float64, device=DEV),
+                       big.workspace(DEV, per_leaf=True))
+    assert e.value.code == L.OPT_EINVAL
+
+
+def test_misaligned_device_pointer_rejected(L):
+    tree = L.Tree(numel=64, device=DEV)
+    buf = torch.zeros(80, device=DEV)
+    with pytest.raises(L.DiffoptError) as e:
+        L.opt_sgd_fwd(tree, (0.1, 0.0, False), 0, 0, buf[1:], None, buf[:64], None)
+    assert e.value.code == L.OPT_EALIGN
+
+
+def test_nan_propagates_locally(L):
+    """Device-side NaN inputs are not checked: they propagate to that
+    element's outputs and to the hyper-gradient sums, nowhere else."""
+    x = synth.state_tree(0xAA, [4096])
+    x["g"][100] = np.nan
+    tree = L.Tree(numel=4096, device=DEV)
+    hp = (1e-3, 0.9, 0.999, 1e-8, 0.0)
+    g, m, v, du = dev_f32(x["g"]), dev_f32(x["m"]), dev_f32(x["v"]), dev_f32(x["du"])
+    u, m1, v1 = torch.empty_like(g), torch.empty_like(g), torch.empty_like(g)
+    L.opt_adam_fwd(tree, 5, hp, 0, 0, g, m, v, u, m1, v1)
+    uh = host(u)
+    assert np.isnan(uh[100]) and np.isfinite(np.delete(uh, 100)).all()
+    dg = torch.empty_like(g)
+    dhp = torch.empty(4, dtype=torch.float64, device=DEV)
+    L.opt_adam_bwd(tree, 5, hp, 0, 0, g, m, v, du, None, None, dg, None, None, dhp, None,
+                   tree.workspace(DEV))
+    dgh = host(dg)
+    assert np.isnan(dgh[100]) and np.isfinite(np.delete(dgh, 100)).all()
+    assert np.isnan(host(dhp)[0])
+
+
+@pytest.mark.parametrize("kind", ["rmsprop", "sgd", "sgd_nesterov"])
+@pytest.mark.parametrize("lr", [1e-3, 1.0])
+def test_cold_start_null_state(L, kind, lr):
+    """t = 1 style zero state passed as NULL (no HBM read) equals explicit
+    zeros, and matches the oracle (C1 inputs, 1/64 exact zeros)."""
+    x = synth.c1_inputs()
+    n = x["g"].size
+    tree = L.Tree(numel=n, device=DEV)
+    g, du, ds1 = dev_f32(x["g"]), dev_f32(x["du"]), dev_f32(x["dm1"])
+    z = torch.zeros_like(g)
+    outs = []
+    for state in (None, z):
+        u, s1 = torch.empty_like(g), torch.empty_like(g)
+        dg, ds = torch.empty_like(g), torch.empty_like(g)
+        if kind == "rmsprop":
+            hp = (lr, 0.99, 1e-8)
+            L.opt_rmsprop_fwd(tree, hp, 0, 0, g, state, u, s1)
+            dhp = torch.empty(3, dtype=torch.float64, device=DEV)
+            L.opt_rmsprop_bwd(tree, hp, 0, 0, g, state, du, ds1, dg, ds, dhp, None,
+                              tree.workspace(DEV))
+        else:
+            hp = (lr, 0.9, kind == "sgd_nesterov")
+            L.opt_sgd_fwd(tree, hp, 0, 0, g, state, u, s1)
+            dhp = torch.empty(2, dtype=torch.float64, device=DEV)
+            L.opt_sgd_bwd(tree, hp, 0, 0, g, state, du, ds1, dg, ds, dhp, None,
+                          tree.workspace(DEV))
+        outs.append([host(t) for t in (u, s1, dg, ds, dhp)])
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
+    u, s1, dg, ds, dhp = outs[0]
+    if kind == "rmsprop":
+        ru, rs1 = oracle.rmsprop_fwd(x["g"], None, *hp, prec=1)
+        r = oracle.rmsprop_vjp(x["g"], None, x["du"], x["dm1"], *hp, prec=1)
+        mag = oracle.rmsprop_mag(x["g"], None, x["du"], x["dm1"], *hp)
+        names = (("u", u, ru), ("v1", s1, rs1), ("dg", dg, r["dg"]), ("dv", ds, r["dv"]))
+    else:
+        ru, rs1 = oracle.sgd_fwd(x["g"], None, *hp, prec=1)
+        r = oracle.sgd_vjp(x["g"], None, x["du"], x["dm1"], *hp, prec=1)
+        mag = oracle.sgd_mag(x["g"], None, x["du"], x["dm1"], *hp)
+        names = (("u", u, ru), ("b1", s1, rs1), ("dg", dg, r["dg"]), ("db", ds, r["db"]))
+    for name, got, ref in names:
+        check(name, got, ref, mag[name], 1)
+    assert_sum_close("dhp", dhp, r["dhp"], np.maximum(r["dhp_abs"], mag["dhp"]))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("kind", ["rmsprop", "sgd"])
+@pytest.mark.parametrize("bf16", [False, True])
+def test_c2_full_size_sampled_rmsprop_sgd(L, kind, bf16):
+    leaves = synth.RESNET18_LEAVES
+    x = synth.state_tree(0xC2, leaves)
+    n = int(sum(leaves))
+    tree = L.Tree(offsets=synth.offsets_of(leaves), device=DEV)
+    st_h = state_host_bits(x["v"] if kind == "rmsprop" else x["m"], bf16)
+    g, st = dev_f32(x["g"]), dev_state(x["v"] if kind == "rmsprop" else x["m"], bf16)
+    du, ds1 = dev_f32(x["du"]), dev_f32(x["dv1"] if kind == "rmsprop" else x["dm1"])
+    u = torch.empty_like(g)
+    s1 = torch.empty(n, dtype=torch.bfloat16 if bf16 else torch.float32, device=DEV)
+    dg, ds = torch.empty_like(g), torch.empty_like(g)
+    sd = 1 if bf16 else 0
+    if kind == "rmsprop":
+        hp = (1e-2, 0.99, 1e-8)
+        L.opt_rmsprop_fwd(tree, hp, sd, 0, g, st, u, s1)
+        L.opt_rmsprop_bwd(tree, hp, sd, 0, g, st, du, ds1, dg, ds)
+    else:
+        hp = (0.1, 0.9, True)
+        L.opt_sgd_fwd(tree, hp, sd, 0, g, st, u, s1)
+        L.opt_sgd_bwd(tree, hp, sd, 0, g, st, du, ds1, dg, ds)
+    idx = np.sort(np.random.default_rng(1).choice(n, 1 << 16, replace=False))
+    sg, sst = x["g"][idx], st_h[idx]
+    sdu = x["du"][idx]
+    sds1 = (x["dv1"] if kind == "rmsprop" else x["dm1"])[idx]
+    if kind == "rmsprop":
+        ru, rs1 = oracle.rmsprop_fwd(sg, sst, *hp, state_bf16=bf16, prec=1)
+        r = oracle.rmsprop_vjp(sg, sst, sdu, sds1, *hp, state_bf16=bf16, prec=1)
+        mag = oracle.rmsprop_mag(sg, sst, sdu, sds1, *hp, state_bf16=bf16)
+        pairs = (("u", u, ru), ("dg", dg, r["dg"]), ("dv", ds, r["dv"]))
+    else:
+        ru, rs1 = oracle.sgd_fwd(sg, sst, *hp, state_bf16=bf16, prec=1)
+        r = oracle.sgd_vjp(sg, sst, sdu, sds1, *hp, state_bf16=bf16, prec=1)
+        mag = oracle.sgd_mag(sg, sst, sdu, sds1, *hp, state_bf16=bf16)
+        pairs = (("u", u, ru), ("dg", dg, r["dg"]), ("db", ds, r["db"]))
+    for name, got, ref in pairs:
+        check(name, host(got)[idx], ref, mag[name], 1)
+    s1h = host(s1)[idx]
+    if bf16:
+        assert_close("state'", oracle.bf16_to_f64(s1h), rs1, rtol=1e-2, atol=0)
+    else:
+        check("state'", s1h, rs1, mag["v1" if kind == "rmsprop" else "b1"], 1)
