@@ -345,3 +345,238 @@ def sgd_mag(g, b, du, db1, lr, momentum, nesterov=False, state_bf16=False):
                               _p(hs))
     o = out.reshape(4, n)
     return dict(u=o[0], b1=o[1], dg=o[2], db=o[3], dhp=hs)
+
+
+# ------------------------------------------- optimizer variants (NEXT-1)
+def _ex_lib():
+    L = lib()
+    if getattr(L, "_ex_ready", False):
+        return L
+    P, i64, I, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    L.oracle_adam_fwd_ex.argtypes = [i64, i64, P, P, P, i64, P, I, I, P, P, P, P, P, P, P]
+    L.oracle_adam_vjp_ex.argtypes = [i64, i64, P, P, P, i64, P, I, I] + [P] * 14
+    L.oracle_rmsprop_fwd_ex.argtypes = [i64, P, P, P, i64, P, I, I, P, P, P, P, P]
+    L.oracle_rmsprop_vjp_ex.argtypes = [i64, P, P, P, i64, P, I, I] + [P] * 11
+    L.oracle_sgd_fwd_ex.argtypes = [i64, P, P, P, i64, P, I, I, P, P, P, P, P]
+    L.oracle_sgd_vjp_ex.argtypes = [i64, P, P, P, i64, P, I, I] + [P] * 11
+    L.oracle_adam_fwd_ex_cplx.argtypes = [i64, i64, P, P, D, D, I, I] + [P] * 16
+    L.oracle_rmsprop_fwd_ex_cplx.argtypes = [i64, P, P, D, D, I] + [P] * 12
+    L.oracle_sgd_fwd_ex_cplx.argtypes = [i64, P, P, I, D, D, I] + [P] * 12
+    L._ex_ready = True
+    return L
+
+
+def _ext(weight_decay, decoupled, maximize):
+    return _hp([weight_decay, 1.0 if decoupled else 0.0, 1.0 if maximize else 0.0])
+
+
+def _leaf_args(lr_leaf, offsets):
+    if lr_leaf is None and offsets is None:
+        return None, 0, None
+    nl, off = _offsets(offsets)
+    lrl = None if lr_leaf is None else np.ascontiguousarray(lr_leaf, dtype=np.float64)
+    return lrl, nl, off
+
+
+def adam_fwd_ex(g, m, v, theta, t, lr, b1, b2, eps, eps_root=0.0, weight_decay=0.0,
+                decoupled=False, maximize=False, lr_leaf=None, offsets=None, state_bf16=False,
+                prec=0):
+    """Adam step with weight decay (L2 or decoupled/AdamW), maximize and
+    per-leaf learning rates (lr_leaf[l] replaces lr on leaf l)."""
+    g, theta = _f32(g), _f32(theta)
+    n = g.size
+    m, v = _state(m, state_bf16), _state(v, state_bf16)
+    hp = _hp([lr, b1, b2, eps, eps_root])
+    ext = _ext(weight_decay, decoupled, maximize)
+    lrl, nl, off = _leaf_args(lr_leaf, offsets)
+    u, m1, v1 = _out(n), _out(n), _out(n)
+    _ex_lib().oracle_adam_fwd_ex(n, int(t), _p(hp), _p(ext), _p(lrl), nl, _p(off),
+                                 int(state_bf16), int(prec), _p(g), _p(m), _p(v), _p(theta),
+                                 _p(u), _p(m1), _p(v1))
+    return u, m1, v1
+
+
+def adam_vjp_ex(g, m, v, theta, du, dm1, dv1, t, lr, b1, b2, eps, eps_root=0.0,
+                weight_decay=0.0, decoupled=False, maximize=False, lr_leaf=None, offsets=None,
+                state_bf16=False, prec=0):
+    """VJP of adam_fwd_ex: dg, dm, dv, dtheta (through the update only) and
+    dhp = (lr, b1, b2, eps, wd) sums (+ dhp_leaf per leaf when offsets)."""
+    g, theta = _f32(g), _f32(theta)
+    n = g.size
+    m, v = _state(m, state_bf16), _state(v, state_bf16)
+    du, dm1, dv1 = _f32(du), _f32(dm1), _f32(dv1)
+    hp = _hp([lr, b1, b2, eps, eps_root])
+    ext = _ext(weight_decay, decoupled, maximize)
+    lrl, nl, off = _leaf_args(lr_leaf, offsets)
+    dg, dm, dv, dth = _out(n), _out(n), _out(n), _out(n)
+    dhp, dabs = np.zeros(5), np.zeros(5)
+    leaf = np.zeros((nl, 5)) if off is not None else None
+    _ex_lib().oracle_adam_vjp_ex(n, int(t), _p(hp), _p(ext), _p(lrl), nl, _p(off),
+                                 int(state_bf16), int(prec), _p(g), _p(m), _p(v), _p(theta),
+                                 _p(du), _p(dm1), _p(dv1), _p(dg), _p(dm), _p(dv), _p(dth),
+                                 _p(dhp), _p(dabs), _p(leaf))
+    return dict(dg=dg, dm=dm, dv=dv, dtheta=dth, dhp=dhp, dhp_abs=dabs, dhp_leaf=leaf)
+
+
+def rmsprop_fwd_ex(g, v, theta, lr, alpha, eps, weight_decay=0.0, maximize=False, lr_leaf=None,
+                   offsets=None, state_bf16=False, prec=0):
+    g, theta = _f32(g), _f32(theta)
+    n = g.size
+    v = _state(v, state_bf16)
+    hp = _hp([lr, alpha, eps])
+    ext = _ext(weight_decay, False, maximize)
+    lrl, nl, off = _leaf_args(lr_leaf, offsets)
+    u, v1 = _out(n), _out(n)
+    _ex_lib().oracle_rmsprop_fwd_ex(n, _p(hp), _p(ext), _p(lrl), nl, _p(off), int(state_bf16),
+                                    int(prec), _p(g), _p(v), _p(theta), _p(u), _p(v1))
+    return u, v1
+
+
+def rmsprop_vjp_ex(g, v, theta, du, dv1, lr, alpha, eps, weight_decay=0.0, maximize=False,
+                   lr_leaf=None, offsets=None, state_bf16=False, prec=0):
+    """dhp = (lr, alpha, eps, wd)."""
+    g, theta = _f32(g), _f32(theta)
+    n = g.size
+    v = _state(v, state_bf16)
+    du, dv1 = _f32(du), _f32(dv1)
+    hp = _hp([lr, alpha, eps])
+    ext = _ext(weight_decay, False, maximize)
+    lrl, nl, off = _leaf_args(lr_leaf, offsets)
+    dg, dv, dth = _out(n), _out(n), _out(n)
+    dhp, dabs = np.zeros(4), np.zeros(4)
+    leaf = np.zeros((nl, 4)) if off is not None else None
+    _ex_lib().oracle_rmsprop_vjp_ex(n, _p(hp), _p(ext), _p(lrl), nl, _p(off), int(state_bf16),
+                                    int(prec), _p(g), _p(v), _p(theta), _p(du), _p(dv1), _p(dg),
+                                    _p(dv), _p(dth), _p(dhp), _p(dabs), _p(leaf))
+    return dict(dg=dg, dv=dv, dtheta=dth, dhp=dhp, dhp_abs=dabs, dhp_leaf=leaf)
+
+
+def sgd_fwd_ex(g, b, theta, lr, momentum, nesterov=False, weight_decay=0.0, maximize=False,
+               lr_leaf=None, offsets=None, state_bf16=False, prec=0):
+    g, theta = _f32(g), _f32(theta)
+    n = g.size
+    b = _state(b, state_bf16)
+    hp = _hp([lr, momentum, 1.0 if nesterov else 0.0])
+    ext = _ext(weight_decay, False, maximize)
+    lrl, nl, off = _leaf_args(lr_leaf, offsets)
+    u, b1 = _out(n), _out(n)
+    _ex_lib().oracle_sgd_fwd_ex(n, _p(hp), _p(ext), _p(lrl), nl, _p(off), int(state_bf16),
+                                int(prec), _p(g), _p(b), _p(theta), _p(u), _p(b1))
+    return u, b1
+
+
+def sgd_vjp_ex(g, b, theta, du, db1, lr, momentum, nesterov=False, weight_decay=0.0,
+               maximize=False, lr_leaf=None, offsets=None, state_bf16=False, prec=0):
+    """dhp = (lr, momentum, wd)."""
+    g, theta = _f32(g), _f32(theta)
+    n = g.size
+    b = _state(b, state_bf16)
+    du, db1 = _f32(du), _f32(db1)
+    hp = _hp([lr, momentum, 1.0 if nesterov else 0.0])
+    ext = _ext(weight_decay, False, maximize)
+    lrl, nl, off = _leaf_args(lr_leaf, offsets)
+    dg, db, dth = _out(n), _out(n), _out(n)
+    dhp, dabs = np.zeros(3), np.zeros(3)
+    leaf = np.zeros((nl, 3)) if off is not None else None
+    _ex_lib().oracle_sgd_vjp_ex(n, _p(hp), _p(ext), _p(lrl), nl, _p(off), int(state_bf16),
+                                int(prec), _p(g), _p(b), _p(theta), _p(du), _p(db1), _p(dg),
+                                _p(db), _p(dth), _p(dhp), _p(dabs), _p(leaf))
+    return dict(dg=dg, db=db, dtheta=dth, dhp=dhp, dhp_abs=dabs, dhp_leaf=leaf)
+
+
+def adam_fwd_ex_complex(g, m, v, theta, t, hp, lr_elem, weight_decay=0.0, decoupled=False,
+                        maximize=False):
+    """Complex forward of adam_fwd_ex; hp[0] unused, lr given per element."""
+    g = np.asarray(g, dtype=np.complex128)
+    n = g.size
+    hr, hi = _cparts(hp, 5)
+    lr_r, lr_i = _cparts(lr_elem, n)
+    gr, gi = _cparts(g, n)
+    mr, mi = _cparts(m, n)
+    vr, vi = _cparts(v, n)
+    tr, ti = _cparts(theta, n)
+    wd = complex(weight_decay)
+    outs = [np.empty(n) for _ in range(6)]
+    _ex_lib().oracle_adam_fwd_ex_cplx(n, int(t), _p(hr), _p(hi), wd.real, wd.imag, int(decoupled),
+                                      int(maximize), _p(lr_r), _p(lr_i), _p(gr), _p(gi), _p(mr),
+                                      _p(mi), _p(vr), _p(vi), _p(tr), _p(ti),
+                                      *[_p(o) for o in outs])
+    return tuple(outs[2 * k] + 1j * outs[2 * k + 1] for k in range(3))
+
+
+def rmsprop_fwd_ex_complex(g, v, theta, hp, lr_elem, weight_decay=0.0, maximize=False):
+    g = np.asarray(g, dtype=np.complex128)
+    n = g.size
+    hr, hi = _cparts(hp, 3)
+    lr_r, lr_i = _cparts(lr_elem, n)
+    gr, gi = _cparts(g, n)
+    vr, vi = _cparts(v, n)
+    tr, ti = _cparts(theta, n)
+    wd = complex(weight_decay)
+    outs = [np.empty(n) for _ in range(4)]
+    _ex_lib().oracle_rmsprop_fwd_ex_cplx(n, _p(hr), _p(hi), wd.real, wd.imag, int(maximize),
+                                         _p(lr_r), _p(lr_i), _p(gr), _p(gi), _p(vr), _p(vi),
+                                         _p(tr), _p(ti), *[_p(o) for o in outs])
+    return tuple(outs[2 * k] + 1j * outs[2 * k + 1] for k in range(2))
+
+
+def sgd_fwd_ex_complex(g, b, theta, hp, lr_elem, nesterov=False, weight_decay=0.0,
+                       maximize=False):
+    g = np.asarray(g, dtype=np.complex128)
+    n = g.size
+    hr, hi = _cparts(hp, 2)
+    lr_r, lr_i = _cparts(lr_elem, n)
+    gr, gi = _cparts(g, n)
+    br, bi = _cparts(b, n)
+    tr, ti = _cparts(theta, n)
+    wd = complex(weight_decay)
+    outs = [np.empty(n) for _ in range(4)]
+    _ex_lib().oracle_sgd_fwd_ex_cplx(n, _p(hr), _p(hi), int(nesterov), wd.real, wd.imag,
+                                     int(maximize), _p(lr_r), _p(lr_i), _p(gr), _p(gi), _p(br),
+                                     _p(bi), _p(tr), _p(ti), *[_p(o) for o in outs])
+    return tuple(outs[2 * k] + 1j * outs[2 * k + 1] for k in range(2))
+
+
+def ex_mag(kind, g, state, theta, du, ds1, dv1=None, t=1, hp=(), weight_decay=0.0,
+           decoupled=False, maximize=False, lr_leaf=None, offsets=None, state_bf16=False):
+    """Magnitude twins (Z10) of the variant outputs: the base twins evaluated
+    at |g~| <= |g| + wd |theta| (the rounding scale of the decayed gradient)
+    with each element's lr, plus the weight-decay terms. ``state`` is
+    (m, v) for adam, the single state array otherwise. Returns arrays keyed
+    like the base twins plus 'dtheta', 'dwd' and 'extra_lr' (per element)."""
+    g64 = _f32(g).astype(np.float64)
+    th = np.abs(_f32(theta).astype(np.float64))
+    n = g64.size
+    if lr_leaf is not None:
+        lr_e = np.repeat(np.asarray(lr_leaf, np.float64), np.diff(np.asarray(offsets)))
+    else:
+        lr_e = np.full(n, float(hp[0]))
+    gmag = np.abs(g64) + weight_decay * th
+    sub = lambda a, sel: None if a is None else np.asarray(a)[sel]
+    base = {}
+    for lr in np.unique(lr_e):
+        sel = lr_e == lr
+        if kind == "adam":
+            b = adam_mag(gmag[sel], sub(state[0], sel), sub(state[1], sel), du[sel], sub(ds1, sel),
+                         sub(dv1, sel), t, lr, *hp[1:], state_bf16=state_bf16)
+        elif kind == "rmsprop":
+            b = rmsprop_mag(gmag[sel], sub(state, sel), du[sel], sub(ds1, sel), lr, *hp[1:],
+                            state_bf16=state_bf16)
+        else:
+            b = sgd_mag(gmag[sel], sub(state, sel), du[sel], sub(ds1, sel), lr, *hp[1:],
+                        state_bf16=state_bf16)
+        for k, val in b.items():
+            if k != "dhp":
+                base.setdefault(k, np.zeros(n))[sel] = val
+    adu = np.abs(_f32(du).astype(np.float64))
+    out = dict(base)
+    if kind == "adam" and decoupled:
+        out["u"] = base["u"] + np.abs(lr_e) * weight_decay * th
+        out["dtheta"] = np.abs(lr_e) * weight_decay * adu
+        out["dwd"] = adu * np.abs(lr_e) * th
+        out["extra_lr"] = adu * weight_decay * th
+    else:
+        out["dtheta"] = weight_decay * base["dg"]
+        out["dwd"] = base["dg"] * th
+        out["extra_lr"] = np.zeros(n)
+    return out

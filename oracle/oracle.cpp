@@ -618,3 +618,273 @@ void oracle_sgd_mag(int64_t n, const double* hp, int bf, const float* g, const v
 }
 
 }  // extern "C"
+
+// ----------------------------------- optimizer variants (NEXT-1) entry points
+// ext[3] = {weight_decay, decoupled, maximize}; lr_leaf (double[n_leaves]) or
+// NULL: element i uses the learning rate of its leaf (offsets), else hp[0].
+// Hyper-gradient slots: adam (lr, b1, b2, eps, wd), rmsprop (lr, alpha, eps,
+// wd), sgd (lr, mu, wd); dhp_leaf[l*nh + k] are the same sums per leaf.
+namespace {
+
+template <class Fn>
+void per_leaf_elements(int64_t n, int64_t n_leaves, const int64_t* off, Fn fn) {
+  if (!off || n_leaves <= 0) {
+    for (int64_t i = 0; i < n; ++i) fn(i, (int64_t)0);
+    return;
+  }
+  for (int64_t l = 0; l < n_leaves; ++l)
+    for (int64_t i = off[l]; i < off[l + 1]; ++i) fn(i, l);
+}
+
+template <class T>
+oracle::ExHP<T> ex_hp(const double* ext) {
+  return {T(ext[0]), ext[1] != 0.0 ? 1 : 0, ext[2] != 0.0 ? 1 : 0};
+}
+
+template <class T, int NH, class Elem>
+void vjp_ex_loop(int64_t n, int64_t n_leaves, const int64_t* off, double* dhp, double* dhp_abs,
+                 double* dhp_leaf, Elem elem) {
+  long double s[NH] = {}, a[NH] = {};
+  std::vector<long double> leaf((size_t)(n_leaves > 0 ? n_leaves : 1) * NH, 0.0L);
+  per_leaf_elements(n, n_leaves, off, [&](int64_t i, int64_t l) {
+    T h[NH];
+    elem(i, l, h);
+    for (int k = 0; k < NH; ++k) {
+      long double x = (long double)h[k];
+      s[k] += x;
+      a[k] += x < 0 ? -x : x;
+      leaf[(size_t)l * NH + k] += x;
+    }
+  });
+  for (int k = 0; k < NH; ++k) {
+    if (dhp) dhp[k] = (double)s[k];
+    if (dhp_abs) dhp_abs[k] = (double)a[k];
+  }
+  if (dhp_leaf && off)
+    for (int64_t l = 0; l < n_leaves; ++l)
+      for (int k = 0; k < NH; ++k) dhp_leaf[l * NH + k] = (double)leaf[(size_t)l * NH + k];
+}
+
+template <class T>
+void adam_fwd_ex_arr(int64_t n, int64_t t, const double* hp, const double* ext,
+                     const double* lr_leaf, int64_t nl, const int64_t* off, int bf, const float* g,
+                     const void* m, const void* v, const float* th, double* u, double* m1,
+                     double* v1) {
+  const oracle::ExHP<T> x = ex_hp<T>(ext);
+  per_leaf_elements(n, nl, off, [&](int64_t i, int64_t l) {
+    AdamHP<T> h = adam_hp<T>(hp);
+    if (lr_leaf) h.lr = T(lr_leaf[l]);
+    auto r = oracle::adam_fwd_ex<T>(T(f32_in(g, i)), T(state_in(m, bf, i)), T(state_in(v, bf, i)),
+                                    T(f32_in(th, i)), h, x, t);
+    put(u, i, (double)r.u);
+    put(m1, i, (double)r.m1);
+    put(v1, i, (double)r.v1);
+  });
+}
+
+template <class T>
+void adam_vjp_ex_arr(int64_t n, int64_t t, const double* hp, const double* ext,
+                     const double* lr_leaf, int64_t nl, const int64_t* off, int bf, const float* g,
+                     const void* m, const void* v, const float* th, const float* du,
+                     const float* dm1, const float* dv1, double* dg, double* dm, double* dv,
+                     double* dth, double* dhp, double* dhp_abs, double* dhp_leaf) {
+  const oracle::ExHP<T> x = ex_hp<T>(ext);
+  vjp_ex_loop<T, 5>(n, nl, off, dhp, dhp_abs, dhp_leaf, [&](int64_t i, int64_t l, T* h) {
+    AdamHP<T> hh = adam_hp<T>(hp);
+    if (lr_leaf) hh.lr = T(lr_leaf[l]);
+    auto r = oracle::adam_vjp_ex<T>(T(f32_in(g, i)), T(state_in(m, bf, i)), T(state_in(v, bf, i)),
+                                    T(f32_in(th, i)), T(f32_in(du, i)), T(f32_in(dm1, i)),
+                                    T(f32_in(dv1, i)), hh, x, t);
+    put(dg, i, (double)r.dg);
+    put(dm, i, (double)r.dm);
+    put(dv, i, (double)r.dv);
+    put(dth, i, (double)r.dtheta);
+    h[0] = r.dlr; h[1] = r.db1; h[2] = r.db2; h[3] = r.deps; h[4] = r.dwd;
+  });
+}
+
+template <class T>
+void rms_fwd_ex_arr(int64_t n, const double* hp, const double* ext, const double* lr_leaf,
+                    int64_t nl, const int64_t* off, int bf, const float* g, const void* v,
+                    const float* th, double* u, double* v1) {
+  const oracle::ExHP<T> x = ex_hp<T>(ext);
+  per_leaf_elements(n, nl, off, [&](int64_t i, int64_t l) {
+    RmsHP<T> h = rms_hp<T>(hp);
+    if (lr_leaf) h.lr = T(lr_leaf[l]);
+    auto r = oracle::rmsprop_fwd_ex<T>(T(f32_in(g, i)), T(state_in(v, bf, i)), T(f32_in(th, i)),
+                                       h, x);
+    put(u, i, (double)r.u);
+    put(v1, i, (double)r.v1);
+  });
+}
+
+template <class T>
+void rms_vjp_ex_arr(int64_t n, const double* hp, const double* ext, const double* lr_leaf,
+                    int64_t nl, const int64_t* off, int bf, const float* g, const void* v,
+                    const float* th, const float* du, const float* dv1, double* dg, double* dv,
+                    double* dth, double* dhp, double* dhp_abs, double* dhp_leaf) {
+  const oracle::ExHP<T> x = ex_hp<T>(ext);
+  vjp_ex_loop<T, 4>(n, nl, off, dhp, dhp_abs, dhp_leaf, [&](int64_t i, int64_t l, T* h) {
+    RmsHP<T> hh = rms_hp<T>(hp);
+    if (lr_leaf) hh.lr = T(lr_leaf[l]);
+    auto r = oracle::rmsprop_vjp_ex<T>(T(f32_in(g, i)), T(state_in(v, bf, i)), T(f32_in(th, i)),
+                                       T(f32_in(du, i)), T(f32_in(dv1, i)), hh, x);
+    put(dg, i, (double)r.dg);
+    put(dv, i, (double)r.dv);
+    put(dth, i, (double)r.dtheta);
+    h[0] = r.dlr; h[1] = r.dalpha; h[2] = r.deps; h[3] = r.dwd;
+  });
+}
+
+template <class T>
+void sgd_fwd_ex_arr(int64_t n, const double* hp, const double* ext, const double* lr_leaf,
+                    int64_t nl, const int64_t* off, int bf, const float* g, const void* b,
+                    const float* th, double* u, double* b1) {
+  const oracle::ExHP<T> x = ex_hp<T>(ext);
+  per_leaf_elements(n, nl, off, [&](int64_t i, int64_t l) {
+    SgdHP<T> h = sgd_hp<T>(hp);
+    if (lr_leaf) h.lr = T(lr_leaf[l]);
+    auto r = oracle::sgd_fwd_ex<T>(T(f32_in(g, i)), T(state_in(b, bf, i)), T(f32_in(th, i)), h, x);
+    put(u, i, (double)r.u);
+    put(b1, i, (double)r.b1);
+  });
+}
+
+template <class T>
+void sgd_vjp_ex_arr(int64_t n, const double* hp, const double* ext, const double* lr_leaf,
+                    int64_t nl, const int64_t* off, int bf, const float* g, const void* b,
+                    const float* th, const float* du, const float* db1, double* dg, double* db,
+                    double* dth, double* dhp, double* dhp_abs, double* dhp_leaf) {
+  const oracle::ExHP<T> x = ex_hp<T>(ext);
+  vjp_ex_loop<T, 3>(n, nl, off, dhp, dhp_abs, dhp_leaf, [&](int64_t i, int64_t l, T* h) {
+    SgdHP<T> hh = sgd_hp<T>(hp);
+    if (lr_leaf) hh.lr = T(lr_leaf[l]);
+    auto r = oracle::sgd_vjp_ex<T>(T(f32_in(g, i)), T(state_in(b, bf, i)), T(f32_in(th, i)),
+                                   T(f32_in(du, i)), T(f32_in(db1, i)), hh, x);
+    put(dg, i, (double)r.dg);
+    put(db, i, (double)r.db);
+    put(dth, i, (double)r.dtheta);
+    h[0] = r.dlr; h[1] = r.dmu; h[2] = r.dwd;
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+void oracle_adam_fwd_ex(int64_t n, int64_t t, const double* hp, const double* ext,
+                        const double* lr_leaf, int64_t nl, const int64_t* off, int bf, int prec,
+                        const float* g, const void* m, const void* v, const float* th, double* u,
+                        double* m1, double* v1) {
+  if (prec) adam_fwd_ex_arr<long double>(n, t, hp, ext, lr_leaf, nl, off, bf, g, m, v, th, u, m1, v1);
+  else adam_fwd_ex_arr<double>(n, t, hp, ext, lr_leaf, nl, off, bf, g, m, v, th, u, m1, v1);
+}
+
+void oracle_adam_vjp_ex(int64_t n, int64_t t, const double* hp, const double* ext,
+                        const double* lr_leaf, int64_t nl, const int64_t* off, int bf, int prec,
+                        const float* g, const void* m, const void* v, const float* th,
+                        const float* du, const float* dm1, const float* dv1, double* dg,
+                        double* dm, double* dv, double* dth, double* dhp, double* dhp_abs,
+                        double* dhp_leaf) {
+  if (prec)
+    adam_vjp_ex_arr<long double>(n, t, hp, ext, lr_leaf, nl, off, bf, g, m, v, th, du, dm1, dv1,
+                                 dg, dm, dv, dth, dhp, dhp_abs, dhp_leaf);
+  else
+    adam_vjp_ex_arr<double>(n, t, hp, ext, lr_leaf, nl, off, bf, g, m, v, th, du, dm1, dv1, dg,
+                            dm, dv, dth, dhp, dhp_abs, dhp_leaf);
+}
+
+void oracle_rmsprop_fwd_ex(int64_t n, const double* hp, const double* ext, const double* lr_leaf,
+                           int64_t nl, const int64_t* off, int bf, int prec, const float* g,
+                           const void* v, const float* th, double* u, double* v1) {
+  if (prec) rms_fwd_ex_arr<long double>(n, hp, ext, lr_leaf, nl, off, bf, g, v, th, u, v1);
+  else rms_fwd_ex_arr<double>(n, hp, ext, lr_leaf, nl, off, bf, g, v, th, u, v1);
+}
+
+void oracle_rmsprop_vjp_ex(int64_t n, const double* hp, const double* ext, const double* lr_leaf,
+                           int64_t nl, const int64_t* off, int bf, int prec, const float* g,
+                           const void* v, const float* th, const float* du, const float* dv1,
+                           double* dg, double* dv, double* dth, double* dhp, double* dhp_abs,
+                           double* dhp_leaf) {
+  if (prec)
+    rms_vjp_ex_arr<long double>(n, hp, ext, lr_leaf, nl, off, bf, g, v, th, du, dv1, dg, dv, dth,
+                                dhp, dhp_abs, dhp_leaf);
+  else
+    rms_vjp_ex_arr<double>(n, hp, ext, lr_leaf, nl, off, bf, g, v, th, du, dv1, dg, dv, dth, dhp,
+                           dhp_abs, dhp_leaf);
+}
+
+void oracle_sgd_fwd_ex(int64_t n, const double* hp, const double* ext, const double* lr_leaf,
+                       int64_t nl, const int64_t* off, int bf, int prec, const float* g,
+                       const void* b, const float* th, double* u, double* b1) {
+  if (prec) sgd_fwd_ex_arr<long double>(n, hp, ext, lr_leaf, nl, off, bf, g, b, th, u, b1);
+  else sgd_fwd_ex_arr<double>(n, hp, ext, lr_leaf, nl, off, bf, g, b, th, u, b1);
+}
+
+void oracle_sgd_vjp_ex(int64_t n, const double* hp, const double* ext, const double* lr_leaf,
+                       int64_t nl, const int64_t* off, int bf, int prec, const float* g,
+                       const void* b, const float* th, const float* du, const float* db1,
+                       double* dg, double* db, double* dth, double* dhp, double* dhp_abs,
+                       double* dhp_leaf) {
+  if (prec)
+    sgd_vjp_ex_arr<long double>(n, hp, ext, lr_leaf, nl, off, bf, g, b, th, du, db1, dg, db, dth,
+                                dhp, dhp_abs, dhp_leaf);
+  else
+    sgd_vjp_ex_arr<double>(n, hp, ext, lr_leaf, nl, off, bf, g, b, th, du, db1, dg, db, dth, dhp,
+                           dhp_abs, dhp_leaf);
+}
+
+// complex forward of the variants (complex-step pins); per-ELEMENT lr
+// (lr_re/lr_im of n) so that a per-leaf lr perturbation can be expressed.
+void oracle_adam_fwd_ex_cplx(int64_t n, int64_t t, const double* hp_re, const double* hp_im,
+                             double wd_re, double wd_im, int decoupled, int maximize,
+                             const double* lr_re, const double* lr_im, const double* g_re,
+                             const double* g_im, const double* m_re, const double* m_im,
+                             const double* v_re, const double* v_im, const double* th_re,
+                             const double* th_im, double* u_re, double* u_im, double* m1_re,
+                             double* m1_im, double* v1_re, double* v1_im) {
+  oracle::ExHP<cd> x{cd(wd_re, wd_im), decoupled, maximize};
+  for (int64_t i = 0; i < n; ++i) {
+    AdamHP<cd> h{cin(lr_re, lr_im, i), cin(hp_re, hp_im, 1), cin(hp_re, hp_im, 2),
+                 cin(hp_re, hp_im, 3), cin(hp_re, hp_im, 4)};
+    auto r = oracle::adam_fwd_ex<cd>(cin(g_re, g_im, i), cin(m_re, m_im, i), cin(v_re, v_im, i),
+                                     cin(th_re, th_im, i), h, x, t);
+    cout_(u_re, u_im, i, r.u);
+    cout_(m1_re, m1_im, i, r.m1);
+    cout_(v1_re, v1_im, i, r.v1);
+  }
+}
+
+void oracle_rmsprop_fwd_ex_cplx(int64_t n, const double* hp_re, const double* hp_im, double wd_re,
+                                double wd_im, int maximize, const double* lr_re,
+                                const double* lr_im, const double* g_re, const double* g_im,
+                                const double* v_re, const double* v_im, const double* th_re,
+                                const double* th_im, double* u_re, double* u_im, double* v1_re,
+                                double* v1_im) {
+  oracle::ExHP<cd> x{cd(wd_re, wd_im), 0, maximize};
+  for (int64_t i = 0; i < n; ++i) {
+    RmsHP<cd> h{cin(lr_re, lr_im, i), cin(hp_re, hp_im, 1), cin(hp_re, hp_im, 2)};
+    auto r = oracle::rmsprop_fwd_ex<cd>(cin(g_re, g_im, i), cin(v_re, v_im, i),
+                                        cin(th_re, th_im, i), h, x);
+    cout_(u_re, u_im, i, r.u);
+    cout_(v1_re, v1_im, i, r.v1);
+  }
+}
+
+void oracle_sgd_fwd_ex_cplx(int64_t n, const double* hp_re, const double* hp_im, int nesterov,
+                            double wd_re, double wd_im, int maximize, const double* lr_re,
+                            const double* lr_im, const double* g_re, const double* g_im,
+                            const double* b_re, const double* b_im, const double* th_re,
+                            const double* th_im, double* u_re, double* u_im, double* b1_re,
+                            double* b1_im) {
+  oracle::ExHP<cd> x{cd(wd_re, wd_im), 0, maximize};
+  for (int64_t i = 0; i < n; ++i) {
+    SgdHP<cd> h{cin(lr_re, lr_im, i), cin(hp_re, hp_im, 1), nesterov};
+    auto r = oracle::sgd_fwd_ex<cd>(cin(g_re, g_im, i), cin(b_re, b_im, i), cin(th_re, th_im, i),
+                                    h, x);
+    cout_(u_re, u_im, i, r.u);
+    cout_(b1_re, b1_im, i, r.b1);
+  }
+}
+
+}  // extern "C"

@@ -339,3 +339,117 @@ inline SgdMag sgd_mag(double g, double b, double du, double db1, const SgdHP<dou
 }
 
 }  // namespace oracle
+
+// ------------------------------------------- optimizer variants (NEXT-1)
+// weight decay, maximize and per-leaf learning rates
+// (learnable per-leaf lr: meta-learned hyper-parameters, MGRL P:21/P:111).
+// The paper does not define these; the semantics follow torch.optim
+// (reading N1 in DESIGN.md): maximize negates g first; L2 weight decay adds
+// wd*theta to the (possibly negated) gradient; AdamW ("decoupled") instead
+// adds -lr*wd*theta to the update. lr is the element's leaf learning rate.
+// Reverse mode is again written one adjoint per forward intermediate.
+namespace oracle {
+
+template <class T>
+struct ExHP {
+  T wd;
+  int decoupled;  // Adam only
+  int maximize;
+};
+
+template <class T>
+AdamFwd<T> adam_fwd_ex(T g, T m, T v, T theta, const AdamHP<T>& h, const ExHP<T>& x, int64_t t) {
+  const T one(1);
+  T gm = x.maximize ? -g : g;
+  T gt = x.decoupled ? gm : gm + x.wd * theta;   // gradient fed to the moments
+  T m1 = h.b1 * m + (one - h.b1) * gt;
+  T v1 = h.b2 * v + (one - h.b2) * gt * gt;
+  T bc1 = one - ipow(h.b1, t), bc2 = one - ipow(h.b2, t);
+  T mhat = m1 / bc1, vhat = v1 / bc2;
+  T s = tsqrt(vhat + h.eps_root);
+  T d = s + h.eps;
+  T u = (re(d) == 0.0) ? T(0) : -h.lr * mhat / d;
+  if (x.decoupled) u = u - h.lr * x.wd * theta;
+  return {u, m1, v1};
+}
+
+template <class T>
+struct AdamVjpEx {
+  T dg, dm, dv, dtheta;           // dtheta: through the update only (not the apply identity)
+  T dlr, db1, db2, deps, dwd;
+};
+
+template <class T>
+AdamVjpEx<T> adam_vjp_ex(T g, T m, T v, T theta, T du, T dm1_out, T dv1_out,
+                         const AdamHP<T>& h, const ExHP<T>& x, int64_t t) {
+  const T one(1);
+  T gm = x.maximize ? -g : g;
+  T gt = x.decoupled ? gm : gm + x.wd * theta;
+  // the plain step on gt (adjoints of every intermediate, adam_vjp above)
+  AdamVjp<T> c = adam_vjp<T>(gt, m, v, du, dm1_out, dv1_out, h, t);
+  AdamVjpEx<T> r;
+  r.dm = c.dm;
+  r.dv = c.dv;
+  r.db1 = c.db1;
+  r.db2 = c.db2;
+  r.deps = c.deps;
+  r.dlr = c.dlr;
+  if (x.decoupled) {
+    // u += -lr * wd * theta
+    r.dlr = r.dlr + du * (-x.wd * theta);
+    r.dwd = du * (-h.lr * theta);
+    r.dtheta = du * (-h.lr * x.wd);
+  } else {
+    // gt = gm + wd * theta
+    r.dwd = c.dg * theta;
+    r.dtheta = c.dg * x.wd;
+  }
+  r.dg = x.maximize ? -c.dg : c.dg;
+  return r;
+}
+
+template <class T>
+RmsFwd<T> rmsprop_fwd_ex(T g, T v, T theta, const RmsHP<T>& h, const ExHP<T>& x) {
+  T gm = x.maximize ? -g : g;
+  return rmsprop_fwd<T>(gm + x.wd * theta, v, h);
+}
+
+template <class T>
+struct RmsVjpEx {
+  T dg, dv, dtheta;
+  T dlr, dalpha, deps, dwd;
+};
+
+template <class T>
+RmsVjpEx<T> rmsprop_vjp_ex(T g, T v, T theta, T du, T dv1_out, const RmsHP<T>& h,
+                           const ExHP<T>& x) {
+  T gm = x.maximize ? -g : g;
+  T gt = gm + x.wd * theta;
+  RmsVjp<T> c = rmsprop_vjp<T>(gt, v, du, dv1_out, h);
+  RmsVjpEx<T> r{x.maximize ? -c.dg : c.dg, c.dv, c.dg * x.wd, c.dlr, c.dalpha, c.deps,
+                c.dg * theta};
+  return r;
+}
+
+template <class T>
+SgdFwd<T> sgd_fwd_ex(T g, T b, T theta, const SgdHP<T>& h, const ExHP<T>& x) {
+  T gm = x.maximize ? -g : g;
+  return sgd_fwd<T>(gm + x.wd * theta, b, h);
+}
+
+template <class T>
+struct SgdVjpEx {
+  T dg, db, dtheta;
+  T dlr, dmu, dwd;
+};
+
+template <class T>
+SgdVjpEx<T> sgd_vjp_ex(T g, T b, T theta, T du, T db1_out, const SgdHP<T>& h, const ExHP<T>& x) {
+  T gm = x.maximize ? -g : g;
+  T gt = gm + x.wd * theta;
+  SgdVjp<T> c = sgd_vjp<T>(gt, b, du, db1_out, h);
+  SgdVjpEx<T> r{x.maximize ? -c.dg : c.dg, c.db, c.dg * x.wd, c.dlr, c.dmu, c.dg * theta};
+  return r;
+}
+
+}  // namespace oracle

@@ -538,3 +538,159 @@ def test_mag_criterion_has_teeth(orc):
         mag["dg"], np.abs(r["dg"]))
     assert ok(_f32_adam_dg(g, du, *hp, reduced=True)).mean() == 1.0
     assert ok(_f32_adam_dg(g, du, *hp, reduced=False)).mean() < 0.5
+
+
+# ------------------------------------ optimizer variants (NEXT-1 pins)
+def _torch_steps_p(opt_cls, kwargs, grads, p0):
+    p = torch.tensor(p0, dtype=torch.float64, requires_grad=True)
+    opt = opt_cls([p], **kwargs)
+    ups, ps = [], []
+    for g in grads:
+        before = p.detach().clone()
+        ps.append(before.numpy().copy())
+        p.grad = torch.as_tensor(g, dtype=torch.float64)
+        opt.step()
+        ups.append((p.detach() - before).numpy())
+    return ups, ps
+
+
+@pytest.mark.parametrize("maximize", [False, True])
+@pytest.mark.parametrize("decoupled", [False, True])
+def test_adam_variants_match_torch_optim(orc, maximize, decoupled):
+    """Weight decay (torch.optim.Adam L2 / torch.optim.AdamW decoupled) and
+    maximize: the oracle's variant forward reproduces torch.optim in float64
+    over 8 steps (reading N1)."""
+    rng = np.random.default_rng(11)
+    n = 129
+    grads = [(rng.standard_normal(n) * 10.0 ** rng.uniform(-3, 0, n)) for _ in range(8)]
+    p0 = rng.standard_normal(n)
+    wd, lr = 0.05, 1e-2
+    cls = torch.optim.AdamW if decoupled else torch.optim.Adam
+    ups, ps = _torch_steps_p(cls, dict(lr=lr, weight_decay=wd, maximize=maximize), grads, p0)
+    m = v = np.zeros(n)
+    for t, (g, th) in enumerate(zip(grads, ps), 1):
+        u, m, v = (x.real for x in orc.adam_fwd_ex_complex(
+            g, m, v, th, t, [lr, 0.9, 0.999, 1e-8, 0.0], np.full(n, lr), wd, decoupled, maximize))
+        np.testing.assert_allclose(u, ups[t - 1], rtol=1e-9, atol=1e-14)
+
+
+@pytest.mark.parametrize("maximize", [False, True])
+def test_rmsprop_sgd_variants_match_torch_optim(orc, maximize):
+    rng = np.random.default_rng(12)
+    n = 77
+    grads = [rng.standard_normal(n) for _ in range(6)]
+    p0 = rng.standard_normal(n)
+    ups, ps = _torch_steps_p(torch.optim.RMSprop, dict(lr=1e-2, alpha=0.9, weight_decay=0.1,
+                                                       maximize=maximize), grads, p0)
+    v = np.zeros(n)
+    for t, (g, th) in enumerate(zip(grads, ps), 1):
+        u, v = (x.real for x in orc.rmsprop_fwd_ex_complex(g, v, th, [1e-2, 0.9, 1e-8],
+                                                            np.full(n, 1e-2), 0.1, maximize))
+        np.testing.assert_allclose(u, ups[t - 1], rtol=1e-9, atol=1e-14)
+    for nest in (False, True):
+        ups, ps = _torch_steps_p(torch.optim.SGD, dict(lr=0.1, momentum=0.9, nesterov=nest,
+                                                       weight_decay=0.1, maximize=maximize),
+                                 grads, p0)
+        b = np.zeros(n)
+        for t, (g, th) in enumerate(zip(grads, ps), 1):
+            u, b = (x.real for x in orc.sgd_fwd_ex_complex(g, b, th, [0.1, 0.9], np.full(n, 0.1),
+                                                            nest, 0.1, maximize))
+            np.testing.assert_allclose(u, ups[t - 1], rtol=1e-9, atol=1e-14)
+
+
+def test_variants_reduce_to_base(orc):
+    """wd = 0, maximize off, one lr for every leaf: the variant equals the
+    plain step bitwise (dtheta = 0)."""
+    x = synth.state_tree(81, [300, 200])
+    th = x["du"]
+    off = synth.offsets_of([300, 200])
+    hp = (1e-3, 0.9, 0.999, 1e-8)
+    a = orc.adam_vjp(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], 4, *hp)
+    b = orc.adam_vjp_ex(x["g"], x["m"], x["v"], th, x["du"], x["dm1"], x["dv1"], 4, *hp,
+                        lr_leaf=[1e-3, 1e-3], offsets=off)
+    for k in ("dg", "dm", "dv"):
+        np.testing.assert_array_equal(a[k], b[k])
+    assert np.all(b["dtheta"] == 0)
+    # d/dwd at wd = 0 (L2): sum of dg~ * theta
+    assert b["dhp"][4] == pytest.approx(np.sum(a["dg"] * th.astype(np.float64)), rel=1e-12)
+    np.testing.assert_allclose(a["dhp"], b["dhp"][:4], rtol=1e-14, atol=1e-300)
+
+
+@pytest.mark.parametrize("decoupled", [False, True])
+@pytest.mark.parametrize("maximize", [False, True])
+def test_adam_variant_vjp_vs_complex_step(orc, decoupled, maximize):
+    """Every VJP output of the variant (dg, dm, dv, dtheta, the five global
+    hyper-gradients and the per-leaf lr gradients) equals the complex-step
+    derivative of the (torch-pinned) variant forward."""
+    leaves = [60, 90, 50]
+    off = synth.offsets_of(leaves)
+    x = synth.state_tree(91, leaves, zero_frac=0.0)
+    th = synth.normal(91, synth.S_THETA0, 200).astype(np.float32)
+    lr_leaf = np.array([1e-2, 3e-2, 5e-3])
+    lr_e = np.repeat(lr_leaf, leaves)
+    hp = np.array([0.0, 0.9, 0.999, 1e-8, 0.0])
+    wd, t = 0.07, 6
+    gd, md, vd, td = (a.astype(np.float64) for a in (x["g"], x["m"], x["v"], th))
+    cot = (x["du"].astype(np.float64), x["dm1"].astype(np.float64), x["dv1"].astype(np.float64))
+    contract = lambda outs: sum(c * o.imag / H for c, o in zip(cot, outs))
+    F = lambda g=gd, m=md, v=vd, th_=td, hp_=hp, lr=lr_e, w=wd: orc.adam_fwd_ex_complex(
+        g, m, v, th_, t, hp_, lr, w, decoupled, maximize)
+    r = orc.adam_vjp_ex(x["g"], x["m"], x["v"], th, x["du"], x["dm1"], x["dv1"], t, 0.0, 0.9,
+                        0.999, 1e-8, weight_decay=wd, decoupled=decoupled, maximize=maximize,
+                        lr_leaf=lr_leaf, offsets=off, prec=1)
+    for name, kw in (("dg", dict(g=gd + 1j * H)), ("dm", dict(m=md + 1j * H)),
+                     ("dv", dict(v=vd + 1j * H)), ("dtheta", dict(th_=td + 1j * H))):
+        cs = contract(F(**kw))
+        np.testing.assert_allclose(r[name], cs, rtol=1e-8, atol=1e-12 * np.abs(cs).max())
+    for k in (1, 2, 3):  # b1, b2, eps
+        hpc = hp.astype(np.complex128)
+        hpc[k] += 1j * H
+        assert r["dhp"][k] == pytest.approx(contract(F(hp_=hpc)).sum(), rel=1e-8, abs=1e-12)
+    assert r["dhp"][4] == pytest.approx(contract(F(w=wd + 1j * H)).sum(), rel=1e-8)
+    for l in range(3):  # per-leaf lr gradients
+        lrc = lr_e.astype(np.complex128)
+        lrc[off[l]:off[l + 1]] += 1j * H
+        assert r["dhp_leaf"][l, 0] == pytest.approx(contract(F(lr=lrc)).sum(), rel=1e-8)
+    assert r["dhp"][0] == pytest.approx(r["dhp_leaf"][:, 0].sum(), rel=1e-12)
+
+
+@pytest.mark.parametrize("kind", ["rmsprop", "sgd", "sgd_nesterov"])
+def test_rms_sgd_variant_vjp_vs_complex_step(orc, kind):
+    leaves = [70, 80]
+    off = synth.offsets_of(leaves)
+    x = synth.state_tree(92, leaves, zero_frac=0.0)
+    th = synth.normal(92, synth.S_THETA0, 150).astype(np.float32)
+    lr_leaf = np.array([2e-2, 7e-3])
+    lr_e = np.repeat(lr_leaf, leaves)
+    wd = 0.03
+    s = x["v"] if kind == "rmsprop" else x["m"]
+    gd, sd, td = (a.astype(np.float64) for a in (x["g"], s, th))
+    cot = (x["du"].astype(np.float64), x["dm1"].astype(np.float64))
+    contract = lambda outs: sum(c * o.imag / H for c, o in zip(cot, outs))
+    nest = kind == "sgd_nesterov"
+    if kind == "rmsprop":
+        hp = np.array([0.0, 0.95, 1e-8])
+        F = lambda g=gd, st=sd, th_=td, hp_=hp, lr=lr_e, w=wd: orc.rmsprop_fwd_ex_complex(
+            g, st, th_, hp_, lr, w, True)
+        r = orc.rmsprop_vjp_ex(x["g"], s, th, x["du"], x["dm1"], 0.0, 0.95, 1e-8, weight_decay=wd,
+                               maximize=True, lr_leaf=lr_leaf, offsets=off, prec=1)
+        sname, hps = "dv", (1, 2)
+    else:
+        hp = np.array([0.0, 0.9])
+        F = lambda g=gd, st=sd, th_=td, hp_=hp, lr=lr_e, w=wd: orc.sgd_fwd_ex_complex(
+            g, st, th_, hp_, lr, nest, w, True)
+        r = orc.sgd_vjp_ex(x["g"], s, th, x["du"], x["dm1"], 0.0, 0.9, nest, weight_decay=wd,
+                           maximize=True, lr_leaf=lr_leaf, offsets=off, prec=1)
+        sname, hps = "db", (1,)
+    for name, kw in (("dg", dict(g=gd + 1j * H)), (sname, dict(st=sd + 1j * H)),
+                     ("dtheta", dict(th_=td + 1j * H))):
+        np.testing.assert_allclose(r[name], contract(F(**kw)), rtol=1e-8, atol=1e-14)
+    for k in hps:
+        hpc = hp.astype(np.complex128)
+        hpc[k] += 1j * H
+        assert r["dhp"][k] == pytest.approx(contract(F(hp_=hpc)).sum(), rel=1e-8)
+    assert r["dhp"][-1] == pytest.approx(contract(F(w=wd + 1j * H)).sum(), rel=1e-8)
+    for l in range(2):
+        lrc = lr_e.astype(np.complex128)
+        lrc[off[l]:off[l + 1]] += 1j * H
+        assert r["dhp_leaf"][l, 0] == pytest.approx(contract(F(lr=lrc)).sum(), rel=1e-8)
