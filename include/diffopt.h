@@ -56,7 +56,7 @@
 extern "C" {
 #endif
 
-#define DIFFOPT_ABI_VERSION 1
+#define DIFFOPT_ABI_VERSION 2
 
 typedef enum {
   OPT_OK = 0,
@@ -160,6 +160,59 @@ int opt_sgd_bwd(const opt_tree* tree, const opt_sgd_hp* hp,
                 float* d_g, float* d_mom,
                 double* d_hp, double* d_hp_leaf,
                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------- optimizer variants (SV §8(f) NEXT-1)
+ * The paper's optimizers are the plain ones; these variants follow
+ * torch.optim semantics (reading N1) and make hyper-parameters
+ * beyond lr/betas/eps meta-learnable (MGRL-style meta-gradients):
+ *   maximize      : the step ascends: g is replaced by -g first;
+ *   weight_decay  : L2 (all three): g~ = (maximize ? -g : g) + wd * theta,
+ *                   or, Adam with decoupled = 1 (AdamW): u += -lr * wd * theta;
+ *   lr_leaf       : device float[n_leaves]; leaf l uses lr_leaf[l] instead of
+ *                   hp->lr (per-leaf learnable learning rates). Needs
+ *                   tree->d_offsets and at most 4096 leaves; the per-leaf lr
+ *                   gradients are slot 0 of d_hp_leaf.
+ * theta = params (required when weight_decay != 0). The *_ex forward writes
+ * params_out = params + updates when both are non-NULL. The *_ex backward
+ * writes d_params = the cotangent of params THROUGH THE UPDATE ONLY (the
+ * weight-decay path); a caller that fused apply_updates adds d_updates for
+ * the identity. Hyper-gradient slots gain weight_decay as the last slot:
+ * Adam (lr, b1, b2, eps, wd), RMSProp (lr, alpha, eps, wd), SGD (lr, mu, wd). */
+typedef struct {
+  double weight_decay;   /* >= 0 */
+  int decoupled;         /* Adam only: 1 = AdamW decoupled decay */
+  int maximize;          /* 1 = gradient ascent */
+  const float* lr_leaf;  /* device [n_leaves] or NULL; 16-byte aligned */
+} opt_ext;
+
+int opt_adam_fwd_ex(const opt_tree* tree, int64_t step, const opt_adam_hp* hp, const opt_ext* ext,
+                    int state_dtype, int compute, const float* g, const void* mu, const void* nu,
+                    const float* params, float* updates, void* mu_out, void* nu_out,
+                    float* params_out, void* stream);
+int opt_adam_bwd_ex(const opt_tree* tree, int64_t step, const opt_adam_hp* hp, const opt_ext* ext,
+                    int state_dtype, int compute, const float* g, const void* mu, const void* nu,
+                    const float* params, const float* d_updates, const float* d_mu_out,
+                    const float* d_nu_out, float* d_g, float* d_mu, float* d_nu, float* d_params,
+                    double* d_hp, double* d_hp_leaf, void* workspace, size_t workspace_bytes,
+                    void* stream);
+int opt_rmsprop_fwd_ex(const opt_tree* tree, const opt_rmsprop_hp* hp, const opt_ext* ext,
+                       int state_dtype, int compute, const float* g, const void* nu,
+                       const float* params, float* updates, void* nu_out, float* params_out,
+                       void* stream);
+int opt_rmsprop_bwd_ex(const opt_tree* tree, const opt_rmsprop_hp* hp, const opt_ext* ext,
+                       int state_dtype, int compute, const float* g, const void* nu,
+                       const float* params, const float* d_updates, const float* d_nu_out,
+                       float* d_g, float* d_nu, float* d_params, double* d_hp, double* d_hp_leaf,
+                       void* workspace, size_t workspace_bytes, void* stream);
+int opt_sgd_fwd_ex(const opt_tree* tree, const opt_sgd_hp* hp, const opt_ext* ext,
+                   int state_dtype, int compute, const float* g, const void* mom,
+                   const float* params, float* updates, void* mom_out, float* params_out,
+                   void* stream);
+int opt_sgd_bwd_ex(const opt_tree* tree, const opt_sgd_hp* hp, const opt_ext* ext,
+                   int state_dtype, int compute, const float* g, const void* mom,
+                   const float* params, const float* d_updates, const float* d_mom_out,
+                   float* d_g, float* d_mom, float* d_params, double* d_hp, double* d_hp_leaf,
+                   void* workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------- apply_updates (row a8)
  * out = params + updates (out may alias params). Its VJP is the identity. */

@@ -253,3 +253,88 @@ def opt_launch_count():
 
 def opt_abi_version():
     return int(lib.opt_abi_version())
+
+
+# ---------------------------------------------- optimizer variants (NEXT-1)
+class opt_ext(ctypes.Structure):
+    _fields_ = [("weight_decay", ctypes.c_double), ("decoupled", ctypes.c_int),
+                ("maximize", ctypes.c_int), ("lr_leaf", ctypes.c_void_p)]
+
+
+def _ext(weight_decay=0.0, decoupled=False, maximize=False, lr_leaf=None):
+    return opt_ext(float(weight_decay), int(bool(decoupled)), int(bool(maximize)), _ptr(lr_leaf))
+
+
+def _setup_ex():
+    P, i64, I, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+    T, E = ctypes.POINTER(opt_tree), ctypes.POINTER(opt_ext)
+    lib.opt_adam_fwd_ex.argtypes = [T, i64, ctypes.POINTER(opt_adam_hp), E, I, I] + [P] * 9
+    lib.opt_adam_bwd_ex.argtypes = [T, i64, ctypes.POINTER(opt_adam_hp), E, I, I] + [P] * 14 + [sz, P]
+    lib.opt_rmsprop_fwd_ex.argtypes = [T, ctypes.POINTER(opt_rmsprop_hp), E, I, I] + [P] * 7
+    lib.opt_rmsprop_bwd_ex.argtypes = [T, ctypes.POINTER(opt_rmsprop_hp), E, I, I] + [P] * 11 + [sz, P]
+    lib.opt_sgd_fwd_ex.argtypes = [T, ctypes.POINTER(opt_sgd_hp), E, I, I] + [P] * 7
+    lib.opt_sgd_bwd_ex.argtypes = [T, ctypes.POINTER(opt_sgd_hp), E, I, I] + [P] * 11 + [sz, P]
+    for name in ("opt_adam_fwd_ex", "opt_adam_bwd_ex", "opt_rmsprop_fwd_ex", "opt_rmsprop_bwd_ex",
+                 "opt_sgd_fwd_ex", "opt_sgd_bwd_ex"):
+        getattr(lib, name).restype = I
+
+
+_setup_ex()
+EXPORTS += ["opt_adam_fwd_ex", "opt_adam_bwd_ex", "opt_rmsprop_fwd_ex", "opt_rmsprop_bwd_ex",
+            "opt_sgd_fwd_ex", "opt_sgd_bwd_ex"]
+
+
+def opt_adam_fwd_ex(tree, step, hp, ext, state_dtype, compute, g, mu, nu, params, updates,
+                    mu_out, nu_out, params_out=None, stream=None):
+    _check(lib.opt_adam_fwd_ex(ctypes.byref(tree.c), int(step), ctypes.byref(_hp(opt_adam_hp, hp)),
+                               ctypes.byref(ext), int(state_dtype), int(compute), _ptr(g), _ptr(mu),
+                               _ptr(nu), _ptr(params), _ptr(updates), _ptr(mu_out), _ptr(nu_out),
+                               _ptr(params_out), _stream(stream)))
+
+
+def opt_adam_bwd_ex(tree, step, hp, ext, state_dtype, compute, g, mu, nu, params, d_updates,
+                    d_mu_out, d_nu_out, d_g, d_mu, d_nu, d_params, d_hp=None, d_hp_leaf=None,
+                    workspace=None, stream=None):
+    wp, wb = _ws(workspace)
+    _check(lib.opt_adam_bwd_ex(ctypes.byref(tree.c), int(step), ctypes.byref(_hp(opt_adam_hp, hp)),
+                               ctypes.byref(ext), int(state_dtype), int(compute), _ptr(g), _ptr(mu),
+                               _ptr(nu), _ptr(params), _ptr(d_updates), _ptr(d_mu_out),
+                               _ptr(d_nu_out), _ptr(d_g), _ptr(d_mu), _ptr(d_nu), _ptr(d_params),
+                               _ptr(d_hp), _ptr(d_hp_leaf), wp, wb, _stream(stream)))
+
+
+def opt_rmsprop_fwd_ex(tree, hp, ext, state_dtype, compute, g, nu, params, updates, nu_out,
+                       params_out=None, stream=None):
+    _check(lib.opt_rmsprop_fwd_ex(ctypes.byref(tree.c), ctypes.byref(_hp(opt_rmsprop_hp, hp)),
+                                  ctypes.byref(ext), int(state_dtype), int(compute), _ptr(g),
+                                  _ptr(nu), _ptr(params), _ptr(updates), _ptr(nu_out),
+                                  _ptr(params_out), _stream(stream)))
+
+
+def opt_rmsprop_bwd_ex(tree, hp, ext, state_dtype, compute, g, nu, params, d_updates, d_nu_out,
+                       d_g, d_nu, d_params, d_hp=None, d_hp_leaf=None, workspace=None,
+                       stream=None):
+    wp, wb = _ws(workspace)
+    _check(lib.opt_rmsprop_bwd_ex(ctypes.byref(tree.c), ctypes.byref(_hp(opt_rmsprop_hp, hp)),
+                                  ctypes.byref(ext), int(state_dtype), int(compute), _ptr(g),
+                                  _ptr(nu), _ptr(params), _ptr(d_updates), _ptr(d_nu_out),
+                                  _ptr(d_g), _ptr(d_nu), _ptr(d_params), _ptr(d_hp),
+                                  _ptr(d_hp_leaf), wp, wb, _stream(stream)))
+
+
+def opt_sgd_fwd_ex(tree, hp, ext, state_dtype, compute, g, mom, params, updates, mom_out,
+                   params_out=None, stream=None):
+    _check(lib.opt_sgd_fwd_ex(ctypes.byref(tree.c), ctypes.byref(_hp(opt_sgd_hp, hp)),
+                              ctypes.byref(ext), int(state_dtype), int(compute), _ptr(g),
+                              _ptr(mom), _ptr(params), _ptr(updates), _ptr(mom_out),
+                              _ptr(params_out), _stream(stream)))
+
+
+def opt_sgd_bwd_ex(tree, hp, ext, state_dtype, compute, g, mom, params, d_updates, d_mom_out,
+                   d_g, d_mom, d_params, d_hp=None, d_hp_leaf=None, workspace=None, stream=None):
+    wp, wb = _ws(workspace)
+    _check(lib.opt_sgd_bwd_ex(ctypes.byref(tree.c), ctypes.byref(_hp(opt_sgd_hp, hp)),
+                              ctypes.byref(ext), int(state_dtype), int(compute), _ptr(g),
+                              _ptr(mom), _ptr(params), _ptr(d_updates), _ptr(d_mom_out),
+                              _ptr(d_g), _ptr(d_mom), _ptr(d_params), _ptr(d_hp),
+                              _ptr(d_hp_leaf), wp, wb, _stream(stream)))

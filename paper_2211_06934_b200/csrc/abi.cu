@@ -27,7 +27,7 @@ std::atomic<int64_t> g_launches{0};
 
 constexpr int64_t kMaxGrid = 4096;       // upper bound on blocks of any launch
 constexpr size_t kCounterBytes = 256;    // workspace head (ticket counter)
-constexpr int kNhMax = 4;
+constexpr int kNhMax = 5;
 constexpr int kDefaultCompute = OPT_COMPUTE_F32;
 
 int fail(int code, const char* fmt, ...) {
@@ -181,37 +181,41 @@ int launched(cudaStream_t) {
 }
 
 // Workspace and reduction plumbing shared by the three backward ops.
+// Reduction / leaf-mode plumbing of one launch. Leaf mode (leaf-aligned
+// tiles over the shared-memory offset table) is used when per-leaf outputs
+// or per-leaf learning rates are requested.
 struct Reduce {
   double* d_hp;
   double* d_hp_leaf;
+  const float* lr_leaf;
   bool leaf;
   int64_t n_tiles;
   double* partials;
   unsigned int* counter;
 };
 
-int setup_reduce(const opt_tree* t, int nh, double* d_hp, double* d_hp_leaf, void* ws,
-                 size_t ws_bytes, Reduce* r) {
+int setup_reduce(const opt_tree* t, double* d_hp, double* d_hp_leaf, const float* lr_leaf,
+                 void* ws, size_t ws_bytes, Reduce* r) {
   r->d_hp = d_hp;
   r->d_hp_leaf = d_hp_leaf;
-  r->leaf = d_hp_leaf != nullptr;
+  r->lr_leaf = lr_leaf;
+  r->leaf = d_hp_leaf != nullptr || lr_leaf != nullptr;
   r->n_tiles = 0;
   r->partials = nullptr;
   r->counter = nullptr;
-  if (!d_hp && !d_hp_leaf) return OPT_OK;
   if (r->leaf) {
-    if (t->n_leaves < 1) return fail(OPT_EINVAL, "d_hp_leaf needs n_leaves >= 1");
+    if (t->n_leaves < 1) return fail(OPT_EINVAL, "per-leaf outputs/lr need n_leaves >= 1");
     if (t->n_leaves > kMaxLeafSmem)
-      return fail(OPT_EINVAL, "d_hp_leaf supports at most %d leaves (got %lld)", kMaxLeafSmem,
-                  (long long)t->n_leaves);
-    if (!t->d_offsets) return fail(OPT_EINVAL, "d_hp_leaf needs tree->d_offsets");
-    r->n_tiles = count_tiles(t);
+      return fail(OPT_EINVAL, "per-leaf outputs/lr support at most %d leaves (got %lld)",
+                  kMaxLeafSmem, (long long)t->n_leaves);
+    if (!t->d_offsets) return fail(OPT_EINVAL, "per-leaf outputs/lr need tree->d_offsets");
+        r->n_tiles = count_tiles(t);
   }
+  if (!d_hp && !d_hp_leaf) return OPT_OK;
   size_t need = opt_workspace_bytes(t, r->leaf ? 1 : 0);
   if (!ws || ws_bytes < need)
     return fail(OPT_EWORKSPACE, "workspace %p of %zu bytes; need %zu", ws, ws_bytes, need);
   if (reinterpret_cast<uintptr_t>(ws) & 15u) return fail(OPT_EALIGN, "workspace not 16-byte aligned");
-  (void)nh;
   r->counter = static_cast<unsigned int*>(ws);
   r->partials = reinterpret_cast<double*>(static_cast<char*>(ws) + kCounterBytes);
   return OPT_OK;
@@ -286,33 +290,26 @@ constexpr int minb_bwd() {
   return sizeof(typename Op::CT) == 8 ? (DOPT_MINB_BWD < 2 ? DOPT_MINB_BWD : 2) : DOPT_MINB_BWD;
 }
 
-// Launch an op (forward: no reduction) with state type ST.
-template <class Op, class ST, int U>
-int launch_fwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, cudaStream_t s) {
-  if (DOPT_TMA_FWD) return launch_tma<Op, ST>(op, a, s);
-  auto k = step_uniform<Op, ST, U, DOPT_MINB_FWD>;
-  int grid = 0;
-  int64_t work = ((a.numel >> 2) + kBlock - 1) / kBlock + 1;
-  int rc = grid_for(k, work, 0, &grid);
-  if (rc) return rc;
-  cudaError_t le = launch_k(k, grid, kBlock, 0, s, op, a);
-  if (le != cudaSuccess) return fail(OPT_ECUDA, "launch: %s", cudaGetErrorString(le));
-  return launched(s);
+template <class Op, bool kBwd>
+constexpr int minb_for() {
+  return kBwd ? minb_bwd<Op>() : DOPT_MINB_FWD;
 }
 
-template <class Op, class ST, int U>
-int launch_bwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r,
-               const opt_tree* t, cudaStream_t s) {
+// Launch one op: leaf mode, TMA variant or the uniform streaming kernel.
+template <class Op, class ST, int U, int MINB, bool kTma>
+int launch(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r, const opt_tree* t,
+           cudaStream_t s) {
   a.d_hp = r.d_hp;
   a.d_hp_leaf = r.d_hp_leaf;
   a.partials = r.partials;
   a.counter = r.counter;
+  a.lr_leaf = r.lr_leaf;
   a.want_hp = (r.d_hp || r.d_hp_leaf) ? 1 : 0;
   if (r.leaf) {
     a.offsets = t->d_offsets;
     a.n_leaves = t->n_leaves;
     a.n_tiles = r.n_tiles;
-    auto k = step_leaf<Op, ST, U, minb_bwd<Op>()>;
+    auto k = step_leaf<Op, ST, U, MINB>;
     size_t smem = sizeof(int64_t) * 2 * (size_t)(t->n_leaves + 1);
     static const cudaError_t attr = cudaFuncSetAttribute(
         k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(int64_t) * 2 * (kMaxLeafSmem + 1)));
@@ -324,8 +321,8 @@ int launch_bwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r,
     if (le != cudaSuccess) return fail(OPT_ECUDA, "launch: %s", cudaGetErrorString(le));
     return launched(s);
   }
-  if (DOPT_TMA_BWD) return launch_tma<Op, ST>(op, a, s);
-  auto k = step_uniform<Op, ST, U, minb_bwd<Op>()>;
+  if (kTma) return launch_tma<Op, ST>(op, a, s);
+  auto k = step_uniform<Op, ST, U, MINB>;
   int grid = 0;
   int64_t work = ((a.numel >> 2) + kBlock - 1) / kBlock + 1;
   int rc = grid_for(k, work, 0, &grid);
@@ -338,26 +335,21 @@ int launch_bwd(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r,
 // Dispatch on (state dtype, compute precision).
 template <template <class> class OpT, bool kBwd, class Fill>
 int dispatch(int state_dtype, int ct, StepArgs<OpT<float>::NIN, OpT<float>::NOUT>& a,
-             const Reduce* r, const opt_tree* t, cudaStream_t s, Fill fill) {
+             const Reduce& r, const opt_tree* t, cudaStream_t s, Fill fill) {
   constexpr int U = kBwd ? DOPT_U_BWD : DOPT_U_FWD;
+  constexpr bool TMA = kBwd ? (DOPT_TMA_BWD != 0) : (DOPT_TMA_FWD != 0);
   if (ct == OPT_COMPUTE_F64) {
     OpT<double> op;
     fill(op);
-    if (state_dtype == OPT_BF16) {
-      if constexpr (kBwd) return launch_bwd<OpT<double>, bf16, U>(op, a, *r, t, s);
-      else return launch_fwd<OpT<double>, bf16, U>(op, a, s);
-    }
-    if constexpr (kBwd) return launch_bwd<OpT<double>, float, U>(op, a, *r, t, s);
-    else return launch_fwd<OpT<double>, float, U>(op, a, s);
+    constexpr int MB = minb_for<OpT<double>, kBwd>();
+    if (state_dtype == OPT_BF16) return launch<OpT<double>, bf16, U, MB, TMA>(op, a, r, t, s);
+    return launch<OpT<double>, float, U, MB, TMA>(op, a, r, t, s);
   }
   OpT<float> op;
   fill(op);
-  if (state_dtype == OPT_BF16) {
-    if constexpr (kBwd) return launch_bwd<OpT<float>, bf16, U>(op, a, *r, t, s);
-    else return launch_fwd<OpT<float>, bf16, U>(op, a, s);
-  }
-  if constexpr (kBwd) return launch_bwd<OpT<float>, float, U>(op, a, *r, t, s);
-  else return launch_fwd<OpT<float>, float, U>(op, a, s);
+  constexpr int MB = minb_for<OpT<float>, kBwd>();
+  if (state_dtype == OPT_BF16) return launch<OpT<float>, bf16, U, MB, TMA>(op, a, r, t, s);
+  return launch<OpT<float>, float, U, MB, TMA>(op, a, r, t, s);
 }
 
 // b^t by repeated squaring in double (exact integer power).
@@ -404,6 +396,81 @@ int check_sgd(const opt_sgd_hp* hp) {
     if (rc_) return rc_;      \
   } while (0)
 
+
+// Per-step constants of each op (row a2): computed in double, rounded once
+// to the compute type CT (reading Z8).
+template <class Op>
+void fill_adam_fwd(Op& op, int64_t step, const opt_adam_hp* hp) {
+  typedef typename Op::CT CT;
+  const double b1 = hp->b1, b2 = hp->b2;
+  const double bc1 = 1.0 - ipow(b1, step), bc2 = 1.0 - ipow(b2, step);
+  op.b1 = (CT)b1; op.om1 = (CT)(1.0 - b1); op.b2 = (CT)b2; op.om2 = (CT)(1.0 - b2);
+  op.ibc1 = (CT)(1.0 / bc1); op.ibc2 = (CT)(1.0 / bc2); op.lr = (CT)hp->lr;
+  op.eps = (CT)hp->eps; op.eps_root = (CT)hp->eps_root;
+}
+
+template <class Op>
+void fill_adam_bwd(Op& op, int64_t step, const opt_adam_hp* hp) {
+  typedef typename Op::CT CT;
+  const double b1 = hp->b1, b2 = hp->b2, t = (double)step;
+  const double p1 = ipow(b1, step), p2 = ipow(b2, step);
+  const double p1m = ipow(b1, step - 1), p2m = ipow(b2, step - 1);
+  const double bc1 = 1.0 - p1, bc2 = 1.0 - p2;
+  // d mhat/d b1 = m K1 - g K2 ; d vhat/d b2 = v K3 - g^2 K4   (DESIGN.md §3)
+  const double K1 = (1.0 - p1 + t * p1) / (bc1 * bc1);
+  const double K2 = (1.0 - p1 - t * p1m * (1.0 - b1)) / (bc1 * bc1);
+  const double K3 = (1.0 - p2 + t * p2) / (bc2 * bc2);
+  const double K4 = (1.0 - p2 - t * p2m * (1.0 - b2)) / (bc2 * bc2);
+  op.b1 = (CT)b1; op.om1 = (CT)(1.0 - b1); op.b2 = (CT)b2; op.two_om2 = (CT)(2.0 * (1.0 - b2));
+  op.A = (CT)((1.0 - b1) / bc1); op.C = (CT)((1.0 - b2) / bc2);
+  op.b1ibc1 = (CT)(b1 / bc1); op.b2ibc2 = (CT)(b2 / bc2);
+  op.eps_root = (CT)hp->eps_root; op.lr = (CT)hp->lr; op.eps = (CT)hp->eps;
+  op.Aeps = (CT)((1.0 - b1) / bc1 * hp->eps);
+  op.kM = (CT)(b1 * hp->lr / bc1); op.kV = (CT)(0.5 * b2 * hp->lr / bc2);
+  op.hlr = (CT)(0.5 * hp->lr);
+  op.kM0 = (CT)(b1 / bc1); op.kV0 = (CT)(0.5 * b2 / bc2);
+  op.K1 = (CT)K1; op.K2 = (CT)K2; op.K3 = (CT)K3; op.K4 = (CT)K4;
+}
+
+template <class Op>
+void fill_rms_fwd(Op& op, const opt_rmsprop_hp* hp) {
+  typedef typename Op::CT CT;
+  op.alpha = (CT)hp->alpha; op.oma = (CT)(1.0 - hp->alpha); op.lr = (CT)hp->lr;
+  op.eps = (CT)hp->eps;
+}
+
+template <class Op>
+void fill_rms_bwd(Op& op, const opt_rmsprop_hp* hp) {
+  typedef typename Op::CT CT;
+  op.alpha = (CT)hp->alpha; op.oma = (CT)(1.0 - hp->alpha);
+  op.two_oma = (CT)(2.0 * (1.0 - hp->alpha)); op.lr = (CT)hp->lr; op.eps = (CT)hp->eps;
+  op.hlr = (CT)(0.5 * hp->lr);
+}
+
+template <class Op>
+void fill_sgd(Op& op, const opt_sgd_hp* hp) {
+  typedef typename Op::CT CT;
+  op.lr = (CT)hp->lr; op.mu = (CT)hp->momentum; op.nesterov = hp->nesterov ? 1 : 0;
+}
+
+template <class Op>
+void fill_ext(Op& op, const opt_ext* e, bool adam) {
+  typedef typename Op::CT CT;
+  op.wd = (CT)e->weight_decay;
+  op.decoupled = (adam && e->decoupled) ? 1 : 0;
+  op.maximize = e->maximize ? 1 : 0;
+}
+
+int check_ext(const opt_ext* e, const float* params, const opt_tree* t) {
+  if (!e) return fail(OPT_EINVAL, "ext is NULL");
+  if (!(finite(e->weight_decay) && e->weight_decay >= 0))
+    return fail(OPT_EINVAL, "weight_decay = %g < 0", e->weight_decay);
+  if (e->weight_decay != 0.0 && !params && t->numel > 0)
+    return fail(OPT_EINVAL, "weight_decay != 0 needs params");
+  if (misaligned(e->lr_leaf)) return fail(OPT_EALIGN, "lr_leaf not 16-byte aligned");
+  return OPT_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -432,20 +499,14 @@ int opt_adam_fwd(const opt_tree* tree, int64_t step, const opt_adam_hp* hp, int 
   TRY(check_align({g, mu, nu, updates, mu_out, nu_out, params, params_out}));
   if (tree->numel == 0) return OPT_OK;
   if (!g) return fail(OPT_EINVAL, "g is NULL");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const double b1 = hp->b1, b2 = hp->b2;
-  const double bc1 = 1.0 - ipow(b1, step), bc2 = 1.0 - ipow(b2, step);
   StepArgs<4, 4> a{};
   a.in[0] = g; a.in[1] = mu; a.in[2] = nu; a.in[3] = (params && params_out) ? params : nullptr;
   a.out[0] = updates; a.out[1] = mu_out; a.out[2] = nu_out;
   a.out[3] = (params && params_out) ? params_out : nullptr;
   a.numel = tree->numel;
-  return dispatch<AdamFwd, false>(state_dtype, ct, a, nullptr, tree, s, [&](auto& op) {
-    typedef typename std::remove_reference<decltype(op)>::type::CT CT;
-    op.b1 = (CT)b1; op.om1 = (CT)(1.0 - b1); op.b2 = (CT)b2; op.om2 = (CT)(1.0 - b2);
-    op.ibc1 = (CT)(1.0 / bc1); op.ibc2 = (CT)(1.0 / bc2); op.lr = (CT)hp->lr;
-    op.eps = (CT)hp->eps; op.eps_root = (CT)hp->eps_root;
-  });
+  return dispatch<AdamFwd, false>(state_dtype, ct, a, Reduce{}, tree,
+                                  static_cast<cudaStream_t>(stream),
+                                  [&](auto& op) { fill_adam_fwd(op, step, hp); });
 }
 
 int opt_adam_bwd(const opt_tree* tree, int64_t step, const opt_adam_hp* hp, int state_dtype,
@@ -464,32 +525,71 @@ int opt_adam_bwd(const opt_tree* tree, int64_t step, const opt_adam_hp* hp, int 
   if (tree->numel == 0) return zero_outputs(tree, 4, d_hp, d_hp_leaf, s);
   if (!g) return fail(OPT_EINVAL, "g is NULL");
   Reduce r;
-  TRY(setup_reduce(tree, 4, d_hp, d_hp_leaf, workspace, workspace_bytes, &r));
-  // Per-step constants in double (row a2), rounded once to the compute type.
-  const double b1 = hp->b1, b2 = hp->b2, t = (double)step;
-  const double p1 = ipow(b1, step), p2 = ipow(b2, step);
-  const double p1m = ipow(b1, step - 1), p2m = ipow(b2, step - 1);
-  const double bc1 = 1.0 - p1, bc2 = 1.0 - p2;
-  // d mhat/d b1 = m K1 - g K2 ; d vhat/d b2 = v K3 - g^2 K4   (DESIGN.md)
-  const double K1 = (1.0 - p1 + t * p1) / (bc1 * bc1);
-  const double K2 = (1.0 - p1 - t * p1m * (1.0 - b1)) / (bc1 * bc1);
-  const double K3 = (1.0 - p2 + t * p2) / (bc2 * bc2);
-  const double K4 = (1.0 - p2 - t * p2m * (1.0 - b2)) / (bc2 * bc2);
+  TRY(setup_reduce(tree, d_hp, d_hp_leaf, nullptr, workspace, workspace_bytes, &r));
   StepArgs<6, 3> a{};
   a.in[0] = g; a.in[1] = mu; a.in[2] = nu; a.in[3] = d_updates; a.in[4] = d_mu_out;
   a.in[5] = d_nu_out;
   a.out[0] = d_g; a.out[1] = d_mu; a.out[2] = d_nu;
   a.numel = tree->numel;
-  return dispatch<AdamBwd, true>(state_dtype, ct, a, &r, tree, s, [&](auto& op) {
-    typedef typename std::remove_reference<decltype(op)>::type::CT CT;
-    op.b1 = (CT)b1; op.om1 = (CT)(1.0 - b1); op.b2 = (CT)b2; op.two_om2 = (CT)(2.0 * (1.0 - b2));
-    op.A = (CT)((1.0 - b1) / bc1); op.C = (CT)((1.0 - b2) / bc2);
-    op.b1ibc1 = (CT)(b1 / bc1); op.b2ibc2 = (CT)(b2 / bc2);
-    op.eps_root = (CT)hp->eps_root; op.lr = (CT)hp->lr; op.eps = (CT)hp->eps;
-    op.Aeps = (CT)((1.0 - b1) / bc1 * hp->eps);
-    op.kM = (CT)(b1 * hp->lr / bc1); op.kV = (CT)(0.5 * b2 * hp->lr / bc2);
-    op.hlr = (CT)(0.5 * hp->lr);
-    op.K1 = (CT)K1; op.K2 = (CT)K2; op.K3 = (CT)K3; op.K4 = (CT)K4;
+  return dispatch<AdamBwd, true>(state_dtype, ct, a, r, tree, s,
+                                 [&](auto& op) { fill_adam_bwd(op, step, hp); });
+}
+
+int opt_adam_fwd_ex(const opt_tree* tree, int64_t step, const opt_adam_hp* hp,
+                    const opt_ext* ext, int state_dtype, int compute, const float* g,
+                    const void* mu, const void* nu, const float* params, float* updates,
+                    void* mu_out, void* nu_out, float* params_out, void* stream) {
+  g_err.clear();
+  int ct = 0;
+  TRY(check_tree(tree));
+  TRY(check_adam(step, hp));
+  TRY(check_ext(ext, params, tree));
+  TRY(check_state_dtype(state_dtype));
+  TRY(resolve_compute(compute, &ct));
+  TRY(check_align({g, mu, nu, params, updates, mu_out, nu_out, params_out}));
+  if (tree->numel == 0) return OPT_OK;
+  if (!g) return fail(OPT_EINVAL, "g is NULL");
+  Reduce r;
+  TRY(setup_reduce(tree, nullptr, nullptr, ext->lr_leaf, nullptr, 0, &r));
+  StepArgs<4, 4> a{};
+  a.in[0] = g; a.in[1] = mu; a.in[2] = nu; a.in[3] = params;
+  a.out[0] = updates; a.out[1] = mu_out; a.out[2] = nu_out;
+  a.out[3] = params ? params_out : nullptr;
+  a.numel = tree->numel;
+  return dispatch<AdamFwdEx, false>(state_dtype, ct, a, r, tree, static_cast<cudaStream_t>(stream),
+                                    [&](auto& op) {
+                                      fill_adam_fwd(op.base, step, hp);
+                                      fill_ext(op, ext, true);
+                                    });
+}
+
+int opt_adam_bwd_ex(const opt_tree* tree, int64_t step, const opt_adam_hp* hp,
+                    const opt_ext* ext, int state_dtype, int compute, const float* g,
+                    const void* mu, const void* nu, const float* params, const float* d_updates,
+                    const float* d_mu_out, const float* d_nu_out, float* d_g, float* d_mu,
+                    float* d_nu, float* d_params, double* d_hp, double* d_hp_leaf,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  int ct = 0;
+  TRY(check_tree(tree));
+  TRY(check_adam(step, hp));
+  TRY(check_ext(ext, params, tree));
+  TRY(check_state_dtype(state_dtype));
+  TRY(resolve_compute(compute, &ct));
+  TRY(check_align({g, mu, nu, params, d_updates, d_mu_out, d_nu_out, d_g, d_mu, d_nu, d_params}));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (tree->numel == 0) return zero_outputs(tree, 5, d_hp, d_hp_leaf, s);
+  if (!g) return fail(OPT_EINVAL, "g is NULL");
+  Reduce r;
+  TRY(setup_reduce(tree, d_hp, d_hp_leaf, ext->lr_leaf, workspace, workspace_bytes, &r));
+  StepArgs<7, 4> a{};
+  a.in[0] = g; a.in[1] = mu; a.in[2] = nu; a.in[3] = params; a.in[4] = d_updates;
+  a.in[5] = d_mu_out; a.in[6] = d_nu_out;
+  a.out[0] = d_g; a.out[1] = d_mu; a.out[2] = d_nu; a.out[3] = d_params;
+  a.numel = tree->numel;
+  return dispatch<AdamBwdEx, true>(state_dtype, ct, a, r, tree, s, [&](auto& op) {
+    fill_adam_bwd(op.base, step, hp);
+    fill_ext(op, ext, true);
   });
 }
 
@@ -506,16 +606,13 @@ int opt_rmsprop_fwd(const opt_tree* tree, const opt_rmsprop_hp* hp, int state_dt
   TRY(check_align({g, nu, updates, nu_out, params, params_out}));
   if (tree->numel == 0) return OPT_OK;
   if (!g) return fail(OPT_EINVAL, "g is NULL");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   StepArgs<3, 3> a{};
   a.in[0] = g; a.in[1] = nu; a.in[2] = (params && params_out) ? params : nullptr;
   a.out[0] = updates; a.out[1] = nu_out; a.out[2] = (params && params_out) ? params_out : nullptr;
   a.numel = tree->numel;
-  return dispatch<RmsFwd, false>(state_dtype, ct, a, nullptr, tree, s, [&](auto& op) {
-    typedef typename std::remove_reference<decltype(op)>::type::CT CT;
-    op.alpha = (CT)hp->alpha; op.oma = (CT)(1.0 - hp->alpha); op.lr = (CT)hp->lr;
-    op.eps = (CT)hp->eps;
-  });
+  return dispatch<RmsFwd, false>(state_dtype, ct, a, Reduce{}, tree,
+                                 static_cast<cudaStream_t>(stream),
+                                 [&](auto& op) { fill_rms_fwd(op, hp); });
 }
 
 int opt_rmsprop_bwd(const opt_tree* tree, const opt_rmsprop_hp* hp, int state_dtype,
@@ -533,16 +630,67 @@ int opt_rmsprop_bwd(const opt_tree* tree, const opt_rmsprop_hp* hp, int state_dt
   if (tree->numel == 0) return zero_outputs(tree, 3, d_hp, d_hp_leaf, s);
   if (!g) return fail(OPT_EINVAL, "g is NULL");
   Reduce r;
-  TRY(setup_reduce(tree, 3, d_hp, d_hp_leaf, workspace, workspace_bytes, &r));
+  TRY(setup_reduce(tree, d_hp, d_hp_leaf, nullptr, workspace, workspace_bytes, &r));
   StepArgs<4, 2> a{};
   a.in[0] = g; a.in[1] = nu; a.in[2] = d_updates; a.in[3] = d_nu_out;
   a.out[0] = d_g; a.out[1] = d_nu;
   a.numel = tree->numel;
-  return dispatch<RmsBwd, true>(state_dtype, ct, a, &r, tree, s, [&](auto& op) {
-    typedef typename std::remove_reference<decltype(op)>::type::CT CT;
-    op.alpha = (CT)hp->alpha; op.oma = (CT)(1.0 - hp->alpha);
-    op.two_oma = (CT)(2.0 * (1.0 - hp->alpha)); op.lr = (CT)hp->lr; op.eps = (CT)hp->eps;
-    op.hlr = (CT)(0.5 * hp->lr);
+  return dispatch<RmsBwd, true>(state_dtype, ct, a, r, tree, s,
+                                [&](auto& op) { fill_rms_bwd(op, hp); });
+}
+
+int opt_rmsprop_fwd_ex(const opt_tree* tree, const opt_rmsprop_hp* hp, const opt_ext* ext,
+                       int state_dtype, int compute, const float* g, const void* nu,
+                       const float* params, float* updates, void* nu_out, float* params_out,
+                       void* stream) {
+  g_err.clear();
+  int ct = 0;
+  TRY(check_tree(tree));
+  TRY(check_rms(hp));
+  TRY(check_ext(ext, params, tree));
+  TRY(check_state_dtype(state_dtype));
+  TRY(resolve_compute(compute, &ct));
+  TRY(check_align({g, nu, params, updates, nu_out, params_out}));
+  if (tree->numel == 0) return OPT_OK;
+  if (!g) return fail(OPT_EINVAL, "g is NULL");
+  Reduce r;
+  TRY(setup_reduce(tree, nullptr, nullptr, ext->lr_leaf, nullptr, 0, &r));
+  StepArgs<3, 3> a{};
+  a.in[0] = g; a.in[1] = nu; a.in[2] = params;
+  a.out[0] = updates; a.out[1] = nu_out; a.out[2] = params ? params_out : nullptr;
+  a.numel = tree->numel;
+  return dispatch<RmsFwdEx, false>(state_dtype, ct, a, r, tree, static_cast<cudaStream_t>(stream),
+                                   [&](auto& op) {
+                                     fill_rms_fwd(op.base, hp);
+                                     fill_ext(op, ext, false);
+                                   });
+}
+
+int opt_rmsprop_bwd_ex(const opt_tree* tree, const opt_rmsprop_hp* hp, const opt_ext* ext,
+                       int state_dtype, int compute, const float* g, const void* nu,
+                       const float* params, const float* d_updates, const float* d_nu_out,
+                       float* d_g, float* d_nu, float* d_params, double* d_hp, double* d_hp_leaf,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  int ct = 0;
+  TRY(check_tree(tree));
+  TRY(check_rms(hp));
+  TRY(check_ext(ext, params, tree));
+  TRY(check_state_dtype(state_dtype));
+  TRY(resolve_compute(compute, &ct));
+  TRY(check_align({g, nu, params, d_updates, d_nu_out, d_g, d_nu, d_params}));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (tree->numel == 0) return zero_outputs(tree, 4, d_hp, d_hp_leaf, s);
+  if (!g) return fail(OPT_EINVAL, "g is NULL");
+  Reduce r;
+  TRY(setup_reduce(tree, d_hp, d_hp_leaf, ext->lr_leaf, workspace, workspace_bytes, &r));
+  StepArgs<5, 3> a{};
+  a.in[0] = g; a.in[1] = nu; a.in[2] = params; a.in[3] = d_updates; a.in[4] = d_nu_out;
+  a.out[0] = d_g; a.out[1] = d_nu; a.out[2] = d_params;
+  a.numel = tree->numel;
+  return dispatch<RmsBwdEx, true>(state_dtype, ct, a, r, tree, s, [&](auto& op) {
+    fill_rms_bwd(op.base, hp);
+    fill_ext(op, ext, false);
   });
 }
 
@@ -559,15 +707,13 @@ int opt_sgd_fwd(const opt_tree* tree, const opt_sgd_hp* hp, int state_dtype, int
   TRY(check_align({g, mom, updates, mom_out, params, params_out}));
   if (tree->numel == 0) return OPT_OK;
   if (!g) return fail(OPT_EINVAL, "g is NULL");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   StepArgs<3, 3> a{};
   a.in[0] = g; a.in[1] = mom; a.in[2] = (params && params_out) ? params : nullptr;
   a.out[0] = updates; a.out[1] = mom_out; a.out[2] = (params && params_out) ? params_out : nullptr;
   a.numel = tree->numel;
-  return dispatch<SgdFwd, false>(state_dtype, ct, a, nullptr, tree, s, [&](auto& op) {
-    typedef typename std::remove_reference<decltype(op)>::type::CT CT;
-    op.lr = (CT)hp->lr; op.mu = (CT)hp->momentum; op.nesterov = hp->nesterov ? 1 : 0;
-  });
+  return dispatch<SgdFwd, false>(state_dtype, ct, a, Reduce{}, tree,
+                                 static_cast<cudaStream_t>(stream),
+                                 [&](auto& op) { fill_sgd(op, hp); });
 }
 
 int opt_sgd_bwd(const opt_tree* tree, const opt_sgd_hp* hp, int state_dtype, int compute,
@@ -585,14 +731,66 @@ int opt_sgd_bwd(const opt_tree* tree, const opt_sgd_hp* hp, int state_dtype, int
   if (tree->numel == 0) return zero_outputs(tree, 2, d_hp, d_hp_leaf, s);
   if (!g) return fail(OPT_EINVAL, "g is NULL");
   Reduce r;
-  TRY(setup_reduce(tree, 2, d_hp, d_hp_leaf, workspace, workspace_bytes, &r));
+  TRY(setup_reduce(tree, d_hp, d_hp_leaf, nullptr, workspace, workspace_bytes, &r));
   StepArgs<4, 2> a{};
   a.in[0] = g; a.in[1] = mom; a.in[2] = d_updates; a.in[3] = d_mom_out;
   a.out[0] = d_g; a.out[1] = d_mom;
   a.numel = tree->numel;
-  return dispatch<SgdBwd, true>(state_dtype, ct, a, &r, tree, s, [&](auto& op) {
-    typedef typename std::remove_reference<decltype(op)>::type::CT CT;
-    op.lr = (CT)hp->lr; op.mu = (CT)hp->momentum; op.nesterov = hp->nesterov ? 1 : 0;
+  return dispatch<SgdBwd, true>(state_dtype, ct, a, r, tree, s, [&](auto& op) { fill_sgd(op, hp); });
+}
+
+int opt_sgd_fwd_ex(const opt_tree* tree, const opt_sgd_hp* hp, const opt_ext* ext,
+                   int state_dtype, int compute, const float* g, const void* mom,
+                   const float* params, float* updates, void* mom_out, float* params_out,
+                   void* stream) {
+  g_err.clear();
+  int ct = 0;
+  TRY(check_tree(tree));
+  TRY(check_sgd(hp));
+  TRY(check_ext(ext, params, tree));
+  TRY(check_state_dtype(state_dtype));
+  TRY(resolve_compute(compute, &ct));
+  TRY(check_align({g, mom, params, updates, mom_out, params_out}));
+  if (tree->numel == 0) return OPT_OK;
+  if (!g) return fail(OPT_EINVAL, "g is NULL");
+  Reduce r;
+  TRY(setup_reduce(tree, nullptr, nullptr, ext->lr_leaf, nullptr, 0, &r));
+  StepArgs<3, 3> a{};
+  a.in[0] = g; a.in[1] = mom; a.in[2] = params;
+  a.out[0] = updates; a.out[1] = mom_out; a.out[2] = params ? params_out : nullptr;
+  a.numel = tree->numel;
+  return dispatch<SgdFwdEx, false>(state_dtype, ct, a, r, tree, static_cast<cudaStream_t>(stream),
+                                   [&](auto& op) {
+                                     fill_sgd(op.base, hp);
+                                     fill_ext(op, ext, false);
+                                   });
+}
+
+int opt_sgd_bwd_ex(const opt_tree* tree, const opt_sgd_hp* hp, const opt_ext* ext,
+                   int state_dtype, int compute, const float* g, const void* mom,
+                   const float* params, const float* d_updates, const float* d_mom_out,
+                   float* d_g, float* d_mom, float* d_params, double* d_hp, double* d_hp_leaf,
+                   void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  int ct = 0;
+  TRY(check_tree(tree));
+  TRY(check_sgd(hp));
+  TRY(check_ext(ext, params, tree));
+  TRY(check_state_dtype(state_dtype));
+  TRY(resolve_compute(compute, &ct));
+  TRY(check_align({g, mom, params, d_updates, d_mom_out, d_g, d_mom, d_params}));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (tree->numel == 0) return zero_outputs(tree, 3, d_hp, d_hp_leaf, s);
+  if (!g) return fail(OPT_EINVAL, "g is NULL");
+  Reduce r;
+  TRY(setup_reduce(tree, d_hp, d_hp_leaf, ext->lr_leaf, workspace, workspace_bytes, &r));
+  StepArgs<5, 3> a{};
+  a.in[0] = g; a.in[1] = mom; a.in[2] = params; a.in[3] = d_updates; a.in[4] = d_mom_out;
+  a.out[0] = d_g; a.out[1] = d_mom; a.out[2] = d_params;
+  a.numel = tree->numel;
+  return dispatch<SgdBwdEx, true>(state_dtype, ct, a, r, tree, s, [&](auto& op) {
+    fill_sgd(op.base, hp);
+    fill_ext(op, ext, false);
   });
 }
 

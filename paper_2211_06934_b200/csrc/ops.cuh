@@ -42,6 +42,10 @@ __device__ __forceinline__ float ct_div(float a, float b) { return __fdividef(a,
 __device__ __forceinline__ float rsqrt_or_zero(float x) { return x > 0.f ? rsqrtf(x) : 0.f; }
 #endif
 
+// Every op exposes apply() on compute-type scalars (so the variants below
+// can feed it a transformed gradient) and set_lr() (per-leaf learning rates:
+// the leaf kernel re-targets a copy of the op once per tile).
+
 // ------------------------------------------------------------------ Adam
 template <class CT_>
 struct AdamFwd {
@@ -51,18 +55,19 @@ struct AdamFwd {
   __host__ __device__ static constexpr bool out_state(int i) { return i == 1 || i == 2; }
   CT b1, om1, b2, om2, ibc1, ibc2, lr, eps, eps_root;
 
-  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT*,
-                                             bool) const {
-    const CT g = x[0], m = x[1], v = x[2];
-    const CT m1 = b1 * m + om1 * g;
-    const CT v1 = b2 * v + om2 * (g * g);
+  __device__ __forceinline__ void set_lr(CT l) { lr = l; }
+  // (u, m', v') of gradient g
+  __device__ __forceinline__ void apply(CT g, CT m, CT v, CT& u, CT& m1, CT& v1) const {
+    m1 = b1 * m + om1 * g;
+    v1 = b2 * v + om2 * (g * g);
     const CT s = ct_sqrt(v1 * ibc2 + eps_root);
     const CT d = s + eps;
-    const CT u = d == CT(0) ? CT(0) : ct_div(-lr * (m1 * ibc1), d);
-    y[0] = u;
-    y[1] = m1;
-    y[2] = v1;
-    y[3] = CT(x[3]) + u;
+    u = d == CT(0) ? CT(0) : ct_div(-lr * (m1 * ibc1), d);
+  }
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT*,
+                                             bool) const {
+    apply(x[0], x[1], x[2], y[0], y[1], y[2]);
+    y[3] = CT(x[3]) + y[0];
   }
 };
 
@@ -73,13 +78,20 @@ struct AdamBwd {
   __host__ __device__ static constexpr bool in_state(int i) { return i == 1 || i == 2; }
   __host__ __device__ static constexpr bool out_state(int) { return false; }
   // host-precomputed (abi.cu): A=(1-b1)/bc1, C=(1-b2)/bc2, b1ibc1=b1/bc1,
-  // b2ibc2=b2/bc2, Aeps=A*eps, kM=b1*lr/bc1, kV=b2*lr/(2*bc2), hlr=lr/2
+  // b2ibc2=b2/bc2, Aeps=A*eps, kM0=b1/bc1, kV0=b2/(2*bc2); set_lr derives
+  // kM=kM0*lr, kV=kV0*lr, hlr=lr/2
   CT b1, om1, b2, two_om2, A, C, b1ibc1, b2ibc2, eps_root, lr, eps, Aeps, kM, kV, hlr;
-  CT K1, K2, K3, K4;
+  CT kM0, kV0, K1, K2, K3, K4;
 
-  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT* h,
-                                             bool want_hp) const {
-    const CT g = x[0], m = x[1], v = x[2], du = x[3], dm1 = x[4], dv1 = x[5];
+  __device__ __forceinline__ void set_lr(CT l) {
+    lr = l;
+    kM = kM0 * l;
+    kV = kV0 * l;
+    hlr = CT(0.5) * l;
+  }
+  // dg, dm, dv of gradient g; hyper terms (lr, b1, b2, eps) into h
+  __device__ __forceinline__ void apply(CT g, CT m, CT v, CT du, CT dm1, CT dv1, CT& dg, CT& dm,
+                                        CT& dv, CT* h, bool want_hp) const {
     const CT P = b1ibc1 * m;                 // mhat = A g + P
     const CT Q = b2ibc2 * v + eps_root;      // s^2  = C g^2 + Q
     const CT gg = g * g;
@@ -92,15 +104,19 @@ struct AdamBwd {
     const CT T = R * rd;                     // du/d^2
     const CT U = mhat * T * rs;              // du mhat/(s d^2)
     // dg = (1-b1) dm1 + 2(1-b2) g dv1 - lr du [A eps + (A Q - P C g)/s]/d^2
-    y[0] = om1 * dm1 + two_om2 * g * dv1 - (lr * T) * (Aeps + (A * Q - P * C * g) * rs);
-    y[1] = b1 * dm1 - kM * R;                // b1 (dm1 - du lr/(bc1 d))
-    y[2] = b2 * dv1 + kV * U;                // b2 (dv1 + du lr mhat/(2 s bc2 d^2))
+    dg = om1 * dm1 + two_om2 * g * dv1 - (lr * T) * (Aeps + (A * Q - P * C * g) * rs);
+    dm = b1 * dm1 - kM * R;                  // b1 (dm1 - du lr/(bc1 d))
+    dv = b2 * dv1 + kV * U;                  // b2 (dv1 + du lr mhat/(2 s bc2 d^2))
     if (want_hp) {
-      h[0] -= mhat * R;                                       // lr
-      h[1] += dm1 * (m - g) - (lr * R) * (m * K1 - g * K2);   // b1
+      h[0] -= mhat * R;                                         // lr
+      h[1] += dm1 * (m - g) - (lr * R) * (m * K1 - g * K2);     // b1
       h[2] += dv1 * (v - gg) + (hlr * U) * (v * K3 - gg * K4);  // b2
-      h[3] += lr * (mhat * T);                                // eps
+      h[3] += lr * (mhat * T);                                  // eps
     }
+  }
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT* h,
+                                             bool want_hp) const {
+    apply(x[0], x[1], x[2], x[3], x[4], x[5], y[0], y[1], y[2], h, want_hp);
   }
 };
 
@@ -113,15 +129,16 @@ struct RmsFwd {
   __host__ __device__ static constexpr bool out_state(int i) { return i == 1; }
   CT alpha, oma, lr, eps;
 
+  __device__ __forceinline__ void set_lr(CT l) { lr = l; }
+  __device__ __forceinline__ void apply(CT g, CT v, CT& u, CT& v1) const {
+    v1 = alpha * v + oma * (g * g);
+    const CT d = ct_sqrt(v1) + eps;
+    u = d == CT(0) ? CT(0) : ct_div(-lr * g, d);
+  }
   __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT*,
                                              bool) const {
-    const CT g = x[0], v = x[1];
-    const CT v1 = alpha * v + oma * (g * g);
-    const CT d = ct_sqrt(v1) + eps;
-    const CT u = d == CT(0) ? CT(0) : ct_div(-lr * g, d);
-    y[0] = u;
-    y[1] = v1;
-    y[2] = CT(x[2]) + u;
+    apply(x[0], x[1], y[0], y[1]);
+    y[2] = CT(x[2]) + y[0];
   }
 };
 
@@ -134,9 +151,13 @@ struct RmsBwd {
   __host__ __device__ static constexpr bool out_state(int) { return false; }
   CT alpha, oma, two_oma, lr, eps, hlr;  // hlr = lr/2
 
-  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT* h,
-                                             bool want_hp) const {
-    const CT g = x[0], v = x[1], du = x[2], dv1 = x[3];
+  __device__ __forceinline__ void set_lr(CT l) {
+    lr = l;
+    hlr = CT(0.5) * l;
+  }
+  // dg, dv; hyper terms (lr, alpha, eps)
+  __device__ __forceinline__ void apply(CT g, CT v, CT du, CT dv1, CT& dg, CT& dv, CT* h,
+                                        bool want_hp) const {
     const CT gg = g * g;
     const CT s2 = alpha * v + oma * gg;
     const CT rs = rsqrt_or_zero(s2);
@@ -145,13 +166,17 @@ struct RmsBwd {
     const CT R = du * rd;                   // du/d
     const CT T = R * rd;                    // du/d^2
     const CT V = dv1 + hlr * (g * T) * rs;  // dv1 + du lr g/(2 s d^2)
-    y[0] = two_oma * g * dv1 - (lr * T) * (eps + alpha * v * rs);
-    y[1] = alpha * V;
+    dg = two_oma * g * dv1 - (lr * T) * (eps + alpha * v * rs);
+    dv = alpha * V;
     if (want_hp) {
       h[0] -= g * R;
       h[1] += V * (v - gg);
       h[2] += lr * (g * T);
     }
+  }
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT* h,
+                                             bool want_hp) const {
+    apply(x[0], x[1], x[2], x[3], y[0], y[1], h, want_hp);
   }
 };
 
@@ -165,14 +190,15 @@ struct SgdFwd {
   CT lr, mu;
   int nesterov;
 
+  __device__ __forceinline__ void set_lr(CT l) { lr = l; }
+  __device__ __forceinline__ void apply(CT g, CT b, CT& u, CT& b1) const {
+    b1 = mu * b + g;
+    u = nesterov ? -lr * (g + mu * b1) : -lr * b1;
+  }
   __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT*,
                                              bool) const {
-    const CT g = x[0], b = x[1];
-    const CT b1 = mu * b + g;
-    const CT u = nesterov ? -lr * (g + mu * b1) : -lr * b1;
-    y[0] = u;
-    y[1] = b1;
-    y[2] = CT(x[2]) + u;
+    apply(x[0], x[1], y[0], y[1]);
+    y[2] = CT(x[2]) + y[0];
   }
 };
 
@@ -185,27 +211,159 @@ struct SgdBwd {
   CT lr, mu;
   int nesterov;
 
-  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT* h,
-                                             bool want_hp) const {
-    const CT g = x[0], b = x[1], du = x[2], db1 = x[3];
+  __device__ __forceinline__ void set_lr(CT l) { lr = l; }
+  // dg, db; hyper terms (lr, mu)
+  __device__ __forceinline__ void apply(CT g, CT b, CT du, CT db1, CT& dg, CT& db, CT* h,
+                                        bool want_hp) const {
     const CT b1 = mu * b + g;
     if (nesterov) {
       const CT B = db1 - lr * mu * du;
-      y[0] = B - lr * du;
-      y[1] = mu * B;
+      dg = B - lr * du;
+      db = mu * B;
       if (want_hp) {
         h[0] += (-du * (g + mu * b1));
         h[1] += (B * b - du * lr * b1);
       }
     } else {
       const CT B = db1 - lr * du;
-      y[0] = B;
-      y[1] = mu * B;
+      dg = B;
+      db = mu * B;
       if (want_hp) {
         h[0] += (-du * b1);
         h[1] += (B * b);
       }
     }
+  }
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT* h,
+                                             bool want_hp) const {
+    apply(x[0], x[1], x[2], x[3], y[0], y[1], h, want_hp);
+  }
+};
+
+// ------------------------------------------- optimizer variants (NEXT-1)
+// Weight decay, maximize and per-leaf lr (reading N1, torch.optim
+// semantics): g~ = (maximize ? -g : g) + wd theta (L2), or for Adam with
+// `decoupled` (AdamW) u += -lr wd theta instead. theta is the params input.
+// The VJP chains the base op's VJP through g~ and adds the theta cotangent
+// through the decay (`dtheta`, NOT including the identity of a fused apply)
+// and the weight-decay hyper-gradient (last hyper slot).
+template <class Base>
+struct ExCommon {
+  typedef typename Base::CT CT;
+  Base base;
+  CT wd;
+  int decoupled, maximize;
+  __device__ __forceinline__ void set_lr(CT l) { base.set_lr(l); }
+  __device__ __forceinline__ CT gtilde(CT g, CT th) const {
+    const CT gm = maximize ? -g : g;
+    return decoupled ? gm : gm + wd * th;
+  }
+};
+
+template <class CT_>
+struct AdamFwdEx : ExCommon<AdamFwd<CT_>> {
+  typedef CT_ CT;
+  static constexpr int NIN = 4, NOUT = 4, NH = 0;  // in: g m v theta ; out: u m' v' theta'
+  __host__ __device__ static constexpr bool in_state(int i) { return i == 1 || i == 2; }
+  __host__ __device__ static constexpr bool out_state(int i) { return i == 1 || i == 2; }
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT*,
+                                             bool) const {
+    const CT th = x[3];
+    this->base.apply(this->gtilde(x[0], th), x[1], x[2], y[0], y[1], y[2]);
+    if (this->decoupled) y[0] -= (this->base.lr * this->wd) * th;
+    y[3] = th + y[0];
+  }
+};
+
+template <class CT_>
+struct AdamBwdEx : ExCommon<AdamBwd<CT_>> {
+  typedef CT_ CT;
+  // in: g m v theta du dm1 dv1 ; out: dg dm dv dtheta ; hyper: lr b1 b2 eps wd
+  static constexpr int NIN = 7, NOUT = 4, NH = 5;
+  __host__ __device__ static constexpr bool in_state(int i) { return i == 1 || i == 2; }
+  __host__ __device__ static constexpr bool out_state(int) { return false; }
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT* h,
+                                             bool want_hp) const {
+    const CT th = x[3], du = x[4];
+    CT dgt;
+    this->base.apply(this->gtilde(x[0], th), x[1], x[2], du, x[5], x[6], dgt, y[1], y[2], h,
+                     want_hp);
+    y[0] = this->maximize ? -dgt : dgt;
+    const CT lr = this->base.lr;
+    if (this->decoupled) {
+      y[3] = -(lr * this->wd) * du;
+      if (want_hp) {
+        h[0] -= du * (this->wd * th);
+        h[4] -= du * (lr * th);
+      }
+    } else {
+      y[3] = this->wd * dgt;
+      if (want_hp) h[4] += dgt * th;
+    }
+  }
+};
+
+template <class CT_>
+struct RmsFwdEx : ExCommon<RmsFwd<CT_>> {
+  typedef CT_ CT;
+  static constexpr int NIN = 3, NOUT = 3, NH = 0;  // in: g v theta ; out: u v' theta'
+  __host__ __device__ static constexpr bool in_state(int i) { return i == 1; }
+  __host__ __device__ static constexpr bool out_state(int i) { return i == 1; }
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT*,
+                                             bool) const {
+    const CT th = x[2];
+    this->base.apply(this->gtilde(x[0], th), x[1], y[0], y[1]);
+    y[2] = th + y[0];
+  }
+};
+
+template <class CT_>
+struct RmsBwdEx : ExCommon<RmsBwd<CT_>> {
+  typedef CT_ CT;
+  // in: g v theta du dv1 ; out: dg dv dtheta ; hyper: lr alpha eps wd
+  static constexpr int NIN = 5, NOUT = 3, NH = 4;
+  __host__ __device__ static constexpr bool in_state(int i) { return i == 1; }
+  __host__ __device__ static constexpr bool out_state(int) { return false; }
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT* h,
+                                             bool want_hp) const {
+    const CT th = x[2];
+    CT dgt;
+    this->base.apply(this->gtilde(x[0], th), x[1], x[3], x[4], dgt, y[1], h, want_hp);
+    y[0] = this->maximize ? -dgt : dgt;
+    y[2] = this->wd * dgt;
+    if (want_hp) h[3] += dgt * th;
+  }
+};
+
+template <class CT_>
+struct SgdFwdEx : ExCommon<SgdFwd<CT_>> {
+  typedef CT_ CT;
+  static constexpr int NIN = 3, NOUT = 3, NH = 0;  // in: g b theta ; out: u b' theta'
+  __host__ __device__ static constexpr bool in_state(int i) { return i == 1; }
+  __host__ __device__ static constexpr bool out_state(int i) { return i == 1; }
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT*,
+                                             bool) const {
+    const CT th = x[2];
+    this->base.apply(this->gtilde(x[0], th), x[1], y[0], y[1]);
+    y[2] = th + y[0];
+  }
+};
+
+template <class CT_>
+struct SgdBwdEx : ExCommon<SgdBwd<CT_>> {
+  typedef CT_ CT;
+  // in: g b theta du db1 ; out: dg db dtheta ; hyper: lr mu wd
+  static constexpr int NIN = 5, NOUT = 3, NH = 3;
+  __host__ __device__ static constexpr bool in_state(int i) { return i == 1; }
+  __host__ __device__ static constexpr bool out_state(int) { return false; }
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT* h,
+                                             bool want_hp) const {
+    const CT th = x[2];
+    CT dgt;
+    this->base.apply(this->gtilde(x[0], th), x[1], x[3], x[4], dgt, y[1], h, want_hp);
+    y[0] = this->maximize ? -dgt : dgt;
+    y[2] = this->wd * dgt;
+    if (want_hp) h[2] += dgt * th;
   }
 };
 

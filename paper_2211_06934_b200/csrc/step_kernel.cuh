@@ -38,6 +38,7 @@ struct StepArgs {
   double* partials;      // workspace: per block (uniform) or per tile (leaf)
   unsigned int* counter; // workspace: arrival ticket, left at 0
   const int64_t* offsets;  // device offsets (leaf mode)
+  const float* lr_leaf;    // per-leaf learning rates (leaf mode) or NULL
   int64_t n_leaves;
   int64_t n_tiles;
   int want_hp;
@@ -255,8 +256,8 @@ __device__ __forceinline__ int64_t tiles_of(int64_t len) { return (len + kTile -
 template <class Op, class ST, int U, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) step_leaf(const Op op,
                                                     const StepArgs<Op::NIN, Op::NOUT> a) {
-  static_assert(Op::NH > 0, "leaf mode is for ops with hyper-gradient sums");
-  constexpr int NH = Op::NH;
+  constexpr int NH = Op::NH > 0 ? Op::NH : 1;
+  const bool want_hp = Op::NH > 0 && a.want_hp;
   extern __shared__ int64_t s_dyn[];
   int64_t* s_off = s_dyn;
   int64_t* s_tp = s_dyn + (a.n_leaves + 1);
@@ -303,23 +304,31 @@ __global__ void __launch_bounds__(kBlock, MINB) step_leaf(const Op op,
     const int64_t leaf_end = s_off[lo + 1];
     const int64_t start = s_off[lo] + (tile - s_tp[lo]) * kTile;
     const int64_t end = min(start + kTile, leaf_end);
+    Op opt = op;  // this tile's leaf learning rate (per-leaf lr variants)
+    if (a.lr_leaf) opt.set_lr((typename Op::CT)a.lr_leaf[lo]);
     double acc[NH];
 #pragma unroll
     for (int k = 0; k < NH; ++k) acc[k] = 0.0;
     const int64_t va = (start + 3) >> 2, vb = end >> 2;
     if (va < vb) {
-      process_vectors<Op, ST, U>(op, a, va, vb, threadIdx.x, kBlock, acc, true);
-      if (start + threadIdx.x < (va << 2)) process_elem<Op, ST>(op, a, start + threadIdx.x, acc, true);
-      if ((vb << 2) + threadIdx.x < end) process_elem<Op, ST>(op, a, (vb << 2) + threadIdx.x, acc, true);
+      process_vectors<Op, ST, U>(opt, a, va, vb, threadIdx.x, kBlock, acc, want_hp);
+      if (start + threadIdx.x < (va << 2))
+        process_elem<Op, ST>(opt, a, start + threadIdx.x, acc, want_hp);
+      if ((vb << 2) + threadIdx.x < end)
+        process_elem<Op, ST>(opt, a, (vb << 2) + threadIdx.x, acc, want_hp);
     } else {
-      for (int64_t i = start + threadIdx.x; i < end; i += kBlock) process_elem<Op, ST>(op, a, i, acc, true);
+      for (int64_t i = start + threadIdx.x; i < end; i += kBlock)
+        process_elem<Op, ST>(opt, a, i, acc, want_hp);
     }
-    block_sum<NH>(acc, sm);
-    if (threadIdx.x == 0)
+    if (want_hp) {
+      block_sum<NH>(acc, sm);
+      if (threadIdx.x == 0)
 #pragma unroll
-      for (int k = 0; k < NH; ++k) a.partials[tile * NH + k] = acc[k];
+        for (int k = 0; k < NH; ++k) a.partials[tile * NH + k] = acc[k];
+    }
   }
 
+  if (!want_hp) return;
   if (last_block(a.counter, gridDim.x)) {
     double tot[NH];
 #pragma unroll

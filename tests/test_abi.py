@@ -130,3 +130,25 @@ def test_python_api_validation():
         rmsprop(alpha=1.5)
     with pytest.raises(ValueError):
         sgd(lr=0.1, momentum=1.0)
+
+
+def test_variant_validation(L):
+    t = L.Tree(numel=64)
+    h = L.opt_adam_hp(1e-3, 0.9, 0.999, 1e-8, 0.0)
+    P = 0x10000
+
+    def fwd(ext, params=P):
+        return L.lib.opt_adam_fwd_ex(ctypes.byref(t.c), 1, ctypes.byref(h), ctypes.byref(ext), 0,
+                                     0, P, None, None, params, P, P, P, None, 0)
+
+    assert fwd(L._ext(weight_decay=-1.0)) == L.OPT_EINVAL
+    assert fwd(L._ext(weight_decay=0.1), params=None) == L.OPT_EINVAL
+    assert fwd(L._ext(lr_leaf=0x20004)) == L.OPT_EALIGN
+    # per-leaf lr needs leaves and device offsets
+    assert fwd(L._ext(lr_leaf=0x20000)) == L.OPT_EINVAL
+    assert "n_leaves" in L.lib.opt_last_error().decode() or "d_offsets" in L.lib.opt_last_error().decode()
+    t2 = L.Tree.from_sizes([32, 32])
+    rc = L.lib.opt_sgd_bwd_ex(ctypes.byref(t2.c), ctypes.byref(L.opt_sgd_hp(0.1, 0.9, 0)),
+                              ctypes.byref(L._ext(lr_leaf=0x20000)), 0, 0, P, P, P, P, P, P, P, P,
+                              None, None, None, 0, 0)
+    assert rc == L.OPT_EINVAL and "d_offsets" in L.lib.opt_last_error().decode()
