@@ -195,6 +195,88 @@ class SgdStep(torch.autograd.Function):
         return (d_g, d_mom, d_out if fused else None, *hg, None, None)
 
 
+# ---------------------------------------------- variants (NEXT-1, *_ex ABI)
+_EX_NH = {"adam": 5, "rmsprop": 4, "sgd": 3}
+
+
+class StepEx(torch.autograd.Function):
+    """Any of the three optimizers with weight decay (L2 / AdamW), maximize
+    and per-leaf learning rates (``lr_leaf``: a float32 CUDA tensor of
+    n_leaves entries that may require grad -- Meta-SGD/MGRL-style learnable
+    per-leaf lr). Inputs: (g, s0, s1, params, hyper tuple, wd, lr_leaf).
+    Outputs: (params + u if ``fused`` else u, s0', s1'). ``hps`` are the
+    optimizer's hyper-parameters after lr (adam: b1, b2, eps; rmsprop: alpha,
+    eps; sgd: momentum)."""
+
+    @staticmethod
+    def forward(ctx, g, s0, s1, params, lr, wd, lr_leaf, hps, kind, step, opts, cfg):
+        decoupled, maximize, nesterov, eps_root, fused = opts
+        g, s0, s1, params = _contig(g), _contig(s0), _contig(s1), _contig(params)
+        sd = cfg.state_dtype if cfg.state_dtype is not None else _sd(s0, s1)
+        ext = L._ext(_f(wd), decoupled, maximize, None if lr_leaf is None else lr_leaf.detach())
+        out = torch.empty_like(g)
+        n0 = _empty_state(g, sd)
+        if kind == "adam":
+            hp = (_f(lr), _f(hps[0]), _f(hps[1]), _f(hps[2]), float(eps_root))
+            n1 = _empty_state(g, sd)
+            L.opt_adam_fwd_ex(cfg.tree, step, hp, ext, sd, cfg.compute, g, s0, s1, params,
+                              None if fused else out, n0, n1, out if fused else None)
+        elif kind == "rmsprop":
+            hp = (_f(lr), _f(hps[0]), _f(hps[1]))
+            n1 = g.new_zeros(0)
+            L.opt_rmsprop_fwd_ex(cfg.tree, hp, ext, sd, cfg.compute, g, s0, params,
+                                 None if fused else out, n0, out if fused else None)
+        else:
+            hp = (_f(lr), _f(hps[0]), bool(nesterov))
+            n1 = g.new_zeros(0)
+            L.opt_sgd_fwd_ex(cfg.tree, hp, ext, sd, cfg.compute, g, s0, params,
+                             None if fused else out, n0, out if fused else None)
+        ctx.save_for_backward(g, s0, s1, params, lr_leaf)
+        ctx.meta = (kind, hp, ext, sd, cfg, fused, (lr,) + tuple(hps) + (wd,), step)
+        return out, n0, n1
+
+    @staticmethod
+    @once_differentiable
+    def backward(ctx, d_out, d_n0, d_n1):
+        g, s0, s1, params, lr_leaf = ctx.saved_tensors
+        kind, hp, ext, sd, cfg, fused, hyp, step = ctx.meta
+        nh = _EX_NH[kind]
+        want_leaf = lr_leaf is not None and lr_leaf.requires_grad
+        want_hp = want_leaf or any(_needs(x) for x in hyp)
+        d_g = torch.empty_like(g)
+        d_s0 = None if s0 is None else torch.empty_like(g)
+        d_s1 = None if (s1 is None or kind != "adam") else torch.empty_like(g)
+        d_p = None if params is None else torch.empty_like(g)
+        d_hp = torch.empty(nh, dtype=torch.float64, device=g.device) if want_hp else None
+        d_leaf = (torch.empty(cfg.tree.n_leaves * nh, dtype=torch.float64, device=g.device)
+                  if want_leaf else None)
+        ws = _workspace(cfg.tree, g.device, per_leaf=want_leaf) if want_hp else None
+        d_out = _contig(d_out)
+        if d_n1 is not None and d_n1.numel() == 0:
+            d_n1 = None
+        if kind == "adam":
+            L.opt_adam_bwd_ex(cfg.tree, step, hp, ext, sd, cfg.compute, g, s0, s1, params, d_out,
+                              _contig(d_n0), _contig(d_n1), d_g, d_s0, d_s1, d_p, d_hp, d_leaf, ws)
+        elif kind == "rmsprop":
+            L.opt_rmsprop_bwd_ex(cfg.tree, hp, ext, sd, cfg.compute, g, s0, params, d_out,
+                                 _contig(d_n0), d_g, d_s0, d_p, d_hp, d_leaf, ws)
+        else:
+            L.opt_sgd_bwd_ex(cfg.tree, hp, ext, sd, cfg.compute, g, s0, params, d_out,
+                             _contig(d_n0), d_g, d_s0, d_p, d_hp, d_leaf, ws)
+        if d_p is not None and fused:
+            d_p = d_p + d_out  # identity of the fused apply_updates
+        lr, *rest = hyp
+        hg = [None] * len(hyp)
+        if d_hp is not None:
+            hg = [_hp_grad(x, d_hp[k]) for k, x in enumerate(hyp[:-1])] + [
+                _hp_grad(hyp[-1], d_hp[nh - 1])]
+        d_lrl = None
+        if want_leaf:
+            d_lrl = d_leaf.view(-1, nh)[:, 0].to(lr_leaf.dtype)
+        hps_grad = None  # hyper-parameters after lr are passed as a tuple (no grads)
+        return (d_g, d_s0, d_s1, d_p, hg[0], hg[-1], d_lrl, hps_grad, None, None, None, None)
+
+
 class ApplyUpdates(torch.autograd.Function):
     """params + updates (row a8); backward is the identity for both."""
 
@@ -247,9 +329,11 @@ class GradientTransformation:
     """init/update pair. ``update`` accepts a flat gradient
     buffer or a sequence of leaf gradients (flattened once into one buffer)."""
 
-    def __init__(self, kind, hp, n_slots, compute=L.OPT_COMPUTE_DEFAULT, state_dtype=L.OPT_F32):
+    def __init__(self, kind, hp, n_slots, compute=L.OPT_COMPUTE_DEFAULT, state_dtype=L.OPT_F32,
+                 ext=None):
         self.kind, self.hp, self.n_slots = kind, hp, n_slots
         self.compute, self.state_dtype = compute, state_dtype
+        self.ext = ext  # None or dict(weight_decay, decoupled, maximize, lr_leaf) (NEXT-1)
 
     def init(self, params):
         """Zero state. Slots are None until the first update: the
@@ -273,18 +357,20 @@ class GradientTransformation:
         flat_p = None
         if params is not None:
             flat_p = params if isinstance(params, torch.Tensor) else layout.flatten(params)
+        if self.ext is not None:
+            return self._update_ex(flat, state, flat_p, cfg, t, inplace, differentiable)
         if self.kind == "adam":
             lr, b1, b2, eps, eps_root = self.hp
-            out, m1, v1 = AdamStep.apply(flat, state.slots[0], state.slots[1], flat_p, lr, b1,
+            out, m1, v1 = AdamStep.apply(flat, state.slots[0], state.slots[1], None, lr, b1,
                                          b2, eps, t, eps_root, cfg)
             slots = (m1, v1)
         elif self.kind == "rmsprop":
             lr, alpha, eps = self.hp
-            out, v1 = RmsPropStep.apply(flat, state.slots[0], flat_p, lr, alpha, eps, cfg)
+            out, v1 = RmsPropStep.apply(flat, state.slots[0], None, lr, alpha, eps, cfg)
             slots = (v1,)
         else:
             lr, mom, nest = self.hp
-            out, b1 = SgdStep.apply(flat, state.slots[0] if state.slots else None, flat_p, lr,
+            out, b1 = SgdStep.apply(flat, state.slots[0] if state.slots else None, None, lr,
                                     mom, nest, cfg)
             slots = (b1 if _f(mom) != 0.0 else None,)
         if inplace and not differentiable:
@@ -292,6 +378,35 @@ class GradientTransformation:
                 if old is not None and new is not None:
                     old.copy_(new)
         return out, OptState(t, slots, layout)
+
+    def _update_ex(self, flat, state, flat_p, cfg, t, inplace, differentiable):
+        e = self.ext
+        if _f(e["weight_decay"]) != 0.0 and flat_p is None:
+            raise ValueError("weight_decay needs update(..., params=...)")
+        lr_leaf = e.get("lr_leaf")
+        if lr_leaf is not None and lr_leaf.numel() != cfg.tree.n_leaves:
+            raise ValueError("lr_leaf must have one entry per leaf")
+        if self.kind == "adam":
+            lr, b1, b2, eps, eps_root = self.hp
+            hps, nest = (b1, b2, eps), False
+        elif self.kind == "rmsprop":
+            lr, alpha, eps = self.hp
+            hps, nest, eps_root = (alpha, eps), False, 0.0
+        else:
+            lr, mom, nest = self.hp
+            hps, eps_root = (mom,), 0.0
+        s0 = state.slots[0] if state.slots else None
+        s1 = state.slots[1] if len(state.slots) > 1 else None
+        opts = (bool(e.get("decoupled", False)), bool(e.get("maximize", False)), bool(nest),
+                eps_root, False)
+        out, n0, n1 = StepEx.apply(flat, s0, s1, flat_p, lr, e["weight_decay"], lr_leaf, hps,
+                                   self.kind, t, opts, cfg)
+        slots = (n0, n1) if self.kind == "adam" else (n0,)
+        if inplace and not differentiable:
+            for old, new in zip(state.slots, slots):
+                if old is not None and new is not None:
+                    old.copy_(new)
+        return out, OptState(t, slots, state.layout)
 
 
 def _any_requires_grad(grads, state):
@@ -311,31 +426,46 @@ def _check_lr(lr):
         raise ValueError(f"lr must be > 0, got {_f(lr)}")
 
 
-def adam(lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, eps_root=0.0, compute=L.OPT_COMPUTE_DEFAULT,
-         state_dtype=L.OPT_F32):
-    """Adam (defaults; validation S:189)."""
+def _ext_opts(weight_decay, decoupled, maximize, lr_leaf):
+    if _f(weight_decay) < 0.0:
+        raise ValueError("weight_decay must be >= 0")
+    if _f(weight_decay) == 0.0 and not decoupled and not maximize and lr_leaf is None:
+        return None
+    return dict(weight_decay=weight_decay, decoupled=decoupled, maximize=maximize,
+                lr_leaf=lr_leaf)
+
+
+def adam(lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, eps_root=0.0, weight_decay=0.0, decoupled=False,
+         maximize=False, lr_leaf=None, compute=L.OPT_COMPUTE_DEFAULT, state_dtype=L.OPT_F32):
+    """Adam (defaults; validation S:189). weight_decay/decoupled
+    (AdamW)/maximize/lr_leaf are the NEXT-1 variants (reading N1)."""
     _check_lr(lr)
     _check_unit("b1", b1)
     _check_unit("b2", b2)
     if not _f(eps) > 0.0:
         raise ValueError("eps must be > 0")
-    return GradientTransformation("adam", (lr, b1, b2, eps, eps_root), 2, compute, state_dtype)
+    return GradientTransformation("adam", (lr, b1, b2, eps, eps_root), 2, compute, state_dtype,
+                                  _ext_opts(weight_decay, decoupled, maximize, lr_leaf))
 
 
-def rmsprop(lr=1e-2, alpha=0.99, eps=1e-8, compute=L.OPT_COMPUTE_DEFAULT, state_dtype=L.OPT_F32):
+def rmsprop(lr=1e-2, alpha=0.99, eps=1e-8, weight_decay=0.0, maximize=False, lr_leaf=None,
+            compute=L.OPT_COMPUTE_DEFAULT, state_dtype=L.OPT_F32):
     """RMSProp (S:206-207)."""
     _check_lr(lr)
     _check_unit("alpha", alpha)
     if not _f(eps) >= 0.0:
         raise ValueError("eps must be >= 0")
-    return GradientTransformation("rmsprop", (lr, alpha, eps), 1, compute, state_dtype)
+    return GradientTransformation("rmsprop", (lr, alpha, eps), 1, compute, state_dtype,
+                                  _ext_opts(weight_decay, False, maximize, lr_leaf))
 
 
-def sgd(lr, momentum=0.0, nesterov=False, compute=L.OPT_COMPUTE_DEFAULT, state_dtype=L.OPT_F32):
+def sgd(lr, momentum=0.0, nesterov=False, weight_decay=0.0, maximize=False, lr_leaf=None,
+        compute=L.OPT_COMPUTE_DEFAULT, state_dtype=L.OPT_F32):
     """SGD with optional (Nesterov) momentum (S:196-199)."""
     _check_lr(lr)
     _check_unit("momentum", momentum)
-    return GradientTransformation("sgd", (lr, momentum, nesterov), 1, compute, state_dtype)
+    return GradientTransformation("sgd", (lr, momentum, nesterov), 1, compute, state_dtype,
+                                  _ext_opts(weight_decay, False, maximize, lr_leaf))
 
 
 def apply_updates(params, updates):
