@@ -349,6 +349,8 @@ def main():
     ap.add_argument("--compute", default="default", choices=["default", "f32", "f64"])
     ap.add_argument("--workload", default="c2", choices=["c2", "c1", "c5", "c3", "maml"])
     ap.add_argument("--tasks", type=int, default=32, help="MAML meta-batch (C4)")
+    ap.add_argument("--checkpoint-every", type=int, default=None,
+                    help="C3: keep only every c-th state and recompute segments (NEXT-2)")
     ap.add_argument("--no-graph", action="store_true", help="MAML without CUDA-graph capture")
     ap.add_argument("--size", type=int, default=1 << 24)
     ap.add_argument("--bf16", action="store_true", help="bf16 optimizer state")
@@ -472,7 +474,7 @@ def run_sweep(args, dev, rank, world):
     q = synth.quadratic_problem(0xC3, n)
     tree = L.Tree(offsets=off, device=dev)
     hp = (1e-2, 0.9, 0.999, 1e-8, 0.0)
-    sw = QuadraticSweep(tree, "adam", hp, 5, dev)
+    sw = QuadraticSweep(tree, "adam", hp, 5, dev, checkpoint_every=args.checkpoint_every)
     a, th0, phi, y = (torch.from_numpy(q[k]).to(dev) for k in ("a", "theta0", "phi", "y"))
     del q
     l0 = L.opt_launch_count()
@@ -487,6 +489,7 @@ def run_sweep(args, dev, rank, world):
            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
            "config": {"workload": "C3 5-step unrolled Adam + reverse sweep, 9x resnet18 tree",
                       "numel": n, "n_leaves": len(leaves), "K": 5,
+                      "checkpoint_every": sw.c, "saved_state_bytes": sw.saved_bytes(),
                       "alg_bytes_per_step": per, "launches_per_step": sw.launches_per_sweep},
            "frac_of_measured_hbm": round(value / world / peak, 4),
            "gpu_launches": launches}

@@ -48,7 +48,31 @@ def test_sweep_matches_oracle(pkg, kind, hp, K):
     hs = host(hyper).sum(0)
     nh = NH[kind]
     assert_sum_close("hyper", hs[:nh], ref["hyper_bar"][:nh], ref["hyper_abs"][:nh])
-    assert sw.launches_per_sweep == 4 * K + 2
+    assert sw.launches_per_sweep == 4 * K + 1
+
+
+@pytest.mark.parametrize("kind,hp", SWEEP_CASES[:2])
+@pytest.mark.parametrize("K,c", [(5, 2), (7, 3), (6, 1), (5, 5)])
+def test_checkpointed_sweep_is_bitwise_full_storage(pkg, kind, hp, K, c):
+    """NEXT-2: recomputing segments from checkpoints reproduces the full-
+    storage sweep bitwise (same deterministic kernels on the same inputs),
+    with the launch count the class reports and less saved state."""
+    from paper_2211_06934_b200.unroll import QuadraticSweep
+
+    leaves = [7, 4096, 333, 5000, 1]
+    q = synth.quadratic_problem(0xC4, sum(leaves))
+    tree = pkg.Tree(offsets=synth.offsets_of(leaves), device=DEV)
+    args = [dev_f32(q[k]) for k in ("a", "theta0", "phi", "y")]
+    full = QuadraticSweep(tree, kind, hp, K, DEV)
+    ref = [t.clone() for t in full.run(*args)]
+    ck = QuadraticSweep(tree, kind, hp, K, DEV, checkpoint_every=c)
+    n0 = pkg._lib.opt_launch_count()
+    out = ck.run(*args)
+    torch.cuda.synchronize()
+    assert pkg._lib.opt_launch_count() - n0 == ck.launches_per_sweep
+    for a, b in zip(ref, out):
+        assert torch.equal(a, b)
+    assert ck.saved_bytes() <= full.saved_bytes()
 
 
 def test_sweep_bytes_accounting(pkg):
