@@ -580,3 +580,42 @@ def ex_mag(kind, g, state, theta, du, ds1, dv1=None, t=1, hp=(), weight_decay=0.
         out["dwd"] = base["dg"] * th
         out["extra_lr"] = np.zeros(n)
     return out
+
+
+# ------------------------------------------------ zero-order ES (NEXT-3)
+def _es_lib():
+    L = lib()
+    if not getattr(L, "_es_ready", False):
+        P, i64, I, D, U = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
+                           ctypes.c_uint64)
+        L.oracle_es_noise.argtypes = [i64, i64, U, P]
+        L.oracle_es_perturb.argtypes = [i64, i64, I, D, U, P, P]
+        L.oracle_es_grad.argtypes = [i64, i64, I, D, U, P, P, P]
+        L._es_ready = True
+    return L
+
+
+def es_noise(numel, n_samples, seed):
+    z = np.empty((n_samples, numel))
+    _es_lib().oracle_es_noise(int(numel), int(n_samples), int(seed), _p(z))
+    return z
+
+
+def es_perturb(theta, n_samples, sigma, seed, antithetic=True):
+    """Rows theta + sigma z_i (antithetic: +/- interleaved), float64."""
+    theta = _f32(theta)
+    reps = 2 if antithetic else 1
+    out = np.empty((n_samples * reps, theta.size))
+    _es_lib().oracle_es_perturb(theta.size, int(n_samples), int(antithetic), float(sigma),
+                                int(seed), _p(theta), _p(out))
+    return out
+
+
+def es_grad(f_values, numel, n_samples, sigma, seed, antithetic=True):
+    """ES gradient estimate from f at the perturbed rows; returns
+    (g, g_abs) where g_abs = sum_i |term_ij| (tolerance scale)."""
+    f = np.ascontiguousarray(f_values, dtype=np.float64)
+    g, ga = np.empty(numel), np.empty(numel)
+    _es_lib().oracle_es_grad(int(numel), int(n_samples), int(antithetic), float(sigma),
+                             int(seed), _p(f), _p(g), _p(ga))
+    return g, ga

@@ -888,3 +888,45 @@ void oracle_sgd_fwd_ex_cplx(int64_t n, const double* hp_re, const double* hp_im,
 }
 
 }  // extern "C"
+
+// ------------------------------------------------ zero-order ES (NEXT-3)
+extern "C" {
+
+// z[i][j] for i < n_samples, j < numel (the noise itself, for tests).
+void oracle_es_noise(int64_t numel, int64_t n_samples, uint64_t seed, double* z) {
+  for (int64_t i = 0; i < n_samples; ++i)
+    for (int64_t j = 0; j < numel; ++j) z[i * numel + j] = oracle::es_normal(seed, i, j);
+}
+
+// Perturbed points, row r of out: theta + sigma z_i (naive: r = i;
+// antithetic: r = 2i is +, r = 2i+1 is -).
+void oracle_es_perturb(int64_t numel, int64_t n_samples, int antithetic, double sigma,
+                       uint64_t seed, const float* theta, double* out) {
+  const int reps = antithetic ? 2 : 1;
+  for (int64_t i = 0; i < n_samples; ++i)
+    for (int64_t j = 0; j < numel; ++j) {
+      const double z = oracle::es_normal(seed, i, j);
+      out[(i * reps) * numel + j] = (double)theta[j] + sigma * z;
+      if (antithetic) out[(i * reps + 1) * numel + j] = (double)theta[j] - sigma * z;
+    }
+}
+
+// Gradient estimate from the f values of the perturbed points (same row
+// order as oracle_es_perturb). g_abs (optional): sum over i of |term|.
+void oracle_es_grad(int64_t numel, int64_t n_samples, int antithetic, double sigma,
+                    uint64_t seed, const double* f, double* g, double* g_abs) {
+  const double scale = antithetic ? 1.0 / (2.0 * n_samples * sigma) : 1.0 / (n_samples * sigma);
+  for (int64_t j = 0; j < numel; ++j) {
+    long double s = 0.0L, a = 0.0L;
+    for (int64_t i = 0; i < n_samples; ++i) {
+      const double w = antithetic ? f[2 * i] - f[2 * i + 1] : f[i];
+      const long double term = (long double)w * oracle::es_normal(seed, i, j);
+      s += term;
+      a += term < 0 ? -term : term;
+    }
+    g[j] = (double)(s * scale);
+    if (g_abs) g_abs[j] = (double)(a * (scale < 0 ? -scale : scale));
+  }
+}
+
+}  // extern "C"

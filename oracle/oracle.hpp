@@ -453,3 +453,37 @@ SgdVjpEx<T> sgd_vjp_ex(T g, T b, T theta, T du, T db1_out, const SgdHP<T>& h, co
 }
 
 }  // namespace oracle
+
+// ------------------------------------------------ zero-order ES (NEXT-3)
+// PAPER.md §2.2 "Zero-order Differentiation (ZD)": ES optimizes the
+// Gaussian smoothing f~_sigma(theta) = E_z[f(theta + sigma z)], z ~ N(0, I_d),
+// whose gradient is (1/sigma) E_z[f(theta + sigma z) z]. Monte-Carlo estimate
+// over n samples (the naive form of P:204), or the antithetic form of the
+// cited ES literature (reading N3):
+//   naive:      g = 1/(n sigma)  sum_i f(theta + sigma z_i) z_i
+//   antithetic: g = 1/(2 n sigma) sum_i [f(theta + sigma z_i) - f(theta - sigma z_i)] z_i
+// The noise z_ij is a counter-based draw keyed on (seed, sample i, element j)
+// so that it never has to be stored (reading N3); this file implements that
+// generator itself (it shares no code with the CUDA side, which implements
+// the same definition):
+//   key  = mix(seed ^ mix(i + 0x9E3779B97F4A7C15)),  w = mix(key + j)
+//   u1 = ((w >> 40) + 0.5) 2^-24,  u2 = ((w & 0xFFFFFF) + 0.5) 2^-24
+//   z  = sqrt(-2 ln u1) cos(2 pi u2)                       (Box-Muller)
+// with mix the SplitMix64 finaliser.
+namespace oracle {
+
+inline uint64_t es_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+inline double es_normal(uint64_t seed, int64_t i, int64_t j) {
+  const uint64_t key = es_mix(seed ^ es_mix((uint64_t)i + 0x9E3779B97F4A7C15ull));
+  const uint64_t w = es_mix(key + (uint64_t)j);
+  const double u1 = ((double)(w >> 40) + 0.5) * (1.0 / 16777216.0);
+  const double u2 = ((double)(w & 0xFFFFFFull) + 0.5) * (1.0 / 16777216.0);
+  return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.14159265358979323846 * u2);
+}
+
+}  // namespace oracle

@@ -694,3 +694,68 @@ def test_rms_sgd_variant_vjp_vs_complex_step(orc, kind):
         lrc = lr_e.astype(np.complex128)
         lrc[off[l]:off[l + 1]] += 1j * H
         assert r["dhp_leaf"][l, 0] == pytest.approx(contract(F(lr=lrc)).sum(), rel=1e-8)
+
+
+# --------------------------------------------- zero-order ES (NEXT-3 pins)
+def test_es_noise_is_standard_normal_and_independent(orc):
+    """The counter-based noise (reading N3) has the moments of N(0,1), matches
+    the normal CDF at a few quantiles, and is uncorrelated across samples
+    and elements; the same seed reproduces it, another seed does not."""
+    z = orc.es_noise(4096, 64, seed=11)
+    flat = z.ravel()
+    N = flat.size
+    assert abs(flat.mean()) < 5 / np.sqrt(N)
+    assert abs(flat.var() - 1) < 5 * np.sqrt(2 / N)
+    assert abs(np.mean(flat ** 4) - 3) < 5 * np.sqrt(96 / N)
+    from math import erf
+    for q in (-2.0, -1.0, 0.0, 0.5, 1.5):
+        p = 0.5 * (1 + erf(q / np.sqrt(2)))
+        assert abs(np.mean(flat < q) - p) < 5 * np.sqrt(p * (1 - p) / N)
+    c = np.corrcoef(z[:8])  # across samples
+    assert np.max(np.abs(c - np.eye(8))) < 5 / np.sqrt(4096)
+    assert abs(np.corrcoef(z[:, :-1].ravel(), z[:, 1:].ravel())[0, 1]) < 5 / np.sqrt(N)
+    np.testing.assert_array_equal(z, orc.es_noise(4096, 64, seed=11))
+    assert not np.array_equal(z, orc.es_noise(4096, 64, seed=12))
+
+
+def test_es_constant_f_antithetic_is_exactly_zero(orc):
+    g, _ = orc.es_grad(np.full(2 * 50, 3.25), 100, 50, 0.1, seed=3, antithetic=True)
+    assert np.all(g == 0)
+
+
+@pytest.mark.parametrize("antithetic", [True, False])
+def test_es_linear_f_estimates_c(orc, antithetic):
+    """SPEC zero-order-diff example: f(theta) = c.theta; E[g] = c (E[zz^T] = I);
+    each antithetic sample contributes exactly (c.z) z. Checked at 5 standard
+    errors with n = 20000."""
+    d, n, sigma = 6, 20000, 0.05
+    c = np.array([1.0, -2.0, 0.5, 0.0, 3.0, -1.0])
+    theta = np.linspace(-1, 1, d).astype(np.float32)
+    pts = orc.es_perturb(theta, n, sigma, seed=5, antithetic=antithetic)
+    f = pts @ c
+    g, _ = orc.es_grad(f, d, n, sigma, seed=5, antithetic=antithetic)
+    if antithetic:
+        se = np.sqrt((c @ c + c ** 2) / n)
+    else:  # naive carries f(theta)/sigma noise too
+        f0 = float(theta.astype(np.float64) @ c)
+        se = np.sqrt((c @ c + c ** 2 + (f0 / sigma) ** 2) / n)
+    assert np.all(np.abs(g - c) < 5 * se)
+    # antithetic: the per-sample contributions are exactly (c.z) z
+    if antithetic:
+        z = orc.es_noise(d, 4, seed=5)
+        g4, _ = orc.es_grad(f[:8], d, 4, sigma, seed=5)
+        np.testing.assert_allclose(g4, np.mean([(c @ zi) * zi for zi in z], axis=0), rtol=1e-9,
+                                   atol=1e-12)
+
+
+def test_es_quadratic_smoothing_identity(orc):
+    """f = 1/2 ||theta||^2: f~_sigma = f + sigma^2 d/2, so E[g] = theta exactly
+    for any sigma (Gaussian-moment identity); 5 standard errors, n = 20000."""
+    d, n, sigma = 5, 20000, 0.1
+    theta = np.array([0.3, -1.2, 2.0, 0.0, 0.7], np.float32)
+    pts = orc.es_perturb(theta, n, sigma, seed=9, antithetic=True)
+    f = 0.5 * np.sum(pts ** 2, axis=1)
+    g, _ = orc.es_grad(f, d, n, sigma, seed=9)
+    th = theta.astype(np.float64)
+    se = np.sqrt((th @ th + th ** 2) / n)
+    assert np.all(np.abs(g - th) < 5 * se + 1e-12)
