@@ -232,6 +232,27 @@ int opt_quadratic_grad(int64_t numel, const float* a, const float* theta,
 int opt_quadratic_rev(int64_t numel, const float* a, const float* g_bar,
                       float* theta_bar, float* phi_bar, int init_phi, void* stream);
 
+/* ------------------------------------ zero-order ES (SV §8(f) NEXT-3)
+ * PAPER.md §2.2 "Zero-order Differentiation (ZD)": ES optimises the
+ * Gaussian smoothing f~(theta) = E_z[f(theta + sigma z)], z ~ N(0, I), with
+ * gradient (1/sigma) E_z[f(theta + sigma z) z]. The noise z_ij is never
+ * stored: it is a counter-based draw keyed on (seed, sample i, element j)
+ * (reading N3 gives the exact definition), regenerated by both
+ * calls.
+ * opt_es_perturb writes the points the caller's black-box f is evaluated at:
+ *   row r of `out` (row stride ld = numel rounded up to a multiple of 4
+ *   floats) is theta + sigma z_(sample0 + i) for r = i (antithetic == 0), or
+ *   theta + sigma z_i for r = 2i and theta - sigma z_i for r = 2i+1.
+ *   out holds n_samples * (antithetic ? 2 : 1) * ld floats.
+ * opt_es_grad: given f_values (device float, same row order, samples
+ *   0..n_samples-1), grad = 1/(n sigma) sum_i f_i z_i (naive) or
+ *   1/(2 n sigma) sum_i (f_(2i) - f_(2i+1)) z_i (antithetic).
+ * n_samples <= 4096 per call; sigma > 0. theta/out/grad 16-byte aligned. */
+int opt_es_perturb(int64_t numel, int64_t n_samples, int64_t sample0, int antithetic,
+                   double sigma, uint64_t seed, const float* theta, float* out, void* stream);
+int opt_es_grad(int64_t numel, int64_t n_samples, int antithetic, double sigma, uint64_t seed,
+                const float* f_values, float* grad, void* stream);
+
 /* -------------------------------------------------------------- misc */
 const char* opt_status_string(int status);
 /* Message of the last failing call on this host thread ("" if none). */

@@ -338,3 +338,28 @@ def opt_sgd_bwd_ex(tree, hp, ext, state_dtype, compute, g, mom, params, d_update
                               _ptr(mom), _ptr(params), _ptr(d_updates), _ptr(d_mom_out),
                               _ptr(d_g), _ptr(d_mom), _ptr(d_params), _ptr(d_hp),
                               _ptr(d_hp_leaf), wp, wb, _stream(stream)))
+
+
+# ------------------------------------------------ zero-order ES (NEXT-3)
+lib.opt_es_perturb.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                               ctypes.c_double, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
+                               ctypes.c_void_p]
+lib.opt_es_perturb.restype = ctypes.c_int
+lib.opt_es_grad.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
+                            ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+lib.opt_es_grad.restype = ctypes.c_int
+EXPORTS += ["opt_es_perturb", "opt_es_grad"]
+
+
+def es_row_stride(numel):
+    return (int(numel) + 3) & ~3
+
+
+def opt_es_perturb(numel, n_samples, sample0, antithetic, sigma, seed, theta, out, stream=None):
+    _check(lib.opt_es_perturb(int(numel), int(n_samples), int(sample0), int(bool(antithetic)),
+                              float(sigma), int(seed), _ptr(theta), _ptr(out), _stream(stream)))
+
+
+def opt_es_grad(numel, n_samples, antithetic, sigma, seed, f_values, grad, stream=None):
+    _check(lib.opt_es_grad(int(numel), int(n_samples), int(bool(antithetic)), float(sigma),
+                           int(seed), _ptr(f_values), _ptr(grad), _stream(stream)))

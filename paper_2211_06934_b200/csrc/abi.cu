@@ -932,3 +932,65 @@ int opt_quadratic_rev(int64_t numel, const float* a, const float* g_bar, float* 
 }
 
 }  // extern "C"
+
+// ------------------------------------------- zero-order ES (NEXT-3, es.cuh)
+#include "es.cuh"
+
+extern "C" {
+
+int opt_es_perturb(int64_t numel, int64_t n_samples, int64_t sample0, int antithetic,
+                   double sigma, uint64_t seed, const float* theta, float* out, void* stream) {
+  g_err.clear();
+  if (numel < 0 || n_samples < 0 || sample0 < 0) return fail(OPT_EINVAL, "negative size");
+  if (n_samples > kEsMaxSamples)
+    return fail(OPT_EINVAL, "n_samples = %lld > %d per call (use sample0 chunks)",
+                (long long)n_samples, kEsMaxSamples);
+  if (!(std::isfinite(sigma) && sigma > 0)) return fail(OPT_EINVAL, "sigma must be > 0");
+  TRY(check_align({theta, out}));
+  if (numel == 0 || n_samples == 0) return OPT_OK;
+  if (!theta || !out) return fail(OPT_EINVAL, "NULL array");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int sms = 0;
+  TRY(sm_count(&sms));
+  const int64_t nvec = numel >> 2;
+  int64_t grid = (nvec + 255) / 256 + 1;
+  if (grid > (int64_t)sms * 8) grid = (int64_t)sms * 8;
+  const size_t smem = sizeof(uint64_t) * (size_t)n_samples;
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      es_perturb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      (int)(sizeof(uint64_t) * kEsMaxSamples));
+  if (attr != cudaSuccess) return fail(OPT_ECUDA, "smem attribute: %s", cudaGetErrorString(attr));
+  es_perturb_kernel<<<(int)grid, 256, smem, s>>>(numel, n_samples, sample0, antithetic,
+                                                 (float)sigma, seed, theta, out);
+  return launched(s);
+}
+
+int opt_es_grad(int64_t numel, int64_t n_samples, int antithetic, double sigma, uint64_t seed,
+                const float* f_values, float* grad, void* stream) {
+  g_err.clear();
+  if (numel < 0 || n_samples < 1) return fail(OPT_EINVAL, "numel < 0 or n_samples < 1");
+  if (n_samples > kEsMaxSamples)
+    return fail(OPT_EINVAL, "n_samples = %lld > %d", (long long)n_samples, kEsMaxSamples);
+  if (!(std::isfinite(sigma) && sigma > 0)) return fail(OPT_EINVAL, "sigma must be > 0");
+  TRY(check_align({grad}));
+  if (numel == 0) return OPT_OK;
+  if (!f_values || !grad) return fail(OPT_EINVAL, "NULL array");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int sms = 0;
+  TRY(sm_count(&sms));
+  const int64_t nvec = numel >> 2;
+  int64_t grid = (nvec + 255) / 256 + 1;
+  if (grid > (int64_t)sms * 8) grid = (int64_t)sms * 8;
+  const size_t smem = (sizeof(uint64_t) + sizeof(float)) * (size_t)n_samples;
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      es_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      (int)((sizeof(uint64_t) + sizeof(float)) * kEsMaxSamples));
+  if (attr != cudaSuccess) return fail(OPT_ECUDA, "smem attribute: %s", cudaGetErrorString(attr));
+  const double scale = antithetic ? 1.0 / (2.0 * (double)n_samples * sigma)
+                                  : 1.0 / ((double)n_samples * sigma);
+  es_grad_kernel<<<(int)grid, 256, smem, s>>>(numel, n_samples, antithetic, scale, seed,
+                                              f_values, grad);
+  return launched(s);
+}
+
+}  // extern "C"

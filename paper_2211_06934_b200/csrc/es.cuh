@@ -1,0 +1,117 @@
+// es.cuh -- zero-order ES estimator kernels.
+//
+// PAPER.md §2.2 "Zero-order Differentiation (ZD)": the gradient of
+// the Gaussian smoothing f~(theta) = E[f(theta + sigma z)] is
+// (1/sigma) E[f(theta + sigma z) z]. Two kernels:
+//   es_perturb: rows theta +/- sigma z_i for the caller's black-box f;
+//   es_grad:    g = c sum_i w_i z_i with w_i = f_i (naive) or
+//               f_i^+ - f_i^- (antithetic), c = 1/(n sigma) or 1/(2 n sigma).
+// The noise is never stored: z_ij is regenerated from a counter-based draw
+// keyed on (seed, sample i, element j) (reading N3):
+//   key_i = mix(seed ^ mix(i + golden)),  w = mix(key_i + j),
+//   u1 = ((w >> 41) + .5) 2^-23,  u2 = ((w & 0x7FFFFF) + .5) 2^-23,
+//   z = sqrt(-2 ln u1) cos(2 pi u2)       (SplitMix64 finaliser `mix`)
+// u1, u2 are exact in fp32; log/sqrt/cospi are the accurate fp32 functions.
+#pragma once
+#include <stdint.h>
+
+#include "vec.cuh"
+
+namespace dopt {
+
+constexpr int kEsMaxSamples = 4096;  // keys + weights staged in shared memory
+
+__host__ __device__ __forceinline__ uint64_t es_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t es_key(uint64_t seed, int64_t i) {
+  return es_mix(seed ^ es_mix((uint64_t)i + 0x9E3779B97F4A7C15ull));
+}
+
+__device__ __forceinline__ float es_normal(uint64_t key, int64_t j) {
+  const uint64_t w = es_mix(key + (uint64_t)j);
+  const float u1 = ((float)(uint32_t)(w >> 41) + 0.5f) * (1.0f / 8388608.0f);
+  const float u2 = ((float)(uint32_t)(w & 0x7FFFFFull) + 0.5f) * (1.0f / 8388608.0f);
+  return sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+}
+
+// out row r starts at r * ld (ld = numel rounded up to 4 elements, so every
+// row is 16-byte aligned): naive r = i, antithetic r = 2i (+) and 2i+1 (-).
+__global__ void __launch_bounds__(256) es_perturb_kernel(int64_t numel, int64_t n_samples,
+                                                         int64_t sample0, int antithetic,
+                                                         float sigma, uint64_t seed,
+                                                         const float* __restrict__ theta,
+                                                         float* __restrict__ out) {
+  extern __shared__ uint64_t s_es[];
+  uint64_t* s_key = s_es;
+  for (int64_t i = threadIdx.x; i < n_samples; i += blockDim.x) s_key[i] = es_key(seed, sample0 + i);
+  __syncthreads();
+  const int reps = antithetic ? 2 : 1;
+  const int64_t ld = (numel + 3) & ~int64_t(3);
+  const int64_t nvec = numel >> 2, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
+    float th[4];
+    load4(theta, v, th);
+    for (int64_t i = 0; i < n_samples; ++i) {
+      const uint64_t key = s_key[i];
+      float p[4], m[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float sz = sigma * es_normal(key, 4 * v + e);
+        p[e] = th[e] + sz;
+        m[e] = th[e] - sz;
+      }
+      float* row = out + (i * reps) * ld;
+      store4(row, v, p);
+      if (antithetic) store4(row + ld, v, m);
+    }
+  }
+  // ragged tail (numel % 4) -> last block
+  const int64_t j = (nvec << 2) + threadIdx.x;
+  if (blockIdx.x == gridDim.x - 1 && j < numel) {
+    for (int64_t i = 0; i < n_samples; ++i) {
+      const float sz = sigma * es_normal(s_key[i], j);
+      out[(i * reps) * ld + j] = theta[j] + sz;
+      if (antithetic) out[(i * reps + 1) * ld + j] = theta[j] - sz;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) es_grad_kernel(int64_t numel, int64_t n_samples,
+                                                      int antithetic, double scale,
+                                                      uint64_t seed,
+                                                      const float* __restrict__ f,
+                                                      float* __restrict__ grad) {
+  extern __shared__ uint64_t s_es[];
+  uint64_t* s_key = s_es;
+  float* s_w = reinterpret_cast<float*>(s_es + n_samples);
+  for (int64_t i = threadIdx.x; i < n_samples; i += blockDim.x) {
+    s_key[i] = es_key(seed, i);
+    s_w[i] = antithetic ? f[2 * i] - f[2 * i + 1] : f[i];
+  }
+  __syncthreads();
+  const int64_t nvec = numel >> 2, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t i = 0; i < n_samples; ++i) {
+      const uint64_t key = s_key[i];
+      const float w = s_w[i];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[e] += (double)(w * es_normal(key, 4 * v + e));
+    }
+    const float o[4] = {(float)(acc[0] * scale), (float)(acc[1] * scale), (float)(acc[2] * scale),
+                        (float)(acc[3] * scale)};
+    store4(grad, v, o);
+  }
+  const int64_t j = (nvec << 2) + threadIdx.x;
+  if (blockIdx.x == gridDim.x - 1 && j < numel) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < n_samples; ++i) acc += (double)(s_w[i] * es_normal(s_key[i], j));
+    grad[j] = (float)(acc * scale);
+  }
+}
+
+}  // namespace dopt

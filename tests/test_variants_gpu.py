@@ -135,24 +135,26 @@ def test_rmsprop_sgd_variants(L, kind, per_leaf, maximize, ct):
 
 
 def test_variant_with_defaults_equals_base(L):
-    """wd = 0, no maximize, lr_leaf = NULL: the *_ex entry points reproduce
-    the base kernels on u, m', v' and dg, dm, dv to an ulp (FMA contraction
-    may differ between the two instantiations), and dtheta = 0 exactly."""
+    """wd = 0, no maximize, lr_leaf = NULL: the *_ex entry points agree with
+    the base kernels to within fp32 rounding of the same arithmetic (FMA
+    contraction may differ between the two instantiations, so the scale is
+    the magnitude twin), and dtheta = 0 exactly."""
     x, th, off, _ = _setup(False)
     tree = L.Tree(offsets=off, device=DEV)
     hp = (1e-2, 0.9, 0.999, 1e-8, 0.0)
     g, m, v, p = dev_f32(x["g"]), dev_f32(x["m"]), dev_f32(x["v"]), dev_f32(th)
+    mag = oracle.adam_mag(x["g"], x["m"], x["v"], x["du"], None, None, 3, *hp)
     a = [torch.empty_like(g) for _ in range(3)]
     b = [torch.empty_like(g) for _ in range(3)]
     L.opt_adam_fwd(tree, 3, hp, 0, 1, g, m, v, *a)
     L.opt_adam_fwd_ex(tree, 3, hp, L._ext(), 0, 1, g, m, v, p, *b)
-    for x1, x2 in zip(a, b):
-        torch.testing.assert_close(x1, x2, rtol=1e-6, atol=1e-12)
+    for x1, x2, k in zip(a, b, ("u", "m1", "v1")):
+        assert np.all(np.abs(host(x1) - host(x2)) <= 1e-6 * mag[k] + 1e-30), k
     du = dev_f32(x["du"])
     a = [torch.empty_like(g) for _ in range(3)]
     b = [torch.empty_like(g) for _ in range(4)]
     L.opt_adam_bwd(tree, 3, hp, 0, 1, g, m, v, du, None, None, *a)
     L.opt_adam_bwd_ex(tree, 3, hp, L._ext(), 0, 1, g, m, v, p, du, None, None, *b)
-    for x1, x2 in zip(a, b[:3]):
-        torch.testing.assert_close(x1, x2, rtol=1e-6, atol=1e-9 * float(x1.abs().max()))
+    for x1, x2, k in zip(a, b[:3], ("dg", "dm", "dv")):
+        assert np.all(np.abs(host(x1) - host(x2)) <= 1e-6 * mag[k] + 1e-30), k
     assert torch.all(b[3] == 0)
