@@ -347,7 +347,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--compute", default="default", choices=["default", "f32", "f64"])
-    ap.add_argument("--workload", default="c2", choices=["c2", "c1", "c5", "c3", "maml"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c1", "c5", "c3", "maml", "es"])
     ap.add_argument("--tasks", type=int, default=32, help="MAML meta-batch (C4)")
     ap.add_argument("--checkpoint-every", type=int, default=None,
                     help="C3: keep only every c-th state and recompute segments (NEXT-2)")
@@ -376,6 +376,8 @@ def main():
         return run_sweep(args, dev, rank, world)
     if args.workload == "maml":
         return run_maml(args, dev, rank, world)
+    if args.workload == "es":
+        return run_es(args, dev, rank, world)
     wl = workload(args)
     r = time_ours(args, wl, dev, rank, world)
     W = r["W"]
@@ -493,6 +495,39 @@ def run_sweep(args, dev, rank, world):
                       "alg_bytes_per_step": per, "launches_per_step": sw.launches_per_sweep},
            "frac_of_measured_hbm": round(value / world / peak, 4),
            "gpu_launches": launches}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def run_es(args, dev, rank, world):
+    """NEXT-3: zero-order ES on a C2-sized parameter vector: perturbation
+    generation (bytes written) and the estimate (normals regenerated / s)."""
+    import torch
+
+    from paper_2211_06934_b200 import _lib as L
+
+    n = int(sum(synth.RESNET18_LEAVES))
+    ns, sigma, seed = 16, 0.01, 5
+    ld = L.es_row_stride(n)
+    theta = torch.randn(n, device=dev, generator=torch.Generator(device=dev).manual_seed(0))
+    pts = torch.empty(2 * ns, ld, device=dev)
+    f = torch.randn(2 * ns, device=dev, generator=torch.Generator(device=dev).manual_seed(1))
+    g = torch.empty(n, device=dev)
+    ms_p = _timed(lambda i: L.opt_es_perturb(n, ns, 0, True, sigma, seed, theta, pts),
+                  args.steps, args.warmup, world)
+    ms_g = _timed(lambda i: L.opt_es_grad(n, ns, True, sigma, seed, f, g), args.steps, args.warmup,
+                  world)
+    wbytes = (2 * ns * n + n) * 4
+    peak, _ = peaks()
+    out = {"metric": "ES perturb GB/s", "value": round(wbytes * args.steps / (ms_p * 1e-3) / 1e9, 1),
+           "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(ms_p / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": "NEXT-3 ES antithetic, C2-sized theta", "numel": n,
+                      "samples": ns, "alg_bytes_perturb": wbytes},
+           "frac_of_measured_hbm": round(wbytes * args.steps / (ms_p * 1e-3) / 1e9 / peak, 4),
+           "es_grad_ms": round(ms_g / args.steps, 4),
+           "es_grad_gnormals_per_s": round(ns * n * args.steps / (ms_g * 1e-3) / 1e9, 2)}
     if rank == 0:
         print(json.dumps(out), flush=True)
 
