@@ -619,3 +619,42 @@ def es_grad(f_values, numel, n_samples, sigma, seed, antithetic=True):
     _es_lib().oracle_es_grad(int(numel), int(n_samples), int(antithetic), float(sigma),
                              int(seed), _p(f), _p(g), _p(ga))
     return g, ga
+
+
+# ---------------------------------------- implicit gradients (NEXT-4)
+def _ig_lib():
+    L = lib()
+    if not getattr(L, "_ig_ready", False):
+        P, i64, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double
+        L.oracle_cg_iter.argtypes = [i64, P, P, P, P, D, P, P, P, P]
+        L.oracle_cg_dense.argtypes = [i64, P, P, i64, P]
+        L.oracle_neumann_dense.argtypes = [i64, P, P, i64, D, P]
+        L._ig_ready = True
+    return L
+
+
+def cg_iter(x, r, p, Ap, rr):
+    """One textbook CG iteration (iMAML); returns x', r', p' and
+    dict(pAp, alpha, rr_new, beta)."""
+    x, r, p, Ap = (_f32(a) for a in (x, r, p, Ap))
+    n = x.size
+    x1, r1, p1, s = _out(n), _out(n), _out(n), np.zeros(4)
+    _ig_lib().oracle_cg_iter(n, _p(x), _p(r), _p(p), _p(Ap), float(rr), _p(x1), _p(r1), _p(p1),
+                             _p(s))
+    return x1, r1, p1, dict(pAp=s[0], alpha=s[1], rr_new=s[2], beta=s[3])
+
+
+def cg_dense(A, b, iters):
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.empty(b.size)
+    _ig_lib().oracle_cg_dense(b.size, _p(A), _p(b), int(iters), _p(x))
+    return x
+
+
+def neumann_dense(A, b, K, alpha):
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.empty(b.size)
+    _ig_lib().oracle_neumann_dense(b.size, _p(A), _p(b), int(K), float(alpha), _p(x))
+    return x

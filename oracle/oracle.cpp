@@ -930,3 +930,84 @@ void oracle_es_grad(int64_t numel, int64_t n_samples, int antithetic, double sig
 }
 
 }  // extern "C"
+
+// ---------------------------------------- implicit gradients (NEXT-4)
+// PAPER.md §2.2 "Implicit Gradient (IG)": the best-response
+// derivative comes from the implicit function theorem, which needs linear
+// solves with dF/dtheta; TorchOpt offers conjugate gradient (iMAML) and
+// Neumann series solvers. Plain textbook forms on explicit data:
+//   CG: r0 = b - A x0, p0 = r0; alpha = r.r / p.Ap; x += alpha p;
+//       r -= alpha Ap; beta = r'.r' / r.r; p = r' + beta p
+//   Neumann: x = alpha sum_{k=0}^{K} (I - alpha A)^k b
+extern "C" {
+
+// One CG iteration on given vectors (fp32 inputs as the GPU holds them):
+// outputs x', r', p' and scalars s = {pAp, alpha, rr_new, beta}.
+void oracle_cg_iter(int64_t n, const float* x, const float* r, const float* p, const float* Ap,
+                    double rr, double* x1, double* r1, double* p1, double* s) {
+  long double pap = 0.0L;
+  for (int64_t i = 0; i < n; ++i) pap += (long double)p[i] * (long double)Ap[i];
+  const double alpha = pap == 0.0L ? 0.0 : rr / (double)pap;
+  long double rrn = 0.0L;
+  for (int64_t i = 0; i < n; ++i) {
+    x1[i] = (double)x[i] + alpha * (double)p[i];
+    r1[i] = (double)r[i] - alpha * (double)Ap[i];
+    rrn += (long double)r1[i] * r1[i];
+  }
+  const double beta = rr == 0.0 ? 0.0 : (double)rrn / rr;
+  for (int64_t i = 0; i < n; ++i) p1[i] = r1[i] + beta * (double)p[i];
+  s[0] = (double)pap;
+  s[1] = alpha;
+  s[2] = (double)rrn;
+  s[3] = beta;
+}
+
+// CG on a dense row-major SPD matrix, `iters` iterations from x0 = 0.
+void oracle_cg_dense(int64_t n, const double* A, const double* b, int64_t iters, double* x) {
+  std::vector<double> r(b, b + n), p(b, b + n), Ap(n);
+  for (int64_t i = 0; i < n; ++i) x[i] = 0.0;
+  double rr = 0.0;
+  for (int64_t i = 0; i < n; ++i) rr += r[i] * r[i];
+  for (int64_t it = 0; it < iters && rr > 0.0; ++it) {
+    for (int64_t i = 0; i < n; ++i) {
+      double s = 0.0;
+      for (int64_t j = 0; j < n; ++j) s += A[i * n + j] * p[j];
+      Ap[i] = s;
+    }
+    double pap = 0.0;
+    for (int64_t i = 0; i < n; ++i) pap += p[i] * Ap[i];
+    const double alpha = rr / pap;
+    double rrn = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      x[i] += alpha * p[i];
+      r[i] -= alpha * Ap[i];
+      rrn += r[i] * r[i];
+    }
+    const double beta = rrn / rr;
+    for (int64_t i = 0; i < n; ++i) p[i] = r[i] + beta * p[i];
+    rr = rrn;
+  }
+}
+
+// Truncated Neumann series x = alpha sum_{k=0}^{K} (I - alpha A)^k b (dense).
+void oracle_neumann_dense(int64_t n, const double* A, const double* b, int64_t K, double alpha,
+                          double* x) {
+  std::vector<double> v(n), t(n);
+  for (int64_t i = 0; i < n; ++i) {
+    v[i] = alpha * b[i];  // alpha (I - alpha A)^0 b
+    x[i] = v[i];
+  }
+  for (int64_t k = 1; k <= K; ++k) {
+    for (int64_t i = 0; i < n; ++i) {
+      double s = 0.0;
+      for (int64_t j = 0; j < n; ++j) s += A[i * n + j] * v[j];
+      t[i] = v[i] - alpha * s;
+    }
+    for (int64_t i = 0; i < n; ++i) {
+      v[i] = t[i];
+      x[i] += v[i];
+    }
+  }
+}
+
+}  // extern "C"

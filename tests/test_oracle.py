@@ -759,3 +759,64 @@ def test_es_quadratic_smoothing_identity(orc):
     th = theta.astype(np.float64)
     se = np.sqrt((th @ th + th ** 2) / n)
     assert np.all(np.abs(g - th) < 5 * se + 1e-12)
+
+
+# ------------------------------------ implicit-gradient solvers (NEXT-4 pins)
+def _spd(n, seed, shift=1.0):
+    rng = np.random.default_rng(seed)
+    M = rng.standard_normal((n, n))
+    return M.T @ M / n + shift * np.eye(n)
+
+
+def test_cg_dense_hand_cases_and_library_solve(orc):
+    """SPEC implicit-diff examples: A = I -> x = b in one iteration;
+    A = diag(1, 2), b = (1, 2) -> x = (1, 1); random SPD 8x8 matches the
+    dense LU solve of numpy.linalg.solve (a different method) to 1e-8."""
+    b = np.array([0.3, -1.0, 2.0])
+    np.testing.assert_allclose(orc.cg_dense(np.eye(3), b, 1), b, rtol=1e-15)
+    np.testing.assert_allclose(orc.cg_dense(np.diag([1.0, 2.0]), [1.0, 2.0], 2), [1.0, 1.0],
+                               rtol=1e-14)
+    A = _spd(8, 1)
+    b = np.random.default_rng(2).standard_normal(8)
+    np.testing.assert_allclose(orc.cg_dense(A, b, 30), np.linalg.solve(A, b), rtol=1e-8)
+
+
+def test_cg_iteration_terminates_in_n_steps(orc):
+    """n textbook CG iterations solve an n x n SPD system (finite termination
+    in exact arithmetic): cg_iter chained n times reaches the dense solve."""
+    n = 6
+    A = _spd(n, 3, shift=2.0)
+    b = np.random.default_rng(4).standard_normal(n)
+    x, r, p = np.zeros(n), b.copy(), b.copy()
+    rr = float(b @ b)
+    for _ in range(n):
+        Ap = A @ p
+        # cg_iter takes fp32 inputs: use float32-exact values via a scaled grid
+        x, r, p, s = orc.cg_iter(x.astype(np.float32), r.astype(np.float32),
+                                 p.astype(np.float32), Ap.astype(np.float32), rr)
+        rr = s["rr_new"]
+    np.testing.assert_allclose(x, np.linalg.solve(A, b), rtol=2e-3, atol=2e-3)
+
+
+def test_cg_iteration_scalars(orc):
+    rng = np.random.default_rng(5)
+    x, r, p, Ap = (rng.standard_normal(50).astype(np.float32) for _ in range(4))
+    rr = float(r.astype(np.float64) @ r.astype(np.float64))
+    x1, r1, p1, s = orc.cg_iter(x, r, p, Ap, rr)
+    pap = float(p.astype(np.float64) @ Ap.astype(np.float64))
+    assert s["pAp"] == pytest.approx(pap, rel=1e-14)
+    assert s["alpha"] == pytest.approx(rr / pap, rel=1e-14)
+    assert s["rr_new"] == pytest.approx(float(r1 @ r1), rel=1e-12)
+    np.testing.assert_allclose(p1, r1 + s["beta"] * p.astype(np.float64), rtol=1e-14)
+
+
+def test_neumann_series_closed_forms(orc):
+    """SPEC: A = I, alpha = 1 -> x = b for any K; A = 2I, alpha = 0.25:
+    x_K = (b/2)(1 - (1/2)^(K+1)) (geometric series) -> b/2, K = 20 within 1e-5."""
+    b = np.array([1.0, -4.0, 0.5])
+    for K in (0, 3, 10):
+        np.testing.assert_allclose(orc.neumann_dense(np.eye(3), b, K, 1.0), b, rtol=1e-15)
+    for K in (0, 5, 20):
+        x = orc.neumann_dense(2 * np.eye(3), b, K, 0.25)
+        np.testing.assert_allclose(x, b / 2 * (1 - 0.5 ** (K + 1)), rtol=1e-14)
+    assert np.max(np.abs(orc.neumann_dense(2 * np.eye(3), b, 20, 0.25) - b / 2)) < 1e-5
