@@ -253,6 +253,31 @@ int opt_es_perturb(int64_t numel, int64_t n_samples, int64_t sample0, int antith
 int opt_es_grad(int64_t numel, int64_t n_samples, int antithetic, double sigma, uint64_t seed,
                 const float* f_values, float* grad, void* stream);
 
+/* ------------------------------ implicit-gradient solvers (SV §8(f) NEXT-4)
+ * PAPER.md §2.2 "Implicit Gradient (IG)": the implicit function
+ * theorem needs linear solves with dF/dtheta, by conjugate gradient (iMAML)
+ * or a Neumann series. The matrix-vector product is the caller's (autograd
+ * HVP/JVP); these calls are the rest of each iteration, fused, on flat fp32
+ * vectors of n elements, with the scalars kept on the device in a
+ * caller-owned double state[8] (state[0] = r.r, [1] = p.Ap, [2] = alpha,
+ * [3] = beta, [4] = r0.r0, [5] = iterations) so no call synchronises:
+ *   opt_cg_init:      r = b - Ax0 (Ax0 NULL: x0 = 0), p = r, rr = rr0 = r.r
+ *   opt_cg_alpha:     pAp = p.Ap, alpha = rr / pAp (0 if pAp == 0)
+ *   opt_cg_update:    x += alpha p, r -= alpha Ap, beta = r.r / rr, rr = r.r
+ *   opt_cg_direction: p = r + beta p
+ *   opt_neumann_step: v = v - alpha Av, x = x + v   (x = alpha sum (I - alpha A)^k b
+ *                     when started from v = x = alpha b)
+ * Dot products are fp64, deterministic (fixed grid and order). workspace:
+ * >= opt_workspace_bytes of a one-leaf tree, zero-filled once. */
+int opt_cg_init(int64_t n, const float* b, const float* Ax0, float* r, float* p, double* state,
+                void* workspace, size_t workspace_bytes, void* stream);
+int opt_cg_alpha(int64_t n, const float* p, const float* Ap, double* state, void* workspace,
+                 size_t workspace_bytes, void* stream);
+int opt_cg_update(int64_t n, float* x, float* r, const float* p, const float* Ap, double* state,
+                  void* workspace, size_t workspace_bytes, void* stream);
+int opt_cg_direction(int64_t n, float* p, const float* r, const double* state, void* stream);
+int opt_neumann_step(int64_t n, float* v, const float* Av, float* x, double alpha, void* stream);
+
 /* -------------------------------------------------------------- misc */
 const char* opt_status_string(int status);
 /* Message of the last failing call on this host thread ("" if none). */

@@ -18,3 +18,4 @@ from .functional import (AdamStep, RmsPropStep, SgdStep, ApplyUpdates, FlatTree,
 __all__ = ["Tree", "DiffoptError", "AdamStep", "RmsPropStep", "SgdStep", "ApplyUpdates",
            "FlatTree", "adam", "rmsprop", "sgd", "apply_updates", "OPT_F32", "OPT_BF16",
            "OPT_COMPUTE_DEFAULT", "OPT_COMPUTE_F32", "OPT_COMPUTE_F64"]
+from . import implicit, offload, unroll  # noqa: E402  (drivers above the C ABI)

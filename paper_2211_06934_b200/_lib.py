@@ -363,3 +363,43 @@ def opt_es_perturb(numel, n_samples, sample0, antithetic, sigma, seed, theta, ou
 def opt_es_grad(numel, n_samples, antithetic, sigma, seed, f_values, grad, stream=None):
     _check(lib.opt_es_grad(int(numel), int(n_samples), int(bool(antithetic)), float(sigma),
                            int(seed), _ptr(f_values), _ptr(grad), _stream(stream)))
+
+
+# ---------------------------------------- implicit-gradient solvers (NEXT-4)
+_P, _i64, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t
+lib.opt_cg_init.argtypes = [_i64] + [_P] * 6 + [_sz, _P]
+lib.opt_cg_alpha.argtypes = [_i64] + [_P] * 4 + [_sz, _P]
+lib.opt_cg_update.argtypes = [_i64] + [_P] * 6 + [_sz, _P]
+lib.opt_cg_direction.argtypes = [_i64, _P, _P, _P, _P]
+lib.opt_neumann_step.argtypes = [_i64, _P, _P, _P, ctypes.c_double, _P]
+for _n in ("opt_cg_init", "opt_cg_alpha", "opt_cg_update", "opt_cg_direction",
+           "opt_neumann_step"):
+    getattr(lib, _n).restype = ctypes.c_int
+EXPORTS += ["opt_cg_init", "opt_cg_alpha", "opt_cg_update", "opt_cg_direction",
+            "opt_neumann_step"]
+
+
+def opt_cg_init(n, b, Ax0, r, p, state, workspace, stream=None):
+    wp, wb = _ws(workspace)
+    _check(lib.opt_cg_init(int(n), _ptr(b), _ptr(Ax0), _ptr(r), _ptr(p), _ptr(state), wp, wb,
+                           _stream(stream)))
+
+
+def opt_cg_alpha(n, p, Ap, state, workspace, stream=None):
+    wp, wb = _ws(workspace)
+    _check(lib.opt_cg_alpha(int(n), _ptr(p), _ptr(Ap), _ptr(state), wp, wb, _stream(stream)))
+
+
+def opt_cg_update(n, x, r, p, Ap, state, workspace, stream=None):
+    wp, wb = _ws(workspace)
+    _check(lib.opt_cg_update(int(n), _ptr(x), _ptr(r), _ptr(p), _ptr(Ap), _ptr(state), wp, wb,
+                             _stream(stream)))
+
+
+def opt_cg_direction(n, p, r, state, stream=None):
+    _check(lib.opt_cg_direction(int(n), _ptr(p), _ptr(r), _ptr(state), _stream(stream)))
+
+
+def opt_neumann_step(n, v, Av, x, alpha, stream=None):
+    _check(lib.opt_neumann_step(int(n), _ptr(v), _ptr(Av), _ptr(x), float(alpha),
+                                _stream(stream)))

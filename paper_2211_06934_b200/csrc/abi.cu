@@ -994,3 +994,84 @@ int opt_es_grad(int64_t numel, int64_t n_samples, int antithetic, double sigma, 
 }
 
 }  // extern "C"
+
+// ------------------------------------- implicit gradients (NEXT-4, implicit.cuh)
+#include "implicit.cuh"
+
+namespace {
+
+template <int MODE>
+int cg_launch(int64_t n, float* x, float* r, float* p, const float* Ap, const float* b,
+              const float* Ax0, double* state, void* ws, size_t wsb, void* stream) {
+  if (n < 0) return fail(OPT_EINVAL, "n < 0");
+  TRY(check_align({x, r, p, Ap, b, Ax0}));
+  if (!state) return fail(OPT_EINVAL, "state is NULL");
+  const bool reduce = MODE != CG_DIR;
+  const size_t need = kCounterBytes + sizeof(double) * (size_t)kMaxGrid;
+  if (reduce && (!ws || wsb < need))
+    return fail(OPT_EWORKSPACE, "workspace %p of %zu bytes; need %zu", ws, wsb, need);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CgArgs a{};
+  a.n = n; a.x = x; a.r = r; a.p = p; a.Ap = Ap; a.b = b; a.Ax0 = Ax0; a.state = state;
+  if (reduce) {
+    a.counter = static_cast<unsigned int*>(ws);
+    a.partials = reinterpret_cast<double*>(static_cast<char*>(ws) + kCounterBytes);
+  }
+  auto k = cg_kernel<MODE>;
+  int grid = 0;
+  TRY(grid_for(k, ((n >> 2) + kBlock - 1) / kBlock + 1, 0, &grid));
+  k<<<grid, kBlock, 0, s>>>(a);
+  return launched(s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int opt_cg_init(int64_t n, const float* b, const float* Ax0, float* r, float* p, double* state,
+                void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (!b || !r || !p) return fail(OPT_EINVAL, "NULL array");
+  return cg_launch<CG_INIT>(n, nullptr, r, p, nullptr, b, Ax0, state, workspace,
+                            workspace_bytes, stream);
+}
+
+int opt_cg_alpha(int64_t n, const float* p, const float* Ap, double* state, void* workspace,
+                 size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (!p || !Ap) return fail(OPT_EINVAL, "NULL array");
+  return cg_launch<CG_ALPHA_MODE>(n, nullptr, nullptr, const_cast<float*>(p), Ap, nullptr,
+                                  nullptr, state, workspace, workspace_bytes, stream);
+}
+
+int opt_cg_update(int64_t n, float* x, float* r, const float* p, const float* Ap, double* state,
+                  void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (!x || !r || !p || !Ap) return fail(OPT_EINVAL, "NULL array");
+  return cg_launch<CG_UPD>(n, x, r, const_cast<float*>(p), Ap, nullptr, nullptr, state,
+                           workspace, workspace_bytes, stream);
+}
+
+int opt_cg_direction(int64_t n, float* p, const float* r, const double* state, void* stream) {
+  g_err.clear();
+  if (!p || !r) return fail(OPT_EINVAL, "NULL array");
+  return cg_launch<CG_DIR>(n, nullptr, const_cast<float*>(r), p, nullptr, nullptr, nullptr,
+                           const_cast<double*>(state), nullptr, 0, stream);
+}
+
+int opt_neumann_step(int64_t n, float* v, const float* Av, float* x, double alpha,
+                     void* stream) {
+  g_err.clear();
+  if (n < 0) return fail(OPT_EINVAL, "n < 0");
+  if (!std::isfinite(alpha)) return fail(OPT_EINVAL, "alpha not finite");
+  TRY(check_align({v, Av, x}));
+  if (n == 0) return OPT_OK;
+  if (!v || !Av || !x) return fail(OPT_EINVAL, "NULL array");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int grid = 0;
+  TRY(grid_for(neumann_kernel, ((n >> 2) + kBlock - 1) / kBlock + 1, 0, &grid));
+  neumann_kernel<<<grid, kBlock, 0, s>>>(n, v, Av, x, (float)alpha);
+  return launched(s);
+}
+
+}  // extern "C"
