@@ -209,7 +209,7 @@ int setup_reduce(const opt_tree* t, double* d_hp, double* d_hp_leaf, const float
       return fail(OPT_EINVAL, "per-leaf outputs/lr support at most %d leaves (got %lld)",
                   kMaxLeafSmem, (long long)t->n_leaves);
     if (!t->d_offsets) return fail(OPT_EINVAL, "per-leaf outputs/lr need tree->d_offsets");
-        r->n_tiles = count_tiles(t);
+    r->n_tiles = count_tiles(t);
   }
   if (!d_hp && !d_hp_leaf) return OPT_OK;
   size_t need = opt_workspace_bytes(t, r->leaf ? 1 : 0);
@@ -244,6 +244,12 @@ int zero_outputs(const opt_tree* t, int nh, double* d_hp, double* d_hp_leaf, cud
 #endif
 #ifndef DOPT_MINB_BWD
 #define DOPT_MINB_BWD 3
+#endif
+#ifndef DOPT_U_FWD_BF16
+#define DOPT_U_FWD_BF16 DOPT_U_FWD
+#endif
+#ifndef DOPT_U_BWD_BF16
+#define DOPT_U_BWD_BF16 DOPT_U_BWD
 #endif
 
 #ifndef DOPT_TMA_FWD
@@ -337,6 +343,8 @@ template <template <class> class OpT, bool kBwd, class Fill>
 int dispatch(int state_dtype, int ct, StepArgs<OpT<float>::NIN, OpT<float>::NOUT>& a,
              const Reduce& r, const opt_tree* t, cudaStream_t s, Fill fill) {
   constexpr int U = kBwd ? DOPT_U_BWD : DOPT_U_FWD;
+  // bf16 state moves 8-byte vectors: more of them in flight per thread
+  constexpr int UB = kBwd ? DOPT_U_BWD_BF16 : DOPT_U_FWD_BF16;
   constexpr bool TMA = kBwd ? (DOPT_TMA_BWD != 0) : (DOPT_TMA_FWD != 0);
   if (ct == OPT_COMPUTE_F64) {
     OpT<double> op;
@@ -348,7 +356,7 @@ int dispatch(int state_dtype, int ct, StepArgs<OpT<float>::NIN, OpT<float>::NOUT
   OpT<float> op;
   fill(op);
   constexpr int MB = minb_for<OpT<float>, kBwd>();
-  if (state_dtype == OPT_BF16) return launch<OpT<float>, bf16, U, MB, TMA>(op, a, r, t, s);
+  if (state_dtype == OPT_BF16) return launch<OpT<float>, bf16, UB, MB, TMA>(op, a, r, t, s);
   return launch<OpT<float>, float, U, MB, TMA>(op, a, r, t, s);
 }
 

@@ -16,6 +16,9 @@ def one(cfg):
     uf, mf, ub, mb, extra = cfg
     tag = f"{uf}-{mf}-{ub}-{mb}" + (f"-{extra}" if extra else "")
     defs = [f"DOPT_U_FWD={uf}", f"DOPT_MINB_FWD={mf}", f"DOPT_U_BWD={ub}", f"DOPT_MINB_BWD={mb}"]
+    if "ub" in extra:  # e.g. ub2x2: bf16 U fwd x bwd
+        spec = extra.split("ub")[1][:3]
+        defs += [f"DOPT_U_FWD_BF16={spec[0]}", f"DOPT_U_BWD_BF16={spec[2]}"]
     if "pdl" in extra:
         defs.append("DOPT_PDL=1")
     if "ieee" in extra:
