@@ -465,11 +465,11 @@ SgdVjpEx<T> sgd_vjp_ex(T g, T b, T theta, T du, T db1_out, const SgdHP<T>& h, co
 // The noise z_ij is a counter-based draw keyed on (seed, sample i, element j)
 // so that it never has to be stored (reading N3); this file implements that
 // generator itself (it shares no code with the CUDA side, which implements
-// the same definition):
-//   key  = mix(seed ^ mix(i + 0x9E3779B97F4A7C15)),  w = mix(key + j)
+// the same definition). Box-Muller pairs: elements 2k and 2k+1 share one draw
+//   key  = mix(seed ^ mix(i + 0x9E3779B97F4A7C15)),  w = mix(key + k)
 //   u1 = ((w >> 41) + 0.5) 2^-23,  u2 = ((w & 0x7FFFFF) + 0.5) 2^-23
-// (23-bit uniforms: k + 0.5 is then exact in fp32 as well as fp64)
-//   z  = sqrt(-2 ln u1) cos(2 pi u2)                       (Box-Muller)
+//   (23-bit uniforms: k + 0.5 is then exact in fp32 as well as fp64)
+//   z_2k = sqrt(-2 ln u1) cos(2 pi u2),  z_2k+1 = sqrt(-2 ln u1) sin(2 pi u2)
 // with mix the SplitMix64 finaliser.
 namespace oracle {
 
@@ -481,10 +481,11 @@ inline uint64_t es_mix(uint64_t z) {
 
 inline double es_normal(uint64_t seed, int64_t i, int64_t j) {
   const uint64_t key = es_mix(seed ^ es_mix((uint64_t)i + 0x9E3779B97F4A7C15ull));
-  const uint64_t w = es_mix(key + (uint64_t)j);
+  const uint64_t w = es_mix(key + (uint64_t)(j >> 1));
   const double u1 = ((double)(w >> 41) + 0.5) * (1.0 / 8388608.0);
   const double u2 = ((double)(w & 0x7FFFFFull) + 0.5) * (1.0 / 8388608.0);
-  return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.14159265358979323846 * u2);
+  const double r = std::sqrt(-2.0 * std::log(u1)), a = 2.0 * 3.14159265358979323846 * u2;
+  return (j & 1) ? r * std::sin(a) : r * std::cos(a);
 }
 
 }  // namespace oracle

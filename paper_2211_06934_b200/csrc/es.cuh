@@ -7,11 +7,12 @@
 //   es_grad:    g = c sum_i w_i z_i with w_i = f_i (naive) or
 //               f_i^+ - f_i^- (antithetic), c = 1/(n sigma) or 1/(2 n sigma).
 // The noise is never stored: z_ij is regenerated from a counter-based draw
-// keyed on (seed, sample i, element j) (reading N3):
-//   key_i = mix(seed ^ mix(i + golden)),  w = mix(key_i + j),
+// keyed on (seed, sample i, element pair k = j/2) (reading N3):
+//   key_i = mix(seed ^ mix(i + golden)),  w = mix(key_i + k),
 //   u1 = ((w >> 41) + .5) 2^-23,  u2 = ((w & 0x7FFFFF) + .5) 2^-23,
-//   z = sqrt(-2 ln u1) cos(2 pi u2)       (SplitMix64 finaliser `mix`)
-// u1, u2 are exact in fp32; log/sqrt/cospi are the accurate fp32 functions.
+//   z_2k = sqrt(-2 ln u1) cos(2 pi u2), z_2k+1 = sqrt(-2 ln u1) sin(2 pi u2)
+// (SplitMix64 finaliser `mix`; one draw per Box-Muller pair). u1, u2 are
+// exact in fp32; log/sqrt/sincospi are the accurate fp32 functions.
 #pragma once
 #include <stdint.h>
 
@@ -31,11 +32,28 @@ __device__ __forceinline__ uint64_t es_key(uint64_t seed, int64_t i) {
   return es_mix(seed ^ es_mix((uint64_t)i + 0x9E3779B97F4A7C15ull));
 }
 
-__device__ __forceinline__ float es_normal(uint64_t key, int64_t j) {
-  const uint64_t w = es_mix(key + (uint64_t)j);
+// the Box-Muller pair (z_2k, z_2k+1)
+__device__ __forceinline__ void es_pair(uint64_t key, int64_t k, float& z0, float& z1) {
+  const uint64_t w = es_mix(key + (uint64_t)k);
   const float u1 = ((float)(uint32_t)(w >> 41) + 0.5f) * (1.0f / 8388608.0f);
   const float u2 = ((float)(uint32_t)(w & 0x7FFFFFull) + 0.5f) * (1.0f / 8388608.0f);
-  return sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+  const float r = sqrtf(-2.0f * logf(u1));
+  float sn, cs;
+  sincospif(2.0f * u2, &sn, &cs);
+  z0 = r * cs;
+  z1 = r * sn;
+}
+
+__device__ __forceinline__ float es_normal(uint64_t key, int64_t j) {
+  float z0, z1;
+  es_pair(key, j >> 1, z0, z1);
+  return (j & 1) ? z1 : z0;
+}
+
+// the 4 draws of vector v (elements 4v .. 4v+3 = pairs 2v, 2v+1)
+__device__ __forceinline__ void es_quad(uint64_t key, int64_t v, float (&z)[4]) {
+  es_pair(key, 2 * v, z[0], z[1]);
+  es_pair(key, 2 * v + 1, z[2], z[3]);
 }
 
 // out row r starts at r * ld (ld = numel rounded up to 4 elements, so every
@@ -56,11 +74,11 @@ __global__ void __launch_bounds__(256) es_perturb_kernel(int64_t numel, int64_t 
     float th[4];
     load4(theta, v, th);
     for (int64_t i = 0; i < n_samples; ++i) {
-      const uint64_t key = s_key[i];
-      float p[4], m[4];
+      float z[4], p[4], m[4];
+      es_quad(s_key[i], v, z);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float sz = sigma * es_normal(key, 4 * v + e);
+        const float sz = sigma * z[e];
         p[e] = th[e] + sz;
         m[e] = th[e] - sz;
       }
@@ -97,10 +115,11 @@ __global__ void __launch_bounds__(256) es_grad_kernel(int64_t numel, int64_t n_s
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t i = 0; i < n_samples; ++i) {
-      const uint64_t key = s_key[i];
       const float w = s_w[i];
+      float z[4];
+      es_quad(s_key[i], v, z);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[e] += (double)(w * es_normal(key, 4 * v + e));
+      for (int e = 0; e < 4; ++e) acc[e] += (double)(w * z[e]);
     }
     const float o[4] = {(float)(acc[0] * scale), (float)(acc[1] * scale), (float)(acc[2] * scale),
                         (float)(acc[3] * scale)};
