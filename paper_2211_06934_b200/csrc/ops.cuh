@@ -36,10 +36,25 @@ __device__ __forceinline__ float ct_sqrt(float x) { return sqrtf(x); }
 __device__ __forceinline__ float ct_div(float a, float b) { return a / b; }
 __device__ __forceinline__ float rsqrt_or_zero(float x) { return x > 0.f ? 1.f / sqrtf(x) : 0.f; }
 #else
-__device__ __forceinline__ float safe_rcp(float x) { return x == 0.f ? 0.f : __fdividef(1.f, x); }
-__device__ __forceinline__ float ct_sqrt(float x) { return x > 0.f ? x * rsqrtf(x) : 0.f; }
-__device__ __forceinline__ float ct_div(float a, float b) { return __fdividef(a, b); }
-__device__ __forceinline__ float rsqrt_or_zero(float x) { return x > 0.f ? rsqrtf(x) : 0.f; }
+// Raw MUFU approximations (rcp.approx / rsqrt.approx, ftz on the MUFU
+// operand only): branch-free, no denormal fix-up sequences. Operands below
+// FLT_MIN take the zero branch of the Z6/Z7 conventions (s or d treated as
+// 0); such an s is < 1e-19, 11 orders below eps, so only eps = 0 can see it.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr float kFltMin = 1.17549435e-38f;
+__device__ __forceinline__ float safe_rcp(float x) { return x >= kFltMin ? rcp_approx(x) : 0.f; }
+__device__ __forceinline__ float ct_sqrt(float x) { return x >= kFltMin ? x * rsqrt_approx(x) : 0.f; }
+__device__ __forceinline__ float ct_div(float a, float b) { return a * safe_rcp(b); }
+__device__ __forceinline__ float rsqrt_or_zero(float x) { return x >= kFltMin ? rsqrt_approx(x) : 0.f; }
 #endif
 
 // Every op exposes apply() on compute-type scalars (so the variants below
@@ -62,7 +77,7 @@ struct AdamFwd {
     v1 = b2 * v + om2 * (g * g);
     const CT s = ct_sqrt(v1 * ibc2 + eps_root);
     const CT d = s + eps;
-    u = d == CT(0) ? CT(0) : ct_div(-lr * (m1 * ibc1), d);
+    u = (-lr * (m1 * ibc1)) * safe_rcp(d);  // Z7: u = 0 when d = 0
   }
   __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT*,
                                              bool) const {
@@ -133,7 +148,7 @@ struct RmsFwd {
   __device__ __forceinline__ void apply(CT g, CT v, CT& u, CT& v1) const {
     v1 = alpha * v + oma * (g * g);
     const CT d = ct_sqrt(v1) + eps;
-    u = d == CT(0) ? CT(0) : ct_div(-lr * g, d);
+    u = (-lr * g) * safe_rcp(d);  // Z7: u = 0 when d = 0
   }
   __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT*,
                                              bool) const {
