@@ -29,7 +29,7 @@ class HostStreamedAdam:
         self.bounds = [(s, min(s + per, self.n)) for s in range(0, self.n, per)]
         self.trees = [L.Tree(numel=e - s, device=device) for s, e in self.bounds]
         self.ws = [t.workspace(device) for t in self.trees]
-        nb = 2  # double-buffered device staging
+        self.nb = nb = 3  # staging slots: H2D of chunk c overlaps D2H of c-1 and c-2
         self.buf = [{k: torch.empty(per, device=device) for k in IN_KEYS + OUT_KEYS}
                     for _ in range(nb)]
         self.dhp = torch.empty(len(self.bounds), 4, dtype=torch.float64, device=device)
@@ -53,11 +53,11 @@ class HostStreamedAdam:
             s.wait_stream(cur)
         h2d_done, cmp_done, d2h_done = [], [], []
         for c, (lo, hi) in enumerate(self.bounds):
-            b = self.buf[c % 2]
+            b = self.buf[c % self.nb]
             k = hi - lo
             with torch.cuda.stream(self.s_h2d):
-                if c >= 2:  # staging slot reused: wait until chunk c-2 left the device
-                    self.s_h2d.wait_event(d2h_done[c - 2])
+                if c >= self.nb:  # staging slot reused: wait until chunk c-nb left the device
+                    self.s_h2d.wait_event(d2h_done[c - self.nb])
                 for key in IN_KEYS:
                     b[key][:k].copy_(host_in[key][lo:hi], non_blocking=True)
                 e = torch.cuda.Event()
