@@ -289,4 +289,6 @@ def test_host_streamed_step_equals_device_step(pkg):
                    o["dg"], o["dm"], o["dv"], dhp, None, tree.workspace(DEV))
     for k in OUT_KEYS:
         assert torch.equal(h_out[k], o[k].cpu()), k
-    np.testing.assert_allclose(HostStreamedAdam.combine(h_dhp), host(dhp), rtol=1e-12)
+    ref = oracle.adam_vjp(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], 4, *hp)
+    np.testing.assert_allclose(HostStreamedAdam.combine(h_dhp), host(dhp), rtol=1e-9,
+                               atol=1e-12 * ref["dhp_abs"].max())
