@@ -236,6 +236,14 @@ def time_ours(args, workload_inputs, dev, rank, world):
 
     # end-to-end through the C ABI with host buffers (pinned), copies timed
     e2e = None if args.quick else time_e2e(args, W, dev)
+    if e2e is not None and world > 1:  # whole-job value: slowest rank, all ranks' bytes
+        tt = torch.tensor([e2e["ms_per_step"]], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e["ms_per_step"] = float(tt.item())
+        e2e["value"] = round(world * (W.bytes_fwd + W.bytes_bwd) / (e2e["ms_per_step"] * 1e-3)
+                             / 1e9, 2)
+        e2e["h2d_bytes_per_step"] *= world
+        e2e["d2h_bytes_per_step"] *= world
     return dict(ms=ms, fwd_ms=fwd_ms, bwd_ms=bwd_ms, clocks=clocks, launches=launches, W=W,
                 e2e=e2e, wname=wname, sets=sets)
 

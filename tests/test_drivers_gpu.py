@@ -292,3 +292,23 @@ def test_host_streamed_step_equals_device_step(pkg):
     ref = oracle.adam_vjp(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], 4, *hp)
     np.testing.assert_allclose(HostStreamedAdam.combine(h_dhp), host(dhp), rtol=1e-9,
                                atol=1e-12 * ref["dhp_abs"].max())
+
+
+def test_sharded_adam_fused_local_step(pkg):
+    """ShardedAdam's fused shard step (world = 1: the whole padded tree is
+    the shard) equals three plain opt_adam_fwd steps with apply."""
+    from paper_2211_06934_b200 import sharded
+
+    n = 70001
+    opt = sharded.ShardedAdam(n, 1, 0, DEV, lr=1e-2)
+    p = torch.zeros(opt.n_pad, device=DEV)
+    p[:n] = torch.linspace(-1, 1, n, device=DEV)
+    ref = p.clone()
+    L = pkg._lib
+    tree = L.Tree(numel=opt.n_pad, device=DEV)
+    m, v = torch.zeros_like(p), torch.zeros_like(p)
+    for t in range(1, 4):
+        g = torch.randn(opt.n_pad, device=DEV, generator=torch.Generator(device=DEV).manual_seed(t))
+        opt.step(p, g)
+        L.opt_adam_fwd(tree, t, (1e-2, 0.9, 0.999, 1e-8, 0.0), 0, 0, g, m, v, None, m, v, ref, ref)
+    assert torch.equal(p, ref)
