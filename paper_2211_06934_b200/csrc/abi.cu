@@ -173,6 +173,12 @@ cudaError_t launch_k(K kernel, int grid, int block, size_t smem, cudaStream_t s,
 #endif
 }
 
+#define TRY(x)                \
+  do {                        \
+    int rc_ = (x);            \
+    if (rc_) return rc_;      \
+  } while (0)
+
 int launched(cudaStream_t) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(OPT_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
@@ -192,6 +198,8 @@ struct Reduce {
   int64_t n_tiles;
   double* partials;
   unsigned int* counter;
+  int64_t* tile_prefix;  // leaf mode: [n_leaves+1]
+  double* block_part;    // leaf mode: leaf_finalize block partials
 };
 
 int setup_reduce(const opt_tree* t, double* d_hp, double* d_hp_leaf, const float* lr_leaf,
@@ -203,6 +211,8 @@ int setup_reduce(const opt_tree* t, double* d_hp, double* d_hp_leaf, const float
   r->n_tiles = 0;
   r->partials = nullptr;
   r->counter = nullptr;
+  r->tile_prefix = nullptr;
+  r->block_part = nullptr;
   if (r->leaf) {
     if (t->n_leaves < 1) return fail(OPT_EINVAL, "per-leaf outputs/lr need n_leaves >= 1");
     if (t->n_leaves > kMaxLeafSmem)
@@ -218,6 +228,11 @@ int setup_reduce(const opt_tree* t, double* d_hp, double* d_hp_leaf, const float
   if (reinterpret_cast<uintptr_t>(ws) & 15u) return fail(OPT_EALIGN, "workspace not 16-byte aligned");
   r->counter = static_cast<unsigned int*>(ws);
   r->partials = reinterpret_cast<double*>(static_cast<char*>(ws) + kCounterBytes);
+  if (r->leaf) {
+    const int64_t slots = r->n_tiles > kMaxGrid ? r->n_tiles : kMaxGrid;
+    r->tile_prefix = reinterpret_cast<int64_t*>(r->partials + kNhMax * slots);
+    r->block_part = reinterpret_cast<double*>(r->tile_prefix + t->n_leaves + 1);
+  }
   return OPT_OK;
 }
 
@@ -310,6 +325,7 @@ int launch(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r, const 
   a.partials = r.partials;
   a.counter = r.counter;
   a.lr_leaf = r.lr_leaf;
+  a.tile_prefix = r.tile_prefix;
   a.want_hp = (r.d_hp || r.d_hp_leaf) ? 1 : 0;
   if (r.leaf) {
     a.offsets = t->d_offsets;
@@ -325,7 +341,17 @@ int launch(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r, const 
     if (rc) return rc;
     cudaError_t le = launch_k(k, grid, kBlock, smem, s, op, a);
     if (le != cudaSuccess) return fail(OPT_ECUDA, "launch: %s", cudaGetErrorString(le));
-    return launched(s);
+    TRY(launched(s));
+    if constexpr (Op::NH > 0) {
+      if (a.want_hp) {  // per-leaf and global sums of the tile partials
+        constexpr int NH = Op::NH;
+        const int fg = (int)((t->n_leaves + kWarps - 1) / kWarps);
+        leaf_finalize<NH><<<fg, kBlock, 0, s>>>(r.partials, r.tile_prefix, t->n_leaves,
+                                               r.d_hp_leaf, r.d_hp, r.block_part, r.counter);
+        TRY(launched(s));
+      }
+    }
+    return OPT_OK;
   }
   if (kTma) return launch_tma<Op, ST>(op, a, s);
   auto k = step_uniform<Op, ST, U, MINB>;
@@ -398,11 +424,6 @@ int check_sgd(const opt_sgd_hp* hp) {
   return OPT_OK;
 }
 
-#define TRY(x)                \
-  do {                        \
-    int rc_ = (x);            \
-    if (rc_) return rc_;      \
-  } while (0)
 
 
 // Per-step constants of each op (row a2): computed in double, rounded once
@@ -486,11 +507,15 @@ extern "C" {
 size_t opt_workspace_bytes(const opt_tree* tree, int per_leaf) {
   if (check_tree(tree)) return 0;
   int64_t slots = kMaxGrid;
+  size_t extra = 0;
   if (per_leaf) {
     int64_t nt = count_tiles(tree);
     if (nt > slots) slots = nt;
+    // tile prefix [n_leaves+1] + leaf_finalize block partials
+    extra = sizeof(int64_t) * (size_t)(tree->n_leaves + 1) +
+            sizeof(double) * kNhMax * (size_t)((tree->n_leaves + kWarps - 1) / kWarps);
   }
-  return kCounterBytes + sizeof(double) * kNhMax * (size_t)slots;
+  return kCounterBytes + sizeof(double) * kNhMax * (size_t)slots + extra;
 }
 
 // ------------------------------------------------------------------ Adam

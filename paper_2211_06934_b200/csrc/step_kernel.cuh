@@ -39,6 +39,7 @@ struct StepArgs {
   unsigned int* counter; // workspace: arrival ticket, left at 0
   const int64_t* offsets;  // device offsets (leaf mode)
   const float* lr_leaf;    // per-leaf learning rates (leaf mode) or NULL
+  int64_t* tile_prefix;    // workspace (leaf mode): first tile of every leaf, [n_leaves+1]
   int64_t n_leaves;
   int64_t n_tiles;
   int want_hp;
@@ -293,6 +294,8 @@ __global__ void __launch_bounds__(kBlock, MINB) step_leaf(const Op op,
     if (threadIdx.x == kBlock - 1) s_tp[nl] = a.n_tiles;
   }
   __syncthreads();
+  if (blockIdx.x == 0 && want_hp)  // for leaf_finalize
+    for (int64_t l = threadIdx.x; l <= nl; l += kBlock) a.tile_prefix[l] = s_tp[l];
 
   for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
     // leaf = last l with s_tp[l] <= tile and a non-empty range
@@ -328,30 +331,62 @@ __global__ void __launch_bounds__(kBlock, MINB) step_leaf(const Op op,
     }
   }
 
-  if (!want_hp) return;
-  if (last_block(a.counter, gridDim.x)) {
+}
+
+// Per-leaf sums of the tile partials (second launch of leaf mode): one warp
+// per leaf, lanes stride over the leaf's tiles, xor-shuffle; one fp64 partial
+// per block of the leaf sums (in warp = leaf order) and the last block sums
+// those in block order into d_hp. Deterministic for a fixed grid.
+template <int NH>
+__global__ void __launch_bounds__(kBlock) leaf_finalize(const double* partials,
+                                                        const int64_t* tile_prefix,
+                                                        int64_t n_leaves, double* d_hp_leaf,
+                                                        double* d_hp, double* block_part,
+                                                        unsigned int* counter) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t l = (int64_t)blockIdx.x * kWarps + warp;
+  double s[NH];
+#pragma unroll
+  for (int k = 0; k < NH; ++k) s[k] = 0.0;
+  if (l < n_leaves) {
+    const int64_t t0 = tile_prefix[l], t1 = tile_prefix[l + 1];
+    for (int64_t t = t0 + lane; t < t1; t += 32)
+#pragma unroll
+      for (int k = 0; k < NH; ++k) s[k] += __ldcg(&partials[t * NH + k]);
+  }
+#pragma unroll
+  for (int k = 0; k < NH; ++k) s[k] = warp_sum(s[k]);
+  __shared__ double sm[NH][kWarps];
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+      if (l < n_leaves && d_hp_leaf) d_hp_leaf[l * NH + k] = s[k];
+      sm[k][warp] = l < n_leaves ? s[k] : 0.0;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+      double b = 0.0;
+      for (int w = 0; w < kWarps; ++w) b += sm[k][w];
+      block_part[(int64_t)blockIdx.x * NH + k] = b;
+    }
+  }
+  if (last_block(counter, gridDim.x)) {
     double tot[NH];
 #pragma unroll
     for (int k = 0; k < NH; ++k) tot[k] = 0.0;
-    for (int64_t l = threadIdx.x; l < nl; l += kBlock) {
-      double s[NH];
+    for (int64_t b = threadIdx.x; b < gridDim.x; b += kBlock)
 #pragma unroll
-      for (int k = 0; k < NH; ++k) s[k] = 0.0;
-      for (int64_t t = s_tp[l]; t < s_tp[l + 1]; ++t)
-#pragma unroll
-        for (int k = 0; k < NH; ++k) s[k] += __ldcg(&a.partials[t * NH + k]);
-#pragma unroll
-      for (int k = 0; k < NH; ++k) {
-        if (a.d_hp_leaf) a.d_hp_leaf[l * NH + k] = s[k];
-        tot[k] += s[k];
-      }
-    }
+      for (int k = 0; k < NH; ++k) tot[k] += __ldcg(&block_part[b * NH + k]);
     block_sum<NH>(tot, sm);
     if (threadIdx.x == 0) {
 #pragma unroll
       for (int k = 0; k < NH; ++k)
-        if (a.d_hp) a.d_hp[k] = tot[k];
-      *a.counter = 0u;
+        if (d_hp) d_hp[k] = tot[k];
+      *counter = 0u;
     }
   }
 }
