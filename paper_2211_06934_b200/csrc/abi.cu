@@ -337,7 +337,7 @@ int launch(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r, const 
         k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(int64_t) * 2 * (kMaxLeafSmem + 1)));
     if (attr != cudaSuccess) return fail(OPT_ECUDA, "smem attribute: %s", cudaGetErrorString(attr));
     int grid = 0;
-    int rc = grid_for(k, r.n_tiles, smem, &grid);
+    int rc = grid_for(k, (r.n_tiles + kWarps - 1) / kWarps, smem, &grid);
     if (rc) return rc;
     cudaError_t le = launch_k(k, grid, kBlock, smem, s, op, a);
     if (le != cudaSuccess) return fail(OPT_ECUDA, "launch: %s", cudaGetErrorString(le));
@@ -985,16 +985,24 @@ int opt_es_perturb(int64_t numel, int64_t n_samples, int64_t sample0, int antith
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int sms = 0;
   TRY(sm_count(&sms));
-  const int64_t nvec = numel >> 2;
-  int64_t grid = (nvec + 255) / 256 + 1;
+  const int64_t nvec = (numel + 3) >> 2;
+  const int64_t capacity = (int64_t)sms * 2048;  // resident threads
+  // samples per thread: all of them when the tree alone fills the GPU
+  int64_t groups = capacity / (nvec > 0 ? nvec : 1);
+  if (groups < 1) groups = 1;
+  if (groups > n_samples) groups = n_samples;
+  const int64_t spg = (n_samples + groups - 1) / groups;
+  const int64_t work = nvec * ((n_samples + spg - 1) / spg);
+  int64_t grid = (work + 255) / 256;
   if (grid > (int64_t)sms * 8) grid = (int64_t)sms * 8;
+  if (grid < 1) grid = 1;
   const size_t smem = sizeof(uint64_t) * (size_t)n_samples;
   static const cudaError_t attr = cudaFuncSetAttribute(
       es_perturb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
       (int)(sizeof(uint64_t) * kEsMaxSamples));
   if (attr != cudaSuccess) return fail(OPT_ECUDA, "smem attribute: %s", cudaGetErrorString(attr));
   es_perturb_kernel<<<(int)grid, 256, smem, s>>>(numel, n_samples, sample0, antithetic,
-                                                 (float)sigma, seed, theta, out);
+                                                 (float)sigma, seed, spg, theta, out);
   return launched(s);
 }
 
@@ -1011,18 +1019,28 @@ int opt_es_grad(int64_t numel, int64_t n_samples, int antithetic, double sigma, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int sms = 0;
   TRY(sm_count(&sms));
-  const int64_t nvec = numel >> 2;
-  int64_t grid = (nvec + 255) / 256 + 1;
+  const int64_t nvec = (numel + 3) >> 2;
+  const bool split = nvec < (int64_t)sms * 512 && n_samples >= 64;  // small tree, many samples
+  const int64_t threads = split ? nvec * 32 : nvec;
+  int64_t grid = (threads + 255) / 256;
   if (grid > (int64_t)sms * 8) grid = (int64_t)sms * 8;
+  if (grid < 1) grid = 1;
   const size_t smem = (sizeof(uint64_t) + sizeof(float)) * (size_t)n_samples;
-  static const cudaError_t attr = cudaFuncSetAttribute(
-      es_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-      (int)((sizeof(uint64_t) + sizeof(float)) * kEsMaxSamples));
-  if (attr != cudaSuccess) return fail(OPT_ECUDA, "smem attribute: %s", cudaGetErrorString(attr));
+  const int max_smem = (int)((sizeof(uint64_t) + sizeof(float)) * kEsMaxSamples);
+  static const cudaError_t attr0 = cudaFuncSetAttribute(
+      es_grad_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+  static const cudaError_t attr1 = cudaFuncSetAttribute(
+      es_grad_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+  if (attr0 != cudaSuccess || attr1 != cudaSuccess)
+    return fail(OPT_ECUDA, "smem attribute failed");
   const double scale = antithetic ? 1.0 / (2.0 * (double)n_samples * sigma)
                                   : 1.0 / ((double)n_samples * sigma);
-  es_grad_kernel<<<(int)grid, 256, smem, s>>>(numel, n_samples, antithetic, scale, seed,
-                                              f_values, grad);
+  if (split)
+    es_grad_kernel<true><<<(int)grid, 256, smem, s>>>(numel, n_samples, antithetic, scale, seed,
+                                                      f_values, grad);
+  else
+    es_grad_kernel<false><<<(int)grid, 256, smem, s>>>(numel, n_samples, antithetic, scale, seed,
+                                                       f_values, grad);
   return launched(s);
 }
 

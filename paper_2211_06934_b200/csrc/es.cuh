@@ -58,9 +58,14 @@ __device__ __forceinline__ void es_quad(uint64_t key, int64_t v, float (&z)[4]) 
 
 // out row r starts at r * ld (ld = numel rounded up to 4 elements, so every
 // row is 16-byte aligned): naive r = i, antithetic r = 2i (+) and 2i+1 (-).
+// Work item w = (vector v, sample group q): a thread computes samples
+// [q*spg, (q+1)*spg) of vector v. Large trees use spg = n_samples (theta is
+// read once, each warp writes coalesced rows); small trees split the samples
+// so that the grid still fills the GPU.
 __global__ void __launch_bounds__(256) es_perturb_kernel(int64_t numel, int64_t n_samples,
                                                          int64_t sample0, int antithetic,
                                                          float sigma, uint64_t seed,
+                                                         int64_t spg,
                                                          const float* __restrict__ theta,
                                                          float* __restrict__ out) {
   extern __shared__ uint64_t s_es[];
@@ -69,11 +74,21 @@ __global__ void __launch_bounds__(256) es_perturb_kernel(int64_t numel, int64_t 
   __syncthreads();
   const int reps = antithetic ? 2 : 1;
   const int64_t ld = (numel + 3) & ~int64_t(3);
-  const int64_t nvec = numel >> 2, stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
+  const int64_t nvec = (numel + 3) >> 2;  // last vector may be partial
+  const int64_t groups = (n_samples + spg - 1) / spg;
+  const int64_t total = nvec * groups, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total; w += stride) {
+    const int64_t v = w % nvec, q = w / nvec;
+    const bool full = 4 * v + 4 <= numel;
     float th[4];
-    load4(theta, v, th);
-    for (int64_t i = 0; i < n_samples; ++i) {
+    if (full) {
+      load4(theta, v, th);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) th[e] = 4 * v + e < numel ? theta[4 * v + e] : 0.f;
+    }
+    const int64_t i1 = min(n_samples, (q + 1) * spg);
+    for (int64_t i = q * spg; i < i1; ++i) {
       float z[4], p[4], m[4];
       es_quad(s_key[i], v, z);
 #pragma unroll
@@ -83,21 +98,24 @@ __global__ void __launch_bounds__(256) es_perturb_kernel(int64_t numel, int64_t 
         m[e] = th[e] - sz;
       }
       float* row = out + (i * reps) * ld;
-      store4(row, v, p);
-      if (antithetic) store4(row + ld, v, m);
-    }
-  }
-  // ragged tail (numel % 4) -> last block
-  const int64_t j = (nvec << 2) + threadIdx.x;
-  if (blockIdx.x == gridDim.x - 1 && j < numel) {
-    for (int64_t i = 0; i < n_samples; ++i) {
-      const float sz = sigma * es_normal(s_key[i], j);
-      out[(i * reps) * ld + j] = theta[j] + sz;
-      if (antithetic) out[(i * reps + 1) * ld + j] = theta[j] - sz;
+      if (full) {
+        store4(row, v, p);
+        if (antithetic) store4(row + ld, v, m);
+      } else {
+        for (int e = 0; 4 * v + e < numel; ++e) {
+          row[4 * v + e] = p[e];
+          if (antithetic) row[ld + 4 * v + e] = m[e];
+        }
+      }
     }
   }
 }
 
+// grad[j] = scale * sum_i w_i z_ij. SPLIT = false: a thread owns a vector and
+// loops over all samples (large trees). SPLIT = true: a warp owns a vector,
+// lanes take samples lane, lane+32, ..., then a fixed-order xor-shuffle sum
+// (small trees with many samples). Both fp64-accumulated, deterministic.
+template <bool SPLIT>
 __global__ void __launch_bounds__(256) es_grad_kernel(int64_t numel, int64_t n_samples,
                                                       int antithetic, double scale,
                                                       uint64_t seed,
@@ -111,25 +129,34 @@ __global__ void __launch_bounds__(256) es_grad_kernel(int64_t numel, int64_t n_s
     s_w[i] = antithetic ? f[2 * i] - f[2 * i + 1] : f[i];
   }
   __syncthreads();
-  const int64_t nvec = numel >> 2, stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
+  const int64_t nvec = (numel + 3) >> 2;
+  const int lanes = SPLIT ? 32 : 1;
+  const int lane = SPLIT ? (threadIdx.x & 31) : 0;
+  const int64_t stride = (int64_t)gridDim.x * (blockDim.x / lanes);
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / lanes; v < nvec; v += stride) {
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int64_t i = 0; i < n_samples; ++i) {
+    for (int64_t i = lane; i < n_samples; i += lanes) {
       const float w = s_w[i];
       float z[4];
       es_quad(s_key[i], v, z);
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[e] += (double)(w * z[e]);
     }
-    const float o[4] = {(float)(acc[0] * scale), (float)(acc[1] * scale), (float)(acc[2] * scale),
-                        (float)(acc[3] * scale)};
-    store4(grad, v, o);
-  }
-  const int64_t j = (nvec << 2) + threadIdx.x;
-  if (blockIdx.x == gridDim.x - 1 && j < numel) {
-    double acc = 0.0;
-    for (int64_t i = 0; i < n_samples; ++i) acc += (double)(s_w[i] * es_normal(s_key[i], j));
-    grad[j] = (float)(acc * scale);
+    if (SPLIT) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+    }
+    if (lane == 0) {
+      const float o[4] = {(float)(acc[0] * scale), (float)(acc[1] * scale),
+                          (float)(acc[2] * scale), (float)(acc[3] * scale)};
+      if (4 * v + 4 <= numel) {
+        store4(grad, v, o);
+      } else {
+        for (int e = 0; 4 * v + e < numel; ++e) grad[4 * v + e] = o[e];
+      }
+    }
   }
 }
 

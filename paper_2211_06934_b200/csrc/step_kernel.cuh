@@ -25,7 +25,7 @@ namespace dopt {
 
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
-constexpr int64_t kTile = 4096;      // leaf-mode tile (elements)
+constexpr int64_t kTile = 1024;      // leaf-mode tile (elements), one warp each
 constexpr int kMaxLeafSmem = 4096;   // leaf-mode limit on n_leaves (smem table)
 
 template <int NIN, int NOUT>
@@ -262,7 +262,6 @@ __global__ void __launch_bounds__(kBlock, MINB) step_leaf(const Op op,
   extern __shared__ int64_t s_dyn[];
   int64_t* s_off = s_dyn;
   int64_t* s_tp = s_dyn + (a.n_leaves + 1);
-  __shared__ double sm[NH][kWarps];
   __shared__ int64_t s_scan[kBlock];
 
   const int64_t nl = a.n_leaves;
@@ -297,7 +296,12 @@ __global__ void __launch_bounds__(kBlock, MINB) step_leaf(const Op op,
   if (blockIdx.x == 0 && want_hp)  // for leaf_finalize
     for (int64_t l = threadIdx.x; l <= nl; l += kBlock) a.tile_prefix[l] = s_tp[l];
 
-  for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+  // Warp tiles: warp w of the grid takes tiles w, w + nwarps, ...; the tile's
+  // hyper sums are reduced with shuffles only (no block barrier in the loop).
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+  for (int64_t tile = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); tile < a.n_tiles;
+       tile += nwarps) {
     // leaf = last l with s_tp[l] <= tile and a non-empty range
     int64_t lo = 0, hi = nl - 1;
     while (lo < hi) {
@@ -314,23 +318,20 @@ __global__ void __launch_bounds__(kBlock, MINB) step_leaf(const Op op,
     for (int k = 0; k < NH; ++k) acc[k] = 0.0;
     const int64_t va = (start + 3) >> 2, vb = end >> 2;
     if (va < vb) {
-      process_vectors<Op, ST, U>(opt, a, va, vb, threadIdx.x, kBlock, acc, want_hp);
-      if (start + threadIdx.x < (va << 2))
-        process_elem<Op, ST>(opt, a, start + threadIdx.x, acc, want_hp);
-      if ((vb << 2) + threadIdx.x < end)
-        process_elem<Op, ST>(opt, a, (vb << 2) + threadIdx.x, acc, want_hp);
+      process_vectors<Op, ST, U>(opt, a, va, vb, lane, 32, acc, want_hp);
+      if (start + lane < (va << 2)) process_elem<Op, ST>(opt, a, start + lane, acc, want_hp);
+      if ((vb << 2) + lane < end) process_elem<Op, ST>(opt, a, (vb << 2) + lane, acc, want_hp);
     } else {
-      for (int64_t i = start + threadIdx.x; i < end; i += kBlock)
-        process_elem<Op, ST>(opt, a, i, acc, want_hp);
+      for (int64_t i = start + lane; i < end; i += 32) process_elem<Op, ST>(opt, a, i, acc, want_hp);
     }
     if (want_hp) {
-      block_sum<NH>(acc, sm);
-      if (threadIdx.x == 0)
+#pragma unroll
+      for (int k = 0; k < NH; ++k) acc[k] = warp_sum(acc[k]);
+      if (lane == 0)
 #pragma unroll
         for (int k = 0; k < NH; ++k) a.partials[tile * NH + k] = acc[k];
     }
   }
-
 }
 
 // Per-leaf sums of the tile partials (second launch of leaf mode): one warp
