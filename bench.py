@@ -360,6 +360,12 @@ def main():
     ap.add_argument("--checkpoint-every", type=int, default=None,
                     help="C3: keep only every c-th state and recompute segments (NEXT-2)")
     ap.add_argument("--no-graph", action="store_true", help="MAML without CUDA-graph capture")
+    ap.add_argument("--maml-impl", default="batched", choices=["batched", "streams"],
+                    help="MAML shard: one task-batched network, or per-task graph branches")
+    ap.add_argument("--maml-net", default="gemm", choices=["gemm", "cudnn"],
+                    help="MAML task-batched network form (maml.conv4_forward_tasks)")
+    ap.add_argument("--maml-streams", type=int, default=8,
+                    help="MAML (--maml-impl streams): parallel task branches in the graph")
     ap.add_argument("--size", type=int, default=1 << 24)
     ap.add_argument("--bf16", action="store_true", help="bf16 optimizer state")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -548,7 +554,7 @@ def run_maml(args, dev, rank, world):
     from paper_2211_06934_b200 import _lib as L
     from paper_2211_06934_b200 import maml
 
-    cfg = maml.MamlConfig(tasks=args.tasks)
+    cfg = maml.MamlConfig(tasks=args.tasks, net=args.maml_net)
     phi = maml.init_params(0, dev)
     inner = maml.FusedSgdInner(maml.sizes_of(maml.CONV4_SHAPES), dev, cfg)
     outer = maml.FusedAdamOuter(phi.numel(), dev, cfg.outer_lr)
@@ -558,7 +564,9 @@ def run_maml(args, dev, rank, world):
     torch.backends.cuda.matmul.allow_tf32 = False
     shard = None
     if not args.no_graph:
-        shard = maml.GraphedShard(maml.task_range(world, rank, cfg.tasks), cfg, inner, dev)
+        shard = maml.GraphedShard(maml.task_range(world, rank, cfg.tasks), cfg, inner, dev,
+                                  streams=args.maml_streams,
+                                  batched=args.maml_impl == "batched")
 
     def step(i):
         state["phi"], loss, _ = maml.outer_step(state["phi"], i, cfg, inner, outer, world, rank,
@@ -577,7 +585,10 @@ def run_maml(args, dev, rank, world):
            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded 5-way tasks)",
            "config": {"workload": "C4 MAML 4-conv64, 5-way 5-shot 15-query, 5 inner SGD-mom steps",
                       "tasks": cfg.tasks, "parallelism": f"task-sharded x{world}, NCCL all-reduce",
-                      "cuda_graph": shard is not None},
+                      "cuda_graph": shard is not None,
+                      "shard_impl": ("eager per-task" if shard is None else
+                                     f"task-batched graph ({cfg.net})" if shard.batched else
+                                     f"graph, {shard.nstreams} task branches")},
            "gpu_launches": launches}
     if rank == 0:
         print(json.dumps(out), flush=True)

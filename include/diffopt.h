@@ -118,7 +118,7 @@ int opt_adam_fwd(const opt_tree* tree, int64_t step, const opt_adam_hp* hp,
  * and the cotangents d_updates, d_mu_out, d_nu_out of its outputs, writes
  * d_g, d_mu, d_nu (fp32) and, if non-NULL, d_hp[4] = (lr, b1, b2, eps)
  * hyper-gradients summed over all elements, and d_hp_leaf[n_leaves][4] the
- * same sums per leaf (needs tree->d_offsets; at most 4096 leaves). eps_root
+ * same sums per leaf (needs tree->d_offsets; any leaf count). eps_root
  * is not differentiated. workspace: see opt_workspace_bytes. */
 int opt_adam_bwd(const opt_tree* tree, int64_t step, const opt_adam_hp* hp,
                  int state_dtype, int compute,
@@ -170,7 +170,7 @@ int opt_sgd_bwd(const opt_tree* tree, const opt_sgd_hp* hp,
  *                   or, Adam with decoupled = 1 (AdamW): u += -lr * wd * theta;
  *   lr_leaf       : device float[n_leaves]; leaf l uses lr_leaf[l] instead of
  *                   hp->lr (per-leaf learnable learning rates). Needs
- *                   tree->d_offsets and at most 4096 leaves; the per-leaf lr
+ *                   tree->d_offsets (any leaf count); the per-leaf lr
  *                   gradients are slot 0 of d_hp_leaf.
  * theta = params (required when weight_decay != 0). The *_ex forward writes
  * params_out = params + updates when both are non-NULL. The *_ex backward

@@ -69,11 +69,14 @@ int check_tree(const opt_tree* t) {
   return OPT_OK;
 }
 
-int64_t count_tiles(const opt_tree* t) {
-  int64_t n = 0;
-  for (int64_t l = 0; l < t->n_leaves; ++l)
-    n += (t->h_offsets[l + 1] - t->h_offsets[l] + kTile - 1) / kTile;
-  return n;
+// Leaf-mode workspace slots (doubles / kNhMax): piece partials (chunk +
+// leaf slots), super-chunk partials, leaf_finalize block partials.
+struct LeafSlots {
+  int64_t part1, part2, blocks;
+};
+LeafSlots leaf_slots(const opt_tree* t) {
+  const int64_t nl = t->n_leaves;
+  return {n_chunks_of(t->numel) + nl, n_supers_of(t->numel) + nl, (nl + kWarps - 1) / kWarps};
 }
 
 bool finite(double x) { return std::isfinite(x); }
@@ -152,9 +155,8 @@ int grid_for(K kernel, int64_t work_blocks, size_t smem, int* grid) {
 // Launch with programmatic dependent launch (PDL): the grid may be scheduled
 // while the previous kernel on the stream drains; every step kernel starts
 // with griddepcontrol.wait, so it still observes all prior work.
-template <class Op, class K>
-cudaError_t launch_k(K kernel, int grid, int block, size_t smem, cudaStream_t s, const Op& op,
-                     const StepArgs<Op::NIN, Op::NOUT>& a) {
+template <class K, class... Args>
+cudaError_t launch_k(K kernel, int grid, int block, size_t smem, cudaStream_t s, Args... args) {
 #if DOPT_PDL
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -166,10 +168,10 @@ cudaError_t launch_k(K kernel, int grid, int block, size_t smem, cudaStream_t s,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, op, a);
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
 #else
-  kernel<<<grid, block, smem, s>>>(op, a);
-  return cudaSuccess;
+  kernel<<<grid, block, smem, s>>>(args...);
+  return cudaGetLastError();
 #endif
 }
 
@@ -187,18 +189,17 @@ int launched(cudaStream_t) {
 }
 
 // Workspace and reduction plumbing shared by the three backward ops.
-// Reduction / leaf-mode plumbing of one launch. Leaf mode (leaf-aligned
-// tiles over the shared-memory offset table) is used when per-leaf outputs
-// or per-leaf learning rates are requested.
+// Reduction / leaf-mode plumbing of one launch. Leaf mode (chunks split at
+// leaf boundaries, step_kernel.cuh) is used when per-leaf outputs or
+// per-leaf learning rates are requested.
 struct Reduce {
   double* d_hp;
   double* d_hp_leaf;
   const float* lr_leaf;
   bool leaf;
-  int64_t n_tiles;
-  double* partials;
+  double* partials;      // uniform: per block; leaf: per piece slot
   unsigned int* counter;
-  int64_t* tile_prefix;  // leaf mode: [n_leaves+1]
+  double* part2;         // leaf mode: super-chunk slots
   double* block_part;    // leaf mode: leaf_finalize block partials
 };
 
@@ -208,18 +209,13 @@ int setup_reduce(const opt_tree* t, double* d_hp, double* d_hp_leaf, const float
   r->d_hp_leaf = d_hp_leaf;
   r->lr_leaf = lr_leaf;
   r->leaf = d_hp_leaf != nullptr || lr_leaf != nullptr;
-  r->n_tiles = 0;
   r->partials = nullptr;
   r->counter = nullptr;
-  r->tile_prefix = nullptr;
+  r->part2 = nullptr;
   r->block_part = nullptr;
   if (r->leaf) {
     if (t->n_leaves < 1) return fail(OPT_EINVAL, "per-leaf outputs/lr need n_leaves >= 1");
-    if (t->n_leaves > kMaxLeafSmem)
-      return fail(OPT_EINVAL, "per-leaf outputs/lr support at most %d leaves (got %lld)",
-                  kMaxLeafSmem, (long long)t->n_leaves);
     if (!t->d_offsets) return fail(OPT_EINVAL, "per-leaf outputs/lr need tree->d_offsets");
-    r->n_tiles = count_tiles(t);
   }
   if (!d_hp && !d_hp_leaf) return OPT_OK;
   size_t need = opt_workspace_bytes(t, r->leaf ? 1 : 0);
@@ -229,9 +225,9 @@ int setup_reduce(const opt_tree* t, double* d_hp, double* d_hp_leaf, const float
   r->counter = static_cast<unsigned int*>(ws);
   r->partials = reinterpret_cast<double*>(static_cast<char*>(ws) + kCounterBytes);
   if (r->leaf) {
-    const int64_t slots = r->n_tiles > kMaxGrid ? r->n_tiles : kMaxGrid;
-    r->tile_prefix = reinterpret_cast<int64_t*>(r->partials + kNhMax * slots);
-    r->block_part = reinterpret_cast<double*>(r->tile_prefix + t->n_leaves + 1);
+    const LeafSlots ls = leaf_slots(t);
+    r->part2 = r->partials + kNhMax * ls.part1;
+    r->block_part = r->part2 + kNhMax * ls.part2;
   }
   return OPT_OK;
 }
@@ -325,29 +321,34 @@ int launch(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r, const 
   a.partials = r.partials;
   a.counter = r.counter;
   a.lr_leaf = r.lr_leaf;
-  a.tile_prefix = r.tile_prefix;
   a.want_hp = (r.d_hp || r.d_hp_leaf) ? 1 : 0;
   if (r.leaf) {
     a.offsets = t->d_offsets;
     a.n_leaves = t->n_leaves;
-    a.n_tiles = r.n_tiles;
     auto k = step_leaf<Op, ST, U, MINB>;
-    size_t smem = sizeof(int64_t) * 2 * (size_t)(t->n_leaves + 1);
+    const size_t smem =
+        t->n_leaves <= kMaxLeafSmem ? sizeof(int64_t) * (size_t)(t->n_leaves + 1) : 0;
     static const cudaError_t attr = cudaFuncSetAttribute(
-        k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(int64_t) * 2 * (kMaxLeafSmem + 1)));
+        k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(int64_t) * (kMaxLeafSmem + 1)));
     if (attr != cudaSuccess) return fail(OPT_ECUDA, "smem attribute: %s", cudaGetErrorString(attr));
     int grid = 0;
-    int rc = grid_for(k, (r.n_tiles + kWarps - 1) / kWarps, smem, &grid);
+    int rc = grid_for(k, (n_chunks_of(a.numel) + kWarps - 1) / kWarps, smem, &grid);
     if (rc) return rc;
     cudaError_t le = launch_k(k, grid, kBlock, smem, s, op, a);
     if (le != cudaSuccess) return fail(OPT_ECUDA, "launch: %s", cudaGetErrorString(le));
     TRY(launched(s));
     if constexpr (Op::NH > 0) {
-      if (a.want_hp) {  // per-leaf and global sums of the tile partials
+      if (a.want_hp) {  // piece slots -> super-chunk slots -> per-leaf and global sums
         constexpr int NH = Op::NH;
+        const int64_t fold_blocks = (n_supers_of(a.numel) + kWarps - 1) / kWarps;
+        le = launch_k(leaf_fold<NH>, (int)fold_blocks, kBlock, 0, s, (const double*)r.partials,
+                      t->d_offsets, t->n_leaves, a.numel, r.part2);
+        if (le != cudaSuccess) return fail(OPT_ECUDA, "launch: %s", cudaGetErrorString(le));
+        TRY(launched(s));
         const int fg = (int)((t->n_leaves + kWarps - 1) / kWarps);
-        leaf_finalize<NH><<<fg, kBlock, 0, s>>>(r.partials, r.tile_prefix, t->n_leaves,
-                                               r.d_hp_leaf, r.d_hp, r.block_part, r.counter);
+        le = launch_k(leaf_finalize<NH>, fg, kBlock, 0, s, (const double*)r.part2, t->d_offsets,
+                      t->n_leaves, r.d_hp_leaf, r.d_hp, r.block_part, r.counter);
+        if (le != cudaSuccess) return fail(OPT_ECUDA, "launch: %s", cudaGetErrorString(le));
         TRY(launched(s));
       }
     }
@@ -507,15 +508,12 @@ extern "C" {
 size_t opt_workspace_bytes(const opt_tree* tree, int per_leaf) {
   if (check_tree(tree)) return 0;
   int64_t slots = kMaxGrid;
-  size_t extra = 0;
   if (per_leaf) {
-    int64_t nt = count_tiles(tree);
-    if (nt > slots) slots = nt;
-    // tile prefix [n_leaves+1] + leaf_finalize block partials
-    extra = sizeof(int64_t) * (size_t)(tree->n_leaves + 1) +
-            sizeof(double) * kNhMax * (size_t)((tree->n_leaves + kWarps - 1) / kWarps);
+    const LeafSlots ls = leaf_slots(tree);
+    const int64_t leaf = ls.part1 + ls.part2 + ls.blocks;
+    if (leaf > slots) slots = leaf;
   }
-  return kCounterBytes + sizeof(double) * kNhMax * (size_t)slots + extra;
+  return kCounterBytes + sizeof(double) * kNhMax * (size_t)slots;
 }
 
 // ------------------------------------------------------------------ Adam

@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(256) es_perturb_kernel(int64_t numel, int64_t 
   const int64_t groups = (n_samples + spg - 1) / spg;
   const int64_t total = nvec * groups, stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total; w += stride) {
-    const int64_t v = w % nvec, q = w / nvec;
+    const int64_t q = groups == 1 ? 0 : w / nvec;  // (no 64-bit division when unsplit)
+    const int64_t v = w - q * nvec;
     const bool full = 4 * v + 4 <= numel;
     float th[4];
     if (full) {
@@ -102,9 +103,12 @@ __global__ void __launch_bounds__(256) es_perturb_kernel(int64_t numel, int64_t 
         store4(row, v, p);
         if (antithetic) store4(row + ld, v, m);
       } else {
-        for (int e = 0; 4 * v + e < numel; ++e) {
-          row[4 * v + e] = p[e];
-          if (antithetic) row[ld + 4 * v + e] = m[e];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {  // constant indices: p, m stay in registers
+          if (4 * v + e < numel) {
+            row[4 * v + e] = p[e];
+            if (antithetic) row[ld + 4 * v + e] = m[e];
+          }
         }
       }
     }
@@ -154,7 +158,9 @@ __global__ void __launch_bounds__(256) es_grad_kernel(int64_t numel, int64_t n_s
       if (4 * v + 4 <= numel) {
         store4(grad, v, o);
       } else {
-        for (int e = 0; 4 * v + e < numel; ++e) grad[4 * v + e] = o[e];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (4 * v + e < numel) grad[4 * v + e] = o[e];
       }
     }
   }

@@ -11,10 +11,10 @@
 //     workspace -> the last block to arrive (atomic ticket + threadfence)
 //     sums the partials in block order. One launch, no atomics on data, and
 //     bitwise reproducible for a fixed grid (reading Z12).
-//   * Per-leaf sums (d_hp_leaf): the offset table is staged in shared memory
-//     and split into leaf-aligned tiles of kTile elements (a scan of
-//     ceil(len/kTile) per leaf, done by every block); each tile's partial goes
-//     to the workspace and the last block sums every leaf's tiles in order.
+//   * Per-leaf sums (d_hp_leaf) / per-leaf lr: the same grid-stride over
+//     256-element chunks, each chunk split at leaf boundaries (binary search
+//     in the shared-memory offset table); one fp64 partial per (chunk, leaf)
+//     piece at slot chunk + leaf, then two fixed-order folds (see below).
 #pragma once
 #include <stdint.h>
 
@@ -25,8 +25,17 @@ namespace dopt {
 
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
-constexpr int64_t kTile = 1024;      // leaf-mode tile (elements), one warp each
-constexpr int kMaxLeafSmem = 4096;   // leaf-mode limit on n_leaves (smem table)
+constexpr int kChunkShift = 8;                // leaf mode: 256-element chunks, one warp each
+constexpr int64_t kChunk = int64_t(1) << kChunkShift;
+constexpr int kSuperShift = kChunkShift + 5;  // leaf mode: super-chunks of 32 chunks
+constexpr int kMaxLeafSmem = 4096;            // offset table staged in smem up to this
+
+__host__ __device__ constexpr int64_t n_chunks_of(int64_t numel) {
+  return (numel + kChunk - 1) >> kChunkShift;
+}
+__host__ __device__ constexpr int64_t n_supers_of(int64_t numel) {
+  return (numel + (int64_t(1) << kSuperShift) - 1) >> kSuperShift;
+}
 
 template <int NIN, int NOUT>
 struct StepArgs {
@@ -35,13 +44,11 @@ struct StepArgs {
   int64_t numel;
   double* d_hp;          // [NH] final sums (may be NULL)
   double* d_hp_leaf;     // [n_leaves][NH] (leaf mode)
-  double* partials;      // workspace: per block (uniform) or per tile (leaf)
+  double* partials;      // workspace: per block (uniform) or per piece slot (leaf)
   unsigned int* counter; // workspace: arrival ticket, left at 0
   const int64_t* offsets;  // device offsets (leaf mode)
   const float* lr_leaf;    // per-leaf learning rates (leaf mode) or NULL
-  int64_t* tile_prefix;    // workspace (leaf mode): first tile of every leaf, [n_leaves+1]
   int64_t n_leaves;
-  int64_t n_tiles;
   int want_hp;
 };
 
@@ -250,97 +257,126 @@ __global__ void __launch_bounds__(kBlock, MINB) step_uniform(const Op op,
   }
 }
 
-// ---------------------------------------------------------- leaf kernel
-// Dynamic smem: s_off[n_leaves+1], s_tp[n_leaves+1] (first tile of leaf l).
-__device__ __forceinline__ int64_t tiles_of(int64_t len) { return (len + kTile - 1) / kTile; }
+// ---------------------------------------------------------- leaf mode
+// Pieces. The flat element range is cut into chunks of kChunk elements and
+// every chunk into its intersections with the leaves. Piece (chunk c, leaf
+// l) owns partial slot c + l: leaves are contiguous and ordered, so two
+// non-empty pieces never share a slot, and leaf l's pieces are the
+// consecutive slots [c_first(l) + l, c_last(l) + l] -- no scan and no table.
+// The same rule one level up (super-chunks of 32 chunks) gives the slots of
+// the second level. So the streaming kernel keeps the uniform kernel's
+// grid-stride over equal work items (chunks; leaf count is free), and the
+// per-leaf sums are two short fixed-order folds (leaf_fold, leaf_finalize).
+__device__ __forceinline__ int64_t leaf_of(const int64_t* off, int64_t nl, int64_t e) {
+  // the non-empty leaf holding element e: last l with off[l] <= e
+  int64_t lo = 0, hi = nl - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= e) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
 
+// Elements [s, e) (one piece, <= kChunk) by the 32 lanes of a warp.
+template <class Op, class ST, int U>
+__device__ __forceinline__ void process_piece(const Op& op, const StepArgs<Op::NIN, Op::NOUT>& a,
+                                              int64_t s, int64_t e, int lane, double* acc,
+                                              bool want_hp) {
+  const int64_t va = (s + 3) >> 2, vb = e >> 2;
+  if (va < vb) {
+    process_vectors<Op, ST, U>(op, a, va, vb, lane, 32, acc, want_hp);
+    if (s + lane < (va << 2)) process_elem<Op, ST>(op, a, s + lane, acc, want_hp);
+    if ((vb << 2) + lane < e) process_elem<Op, ST>(op, a, (vb << 2) + lane, acc, want_hp);
+  } else {
+    for (int64_t i = s + lane; i < e; i += 32) process_elem<Op, ST>(op, a, i, acc, want_hp);
+  }
+}
+
+// Dynamic smem: the offset table (n_leaves + 1) when n_leaves <= kMaxLeafSmem,
+// else the binary searches read it from global memory (L1-cached).
 template <class Op, class ST, int U, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) step_leaf(const Op op,
                                                     const StepArgs<Op::NIN, Op::NOUT> a) {
   constexpr int NH = Op::NH > 0 ? Op::NH : 1;
   const bool want_hp = Op::NH > 0 && a.want_hp;
   extern __shared__ int64_t s_dyn[];
-  int64_t* s_off = s_dyn;
-  int64_t* s_tp = s_dyn + (a.n_leaves + 1);
-  __shared__ int64_t s_scan[kBlock];
-
   const int64_t nl = a.n_leaves;
+  const bool staged = nl <= kMaxLeafSmem;
   pdl_wait();
-  // stage offsets; per-thread contiguous chunk for the scan
-  for (int64_t l = threadIdx.x; l <= nl; l += kBlock) s_off[l] = a.offsets[l];
-  __syncthreads();
-  const int64_t per = (nl + kBlock - 1) / kBlock;
-  const int64_t l0 = threadIdx.x * per, l1 = min(l0 + per, nl);
-  int64_t local = 0;
-  for (int64_t l = l0; l < l1; ++l) local += tiles_of(s_off[l + 1] - s_off[l]);
-  s_scan[threadIdx.x] = local;
-  __syncthreads();
-  if (threadIdx.x == 0) {  // 256-entry exclusive scan
-    int64_t run = 0;
-    for (int t = 0; t < kBlock; ++t) {
-      int64_t c = s_scan[t];
-      s_scan[t] = run;
-      run += c;
-    }
+  if (staged) {
+    for (int64_t l = threadIdx.x; l <= nl; l += kBlock) s_dyn[l] = __ldg(&a.offsets[l]);
+    __syncthreads();
   }
-  __syncthreads();
-  {
-    int64_t run = s_scan[threadIdx.x];
-    for (int64_t l = l0; l < l1; ++l) {
-      s_tp[l] = run;
-      run += tiles_of(s_off[l + 1] - s_off[l]);
-    }
-    if (threadIdx.x == kBlock - 1) s_tp[nl] = a.n_tiles;
-  }
-  __syncthreads();
-  if (blockIdx.x == 0 && want_hp)  // for leaf_finalize
-    for (int64_t l = threadIdx.x; l <= nl; l += kBlock) a.tile_prefix[l] = s_tp[l];
-
-  // Warp tiles: warp w of the grid takes tiles w, w + nwarps, ...; the tile's
-  // hyper sums are reduced with shuffles only (no block barrier in the loop).
+  const int64_t* off = staged ? s_dyn : a.offsets;
   const int lane = threadIdx.x & 31;
-  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
-  for (int64_t tile = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); tile < a.n_tiles;
-       tile += nwarps) {
-    // leaf = last l with s_tp[l] <= tile and a non-empty range
-    int64_t lo = 0, hi = nl - 1;
-    while (lo < hi) {
-      int64_t mid = (lo + hi + 1) >> 1;
-      if (s_tp[mid] <= tile) lo = mid; else hi = mid - 1;
-    }
-    const int64_t leaf_end = s_off[lo + 1];
-    const int64_t start = s_off[lo] + (tile - s_tp[lo]) * kTile;
-    const int64_t end = min(start + kTile, leaf_end);
-    Op opt = op;  // this tile's leaf learning rate (per-leaf lr variants)
-    if (a.lr_leaf) opt.set_lr((typename Op::CT)a.lr_leaf[lo]);
-    double acc[NH];
+  const int64_t nchunks = n_chunks_of(a.numel), nwarps = (int64_t)gridDim.x * kWarps;
+  for (int64_t c = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); c < nchunks; c += nwarps) {
+    const int64_t c1 = min((c + 1) << kChunkShift, a.numel);
+    int64_t s = c << kChunkShift;
+    int64_t l = leaf_of(off, nl, s);
+    while (true) {
+      const int64_t e = min(c1, off[l + 1]);
+      Op opt = op;  // the piece's leaf learning rate (per-leaf lr variants)
+      if (a.lr_leaf) opt.set_lr((typename Op::CT)a.lr_leaf[l]);
+      double acc[NH];
 #pragma unroll
-    for (int k = 0; k < NH; ++k) acc[k] = 0.0;
-    const int64_t va = (start + 3) >> 2, vb = end >> 2;
-    if (va < vb) {
-      process_vectors<Op, ST, U>(opt, a, va, vb, lane, 32, acc, want_hp);
-      if (start + lane < (va << 2)) process_elem<Op, ST>(opt, a, start + lane, acc, want_hp);
-      if ((vb << 2) + lane < end) process_elem<Op, ST>(opt, a, (vb << 2) + lane, acc, want_hp);
-    } else {
-      for (int64_t i = start + lane; i < end; i += 32) process_elem<Op, ST>(opt, a, i, acc, want_hp);
-    }
-    if (want_hp) {
+      for (int k = 0; k < NH; ++k) acc[k] = 0.0;
+      process_piece<Op, ST, U>(opt, a, s, e, lane, acc, want_hp);
+      if (want_hp) {
 #pragma unroll
-      for (int k = 0; k < NH; ++k) acc[k] = warp_sum(acc[k]);
-      if (lane == 0)
+        for (int k = 0; k < NH; ++k) acc[k] = warp_sum(acc[k]);
+        if (lane == 0)
 #pragma unroll
-        for (int k = 0; k < NH; ++k) a.partials[tile * NH + k] = acc[k];
+          for (int k = 0; k < NH; ++k) a.partials[(c + l) * NH + k] = acc[k];
+      }
+      if (e >= c1) break;
+      s = e;
+      do { ++l; } while (off[l + 1] <= s);  // next non-empty leaf
     }
   }
+  pdl_trigger();
 }
 
-// Per-leaf sums of the tile partials (second launch of leaf mode): one warp
-// per leaf, lanes stride over the leaf's tiles, xor-shuffle; one fp64 partial
-// per block of the leaf sums (in warp = leaf order) and the last block sums
-// those in block order into d_hp. Deterministic for a fixed grid.
+// Level 2: one warp per super-chunk sc; for every leaf l meeting it, lane j
+// takes chunk 32 sc + j's slot (c + l) and the xor-shuffle sum goes to slot
+// sc + l of part2.
 template <int NH>
-__global__ void __launch_bounds__(kBlock) leaf_finalize(const double* partials,
-                                                        const int64_t* tile_prefix,
+__global__ void __launch_bounds__(kBlock) leaf_fold(const double* part1, const int64_t* off,
+                                                    int64_t nl, int64_t numel, double* part2) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t sc = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (sc < n_supers_of(numel)) {
+    const int64_t e1 = min((sc + 1) << kSuperShift, numel);
+    const int64_t c = (sc << (kSuperShift - kChunkShift)) + lane;
+    const bool chunk_ok = (c << kChunkShift) < e1;
+    int64_t s = sc << kSuperShift;
+    int64_t l = leaf_of(off, nl, s);
+    while (true) {
+      const int64_t lb = __ldg(&off[l]), le = __ldg(&off[l + 1]);
+      const bool in = chunk_ok && c >= (lb >> kChunkShift) && c <= ((le - 1) >> kChunkShift);
+      double v[NH];
+#pragma unroll
+      for (int k = 0; k < NH; ++k) v[k] = in ? __ldcg(&part1[(c + l) * NH + k]) : 0.0;
+#pragma unroll
+      for (int k = 0; k < NH; ++k) v[k] = warp_sum(v[k]);
+      if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < NH; ++k) part2[(sc + l) * NH + k] = v[k];
+      if (le >= e1) break;
+      s = le;
+      do { ++l; } while (__ldg(&off[l + 1]) <= s);
+    }
+  }
+  pdl_trigger();
+}
+
+// Level 3: one warp per leaf sums its super-chunk slots (lanes stride, then
+// xor-shuffle) into d_hp_leaf; one fp64 partial per block of those sums (in
+// leaf order) and the last block sums the partials in block order into d_hp.
+// Every sum has a fixed order: bitwise reproducible.
+template <int NH>
+__global__ void __launch_bounds__(kBlock) leaf_finalize(const double* part2, const int64_t* off,
                                                         int64_t n_leaves, double* d_hp_leaf,
                                                         double* d_hp, double* block_part,
                                                         unsigned int* counter) {
@@ -351,10 +387,14 @@ __global__ void __launch_bounds__(kBlock) leaf_finalize(const double* partials,
 #pragma unroll
   for (int k = 0; k < NH; ++k) s[k] = 0.0;
   if (l < n_leaves) {
-    const int64_t t0 = tile_prefix[l], t1 = tile_prefix[l + 1];
-    for (int64_t t = t0 + lane; t < t1; t += 32)
+    const int64_t lb = __ldg(&off[l]), le = __ldg(&off[l + 1]);
+    if (le > lb) {
+      const int64_t sb = (le - 1) >> kSuperShift;
+#pragma unroll 4
+      for (int64_t sc = (lb >> kSuperShift) + lane; sc <= sb; sc += 32)
 #pragma unroll
-      for (int k = 0; k < NH; ++k) s[k] += __ldcg(&partials[t * NH + k]);
+        for (int k = 0; k < NH; ++k) s[k] += __ldcg(&part2[(sc + l) * NH + k]);
+    }
   }
 #pragma unroll
   for (int k = 0; k < NH; ++k) s[k] = warp_sum(s[k]);

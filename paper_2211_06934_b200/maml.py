@@ -89,6 +89,7 @@ class MamlConfig:
     nesterov: bool = False
     outer_lr: float = 1e-3
     seed: int = 0
+    net: str = "gemm"  # network form (conv4_forward_tasks)
 
 
 class FusedSgdInner:
@@ -144,25 +145,178 @@ def meta_grad_tasks(phi, task_ids, outer_step, cfg: MamlConfig, inner):
     return meta_grad_data(phi, data, cfg, inner)
 
 
+def _task_logits(theta, x, net):
+    """One task's logits; net as in conv4_forward_tasks (T = 1)."""
+    sizes = sizes_of(CONV4_SHAPES)
+    if net == "gemm":
+        params = [p.view(1, *s) for p, s in zip(torch.split(theta, sizes), CONV4_SHAPES)]
+        return conv4_forward_tasks(params, x.view(x.shape[0], 1, HW, HW), 1, "gemm")[0]
+    params = [p.view(s) for p, s in zip(torch.split(theta, sizes), CONV4_SHAPES)]
+    return conv4_forward(params, x)
+
+
 def meta_grad_data(phi, data, cfg: MamlConfig, inner):
     """meta_grad_tasks on pre-generated task data [(xs, ys, xq, yq), ...]."""
     sizes = sizes_of(CONV4_SHAPES)
     phi_v = phi.detach().requires_grad_(True)
     total = torch.zeros_like(phi)
-    loss_sum = torch.zeros((), device=phi.device)
+    loss_sum = torch.zeros((), device=phi.device, dtype=phi.dtype)
     for xs, ys, xq, yq in data:
         theta, b = phi_v, None
         for _ in range(cfg.inner_steps):
-            params = [p.view(s) for p, s in zip(torch.split(theta, sizes), CONV4_SHAPES)]
-            loss = F.cross_entropy(conv4_forward(params, xs), ys)
+            loss = F.cross_entropy(_task_logits(theta, xs, cfg.net), ys)
             (g,) = torch.autograd.grad(loss, theta, create_graph=True)
             theta, b = inner(g, b, theta)
-        params = [p.view(s) for p, s in zip(torch.split(theta, sizes), CONV4_SHAPES)]
-        qloss = F.cross_entropy(conv4_forward(params, xq), yq)
+        qloss = F.cross_entropy(_task_logits(theta, xq, cfg.net), yq)
         (mg,) = torch.autograd.grad(qloss, phi_v)
         total += mg
         loss_sum += qloss.detach()
     return total, loss_sum
+
+
+# ---------------------------------------------------- task-batched form
+def theta0_tasks(phi_leaves, T):
+    """theta_0 of T tasks, leaf-major: leaf l becomes a [T, size_l] block
+    (every task starts from phi; the backward of the broadcast is the sum
+    over tasks of the meta-gradients)."""
+    return torch.cat([p.reshape(1, -1).expand(T, -1).reshape(-1) for p in phi_leaves])
+
+
+class _Im2Col(torch.autograd.Function):
+    """3x3 / padding-1 im2col of the task-major layout: h [T, C, B, H, W] ->
+    columns [T, C*9, B*H*W], row cin*9 + 3i + j = h shifted by (i-1, j-1)
+    (zero outside). Its adjoint is _Col2Im and each one's backward is the
+    other, so the pair is differentiable to any order (MAML's second-order
+    meta-gradient differentiates through the convolution backward)."""
+
+    @staticmethod
+    def forward(ctx, h):
+        T, C, B, H, W = h.shape
+        ctx.shape = tuple(h.shape)
+        hp = F.pad(h, (1, 1, 1, 1))
+        cols = torch.stack([hp[..., i:i + H, j:j + W] for i in range(3) for j in range(3)], 2)
+        return cols.view(T, C * 9, B * H * W)
+
+    @staticmethod
+    def backward(ctx, dcols):
+        return _Col2Im.apply(dcols, ctx.shape)
+
+
+class _Col2Im(torch.autograd.Function):
+    """Adjoint of _Im2Col: dh[y + i - 1, x + j - 1] += cols_(i,j)[y, x]."""
+
+    @staticmethod
+    def forward(ctx, cols, shape):
+        T, C, B, H, W = shape
+        c = cols.reshape(T, C, 9, B, H, W)
+        dh = cols.new_zeros(shape)
+        for k in range(9):
+            di, dj = k // 3 - 1, k % 3 - 1
+            ya, yb, xa, xb = max(0, di), min(H, H + di), max(0, dj), min(W, W + dj)
+            dh[..., ya:yb, xa:xb] += c[:, :, k, :, ya - di:yb - di, xa - dj:xb - dj]
+        return dh
+
+    @staticmethod
+    def backward(ctx, dh):
+        return _Im2Col.apply(dh), None
+
+
+def _conv3x3_tasks(h, w, b):
+    """Task-batched 3x3 conv (padding 1) as one batched GEMM: h [T, Cin, B,
+    H, W], w [T, Cout, Cin, 3, 3], b [T, Cout] -> [T, Cout, B, H, W]."""
+    T, Cin, B, H, W = h.shape
+    out = torch.baddbmm(b.unsqueeze(-1), w.reshape(T, w.shape[1], Cin * 9), _Im2Col.apply(h))
+    return out.view(T, -1, B, H, W)
+
+
+def _bn_tasks(h, gamma, beta):
+    """Training-mode batch norm with per-(task, channel) batch statistics on
+    the [T, C, B, H, W] layout: F.batch_norm on the [1, T*C, B*H*W] view."""
+    T, C = h.shape[:2]
+    y = F.batch_norm(h.reshape(1, T * C, -1), None, None, gamma.reshape(-1), beta.reshape(-1),
+                     training=True)
+    return y.view_as(h)
+
+
+def _pool_relu_tasks(h):
+    """relu(max_pool2d(., 2)) (= max_pool2d(relu(.)), floor mode) on the
+    [T, C, B, H, W] layout as a 2x2 window max."""
+    T, C, B, H, W = h.shape
+    H2, W2 = H // 2, W // 2
+    if H != 2 * H2 or W != 2 * W2:
+        h = h[..., :2 * H2, :2 * W2]
+    return F.relu(h.reshape(T, C, B, H2, 2, W2, 2).amax(dim=(4, 6)))
+
+
+def conv4_forward_tasks(params, x, T, net="cudnn"):
+    """The T networks of a task batch as ONE network: params are the 18
+    leaves with a leading task dim [T, *shape]; x: [B, T, 28, 28] (channel t
+    = task t). Task t's logits depend on task t's parameters and images only
+    and equal conv4_forward(params[t], x[:, t:t+1]). Returns [T, B, WAYS].
+      net="cudnn": grouped convolutions (groups = T) and F.batch_norm over
+                   the T*64 channels (= per (task, channel) statistics);
+      net="gemm" : activations kept task-major [T, C, B, H, W], every conv
+                   one batched GEMM over the T tasks (_conv3x3_tasks), BN
+                   statistics per (task, channel) (_bn_tasks), 2x2 window
+                   max (_pool_relu_tasks). On B200, cuDNN's fp32 convolution
+                   algorithms lose ~2% on this second-order meta-gradient
+                   while the SGEMM form keeps fp32 accuracy (~3e-6 vs a
+                   float64 run, tools/maml_net_check.py), so it is the
+                   default."""
+    if net == "gemm":
+        h = x.permute(1, 0, 2, 3).unsqueeze(1)  # [T, 1, B, 28, 28]
+        for blk in range(4):
+            w, b, gam, bet = params[4 * blk: 4 * blk + 4]
+            h = _pool_relu_tasks(_bn_tasks(_conv3x3_tasks(h, w, b), gam, bet))
+        h = h.reshape(T, 64, -1).transpose(1, 2)  # [T, B, 64]
+    else:
+        h = x
+        for blk in range(4):
+            w, b, gam, bet = params[4 * blk: 4 * blk + 4]
+            h = F.conv2d(h, w.reshape(-1, *w.shape[2:]), b.reshape(-1), padding=1, groups=T)
+            h = F.batch_norm(h, None, None, gam.reshape(-1), bet.reshape(-1), training=True)
+            h = F.max_pool2d(F.relu(h), 2)
+        h = h.reshape(h.shape[0], T, -1).transpose(0, 1)  # [T, B, 64]
+    return torch.baddbmm(params[17].unsqueeze(1), h, params[16].transpose(1, 2))
+
+
+class TaskBatchInner(FusedSgdInner):
+    """The inner SGD-momentum step of all T tasks of a batch: one fused
+    differentiable libdiffopt.so launch over the T x 112,261 flat buffer."""
+
+    def __init__(self, T, device, cfg: MamlConfig):
+        super().__init__([T * n for n in sizes_of(CONV4_SHAPES)], device, cfg)
+        self.T = T
+
+
+def meta_grad_batched(phi, data, cfg: MamlConfig, inner: TaskBatchInner):
+    """meta_grad_data for a batch of tasks run as one task-batched network
+    (conv4_forward_tasks): Sum_t d L_query,t(theta_K,t(phi)) / d phi and the
+    summed query loss. Each task's inner loop is the same recurrence as in
+    meta_grad_data (its loss is a mean over its own images); only the
+    summation order of the meta-gradient over tasks differs."""
+    T = len(data)
+    assert inner.T == T
+    sizes = sizes_of(CONV4_SHAPES)
+    blk = [T * n for n in sizes]
+    xs = torch.stack([d[0] for d in data], 1).flatten(1, 2)
+    ys = torch.stack([d[1] for d in data])
+    xq = torch.stack([d[2] for d in data], 1).flatten(1, 2)
+    yq = torch.stack([d[3] for d in data])
+
+    def loss_of(theta, x, y):
+        params = [p.view(T, *s) for p, s in zip(torch.split(theta, blk), CONV4_SHAPES)]
+        logits = conv4_forward_tasks(params, x, T, cfg.net)
+        return F.cross_entropy(logits.reshape(-1, WAYS), y.reshape(-1), reduction="sum") / y.shape[1]
+
+    phi_v = phi.detach().requires_grad_(True)
+    theta, b = theta0_tasks(torch.split(phi_v, sizes), T), None
+    for _ in range(cfg.inner_steps):
+        (g,) = torch.autograd.grad(loss_of(theta, xs, ys), theta, create_graph=True)
+        theta, b = inner(g, b, theta)
+    qloss = loss_of(theta, xq, yq)
+    (mg,) = torch.autograd.grad(qloss, phi_v)
+    return mg, qloss.detach()
 
 
 class GraphedShard:
@@ -171,25 +325,59 @@ class GraphedShard:
     meta-gradient sum): per outer step only the task data and phi are
     copied into static buffers and the graph is replayed, removing the
     per-kernel launch cost that dominates these tiny convolutions.
+    With ``streams = S > 1`` the tasks are captured on S forked streams, so
+    the graph holds S independent branches that the GPU runs concurrently
+    (one task's small convolutions leave most SMs idle); the per-task
+    meta-gradients are summed in task order after the join (the same sum as
+    the sequential version). With ``batched=True`` the shard's tasks run as
+    one task-batched network (meta_grad_batched: grouped convolutions, one
+    fused inner step for all tasks), ~T x fewer kernels per replay.
     Call it like meta_grad_tasks."""
 
-    def __init__(self, task_ids, cfg: MamlConfig, inner, device, warmup=2):
+    def __init__(self, task_ids, cfg: MamlConfig, inner, device, warmup=2, streams=1,
+                 batched=False):
         self.ids, self.cfg, self.inner = list(task_ids), cfg, inner
+        self.batched = bool(batched)
+        if self.batched:
+            self.inner = TaskBatchInner(len(self.ids), device, cfg)
         self.phi = torch.zeros(sum(sizes_of(CONV4_SHAPES)), device=device)
         self.data = [task_data(0, t, device, cfg.seed) for t in self.ids]
+        self.nstreams = 1 if self.batched else max(1, min(int(streams), len(self.ids)))
+        self.streams = [torch.cuda.Stream(device) for _ in range(self.nstreams)]
         side = torch.cuda.Stream(device)
         side.wait_stream(torch.cuda.current_stream(device))
         with torch.cuda.stream(side):
             for _ in range(warmup):
-                meta_grad_data(self.phi, self.data, cfg, inner)
+                self._body()
         torch.cuda.current_stream(device).wait_stream(side)
         from . import _lib as L
 
         self.graph = torch.cuda.CUDAGraph()
         n0 = L.opt_launch_count()
         with torch.cuda.graph(self.graph):
-            self.mg, self.loss = meta_grad_data(self.phi, self.data, cfg, inner)
+            self.mg, self.loss = self._body()
         self.launches_per_replay = L.opt_launch_count() - n0  # captured library kernels
+
+    def _body(self):
+        if self.batched:
+            return meta_grad_batched(self.phi, self.data, self.cfg, self.inner)
+        if self.nstreams == 1:
+            return meta_grad_data(self.phi, self.data, self.cfg, self.inner)
+        cur = torch.cuda.current_stream()
+        parts = []
+        for k, d in enumerate(self.data):
+            s = self.streams[k % self.nstreams]
+            s.wait_stream(cur)
+            with torch.cuda.stream(s):
+                parts.append(meta_grad_data(self.phi, [d], self.cfg, self.inner))
+        for s in self.streams:
+            cur.wait_stream(s)
+        total = torch.zeros_like(self.phi)
+        loss = torch.zeros((), device=self.phi.device)
+        for mg, l in parts:  # task order
+            total += mg
+            loss += l
+        return total, loss
 
     def __call__(self, phi, task_ids, outer_step, cfg, inner):
         assert list(task_ids) == self.ids

@@ -88,8 +88,9 @@ def test_workspace_sizes_and_error(L):
     small = t.workspace_bytes(False)
     big = t.workspace_bytes(True)
     assert small >= 256 + 8 * 4 * 4096 and big >= small
-    many = L.Tree.from_sizes([4096 * 3] * 2000)  # 6000 tiles > 4096 blocks
-    assert many.workspace_bytes(True) >= 256 + 8 * 4 * 6000
+    many = L.Tree.from_sizes([4096 * 3] * 2000)  # per-leaf: one slot per (chunk, leaf) piece
+    n = 4096 * 3 * 2000
+    assert many.workspace_bytes(True) >= 256 + 8 * 4 * (n // 256 + 2000 + n // 8192 + 2000)
     h = L.opt_adam_hp(1e-3, 0.9, 0.999, 1e-8, 0.0)
     P = 0x10000
     dhp = 0x20000

@@ -194,24 +194,89 @@ def test_maml_fused_inner_matches_torch_inner(pkg):
     assert torch.isfinite(phi2).all() and not torch.equal(phi2, phi)
 
 
-def test_maml_graphed_shard_equals_eager(pkg):
-    """The CUDA-graph replay of a rank's task shard gives the eager result,
-    for two different outer steps (fresh task data through static buffers)."""
+@pytest.mark.parametrize("batched", [False, True])
+def test_maml_meta_gradient_fp32_accuracy(pkg, batched):
+    """The production MAML path (fp32 SGEMM network, fused CUDA inner step;
+    per-task loop or task-batched) against the same meta-gradient computed
+    in float64 with a plain-torch inner step: relative error < 2e-4 (fp32
+    rounding through 3 second-order inner steps; cuDNN's fp32 convolutions
+    miss this by ~2%, tools/maml_net_check.py)."""
     from paper_2211_06934_b200 import maml
 
-    cfg = maml.MamlConfig(tasks=2, inner_steps=2)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    cfg = maml.MamlConfig(tasks=2, inner_steps=3)
+    phi = maml.init_params(0, DEV)
+
+    def torch_inner(g, b, theta):
+        b1 = g if b is None else cfg.inner_momentum * b + g
+        return theta - cfg.inner_lr * b1, b1
+
+    if batched:
+        data32 = [maml.task_data(1, t, DEV) for t in range(2)]
+        mg, loss = maml.meta_grad_batched(phi, data32, cfg, maml.TaskBatchInner(2, DEV, cfg))
+    else:
+        inner = maml.FusedSgdInner(maml.sizes_of(maml.CONV4_SHAPES), DEV, cfg)
+        mg, loss = maml.meta_grad_tasks(phi, range(2), 1, cfg, inner)
+    data = [[a.double() if a.is_floating_point() else a for a in maml.task_data(1, t, DEV)]
+            for t in range(2)]
+    mg64, loss64 = maml.meta_grad_data(phi.double(), data, cfg, torch_inner)
+    err = float((mg.double() - mg64).norm() / mg64.norm())
+    assert err < 2e-4, err
+    assert float(loss) == pytest.approx(float(loss64), rel=1e-5)
+
+
+@pytest.mark.parametrize("streams", [1, 3])
+def test_maml_graphed_shard_equals_eager(pkg, streams):
+    """The CUDA-graph replay of a rank's task shard gives the eager result,
+    for two different outer steps (fresh task data through static buffers),
+    with the tasks captured on one stream or as parallel graph branches."""
+    from paper_2211_06934_b200 import maml
+
+    ntask = 4
+    cfg = maml.MamlConfig(tasks=ntask, inner_steps=2)
     inner = maml.FusedSgdInner(maml.sizes_of(maml.CONV4_SHAPES), DEV, cfg)
     torch.backends.cudnn.deterministic = True
     torch.backends.cudnn.benchmark = False
     torch.backends.cudnn.allow_tf32 = False
-    shard = maml.GraphedShard(range(2), cfg, inner, DEV)
+    shard = maml.GraphedShard(range(ntask), cfg, inner, DEV, streams=streams)
+    assert shard.nstreams == streams
     phi = maml.init_params(0, DEV)
     for step in (0, 3):
-        mg_e, loss_e = maml.meta_grad_tasks(phi, range(2), step, cfg, inner)
-        mg_g, loss_g = shard(phi, range(2), step, cfg, inner)
+        mg_e, loss_e = maml.meta_grad_tasks(phi, range(ntask), step, cfg, inner)
+        mg_g, loss_g = shard(phi, range(ntask), step, cfg, inner)
         torch.testing.assert_close(mg_g, mg_e, rtol=1e-4, atol=1e-6)
         assert float(loss_g) == pytest.approx(float(loss_e), rel=1e-5)
         phi = phi + 1e-3 * mg_e
+
+
+@pytest.mark.parametrize("net", ["cudnn", "gemm"])
+def test_maml_task_batched_equals_per_task(pkg, net):
+    """The task-batched network (grouped convolutions, per-(task, channel)
+    batch norm, one fused inner step over all tasks) gives the per-task
+    loop's meta-gradient and loss; eager and CUDA-graph replay."""
+    from paper_2211_06934_b200 import maml
+
+    ntask = 3
+    cfg = maml.MamlConfig(tasks=ntask, inner_steps=3, net=net)
+    torch.backends.cudnn.deterministic = True
+    torch.backends.cudnn.benchmark = False
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    inner = maml.FusedSgdInner(maml.sizes_of(maml.CONV4_SHAPES), DEV, cfg)
+    inner_b = maml.TaskBatchInner(ntask, DEV, cfg)
+    phi = maml.init_params(0, DEV)
+    mg_e, loss_e = maml.meta_grad_tasks(phi, range(ntask), 2, cfg, inner)
+    data = [maml.task_data(2, t, DEV, cfg.seed) for t in range(ntask)]
+    mg_b, loss_b = maml.meta_grad_batched(phi, data, cfg, inner_b)
+    # two fp32 evaluations (different GEMM / BN reduction orders) of a
+    # 3-step second-order meta-gradient: ~1e-4 apart (each ~1e-4 from fp64,
+    # test_maml_meta_gradient_fp32_accuracy)
+    assert float((mg_b - mg_e).norm()) <= 5e-4 * float(mg_e.norm())
+    assert float(loss_b) == pytest.approx(float(loss_e), rel=1e-5)
+    shard = maml.GraphedShard(range(ntask), cfg, inner, DEV, batched=True)
+    mg_g, loss_g = shard(phi, range(ntask), 2, cfg, inner)
+    assert float((mg_g - mg_e).norm()) <= 5e-4 * float(mg_e.norm())
+    assert float(loss_g) == pytest.approx(float(loss_e), rel=1e-5)
 
 
 def test_functional_per_leaf_lr_and_adamw_meta_gradients(pkg):

@@ -296,13 +296,15 @@ def test_c2_resnet18_full_size_sampled(L, ct):
 
 
 # ----------------------------------------------- more structural cases
-def test_many_leaves_per_leaf_sums(L):
-    """4096 leaves of ragged sizes (the shared-memory leaf table at its
-    limit): per-leaf hyper-gradient sums equal the oracle's; 4097 leaves
-    are rejected with OPT_EINVAL before any launch."""
+@pytest.mark.parametrize("n_leaves", [4096, 10000])
+def test_many_leaves_per_leaf_sums(L, n_leaves):
+    """Thousands of ragged leaves, empty ones included (4096: the offset table
+    staged in shared memory; 10000: searched in global memory): per-leaf
+    hyper-gradient sums and the total equal the oracle's."""
     rng = np.random.default_rng(5)
-    leaves = rng.integers(0, 600, 4096).tolist()
+    leaves = rng.integers(0, 600, n_leaves).tolist()
     leaves[7] = 0  # an empty leaf
+    leaves[-1] = 0  # empty last leaf
     x = synth.state_tree(0xB5, leaves)
     off = synth.offsets_of(leaves)
     tree = L.Tree(offsets=off, device=DEV)
@@ -310,7 +312,7 @@ def test_many_leaves_per_leaf_sums(L):
     g, m, v, du, dm1, dv1 = (dev_f32(x[k]) for k in ("g", "m", "v", "du", "dm1", "dv1"))
     dg = torch.empty_like(g)
     dhp = torch.empty(4, dtype=torch.float64, device=DEV)
-    dhl = torch.empty(4096 * 4, dtype=torch.float64, device=DEV)
+    dhl = torch.empty(n_leaves * 4, dtype=torch.float64, device=DEV)
     L.opt_adam_bwd(tree, 4, hp, 0, 0, g, m, v, du, dm1, dv1, dg, None, None, dhp, dhl,
                    tree.workspace(DEV, per_leaf=True))
     r = oracle.adam_vjp(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], 4, *hp, prec=1,
@@ -320,15 +322,35 @@ def test_many_leaves_per_leaf_sums(L):
     got = host(dhl).reshape(-1, 4)
     hs = np.maximum(r["dhp_abs"], mag["dhp"])
     np.testing.assert_allclose(got, r["dhp_leaf"], rtol=1e-5, atol=1e-6 + 1e-5 * hs.max())
-    assert np.all(got[7] == 0)
-    big = L.Tree(offsets=synth.offsets_of([1] * 4097), device=DEV)
-    z = torch.zeros(4097, device=DEV)
-    with pytest.raises(L.DiffoptError) as e:
-        L.opt_adam_bwd(big, 1, hp, 0, 0, z, None, None, z, None, None, z, None, None,
-                       torch.empty(4, dtype=torch.float64, device=DEV),
-                       torch.empty(4097 * 4, dtype=torch.float64, device=DEV),
-                       big.workspace(DEV, per_leaf=True))
-    assert e.value.code == L.OPT_EINVAL
+    assert np.all(got[7] == 0) and np.all(got[-1] == 0)
+    assert_sum_close("dhp", host(dhp), r["dhp"], hs)
+
+
+def test_per_leaf_sums_large_leaves(L):
+    """Leaves spanning many 256-element chunks and 8192-element super-chunks,
+    with boundaries inside chunks, an empty leaf and a 1-element leaf: the
+    three-level piece/super-chunk/leaf folds give the oracle's per-leaf sums."""
+    leaves = [1_000_003, 3, 8192 * 5 + 1, 0, 77_777, 1, 255, 257]
+    x = synth.state_tree(0xB6, leaves)
+    off = synth.offsets_of(leaves)
+    tree = L.Tree(offsets=off, device=DEV)
+    hp = (3e-3, 0.9, 0.999, 1e-8, 0.0)
+    g, m, v, du, dm1, dv1 = (dev_f32(x[k]) for k in ("g", "m", "v", "du", "dm1", "dv1"))
+    dg, dm, dv = (torch.empty_like(g) for _ in range(3))
+    dhp = torch.empty(4, dtype=torch.float64, device=DEV)
+    dhl = torch.empty(len(leaves) * 4, dtype=torch.float64, device=DEV)
+    L.opt_adam_bwd(tree, 7, hp, 0, 0, g, m, v, du, dm1, dv1, dg, dm, dv, dhp, dhl,
+                   tree.workspace(DEV, per_leaf=True))
+    r = oracle.adam_vjp(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], 7, *hp, prec=1,
+                        offsets=off)
+    mag = oracle.adam_mag(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], 7, *hp)
+    for k, out in (("dg", dg), ("dm", dm), ("dv", dv)):
+        check(k, host(out), r[k], mag[k], 1)
+    got = host(dhl).reshape(-1, 4)
+    hs = np.maximum(r["dhp_abs"], mag["dhp"])
+    np.testing.assert_allclose(got, r["dhp_leaf"], rtol=1e-5, atol=1e-6 + 1e-5 * hs.max())
+    assert np.all(got[3] == 0)
+    assert_sum_close("dhp", host(dhp), r["dhp"], hs)
 
 
 def test_misaligned_device_pointer_rejected(L):

@@ -1,0 +1,9 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1
+timeout 600 python tools/leaf_sweep.py > gpurun_out/leaf_sweep.log 2>&1
+timeout 600 python bench.py --workload es --steps 20 --warmup 3 > gpurun_out/bench_es.json 2> gpurun_out/bench_es.err
+for s in 1 4 8; do
+  timeout 600 python bench.py --workload maml --steps 10 --warmup 3 --maml-streams $s > gpurun_out/bench_maml_s$s.json 2> gpurun_out/bench_maml_s$s.err
+done
