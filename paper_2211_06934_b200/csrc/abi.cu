@@ -263,6 +263,13 @@ int zero_outputs(const opt_tree* t, int nh, double* d_hp, double* d_hp_leaf, cud
 #define DOPT_U_BWD_BF16 DOPT_U_BWD
 #endif
 
+// cp.async double-buffered streaming kernel (step_pipe)
+#ifndef DOPT_PIPE_FWD
+#define DOPT_PIPE_FWD 0
+#endif
+#ifndef DOPT_PIPE_BWD
+#define DOPT_PIPE_BWD 0
+#endif
 #ifndef DOPT_TMA_FWD
 #define DOPT_TMA_FWD 0
 #endif
@@ -313,7 +320,7 @@ constexpr int minb_for() {
 }
 
 // Launch one op: leaf mode, TMA variant or the uniform streaming kernel.
-template <class Op, class ST, int U, int MINB, bool kTma>
+template <class Op, class ST, int U, int MINB, bool kTma, bool kPipe>
 int launch(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r, const opt_tree* t,
            cudaStream_t s) {
   a.d_hp = r.d_hp;
@@ -355,6 +362,20 @@ int launch(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r, const 
     return OPT_OK;
   }
   if (kTma) return launch_tma<Op, ST>(op, a, s);
+  if constexpr (kPipe) {
+    auto k = step_pipe<Op, ST, MINB>;
+    const size_t smem = sizeof(float4) * 2 * Op::NIN * kBlock;
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (attr != cudaSuccess) return fail(OPT_ECUDA, "smem attribute: %s", cudaGetErrorString(attr));
+    int grid = 0;
+    int64_t work = ((a.numel >> 2) + kBlock - 1) / kBlock + 1;
+    int rc = grid_for(k, work, smem, &grid);
+    if (rc) return rc;
+    cudaError_t le = launch_k(k, grid, kBlock, smem, s, op, a);
+    if (le != cudaSuccess) return fail(OPT_ECUDA, "launch: %s", cudaGetErrorString(le));
+    return launched(s);
+  }
   auto k = step_uniform<Op, ST, U, MINB>;
   int grid = 0;
   int64_t work = ((a.numel >> 2) + kBlock - 1) / kBlock + 1;
@@ -373,18 +394,20 @@ int dispatch(int state_dtype, int ct, StepArgs<OpT<float>::NIN, OpT<float>::NOUT
   // bf16 state moves 8-byte vectors: more of them in flight per thread
   constexpr int UB = kBwd ? DOPT_U_BWD_BF16 : DOPT_U_FWD_BF16;
   constexpr bool TMA = kBwd ? (DOPT_TMA_BWD != 0) : (DOPT_TMA_FWD != 0);
+  constexpr bool PIPE = kBwd ? (DOPT_PIPE_BWD != 0) : (DOPT_PIPE_FWD != 0);
   if (ct == OPT_COMPUTE_F64) {
     OpT<double> op;
     fill(op);
     constexpr int MB = minb_for<OpT<double>, kBwd>();
-    if (state_dtype == OPT_BF16) return launch<OpT<double>, bf16, U, MB, TMA>(op, a, r, t, s);
-    return launch<OpT<double>, float, U, MB, TMA>(op, a, r, t, s);
+    if (state_dtype == OPT_BF16)
+      return launch<OpT<double>, bf16, U, MB, TMA, PIPE>(op, a, r, t, s);
+    return launch<OpT<double>, float, U, MB, TMA, PIPE>(op, a, r, t, s);
   }
   OpT<float> op;
   fill(op);
   constexpr int MB = minb_for<OpT<float>, kBwd>();
-  if (state_dtype == OPT_BF16) return launch<OpT<float>, bf16, UB, MB, TMA>(op, a, r, t, s);
-  return launch<OpT<float>, float, U, MB, TMA>(op, a, r, t, s);
+  if (state_dtype == OPT_BF16) return launch<OpT<float>, bf16, UB, MB, TMA, PIPE>(op, a, r, t, s);
+  return launch<OpT<float>, float, U, MB, TMA, PIPE>(op, a, r, t, s);
 }
 
 // b^t by repeated squaring in double (exact integer power).

@@ -23,6 +23,10 @@
 
 namespace dopt {
 
+#ifndef DOPT_SPAN
+#define DOPT_SPAN 0
+#endif
+
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 constexpr int kChunkShift = 8;                // leaf mode: 256-element chunks, one warp each
@@ -161,6 +165,31 @@ __device__ __forceinline__ void process_vectors(const Op& op,
   }
 }
 
+// Warp-span variant: each warp takes 32*U CONSECUTIVE vectors per iteration
+// (U x 512 B contiguous per array instead of U strided 512 B pieces), grid
+// stride over spans; the < 32*U leftover vectors go thread-strided.
+template <class Op, class ST, int U>
+__device__ __forceinline__ void process_spans(const Op& op, const StepArgs<Op::NIN, Op::NOUT>& a,
+                                              int64_t nvec, int64_t tid, int64_t nthreads,
+                                              double* acc, bool want_hp) {
+  constexpr int64_t SPAN = 32 * U;
+  const int64_t lane = tid & 31, gw = tid >> 5, nw = nthreads >> 5;
+  const int64_t full = nvec / SPAN * SPAN;
+  for (int64_t base = gw * SPAN; base < full; base += nw * SPAN) {
+    float x[U][Op::NIN][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) load_vec<Op, ST>(a, base + u * 32 + lane, x[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      compute_store_vec<Op, ST>(op, a, base + u * 32 + lane, x[u], acc, want_hp);
+  }
+  for (int64_t v = full + tid; v < nvec; v += nthreads) {
+    float x[Op::NIN][4];
+    load_vec<Op, ST>(a, v, x);
+    compute_store_vec<Op, ST>(op, a, v, x, acc, want_hp);
+  }
+}
+
 // --------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
@@ -224,7 +253,11 @@ __global__ void __launch_bounds__(kBlock, MINB) step_uniform(const Op op,
   const int64_t nthreads = (int64_t)gridDim.x * kBlock;
   const int64_t tid = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   pdl_wait();
+#if DOPT_SPAN
+  process_spans<Op, ST, U>(op, a, nvec, tid, nthreads, acc, want_hp);
+#else
   process_vectors<Op, ST, U>(op, a, 0, nvec, tid, nthreads, acc, want_hp);
+#endif
   pdl_trigger();
   // ragged tail (numel % 4 elements) -> the last block
   const int64_t tail0 = nvec << 2;
@@ -233,6 +266,109 @@ __global__ void __launch_bounds__(kBlock, MINB) step_uniform(const Op op,
 
   if constexpr (Op::NH > 0) {
     if (!want_hp) return;  // uniform across the grid
+    __shared__ double sm[NH][kWarps];
+    block_sum<NH>(acc, sm);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < NH; ++k) a.partials[(int64_t)blockIdx.x * NH + k] = acc[k];
+    }
+    if (last_block(a.counter, gridDim.x)) {
+      double s[NH];
+#pragma unroll
+      for (int k = 0; k < NH; ++k) s[k] = 0.0;
+      for (int64_t b = threadIdx.x; b < gridDim.x; b += kBlock)
+#pragma unroll
+        for (int k = 0; k < NH; ++k) s[k] += __ldcg(&a.partials[b * NH + k]);
+      block_sum<NH>(s, sm);
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < NH; ++k)
+          if (a.d_hp) a.d_hp[k] = s[k];
+        *a.counter = 0u;
+      }
+    }
+  }
+}
+
+// --------------------------------------------- cp.async pipelined kernel
+// The uniform kernel with the loads of vector v + nthreads in flight (as
+// cp.async copies into this thread's shared-memory slots) while vector v is
+// computed: the bytes in flight per warp no longer drop to zero during the
+// math, without holding a second vector in registers. Dynamic smem:
+// [2 stages][NIN][kBlock] 16-byte slots.
+template <class Op, class ST>
+__device__ __forceinline__ void pipe_issue(const StepArgs<Op::NIN, Op::NOUT>& a, int64_t v,
+                                           float4* slot /* stage base + threadIdx.x */) {
+#pragma unroll
+  for (int i = 0; i < Op::NIN; ++i) {
+    if (a.in[i]) {
+      if (Op::in_state(i) && sizeof(ST) == 2)
+        cp_async8(slot + i * kBlock, static_cast<const uint2*>(a.in[i]) + v);
+      else
+        cp_async16(slot + i * kBlock, static_cast<const float4*>(a.in[i]) + v);
+    }
+  }
+}
+
+template <class Op, class ST>
+__device__ __forceinline__ void pipe_read(const StepArgs<Op::NIN, Op::NOUT>& a,
+                                          const float4* slot, float (&x)[Op::NIN][4]) {
+#pragma unroll
+  for (int i = 0; i < Op::NIN; ++i) {
+    if (a.in[i]) {
+      if (Op::in_state(i) && sizeof(ST) == 2) {
+        const uint2 t = *reinterpret_cast<const uint2*>(slot + i * kBlock);
+        x[i][0] = __uint_as_float(t.x << 16);
+        x[i][1] = __uint_as_float(t.x & 0xFFFF0000u);
+        x[i][2] = __uint_as_float(t.y << 16);
+        x[i][3] = __uint_as_float(t.y & 0xFFFF0000u);
+      } else {
+        const float4 t = slot[i * kBlock];
+        x[i][0] = t.x; x[i][1] = t.y; x[i][2] = t.z; x[i][3] = t.w;
+      }
+    } else {
+      x[i][0] = x[i][1] = x[i][2] = x[i][3] = 0.f;
+    }
+  }
+}
+
+template <class Op, class ST, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) step_pipe(const Op op,
+                                                    const StepArgs<Op::NIN, Op::NOUT> a) {
+  constexpr int NH = Op::NH > 0 ? Op::NH : 1;
+  const bool want_hp = Op::NH > 0 && a.want_hp;
+  extern __shared__ float4 s_pipe[];
+  float4* slot0 = s_pipe + threadIdx.x;
+  float4* slot1 = s_pipe + Op::NIN * kBlock + threadIdx.x;
+  double acc[NH];
+#pragma unroll
+  for (int k = 0; k < NH; ++k) acc[k] = 0.0;
+
+  const int64_t nvec = a.numel >> 2;
+  const int64_t nthreads = (int64_t)gridDim.x * kBlock;
+  int64_t v = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+  pdl_wait();
+  if (v < nvec) pipe_issue<Op, ST>(a, v, slot0);
+  cp_async_commit();
+  bool odd = false;
+  for (; v < nvec; v += nthreads) {
+    const int64_t vn = v + nthreads;
+    if (vn < nvec) pipe_issue<Op, ST>(a, vn, odd ? slot0 : slot1);
+    cp_async_commit();
+    cp_async_wait<1>();  // this thread's copies of vector v have landed
+    float x[Op::NIN][4];
+    pipe_read<Op, ST>(a, odd ? slot1 : slot0, x);
+    compute_store_vec<Op, ST>(op, a, v, x, acc, want_hp);
+    odd = !odd;
+  }
+  cp_async_wait<0>();
+  pdl_trigger();
+  const int64_t tail0 = nvec << 2;
+  if (blockIdx.x == gridDim.x - 1 && tail0 + threadIdx.x < a.numel)
+    process_elem<Op, ST>(op, a, tail0 + threadIdx.x, acc, want_hp);
+
+  if constexpr (Op::NH > 0) {
+    if (!want_hp) return;
     __shared__ double sm[NH][kWarps];
     block_sum<NH>(acc, sm);
     if (threadIdx.x == 0) {

@@ -21,15 +21,29 @@ OUT_KEYS = ("u", "m1", "v1", "dg", "dm", "dv")
 class HostStreamedAdam:
     """Adam fwd + bwd over pinned host arrays of n fp32 elements."""
 
-    def __init__(self, n, device, chunks=8, compute=L.OPT_COMPUTE_DEFAULT):
+    def __init__(self, n, device, chunks=8, compute=L.OPT_COMPUTE_DEFAULT, slots=3,
+                 ramp=None):
+        """chunks: number of equal chunks; or ramp = relative chunk sizes
+        (e.g. (1, 2, 4, 4, 4, 4, 2, 1)): small first / last chunks shorten
+        the pipeline fill (first H2D alone) and drain (last D2H alone)
+        without paying per-copy overhead on every chunk."""
         self.n, self.dev, self.compute = int(n), device, compute
         align = 4096
-        per = -(-self.n // chunks)
-        per = -(-per // align) * align
-        self.bounds = [(s, min(s + per, self.n)) for s in range(0, self.n, per)]
+        weights = list(ramp) if ramp else [1] * int(chunks)
+        tot = float(sum(weights))
+        cuts = [0]
+        acc = 0.0
+        for w in weights[:-1]:
+            acc += w
+            cut = min(self.n, -(-int(self.n * acc / tot) // align) * align)
+            cuts.append(max(cut, cuts[-1]))
+        cuts.append(self.n)
+        self.bounds = [(a, b) for a, b in zip(cuts, cuts[1:]) if b > a]
+        per = max(b - a for a, b in self.bounds)
         self.trees = [L.Tree(numel=e - s, device=device) for s, e in self.bounds]
         self.ws = [t.workspace(device) for t in self.trees]
-        self.nb = nb = 3  # staging slots: H2D of chunk c overlaps D2H of c-1 and c-2
+        self.nb = nb = max(2, min(int(slots), len(self.bounds)))  # staging slots: H2D of
+        # chunk c overlaps D2H of chunks c-1 .. c-nb+1
         self.buf = [{k: torch.empty(per, device=device) for k in IN_KEYS + OUT_KEYS}
                     for _ in range(nb)]
         self.dhp = torch.empty(len(self.bounds), 4, dtype=torch.float64, device=device)

@@ -19,6 +19,19 @@ def one(cfg):
     if "ub" in extra:  # e.g. ub2x2: bf16 U fwd x bwd
         spec = extra.split("ub")[1][:3]
         defs += [f"DOPT_U_FWD_BF16={spec[0]}", f"DOPT_U_BWD_BF16={spec[2]}"]
+    import re
+    m = re.search(r"ld(\d)", extra)
+    if m:
+        defs.append(f"DOPT_LD_POLICY={m.group(1)}")
+    m = re.search(r"st(\d)", extra)
+    if m:
+        defs.append(f"DOPT_ST_POLICY={m.group(1)}")
+    if "span" in extra:
+        defs.append("DOPT_SPAN=1")
+    if "pipeF" in extra:
+        defs.append("DOPT_PIPE_FWD=1")
+    if "pipeB" in extra:
+        defs.append("DOPT_PIPE_BWD=1")
     if "pdl" in extra:
         defs.append("DOPT_PDL=1")
     if "ieee" in extra:
