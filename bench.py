@@ -290,13 +290,13 @@ def time_e2e(args, W, dev):
     ms_serial = timed(serial)
     out = {"serial_ms_per_step": round(ms_serial, 4)}
     if W.sd == 0 and W.n >= 1 << 16 and len(ins) == 6:
-        hs = HostStreamedAdam(W.n, dev, chunks=16, compute=W.compute)
+        hs = HostStreamedAdam(W.n, dev, chunks=8, compute=W.compute)
         hin = {k: h_in[k] for k in IN_KEYS}
         hout = {k: h_out[k] for k in OUT_KEYS}
         ms = timed(lambda: hs.run(hin, hout, STEP_T, HP))
         h2d, d2h = hs.bytes_h2d(), hs.bytes_d2h()
         how = ("paper_2211_06934_b200.offload.HostStreamedAdam: pinned host inputs/outputs, "
-               "16 chunks, H2D / opt_adam_fwd+bwd / D2H overlapped on 3 streams; all copies "
+               "8 chunks, H2D / opt_adam_fwd+bwd / D2H overlapped on 3 streams; all copies "
                "inside the timed region")
     else:
         ms = ms_serial
