@@ -537,6 +537,102 @@ def sgd_fwd_ex_complex(g, b, theta, hp, lr_elem, nesterov=False, weight_decay=0.
     return tuple(outs[2 * k] + 1j * outs[2 * k + 1] for k in range(2))
 
 
+# ------------------------- RMSProp centred / momentum (NEXT-1, reading N4)
+def _cm_lib():
+    L = _ex_lib()
+    if getattr(L, "_cm_ready", False):
+        return L
+    P, i64, I, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    L.oracle_rmsprop_cm_fwd.argtypes = [i64, P, P, P, i64, P, I, I] + [P] * 9
+    L.oracle_rmsprop_cm_vjp.argtypes = [i64, P, P, P, i64, P, I, I] + [P] * 17
+    L.oracle_rmsprop_cm_mag.argtypes = [i64, P, P, P, i64, P, I] + [P] * 11
+    L.oracle_rmsprop_cm_fwd_cplx.argtypes = [i64, P, P, I, D, D, I] + [P] * 20
+    L._cm_ready = True
+    return L
+
+
+def _cm_hp(lr, alpha, eps, momentum, centered):
+    return _hp([lr, alpha, eps, momentum, 1.0 if centered else 0.0])
+
+
+def rmsprop_cm_fwd(g, v, a, b, theta, lr, alpha, eps, momentum=0.0, centered=False,
+                   weight_decay=0.0, maximize=False, lr_leaf=None, offsets=None,
+                   state_bf16=False, prec=0):
+    """Centred and/or momentum RMSProp step (torch.optim.RMSprop semantics):
+    (u, v', a', b'); v, a (gradient average), b (momentum buffer) None = 0."""
+    g, theta = _f32(g), _f32(theta)
+    n = g.size
+    v, a, b = (_state(x, state_bf16) for x in (v, a, b))
+    lrl, nl, off = _leaf_args(lr_leaf, offsets)
+    u, v1, a1, b1 = _out(n), _out(n), _out(n), _out(n)
+    _cm_lib().oracle_rmsprop_cm_fwd(n, _p(_cm_hp(lr, alpha, eps, momentum, centered)),
+                                    _p(_ext(weight_decay, False, maximize)), _p(lrl), nl,
+                                    _p(off), int(state_bf16), int(prec), _p(g), _p(v), _p(a),
+                                    _p(b), _p(theta), _p(u), _p(v1), _p(a1), _p(b1))
+    return u, v1, a1, b1
+
+
+def rmsprop_cm_vjp(g, v, a, b, theta, du, dv1, da1, db1, lr, alpha, eps, momentum=0.0,
+                   centered=False, weight_decay=0.0, maximize=False, lr_leaf=None, offsets=None,
+                   state_bf16=False, prec=0):
+    """VJP of rmsprop_cm_fwd: dg, dv, da, db, dtheta (through the update) and
+    dhp = (lr, alpha, eps, momentum, wd) (+ dhp_abs, dhp_leaf)."""
+    g, theta = _f32(g), _f32(theta)
+    n = g.size
+    v, a, b = (_state(x, state_bf16) for x in (v, a, b))
+    du, dv1, da1, db1 = _f32(du), _f32(dv1), _f32(da1), _f32(db1)
+    lrl, nl, off = _leaf_args(lr_leaf, offsets)
+    dg, dv, da, db, dth = (_out(n) for _ in range(5))
+    dhp, dabs = np.zeros(5), np.zeros(5)
+    leaf = np.zeros((nl, 5)) if off is not None else None
+    _cm_lib().oracle_rmsprop_cm_vjp(n, _p(_cm_hp(lr, alpha, eps, momentum, centered)),
+                                    _p(_ext(weight_decay, False, maximize)), _p(lrl), nl,
+                                    _p(off), int(state_bf16), int(prec), _p(g), _p(v), _p(a),
+                                    _p(b), _p(theta), _p(du), _p(dv1), _p(da1), _p(db1), _p(dg),
+                                    _p(dv), _p(da), _p(db), _p(dth), _p(dhp), _p(dabs), _p(leaf))
+    return dict(dg=dg, dv=dv, da=da, db=db, dtheta=dth, dhp=dhp, dhp_abs=dabs, dhp_leaf=leaf)
+
+
+def rmsprop_cm_mag(g, v, a, b, theta, du, dv1, da1, db1, lr, alpha, eps, momentum=0.0,
+                   centered=False, weight_decay=0.0, maximize=False, lr_leaf=None, offsets=None,
+                   state_bf16=False):
+    """Magnitude twins (Z10) of every output and of the 5 hyper sums."""
+    g, theta = _f32(g), _f32(theta)
+    n = g.size
+    v, a, b = (_state(x, state_bf16) for x in (v, a, b))
+    du, dv1, da1, db1 = _f32(du), _f32(dv1), _f32(da1), _f32(db1)
+    lrl, nl, off = _leaf_args(lr_leaf, offsets)
+    out = np.empty(9 * n)
+    hs = np.zeros(5)
+    _cm_lib().oracle_rmsprop_cm_mag(n, _p(_cm_hp(lr, alpha, eps, momentum, centered)),
+                                    _p(_ext(weight_decay, False, maximize)), _p(lrl), nl,
+                                    _p(off), int(state_bf16), _p(g), _p(v), _p(a), _p(b),
+                                    _p(theta), _p(du), _p(dv1), _p(da1), _p(db1), _p(out),
+                                    _p(hs))
+    o = out.reshape(9, n)
+    keys = ("u", "v1", "a1", "b1", "dg", "dv", "da", "db", "dtheta")
+    r = {k: o[i] for i, k in enumerate(keys)}
+    r["dhp"] = hs
+    return r
+
+
+def rmsprop_cm_fwd_complex(g, v, a, b, theta, hp, lr_elem, centered=False, weight_decay=0.0,
+                           maximize=False):
+    """Complex forward of rmsprop_cm_fwd (complex-step pins): hp = (lr
+    unused, alpha, eps, momentum), complex; lr given per element."""
+    g = np.asarray(g, dtype=np.complex128)
+    n = g.size
+    hr, hi = _cparts(hp, 4)
+    parts = [_cparts(x, n) for x in (lr_elem, g, v, a, b, theta)]
+    flat = [q for pr in parts for q in pr]
+    wd = complex(weight_decay)
+    outs = [np.empty(n) for _ in range(8)]
+    _cm_lib().oracle_rmsprop_cm_fwd_cplx(n, _p(hr), _p(hi), int(centered), wd.real, wd.imag,
+                                         int(maximize), *[_p(q) for q in flat],
+                                         *[_p(o) for o in outs])
+    return tuple(outs[2 * k] + 1j * outs[2 * k + 1] for k in range(4))
+
+
 def ex_mag(kind, g, state, theta, du, ds1, dv1=None, t=1, hp=(), weight_decay=0.0,
            decoupled=False, maximize=False, lr_leaf=None, offsets=None, state_bf16=False):
     """Magnitude twins (Z10) of the variant outputs: the base twins evaluated

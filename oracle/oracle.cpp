@@ -889,6 +889,137 @@ void oracle_sgd_fwd_ex_cplx(int64_t n, const double* hp_re, const double* hp_im,
 
 }  // extern "C"
 
+// ------------------------- RMSProp centred / momentum (NEXT-1) entry points
+// hp[5] = {lr, alpha, eps, momentum, centered}; ext[3] as above (decoupled
+// ignored); states v, a (gradient average), b (momentum buffer) may be NULL
+// (zero). Hyper slots (lr, alpha, eps, momentum, wd).
+namespace {
+
+template <class T>
+oracle::RmsCmHP<T> rms_cm_hp(const double* hp) {
+  return {T(hp[0]), T(hp[1]), T(hp[2]), T(hp[3]), hp[4] != 0.0 ? 1 : 0};
+}
+
+template <class T>
+void rms_cm_fwd_arr(int64_t n, const double* hp, const double* ext, const double* lr_leaf,
+                    int64_t nl, const int64_t* off, int bf, const float* g, const void* v,
+                    const void* a, const void* b, const float* th, double* u, double* v1,
+                    double* a1, double* b1) {
+  oracle::ExHP<T> x = ex_hp<T>(ext);
+  x.decoupled = 0;
+  per_leaf_elements(n, nl, off, [&](int64_t i, int64_t l) {
+    oracle::RmsCmHP<T> h = rms_cm_hp<T>(hp);
+    if (lr_leaf) h.lr = T(lr_leaf[l]);
+    auto r = oracle::rmsprop_cm_fwd<T>(T(f32_in(g, i)), T(state_in(v, bf, i)),
+                                       T(state_in(a, bf, i)), T(state_in(b, bf, i)),
+                                       T(f32_in(th, i)), h, x);
+    put(u, i, (double)r.u);
+    put(v1, i, (double)r.v1);
+    put(a1, i, (double)r.a1);
+    put(b1, i, (double)r.b1);
+  });
+}
+
+template <class T>
+void rms_cm_vjp_arr(int64_t n, const double* hp, const double* ext, const double* lr_leaf,
+                    int64_t nl, const int64_t* off, int bf, const float* g, const void* v,
+                    const void* a, const void* b, const float* th, const float* du,
+                    const float* dv1, const float* da1, const float* db1, double* dg, double* dv,
+                    double* da, double* db, double* dth, double* dhp, double* dhp_abs,
+                    double* dhp_leaf) {
+  oracle::ExHP<T> x = ex_hp<T>(ext);
+  x.decoupled = 0;
+  vjp_ex_loop<T, 5>(n, nl, off, dhp, dhp_abs, dhp_leaf, [&](int64_t i, int64_t l, T* h) {
+    oracle::RmsCmHP<T> hh = rms_cm_hp<T>(hp);
+    if (lr_leaf) hh.lr = T(lr_leaf[l]);
+    auto r = oracle::rmsprop_cm_vjp<T>(T(f32_in(g, i)), T(state_in(v, bf, i)),
+                                       T(state_in(a, bf, i)), T(state_in(b, bf, i)),
+                                       T(f32_in(th, i)), T(f32_in(du, i)), T(f32_in(dv1, i)),
+                                       T(f32_in(da1, i)), T(f32_in(db1, i)), hh, x);
+    put(dg, i, (double)r.dg);
+    put(dv, i, (double)r.dv);
+    put(da, i, (double)r.da);
+    put(db, i, (double)r.db);
+    put(dth, i, (double)r.dtheta);
+    h[0] = r.dlr; h[1] = r.dalpha; h[2] = r.deps; h[3] = r.dmu; h[4] = r.dwd;
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+void oracle_rmsprop_cm_fwd(int64_t n, const double* hp, const double* ext, const double* lr_leaf,
+                           int64_t nl, const int64_t* off, int bf, int prec, const float* g,
+                           const void* v, const void* a, const void* b, const float* th,
+                           double* u, double* v1, double* a1, double* b1) {
+  if (prec) rms_cm_fwd_arr<long double>(n, hp, ext, lr_leaf, nl, off, bf, g, v, a, b, th, u, v1, a1, b1);
+  else rms_cm_fwd_arr<double>(n, hp, ext, lr_leaf, nl, off, bf, g, v, a, b, th, u, v1, a1, b1);
+}
+
+void oracle_rmsprop_cm_vjp(int64_t n, const double* hp, const double* ext, const double* lr_leaf,
+                           int64_t nl, const int64_t* off, int bf, int prec, const float* g,
+                           const void* v, const void* a, const void* b, const float* th,
+                           const float* du, const float* dv1, const float* da1, const float* db1,
+                           double* dg, double* dv, double* da, double* db, double* dth,
+                           double* dhp, double* dhp_abs, double* dhp_leaf) {
+  if (prec)
+    rms_cm_vjp_arr<long double>(n, hp, ext, lr_leaf, nl, off, bf, g, v, a, b, th, du, dv1, da1,
+                                db1, dg, dv, da, db, dth, dhp, dhp_abs, dhp_leaf);
+  else
+    rms_cm_vjp_arr<double>(n, hp, ext, lr_leaf, nl, off, bf, g, v, a, b, th, du, dv1, da1, db1,
+                           dg, dv, da, db, dth, dhp, dhp_abs, dhp_leaf);
+}
+
+// Magnitude twins: out[k*n + i] for k = u, v1, a1, b1, dg, dv, da, db, dtheta;
+// hsum[5] = Sigma of the hyper twins (element lr from lr_leaf when given).
+void oracle_rmsprop_cm_mag(int64_t n, const double* hp, const double* ext,
+                           const double* lr_leaf, int64_t nl, const int64_t* off, int bf,
+                           const float* g, const void* v, const void* a, const void* b,
+                           const float* th, const float* du, const float* dv1, const float* da1,
+                           const float* db1, double* out, double* hsum) {
+  oracle::ExHP<double> x = ex_hp<double>(ext);
+  x.decoupled = 0;
+  long double hs[5] = {0, 0, 0, 0, 0};
+  per_leaf_elements(n, nl, off, [&](int64_t i, int64_t l) {
+    oracle::RmsCmHP<double> h = rms_cm_hp<double>(hp);
+    if (lr_leaf) h.lr = lr_leaf[l];
+    auto r = oracle::rmsprop_cm_mag(f32_in(g, i), state_in(v, bf, i), state_in(a, bf, i),
+                                    state_in(b, bf, i), f32_in(th, i), f32_in(du, i),
+                                    f32_in(dv1, i), f32_in(da1, i), f32_in(db1, i), h, x);
+    const double o[9] = {r.u, r.v1, r.a1, r.b1, r.dg, r.dv, r.da, r.db, r.dtheta};
+    for (int k = 0; k < 9; ++k) out[k * n + i] = o[k];
+    for (int k = 0; k < 5; ++k) hs[k] += r.h[k];
+  });
+  for (int k = 0; k < 5; ++k) hsum[k] = (double)hs[k];
+}
+
+// Complex forward (complex-step pins); per-ELEMENT lr; hp_re/hp_im[4] =
+// (lr unused, alpha, eps, momentum).
+void oracle_rmsprop_cm_fwd_cplx(int64_t n, const double* hp_re, const double* hp_im,
+                                int centered, double wd_re, double wd_im, int maximize,
+                                const double* lr_re, const double* lr_im, const double* g_re,
+                                const double* g_im, const double* v_re, const double* v_im,
+                                const double* a_re, const double* a_im, const double* b_re,
+                                const double* b_im, const double* th_re, const double* th_im,
+                                double* u_re, double* u_im, double* v1_re, double* v1_im,
+                                double* a1_re, double* a1_im, double* b1_re, double* b1_im) {
+  oracle::ExHP<cd> x{cd(wd_re, wd_im), 0, maximize};
+  for (int64_t i = 0; i < n; ++i) {
+    oracle::RmsCmHP<cd> h{cin(lr_re, lr_im, i), cin(hp_re, hp_im, 1), cin(hp_re, hp_im, 2),
+                          cin(hp_re, hp_im, 3), centered};
+    auto r = oracle::rmsprop_cm_fwd<cd>(cin(g_re, g_im, i), cin(v_re, v_im, i),
+                                        cin(a_re, a_im, i), cin(b_re, b_im, i),
+                                        cin(th_re, th_im, i), h, x);
+    cout_(u_re, u_im, i, r.u);
+    cout_(v1_re, v1_im, i, r.v1);
+    cout_(a1_re, a1_im, i, r.a1);
+    cout_(b1_re, b1_im, i, r.b1);
+  }
+}
+
+}  // extern "C"
+
 // ------------------------------------------------ zero-order ES (NEXT-3)
 extern "C" {
 

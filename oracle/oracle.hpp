@@ -454,6 +454,152 @@ SgdVjpEx<T> sgd_vjp_ex(T g, T b, T theta, T du, T db1_out, const SgdHP<T>& h, co
 
 }  // namespace oracle
 
+// ------------------------- RMSProp, centred and/or with momentum (NEXT-1)
+// SURVEY §8(f) NEXT-1 "centered and momentum RMSProp"; torch.optim.RMSprop
+// semantics (reading N4), with g~ as in the variants above:
+//   v' = alpha v + (1-alpha) g~^2
+//   centred:  a' = alpha a + (1-alpha) g~,  q = v' - a'^2    (else a' = a, q = v')
+//   d  = sqrt(q) + eps,  w = g~ / d
+//   b' = mu b + w,       u = -lr b'          (mu = 0: u = -lr g~/d, the plain step)
+// Conventions: sqrt(q) := 0 for q <= 0 (and its adjoint 1/(2 sqrt q) := 0);
+// w := 0 when d = 0 (Z6/Z7 extended). Reverse mode: one adjoint per forward
+// intermediate, in reverse order.
+namespace oracle {
+
+template <class T>
+struct RmsCmHP {
+  T lr, alpha, eps, mu;
+  int centered;
+};
+
+template <class T>
+struct RmsCmFwd {
+  T u, v1, a1, b1;
+};
+
+template <class T>
+RmsCmFwd<T> rmsprop_cm_fwd(T g, T v, T a, T b, T theta, const RmsCmHP<T>& h, const ExHP<T>& x) {
+  const T one(1);
+  const T gm = x.maximize ? -g : g;
+  const T gt = gm + x.wd * theta;
+  const T v1 = h.alpha * v + (one - h.alpha) * gt * gt;
+  const T a1 = h.centered ? h.alpha * a + (one - h.alpha) * gt : a;
+  const T q = h.centered ? v1 - a1 * a1 : v1;
+  const T r = re(q) > 0.0 ? tsqrt(q) : T(0);
+  const T d = r + h.eps;
+  const T w = re(d) == 0.0 ? T(0) : gt / d;
+  const T b1 = h.mu * b + w;
+  return {-h.lr * b1, v1, a1, b1};
+}
+
+template <class T>
+struct RmsCmVjp {
+  T dg, dv, da, db, dtheta;  // dtheta: through the update only
+  T dlr, dalpha, deps, dmu, dwd;
+};
+
+template <class T>
+RmsCmVjp<T> rmsprop_cm_vjp(T g, T v, T a, T b, T theta, T du, T dv1_out, T da1_out, T db1_out,
+                           const RmsCmHP<T>& h, const ExHP<T>& x) {
+  const T one(1), two(2);
+  // forward intermediates
+  const T gm = x.maximize ? -g : g;
+  const T gt = gm + x.wd * theta;
+  const T v1 = h.alpha * v + (one - h.alpha) * gt * gt;
+  const T a1 = h.centered ? h.alpha * a + (one - h.alpha) * gt : a;
+  const T q = h.centered ? v1 - a1 * a1 : v1;
+  const bool q_pos = re(q) > 0.0;
+  const T r = q_pos ? tsqrt(q) : T(0);
+  const T d = r + h.eps;
+  const bool d_zero = re(d) == 0.0;
+  const T w = d_zero ? T(0) : gt / d;
+  const T b1 = h.mu * b + w;
+  RmsCmVjp<T> o;
+  // u = -lr * b1
+  o.dlr = du * (-b1);
+  const T db1 = db1_out + du * (-h.lr);
+  // b1 = mu * b + w
+  o.dmu = db1 * b;
+  o.db = db1 * h.mu;
+  const T dw = db1;
+  // w = gt / d
+  T dgt = d_zero ? T(0) : dw / d;
+  const T dd = d_zero ? T(0) : -dw * gt / (d * d);
+  // d = r + eps
+  o.deps = dd;
+  const T dr = dd;
+  // r = sqrt(q)
+  const T dq = q_pos ? dr / (two * r) : T(0);
+  // q = v1 - a1^2 (centred) or v1
+  const T dv1 = dv1_out + dq;
+  const T da1 = h.centered ? da1_out - two * a1 * dq : da1_out;
+  // a1 = alpha a + (1 - alpha) gt (centred) or a
+  o.dalpha = T(0);
+  if (h.centered) {
+    o.dalpha = da1 * (a - gt);
+    o.da = da1 * h.alpha;
+    dgt = dgt + da1 * (one - h.alpha);
+  } else {
+    o.da = da1;
+  }
+  // v1 = alpha v + (1 - alpha) gt^2
+  o.dalpha = o.dalpha + dv1 * (v - gt * gt);
+  o.dv = dv1 * h.alpha;
+  dgt = dgt + dv1 * (one - h.alpha) * two * gt;
+  // gt = (maximize ? -g : g) + wd theta
+  o.dwd = dgt * theta;
+  o.dtheta = dgt * x.wd;
+  o.dg = x.maximize ? -dgt : dgt;
+  return o;
+}
+
+// Magnitude twin (Z10) of the reduced kernel forms (ops.cuh RmsCm*):
+//   dg~ = 2(1-alpha) g~ dv1 + (1-alpha) da1 + B [eps + alpha (v - a a1)/r] / d^2,
+//   B = db1 - lr du, qbar = -B g~/(2 r d^2), dv = alpha (dv1 + qbar),
+//   da = alpha (da1 - 2 a1 qbar). Centred q = v' - a'^2 can cancel: every
+// output downstream of q is scaled by kappa = (|v'| + a'^2)_mag / q.
+struct RmsCmMag {
+  double u, v1, a1, b1, dg, dv, da, db, dtheta, h[5];
+};
+
+inline RmsCmMag rmsprop_cm_mag(double g, double v, double a, double b, double theta, double du,
+                               double dv1, double da1, double db1, const RmsCmHP<double>& h,
+                               const ExHP<double>& x) {
+  const double al = h.alpha, om = 1 - al, lr = std::fabs(h.lr), eps = h.eps, mu = h.mu;
+  const double gt = (x.maximize ? -g : g) + x.wd * theta;
+  const double agt = std::fabs(g) + x.wd * std::fabs(theta);
+  const double v1 = al * v + om * gt * gt;
+  const double a1 = h.centered ? al * a + om * gt : a;
+  const double q = h.centered ? v1 - a1 * a1 : v1;
+  const double r = q > 0 ? std::sqrt(q) : 0.0, d = r + eps;
+  const double rd = d == 0 ? 0 : 1 / d, rs = r == 0 ? 0 : 1 / r;
+  RmsCmMag o;
+  o.v1 = al * std::fabs(v) + om * agt * agt;
+  o.a1 = h.centered ? al * std::fabs(a) + om * agt : std::fabs(a);
+  const double qmag = h.centered ? o.v1 + o.a1 * o.a1 : o.v1;
+  const double k = q > 0 ? qmag / q : 1.0;
+  const double w = agt * rd;
+  o.b1 = k * (mu * std::fabs(b) + w);
+  o.u = lr * o.b1;
+  const double B = std::fabs(db1) + lr * std::fabs(du);
+  const double qb = 0.5 * B * agt * rd * rd * rs;
+  o.dg = k * (2 * om * agt * std::fabs(dv1) + om * std::fabs(da1) +
+              B * rd * rd * (eps + al * (std::fabs(v) + std::fabs(a) * o.a1) * rs));
+  o.dv = k * al * (std::fabs(dv1) + qb);
+  o.da = k * al * (std::fabs(da1) + 2 * o.a1 * qb);
+  o.db = mu * B;
+  o.dtheta = x.wd * o.dg;
+  o.h[0] = std::fabs(du) * o.b1;
+  o.h[1] = k * ((std::fabs(dv1) + qb) * (std::fabs(v) + agt * agt) +
+                (h.centered ? (std::fabs(da1) + 2 * o.a1 * qb) * (std::fabs(a) + agt) : 0.0));
+  o.h[2] = k * B * agt * rd * rd;
+  o.h[3] = B * std::fabs(b);
+  o.h[4] = o.dg * std::fabs(theta);
+  return o;
+}
+
+}  // namespace oracle
+
 // ------------------------------------------------ zero-order ES (NEXT-3)
 // PAPER.md §2.2 "Zero-order Differentiation (ZD)": ES optimizes the
 // Gaussian smoothing f~_sigma(theta) = E_z[f(theta + sigma z)], z ~ N(0, I_d),

@@ -19,6 +19,7 @@ _CHUNK = 1 << 22
 # stream ids: one per input role
 S_G, S_M, S_V, S_DU, S_DM1, S_DV1, S_ZERO, S_SCALE = 1, 2, 3, 4, 5, 6, 7, 8
 S_A, S_THETA0, S_PHI, S_Y = 9, 10, 11, 12
+S_GAVG, S_BUF, S_DA1, S_DB1 = 13, 14, 15, 16
 
 RESNET18_LEAVES = [
     9408, 64, 64, 36864, 64, 64, 36864, 64, 64, 36864, 64, 64, 36864, 64, 64, 73728, 128, 128,
@@ -118,6 +119,29 @@ def state_tree(seed, leaves, index=None, warm=True, zero_frac=1.0 / 256, n=None)
     dm1 = normal(seed, S_DM1, index=idx).astype(np.float32)
     dv1 = normal(seed, S_DV1, index=idx).astype(np.float32)
     return dict(g=g.astype(np.float32), m=m, v=v, du=du, dm1=dm1, dv1=dv1)
+
+
+def rms_cm_tree(seed, leaves, index=None, zero_frac=1.0 / 256):
+    """Inputs of the centred / momentum RMSProp step (NEXT-1, reading N4):
+    per-leaf scale s as in state_tree; g = s N; gradient average a = 0.5 s N;
+    v = a^2 + (s (|N| + 0.1))^2 (a consistent centred state: v >= a^2, so
+    q = v' - a'^2 > 0); momentum buffer b ~ N(0,1) (it accumulates g/d);
+    theta ~ N(0,1); cotangents du, dv1, da1, db1 ~ N(0,1); a fraction
+    ``zero_frac`` of elements have g = a = v = 0 exactly."""
+    total = int(sum(leaves))
+    idx = np.arange(total, dtype=np.int64) if index is None else np.asarray(index, np.int64)
+    scale = 10.0 ** (-4.0 * uniform(seed, S_SCALE, index=leaf_ids(offsets_of(leaves), idx)))
+    zero = uniform(seed, S_ZERO, index=idx) < zero_frac
+    g = scale * normal(seed, S_G, index=idx)
+    a = 0.5 * scale * normal(seed, S_GAVG, index=idx)
+    v = a * a + (scale * (np.abs(normal(seed, S_V, index=idx)) + 0.1)) ** 2
+    for x in (g, a, v):
+        x[zero] = 0.0
+    f = lambda x: x.astype(np.float32)
+    return dict(g=f(g), v=f(v), a=f(a), b=f(normal(seed, S_BUF, index=idx)),
+                theta=f(normal(seed, S_THETA0, index=idx)),
+                du=f(normal(seed, S_DU, index=idx)), dv1=f(normal(seed, S_DV1, index=idx)),
+                da1=f(normal(seed, S_DA1, index=idx)), db1=f(normal(seed, S_DB1, index=idx)))
 
 
 def c1_inputs(seed=0xC1, n=4096):

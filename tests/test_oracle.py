@@ -696,6 +696,131 @@ def test_rms_sgd_variant_vjp_vs_complex_step(orc, kind):
         assert r["dhp_leaf"][l, 0] == pytest.approx(contract(F(lr=lrc)).sum(), rel=1e-8)
 
 
+# ------------------------- centred / momentum RMSProp (NEXT-1 pins, N4)
+def _torch_rmsprop_one_step(g, v, a, b, th, lr, alpha, eps, momentum, centered, wd, maximize):
+    """torch.optim.RMSprop (float64), one step from the given state."""
+    p = torch.tensor(th, dtype=torch.float64, requires_grad=True)
+    opt = torch.optim.RMSprop([p], lr=lr, alpha=alpha, eps=eps, momentum=momentum,
+                              centered=centered, weight_decay=wd, maximize=maximize)
+    p.grad = torch.zeros_like(p)
+    opt.step()  # creates the state tensors
+    st = opt.state[p]
+    with torch.no_grad():
+        p.copy_(torch.as_tensor(th, dtype=torch.float64))
+        st["square_avg"].copy_(torch.as_tensor(v, dtype=torch.float64))
+        if centered:
+            st["grad_avg"].copy_(torch.as_tensor(a, dtype=torch.float64))
+        if momentum > 0:
+            st["momentum_buffer"].copy_(torch.as_tensor(b, dtype=torch.float64))
+    p.grad = torch.as_tensor(g, dtype=torch.float64)
+    opt.step()
+    out = dict(u=(p.detach() - torch.as_tensor(th, dtype=torch.float64)).numpy(),
+               v1=st["square_avg"].numpy())
+    if centered:
+        out["a1"] = st["grad_avg"].numpy()
+    if momentum > 0:
+        out["b1"] = st["momentum_buffer"].numpy()
+    return out
+
+
+@pytest.mark.parametrize("centered", [False, True])
+@pytest.mark.parametrize("momentum", [0.0, 0.9])
+@pytest.mark.parametrize("maximize", [False, True])
+def test_rmsprop_cm_matches_torch_optim(orc, centered, momentum, maximize):
+    """The centred / momentum RMSProp forward (reading N4) reproduces one
+    torch.optim.RMSprop step in float64 from a warm state: update, square
+    average, gradient average and momentum buffer."""
+    x = synth.rms_cm_tree(0xC7, [200, 57], zero_frac=0.02)
+    kw = dict(lr=1e-2, alpha=0.95, eps=1e-6, momentum=momentum, centered=centered)
+    wd = 0.05
+    ref = _torch_rmsprop_one_step(x["g"], x["v"], x["a"], x["b"], x["theta"], wd=wd,
+                                  maximize=maximize, **kw)
+    u, v1, a1, b1 = orc.rmsprop_cm_fwd(x["g"], x["v"], x["a"], x["b"], x["theta"],
+                                       weight_decay=wd, maximize=maximize, **kw)
+    np.testing.assert_allclose(u, ref["u"], rtol=1e-10, atol=1e-15)
+    np.testing.assert_allclose(v1, ref["v1"], rtol=1e-12, atol=1e-300)
+    if centered:
+        np.testing.assert_allclose(a1, ref["a1"], rtol=1e-12, atol=1e-300)
+    if momentum > 0:
+        np.testing.assert_allclose(b1, ref["b1"], rtol=1e-10, atol=1e-15)
+
+
+def test_rmsprop_cm_reduces_to_plain_rmsprop(orc):
+    """Not centred, momentum 0: update, v' and every VJP output equal the
+    plain RMSProp variant's; the momentum gradient is Sigma (db1 - lr du) b."""
+    x = synth.rms_cm_tree(0xC8, [300])
+    kw = dict(weight_decay=0.02, maximize=True)
+    u, v1, _, _ = orc.rmsprop_cm_fwd(x["g"], x["v"], None, None, x["theta"], 1e-2, 0.9, 1e-8, **kw)
+    u0, v0 = orc.rmsprop_fwd_ex(x["g"], x["v"], x["theta"], 1e-2, 0.9, 1e-8, **kw)
+    np.testing.assert_allclose(u, u0, rtol=1e-15, atol=0)
+    np.testing.assert_array_equal(v1, v0)
+    r = orc.rmsprop_cm_vjp(x["g"], x["v"], None, x["b"], x["theta"], x["du"], x["dv1"], None,
+                           None, 1e-2, 0.9, 1e-8, **kw)
+    r0 = orc.rmsprop_vjp_ex(x["g"], x["v"], x["theta"], x["du"], x["dv1"], 1e-2, 0.9, 1e-8, **kw)
+    for k in ("dg", "dv", "dtheta"):
+        np.testing.assert_allclose(r[k], r0[k], rtol=1e-13, atol=1e-300)
+    np.testing.assert_allclose(r["dhp"][[0, 1, 2, 4]], r0["dhp"], rtol=1e-12)
+    assert r["dhp"][3] == pytest.approx(
+        np.sum(-1e-2 * x["du"].astype(np.float64) * x["b"].astype(np.float64)), rel=1e-12)
+
+
+@pytest.mark.parametrize("centered", [False, True])
+@pytest.mark.parametrize("momentum", [0.0, 0.9])
+def test_rmsprop_cm_vjp_vs_complex_step(orc, centered, momentum):
+    """Every VJP output of the centred / momentum RMSProp step (dg, dv, da,
+    db, dtheta, the five global hyper-gradients and the per-leaf lr
+    gradients) equals the complex-step derivative of the torch-pinned
+    forward, contracted with the four cotangents."""
+    leaves = [90, 60]
+    off = synth.offsets_of(leaves)
+    x = synth.rms_cm_tree(0xC9, leaves, zero_frac=0.0)
+    lr_leaf = np.array([2e-2, 6e-3])
+    lr_e = np.repeat(lr_leaf, leaves)
+    hp = np.array([0.0, 0.93, 1e-7, momentum])
+    wd = 0.04
+    d = {k: x[k].astype(np.float64) for k in x}
+    cot = (d["du"], d["dv1"], d["da1"], d["db1"])
+    contract = lambda outs: sum(c * o.imag / H for c, o in zip(cot, outs))
+
+    def F(g=d["g"], v=d["v"], a=d["a"], b=d["b"], th=d["theta"], hp_=hp, lr=lr_e, w=wd):
+        return orc.rmsprop_cm_fwd_complex(g, v, a, b, th, hp_, lr, centered, w, True)
+
+    r = orc.rmsprop_cm_vjp(x["g"], x["v"], x["a"], x["b"], x["theta"], x["du"], x["dv1"],
+                           x["da1"], x["db1"], 0.0, 0.93, 1e-7, momentum=momentum,
+                           centered=centered, weight_decay=wd, maximize=True, lr_leaf=lr_leaf,
+                           offsets=off, prec=1)
+    for name, kw in (("dg", dict(g=d["g"] + 1j * H)), ("dv", dict(v=d["v"] + 1j * H)),
+                     ("da", dict(a=d["a"] + 1j * H)), ("db", dict(b=d["b"] + 1j * H)),
+                     ("dtheta", dict(th=d["theta"] + 1j * H))):
+        cs = contract(F(**kw))
+        np.testing.assert_allclose(r[name], cs, rtol=1e-8, atol=1e-12 * np.abs(cs).max())
+    for k in (1, 2, 3):  # alpha, eps, momentum
+        hpc = hp.astype(np.complex128)
+        hpc[k] += 1j * H
+        assert r["dhp"][k] == pytest.approx(contract(F(hp_=hpc)).sum(), rel=1e-8, abs=1e-12)
+    assert r["dhp"][4] == pytest.approx(contract(F(w=wd + 1j * H)).sum(), rel=1e-8)
+    for l in range(2):
+        lrc = lr_e.astype(np.complex128)
+        lrc[off[l]:off[l + 1]] += 1j * H
+        assert r["dhp_leaf"][l, 0] == pytest.approx(contract(F(lr=lrc)).sum(), rel=1e-8)
+
+
+def test_rmsprop_cm_zero_point_conventions(orc):
+    """g = a = v = 0 with eps = 0: q = 0, d = 0, so w := 0 (u = -lr mu b),
+    and the q-adjoint is 0 (no inf/nan anywhere)."""
+    z = np.zeros(4, np.float32)
+    b = np.array([1.0, -2.0, 0.5, 0.0], np.float32)
+    u, v1, a1, b1 = orc.rmsprop_cm_fwd(z, z, z, b, z, 0.1, 0.9, 0.0, momentum=0.5, centered=True)
+    np.testing.assert_array_equal(u, -0.1 * 0.5 * b.astype(np.float64))
+    r = orc.rmsprop_cm_vjp(z, z, z, b, z, np.ones(4, np.float32), np.ones(4, np.float32),
+                           np.ones(4, np.float32), np.ones(4, np.float32), 0.1, 0.9, 0.0,
+                           momentum=0.5, centered=True)
+    for k in ("dg", "dv", "da", "db"):
+        assert np.all(np.isfinite(r[k]))
+    np.testing.assert_allclose(r["dg"], 0.1 * 1.0, rtol=1e-15)  # (1-alpha) da1
+    np.testing.assert_allclose(r["dv"], 0.9, rtol=1e-15)  # alpha dv1
+
+
 # --------------------------------------------- zero-order ES (NEXT-3 pins)
 def test_es_noise_is_standard_normal_and_independent(orc):
     """The counter-based noise (reading N3) has the moments of N(0,1), matches
