@@ -56,7 +56,7 @@
 extern "C" {
 #endif
 
-#define DIFFOPT_ABI_VERSION 2
+#define DIFFOPT_ABI_VERSION 3
 
 typedef enum {
   OPT_OK = 0,
@@ -203,6 +203,34 @@ int opt_rmsprop_bwd_ex(const opt_tree* tree, const opt_rmsprop_hp* hp, const opt
                        int state_dtype, int compute, const float* g, const void* nu,
                        const float* params, const float* d_updates, const float* d_nu_out,
                        float* d_g, float* d_nu, float* d_params, double* d_hp, double* d_hp_leaf,
+                       void* workspace, size_t workspace_bytes, void* stream);
+/* Centred and/or momentum RMSProp (SURVEY §8(f) NEXT-1 "centered and
+ * momentum RMSProp"; torch.optim.RMSprop semantics, reading N4):
+ *   g~ = (maximize ? -g : g) + weight_decay * params   (ext; decoupled ignored)
+ *   v' = alpha v + (1-alpha) g~^2
+ *   centered: a' = alpha a + (1-alpha) g~, q = v' - a'^2   (else q = v')
+ *   d = sqrt(q) + eps  (sqrt(q <= 0) := 0),  w = g~/d  (0 at d = 0)
+ *   b' = momentum b + w,  u = -lr b'   (momentum = 0: u = -lr g~/d)
+ * State: nu (square average), gavg (gradient average; used only when
+ * centered), buf (momentum buffer); each may be NULL on input (zero state)
+ * and NULL on output (not written). Valid: lr finite, 0 <= alpha < 1,
+ * eps >= 0, 0 <= momentum < 1. Per-leaf lr via ext->lr_leaf. */
+typedef struct { double lr, alpha, eps, momentum; int centered; } opt_rmsprop_cm_hp;
+int opt_rmsprop_cm_fwd(const opt_tree* tree, const opt_rmsprop_cm_hp* hp, const opt_ext* ext,
+                       int state_dtype, int compute, const float* g, const void* nu,
+                       const void* gavg, const void* buf, const float* params, float* updates,
+                       void* nu_out, void* gavg_out, void* buf_out, float* params_out,
+                       void* stream);
+/* Backward: cotangents of (updates, nu_out, gavg_out, buf_out) in; d_g,
+ * d_nu, d_gavg, d_buf and d_params (through the update only; add d_updates
+ * for a fused apply) out; d_hp[5] = (lr, alpha, eps, momentum,
+ * weight_decay) sums, d_hp_leaf[n_leaves][5] per leaf. */
+int opt_rmsprop_cm_bwd(const opt_tree* tree, const opt_rmsprop_cm_hp* hp, const opt_ext* ext,
+                       int state_dtype, int compute, const float* g, const void* nu,
+                       const void* gavg, const void* buf, const float* params,
+                       const float* d_updates, const float* d_nu_out, const float* d_gavg_out,
+                       const float* d_buf_out, float* d_g, float* d_nu, float* d_gavg,
+                       float* d_buf, float* d_params, double* d_hp, double* d_hp_leaf,
                        void* workspace, size_t workspace_bytes, void* stream);
 int opt_sgd_fwd_ex(const opt_tree* tree, const opt_sgd_hp* hp, const opt_ext* ext,
                    int state_dtype, int compute, const float* g, const void* mom,

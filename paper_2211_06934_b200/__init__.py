@@ -12,10 +12,10 @@ library raises; there is no CPU fallback.
 from . import _lib
 from ._lib import Tree, DiffoptError, OPT_F32, OPT_BF16, OPT_COMPUTE_DEFAULT, OPT_COMPUTE_F32, \
     OPT_COMPUTE_F64
-from .functional import (AdamStep, RmsPropStep, SgdStep, ApplyUpdates, FlatTree, adam, rmsprop,
-                         sgd, apply_updates)
+from .functional import (AdamStep, RmsPropStep, RmsCmStep, SgdStep, ApplyUpdates, FlatTree,
+                         adam, rmsprop, sgd, apply_updates)
 
-__all__ = ["Tree", "DiffoptError", "AdamStep", "RmsPropStep", "SgdStep", "ApplyUpdates",
+__all__ = ["Tree", "DiffoptError", "AdamStep", "RmsPropStep", "RmsCmStep", "SgdStep", "ApplyUpdates",
            "FlatTree", "adam", "rmsprop", "sgd", "apply_updates", "OPT_F32", "OPT_BF16",
            "OPT_COMPUTE_DEFAULT", "OPT_COMPUTE_F32", "OPT_COMPUTE_F64"]
 from . import implicit, offload, unroll  # noqa: E402  (drivers above the C ABI)

@@ -262,7 +262,9 @@ class opt_ext(ctypes.Structure):
 
 
 def _ext(weight_decay=0.0, decoupled=False, maximize=False, lr_leaf=None):
-    return opt_ext(float(weight_decay), int(bool(decoupled)), int(bool(maximize)), _ptr(lr_leaf))
+    e = opt_ext(float(weight_decay), int(bool(decoupled)), int(bool(maximize)), _ptr(lr_leaf))
+    e._keep = lr_leaf  # the struct holds a raw device pointer: keep the tensor alive with it
+    return e
 
 
 def _setup_ex():
@@ -338,6 +340,52 @@ def opt_sgd_bwd_ex(tree, hp, ext, state_dtype, compute, g, mom, params, d_update
                               _ptr(mom), _ptr(params), _ptr(d_updates), _ptr(d_mom_out),
                               _ptr(d_g), _ptr(d_mom), _ptr(d_params), _ptr(d_hp),
                               _ptr(d_hp_leaf), wp, wb, _stream(stream)))
+
+
+# ------------------------------ RMSProp centred / momentum (NEXT-1, N4)
+class opt_rmsprop_cm_hp(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_double), ("alpha", ctypes.c_double), ("eps", ctypes.c_double),
+                ("momentum", ctypes.c_double), ("centered", ctypes.c_int)]
+
+
+def _rms_cm_hp(hp):
+    lr, alpha, eps, momentum, centered = hp
+    return opt_rmsprop_cm_hp(float(lr), float(alpha), float(eps), float(momentum),
+                             int(bool(centered)))
+
+
+_T, _E = ctypes.POINTER(opt_tree), ctypes.POINTER(opt_ext)
+lib.opt_rmsprop_cm_fwd.argtypes = [_T, ctypes.POINTER(opt_rmsprop_cm_hp), _E, ctypes.c_int,
+                                   ctypes.c_int] + [ctypes.c_void_p] * 11
+lib.opt_rmsprop_cm_bwd.argtypes = [_T, ctypes.POINTER(opt_rmsprop_cm_hp), _E, ctypes.c_int,
+                                   ctypes.c_int] + [ctypes.c_void_p] * 17 + [ctypes.c_size_t,
+                                                                             ctypes.c_void_p]
+lib.opt_rmsprop_cm_fwd.restype = ctypes.c_int
+lib.opt_rmsprop_cm_bwd.restype = ctypes.c_int
+EXPORTS += ["opt_rmsprop_cm_fwd", "opt_rmsprop_cm_bwd"]
+
+
+def opt_rmsprop_cm_fwd(tree, hp, ext, state_dtype, compute, g, nu, gavg, buf, params, updates,
+                       nu_out, gavg_out, buf_out, params_out=None, stream=None):
+    """hp = (lr, alpha, eps, momentum, centered)."""
+    _check(lib.opt_rmsprop_cm_fwd(ctypes.byref(tree.c), ctypes.byref(_rms_cm_hp(hp)),
+                                  ctypes.byref(ext), int(state_dtype), int(compute), _ptr(g),
+                                  _ptr(nu), _ptr(gavg), _ptr(buf), _ptr(params), _ptr(updates),
+                                  _ptr(nu_out), _ptr(gavg_out), _ptr(buf_out), _ptr(params_out),
+                                  _stream(stream)))
+
+
+def opt_rmsprop_cm_bwd(tree, hp, ext, state_dtype, compute, g, nu, gavg, buf, params, d_updates,
+                       d_nu_out, d_gavg_out, d_buf_out, d_g, d_nu, d_gavg, d_buf, d_params,
+                       d_hp=None, d_hp_leaf=None, workspace=None, stream=None):
+    """d_hp (5 doubles) = (lr, alpha, eps, momentum, weight_decay)."""
+    wp, wb = _ws(workspace)
+    _check(lib.opt_rmsprop_cm_bwd(ctypes.byref(tree.c), ctypes.byref(_rms_cm_hp(hp)),
+                                  ctypes.byref(ext), int(state_dtype), int(compute), _ptr(g),
+                                  _ptr(nu), _ptr(gavg), _ptr(buf), _ptr(params), _ptr(d_updates),
+                                  _ptr(d_nu_out), _ptr(d_gavg_out), _ptr(d_buf_out), _ptr(d_g),
+                                  _ptr(d_nu), _ptr(d_gavg), _ptr(d_buf), _ptr(d_params),
+                                  _ptr(d_hp), _ptr(d_hp_leaf), wp, wb, _stream(stream)))
 
 
 # ------------------------------------------------ zero-order ES (NEXT-3)

@@ -514,6 +514,23 @@ void fill_ext(Op& op, const opt_ext* e, bool adam) {
   op.maximize = e->maximize ? 1 : 0;
 }
 
+int check_rms_cm(const opt_rmsprop_cm_hp* hp) {
+  if (!hp) return fail(OPT_EINVAL, "hp is NULL");
+  if (!finite(hp->lr)) return fail(OPT_EINVAL, "lr is not finite");
+  if (!unit(hp->alpha)) return fail(OPT_EINVAL, "alpha = %g outside [0, 1)", hp->alpha);
+  if (!(finite(hp->eps) && hp->eps >= 0)) return fail(OPT_EINVAL, "eps = %g < 0", hp->eps);
+  if (!unit(hp->momentum)) return fail(OPT_EINVAL, "momentum = %g outside [0, 1)", hp->momentum);
+  return OPT_OK;
+}
+
+template <class Op>
+void fill_rms_cm(Op& op, const opt_rmsprop_cm_hp* hp, const opt_ext* e) {
+  typedef typename Op::CT CT;
+  op.alpha = (CT)hp->alpha; op.oma = (CT)(1.0 - hp->alpha); op.lr = (CT)hp->lr;
+  op.eps = (CT)hp->eps; op.mu = (CT)hp->momentum; op.centered = hp->centered ? 1 : 0;
+  op.wd = (CT)e->weight_decay; op.maximize = e->maximize ? 1 : 0;
+}
+
 int check_ext(const opt_ext* e, const float* params, const opt_tree* t) {
   if (!e) return fail(OPT_EINVAL, "ext is NULL");
   if (!(finite(e->weight_decay) && e->weight_decay >= 0))
@@ -746,6 +763,65 @@ int opt_rmsprop_bwd_ex(const opt_tree* tree, const opt_rmsprop_hp* hp, const opt
     fill_rms_bwd(op.base, hp);
     fill_ext(op, ext, false);
   });
+}
+
+// ------------------------------------- RMSProp centred / momentum (NEXT-1)
+int opt_rmsprop_cm_fwd(const opt_tree* tree, const opt_rmsprop_cm_hp* hp, const opt_ext* ext,
+                       int state_dtype, int compute, const float* g, const void* nu,
+                       const void* gavg, const void* buf, const float* params, float* updates,
+                       void* nu_out, void* gavg_out, void* buf_out, float* params_out,
+                       void* stream) {
+  g_err.clear();
+  int ct = 0;
+  TRY(check_tree(tree));
+  TRY(check_rms_cm(hp));
+  TRY(check_ext(ext, params, tree));
+  TRY(check_state_dtype(state_dtype));
+  TRY(resolve_compute(compute, &ct));
+  TRY(check_align({g, nu, gavg, buf, params, updates, nu_out, gavg_out, buf_out, params_out}));
+  if (tree->numel == 0) return OPT_OK;
+  if (!g) return fail(OPT_EINVAL, "g is NULL");
+  Reduce r;
+  TRY(setup_reduce(tree, nullptr, nullptr, ext->lr_leaf, nullptr, 0, &r));
+  StepArgs<5, 5> a{};
+  a.in[0] = g; a.in[1] = nu; a.in[2] = hp->centered ? gavg : nullptr; a.in[3] = buf;
+  a.in[4] = params;
+  a.out[0] = updates; a.out[1] = nu_out; a.out[2] = hp->centered ? gavg_out : nullptr;
+  a.out[3] = buf_out; a.out[4] = params ? params_out : nullptr;
+  a.numel = tree->numel;
+  return dispatch<RmsCmFwd, false>(state_dtype, ct, a, r, tree, static_cast<cudaStream_t>(stream),
+                                   [&](auto& op) { fill_rms_cm(op, hp, ext); });
+}
+
+int opt_rmsprop_cm_bwd(const opt_tree* tree, const opt_rmsprop_cm_hp* hp, const opt_ext* ext,
+                       int state_dtype, int compute, const float* g, const void* nu,
+                       const void* gavg, const void* buf, const float* params,
+                       const float* d_updates, const float* d_nu_out, const float* d_gavg_out,
+                       const float* d_buf_out, float* d_g, float* d_nu, float* d_gavg,
+                       float* d_buf, float* d_params, double* d_hp, double* d_hp_leaf,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  int ct = 0;
+  TRY(check_tree(tree));
+  TRY(check_rms_cm(hp));
+  TRY(check_ext(ext, params, tree));
+  TRY(check_state_dtype(state_dtype));
+  TRY(resolve_compute(compute, &ct));
+  TRY(check_align({g, nu, gavg, buf, params, d_updates, d_nu_out, d_gavg_out, d_buf_out, d_g,
+                   d_nu, d_gavg, d_buf, d_params}));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (tree->numel == 0) return zero_outputs(tree, 5, d_hp, d_hp_leaf, s);
+  if (!g) return fail(OPT_EINVAL, "g is NULL");
+  Reduce r;
+  TRY(setup_reduce(tree, d_hp, d_hp_leaf, ext->lr_leaf, workspace, workspace_bytes, &r));
+  StepArgs<9, 5> a{};
+  a.in[0] = g; a.in[1] = nu; a.in[2] = hp->centered ? gavg : nullptr; a.in[3] = buf;
+  a.in[4] = params; a.in[5] = d_updates; a.in[6] = d_nu_out; a.in[7] = d_gavg_out;
+  a.in[8] = d_buf_out;
+  a.out[0] = d_g; a.out[1] = d_nu; a.out[2] = d_gavg; a.out[3] = d_buf; a.out[4] = d_params;
+  a.numel = tree->numel;
+  return dispatch<RmsCmBwd, true>(state_dtype, ct, a, r, tree, s,
+                                  [&](auto& op) { fill_rms_cm(op, hp, ext); });
 }
 
 // ------------------------------------------------------------------- SGD

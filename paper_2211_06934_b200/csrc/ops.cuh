@@ -382,4 +382,88 @@ struct SgdBwdEx : ExCommon<SgdBwd<CT_>> {
   }
 };
 
+// -------------------------- RMSProp centred / momentum (NEXT-1, reading N4)
+// torch.optim.RMSprop semantics on g~ = (maximize ? -g : g) + wd theta:
+//   v' = alpha v + (1-alpha) g~^2;  centred: a' = alpha a + (1-alpha) g~,
+//   q = v' - a'^2 (else a' = a, q = v');  d = sqrt(q) + eps;  w = g~/d;
+//   b' = mu b + w;  u = -lr b'.
+// Reduced VJP (no cancellation between the w path and the q path), with
+// B = db1 - lr du, T = B/d^2, r = sqrt(q):
+//   dg~ = 2(1-alpha) g~ dv1 + (1-alpha) da1 [centred]
+//         + T (eps + alpha (v - a a1) / r)          (a a1 := 0 if not centred)
+//   qbar = -g~ T/(2 r),  dv = alpha (dv1 + qbar),  da = alpha (da1 - 2 a1 qbar)
+//   db = mu B; hyper: lr -du b1, alpha (dv1+qbar)(v-g~^2) + A (a-g~), eps -g~ T,
+//   mu B b, wd dg~ theta. sqrt(q <= 0) := 0 and its adjoint := 0.
+template <class CT_>
+struct RmsCmFwd {
+  typedef CT_ CT;
+  // in: g v a b theta ; out: u v' a' b' theta'
+  static constexpr int NIN = 5, NOUT = 5, NH = 0;
+  __host__ __device__ static constexpr bool in_state(int i) { return i >= 1 && i <= 3; }
+  __host__ __device__ static constexpr bool out_state(int i) { return i >= 1 && i <= 3; }
+  CT alpha, oma, lr, eps, mu, wd;
+  int centered, maximize;
+
+  __device__ __forceinline__ void set_lr(CT l) { lr = l; }
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT*,
+                                             bool) const {
+    const CT th = x[4];
+    const CT gt = (maximize ? -CT(x[0]) : CT(x[0])) + wd * th;
+    const CT v1 = alpha * CT(x[1]) + oma * (gt * gt);
+    const CT a1 = centered ? alpha * CT(x[2]) + oma * gt : CT(x[2]);
+    const CT q = centered ? v1 - a1 * a1 : v1;
+    const CT d = q * rsqrt_or_zero(q) + eps;
+    const CT b1 = mu * CT(x[3]) + gt * safe_rcp(d);
+    y[0] = -lr * b1;
+    y[1] = v1;
+    y[2] = a1;
+    y[3] = b1;
+    y[4] = th + y[0];
+  }
+};
+
+template <class CT_>
+struct RmsCmBwd {
+  typedef CT_ CT;
+  // in: g v a b theta du dv1 da1 db1 ; out: dg dv da db dtheta
+  // hyper: lr alpha eps mu wd
+  static constexpr int NIN = 9, NOUT = 5, NH = 5;
+  __host__ __device__ static constexpr bool in_state(int i) { return i >= 1 && i <= 3; }
+  __host__ __device__ static constexpr bool out_state(int) { return false; }
+  CT alpha, oma, lr, eps, mu, wd;  // every field set by abi.cu fill_rms_cm
+  int centered, maximize;
+
+  __device__ __forceinline__ void set_lr(CT l) { lr = l; }
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT* h,
+                                             bool want_hp) const {
+    const CT v = x[1], a = x[2], b = x[3], th = x[4], du = x[5], dv1 = x[6], da1 = x[7];
+    const CT gt = (maximize ? -CT(x[0]) : CT(x[0])) + wd * th;
+    const CT gg = gt * gt;
+    const CT v1 = alpha * v + oma * gg;
+    const CT a1 = centered ? alpha * a + oma * gt : a;
+    const CT q = centered ? v1 - a1 * a1 : v1;
+    const CT rs = rsqrt_or_zero(q);          // 1/r  (0 at q <= 0)
+    const CT rd = safe_rcp(q * rs + eps);    // 1/d  (0 at d = 0)
+    const CT B = CT(x[8]) - lr * du;         // total cotangent of b'
+    const CT T = B * rd * rd;
+    const CT qb = CT(-0.5) * (gt * T) * rs;  // cotangent of q
+    const CT V = dv1 + qb;
+    const CT A = centered ? da1 - CT(2) * a1 * qb : da1;
+    const CT dgt = CT(2) * oma * gt * dv1 + (centered ? oma * da1 : CT(0)) +
+                   T * (eps + alpha * (v - (centered ? a * a1 : CT(0))) * rs);
+    y[0] = maximize ? -dgt : dgt;
+    y[1] = alpha * V;
+    y[2] = centered ? alpha * A : A;
+    y[3] = mu * B;
+    y[4] = wd * dgt;
+    if (want_hp) {
+      h[0] -= du * (mu * b + gt * rd);                          // lr
+      h[1] += V * (v - gg) + (centered ? A * (a - gt) : CT(0));  // alpha
+      h[2] -= gt * T;                                            // eps
+      h[3] += B * b;                                             // momentum
+      h[4] += dgt * th;                                          // weight decay
+    }
+  }
+};
+
 }  // namespace dopt

@@ -277,6 +277,57 @@ class StepEx(torch.autograd.Function):
         return (d_g, d_s0, d_s1, d_p, hg[0], hg[-1], d_lrl, hps_grad, None, None, None, None)
 
 
+class RmsCmStep(torch.autograd.Function):
+    """Centred and/or momentum RMSProp (NEXT-1, reading N4) with weight
+    decay, maximize and per-leaf lr: (g, nu, gavg, buf, params, lr, alpha,
+    eps, momentum, wd, lr_leaf) -> (params + u if fused else u, nu', gavg',
+    buf'). Differentiable in every tensor input and hyper-parameter."""
+
+    @staticmethod
+    def forward(ctx, g, nu, gavg, buf, params, lr, alpha, eps, mom, wd, lr_leaf, opts, cfg):
+        centered, maximize, fused = opts
+        g, nu, gavg, buf, params = (_contig(x) for x in (g, nu, gavg, buf, params))
+        sd = cfg.state_dtype if cfg.state_dtype is not None else _sd(nu, gavg, buf)
+        ext = L._ext(_f(wd), False, maximize, None if lr_leaf is None else lr_leaf.detach())
+        hp = (_f(lr), _f(alpha), _f(eps), _f(mom), bool(centered))
+        out = torch.empty_like(g)
+        n_nu, n_buf = _empty_state(g, sd), _empty_state(g, sd)
+        n_gavg = _empty_state(g, sd) if centered else g.new_zeros(0)
+        L.opt_rmsprop_cm_fwd(cfg.tree, hp, ext, sd, cfg.compute, g, nu, gavg, buf, params,
+                             None if fused else out, n_nu, n_gavg if centered else None, n_buf,
+                             out if fused else None)
+        ctx.save_for_backward(g, nu, gavg, buf, params, lr_leaf)
+        ctx.meta = (hp, ext, sd, cfg, fused, centered, (lr, alpha, eps, mom, wd))
+        return out, n_nu, n_gavg, n_buf
+
+    @staticmethod
+    @once_differentiable
+    def backward(ctx, d_out, d_nu1, d_gavg1, d_buf1):
+        g, nu, gavg, buf, params, lr_leaf = ctx.saved_tensors
+        hp, ext, sd, cfg, fused, centered, hyp = ctx.meta
+        want_leaf = lr_leaf is not None and lr_leaf.requires_grad
+        want_hp = want_leaf or any(_needs(x) for x in hyp)
+        d_g = torch.empty_like(g)
+        d_nu = None if nu is None else torch.empty_like(g)
+        d_gavg = None if (gavg is None or not centered) else torch.empty_like(g)
+        d_buf = None if buf is None else torch.empty_like(g)
+        d_p = None if params is None else torch.empty_like(g)
+        d_hp = torch.empty(5, dtype=torch.float64, device=g.device) if want_hp else None
+        d_leaf = (torch.empty(cfg.tree.n_leaves * 5, dtype=torch.float64, device=g.device)
+                  if want_leaf else None)
+        ws = _workspace(cfg.tree, g.device, per_leaf=want_leaf) if want_hp else None
+        if d_gavg1 is not None and d_gavg1.numel() == 0:
+            d_gavg1 = None
+        L.opt_rmsprop_cm_bwd(cfg.tree, hp, ext, sd, cfg.compute, g, nu, gavg, buf, params,
+                             _contig(d_out), _contig(d_nu1), _contig(d_gavg1), _contig(d_buf1),
+                             d_g, d_nu, d_gavg, d_buf, d_p, d_hp, d_leaf, ws)
+        if d_p is not None and fused:
+            d_p = d_p + d_out  # identity of the fused apply_updates
+        hg = [None] * 5 if d_hp is None else [_hp_grad(x, d_hp[k]) for k, x in enumerate(hyp)]
+        d_lrl = d_leaf.view(-1, 5)[:, 0].to(lr_leaf.dtype) if want_leaf else None
+        return (d_g, d_nu, d_gavg, d_buf, d_p, *hg, d_lrl, None, None)
+
+
 class ApplyUpdates(torch.autograd.Function):
     """params + updates (row a8); backward is the identity for both."""
 
@@ -357,6 +408,8 @@ class GradientTransformation:
         flat_p = None
         if params is not None:
             flat_p = params if isinstance(params, torch.Tensor) else layout.flatten(params)
+        if self.kind == "rmsprop_cm":
+            return self._update_cm(flat, state, flat_p, cfg, t, inplace, differentiable)
         if self.ext is not None:
             return self._update_ex(flat, state, flat_p, cfg, t, inplace, differentiable)
         if self.kind == "adam":
@@ -409,6 +462,26 @@ class GradientTransformation:
         return out, OptState(t, slots, state.layout)
 
 
+    def _update_cm(self, flat, state, flat_p, cfg, t, inplace, differentiable):
+        e = self.ext or dict(weight_decay=0.0, maximize=False, lr_leaf=None)
+        if _f(e["weight_decay"]) != 0.0 and flat_p is None:
+            raise ValueError("weight_decay needs update(..., params=...)")
+        lr_leaf = e.get("lr_leaf")
+        if lr_leaf is not None and lr_leaf.numel() != cfg.tree.n_leaves:
+            raise ValueError("lr_leaf must have one entry per leaf")
+        lr, alpha, eps, mom, centered = self.hp
+        nu, gavg, buf = state.slots
+        out, n_nu, n_gavg, n_buf = RmsCmStep.apply(
+            flat, nu, gavg, buf, flat_p, lr, alpha, eps, mom, e["weight_decay"], lr_leaf,
+            (bool(centered), bool(e.get("maximize", False)), False), cfg)
+        slots = (n_nu, n_gavg if centered else None, n_buf)
+        if inplace and not differentiable:
+            for old, new in zip(state.slots, slots):
+                if old is not None and new is not None:
+                    old.copy_(new)
+        return out, OptState(t, slots, state.layout)
+
+
 def _any_requires_grad(grads, state):
     ts = [grads] if isinstance(grads, torch.Tensor) else list(grads)
     ts += [s for s in state.slots if s is not None]
@@ -449,12 +522,19 @@ def adam(lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, eps_root=0.0, weight_decay=0.0, de
 
 
 def rmsprop(lr=1e-2, alpha=0.99, eps=1e-8, weight_decay=0.0, maximize=False, lr_leaf=None,
-            compute=L.OPT_COMPUTE_DEFAULT, state_dtype=L.OPT_F32):
-    """RMSProp (S:206-207)."""
+            centered=False, momentum=0.0, compute=L.OPT_COMPUTE_DEFAULT, state_dtype=L.OPT_F32):
+    """RMSProp; ``centered`` / ``momentum`` select the torch.optim
+    RMSprop forms (NEXT-1, reading N4: opt_rmsprop_cm_fwd/bwd, state = square
+    average, gradient average, momentum buffer)."""
     _check_lr(lr)
     _check_unit("alpha", alpha)
+    _check_unit("momentum", momentum)
     if not _f(eps) >= 0.0:
         raise ValueError("eps must be >= 0")
+    if centered or _f(momentum) != 0.0:
+        return GradientTransformation("rmsprop_cm", (lr, alpha, eps, momentum, bool(centered)), 3,
+                                      compute, state_dtype,
+                                      _ext_opts(weight_decay, False, maximize, lr_leaf))
     return GradientTransformation("rmsprop", (lr, alpha, eps), 1, compute, state_dtype,
                                   _ext_opts(weight_decay, False, maximize, lr_leaf))
 

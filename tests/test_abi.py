@@ -153,3 +153,21 @@ def test_variant_validation(L):
                               ctypes.byref(L._ext(lr_leaf=0x20000)), 0, 0, P, P, P, P, P, P, P, P,
                               None, None, None, 0, 0)
     assert rc == L.OPT_EINVAL and "d_offsets" in L.lib.opt_last_error().decode()
+
+
+def test_rmsprop_cm_validation(L):
+    """Centred / momentum RMSProp: invalid hyper-parameters are rejected on
+    the host before any launch (no GPU needed)."""
+    t = L.Tree(numel=64)
+    P = 0x10000
+    ext = L._ext()
+    for hp in ((1e-2, 1.0, 1e-8, 0.0, 0), (1e-2, 0.9, -1.0, 0.0, 0), (1e-2, 0.9, 1e-8, 1.0, 1),
+               (float("nan"), 0.9, 1e-8, 0.5, 1)):
+        h = L.opt_rmsprop_cm_hp(*hp)
+        rc = L.lib.opt_rmsprop_cm_fwd(ctypes.byref(t.c), ctypes.byref(h), ctypes.byref(ext), 0, 0,
+                                      P, P, P, P, P, P, P, P, P, P, 0)
+        assert rc == L.OPT_EINVAL
+    h = L.opt_rmsprop_cm_hp(1e-2, 0.9, 1e-8, 0.5, 1)
+    rc = L.lib.opt_rmsprop_cm_fwd(ctypes.byref(t.c), ctypes.byref(h), ctypes.byref(ext), 0, 0,
+                                  P + 4, P, P, P, P, P, P, P, P, P, 0)
+    assert rc == L.OPT_EALIGN

@@ -329,6 +329,59 @@ def test_functional_per_leaf_lr_and_adamw_meta_gradients(pkg):
     assert gwd_f == pytest.approx(gwd_r, rel=2e-4, abs=1e-6)
 
 
+def test_functional_centered_momentum_rmsprop_meta_gradients(pkg):
+    """Listing-1 loop with centred momentum RMSProp (weight decay, learnable
+    per-leaf lr, learnable alpha / eps / momentum): meta-gradients equal the
+    same program written with plain float64 torch ops
+    (torch.optim.RMSprop's update rule, composed)."""
+    torch.manual_seed(2)
+    shapes = [(5, 4), (7,), (2, 3)]
+    p0 = [torch.randn(s, device=DEV) for s in shapes]
+    tgt = [torch.randn(s, device=DEV) for s in shapes]
+    lr0 = torch.tensor([0.03, 0.01, 0.05])
+
+    def run(fused):
+        dt = torch.float32 if fused else torch.float64
+        lr_leaf = lr0.to(DEV, dt).clone().requires_grad_(True)
+        mk = lambda x: torch.tensor(x, dtype=torch.float64, requires_grad=True)
+        alpha, eps, mom, wd = mk(0.9), mk(1e-3), mk(0.8), mk(0.02)
+        params = [p.to(dt).clone().requires_grad_(True) for p in p0]
+        if fused:
+            layout = pkg.FlatTree.of(params)
+            flat = layout.flatten(params)
+            opt = pkg.rmsprop(lr=1e-2, alpha=alpha, eps=eps, momentum=mom, centered=True,
+                              weight_decay=wd, lr_leaf=lr_leaf)
+            state = opt.init(params)
+            for _ in range(3):
+                ps = layout.views(flat)
+                inner = sum(((p - t) ** 4).sum() for p, t in zip(ps, tgt))
+                (g,) = torch.autograd.grad(inner, flat, create_graph=True)
+                upd, state = opt.update(g, state, params=flat)
+                flat = pkg.apply_updates(flat, upd)
+            ps = layout.views(flat)
+        else:
+            ps = params
+            v = [torch.zeros_like(p) for p in ps]
+            a = [torch.zeros_like(p) for p in ps]
+            b = [torch.zeros_like(p) for p in ps]
+            for _ in range(3):
+                inner = sum(((p - tt.to(dt)) ** 4).sum() for p, tt in zip(ps, tgt))
+                gs = torch.autograd.grad(inner, ps, create_graph=True)
+                gs = [gg + wd * p for gg, p in zip(gs, ps)]
+                v = [alpha * x + (1 - alpha) * gg * gg for x, gg in zip(v, gs)]
+                a = [alpha * x + (1 - alpha) * gg for x, gg in zip(a, gs)]
+                b = [mom * x + gg / ((vv - aa * aa).sqrt() + eps)
+                     for x, gg, vv, aa in zip(b, gs, v, a)]
+                ps = [p - lr_leaf[i] * bb for i, (p, bb) in enumerate(zip(ps, b))]
+        outer = sum((p.double() ** 2).sum() for p in ps)
+        grads = torch.autograd.grad(outer, [lr_leaf, alpha, eps, mom, wd])
+        return [x.double().cpu() for x in grads]
+
+    got, ref = run(True), run(False)
+    for name, x, y in zip(("lr_leaf", "alpha", "eps", "momentum", "wd"), got, ref):
+        torch.testing.assert_close(x, y, rtol=5e-4, atol=1e-5, msg=name)
+
+
 def test_host_streamed_step_equals_device_step(pkg):
     """offload.HostStreamedAdam (pinned host arrays, chunked H2D / kernels /
     D2H on three streams) gives the device-resident step's outputs bitwise
