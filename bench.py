@@ -360,6 +360,8 @@ def main():
     ap.add_argument("--checkpoint-every", type=int, default=None,
                     help="C3: keep only every c-th state and recompute segments (NEXT-2)")
     ap.add_argument("--no-graph", action="store_true", help="MAML without CUDA-graph capture")
+    ap.add_argument("--no-fuse-glue", action="store_true",
+                    help="C3: separate inner-loss glue kernels (NEXT-2 fusion off)")
     ap.add_argument("--maml-impl", default="batched", choices=["batched", "streams"],
                     help="MAML shard: one task-batched network, or per-task graph branches")
     ap.add_argument("--maml-net", default="gemm", choices=["gemm", "cudnn"],
@@ -490,7 +492,8 @@ def run_sweep(args, dev, rank, world):
     q = synth.quadratic_problem(0xC3, n)
     tree = L.Tree(offsets=off, device=dev)
     hp = (1e-2, 0.9, 0.999, 1e-8, 0.0)
-    sw = QuadraticSweep(tree, "adam", hp, 5, dev, checkpoint_every=args.checkpoint_every)
+    sw = QuadraticSweep(tree, "adam", hp, 5, dev, checkpoint_every=args.checkpoint_every,
+                        fuse_glue=not args.no_fuse_glue)
     a, th0, phi, y = (torch.from_numpy(q[k]).to(dev) for k in ("a", "theta0", "phi", "y"))
     del q
     l0 = L.opt_launch_count()
@@ -506,6 +509,7 @@ def run_sweep(args, dev, rank, world):
            "config": {"workload": "C3 5-step unrolled Adam + reverse sweep, 9x resnet18 tree",
                       "numel": n, "n_leaves": len(leaves), "K": 5,
                       "checkpoint_every": sw.c, "saved_state_bytes": sw.saved_bytes(),
+                      "fused_glue": sw.fuse,
                       "alg_bytes_per_step": per, "launches_per_step": sw.launches_per_sweep},
            "frac_of_measured_hbm": round(value / world / peak, 4),
            "gpu_launches": launches}

@@ -260,6 +260,29 @@ int opt_quadratic_grad(int64_t numel, const float* a, const float* theta,
 int opt_quadratic_rev(int64_t numel, const float* a, const float* g_bar,
                       float* theta_bar, float* phi_bar, int init_phi, void* stream);
 
+/* Fused inner-loss glue (SV §8(f) NEXT-2: "fusing the inner-loss glue into
+ * the step"): one unrolled step of the C3 sweep with the synthetic inner
+ * loss L_in = 1/2 sum a (theta - phi)^2 folded into the Adam kernels.
+ *   opt_adam_quad_fwd: g = a (theta - phi) -> g_out (NULL = not stored);
+ *     Adam step on g (state as opt_adam_fwd); theta_out = theta + u.
+ *     = opt_quadratic_grad + opt_adam_fwd(params=theta) in one pass.
+ *   opt_adam_quad_rev: the Adam VJP at (g, mu, nu) with d_updates =
+ *     theta_bar (cotangent of theta_out), then in place
+ *     theta_bar += a d_g,  phi_bar = (init_phi ? 0 : phi_bar) - a d_g;
+ *     d_mu/d_nu/d_hp as opt_adam_bwd; d_g itself is not stored.
+ *     = opt_adam_bwd + opt_quadratic_rev in one pass.
+ * theta_bar and phi_bar are read and written in place (exact aliasing). */
+int opt_adam_quad_fwd(const opt_tree* tree, int64_t step, const opt_adam_hp* hp,
+                      int state_dtype, int compute, const float* a, const float* phi,
+                      const float* theta, const void* mu, const void* nu, float* g_out,
+                      void* mu_out, void* nu_out, float* theta_out, void* stream);
+int opt_adam_quad_rev(const opt_tree* tree, int64_t step, const opt_adam_hp* hp,
+                      int state_dtype, int compute, const float* a, const float* g,
+                      const void* mu, const void* nu, float* theta_bar, const float* d_mu_out,
+                      const float* d_nu_out, float* d_mu, float* d_nu, float* phi_bar,
+                      int init_phi, double* d_hp, void* workspace, size_t workspace_bytes,
+                      void* stream);
+
 /* ------------------------------------ zero-order ES (SV §8(f) NEXT-3)
  * PAPER.md §2.2 "Zero-order Differentiation (ZD)": ES optimises the
  * Gaussian smoothing f~(theta) = E_z[f(theta + sigma z)], z ~ N(0, I), with

@@ -53,7 +53,7 @@ class DiffoptError(RuntimeError):
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_2211_06934_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_2211_06934_b200/build.py` "
             "(there is no CPU fallback)")
     L = ctypes.CDLL(LIB_PATH)
     P, i64, I, sz, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t, ctypes.c_double
@@ -340,6 +340,41 @@ def opt_sgd_bwd_ex(tree, hp, ext, state_dtype, compute, g, mom, params, d_update
                               _ptr(mom), _ptr(params), _ptr(d_updates), _ptr(d_mom_out),
                               _ptr(d_g), _ptr(d_mom), _ptr(d_params), _ptr(d_hp),
                               _ptr(d_hp_leaf), wp, wb, _stream(stream)))
+
+
+# ---------------------------------- fused inner-loss glue (NEXT-2, C3)
+lib.opt_adam_quad_fwd.argtypes = ([ctypes.POINTER(opt_tree), ctypes.c_int64,
+                                   ctypes.POINTER(opt_adam_hp), ctypes.c_int, ctypes.c_int]
+                                  + [ctypes.c_void_p] * 10)
+lib.opt_adam_quad_rev.argtypes = ([ctypes.POINTER(opt_tree), ctypes.c_int64,
+                                   ctypes.POINTER(opt_adam_hp), ctypes.c_int, ctypes.c_int]
+                                  + [ctypes.c_void_p] * 10 + [ctypes.c_int, ctypes.c_void_p,
+                                                              ctypes.c_void_p, ctypes.c_size_t,
+                                                              ctypes.c_void_p])
+lib.opt_adam_quad_fwd.restype = ctypes.c_int
+lib.opt_adam_quad_rev.restype = ctypes.c_int
+EXPORTS += ["opt_adam_quad_fwd", "opt_adam_quad_rev"]
+
+
+def opt_adam_quad_fwd(tree, step, hp, state_dtype, compute, a, phi, theta, mu, nu, g_out, mu_out,
+                      nu_out, theta_out, stream=None):
+    _check(lib.opt_adam_quad_fwd(ctypes.byref(tree.c), int(step),
+                                 ctypes.byref(_hp(opt_adam_hp, hp)), int(state_dtype),
+                                 int(compute), _ptr(a), _ptr(phi), _ptr(theta), _ptr(mu),
+                                 _ptr(nu), _ptr(g_out), _ptr(mu_out), _ptr(nu_out),
+                                 _ptr(theta_out), _stream(stream)))
+
+
+def opt_adam_quad_rev(tree, step, hp, state_dtype, compute, a, g, mu, nu, theta_bar, d_mu_out,
+                      d_nu_out, d_mu, d_nu, phi_bar, init_phi, d_hp=None, workspace=None,
+                      stream=None):
+    wp, wb = _ws(workspace)
+    _check(lib.opt_adam_quad_rev(ctypes.byref(tree.c), int(step),
+                                 ctypes.byref(_hp(opt_adam_hp, hp)), int(state_dtype),
+                                 int(compute), _ptr(a), _ptr(g), _ptr(mu), _ptr(nu),
+                                 _ptr(theta_bar), _ptr(d_mu_out), _ptr(d_nu_out), _ptr(d_mu),
+                                 _ptr(d_nu), _ptr(phi_bar), int(bool(init_phi)), _ptr(d_hp), wp,
+                                 wb, _stream(stream)))
 
 
 # ------------------------------ RMSProp centred / momentum (NEXT-1, N4)

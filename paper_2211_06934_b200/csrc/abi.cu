@@ -765,6 +765,55 @@ int opt_rmsprop_bwd_ex(const opt_tree* tree, const opt_rmsprop_hp* hp, const opt
   });
 }
 
+// ------------------------------ fused inner-loss glue (NEXT-2, C3 sweep)
+int opt_adam_quad_fwd(const opt_tree* tree, int64_t step, const opt_adam_hp* hp, int state_dtype,
+                      int compute, const float* a, const float* phi, const float* theta,
+                      const void* mu, const void* nu, float* g_out, void* mu_out, void* nu_out,
+                      float* theta_out, void* stream) {
+  g_err.clear();
+  int ct = 0;
+  TRY(check_tree(tree));
+  TRY(check_adam(step, hp));
+  TRY(check_state_dtype(state_dtype));
+  TRY(resolve_compute(compute, &ct));
+  TRY(check_align({a, phi, theta, mu, nu, g_out, mu_out, nu_out, theta_out}));
+  if (tree->numel == 0) return OPT_OK;
+  if (!a || !phi || !theta || !theta_out) return fail(OPT_EINVAL, "a, phi, theta, theta_out required");
+  StepArgs<5, 4> x{};
+  x.in[0] = a; x.in[1] = theta; x.in[2] = phi; x.in[3] = mu; x.in[4] = nu;
+  x.out[0] = g_out; x.out[1] = mu_out; x.out[2] = nu_out; x.out[3] = theta_out;
+  x.numel = tree->numel;
+  return dispatch<AdamQuadFwd, false>(state_dtype, ct, x, Reduce{}, tree,
+                                      static_cast<cudaStream_t>(stream),
+                                      [&](auto& op) { fill_adam_fwd(op.base, step, hp); });
+}
+
+int opt_adam_quad_rev(const opt_tree* tree, int64_t step, const opt_adam_hp* hp, int state_dtype,
+                      int compute, const float* a, const float* g, const void* mu, const void* nu,
+                      float* theta_bar, const float* d_mu_out, const float* d_nu_out, float* d_mu,
+                      float* d_nu, float* phi_bar, int init_phi, double* d_hp, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  int ct = 0;
+  TRY(check_tree(tree));
+  TRY(check_adam(step, hp));
+  TRY(check_state_dtype(state_dtype));
+  TRY(resolve_compute(compute, &ct));
+  TRY(check_align({a, g, mu, nu, theta_bar, d_mu_out, d_nu_out, d_mu, d_nu, phi_bar}));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (tree->numel == 0) return zero_outputs(tree, 4, d_hp, nullptr, s);
+  if (!a || !g || !theta_bar || !phi_bar) return fail(OPT_EINVAL, "a, g, theta_bar, phi_bar required");
+  Reduce r;
+  TRY(setup_reduce(tree, d_hp, nullptr, nullptr, workspace, workspace_bytes, &r));
+  StepArgs<8, 4> x{};
+  x.in[0] = a; x.in[1] = g; x.in[2] = mu; x.in[3] = nu; x.in[4] = theta_bar;
+  x.in[5] = d_mu_out; x.in[6] = d_nu_out; x.in[7] = init_phi ? nullptr : phi_bar;
+  x.out[0] = d_mu; x.out[1] = d_nu; x.out[2] = theta_bar; x.out[3] = phi_bar;
+  x.numel = tree->numel;
+  return dispatch<AdamQuadRev, true>(state_dtype, ct, x, r, tree, s,
+                                     [&](auto& op) { fill_adam_bwd(op.base, step, hp); });
+}
+
 // ------------------------------------- RMSProp centred / momentum (NEXT-1)
 int opt_rmsprop_cm_fwd(const opt_tree* tree, const opt_rmsprop_cm_hp* hp, const opt_ext* ext,
                        int state_dtype, int compute, const float* g, const void* nu,

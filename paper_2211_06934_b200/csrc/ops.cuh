@@ -382,6 +382,54 @@ struct SgdBwdEx : ExCommon<SgdBwd<CT_>> {
   }
 };
 
+// -------------------------- fused inner-loss glue (NEXT-2, C3 sweep step)
+// The synthetic inner loss L_in = 1/2 sum a (theta - phi)^2 (DESIGN.md input
+// recipe, C3) folded into the unrolled Adam step so one pass does what the
+// glue kernels + the plain step do in two:
+//   forward  (in: a theta phi m v ; out: g m' v' theta'):
+//     g = a (theta - phi) (saved for the reverse), Adam step on g, theta' = theta + u
+//   reverse  (in: a g m v theta_bar dm1 dv1 phi_bar ; out: dm dv theta_bar' phi_bar'):
+//     the Adam VJP with du = theta_bar (the cotangent of theta' through the
+//     fused apply), then theta_bar' = theta_bar + a dg (apply identity + H^T dg,
+//     H = diag a) and phi_bar' = phi_bar - a dg; dg itself is never stored.
+template <class CT_>
+struct AdamQuadFwd {
+  typedef CT_ CT;
+  static constexpr int NIN = 5, NOUT = 4, NH = 0;
+  __host__ __device__ static constexpr bool in_state(int i) { return i == 3 || i == 4; }
+  __host__ __device__ static constexpr bool out_state(int i) { return i == 1 || i == 2; }
+  AdamFwd<CT> base;
+  __device__ __forceinline__ void set_lr(CT l) { base.set_lr(l); }
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT*,
+                                             bool) const {
+    const CT th = x[1];
+    const CT g = CT(x[0]) * (th - CT(x[2]));
+    CT u;
+    base.apply(g, x[3], x[4], u, y[1], y[2]);
+    y[0] = g;
+    y[3] = th + u;
+  }
+};
+
+template <class CT_>
+struct AdamQuadRev {
+  typedef CT_ CT;
+  static constexpr int NIN = 8, NOUT = 4, NH = 4;
+  __host__ __device__ static constexpr bool in_state(int i) { return i == 2 || i == 3; }
+  __host__ __device__ static constexpr bool out_state(int) { return false; }
+  AdamBwd<CT> base;
+  __device__ __forceinline__ void set_lr(CT l) { base.set_lr(l); }
+  __device__ __forceinline__ void operator()(const float (&x)[NIN], CT (&y)[NOUT], CT* h,
+                                             bool want_hp) const {
+    const CT a = x[0], thb = x[4];
+    CT dg;
+    base.apply(x[1], x[2], x[3], thb, x[5], x[6], dg, y[0], y[1], h, want_hp);
+    const CT adg = a * dg;
+    y[2] = thb + adg;
+    y[3] = CT(x[7]) - adg;
+  }
+};
+
 // -------------------------- RMSProp centred / momentum (NEXT-1, reading N4)
 // torch.optim.RMSprop semantics on g~ = (maximize ? -g : g) + wd theta:
 //   v' = alpha v + (1-alpha) g~^2;  centred: a' = alpha a + (1-alpha) g~,

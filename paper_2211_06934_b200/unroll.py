@@ -39,7 +39,8 @@ class QuadraticSweep:
     the first K - c steps. c = K (default) is plain full storage."""
 
     def __init__(self, tree: L.Tree, kind: str, hp, K: int, device,
-                 compute=L.OPT_COMPUTE_DEFAULT, state_dtype=L.OPT_F32, checkpoint_every=None):
+                 compute=L.OPT_COMPUTE_DEFAULT, state_dtype=L.OPT_F32, checkpoint_every=None,
+                 fuse_glue=None):
         if kind not in NSLOT:
             raise ValueError(kind)
         if kind == "sgd" and float(hp[1]) == 0.0:
@@ -70,7 +71,14 @@ class QuadraticSweep:
         self.hyper = torch.empty(K, NH[kind], dtype=torch.float64, device=device)
         self.ws = tree.workspace(device)
         recompute = K - self._seg_len(self.nseg - 1)
-        self.launches_per_sweep = 4 * K + 1 + 2 * recompute
+        # NEXT-2 glue fusion (Adam): the quadratic-loss gradient is computed
+        # inside the step (opt_adam_quad_fwd) and its reverse inside the VJP
+        # (opt_adam_quad_rev): 2 launches per step instead of 4
+        self.fuse = (kind == "adam") if fuse_glue is None else bool(fuse_glue)
+        if self.fuse and kind != "adam":
+            raise ValueError("fused glue is implemented for adam")
+        per = 1 if self.fuse else 2
+        self.launches_per_sweep = 2 * per * K + 1 + per * recompute
 
     def _seg_len(self, j):
         return min(self.c, self.K - j * self.c)
@@ -105,6 +113,14 @@ class QuadraticSweep:
             L.opt_sgd_bwd(self.tree, self.hp, self.sd, self.compute, g, s_in[0], self.theta_bar,
                           sb_in[0], self.g_bar, sb_out[0], self.hyper[k], None, self.ws)
 
+    def _quad_rev(self, k, a, g, s_in):
+        last, first = k == self.K - 1, k == 0
+        sb_in = [None, None] if last else self.s_bar
+        sb_out = [None, None] if first else self.s_bar
+        L.opt_adam_quad_rev(self.tree, k + 1, self.hp, self.sd, self.compute, a, g, s_in[0],
+                            s_in[1], self.theta_bar, sb_in[0], sb_in[1], sb_out[0], sb_out[1],
+                            self.phi_bar, last, self.hyper[k], self.ws)
+
     def _segment_fwd(self, j, a, phi, theta_start, keep):
         """Steps of segment j from its checkpoint. keep=True stores g_k and the
         states in the segment buffers (for the reverse); otherwise only the
@@ -128,8 +144,12 @@ class QuadraticSweep:
                 th_out = self.th_ck[j + 1]
             else:
                 th_out = self.theta[r % 2]
-            L.opt_quadratic_grad(n, a, th_in, phi, g)
-            self._fwd(k, g, s_in, s_out, th_in, th_out)
+            if self.fuse:
+                L.opt_adam_quad_fwd(self.tree, k + 1, self.hp, self.sd, self.compute, a, phi,
+                                    th_in, s_in[0], s_in[1], g, s_out[0], s_out[1], th_out)
+            else:
+                L.opt_quadratic_grad(n, a, th_in, phi, g)
+                self._fwd(k, g, s_in, s_out, th_in, th_out)
             th_in, s_in = th_out, s_out
         return th_in
 
@@ -150,9 +170,12 @@ class QuadraticSweep:
             for r in range(self._seg_len(j) - 1, -1, -1):
                 k = j * self.c + r
                 s_in = self.s_ck[j] if r == 0 else self.s_seg[r]
-                self._bwd(k, self.g_seg[r], s_in)
-                L.opt_quadratic_rev(n, a, self.g_bar, self.theta_bar, self.phi_bar,
-                                    init_phi=(k == self.K - 1))
+                if self.fuse:
+                    self._quad_rev(k, a, self.g_seg[r], s_in)
+                else:
+                    self._bwd(k, self.g_seg[r], s_in)
+                    L.opt_quadratic_rev(n, a, self.g_bar, self.theta_bar, self.phi_bar,
+                                        init_phi=(k == self.K - 1))
         return thK, self.phi_bar, self.theta_bar, self.hyper
 
     def saved_bytes(self):
@@ -167,6 +190,16 @@ class QuadraticSweep:
         n, K, ns = self.tree.numel, self.K, NSLOT[self.kind]
         sb = 2 if self.sd == L.OPT_BF16 else 4
         total = 0
+        if self.fuse:
+            for k in range(K):   # a, theta_k, phi, s_k -> g_k, s_{k+1}, theta_{k+1}
+                total += 12 + (ns * sb if k > 0 else 0) + 4 + ns * sb + 4
+            total += 16          # ones, theta_K, y -> theta_bar_K
+            for k in range(K - 1, -1, -1):
+                total += 4 + 4 + (ns * sb if k > 0 else 0)   # a, g_k, s_k
+                total += 4 + (0 if k == K - 1 else 4 * ns)   # theta_bar, s_bar_{k+1}
+                total += 0 if k == K - 1 else 4              # phi_bar (read)
+                total += (0 if k == 0 else 4 * ns) + 4 + 4   # -> s_bar_k, theta_bar, phi_bar
+            return n * total
         for k in range(K):
             total += 16                                     # a, theta_k, phi -> g_k
             total += 4 + 4 + (ns * sb if k > 0 else 0)      # g_k, theta_k, s_k (NULL at k=0)

@@ -13,9 +13,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.fixture(scope="module")
 def L():
-    from paper_2211_06934_b200 import build
+    import __graft_entry__
 
-    build.build()
+    __graft_entry__.build()  # (re)builds a stale libdiffopt.so before the package loads it
     from paper_2211_06934_b200 import _lib
 
     return _lib

@@ -7,7 +7,12 @@ from concurrent.futures import ThreadPoolExecutor
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from paper_2211_06934_b200 import build as B  # noqa: E402
+import importlib.util  # noqa: E402
+
+_spec = importlib.util.spec_from_file_location(
+    "_diffopt_build", os.path.join(ROOT, "paper_2211_06934_b200", "build.py"))
+B = importlib.util.module_from_spec(_spec)
+_spec.loader.exec_module(B)
 
 OUT = os.path.join(ROOT, "tools", "tune_build")
 
