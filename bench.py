@@ -364,7 +364,7 @@ def main():
                     help="C3: separate inner-loss glue kernels (NEXT-2 fusion off)")
     ap.add_argument("--maml-impl", default="batched", choices=["batched", "streams"],
                     help="MAML shard: one task-batched network, or per-task graph branches")
-    ap.add_argument("--maml-net", default="gemm", choices=["gemm", "cudnn"],
+    ap.add_argument("--maml-net", default="fused", choices=["gemm", "cudnn", "fused"],
                     help="MAML task-batched network form (maml.conv4_forward_tasks)")
     ap.add_argument("--maml-streams", type=int, default=8,
                     help="MAML (--maml-impl streams): parallel task branches in the graph")

@@ -1,0 +1,102 @@
+/* include/mamlnet.h -- C ABI of the task-batched MAML network kernels (C4).
+ *
+ * What this is: the loss function a MAML meta-batch differentiates through
+ * (reading Z16: 4 x [conv3x3(64) -> batch norm ->
+ * ReLU -> 2x2 max-pool], fc -> 5 ways; MAML, "large
+ * task-level batch size" P:25, distributed meta-batch P:269). It is the
+ * WORKLOAD of the paper's optimizer hot path, not the method: the inner
+ * SGD-momentum step and its VJP run in libdiffopt.so (include/diffopt.h).
+ * The convolutions' contractions stay cuBLAS batched SGEMMs; this library
+ * supplies the memory-bound layers around them in one pass each, and the
+ * hand-derived second derivative of the norm/pool block that a second-order
+ * meta-gradient (create_graph, reading Z15) needs.
+ *
+ * Data layout: activations are task-major [T, C, B, H, W] fp32, contiguous.
+ * A "group" g = t*C + c is one (task, channel) pair: its B*H*W elements are
+ * contiguous at offset g*B*H*W, and batch-norm statistics are per group
+ * (each task normalises over its own images). Per-group parameters (gamma,
+ * beta) and per-group outputs are arrays of G = T*C floats indexed by g.
+ * Pooled tensors are [T, C, B, H/2, W/2] (floor), codes one byte per pooled
+ * element: 0..3 = window position (dy*2 + dx) of the maximum when the ReLU
+ * is active (maximum > 0), 255 when it is not (zero output, zero gradient).
+ *
+ * Conventions: DEVICE pointers, fp32 unless stated; the caller owns every
+ * buffer; no allocation, no synchronisation; all work enqueued on `stream`
+ * (cudaStream_t, NULL = legacy default). Returns 0 (NET_OK), NET_EINVAL on a
+ * bad size or NULL required pointer (nothing launched, message in
+ * net_last_error()), NET_ECUDA on a launch error. Nullable inputs are
+ * marked; NULL means zero. Group sums are fp64 in a fixed order (bitwise
+ * reproducible run to run).
+ */
+#ifndef MAMLNET_H
+#define MAMLNET_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MAMLNET_ABI_VERSION 1
+#define NET_OK 0
+#define NET_EINVAL 1
+#define NET_ECUDA 3
+
+/* 3x3, padding-1 im2col of h [G, B, H, W] (G = T*Cin) into
+ * cols [G, 9, B, H, W], i.e. [T, Cin*9, B*H*W] with row cin*9 + 3i + j:
+ * cols[g, 3i+j, b, y, x] = h[g, b, y+i-1, x+j-1] (0 outside the image). */
+int net_im2col3x3(int64_t G, int64_t B, int64_t H, int64_t W, const float* h, float* cols,
+                  void* stream);
+
+/* Adjoint of net_im2col3x3: dh[g, b, y, x] = sum over (i, j) with the
+ * source inside the image of cols[g, 3i+j, b, y-i+1, x-j+1]. Written, not
+ * accumulated. */
+int net_col2im3x3(int64_t G, int64_t B, int64_t H, int64_t W, const float* cols, float* dh,
+                  void* stream);
+
+/* Training-mode batch norm (biased batch variance, per group) + 2x2 max-pool
+ * (floor) + ReLU, forward:
+ *   mean_g = mean(x_g), rstd_g = 1/sqrt(var_g + eps),
+ *   z = gamma_g * (x - mean_g) * rstd_g + beta_g,
+ *   out[p] = max(0, max of z over window p), code[p] as above.
+ * x [G,B,H,W] -> out [G,B,H/2,W/2], code (uint8, same shape), mean, rstd [G]
+ * (saved for the backward). Requires H, W >= 2. */
+int net_bnpool_fwd(int64_t G, int64_t B, int64_t H, int64_t W, const float* x,
+                   const float* gamma, const float* beta, double eps, float* out, uint8_t* code,
+                   float* mean, float* rstd, void* stream);
+
+/* VJP of net_bnpool_fwd. dy = the pooled cotangent dp routed to each window's
+ * maximum (zero elsewhere and for inactive windows);
+ *   dbeta_g = sum dy, dgamma_g = sum dy*xh  (xh = (x - mean) * rstd),
+ *   dx = gamma*rstd*(dy - dbeta_g/n - xh*dgamma_g/n), n = B*H*W.
+ * (The pool/ReLU mask is piecewise constant: no term of its own.) */
+int net_bnpool_bwd(int64_t G, int64_t B, int64_t H, int64_t W, const float* dp,
+                   const uint8_t* code, const float* x, const float* gamma, const float* mean,
+                   const float* rstd, float* dx, float* dgamma, float* dbeta, void* stream);
+
+/* VJP of net_bnpool_bwd (the second derivative a second-order meta-gradient
+ * needs), given cotangents gdx [G,B,H,W], gdgamma [G], gdbeta [G] (each
+ * nullable = 0) of its outputs, with dgamma/dbeta the values net_bnpool_bwd
+ * returned. With A = dbeta/n, Bm = dgamma/n, r = rstd, G1 = sum gdx,
+ * Gx = sum gdx*xh, GD = sum gdx*dy - A*G1 (per group):
+ *   h      = -gamma*r*(dy*Gx/n + Bm*gdx) + gdgamma*dy
+ *   g_x    = r*(h - mean(h) - xh*mean(h*xh)) - (gamma*r^2/n)*(GD - Bm*Gx)*xh
+ *   g_dy   = gamma*r*(gdx - G1/n - xh*Gx/n) + gdgamma*xh + gdbeta
+ *   g_dp   = g_dy at each active window's maximum (0 for inactive windows)
+ *   g_gamma= r*(GD - Bm*Gx)
+ * (derivation in DESIGN.md §8; checked against PyTorch's float64 double
+ * backward of batch_norm/max_pool2d/relu in tests/test_mamlnet_gpu.py). */
+int net_bnpool_bwd2(int64_t G, int64_t B, int64_t H, int64_t W, const float* gdx,
+                    const float* gdgamma, const float* gdbeta, const float* dp,
+                    const uint8_t* code, const float* x, const float* gamma, const float* mean,
+                    const float* rstd, const float* dgamma, const float* dbeta, float* g_dp,
+                    float* g_x, float* g_gamma, void* stream);
+
+const char* net_last_error(void);
+int net_abi_version(void);
+int64_t net_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MAMLNET_H */

@@ -1,4 +1,6 @@
-"""Build libdiffopt.so (the C-ABI library) in-tree with nvcc for sm_100a."""
+"""Build the C-ABI libraries in-tree with nvcc for sm_100a: libdiffopt.so
+(the fused differentiable optimizer step, include/diffopt.h) and
+libmamlnet.so (the MAML workload's network layers, include/mamlnet.h)."""
 from __future__ import annotations
 
 import glob
@@ -11,6 +13,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libdiffopt.so")
+NET_SRC = os.path.join(HERE, "csrc_net", "mamlnet.cu")
+NET_LIB = os.path.join(HERE, "libmamlnet.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -42,6 +46,21 @@ def build(force: bool = False, out: str = LIB, defines=(), verbose: bool = False
     return out
 
 
+def build_net(force: bool = False, out: str = NET_LIB, verbose: bool = False) -> str:
+    """Compile csrc_net/mamlnet.cu into ``out``."""
+    srcs = [NET_SRC, os.path.join(INCLUDE, "mamlnet.h")]
+    if (not force and os.path.exists(out)
+            and all(os.path.getmtime(s) <= os.path.getmtime(out) for s in srcs)):
+        return out
+    cmd = [NVCC] + ARCH + FLAGS + ["-I" + INCLUDE]
+    if verbose:
+        cmd += ["-Xptxas", "-v"]
+    cmd += ["-o", out, NET_SRC]
+    subprocess.check_call(cmd)
+    return out
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    build_net(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB, NET_LIB)

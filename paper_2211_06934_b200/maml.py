@@ -89,7 +89,7 @@ class MamlConfig:
     nesterov: bool = False
     outer_lr: float = 1e-3
     seed: int = 0
-    net: str = "gemm"  # network form (conv4_forward_tasks)
+    net: str = "fused"  # network form (conv4_forward_tasks)
 
 
 class FusedSgdInner:
@@ -148,9 +148,9 @@ def meta_grad_tasks(phi, task_ids, outer_step, cfg: MamlConfig, inner):
 def _task_logits(theta, x, net):
     """One task's logits; net as in conv4_forward_tasks (T = 1)."""
     sizes = sizes_of(CONV4_SHAPES)
-    if net == "gemm":
+    if net in ("gemm", "fused"):
         params = [p.view(1, *s) for p, s in zip(torch.split(theta, sizes), CONV4_SHAPES)]
-        return conv4_forward_tasks(params, x.view(x.shape[0], 1, HW, HW), 1, "gemm")[0]
+        return conv4_forward_tasks(params, x.view(x.shape[0], 1, HW, HW), 1, net)[0]
     params = [p.view(s) for p, s in zip(torch.split(theta, sizes), CONV4_SHAPES)]
     return conv4_forward(params, x)
 
@@ -221,12 +221,117 @@ class _Col2Im(torch.autograd.Function):
         return _Im2Col.apply(dh), None
 
 
-def _conv3x3_tasks(h, w, b):
+def _conv3x3_tasks(h, w, b, im2col=None):
     """Task-batched 3x3 conv (padding 1) as one batched GEMM: h [T, Cin, B,
     H, W], w [T, Cout, Cin, 3, 3], b [T, Cout] -> [T, Cout, B, H, W]."""
     T, Cin, B, H, W = h.shape
-    out = torch.baddbmm(b.unsqueeze(-1), w.reshape(T, w.shape[1], Cin * 9), _Im2Col.apply(h))
+    cols = (im2col or _Im2Col.apply)(h)
+    out = torch.baddbmm(b.unsqueeze(-1), w.reshape(T, w.shape[1], Cin * 9), cols)
     return out.view(T, -1, B, H, W)
+
+
+# ------------------------------------- fused network layers (libmamlnet.so)
+BN_EPS = 1e-5  # F.batch_norm's default
+
+
+class _Im2ColK(torch.autograd.Function):
+    """_Im2Col with both directions in libmamlnet.so (net_im2col3x3 /
+    net_col2im3x3): one pass each instead of pad + 9 slices + stack and
+    9 read-modify-write passes."""
+
+    @staticmethod
+    def forward(ctx, h):
+        from . import _net as N
+
+        if h.dtype != torch.float32 or not h.is_cuda:
+            raise TypeError("_Im2ColK: libmamlnet.so takes fp32 CUDA tensors")
+        h = h.contiguous()
+        T, C, B, H, W = h.shape
+        ctx.shape = tuple(h.shape)
+        cols = h.new_empty(T, C * 9, B * H * W)
+        N.net_im2col3x3(T * C, B, H, W, h, cols)
+        return cols
+
+    @staticmethod
+    def backward(ctx, dcols):
+        return _Col2ImK.apply(dcols, ctx.shape)
+
+
+class _Col2ImK(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, cols, shape):
+        from . import _net as N
+
+        T, C, B, H, W = shape
+        cols = cols.contiguous()
+        dh = cols.new_empty(shape)
+        N.net_col2im3x3(T * C, B, H, W, cols, dh)
+        return dh
+
+    @staticmethod
+    def backward(ctx, dh):
+        return _Im2ColK.apply(dh), None
+
+
+class _BnPool(torch.autograd.Function):
+    """relu(max_pool2d(batch_norm(x), 2)) with per-(task, channel) batch
+    statistics, one kernel (net_bnpool_fwd). x [T, C, B, H, W], gamma/beta
+    [T, C]. Backward: _BnPoolBwd (itself differentiable once, for the
+    second-order meta-gradient)."""
+
+    @staticmethod
+    def forward(ctx, x, gamma, beta):
+        from . import _net as N
+
+        if x.dtype != torch.float32 or not x.is_cuda:
+            raise TypeError("_BnPool: libmamlnet.so takes fp32 CUDA tensors")
+        x = x.contiguous()
+        T, C, B, H, W = x.shape
+        out = x.new_empty(T, C, B, H // 2, W // 2)
+        code = torch.empty(out.shape, dtype=torch.uint8, device=x.device)
+        mean, rstd = x.new_empty(T * C), x.new_empty(T * C)
+        N.net_bnpool_fwd(T * C, B, H, W, x, gamma.contiguous(), beta.contiguous(), BN_EPS, out,
+                         code, mean, rstd)
+        ctx.save_for_backward(x, gamma, code, mean, rstd)
+        return out
+
+    @staticmethod
+    def backward(ctx, dp):
+        x, gamma, code, mean, rstd = ctx.saved_tensors
+        dx, dgamma, dbeta = _BnPoolBwd.apply(dp, x, gamma, code, mean, rstd)
+        return dx, dgamma.view_as(gamma), dbeta.view_as(gamma)
+
+
+class _BnPoolBwd(torch.autograd.Function):
+    """VJP of _BnPool (net_bnpool_bwd) as a function of (dp, x, gamma); its
+    own VJP is net_bnpool_bwd2 (include/mamlnet.h)."""
+
+    @staticmethod
+    def forward(ctx, dp, x, gamma, code, mean, rstd):
+        from . import _net as N
+
+        dp = dp.contiguous()
+        T, C, B, H, W = x.shape
+        dx = torch.empty_like(x)
+        dgamma, dbeta = x.new_empty(T * C), x.new_empty(T * C)
+        N.net_bnpool_bwd(T * C, B, H, W, dp, code, x, gamma.contiguous(), mean, rstd, dx, dgamma,
+                         dbeta)
+        ctx.save_for_backward(dp, x, gamma, code, mean, rstd, dgamma, dbeta)
+        return dx, dgamma, dbeta
+
+    @staticmethod
+    @torch.autograd.function.once_differentiable
+    def backward(ctx, gdx, gdgamma, gdbeta):
+        from . import _net as N
+
+        dp, x, gamma, code, mean, rstd, dgamma, dbeta = ctx.saved_tensors
+        T, C, B, H, W = x.shape
+        g_dp, g_x = torch.empty_like(dp), torch.empty_like(x)
+        g_gamma = x.new_empty(T * C)
+        c = lambda t: None if t is None else t.contiguous()
+        N.net_bnpool_bwd2(T * C, B, H, W, c(gdx), c(gdgamma), c(gdbeta), dp, code, x,
+                          gamma.contiguous(), mean, rstd, dgamma, dbeta, g_dp, g_x, g_gamma)
+        return g_dp, g_x, g_gamma.view_as(gamma), None, None, None
 
 
 def _bn_tasks(h, gamma, beta):
@@ -261,9 +366,17 @@ def conv4_forward_tasks(params, x, T, net="cudnn"):
                    max (_pool_relu_tasks). On B200, cuDNN's fp32 convolution
                    algorithms lose ~2% on this second-order meta-gradient
                    while the SGEMM form keeps fp32 accuracy (~3e-6 vs a
-                   float64 run, tools/maml_net_check.py), so it is the
-                   default."""
-    if net == "gemm":
+                   float64 run, tools/maml_net_check.py);
+      net="fused": the gemm form with im2col/col2im and the whole
+                   batch-norm + pool + ReLU block (forward, VJP and the VJP's
+                   VJP) in libmamlnet.so kernels (_Im2ColK, _BnPool)."""
+    if net == "fused":
+        h = x.permute(1, 0, 2, 3).unsqueeze(1).contiguous()  # [T, 1, B, 28, 28]
+        for blk in range(4):
+            w, b, gam, bet = params[4 * blk: 4 * blk + 4]
+            h = _BnPool.apply(_conv3x3_tasks(h, w, b, _Im2ColK.apply), gam, bet)
+        h = h.reshape(T, 64, -1).transpose(1, 2)  # [T, B, 64]
+    elif net == "gemm":
         h = x.permute(1, 0, 2, 3).unsqueeze(1)  # [T, 1, B, 28, 28]
         for blk in range(4):
             w, b, gam, bet = params[4 * blk: 4 * blk + 4]

@@ -13,7 +13,7 @@ import torch.multiprocessing as mp
 
 from paper_2211_06934_b200 import maml
 
-CFG = maml.MamlConfig(tasks=4, inner_steps=2, inner_lr=0.1, inner_momentum=0.9)
+CFG = maml.MamlConfig(tasks=4, inner_steps=2, inner_lr=0.1, inner_momentum=0.9, net="gemm")
 
 
 def torch_inner(g, b, theta):

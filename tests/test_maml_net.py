@@ -55,7 +55,7 @@ def test_task_batched_forms_equal_per_task_network():
 def test_task_batched_second_order_meta_gradient_matches_per_task():
     """Sum over tasks of the 2-inner-step meta-gradients: task-batched gemm
     form == per-task loop (float64, plain SGD-momentum)."""
-    cfg = maml.MamlConfig(tasks=T, inner_steps=2)
+    cfg = maml.MamlConfig(tasks=T, inner_steps=2, net="gemm")
     phi = maml.init_params(0, "cpu").double()
     data = [[a.double() if a.is_floating_point() else a for a in maml.task_data(3, t, "cpu")]
             for t in range(T)]
