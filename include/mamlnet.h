@@ -6,10 +6,12 @@
  * task-level batch size" P:25, distributed meta-batch P:269). It is the
  * WORKLOAD of the paper's optimizer hot path, not the method: the inner
  * SGD-momentum step and its VJP run in libdiffopt.so (include/diffopt.h).
- * The convolutions' contractions stay cuBLAS batched SGEMMs; this library
- * supplies the memory-bound layers around them in one pass each, and the
- * hand-derived second derivative of the norm/pool block that a second-order
- * meta-gradient (create_graph, reading Z15) needs.
+ * The convolutions' forward and input-gradient contractions stay cuBLAS
+ * batched SGEMMs; this library supplies the memory-bound layers around them
+ * in one pass each, the hand-derived second derivative of the norm/pool
+ * block that a second-order meta-gradient (create_graph, reading Z15) needs,
+ * and a split-K fp32 kernel for the weight-gradient contraction (long n,
+ * tiny output) that cuBLAS leaves under-parallel at a few tasks per GPU.
  *
  * Data layout: activations are task-major [T, C, B, H, W] fp32, contiguous.
  * A "group" g = t*C + c is one (task, channel) pair: its B*H*W elements are
@@ -31,6 +33,7 @@
 #ifndef MAMLNET_H
 #define MAMLNET_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -91,6 +94,18 @@ int net_bnpool_bwd2(int64_t G, int64_t B, int64_t H, int64_t W, const float* gdx
                     const uint8_t* code, const float* x, const float* gamma, const float* mean,
                     const float* rstd, const float* dgamma, const float* dbeta, float* g_dp,
                     float* g_x, float* g_gamma, void* stream);
+
+/* Batched "NT" product with a long contraction (the convolution
+ * weight-gradient shape): C[t] = A[t] . B[t]^T, A [T, M, N], B [T, P, N],
+ * C [T, M, P], all contiguous, fp32 arithmetic (fp32 FFMA accumulation over
+ * each of S contiguous n-ranges, then the S partials summed in order;
+ * S chosen from the sizes so that ~4 CTAs per SM exist). Workspace: a
+ * device buffer of net_gemm_nt_workspace_bytes(T, M, P, N) bytes (0 means
+ * none needed), caller-owned, contents irrelevant. N == 0 writes zeros.
+ * Requires T <= 65535. */
+size_t net_gemm_nt_workspace_bytes(int64_t T, int64_t M, int64_t P, int64_t N);
+int net_gemm_nt(int64_t T, int64_t M, int64_t P, int64_t N, const float* A, const float* B,
+                float* C, void* workspace, size_t workspace_bytes, void* stream);
 
 const char* net_last_error(void);
 int net_abi_version(void);

@@ -17,7 +17,8 @@ LIB_PATH = os.path.join(HERE, "libmamlnet.so")
 NET_OK = 0
 
 EXPORTS = ["net_im2col3x3", "net_col2im3x3", "net_bnpool_fwd", "net_bnpool_bwd",
-           "net_bnpool_bwd2", "net_last_error", "net_abi_version", "net_launch_count"]
+           "net_bnpool_bwd2", "net_gemm_nt_workspace_bytes", "net_gemm_nt", "net_last_error",
+           "net_abi_version", "net_launch_count"]
 
 
 def _load():
@@ -31,7 +32,10 @@ def _load():
     L.net_bnpool_fwd.argtypes = [i64] * 4 + [P, P, P, D] + [P] * 4 + [P]
     L.net_bnpool_bwd.argtypes = [i64] * 4 + [P] * 9 + [P]
     L.net_bnpool_bwd2.argtypes = [i64] * 4 + [P] * 14 + [P]
-    for n in ("net_im2col3x3", "net_col2im3x3", "net_bnpool_fwd", "net_bnpool_bwd",
+    L.net_gemm_nt_workspace_bytes.argtypes = [i64] * 4
+    L.net_gemm_nt_workspace_bytes.restype = ctypes.c_size_t
+    L.net_gemm_nt.argtypes = [i64] * 4 + [P, P, P, P, ctypes.c_size_t, P]
+    for n in ("net_gemm_nt", "net_im2col3x3", "net_col2im3x3", "net_bnpool_fwd", "net_bnpool_bwd",
               "net_bnpool_bwd2", "net_abi_version"):
         getattr(L, n).restype = ctypes.c_int
     L.net_last_error.restype = ctypes.c_char_p
@@ -71,6 +75,16 @@ def net_bnpool_bwd2(G, B, H, W, gdx, gdgamma, gdbeta, dp, code, x, gamma, mean, 
                                _ptr(code), _ptr(x), _ptr(gamma), _ptr(mean), _ptr(rstd),
                                _ptr(dgamma), _ptr(dbeta), _ptr(g_dp), _ptr(g_x), _ptr(g_gamma),
                                _stream(stream)))
+
+
+def net_gemm_nt_workspace_bytes(T, M, P, N):
+    return int(lib.net_gemm_nt_workspace_bytes(T, M, P, N))
+
+
+def net_gemm_nt(T, M, P, N, A, B, C, workspace=None, stream=None):
+    wb = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(lib.net_gemm_nt(T, M, P, N, _ptr(A), _ptr(B), _ptr(C), _ptr(workspace), wb,
+                           _stream(stream)))
 
 
 def net_abi_version():

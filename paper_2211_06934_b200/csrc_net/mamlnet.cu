@@ -10,6 +10,7 @@
 // 126 MB L2). Group sums are fp64 (exact squares of fp32 inputs; order fixed
 // by the block-reduction tree, so results are bitwise reproducible).
 #include <cuda_runtime.h>
+#include <stddef.h>
 
 #include <atomic>
 #include <cstdint>
@@ -288,6 +289,184 @@ __global__ void bnpool_bwd2_kernel(int B, int H, int W, const float* __restrict_
   }
 }
 
+
+// ------------------------------------------------ split-K NT GEMM (weight grads)
+// C[t] (M x P) = A[t] (M x N) . B[t]^T (P x N): both operands contiguous along
+// the contraction axis n, which is long (B*H*W, up to 58,800) while M x P is
+// small (64 x 576): the convolution weight-gradient shape. cuBLAS runs it
+// with one CTA per 32x32 output tile walking all of n (36 CTAs per task), so
+// at a few tasks per GPU most SMs idle. Here n is split into S ranges, each
+// CTA computes a 64x64 tile over its range in fp32 (SIMT FFMA: the path must
+// keep fp32 accuracy, reading Z16 / DESIGN §8), and a second kernel sums the
+// S partials in fixed order (bitwise reproducible).
+constexpr int GM = 64, GK = 32, GTHREADS = 128, GTM = 8, GPAD = 4;
+
+// CTA tile GM x GP (GP = 16*TP) over one n-range; 128 threads as 16 (p) x 8 (m),
+// each an 8 x TP register tile. Operands are staged k-major in shared memory:
+// every thread loads 4 consecutive rows at one n (coalesced along n across
+// the warp) and stores them as one 16-byte vector, so stores are
+// conflict-free and the inner loop reads 16-byte vectors.
+template <int TP>
+__global__ void __launch_bounds__(GTHREADS) gemm_nt_partial(int M, int P, int N, int ptiles,
+                                                            int cps, const float* __restrict__ A,
+                                                            const float* __restrict__ B,
+                                                            float* __restrict__ out,
+                                                            int64_t out_t_stride,
+                                                            int64_t out_s_stride) {
+  constexpr int GP = 16 * TP;
+  constexpr int AG = GM / 16, BG = GP / 16;  // 4-row groups per warp
+  __shared__ __align__(16) float As[2][GK][GM + GPAD];
+  __shared__ __align__(16) float Bs[2][GK][GP + GPAD];
+  const int t = blockIdx.z, s = blockIdx.y;
+  const int mt = blockIdx.x / ptiles, pt = blockIdx.x - mt * ptiles;
+  const int m0 = mt * GM, p0 = pt * GP;
+  const int nch = (N + GK - 1) / GK;
+  const int c0 = s * cps, c1 = min(nch, c0 + cps);
+  const float* At = A + (int64_t)t * M * N;
+  const float* Bt = B + (int64_t)t * P * N;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // p: tx*TP.., m: ty*8..
+  float4 ra[AG], rb[BG];
+  auto row = [&](const float* base, int r, int lim, int n, bool nok) {
+    return (nok && r < lim) ? __ldg(base + (int64_t)r * N + n) : 0.f;
+  };
+  auto load = [&](int c) {
+    const int n = c * GK + lane;
+    const bool nok = n < N;
+#pragma unroll
+    for (int j = 0; j < AG; ++j) {
+      const int r = m0 + warp * (GM / 4) + 4 * j;
+      ra[j] = make_float4(row(At, r, M, n, nok), row(At, r + 1, M, n, nok),
+                          row(At, r + 2, M, n, nok), row(At, r + 3, M, n, nok));
+    }
+#pragma unroll
+    for (int j = 0; j < BG; ++j) {
+      const int r = p0 + warp * (GP / 4) + 4 * j;
+      rb[j] = make_float4(row(Bt, r, P, n, nok), row(Bt, r + 1, P, n, nok),
+                          row(Bt, r + 2, P, n, nok), row(Bt, r + 3, P, n, nok));
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int j = 0; j < AG; ++j)
+      *reinterpret_cast<float4*>(&As[buf][lane][warp * (GM / 4) + 4 * j]) = ra[j];
+#pragma unroll
+    for (int j = 0; j < BG; ++j)
+      *reinterpret_cast<float4*>(&Bs[buf][lane][warp * (GP / 4) + 4 * j]) = rb[j];
+  };
+  float acc[GTM][TP];
+#pragma unroll
+  for (int i = 0; i < GTM; ++i)
+#pragma unroll
+    for (int j = 0; j < TP; ++j) acc[i][j] = 0.f;
+  if (c0 < c1) {
+    load(c0);
+    store(0);
+    __syncthreads();
+    for (int c = c0; c < c1; ++c) {
+      const int buf = (c - c0) & 1;
+      if (c + 1 < c1) load(c + 1);
+#pragma unroll 8
+      for (int k = 0; k < GK; ++k) {
+        const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][ty * GTM]);
+        const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][ty * GTM + 4]);
+        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        float bv[TP];
+        if constexpr (TP == 4) {
+          const float4 b = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
+          bv[0] = b.x, bv[1] = b.y, bv[2] = b.z, bv[3] = b.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < TP; ++j) bv[j] = Bs[buf][k][tx * TP + j];
+        }
+#pragma unroll
+        for (int i = 0; i < GTM; ++i)
+#pragma unroll
+          for (int j = 0; j < TP; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+      }
+      if (c + 1 < c1) store(buf ^ 1);
+      __syncthreads();
+    }
+  }
+  float* o = out + (int64_t)t * out_t_stride + (int64_t)s * out_s_stride;
+#pragma unroll
+  for (int i = 0; i < GTM; ++i) {
+    const int m = m0 + ty * GTM + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < TP; ++j) {
+      const int p = p0 + tx * TP + j;
+      if (p < P) o[(int64_t)m * P + p] = acc[i][j];
+    }
+  }
+}
+
+// C[t][e] = sum over s (in order) of part[t][s][e], e < M*P
+__global__ void gemm_nt_reduce(int64_t MP, int S, const float* __restrict__ part,
+                               float* __restrict__ C) {
+  const int64_t t = blockIdx.y;
+  const float* pt = part + t * S * MP;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < MP;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < S; ++s) acc += pt[(int64_t)s * MP + e];
+    C[t * MP + e] = acc;
+  }
+}
+
+struct SplitPlan {
+  int tp, ptiles, mtiles, S, cps;
+};
+
+int resident_slots(int tp) {  // CTAs of gemm_nt_partial<tp> resident on the device
+  static int cached[5] = {0, 0, 0, 0, 0};
+  if (!cached[tp]) {
+    int dev = 0, sms = 148, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (tp == 4)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm_nt_partial<4>, GTHREADS, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm_nt_partial<1>, GTHREADS, 0);
+    cached[tp] = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 148);
+  }
+  return cached[tp];
+}
+
+SplitPlan split_plan(int64_t T, int64_t M, int64_t P, int64_t N) {
+  SplitPlan q;
+  q.tp = P <= 16 ? 1 : 4;
+  const int GP = 16 * q.tp;
+  q.mtiles = (int)((M + GM - 1) / GM);
+  q.ptiles = (int)((P + GP - 1) / GP);
+  const int64_t nch = (N + GK - 1) / GK;
+  const int64_t tiles = T * q.mtiles * q.ptiles;
+  const int64_t slots = resident_slots(q.tp);
+  int64_t most = nch / 8;  // each split walks >= 8 chunks (256 of n)
+  if (most < 1) most = 1;
+  if (most > 4096) most = 4096;
+  // fewest splits whose CTA count fills the resident slots' waves to >= 90%
+  // (first wave full); with few tiles, as many as `most` allows
+  int64_t S = 1;
+  double best = -1.0;
+  for (int64_t c = 1; c <= most; ++c) {
+    const int64_t ctas = tiles * c;
+    const int64_t waves = (ctas + slots - 1) / slots;
+    const double fill = (double)ctas / (double)(waves * slots);
+    const double score = waves == 1 ? fill : fill + 0.001 * (double)waves;
+    if (score > best + 1e-9) {
+      best = score;
+      S = c;
+    }
+    if (waves == 1 && fill >= 0.9) break;
+    if (waves > 1 && fill >= 0.9) break;
+  }
+  q.cps = (int)((nch + S - 1) / S);
+  q.S = (int)((nch + q.cps - 1) / q.cps);
+  if (q.S < 1) q.S = 1;
+  return q;
+}
+
 bool geo_ok(int64_t G, int64_t B, int64_t H, int64_t W, bool pool) {
   if (G < 0 || B < 1 || H < 1 || W < 1) return false;
   if (pool && (H < 2 || W < 2)) return false;
@@ -368,6 +547,48 @@ int net_bnpool_bwd2(int64_t G, int64_t B, int64_t H, int64_t W, const float* gdx
   bnpool_bwd2_kernel<<<(unsigned)G, threads_for(B * H * W), 0, (cudaStream_t)stream>>>(
       (int)B, (int)H, (int)W, gdx, gdgamma, gdbeta, dp, code, x, gamma, mean, rstd, dgamma,
       dbeta, g_dp, g_x, g_gamma);
+  return launched();
+}
+
+size_t net_gemm_nt_workspace_bytes(int64_t T, int64_t M, int64_t P, int64_t N) {
+  if (T < 0 || M < 0 || P < 0 || N < 0) return 0;
+  if (T == 0 || M == 0 || P == 0 || N == 0) return 0;
+  SplitPlan q = split_plan(T, M, P, N);
+  return q.S > 1 ? (size_t)T * q.S * M * P * sizeof(float) : 0;
+}
+
+int net_gemm_nt(int64_t T, int64_t M, int64_t P, int64_t N, const float* A, const float* B,
+                float* C, void* workspace, size_t workspace_bytes, void* stream) {
+  if (T < 0 || M < 0 || P < 0 || N < 0 || T > 65535 || M > (1 << 20) || P > (1 << 20) ||
+      N > ((int64_t)1 << 31) - 64 || M * N > ((int64_t)1 << 40))
+    return fail("net_gemm_nt: bad sizes");
+  if (T == 0 || M == 0 || P == 0) return NET_OK;
+  if (!C) return fail("net_gemm_nt: NULL C");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (N == 0) {
+    if (cudaMemsetAsync(C, 0, (size_t)T * M * P * sizeof(float), st) != cudaSuccess)
+      return fail("net_gemm_nt: memset failed");
+    return NET_OK;
+  }
+  if (!A || !B) return fail("net_gemm_nt: NULL operand");
+  SplitPlan q = split_plan(T, M, P, N);
+  const size_t need = q.S > 1 ? (size_t)T * q.S * M * P * sizeof(float) : 0;
+  if (need && (!workspace || workspace_bytes < need))
+    return fail("net_gemm_nt: workspace too small (net_gemm_nt_workspace_bytes)");
+  dim3 grid((unsigned)(q.mtiles * q.ptiles), (unsigned)q.S, (unsigned)T);
+  float* out = q.S > 1 ? (float*)workspace : C;
+  const int64_t MP = M * P;
+  if (q.tp == 4)
+    gemm_nt_partial<4><<<grid, GTHREADS, 0, st>>>((int)M, (int)P, (int)N, q.ptiles, q.cps, A, B,
+                                                   out, q.S * MP, MP);
+  else
+    gemm_nt_partial<1><<<grid, GTHREADS, 0, st>>>((int)M, (int)P, (int)N, q.ptiles, q.cps, A, B,
+                                                   out, q.S * MP, MP);
+  int rc = launched();
+  if (rc != NET_OK || q.S == 1) return rc;
+  int64_t blocks = (MP + 255) / 256;
+  if (blocks > 1024) blocks = 1024;
+  gemm_nt_reduce<<<dim3((unsigned)blocks, (unsigned)T), 256, 0, st>>>(MP, q.S, out, C);
   return launched();
 }
 

@@ -273,6 +273,91 @@ class _Col2ImK(torch.autograd.Function):
         return _Im2ColK.apply(dh), None
 
 
+def _gemm_nt(a, b):
+    """C[t] = a[t] @ b[t]^T through net_gemm_nt (split-K fp32)."""
+    from . import _net as N
+
+    a, b = a.contiguous(), b.contiguous()
+    T, M, n = a.shape
+    P = b.shape[1]
+    c = a.new_empty(T, M, P)
+    wb = N.net_gemm_nt_workspace_bytes(T, M, P, n)
+    ws = a.new_empty((wb + 3) // 4) if wb else None
+    N.net_gemm_nt(T, M, P, n, a, b, c, ws)
+    return c
+
+
+def _wgrad_uses_split_k(T, M, P):
+    """net_gemm_nt when the output alone cannot fill the GPU (measured on
+    B200, profiles/r01f_gemm_nt_bench.jsonl: split-K wins up to ~16 tasks and
+    for the 9-column first layer at any T; cuBLAS's SIMT SGEMM wins once
+    T x 64 x 576 gives >= 148 output tiles of 64 x 64)."""
+    return P <= 16 or T * ((M + 63) // 64) * ((P + 63) // 64) < 148
+
+
+class _WGrad(torch.autograd.Function):
+    """a @ b^T for a [T, M, n], b [T, P, n] with long n (a convolution's
+    weight-gradient contraction): net_gemm_nt (split-K) or cuBLAS forward,
+    chosen by shape; its VJP is two ordinary batched GEMMs."""
+
+    @staticmethod
+    def forward(ctx, a, b):
+        ctx.save_for_backward(a, b)
+        T, M, _ = a.shape
+        if _wgrad_uses_split_k(T, M, b.shape[1]):
+            return _gemm_nt(a, b)
+        return torch.bmm(a, b.transpose(1, 2))
+
+    @staticmethod
+    def backward(ctx, gc):
+        a, b = ctx.saved_tensors
+        return torch.bmm(gc, b), torch.bmm(gc.transpose(1, 2), a)
+
+
+class _DCols(torch.autograd.Function):
+    """w^T @ dy (a convolution's input-gradient contraction, cuBLAS); its
+    weight-side VJP is the long-n contraction dy @ g^T (_WGrad)."""
+
+    @staticmethod
+    def forward(ctx, w, dy):
+        ctx.save_for_backward(w, dy)
+        return torch.bmm(w.transpose(1, 2), dy)
+
+    @staticmethod
+    def backward(ctx, g):
+        w, dy = ctx.saved_tensors
+        gw = _WGrad.apply(dy, g) if ctx.needs_input_grad[0] else None
+        gdy = torch.bmm(w, g) if ctx.needs_input_grad[1] else None
+        return gw, gdy
+
+
+class _TaskConvGemm(torch.autograd.Function):
+    """bias + w @ cols for the task-batched convolution (cuBLAS batched
+    SGEMM); backward: weight gradient through _WGrad (split-K), input
+    gradient through _DCols, both differentiable for second order."""
+
+    @staticmethod
+    def forward(ctx, w, cols, bias):
+        ctx.save_for_backward(w, cols)
+        return torch.baddbmm(bias.unsqueeze(-1), w, cols)
+
+    @staticmethod
+    def backward(ctx, dy):
+        w, cols = ctx.saved_tensors
+        gw = _WGrad.apply(dy, cols) if ctx.needs_input_grad[0] else None
+        gc = _DCols.apply(w, dy) if ctx.needs_input_grad[1] else None
+        gb = dy.sum(-1) if ctx.needs_input_grad[2] else None
+        return gw, gc, gb
+
+
+def _conv3x3_tasks_fused(h, w, b):
+    """_conv3x3_tasks with libmamlnet.so im2col/col2im and split-K weight
+    gradients."""
+    T, Cin, B, H, W = h.shape
+    out = _TaskConvGemm.apply(w.reshape(T, w.shape[1], Cin * 9), _Im2ColK.apply(h), b)
+    return out.view(T, -1, B, H, W)
+
+
 class _BnPool(torch.autograd.Function):
     """relu(max_pool2d(batch_norm(x), 2)) with per-(task, channel) batch
     statistics, one kernel (net_bnpool_fwd). x [T, C, B, H, W], gamma/beta
@@ -374,7 +459,7 @@ def conv4_forward_tasks(params, x, T, net="cudnn"):
         h = x.permute(1, 0, 2, 3).unsqueeze(1).contiguous()  # [T, 1, B, 28, 28]
         for blk in range(4):
             w, b, gam, bet = params[4 * blk: 4 * blk + 4]
-            h = _BnPool.apply(_conv3x3_tasks(h, w, b, _Im2ColK.apply), gam, bet)
+            h = _BnPool.apply(_conv3x3_tasks_fused(h, w, b), gam, bet)
         h = h.reshape(T, 64, -1).transpose(1, 2)  # [T, B, 64]
     elif net == "gemm":
         h = x.permute(1, 0, 2, 3).unsqueeze(1)  # [T, 1, B, 28, 28]

@@ -155,3 +155,52 @@ def test_fused_network_forward_equals_gemm_form(maml):
     a = maml.conv4_forward_tasks(params, x, T, "fused")
     b = maml.conv4_forward_tasks([p.double() for p in params], x.double(), T, "gemm")
     close(a, b, tol=1e-4)
+
+
+@pytest.mark.parametrize("shape", [(4, 64, 576, 14700), (32, 64, 576, 4900), (3, 64, 9, 58800),
+                                   (2, 5, 7, 33), (1, 64, 576, 1), (2, 70, 130, 1000),
+                                   (4, 64, 576, 225)])
+def test_gemm_nt_against_float64(maml, shape):
+    """net_gemm_nt (split-K fp32) vs the float64 product; ragged tiles,
+    N not a multiple of the k-chunk, several split counts; deterministic."""
+    T, M, P, n = shape
+    gen = torch.Generator(device=DEV).manual_seed(10)
+    a = torch.randn(T, M, n, device=DEV, generator=gen)
+    b = torch.randn(T, P, n, device=DEV, generator=gen)
+    c = maml._gemm_nt(a, b)
+    ref = torch.bmm(a.double(), b.double().transpose(1, 2))
+    # fp32 accumulation over n terms of unit variance: error ~ sqrt(n) * 2^-24 * sqrt(n)
+    tol = 4 * n * 2.0 ** -24 * 8
+    err = float((c.double() - ref).abs().max())
+    assert err <= tol * max(1.0, float(ref.abs().max()) / n ** 0.5), (err, tol)
+    assert torch.equal(c, maml._gemm_nt(a, b))  # fixed split order: bitwise reproducible
+
+
+def test_gemm_nt_empty_contraction(maml):
+    from paper_2211_06934_b200 import _net as N
+
+    c = torch.full((2, 3, 4), 7.0, device=DEV)
+    a = torch.empty(2, 3, 0, device=DEV)
+    N.net_gemm_nt(2, 3, 4, 0, a, a, c)
+    assert torch.equal(c, torch.zeros_like(c))
+
+
+def test_task_conv_second_order(maml):
+    """The fused convolution (im2col kernel, cuBLAS forward, split-K weight
+    gradient) differentiated twice vs the PyTorch-op form in float64."""
+    gen = torch.Generator().manual_seed(11)
+    h = torch.randn(3, 4, 5, 7, 7, generator=gen, dtype=torch.float64)
+    w = torch.randn(3, 6, 4, 3, 3, generator=gen, dtype=torch.float64)
+    b = torch.randn(3, 6, generator=gen, dtype=torch.float64)
+
+    def f(hh, ww, bb, fused):
+        conv = maml._conv3x3_tasks_fused if fused else maml._conv3x3_tasks
+        out = conv(hh, ww, bb)
+        gh, gw, gb = torch.autograd.grad((out ** 2).sum(), (hh, ww, bb), create_graph=True)
+        return torch.autograd.grad((gh ** 2).sum() + (gw ** 3).sum() + (gb * out.sum()).sum(),
+                                   (hh, ww, bb))
+
+    ref = f(*(t.clone().requires_grad_(True) for t in (h, w, b)), False)
+    got = f(*(t.float().to(DEV).requires_grad_(True) for t in (h, w, b)), True)
+    for a, r in zip(got, ref):
+        close(a, r, tol=1e-4)
