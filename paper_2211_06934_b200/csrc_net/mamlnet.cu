@@ -9,6 +9,7 @@
 // layer-1 query group is 235 KB; 148 SMs x a few CTAs stay well inside the
 // 126 MB L2). Group sums are fp64 (exact squares of fp32 inputs; order fixed
 // by the block-reduction tree, so results are bitwise reproducible).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 
@@ -135,34 +136,76 @@ __global__ void __launch_bounds__(256) col2im_kernel(int B, int H, int W, const 
 }
 
 // ----------------------------------------------------- batch norm + pool + relu
+// One group (task, channel) per thread-block CLUSTER of kc CTAs (kc = 1..8,
+// chosen from the group count so that small task batches still fill the
+// 148 SMs): CTA rank r owns the r-th slice of the group's elements and of its
+// pooled elements; group sums are combined across the cluster through
+// distributed shared memory, in rank order (identical in every CTA,
+// bitwise reproducible for a given kc).
+struct Slice {
+  int lo, hi;
+  __device__ Slice(int n, int r, int k) {
+    lo = (int)((int64_t)n * r / k);
+    hi = (int)((int64_t)n * (r + 1) / k);
+  }
+};
+
+// Sum K doubles over the cluster: block tree, then the kc block totals in
+// rank order through DSMEM. sm >= 32*K + K doubles; part >= K doubles.
+template <int K>
+__device__ __forceinline__ void cluster_sum(double (&v)[K], double* sm, double* part) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  block_sum<K>(v, sm);
+  const unsigned kc = cl.num_blocks();
+  if (kc == 1) return;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) part[k] = v[k];
+  }
+  cl.sync();
+  if (threadIdx.x < K) {
+    double t = 0.0;
+    for (unsigned r = 0; r < kc; ++r) t += cl.map_shared_rank(part, r)[threadIdx.x];
+    sm[32 * K + threadIdx.x] = t;
+  }
+  cl.sync();  // every CTA has read every part; none exits while still being read
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = sm[32 * K + k];
+}
+
 __global__ void bnpool_fwd_kernel(int B, int H, int W, const float* __restrict__ x,
                                   const float* __restrict__ gamma, const float* __restrict__ beta,
                                   double eps, float* __restrict__ out, uint8_t* __restrict__ code,
                                   float* __restrict__ mean_out, float* __restrict__ rstd_out) {
   __shared__ double sm[32 * 2 + 2];
+  __shared__ double part[2];
   const Geo q(B, H, W);
-  const int64_t g = blockIdx.x;
+  const int kc = (int)cooperative_groups::this_cluster().num_blocks();
+  const int rank = (int)cooperative_groups::this_cluster().block_rank();
+  const int64_t g = blockIdx.x / kc;
   const float* xg = x + g * q.n;
+  const Slice es(q.n, rank, kc), ps(q.np, rank, kc);
   double v[2] = {0.0, 0.0};
-  for (int i = threadIdx.x; i < q.n; i += blockDim.x) {
+  for (int i = es.lo + threadIdx.x; i < es.hi; i += blockDim.x) {
     double a = (double)xg[i];
     v[0] += a;
     v[1] += a * a;
   }
-  block_sum<2>(v, sm);
+  cluster_sum<2>(v, sm, part);
   const double mu = v[0] / q.n;
   double var = v[1] / q.n - mu * mu;
   var = var > 0.0 ? var : 0.0;
   const double rd = 1.0 / sqrt(var + eps);
   const float m = (float)mu, r = (float)rd, ga = gamma[g], be = beta[g];
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && rank == 0) {
     mean_out[g] = m;
     rstd_out[g] = r;
   }
   const float s = ga * r;  // z = s*(x - m) + be
   float* og = out + g * q.np;
   uint8_t* cg = code + g * q.np;
-  for (int p = threadIdx.x; p < q.np; p += blockDim.x) {
+  for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
     const int e0 = q.elem(p, 0);
     float best = s * (xg[e0] - m) + be;
     int kb = 0;
@@ -193,14 +236,18 @@ __global__ void bnpool_bwd_kernel(int B, int H, int W, const float* __restrict__
                                   const float* __restrict__ rstd, float* __restrict__ dx,
                                   float* __restrict__ dgamma, float* __restrict__ dbeta) {
   __shared__ double sm[32 * 2 + 2];
+  __shared__ double part[2];
   const Geo q(B, H, W);
-  const int64_t g = blockIdx.x;
+  const int kc = (int)cooperative_groups::this_cluster().num_blocks();
+  const int rank = (int)cooperative_groups::this_cluster().block_rank();
+  const int64_t g = blockIdx.x / kc;
+  const Slice es(q.n, rank, kc), ps(q.np, rank, kc);
   const float* xg = x + g * q.n;
   const float* dpg = dp + g * q.np;
   const uint8_t* cg = code + g * q.np;
   const float m = mean[g], r = rstd[g];
   double v[2] = {0.0, 0.0};
-  for (int p = threadIdx.x; p < q.np; p += blockDim.x) {
+  for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
     const uint8_t c = cg[p];
     if (c != kOff) {
       const float d = dpg[p];
@@ -209,14 +256,14 @@ __global__ void bnpool_bwd_kernel(int B, int H, int W, const float* __restrict__
       v[1] += (double)d * (double)xh;
     }
   }
-  block_sum<2>(v, sm);
-  if (threadIdx.x == 0) {
+  cluster_sum<2>(v, sm, part);
+  if (threadIdx.x == 0 && rank == 0) {
     dbeta[g] = (float)v[0];
     dgamma[g] = (float)v[1];
   }
   const float A = (float)(v[0] / q.n), Bm = (float)(v[1] / q.n), c0 = gamma[g] * r;
   float* dxg = dx + g * q.n;
-  for (int i = threadIdx.x; i < q.n; i += blockDim.x) {
+  for (int i = es.lo + threadIdx.x; i < es.hi; i += blockDim.x) {
     const float xh = (xg[i] - m) * r;
     const float dy = routed(q, i, dpg, cg);
     dxg[i] = c0 * (dy - A - xh * Bm);
@@ -232,8 +279,12 @@ __global__ void bnpool_bwd2_kernel(int B, int H, int W, const float* __restrict_
                                    float* __restrict__ g_dp, float* __restrict__ g_x,
                                    float* __restrict__ g_gamma) {
   __shared__ double sm[32 * 3 + 3];
+  __shared__ double part[3];
   const Geo q(B, H, W);
-  const int64_t g = blockIdx.x;
+  const int kc = (int)cooperative_groups::this_cluster().num_blocks();
+  const int rank = (int)cooperative_groups::this_cluster().block_rank();
+  const int64_t g = blockIdx.x / kc;
+  const Slice es(q.n, rank, kc), ps(q.np, rank, kc);
   const float* xg = x + g * q.n;
   const float* dpg = dp + g * q.np;
   const uint8_t* cg = code + g * q.np;
@@ -244,29 +295,29 @@ __global__ void bnpool_bwd2_kernel(int B, int H, int W, const float* __restrict_
   // sums: G1 = sum gdx, Gx = sum gdx*xh, Gd = sum gdx*dy
   double v[3] = {0.0, 0.0, 0.0};
   if (gg) {
-    for (int i = threadIdx.x; i < q.n; i += blockDim.x) {
+    for (int i = es.lo + threadIdx.x; i < es.hi; i += blockDim.x) {
       const float t = gg[i];
       v[0] += (double)t;
       v[1] += (double)t * (double)((xg[i] - m) * r);
     }
-    for (int p = threadIdx.x; p < q.np; p += blockDim.x) {
+    for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
       const uint8_t c = cg[p];
       if (c != kOff) v[2] += (double)dpg[p] * (double)gg[q.elem(p, c)];
     }
   }
-  block_sum<3>(v, sm);
+  cluster_sum<3>(v, sm, part);
   const double A = (double)dbeta[g] / nd, Bm = (double)dgamma[g] / nd;
   const double G1 = v[0], Gx = v[1], GD = v[2] - A * G1;
   const double gr = (double)ga * (double)r;
-  if (threadIdx.x == 0) g_gamma[g] = (float)((double)r * (GD - Bm * Gx));
-  // h = -gr*(dy*Gx/n + Bm*gdx) + gdg*dy = dy*ch + gdx*cg_
+  if (threadIdx.x == 0 && rank == 0) g_gamma[g] = (float)((double)r * (GD - Bm * Gx));
+  // h = -gr*(dy*Gx/n + Bm*gdx) + gdg*dy = dy*ch + gdx*cgd
   const double mean_h = -gr * (A * Gx + Bm * G1) / nd + gdg * A;
   const double mean_hx = -2.0 * gr * Bm * Gx / nd + gdg * Bm;
   const double kx = gr * (double)r * (GD - Bm * Gx) / nd;
   const float ch = (float)(-gr * Gx / nd + gdg), cgd = (float)(-gr * Bm);
   const float mh = (float)mean_h, mhx = (float)mean_hx, fkx = (float)kx;
   float* gxg = g_x + g * q.n;
-  for (int i = threadIdx.x; i < q.n; i += blockDim.x) {
+  for (int i = es.lo + threadIdx.x; i < es.hi; i += blockDim.x) {
     const float xh = (xg[i] - m) * r;
     const float dy = routed(q, i, dpg, cg);
     const float t = gg ? gg[i] : 0.f;
@@ -276,7 +327,7 @@ __global__ void bnpool_bwd2_kernel(int B, int H, int W, const float* __restrict_
   // g_dy = gr*(gdx - G1/n - xh*Gx/n) + gdg*xh + gdb at the routed positions
   const float fgr = (float)gr, g1n = (float)(G1 / nd), gxn = (float)(Gx / nd);
   float* gdpg = g_dp + g * q.np;
-  for (int p = threadIdx.x; p < q.np; p += blockDim.x) {
+  for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
     const uint8_t c = cg[p];
     float o = 0.f;
     if (c != kOff) {
@@ -288,7 +339,6 @@ __global__ void bnpool_bwd2_kernel(int B, int H, int W, const float* __restrict_
     gdpg[p] = o;
   }
 }
-
 
 // ------------------------------------------------ split-K NT GEMM (weight grads)
 // C[t] (M x P) = A[t] (M x N) . B[t]^T (P x N): both operands contiguous along
@@ -474,7 +524,41 @@ bool geo_ok(int64_t G, int64_t B, int64_t H, int64_t W, bool pool) {
   return G < ((int64_t)1 << 31) / 9;
 }
 
-int threads_for(int64_t n) { return n >= 16384 ? 512 : 256; }
+constexpr int kBnThreads = 256;
+
+// CTAs per group (cluster size): enough groups-x-slices to give every SM
+// ~4 CTAs, each slice >= 1024 elements; portable cluster sizes 1, 2, 4, 8.
+int cluster_for(int64_t G, int64_t n) {
+  const int64_t want = 148 * 4;
+  int kc = 1;
+  while (kc < 8 && G * kc < want && n / (2 * kc) >= 1024) kc *= 2;
+  return kc;
+}
+
+template <typename... KArgs, typename... Args>
+int launch_group_kernel(void (*kernel)(KArgs...), int64_t G, int64_t n, cudaStream_t st,
+                        Args... args) {
+  const int kc = cluster_for(G, n);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(G * kc));
+  cfg.blockDim = dim3(kBnThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)kc;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+  if (e != cudaSuccess) {
+    g_err = cudaGetErrorString(e);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return NET_ECUDA;
+  }
+  return launched();
+}
 
 dim3 stream_grid(int64_t rows, int64_t n) {
   // enough blocks to fill 148 SMs x 8 resident blocks; each loops inside its row
@@ -517,9 +601,8 @@ int net_bnpool_fwd(int64_t G, int64_t B, int64_t H, int64_t W, const float* x,
   if (G == 0) return NET_OK;
   if (!x || !gamma || !beta || !out || !code || !mean || !rstd)
     return fail("net_bnpool_fwd: NULL pointer");
-  bnpool_fwd_kernel<<<(unsigned)G, threads_for(B * H * W), 0, (cudaStream_t)stream>>>(
-      (int)B, (int)H, (int)W, x, gamma, beta, eps, out, code, mean, rstd);
-  return launched();
+  return launch_group_kernel(bnpool_fwd_kernel, G, B * H * W, (cudaStream_t)stream, (int)B,
+                             (int)H, (int)W, x, gamma, beta, eps, out, code, mean, rstd);
 }
 
 int net_bnpool_bwd(int64_t G, int64_t B, int64_t H, int64_t W, const float* dp,
@@ -529,9 +612,8 @@ int net_bnpool_bwd(int64_t G, int64_t B, int64_t H, int64_t W, const float* dp,
   if (G == 0) return NET_OK;
   if (!dp || !code || !x || !gamma || !mean || !rstd || !dx || !dgamma || !dbeta)
     return fail("net_bnpool_bwd: NULL pointer");
-  bnpool_bwd_kernel<<<(unsigned)G, threads_for(B * H * W), 0, (cudaStream_t)stream>>>(
-      (int)B, (int)H, (int)W, dp, code, x, gamma, mean, rstd, dx, dgamma, dbeta);
-  return launched();
+  return launch_group_kernel(bnpool_bwd_kernel, G, B * H * W, (cudaStream_t)stream, (int)B,
+                             (int)H, (int)W, dp, code, x, gamma, mean, rstd, dx, dgamma, dbeta);
 }
 
 int net_bnpool_bwd2(int64_t G, int64_t B, int64_t H, int64_t W, const float* gdx,
@@ -544,10 +626,9 @@ int net_bnpool_bwd2(int64_t G, int64_t B, int64_t H, int64_t W, const float* gdx
   if (!dp || !code || !x || !gamma || !mean || !rstd || !dgamma || !dbeta || !g_dp || !g_x ||
       !g_gamma)
     return fail("net_bnpool_bwd2: NULL pointer");
-  bnpool_bwd2_kernel<<<(unsigned)G, threads_for(B * H * W), 0, (cudaStream_t)stream>>>(
-      (int)B, (int)H, (int)W, gdx, gdgamma, gdbeta, dp, code, x, gamma, mean, rstd, dgamma,
-      dbeta, g_dp, g_x, g_gamma);
-  return launched();
+  return launch_group_kernel(bnpool_bwd2_kernel, G, B * H * W, (cudaStream_t)stream, (int)B,
+                             (int)H, (int)W, gdx, gdgamma, gdbeta, dp, code, x, gamma, mean, rstd,
+                             dgamma, dbeta, g_dp, g_x, g_gamma);
 }
 
 size_t net_gemm_nt_workspace_bytes(int64_t T, int64_t M, int64_t P, int64_t N) {

@@ -550,11 +550,19 @@ class GraphedShard:
         torch.cuda.current_stream(device).wait_stream(side)
         from . import _lib as L
 
+        def ours():  # launches of this repo's kernels (libdiffopt.so + libmamlnet.so)
+            n = L.opt_launch_count()
+            if cfg.net == "fused":
+                from . import _net as N
+
+                n += N.net_launch_count()
+            return n
+
         self.graph = torch.cuda.CUDAGraph()
-        n0 = L.opt_launch_count()
+        n0 = ours()
         with torch.cuda.graph(self.graph):
             self.mg, self.loss = self._body()
-        self.launches_per_replay = L.opt_launch_count() - n0  # captured library kernels
+        self.launches_per_replay = ours() - n0  # captured library kernels
 
     def _body(self):
         if self.batched:
