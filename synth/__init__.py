@@ -172,3 +172,37 @@ def to_bf16_bits(x):
     u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
     r = ((u >> 16) & 1) + np.uint32(0x7FFF)
     return ((u + r) >> 16).astype(np.uint16)
+
+
+def device_state_flat(seed, n, device, chunk=1 << 26):
+    """The C5 recipe (one flat leaf, per-4096-block scale 10^(-4U), 1/256
+    exact zeros in g, m, v, warm state m = 0.3 s N, v = (s(|N| + 0.1))^2,
+    cotangents N(0,1)) generated directly in device memory with torch's
+    seeded CUDA generator, chunk by chunk, for sizes too large to build on
+    the host (> 2^31 elements). Not counter based: tests read the sampled
+    inputs back from the device arrays. Returns float32 device tensors
+    g, m, v, du, dm1, dv1."""
+    import torch
+
+    gen = torch.Generator(device=device).manual_seed(int(seed))
+    out = {k: torch.empty(n, dtype=torch.float32, device=device)
+           for k in ("g", "m", "v", "du", "dm1", "dv1")}
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        k = e - s
+        blocks = (e - 1) // 4096 - s // 4096 + 1
+        bscale = 10.0 ** (-4.0 * torch.rand(blocks, generator=gen, device=device,
+                                            dtype=torch.float64))
+        b0 = s // 4096
+        scale = bscale[torch.arange(s, e, device=device) // 4096 - b0]
+        zero = torch.rand(k, generator=gen, device=device) < 1.0 / 256
+        nrm = lambda: torch.randn(k, generator=gen, device=device, dtype=torch.float64)
+        g = scale * nrm()
+        m = 0.3 * scale * nrm()
+        v = (scale * (nrm().abs() + 0.1)) ** 2
+        for name, x in (("g", g), ("m", m), ("v", v)):
+            x[zero] = 0.0
+            out[name][s:e] = x.float()
+        for name in ("du", "dm1", "dv1"):
+            out[name][s:e] = nrm().float()
+    return out

@@ -471,3 +471,66 @@ def test_c2_full_size_sampled_rmsprop_sgd(L, kind, bf16):
         assert_close("state'", oracle.bf16_to_f64(s1h), rs1, rtol=1e-2, atol=0)
     else:
         check("state'", s1h, rs1, mag["v1" if kind == "rmsprop" else "b1"], 1)
+
+
+# ------------------------------------------------- beyond 32-bit indexing
+def test_adam_beyond_int32_elements_sampled(L):
+    """Maximum-size edge case: one flat leaf of 2^31 + 3 elements (past every
+    32-bit index), C5 recipe generated in device memory
+    (synth.device_state_flat), Adam fwd + bwd in the bench launch
+    configuration. 2^16 sampled elements (incl. the last 64 and the ones
+    straddling 2^31) against the oracle on the inputs read back at those
+    indices; the global hyper-gradient sums against the sum of 129 separate
+    launches over 2^24-element pieces (the last straddling 2^31) (different grids, same arithmetic;
+    fp64 partials: agree to ~1e-12 of the sum's magnitude), and the last
+    piece's sums (which lie beyond 2^31) against the oracle."""
+    n = (1 << 31) + 3
+    if torch.cuda.mem_get_info()[0] < 100e9:
+        pytest.skip("needs ~80 GB of free device memory")
+    hp, t = (1e-3, 0.9, 0.999, 1e-8, 0.0), 10
+    x = synth.device_state_flat(0xB16, n, DEV)
+    tree = L.Tree(numel=n, device=DEV)
+    u, m1, v1 = (torch.empty(n, device=DEV) for _ in range(3))
+    L.opt_adam_fwd(tree, t, hp, 0, 1, x["g"], x["m"], x["v"], u, m1, v1)
+    rng = np.random.default_rng(1)
+    idx = np.unique(np.concatenate([rng.choice(n, 1 << 16, replace=False),
+                                    np.arange(n - 64, n), np.arange((1 << 31) - 32, (1 << 31) + 3)]))
+    di = torch.from_numpy(idx).to(DEV)
+    xs = {k: host(x[k][di]) for k in x}
+    ru, rm1, rv1 = oracle.adam_fwd(xs["g"], xs["m"], xs["v"], t, *hp, prec=1)
+    mag = oracle.adam_mag(xs["g"], xs["m"], xs["v"], xs["du"], xs["dm1"], xs["dv1"], t, *hp)
+    for name, got, ref in (("u", u, ru), ("m1", m1, rm1), ("v1", v1, rv1)):
+        check(name, host(got[di]), ref, mag[name], 1)
+    del u, m1, v1
+    dg, dm, dv = (torch.empty(n, device=DEV) for _ in range(3))
+    dhp = torch.empty(4, dtype=torch.float64, device=DEV)
+    L.opt_adam_bwd(tree, t, hp, 0, 1, x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], dg,
+                   dm, dv, dhp, None, tree.workspace(DEV))
+    r = oracle.adam_vjp(xs["g"], xs["m"], xs["v"], xs["du"], xs["dm1"], xs["dv1"], t, *hp, prec=1)
+    for name, got in (("dg", dg), ("dm", dm), ("dv", dv)):
+        check(name, host(got[di]), r[name], mag[name], 1)
+    # global sums: one launch over 2^31+3 vs the sum of 2^24-element pieces
+    piece = 1 << 24
+    starts = list(range(0, n, piece))
+    if n - starts[-1] < piece:
+        starts.pop()  # the last piece takes the remainder: it straddles 2^31
+    parts = []
+    for s, e in zip(starts, starts[1:] + [n]):
+        tr = L.Tree(numel=e - s, device=DEV)
+        hp_s = torch.empty(4, dtype=torch.float64, device=DEV)
+        sl = lambda a: a[s:e]
+        L.opt_adam_bwd(tr, t, hp, 0, 1, sl(x["g"]), sl(x["m"]), sl(x["v"]), sl(x["du"]),
+                       sl(x["dm1"]), sl(x["dv1"]), None, None, None, hp_s, None, tr.workspace(DEV))
+        parts.append(hp_s)
+    total = torch.stack(parts).sum(0)
+    got, want = host(dhp), host(total)
+    np.testing.assert_allclose(got, want, rtol=1e-9, atol=1e-12 * float(np.abs(want).max()))
+    last = {k: host(x[k][starts[-1]:]) for k in x}
+    oracle.set_num_threads(0)
+    full = oracle.adam_vjp(last["g"], last["m"], last["v"], last["du"], last["dm1"], last["dv1"],
+                           t, *hp)
+    oracle.set_num_threads(1)
+    fmag = oracle.adam_mag(last["g"], last["m"], last["v"], last["du"], last["dm1"], last["dv1"],
+                           t, *hp)
+    assert_sum_close("dhp(last piece)", host(parts[-1]), full["dhp"],
+                     np.maximum(full["dhp_abs"], fmag["dhp"]))
