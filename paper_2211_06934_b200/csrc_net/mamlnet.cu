@@ -72,9 +72,28 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* sm) {
   for (int k = 0; k < K; ++k) v[k] = sm[32 * K + k];
 }
 
+// Division by a per-launch constant d as a multiply-high: q = umulhi(i, m)
+// with m = ceil(2^32 / d) is exact whenever i * d < 2^32 (the rounding error
+// i*(m*d - 2^32)/(d*2^32) stays below 1/d); otherwise plain division.
+struct FastDiv {
+  uint32_t d, m;
+  bool fast;
+  __device__ FastDiv() : d(1), m(0), fast(false) {}
+  __device__ FastDiv(uint32_t d_, uint32_t limit) : d(d_ > 0 ? d_ : 1) {
+    fast = d > 1 && (uint64_t)limit * d < (1ull << 32);
+    m = d > 1 ? (uint32_t)(((1ull << 32) + d - 1) / d) : 0u;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t i) const {
+    return d == 1 ? i : (fast ? __umulhi(i, m) : i / d);
+  }
+};
+
 struct Geo {  // one group's geometry
   int B, H, W, HW, H2, W2, P2;  // P2 = H2*W2
   int n, np;                    // elements, pooled elements
+  int L, nl, lw;                // leftover elements (outside every window) per image, total,
+                                // of which the odd last column contributes lw per image
+  FastDiv dHW, dW, dP2, dW2, dL;
   __device__ Geo(int B_, int H_, int W_) : B(B_), H(H_), W(W_) {
     HW = H * W;
     H2 = H >> 1;
@@ -82,37 +101,49 @@ struct Geo {  // one group's geometry
     P2 = H2 * W2;
     n = B * HW;
     np = B * P2;
+    lw = (W & 1) ? 2 * H2 : 0;
+    L = lw + ((H & 1) ? W : 0);
+    nl = B * L;
+    dHW = FastDiv(HW, n);
+    dW = FastDiv(W, n);
+    dP2 = FastDiv(P2 > 0 ? P2 : 1, n);
+    dW2 = FastDiv(W2 > 0 ? W2 : 1, n);
+    dL = FastDiv(L > 0 ? L : 1, n);
   }
-  // flat element index of pooled p's window position k (0..3)
-  __device__ __forceinline__ int elem(int p, int k) const {
-    int b = p / P2, r = p - b * P2, y2 = r / W2, x2 = r - y2 * W2;
-    return b * HW + (2 * y2 + (k >> 1)) * W + 2 * x2 + (k & 1);
+  // flat element index of pooled p's window position 0; position k adds off(k)
+  __device__ __forceinline__ int elem0(int p) const {
+    const int b = (int)dP2.div(p), r = p - b * P2, y2 = (int)dW2.div(r), x2 = r - y2 * W2;
+    return b * HW + 2 * y2 * W + 2 * x2;
   }
-  // pooled index and window position of element i (-1 if outside every window)
-  __device__ __forceinline__ int pooled(int i, int& k) const {
-    int b = i / HW, r = i - b * HW, y = r / W, x = r - y * W;
-    int y2 = y >> 1, x2 = x >> 1;
-    if (y2 >= H2 || x2 >= W2) return -1;
-    k = ((y & 1) << 1) | (x & 1);
-    return b * P2 + y2 * W2 + x2;
+  __device__ __forceinline__ int off(int k) const { return (k >> 1) * W + (k & 1); }
+  __device__ __forceinline__ int elem(int p, int k) const { return elem0(p) + off(k); }
+  // j-th element outside every window (odd last column, then odd last row)
+  __device__ __forceinline__ int left(int j) const {
+    const int b = (int)dL.div(j), r = j - b * L;
+    return b * HW + (r < lw ? r * W + (W - 1) : (H - 1) * W + (r - lw));
   }
 };
 
 // ------------------------------------------------------------ im2col / col2im
+// One thread per source position (b, y, x) of a group: the 9 taps of the
+// output column are written from one index decode (coalesced per tap plane).
 __global__ void __launch_bounds__(256) im2col_kernel(int B, int H, int W, const float* __restrict__ h,
                                                      float* __restrict__ cols) {
-  const int64_t gk = blockIdx.x;  // (group, tap)
-  const int g = (int)(gk / 9), k = (int)(gk - (int64_t)g * 9);
-  const int di = k / 3 - 1, dj = k % 3 - 1;
+  const int64_t g = blockIdx.x;
   const int HW = H * W, n = B * HW;
-  const float* src = h + (int64_t)g * n;
-  float* dst = cols + gk * n;
+  const FastDiv dHW(HW, n), dW(W, n);
+  const float* src = h + g * n;
+  float* dst = cols + g * 9 * (int64_t)n;
   for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < n; i += gridDim.y * blockDim.x) {
-    int b = i / HW, r = i - b * HW, y = r / W, x = r - y * W;
-    int ys = y + di, xs = x + dj;
-    float v = 0.f;
-    if ((unsigned)ys < (unsigned)H && (unsigned)xs < (unsigned)W) v = __ldg(src + b * HW + ys * W + xs);
-    __stcs(dst + i, v);
+    const int b = (int)dHW.div(i), r = i - b * HW, y = (int)dW.div(r), x = r - y * W;
+    const float* row = src + b * HW;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const int ys = y + k / 3 - 1, xs = x + k % 3 - 1;
+      float v = 0.f;
+      if ((unsigned)ys < (unsigned)H && (unsigned)xs < (unsigned)W) v = __ldg(row + ys * W + xs);
+      __stcs(dst + (int64_t)k * n + i, v);
+    }
   }
 }
 
@@ -120,17 +151,22 @@ __global__ void __launch_bounds__(256) col2im_kernel(int B, int H, int W, const 
                                                      float* __restrict__ dh) {
   const int64_t g = blockIdx.x;
   const int HW = H * W, n = B * HW;
+  const FastDiv dHW(HW, n), dW(W, n);
   const float* src = cols + g * 9 * (int64_t)n;
   float* dst = dh + g * n;
   for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < n; i += gridDim.y * blockDim.x) {
-    int b = i / HW, r = i - b * HW, y = r / W, x = r - y * W;
-    float s = 0.f;
+    const int b = (int)dHW.div(i), r = i - b * HW, y = (int)dW.div(r), x = r - y * W;
+    float v[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
-      int ys = y - (k / 3 - 1), xs = x - (k % 3 - 1);
-      if ((unsigned)ys < (unsigned)H && (unsigned)xs < (unsigned)W)
-        s += __ldcs(src + (int64_t)k * n + b * HW + ys * W + xs);
+      const int ys = y - (k / 3 - 1), xs = x - (k % 3 - 1);
+      v[k] = ((unsigned)ys < (unsigned)H && (unsigned)xs < (unsigned)W)
+                 ? __ldcs(src + (int64_t)k * n + b * HW + ys * W + xs)
+                 : 0.f;
     }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) s += v[k];
     dst[i] = s;
   }
 }
@@ -221,15 +257,6 @@ __global__ void bnpool_fwd_kernel(int B, int H, int W, const float* __restrict__
   }
 }
 
-// dy of element i (the pooled cotangent routed to the window maximum)
-__device__ __forceinline__ float routed(const Geo& q, int i, const float* __restrict__ dpg,
-                                        const uint8_t* __restrict__ cg) {
-  int k;
-  const int p = q.pooled(i, k);
-  if (p < 0) return 0.f;
-  return cg[p] == k ? dpg[p] : 0.f;
-}
-
 __global__ void bnpool_bwd_kernel(int B, int H, int W, const float* __restrict__ dp,
                                   const uint8_t* __restrict__ code, const float* __restrict__ x,
                                   const float* __restrict__ gamma, const float* __restrict__ mean,
@@ -241,7 +268,7 @@ __global__ void bnpool_bwd_kernel(int B, int H, int W, const float* __restrict__
   const int kc = (int)cooperative_groups::this_cluster().num_blocks();
   const int rank = (int)cooperative_groups::this_cluster().block_rank();
   const int64_t g = blockIdx.x / kc;
-  const Slice es(q.n, rank, kc), ps(q.np, rank, kc);
+  const Slice ps(q.np, rank, kc);
   const float* xg = x + g * q.n;
   const float* dpg = dp + g * q.np;
   const uint8_t* cg = code + g * q.np;
@@ -263,10 +290,23 @@ __global__ void bnpool_bwd_kernel(int B, int H, int W, const float* __restrict__
   }
   const float A = (float)(v[0] / q.n), Bm = (float)(v[1] / q.n), c0 = gamma[g] * r;
   float* dxg = dx + g * q.n;
-  for (int i = es.lo + threadIdx.x; i < es.hi; i += blockDim.x) {
-    const float xh = (xg[i] - m) * r;
-    const float dy = routed(q, i, dpg, cg);
-    dxg[i] = c0 * (dy - A - xh * Bm);
+  // dx over the windows (dy = dp at the window's code position, else 0) ...
+  for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
+    const int e0 = q.elem0(p);
+    const uint8_t c = cg[p];
+    const float d = c != kOff ? dpg[p] : 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = e0 + q.off(k);
+      const float xh = (xg[e] - m) * r;
+      dxg[e] = c0 * ((c == k ? d : 0.f) - A - xh * Bm);
+    }
+  }
+  // ... and over the elements outside every window (dy = 0)
+  const Slice ls(q.nl, rank, kc);
+  for (int j = ls.lo + threadIdx.x; j < ls.hi; j += blockDim.x) {
+    const int e = q.left(j);
+    dxg[e] = c0 * (-A - (xg[e] - m) * r * Bm);
   }
 }
 
@@ -284,7 +324,7 @@ __global__ void bnpool_bwd2_kernel(int B, int H, int W, const float* __restrict_
   const int kc = (int)cooperative_groups::this_cluster().num_blocks();
   const int rank = (int)cooperative_groups::this_cluster().block_rank();
   const int64_t g = blockIdx.x / kc;
-  const Slice es(q.n, rank, kc), ps(q.np, rank, kc);
+  const Slice ps(q.np, rank, kc);
   const float* xg = x + g * q.n;
   const float* dpg = dp + g * q.np;
   const uint8_t* cg = code + g * q.np;
@@ -292,17 +332,27 @@ __global__ void bnpool_bwd2_kernel(int B, int H, int W, const float* __restrict_
   const float m = mean[g], r = rstd[g], ga = gamma[g];
   const float gdg = gdgamma ? gdgamma[g] : 0.f, gdb = gdbeta ? gdbeta[g] : 0.f;
   const double nd = (double)q.n;
-  // sums: G1 = sum gdx, Gx = sum gdx*xh, Gd = sum gdx*dy
+  // sums: G1 = sum gdx, Gx = sum gdx*xh, Gd = sum gdx*dy (windows, then leftovers)
+  const Slice ls(q.nl, rank, kc);
   double v[3] = {0.0, 0.0, 0.0};
   if (gg) {
-    for (int i = es.lo + threadIdx.x; i < es.hi; i += blockDim.x) {
-      const float t = gg[i];
-      v[0] += (double)t;
-      v[1] += (double)t * (double)((xg[i] - m) * r);
-    }
     for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
+      const int e0 = q.elem0(p);
       const uint8_t c = cg[p];
-      if (c != kOff) v[2] += (double)dpg[p] * (double)gg[q.elem(p, c)];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int e = e0 + q.off(k);
+        const float t = gg[e];
+        v[0] += (double)t;
+        v[1] += (double)t * (double)((xg[e] - m) * r);
+        if (c == k) v[2] += (double)dpg[p] * (double)t;
+      }
+    }
+    for (int j = ls.lo + threadIdx.x; j < ls.hi; j += blockDim.x) {
+      const int e = q.left(j);
+      const float t = gg[e];
+      v[0] += (double)t;
+      v[1] += (double)t * (double)((xg[e] - m) * r);
     }
   }
   cluster_sum<3>(v, sm, part);
@@ -316,27 +366,32 @@ __global__ void bnpool_bwd2_kernel(int B, int H, int W, const float* __restrict_
   const double kx = gr * (double)r * (GD - Bm * Gx) / nd;
   const float ch = (float)(-gr * Gx / nd + gdg), cgd = (float)(-gr * Bm);
   const float mh = (float)mean_h, mhx = (float)mean_hx, fkx = (float)kx;
-  float* gxg = g_x + g * q.n;
-  for (int i = es.lo + threadIdx.x; i < es.hi; i += blockDim.x) {
-    const float xh = (xg[i] - m) * r;
-    const float dy = routed(q, i, dpg, cg);
-    const float t = gg ? gg[i] : 0.f;
-    const float h = dy * ch + t * cgd;
-    gxg[i] = r * (h - mh - xh * mhx) - fkx * xh;
-  }
-  // g_dy = gr*(gdx - G1/n - xh*Gx/n) + gdg*xh + gdb at the routed positions
+  // g_x over the windows (with g_dy at the routed position -> g_dp), then leftovers;
+  // g_dy = gr*(gdx - G1/n - xh*Gx/n) + gdg*xh + gdb
   const float fgr = (float)gr, g1n = (float)(G1 / nd), gxn = (float)(Gx / nd);
+  float* gxg = g_x + g * q.n;
   float* gdpg = g_dp + g * q.np;
   for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
+    const int e0 = q.elem0(p);
     const uint8_t c = cg[p];
+    const float d = c != kOff ? dpg[p] : 0.f;
     float o = 0.f;
-    if (c != kOff) {
-      const int e = q.elem(p, c);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = e0 + q.off(k);
       const float xh = (xg[e] - m) * r;
       const float t = gg ? gg[e] : 0.f;
-      o = fgr * (t - g1n - xh * gxn) + gdg * xh + gdb;
+      const float dy = c == k ? d : 0.f;
+      gxg[e] = r * ((dy * ch + t * cgd) - mh - xh * mhx) - fkx * xh;
+      if (c == k) o = fgr * (t - g1n - xh * gxn) + gdg * xh + gdb;
     }
     gdpg[p] = o;
+  }
+  for (int j = ls.lo + threadIdx.x; j < ls.hi; j += blockDim.x) {
+    const int e = q.left(j);
+    const float xh = (xg[e] - m) * r;
+    const float t = gg ? gg[e] : 0.f;
+    gxg[e] = r * (t * cgd - mh - xh * mhx) - fkx * xh;
   }
 }
 
@@ -527,9 +582,9 @@ bool geo_ok(int64_t G, int64_t B, int64_t H, int64_t W, bool pool) {
 constexpr int kBnThreads = 256;
 
 // CTAs per group (cluster size): enough groups-x-slices to give every SM
-// ~4 CTAs, each slice >= 1024 elements; portable cluster sizes 1, 2, 4, 8.
+// ~8 CTAs, each slice >= 1024 elements; portable cluster sizes 1, 2, 4, 8.
 int cluster_for(int64_t G, int64_t n) {
-  const int64_t want = 148 * 4;
+  const int64_t want = 148 * 8;
   int kc = 1;
   while (kc < 8 && G * kc < want && n / (2 * kc) >= 1024) kc *= 2;
   return kc;
@@ -578,7 +633,7 @@ int net_im2col3x3(int64_t G, int64_t B, int64_t H, int64_t W, const float* h, fl
   if (!geo_ok(G, B, H, W, false)) return fail("net_im2col3x3: bad geometry");
   if (G == 0) return NET_OK;
   if (!h || !cols) return fail("net_im2col3x3: NULL pointer");
-  im2col_kernel<<<stream_grid(G * 9, B * H * W), 256, 0, (cudaStream_t)stream>>>(
+  im2col_kernel<<<stream_grid(G, B * H * W), 256, 0, (cudaStream_t)stream>>>(
       (int)B, (int)H, (int)W, h, cols);
   return launched();
 }
