@@ -116,7 +116,6 @@ struct Geo {  // one group's geometry
     return b * HW + 2 * y2 * W + 2 * x2;
   }
   __device__ __forceinline__ int off(int k) const { return (k >> 1) * W + (k & 1); }
-  __device__ __forceinline__ int elem(int p, int k) const { return elem0(p) + off(k); }
   // j-th element outside every window (odd last column, then odd last row)
   __device__ __forceinline__ int left(int j) const {
     const int b = (int)dL.div(j), r = j - b * L;
@@ -242,7 +241,7 @@ __global__ void bnpool_fwd_kernel(int B, int H, int W, const float* __restrict__
   float* og = out + g * q.np;
   uint8_t* cg = code + g * q.np;
   for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
-    const int e0 = q.elem(p, 0);
+    const int e0 = q.elem0(p);
     float best = s * (xg[e0] - m) + be;
     int kb = 0;
     float z1 = s * (xg[e0 + 1] - m) + be;
@@ -278,7 +277,7 @@ __global__ void bnpool_bwd_kernel(int B, int H, int W, const float* __restrict__
     const uint8_t c = cg[p];
     if (c != kOff) {
       const float d = dpg[p];
-      const float xh = (xg[q.elem(p, c)] - m) * r;
+      const float xh = (xg[q.elem0(p) + q.off(c)] - m) * r;
       v[0] += (double)d;
       v[1] += (double)d * (double)xh;
     }
