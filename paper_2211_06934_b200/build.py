@@ -48,7 +48,8 @@ def build(force: bool = False, out: str = LIB, defines=(), verbose: bool = False
 
 def build_net(force: bool = False, out: str = NET_LIB, verbose: bool = False) -> str:
     """Compile csrc_net/mamlnet.cu into ``out``."""
-    srcs = [NET_SRC, os.path.join(INCLUDE, "mamlnet.h")]
+    srcs = ([NET_SRC, os.path.join(INCLUDE, "mamlnet.h")]
+            + glob.glob(os.path.join(os.path.dirname(NET_SRC), "*.cuh")))
     if (not force and os.path.exists(out)
             and all(os.path.getmtime(s) <= os.path.getmtime(out) for s in srcs)):
         return out
