@@ -763,13 +763,25 @@ int net_tc_gemm(int64_t T, int64_t M, int64_t N, int64_t K, const float* A, int6
     a.D = D, a.ldD = ldD, a.bD = bD, a.sS = 0;
   }
   dim3 grid((unsigned)(mt * nt), (unsigned)S, (unsigned)T);
-  static bool attr[4] = {false, false, false, false};
-  const int which = (a_mn ? 2 : 0) + (b_mn ? 1 : 0);
-  void (*kern)(const tcg::Args) =
-      which == 3 ? tcg::tc3_gemm_kernel<true, true>
-      : which == 2 ? tcg::tc3_gemm_kernel<true, false>
-      : which == 1 ? tcg::tc3_gemm_kernel<false, true>
-                   : tcg::tc3_gemm_kernel<false, false>;
+  // 16-byte async copies when the contiguous axis is 16-byte aligned everywhere
+  auto al16 = [](const float* p, int64_t other, int64_t batch) {
+    return ((uintptr_t)p & 15) == 0 && other % 4 == 0 && batch % 4 == 0;
+  };
+  const bool va = a_mn ? al16(A, sAk, bA) : (sAk == 1 && al16(A, sAm, bA));
+  const bool vb = b_mn ? al16(B, sBk, bB) : (sBk == 1 && al16(B, sBn, bB));
+  using KFn = void (*)(const tcg::Args);
+  static const KFn table[16] = {
+      tcg::tc3_gemm_kernel<false, false, false, false>, tcg::tc3_gemm_kernel<false, false, false, true>,
+      tcg::tc3_gemm_kernel<false, false, true, false>,  tcg::tc3_gemm_kernel<false, false, true, true>,
+      tcg::tc3_gemm_kernel<false, true, false, false>,  tcg::tc3_gemm_kernel<false, true, false, true>,
+      tcg::tc3_gemm_kernel<false, true, true, false>,   tcg::tc3_gemm_kernel<false, true, true, true>,
+      tcg::tc3_gemm_kernel<true, false, false, false>,  tcg::tc3_gemm_kernel<true, false, false, true>,
+      tcg::tc3_gemm_kernel<true, false, true, false>,   tcg::tc3_gemm_kernel<true, false, true, true>,
+      tcg::tc3_gemm_kernel<true, true, false, false>,   tcg::tc3_gemm_kernel<true, true, false, true>,
+      tcg::tc3_gemm_kernel<true, true, true, false>,    tcg::tc3_gemm_kernel<true, true, true, true>};
+  static bool attr[16] = {};
+  const int which = (a_mn ? 8 : 0) + (b_mn ? 4 : 0) + (va ? 2 : 0) + (vb ? 1 : 0);
+  const KFn kern = table[which];
   if (!attr[which]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              tcg::SMEM_BYTES) != cudaSuccess)

@@ -35,11 +35,10 @@
 
 namespace tcg {
 
-constexpr int BM = 128, BN = 64, BK = 32, THREADS = 128;
+constexpr int BM = 128, BN = 64, BK = 32, THREADS = 256, RSTAGES = 4;
 constexpr int A_BYTES = BM * BK * 4;  // 16 KB per split half
 constexpr int B_BYTES = BN * BK * 4;  // 8 KB
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-constexpr int SMEM_BYTES = 2 * STAGE_BYTES + 1024 + 64;  // + 1024-B alignment slack + barriers
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -100,12 +99,129 @@ struct Args {
   int mtiles;
 };
 
-template <bool A_MN, bool B_MN>
+// Raw fp32 tiles as copied (cp.async, zero-filled outside the matrix):
+// m/n-contiguous operands as [k][R + 4], k-contiguous ones as [R][36]; the
+// pads keep 16-byte alignment and make the split's 16-byte reads cover all
+// banks per quarter-warp.
+constexpr int RAW_A = (BK * (BM + 4) > BM * 36) ? BK * (BM + 4) : BM * 36;  // floats
+constexpr int RAW_B = (BK * (BN + 4) > BN * 36) ? BK * (BN + 4) : BN * 36;
+constexpr int RAW_STAGE = (RAW_A + RAW_B) * 4;
+constexpr int FOLD = 4;  // k-blocks (4 x 32 k) accumulated in TMEM before an fp32 fold
+// split stages + raw ring + 1024-B alignment slack + barriers / TMEM slot
+constexpr int SMEM_BYTES = 2 * STAGE_BYTES + RSTAGES * RAW_STAGE + 1024 + 64;
+
+__device__ __forceinline__ void cp_async(uint32_t dst, const float* src, int bytes, int cp) {
+  if (cp == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(bytes));
+}
+
+// Per-thread copy plan for one operand tile of R rows x BK k: the thread's
+// elements (or 4-wide chunks when V) are fixed across k-blocks, so offsets
+// and row validity are computed once; per block only k changes.
+template <bool MN, bool V, int R>
+struct CopyPlan {
+  static constexpr int RS = MN ? R + 4 : 36;                       // raw row stride
+  static constexpr int UNITS = V ? R * BK / 4 : R * BK;            // chunks or elements
+  static constexpr int PER = UNITS / THREADS > 0 ? UNITS / THREADS : 1;
+  int64_t off[PER];   // global offset at k = 0 (floats)
+  int kk[PER];        // k within the block
+  int rows_left[PER]; // rows (MN) valid from this chunk's first row, <= 0 if none
+  uint32_t dst[PER];  // smem byte offset within the raw tile
+  bool live[PER];
+  __device__ void init(int tid, int row0, int M, int64_t s_r, int64_t s_k) {
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int u = tid + THREADS * j;
+      live[j] = u < UNITS;
+      int r, k;
+      if (MN) {  // rows contiguous
+        const int per_k = V ? R / 4 : R;
+        r = (u % per_k) * (V ? 4 : 1), k = u / per_k;
+        dst[j] = (uint32_t)(k * RS + r) * 4;
+      } else {   // k contiguous
+        const int per_r = V ? BK / 4 : BK;
+        k = (u % per_r) * (V ? 4 : 1), r = u / per_r;
+        dst[j] = (uint32_t)(r * RS + k) * 4;
+      }
+      kk[j] = k;
+      rows_left[j] = M - (row0 + r);
+      off[j] = (int64_t)(row0 + r) * s_r + (int64_t)k * s_k;
+    }
+  }
+  __device__ __forceinline__ void issue(uint32_t base, const float* X, int k0, int kend,
+                                        int64_t s_k) const {
+    const int64_t kofs = (int64_t)k0 * s_k;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      if (!live[j]) continue;
+      const int k = k0 + kk[j];
+      int bytes;
+      if (V) {
+        if (MN) bytes = k < kend ? 4 * max(0, min(4, rows_left[j])) : 0;
+        else bytes = rows_left[j] > 0 ? 4 * max(0, min(4, kend - k)) : 0;
+      } else {
+        bytes = (k < kend && rows_left[j] > 0) ? 4 : 0;
+      }
+      cp_async(base + dst[j], bytes ? X + off[j] + kofs : X, bytes, V ? 16 : 4);
+    }
+  }
+};
+
+__device__ __forceinline__ void split4(float4 x, uint4& h, uint4& l) {
+  h.x = to_tf32(x.x), l.x = to_tf32(x.x - __uint_as_float(h.x));
+  h.y = to_tf32(x.y), l.y = to_tf32(x.y - __uint_as_float(h.y));
+  h.z = to_tf32(x.z), l.z = to_tf32(x.z - __uint_as_float(h.z));
+  h.w = to_tf32(x.w), l.w = to_tf32(x.w - __uint_as_float(h.w));
+}
+
+// raw tile -> K-major SW128 hi / lo tiles (R rows x 32 k), threads [0, nthr)
+template <bool MN, int R>
+__device__ __forceinline__ void split_tile(const float* raw, uint8_t* hi, uint8_t* lo, int tid) {
+  if (MN) {  // raw [k][R+4]: thread = (row quad q, k quad kq); 4x4 transpose in registers
+    constexpr int RS = R + 4, NQ = R / 4;
+    if (tid >= NQ * 8) return;
+    const int kq = tid % 8, q = tid / 8;
+    float4 x[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = *(const float4*)(raw + (4 * kq + i) * RS + 4 * q);
+    const float4 c0 = make_float4(x[0].x, x[1].x, x[2].x, x[3].x);
+    const float4 c1 = make_float4(x[0].y, x[1].y, x[2].y, x[3].y);
+    const float4 c2 = make_float4(x[0].z, x[1].z, x[2].z, x[3].z);
+    const float4 c3 = make_float4(x[0].w, x[1].w, x[2].w, x[3].w);
+    const float4 cs[4] = {c0, c1, c2, c3};
+#pragma unroll
+    for (int jr = 0; jr < 4; ++jr) {
+      uint4 h, l;
+      split4(cs[jr], h, l);
+      const uint32_t o = off_k(4 * q + jr, 4 * kq);
+      *(uint4*)(hi + o) = h;
+      *(uint4*)(lo + o) = l;
+    }
+  } else {   // raw [R][36]: thread = row, 16-byte reads along k
+    constexpr int PER = R * BK / 4 / THREADS;  // float4 chunks per thread
+    const int r = tid % R, kq0 = (tid / R) * PER;
+#pragma unroll
+    for (int c = 0; c < PER; ++c) {
+      const float4 x = *(const float4*)(raw + r * 36 + 4 * (kq0 + c));
+      uint4 h, l;
+      split4(x, h, l);
+      const uint32_t o = off_k(r, 4 * (kq0 + c));
+      *(uint4*)(hi + o) = h;
+      *(uint4*)(lo + o) = l;
+    }
+  }
+}
+
+template <bool A_MN, bool B_MN, bool VA, bool VB>
 __global__ void __launch_bounds__(THREADS, 1) tc3_gemm_kernel(const Args a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* bars = (uint64_t*)(smem + 2 * STAGE_BYTES);  // [0], [1]: stage free
-  uint32_t* tslot = (uint32_t*)(bars + 2);
+  uint8_t* raw = smem + 2 * STAGE_BYTES;  // RSTAGES raw fp32 stages
+  uint64_t* bars = (uint64_t*)(raw + RSTAGES * RAW_STAGE);  // [0,1]: stage MMAs done
+  uint64_t* accbar = bars + 2;                              // [0,1]: accumulator ready
+  uint32_t* tslot = (uint32_t*)(accbar + 2);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t = blockIdx.z, s = blockIdx.y;
   const int mt = blockIdx.x % a.mtiles, nt = blockIdx.x / a.mtiles;
@@ -120,8 +236,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc3_gemm_kernel(const Args a) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);  // bars[0..1], accbar[0..1]
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -130,17 +245,34 @@ __global__ void __launch_bounds__(THREADS, 1) tc3_gemm_kernel(const Args a) {
   const uint32_t tmem = *tslot;
 
   const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
-  float racc[BN];
+  CopyPlan<A_MN, VA, BM> pa;
+  CopyPlan<B_MN, VB, BN> pb;
+  pa.init(tid, m0, a.M, A_MN ? a.sAm : a.sAm, a.sAk);
+  pb.init(tid, n0, a.N, a.sBn, a.sBk);
+  const uint32_t raw0 = smem_u32(raw);
+  auto issue = [&](int blk) {
+    if (blk < nkb) {
+      const uint32_t ra = raw0 + (blk % RSTAGES) * RAW_STAGE;
+      const int k0 = kbeg + blk * BK;
+      pa.issue(ra, A, k0, kend, a.sAk);
+      pb.issue(ra + RAW_A * 4, B, k0, kend, a.sBk);
+    }
+    asm volatile("cp.async.commit_group;");  // one group per block (empty past the end)
+  };
+
+  constexpr int HC = BN / 2;  // warps w and w+4 share TMEM lanes 32(w%4).., split columns
+  const int lq = warp & 3, ch = (warp >> 2) * HC;
+  float racc[HC];
 #pragma unroll
-  for (int j = 0; j < BN; ++j) racc[j] = 0.f;
-  auto fold = [&](int blk) {  // wait for block blk's MMAs, add its accumulator
-    mbar_wait(&bars[blk & 1], (blk >> 1) & 1);
+  for (int j = 0; j < HC; ++j) racc[j] = 0.f;
+  auto fold = [&](int g) {  // wait for group g's MMAs, add its accumulator in fp32
+    mbar_wait(&accbar[g & 1], (g >> 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-    for (int c = 0; c < BN; c += 16) {
+    for (int c = 0; c < HC; c += 16) {
       uint32_t v[16];
       const uint32_t taddr =
-          tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)((blk & 1) * BN + c);
+          tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)((g & 1) * BN + ch + c);
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
           "%13,%14,%15}, [%16];"
@@ -154,96 +286,33 @@ __global__ void __launch_bounds__(THREADS, 1) tc3_gemm_kernel(const Args a) {
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
   };
+
+  for (int b = 0; b < RSTAGES - 1; ++b) issue(b);
   for (int it = 0; it < nkb; ++it) {
-    const int st = it & 1;
-    if (it >= 2) mbar_wait(&bars[st], ((it - 2) >> 1) & 1);
+    const int st = it & 1, g = it / FOLD;
+    issue(it + RSTAGES - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(RSTAGES - 1));  // block it landed (own copies)
+    __syncthreads();                                             // ... everyone's
+    if (it >= 2) mbar_wait(&bars[st], ((it - 2) >> 1) & 1);     // split stage st free
+    const float* ra = (const float*)(raw + (it % RSTAGES) * RAW_STAGE);
     uint8_t* base = smem + st * STAGE_BYTES;
     uint8_t *ahi = base, *alo = base + A_BYTES, *bhi = base + 2 * A_BYTES,
             *blo = base + 2 * A_BYTES + B_BYTES;
-    const int k0 = kbeg + it * BK;
-    // ---- A tile: 128 x 32, stored K-major (SW128) in both orientations
-    if (A_MN) {
-      // thread = row m, 32 k's: each load instruction is coalesced along m;
-      // then eight 16-byte stores per half (conflict-free through the swizzle)
-      const int m = m0 + tid;
-      const bool mok = m < a.M;
-#pragma unroll
-      for (int c = 0; c < BK / 4; ++c) {
-        float x[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int k = k0 + 4 * c + j;
-          x[j] = (mok && k < kend) ? __ldg(A + (int64_t)m * a.sAm + (int64_t)k * a.sAk) : 0.f;
-        }
-        uint4 h, l;
-        h.x = to_tf32(x[0]), l.x = to_tf32(x[0] - __uint_as_float(h.x));
-        h.y = to_tf32(x[1]), l.y = to_tf32(x[1] - __uint_as_float(h.y));
-        h.z = to_tf32(x[2]), l.z = to_tf32(x[2] - __uint_as_float(h.z));
-        h.w = to_tf32(x[3]), l.w = to_tf32(x[3] - __uint_as_float(h.w));
-        const uint32_t o = off_k(tid, 4 * c);
-        *(uint4*)(ahi + o) = h;
-        *(uint4*)(alo + o) = l;
-      }
-    } else {
-      const int k = k0 + lane;
-      const bool kok = k < kend;
-#pragma unroll 8
-      for (int i = 0; i < BM / 4; ++i) {
-        const int r = warp + 4 * i, m = m0 + r;
-        const float x = (kok && m < a.M) ? __ldg(A + (int64_t)m * a.sAm + (int64_t)k * a.sAk) : 0.f;
-        const uint32_t h = to_tf32(x), l = to_tf32(x - __uint_as_float(h));
-        const uint32_t o = off_k(r, lane);
-        *(uint32_t*)(ahi + o) = h;
-        *(uint32_t*)(alo + o) = l;
-      }
-    }
-    // ---- B tile: 64 x 32, K-major
-    if (B_MN) {
-      const int r = tid & 63, n = n0 + r, kh = (tid >> 6) * 16;
-      const bool nok = n < a.N;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float x[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int k = k0 + kh + 4 * c + j;
-          x[j] = (nok && k < kend) ? __ldg(B + (int64_t)n * a.sBn + (int64_t)k * a.sBk) : 0.f;
-        }
-        uint4 h, l;
-        h.x = to_tf32(x[0]), l.x = to_tf32(x[0] - __uint_as_float(h.x));
-        h.y = to_tf32(x[1]), l.y = to_tf32(x[1] - __uint_as_float(h.y));
-        h.z = to_tf32(x[2]), l.z = to_tf32(x[2] - __uint_as_float(h.z));
-        h.w = to_tf32(x[3]), l.w = to_tf32(x[3] - __uint_as_float(h.w));
-        const uint32_t o = off_k(r, kh + 4 * c);
-        *(uint4*)(bhi + o) = h;
-        *(uint4*)(blo + o) = l;
-      }
-    } else {
-      const int k = k0 + lane;
-      const bool kok = k < kend;
-#pragma unroll 8
-      for (int i = 0; i < BN / 4; ++i) {
-        const int r = warp + 4 * i, n = n0 + r;
-        const float x = (kok && n < a.N) ? __ldg(B + (int64_t)n * a.sBn + (int64_t)k * a.sBk) : 0.f;
-        const uint32_t h = to_tf32(x), l = to_tf32(x - __uint_as_float(h));
-        const uint32_t o = off_k(r, lane);
-        *(uint32_t*)(bhi + o) = h;
-        *(uint32_t*)(blo + o) = l;
-      }
-    }
+    split_tile<A_MN, BM>(ra, ahi, alo, tid);
+    split_tile<B_MN, BN>(ra + RAW_A, bhi, blo, tid);
     asm volatile("fence.proxy.async.shared::cta;");
     __syncthreads();
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t ah = smem_u32(ahi), al = smem_u32(alo), bh = smem_u32(bhi), bl = smem_u32(blo);
-      const uint32_t tacc = tmem + (uint32_t)(st * BN);  // accumulator of this stage
+      const uint32_t tacc = tmem + (uint32_t)((g & 1) * BN);
       constexpr uint32_t id = idesc<false, false>();  // both operands K-major in smem
 #pragma unroll
       for (int kk = 0; kk < BK / 8; ++kk) {
         // k-step of 8 tf32 = 32 B inside the 128-B swizzle atom
         const uint64_t dah = sdesc(ah + kk * 32, 16, 1024), dal = sdesc(al + kk * 32, 16, 1024);
         const uint64_t dbh = sdesc(bh + kk * 32, 16, 1024), dbl = sdesc(bl + kk * 32, 16, 1024);
-        const uint32_t acc0 = kk > 0 ? 1u : 0u;  // a fresh accumulator per 32-k block
+        const uint32_t acc0 = (it % FOLD != 0 || kk > 0) ? 1u : 0u;  // fresh per group
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
             "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tacc),
@@ -260,22 +329,27 @@ __global__ void __launch_bounds__(THREADS, 1) tc3_gemm_kernel(const Args a) {
       asm volatile(
           "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
               smem_u32(&bars[st])));
+      if (it % FOLD == FOLD - 1 || it == nkb - 1)
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                smem_u32(&accbar[g & 1])));
     }
-    // while the MMAs of this block run: fold the previous block's accumulator
-    // into fp32 registers (round-to-nearest adds: the tensor core's own
-    // accumulation error stays confined to 32-k blocks)
-    if (it >= 1) fold(it - 1);
+    // while this group's MMAs run: fold the previous group into fp32 registers
+    // (round-to-nearest adds; the tensor core's truncating accumulation stays
+    // confined to FOLD*32 k)
+    if (it % FOLD == 0 && it >= FOLD) fold(g - 1);
   }
-  if (nkb >= 1) fold(nkb - 1);
+  if (nkb >= 1) fold((nkb - 1) / FOLD);
+  asm volatile("cp.async.wait_group 0;");
 
-  // ---- epilogue: thread = row m (TMEM lane 32w + lane), 64 columns
-  const int m = m0 + warp * 32 + lane;
+  // ---- epilogue: thread = row m (TMEM lane 32(w%4) + lane), 32 columns
+  const int m = m0 + lq * 32 + lane;
   float* D = a.D + (int64_t)t * a.bD + (int64_t)s * a.sS;
   const float* bias = a.bias ? a.bias + (int64_t)t * a.N : nullptr;
   if (m < a.M) {
 #pragma unroll
-    for (int j = 0; j < BN; ++j) {
-      const int n = n0 + j;
+    for (int j = 0; j < HC; ++j) {
+      const int n = n0 + ch + j;
       if (n < a.N) D[(int64_t)m + (int64_t)n * a.ldD] = bias ? racc[j] + bias[n] : racc[j];
     }
   }
