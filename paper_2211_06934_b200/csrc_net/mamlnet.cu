@@ -16,6 +16,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "mamlnet.h"
@@ -752,6 +753,13 @@ int net_tc_gemm(int64_t T, int64_t M, int64_t N, int64_t K, const float* A, int6
   a.bias = bias;
   a.kchunk = (int)kchunk;
   a.mtiles = (int)mt;
+  a.splits = (int)S;
+  {
+    const char* d = getenv("NET_TC_DBG");  // diagnostics only: see tcg::Args::dbg
+    a.dbg = d ? atoi(d) : 0;
+  }
+  if (mt * nt * S * T > 0x7FFFFFFF) return fail("net_tc_gemm: too many tiles");
+  a.ntiles = (int)(mt * nt * S * T);
   cudaStream_t st = (cudaStream_t)stream;
   if (S > 1) {
     if (bias) return fail("net_tc_gemm: bias with split-K");
@@ -762,7 +770,10 @@ int net_tc_gemm(int64_t T, int64_t M, int64_t N, int64_t K, const float* A, int6
   } else {
     a.D = D, a.ldD = ldD, a.bD = bD, a.sS = 0;
   }
-  dim3 grid((unsigned)(mt * nt), (unsigned)S, (unsigned)T);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  dim3 grid((unsigned)(a.ntiles < sms ? a.ntiles : sms));  // persistent: one CTA per SM
   // 16-byte async copies when the contiguous axis is 16-byte aligned everywhere
   auto al16 = [](const float* p, int64_t other, int64_t batch) {
     return ((uintptr_t)p & 15) == 0 && other % 4 == 0 && batch % 4 == 0;

@@ -5,10 +5,10 @@
 //   D[t](m, n) = sum_k A[t](m, k) * B[t](n, k)   (+ bias[t][n])
 //
 // Each fp32 operand element x is split while it is staged into shared
-// memory: hi = rna_tf32(x), lo = rna_tf32(x - hi) (x - hi is exact in fp32),
-// and the tile product is accumulated in TMEM (fp32) as
-// hi*hi + hi*lo + lo*hi: the dropped lo*lo term and the rounding of lo are
-// ~2^-21 relative, i.e. fp32-GEMM accuracy, which the second-order MAML
+// memory: hi = x truncated to tf32, lo = x - hi (exact in fp32), and the
+// tile product is accumulated in TMEM (fp32) as hi*hi + hi*lo + lo*hi: the
+// dropped lo*lo term and the tensor core's truncation of lo are ~2^-20
+// relative, i.e. fp32-GEMM accuracy, which the second-order MAML
 // meta-gradient needs (single-pass TF32 is ~2^-11). Operands are read with
 // coalesced global loads along whichever axis is contiguous in memory and
 // stored into the 128B-swizzled K-major UMMA canonical layout either way (a
@@ -35,7 +35,10 @@
 
 namespace tcg {
 
-constexpr int BM = 128, BN = 64, BK = 32, THREADS = 256, RSTAGES = 4;
+constexpr int BM = 128, BN = 64, BK = 32, RSTAGES = 4;
+// warp roles: 0-3 copy + split (LOADERS threads), 4-7 fold + epilogue (TMEM
+// lane quarter = warp % 4), 8 MMA issue
+constexpr int LOADERS = 128, THREADS = 288, EPI_WARP0 = 4, MMA_WARP = 8;
 constexpr int A_BYTES = BM * BK * 4;  // 16 KB per split half
 constexpr int B_BYTES = BN * BK * 4;  // 8 KB
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
@@ -96,7 +99,8 @@ struct Args {
   int64_t ldD, bD, sS;
   const float* bias;     // bias[t*N + n] or nullptr
   int kchunk;            // k per split (multiple of BK)
-  int mtiles;
+  int mtiles, splits, ntiles;
+  int dbg;  // diagnostics only (NET_TC_DBG): 1 = no MMA, 2 = no split, 4 = no copies
 };
 
 // Raw fp32 tiles as copied (cp.async, zero-filled outside the matrix):
@@ -124,7 +128,7 @@ template <bool MN, bool V, int R>
 struct CopyPlan {
   static constexpr int RS = MN ? R + 4 : 36;                       // raw row stride
   static constexpr int UNITS = V ? R * BK / 4 : R * BK;            // chunks or elements
-  static constexpr int PER = UNITS / THREADS > 0 ? UNITS / THREADS : 1;
+  static constexpr int PER = UNITS / LOADERS > 0 ? UNITS / LOADERS : 1;
   int64_t off[PER];   // global offset at k = 0 (floats)
   int kk[PER];        // k within the block
   int rows_left[PER]; // rows (MN) valid from this chunk's first row, <= 0 if none
@@ -133,7 +137,7 @@ struct CopyPlan {
   __device__ void init(int tid, int row0, int M, int64_t s_r, int64_t s_k) {
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
-      const int u = tid + THREADS * j;
+      const int u = tid + LOADERS * j;
       live[j] = u < UNITS;
       int r, k;
       if (MN) {  // rows contiguous
@@ -169,74 +173,117 @@ struct CopyPlan {
   }
 };
 
+// hi = x with the low 13 mantissa bits cleared (exactly representable in
+// tf32), lo = x - hi (exact in fp32, |lo| < 2^-10 |x|); the tensor core reads
+// lo's top 19 bits (truncation: <= 2^-20 |x|). Two instructions per element
+// (cvt.rna.tf32 expands to a compare-and-branch sequence in SASS).
+__device__ __forceinline__ uint32_t hi_bits(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
 __device__ __forceinline__ void split4(float4 x, uint4& h, uint4& l) {
-  h.x = to_tf32(x.x), l.x = to_tf32(x.x - __uint_as_float(h.x));
-  h.y = to_tf32(x.y), l.y = to_tf32(x.y - __uint_as_float(h.y));
-  h.z = to_tf32(x.z), l.z = to_tf32(x.z - __uint_as_float(h.z));
-  h.w = to_tf32(x.w), l.w = to_tf32(x.w - __uint_as_float(h.w));
+  h.x = hi_bits(x.x), l.x = __float_as_uint(x.x - __uint_as_float(h.x));
+  h.y = hi_bits(x.y), l.y = __float_as_uint(x.y - __uint_as_float(h.y));
+  h.z = hi_bits(x.z), l.z = __float_as_uint(x.z - __uint_as_float(h.z));
+  h.w = hi_bits(x.w), l.w = __float_as_uint(x.w - __uint_as_float(h.w));
 }
 
-// raw tile -> K-major SW128 hi / lo tiles (R rows x 32 k), threads [0, nthr)
+// raw tile -> K-major SW128 hi / lo tiles (R rows x 32 k), by the LOADERS threads
 template <bool MN, int R>
 __device__ __forceinline__ void split_tile(const float* raw, uint8_t* hi, uint8_t* lo, int tid) {
-  if (MN) {  // raw [k][R+4]: thread = (row quad q, k quad kq); 4x4 transpose in registers
+  if (MN) {  // raw [k][R+4]: unit = (row quad q, k quad kq); 4x4 transpose in registers
     constexpr int RS = R + 4, NQ = R / 4;
-    if (tid >= NQ * 8) return;
-    const int kq = tid % 8, q = tid / 8;
-    float4 x[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) x[i] = *(const float4*)(raw + (4 * kq + i) * RS + 4 * q);
-    const float4 c0 = make_float4(x[0].x, x[1].x, x[2].x, x[3].x);
-    const float4 c1 = make_float4(x[0].y, x[1].y, x[2].y, x[3].y);
-    const float4 c2 = make_float4(x[0].z, x[1].z, x[2].z, x[3].z);
-    const float4 c3 = make_float4(x[0].w, x[1].w, x[2].w, x[3].w);
-    const float4 cs[4] = {c0, c1, c2, c3};
+    for (int u = tid; u < NQ * 8; u += LOADERS) {
+      const int kq = u % 8, q = u / 8;
+      float4 x[4];
 #pragma unroll
-    for (int jr = 0; jr < 4; ++jr) {
-      uint4 h, l;
-      split4(cs[jr], h, l);
-      const uint32_t o = off_k(4 * q + jr, 4 * kq);
-      *(uint4*)(hi + o) = h;
-      *(uint4*)(lo + o) = l;
+      for (int i = 0; i < 4; ++i) x[i] = *(const float4*)(raw + (4 * kq + i) * RS + 4 * q);
+      const float4 cs[4] = {make_float4(x[0].x, x[1].x, x[2].x, x[3].x),
+                            make_float4(x[0].y, x[1].y, x[2].y, x[3].y),
+                            make_float4(x[0].z, x[1].z, x[2].z, x[3].z),
+                            make_float4(x[0].w, x[1].w, x[2].w, x[3].w)};
+#pragma unroll
+      for (int jr = 0; jr < 4; ++jr) {
+        uint4 h, l;
+        split4(cs[jr], h, l);
+        const uint32_t o = off_k(4 * q + jr, 4 * kq);
+        *(uint4*)(hi + o) = h;
+        *(uint4*)(lo + o) = l;
+      }
     }
-  } else {   // raw [R][36]: thread = row, 16-byte reads along k
-    constexpr int PER = R * BK / 4 / THREADS;  // float4 chunks per thread
-    const int r = tid % R, kq0 = (tid / R) * PER;
+  } else {   // raw [R][36]: unit = (row, k quad), 16-byte reads along k
 #pragma unroll
-    for (int c = 0; c < PER; ++c) {
-      const float4 x = *(const float4*)(raw + r * 36 + 4 * (kq0 + c));
+    for (int u = tid; u < R * 8; u += LOADERS) {
+      const int r = u % R, kq = u / R;
+      const float4 x = *(const float4*)(raw + r * 36 + 4 * kq);
       uint4 h, l;
       split4(x, h, l);
-      const uint32_t o = off_k(r, 4 * (kq0 + c));
+      const uint32_t o = off_k(r, 4 * kq);
       *(uint4*)(hi + o) = h;
       *(uint4*)(lo + o) = l;
     }
   }
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void loader_sync() {  // named barrier over the LOADERS threads
+  asm volatile("bar.sync 1, %0;" ::"n"(LOADERS) : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar)));
+}
+
+struct Tile {  // one 128 x 64 output tile of one (batch, k-split)
+  int t, s, m0, n0, kbeg, kend, nkb;
+  __device__ Tile(const Args& a, int idx) {
+    const int ntn = (a.N + BN - 1) / BN, S = a.splits;
+    int r = idx;
+    const int mt = r % a.mtiles;
+    r /= a.mtiles;
+    const int nt = r % ntn;
+    r /= ntn;
+    s = r % S;
+    t = r / S;
+    m0 = mt * BM, n0 = nt * BN;
+    kbeg = s * a.kchunk, kend = min(a.K, kbeg + a.kchunk);
+    nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+  }
+};
+
+// Persistent and warp-specialised: CTA c walks tiles c, c + gridDim.x, ...
+// as one stream of 32-k blocks. Copy/split warps (0-3) keep a 4-deep
+// cp.async ring of raw fp32 tiles and write the split hi / lo stages; the MMA
+// warp (8) issues 12 tcgen05.mma per block into one of two TMEM
+// accumulators; fold/epilogue warps (4-7) add each finished group of FOLD
+// blocks into fp32 registers and store finished tiles. The roles meet only
+// at mbarriers (stage full / empty, accumulator full / empty), so copies,
+// splitting, MMAs and epilogues of different blocks and tiles overlap.
 template <bool A_MN, bool B_MN, bool VA, bool VB>
 __global__ void __launch_bounds__(THREADS, 1) tc3_gemm_kernel(const Args a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* raw = smem + 2 * STAGE_BYTES;  // RSTAGES raw fp32 stages
-  uint64_t* bars = (uint64_t*)(raw + RSTAGES * RAW_STAGE);  // [0,1]: stage MMAs done
-  uint64_t* accbar = bars + 2;                              // [0,1]: accumulator ready
-  uint32_t* tslot = (uint32_t*)(accbar + 2);
+  uint64_t* bars = (uint64_t*)(raw + RSTAGES * RAW_STAGE);
+  uint64_t* hfull = bars;       // [2] split stage written (LOADERS arrivals)
+  uint64_t* hempty = bars + 2;  // [2] split stage consumed (MMA commit)
+  uint64_t* afull = bars + 4;   // [2] accumulator group done (MMA commit)
+  uint64_t* aempty = bars + 6;  // [2] accumulator drained (4 epilogue warps)
+  uint32_t* tslot = (uint32_t*)(bars + 8);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int t = blockIdx.z, s = blockIdx.y;
-  const int mt = blockIdx.x % a.mtiles, nt = blockIdx.x / a.mtiles;
-  const int m0 = mt * BM, n0 = nt * BN;
-  const int kbeg = s * a.kchunk, kend = min(a.K, kbeg + a.kchunk);
-  const float* A = a.A + (int64_t)t * a.bA;
-  const float* B = a.B + (int64_t)t * a.bB;
+  const int ntiles = a.ntiles;
 
-  if (warp == 0) {
+  if (warp == EPI_WARP0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
         smem_u32(tslot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);  // bars[0..1], accbar[0..1]
+    mbar_init(&hfull[0], LOADERS), mbar_init(&hfull[1], LOADERS);
+    mbar_init(&hempty[0], 1), mbar_init(&hempty[1], 1);
+    mbar_init(&afull[0], 1), mbar_init(&afull[1], 1);
+    mbar_init(&aempty[0], 4), mbar_init(&aempty[1], 4);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -244,118 +291,161 @@ __global__ void __launch_bounds__(THREADS, 1) tc3_gemm_kernel(const Args a) {
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tslot;
 
-  const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
-  CopyPlan<A_MN, VA, BM> pa;
-  CopyPlan<B_MN, VB, BN> pb;
-  pa.init(tid, m0, a.M, A_MN ? a.sAm : a.sAm, a.sAk);
-  pb.init(tid, n0, a.N, a.sBn, a.sBk);
-  const uint32_t raw0 = smem_u32(raw);
-  auto issue = [&](int blk) {
-    if (blk < nkb) {
-      const uint32_t ra = raw0 + (blk % RSTAGES) * RAW_STAGE;
-      const int k0 = kbeg + blk * BK;
-      pa.issue(ra, A, k0, kend, a.sAk);
-      pb.issue(ra + RAW_A * 4, B, k0, kend, a.sBk);
-    }
-    asm volatile("cp.async.commit_group;");  // one group per block (empty past the end)
-  };
-
-  constexpr int HC = BN / 2;  // warps w and w+4 share TMEM lanes 32(w%4).., split columns
-  const int lq = warp & 3, ch = (warp >> 2) * HC;
-  float racc[HC];
-#pragma unroll
-  for (int j = 0; j < HC; ++j) racc[j] = 0.f;
-  auto fold = [&](int g) {  // wait for group g's MMAs, add its accumulator in fp32
-    mbar_wait(&accbar[g & 1], (g >> 1) & 1);
-    asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll
-    for (int c = 0; c < HC; c += 16) {
-      uint32_t v[16];
-      const uint32_t taddr =
-          tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)((g & 1) * BN + ch + c);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-          "%13,%14,%15}, [%16];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-            "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-      for (int j = 0; j < 16; ++j) racc[c + j] += __uint_as_float(v[j]);
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-  };
-
-  for (int b = 0; b < RSTAGES - 1; ++b) issue(b);
-  for (int it = 0; it < nkb; ++it) {
-    const int st = it & 1, g = it / FOLD;
-    issue(it + RSTAGES - 1);
-    asm volatile("cp.async.wait_group %0;" ::"n"(RSTAGES - 1));  // block it landed (own copies)
-    __syncthreads();                                             // ... everyone's
-    if (it >= 2) mbar_wait(&bars[st], ((it - 2) >> 1) & 1);     // split stage st free
-    const float* ra = (const float*)(raw + (it % RSTAGES) * RAW_STAGE);
-    uint8_t* base = smem + st * STAGE_BYTES;
-    uint8_t *ahi = base, *alo = base + A_BYTES, *bhi = base + 2 * A_BYTES,
-            *blo = base + 2 * A_BYTES + B_BYTES;
-    split_tile<A_MN, BM>(ra, ahi, alo, tid);
-    split_tile<B_MN, BN>(ra + RAW_A, bhi, blo, tid);
-    asm volatile("fence.proxy.async.shared::cta;");
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t ah = smem_u32(ahi), al = smem_u32(alo), bh = smem_u32(bhi), bl = smem_u32(blo);
-      const uint32_t tacc = tmem + (uint32_t)((g & 1) * BN);
-      constexpr uint32_t id = idesc<false, false>();  // both operands K-major in smem
-#pragma unroll
-      for (int kk = 0; kk < BK / 8; ++kk) {
-        // k-step of 8 tf32 = 32 B inside the 128-B swizzle atom
-        const uint64_t dah = sdesc(ah + kk * 32, 16, 1024), dal = sdesc(al + kk * 32, 16, 1024);
-        const uint64_t dbh = sdesc(bh + kk * 32, 16, 1024), dbl = sdesc(bl + kk * 32, 16, 1024);
-        const uint32_t acc0 = (it % FOLD != 0 || kk > 0) ? 1u : 0u;  // fresh per group
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tacc),
-            "l"(dah), "l"(dbh), "r"(id), "r"(acc0));
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tacc),
-            "l"(dah), "l"(dbl), "r"(id), "r"(1u));
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tacc),
-            "l"(dal), "l"(dbh), "r"(id), "r"(1u));
+  if (warp < EPI_WARP0) {
+    // ===================== copy + split warps =====================
+    CopyPlan<A_MN, VA, BM> pa;
+    CopyPlan<B_MN, VB, BN> pb;
+    const uint32_t raw0 = smem_u32(raw);
+    int itile = blockIdx.x, ikb = 0, iq = 0, ik0 = 0, ikend = 0, inkb = 0;
+    const float *iA = nullptr, *iB = nullptr;
+    auto iset = [&]() {
+      while (itile < ntiles) {
+        const Tile T(a, itile);
+        if (T.nkb > 0) {
+          pa.init(tid, T.m0, a.M, a.sAm, a.sAk);
+          pb.init(tid, T.n0, a.N, a.sBn, a.sBk);
+          iA = a.A + (int64_t)T.t * a.bA, iB = a.B + (int64_t)T.t * a.bB;
+          ik0 = T.kbeg, ikend = T.kend, inkb = T.nkb;
+          return;
+        }
+        itile += gridDim.x;
       }
-      asm volatile(
-          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-              smem_u32(&bars[st])));
-      if (it % FOLD == FOLD - 1 || it == nkb - 1)
-        asm volatile(
-            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                smem_u32(&accbar[g & 1])));
+    };
+    iset();
+    auto issue = [&]() {
+      if (itile < ntiles) {
+        const uint32_t ra = raw0 + (iq % RSTAGES) * RAW_STAGE;
+        const int k0 = ik0 + ikb * BK;
+        if (!(a.dbg & 4)) {
+          pa.issue(ra, iA, k0, ikend, a.sAk);
+          pb.issue(ra + RAW_A * 4, iB, k0, ikend, a.sBk);
+        }
+        ++iq;
+        if (++ikb == inkb) {
+          ikb = 0;
+          itile += gridDim.x;
+          iset();
+        }
+      }
+      asm volatile("cp.async.commit_group;");  // one group per call (empty past the end)
+    };
+    for (int b = 0; b < RSTAGES - 1; ++b) issue();
+    int q = 0;
+    for (int ct = blockIdx.x; ct < ntiles; ct += gridDim.x) {
+      const int nkb = Tile(a, ct).nkb;
+      for (int kb = 0; kb < nkb; ++kb, ++q) {
+        const int st = q & 1;
+        issue();                                                    // block q + RSTAGES - 1
+        asm volatile("cp.async.wait_group %0;" ::"n"(RSTAGES - 1));  // block q: own copies
+        loader_sync();                                              // ... and everyone's
+        if (q >= 2) mbar_wait(&hempty[st], ((q - 2) >> 1) & 1);     // MMAs of q-2 done
+        const float* ra = (const float*)(raw + (q % RSTAGES) * RAW_STAGE);
+        uint8_t* base = smem + st * STAGE_BYTES;
+        if (!(a.dbg & 2)) {
+          split_tile<A_MN, BM>(ra, base, base + A_BYTES, tid);
+          split_tile<B_MN, BN>(ra + RAW_A, base + 2 * A_BYTES, base + 2 * A_BYTES + B_BYTES, tid);
+        }
+        asm volatile("fence.proxy.async.shared::cta;");
+        mbar_arrive(&hfull[st]);
+        loader_sync();  // raw stage q % RSTAGES fully read before it is refilled
+      }
     }
-    // while this group's MMAs run: fold the previous group into fp32 registers
-    // (round-to-nearest adds; the tensor core's truncating accumulation stays
-    // confined to FOLD*32 k)
-    if (it % FOLD == 0 && it >= FOLD) fold(g - 1);
-  }
-  if (nkb >= 1) fold((nkb - 1) / FOLD);
-  asm volatile("cp.async.wait_group 0;");
-
-  // ---- epilogue: thread = row m (TMEM lane 32(w%4) + lane), 32 columns
-  const int m = m0 + lq * 32 + lane;
-  float* D = a.D + (int64_t)t * a.bD + (int64_t)s * a.sS;
-  const float* bias = a.bias ? a.bias + (int64_t)t * a.N : nullptr;
-  if (m < a.M) {
+    asm volatile("cp.async.wait_group 0;");
+  } else if (warp == MMA_WARP) {
+    // ===================== MMA issue (one thread) =====================
+    if (lane == 0) {
+      int q = 0, g = 0;
+      constexpr uint32_t id = idesc<false, false>();  // both operands K-major in smem
+      for (int ct = blockIdx.x; ct < ntiles; ct += gridDim.x) {
+        const int nkb = Tile(a, ct).nkb;
+        for (int kb = 0; kb < nkb; ++kb, ++q) {
+          const int st = q & 1;
+          const bool gstart = kb % FOLD == 0, gend = kb % FOLD == FOLD - 1 || kb == nkb - 1;
+          mbar_wait(&hfull[st], (q >> 1) & 1);
+          if (gstart && g >= 2) mbar_wait(&aempty[g & 1], ((g - 2) >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          uint8_t* base = smem + st * STAGE_BYTES;
+          const uint32_t ah = smem_u32(base), al = ah + A_BYTES, bh = ah + 2 * A_BYTES,
+                         bl = bh + B_BYTES;
+          const uint32_t tacc = tmem + (uint32_t)((g & 1) * BN);
 #pragma unroll
-    for (int j = 0; j < HC; ++j) {
-      const int n = n0 + ch + j;
-      if (n < a.N) D[(int64_t)m + (int64_t)n * a.ldD] = bias ? racc[j] + bias[n] : racc[j];
+          for (int kk = 0; kk < ((a.dbg & 1) ? 0 : BK / 8); ++kk) {
+            // k-step of 8 tf32 = 32 B inside the 128-B swizzle atom
+            const uint64_t dah = sdesc(ah + kk * 32, 16, 1024), dal = sdesc(al + kk * 32, 16, 1024);
+            const uint64_t dbh = sdesc(bh + kk * 32, 16, 1024), dbl = sdesc(bl + kk * 32, 16, 1024);
+            const uint32_t acc0 = (!gstart || kk > 0) ? 1u : 0u;  // fresh per group
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tacc),
+                "l"(dah), "l"(dbh), "r"(id), "r"(acc0));
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tacc),
+                "l"(dah), "l"(dbl), "r"(id), "r"(1u));
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tacc),
+                "l"(dal), "l"(dbh), "r"(id), "r"(1u));
+          }
+          umma_commit(&hempty[st]);
+          if (gend) {
+            umma_commit(&afull[g & 1]);
+            ++g;
+          }
+        }
+      }
+    }
+  } else if (warp >= EPI_WARP0 && warp < EPI_WARP0 + 4) {
+    // ===================== fold + epilogue warps =====================
+    const int lq = warp & 3;  // TMEM lane quarter this warp may access
+    float racc[BN];
+#pragma unroll
+    for (int j = 0; j < BN; ++j) racc[j] = 0.f;
+    int g = 0;
+    for (int ct = blockIdx.x; ct < ntiles; ct += gridDim.x) {
+      const Tile T(a, ct);
+      const int ngroups = (T.nkb + FOLD - 1) / FOLD;
+      for (int gi = 0; gi < ngroups; ++gi, ++g) {
+        mbar_wait(&afull[g & 1], (g >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int c = 0; c < BN; c += 16) {
+          uint32_t v[16];
+          const uint32_t taddr = tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)((g & 1) * BN + c);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+              "%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+          for (int j = 0; j < 16; ++j) racc[c + j] += __uint_as_float(v[j]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&aempty[g & 1]);
+      }
+      // tile done: store (or bias / zero for an empty k range)
+      const int m = T.m0 + lq * 32 + lane;
+      float* D = a.D + (int64_t)T.t * a.bD + (int64_t)T.s * a.sS;
+      const float* bias = a.bias ? a.bias + (int64_t)T.t * a.N : nullptr;
+      if (m < a.M) {
+#pragma unroll
+        for (int j = 0; j < BN; ++j) {
+          const int n = T.n0 + j;
+          if (n < a.N) D[(int64_t)m + (int64_t)n * a.ldD] = bias ? racc[j] + bias[n] : racc[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < BN; ++j) racc[j] = 0.f;
+    }
+    if (warp == EPI_WARP0) {  // every MMA has completed (last afull waited)
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
     }
   }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
 }
 
 }  // namespace tcg
