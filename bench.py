@@ -320,7 +320,8 @@ def time_oracle(x, offsets, max_elems=None, threads=0):
         n = max_elems
     sl = slice(0, n)
     xs = {k: (None if x[k] is None else x[k][sl]) for k in x}
-    used = oracle.set_num_threads(threads)
+    # all host cores (torchrun exports OMP_NUM_THREADS=1, which would cap OpenMP's default)
+    used = oracle.set_num_threads(threads or len(os.sched_getaffinity(0)))
     t0 = time.perf_counter()
     oracle.adam_fwd(xs["g"], xs["m"], xs["v"], STEP_T, *HP)
     oracle.adam_vjp(xs["g"], xs["m"], xs["v"], xs["du"], xs["dm1"], xs["dv1"], STEP_T, *HP)
@@ -371,6 +372,8 @@ def main():
     ap.add_argument("--size", type=int, default=1 << 24)
     ap.add_argument("--bf16", action="store_true", help="bf16 optimizer state")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 plumbing test on fewer GPUs (gloo; not a bench value)")
     ap.add_argument("--no-maml", action="store_true",
                     help="default workload: skip the C4 MAML tasks/s measurement (maml_c4)")
     ap.add_argument("--quick", action="store_true", help="skip e2e and clock soak (tuning)")
@@ -385,10 +388,16 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # one process per GPU; --dist-backend gloo with more ranks than GPUs is a
+    # plumbing test only (ranks share devices; numbers are not bench values)
+    gpu = local % max(1, torch.cuda.device_count())
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
+        torch.cuda.set_device(gpu)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group("gloo")
+    dev = torch.device("cuda", gpu)
     torch.cuda.set_device(dev)
     if args.workload == "c3":
         return run_sweep(args, dev, rank, world)
