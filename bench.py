@@ -369,6 +369,8 @@ def main():
                     help="MAML task-batched network form (maml.conv4_forward_tasks)")
     ap.add_argument("--maml-streams", type=int, default=8,
                     help="MAML (--maml-impl streams): parallel task branches in the graph")
+    ap.add_argument("--maml-groups", type=int, default=1,
+                    help="MAML (batched): task groups run as concurrent graph branches")
     ap.add_argument("--size", type=int, default=1 << 24)
     ap.add_argument("--bf16", action="store_true", help="bf16 optimizer state")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -594,7 +596,8 @@ def measure_maml(args, dev, rank, world, steps=None):
     shard = None
     if not args.no_graph:
         shard = maml.GraphedShard(maml.task_range(world, rank, cfg.tasks), cfg, inner, dev,
-                                  streams=args.maml_streams,
+                                  streams=(args.maml_groups if args.maml_impl == "batched"
+                                           else args.maml_streams),
                                   batched=args.maml_impl == "batched")
 
     def step(i):
@@ -616,7 +619,8 @@ def measure_maml(args, dev, rank, world, steps=None):
                       "tasks": cfg.tasks, "parallelism": f"task-sharded x{world}, NCCL all-reduce",
                       "cuda_graph": shard is not None,
                       "shard_impl": ("eager per-task" if shard is None else
-                                     f"task-batched graph ({cfg.net})" if shard.batched else
+                                     f"task-batched graph ({cfg.net}), {shard.nstreams} "
+                                     "concurrent group(s)" if shard.batched else
                                      f"graph, {shard.nstreams} task branches")},
            "tasks_per_rank": len(maml.task_range(world, rank, cfg.tasks)),
            "gpu_launches": launches}

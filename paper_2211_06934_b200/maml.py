@@ -528,19 +528,28 @@ class GraphedShard:
     (one task's small convolutions leave most SMs idle); the per-task
     meta-gradients are summed in task order after the join (the same sum as
     the sequential version). With ``batched=True`` the shard's tasks run as
-    one task-batched network (meta_grad_batched: grouped convolutions, one
-    fused inner step for all tasks), ~T x fewer kernels per replay.
+    task-batched networks (meta_grad_batched: batched GEMM convolutions, one
+    fused inner step per group), ~T x fewer kernels per replay; with
+    ``streams = S > 1`` as S contiguous task groups on concurrent graph
+    branches (at a few tasks per GPU each kernel underfills the SMs, so
+    concurrent groups recover the idle capacity), summed in group order.
     Call it like meta_grad_tasks."""
 
     def __init__(self, task_ids, cfg: MamlConfig, inner, device, warmup=2, streams=1,
                  batched=False):
         self.ids, self.cfg, self.inner = list(task_ids), cfg, inner
         self.batched = bool(batched)
+        self.nstreams = max(1, min(int(streams), len(self.ids)))
         if self.batched:
-            self.inner = TaskBatchInner(len(self.ids), device, cfg)
+            # contiguous task groups, one task-batched network per graph branch
+            n, S = len(self.ids), self.nstreams
+            cuts = [n * i // S for i in range(S + 1)]
+            self.groups = [(cuts[i], cuts[i + 1]) for i in range(S) if cuts[i + 1] > cuts[i]]
+            self.nstreams = len(self.groups)
+            self.inners = [TaskBatchInner(b - a, device, cfg) for a, b in self.groups]
+            self.inner = self.inners[0]
         self.phi = torch.zeros(sum(sizes_of(CONV4_SHAPES)), device=device)
         self.data = [task_data(0, t, device, cfg.seed) for t in self.ids]
-        self.nstreams = 1 if self.batched else max(1, min(int(streams), len(self.ids)))
         self.streams = [torch.cuda.Stream(device) for _ in range(self.nstreams)]
         side = torch.cuda.Stream(device)
         side.wait_stream(torch.cuda.current_stream(device))
@@ -565,13 +574,18 @@ class GraphedShard:
         self.launches_per_replay = ours() - n0  # captured library kernels
 
     def _body(self):
-        if self.batched:
+        if self.batched and self.nstreams == 1:
             return meta_grad_batched(self.phi, self.data, self.cfg, self.inner)
         if self.nstreams == 1:
             return meta_grad_data(self.phi, self.data, self.cfg, self.inner)
         cur = torch.cuda.current_stream()
         parts = []
-        for k, d in enumerate(self.data):
+        if self.batched:  # task groups as concurrent graph branches
+            for s, (a, b), inner in zip(self.streams, self.groups, self.inners):
+                s.wait_stream(cur)
+                with torch.cuda.stream(s):
+                    parts.append(meta_grad_batched(self.phi, self.data[a:b], self.cfg, inner))
+        for k, d in enumerate(self.data if not self.batched else []):
             s = self.streams[k % self.nstreams]
             s.wait_stream(cur)
             with torch.cuda.stream(s):
