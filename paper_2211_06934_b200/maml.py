@@ -295,46 +295,58 @@ def _wgrad_uses_split_k(T, M, P):
     return P <= 16 or T * ((M + 63) // 64) * ((P + 63) // 64) < 148
 
 
-class _WGrad(torch.autograd.Function):
-    """a @ b^T for a [T, M, n], b [T, P, n] with long n (a convolution's
-    weight-gradient contraction): net_gemm_nt (split-K) or cuBLAS forward,
-    chosen by shape; its VJP is two ordinary batched GEMMs."""
+def _wgrad_fwd(a, b):
+    """a @ b^T, long contraction: split-K kernel or cuBLAS by shape."""
+    T, M, _ = a.shape
+    if _wgrad_uses_split_k(T, M, b.shape[1]):
+        return _gemm_nt(a, b)
+    return torch.bmm(a, b.transpose(1, 2))
+
+
+class _ConvBwd(torch.autograd.Function):
+    """The task-batched convolution's VJP as ONE node: (dy, w, cols) ->
+    (gw = dy cols^T, gcols = w^T dy, gb = sum dy). Its own VJP (needed once,
+    by the second-order meta-gradient) writes the cotangent of dy with two
+    accumulating GEMMs, d_dy = gb_bar + gw_bar cols + w gcols_bar, instead of
+    three autograd nodes whose contributions are summed by separate
+    elementwise adds over the dy-sized tensor."""
 
     @staticmethod
-    def forward(ctx, a, b):
-        ctx.save_for_backward(a, b)
-        T, M, _ = a.shape
-        if _wgrad_uses_split_k(T, M, b.shape[1]):
-            return _gemm_nt(a, b)
-        return torch.bmm(a, b.transpose(1, 2))
+    def forward(ctx, dy, w, cols, need_w, need_cols, need_b):
+        ctx.save_for_backward(dy, w, cols)
+        ctx.set_materialize_grads(False)  # unused outputs: no GEMMs on zero cotangents
+        gw = _wgrad_fwd(dy, cols) if need_w else None
+        gc = torch.bmm(w.transpose(1, 2), dy) if need_cols else None
+        gb = dy.sum(-1) if need_b else None
+        return gw, gc, gb
 
     @staticmethod
-    def backward(ctx, gc):
-        a, b = ctx.saved_tensors
-        return torch.bmm(gc, b), torch.bmm(gc.transpose(1, 2), a)
-
-
-class _DCols(torch.autograd.Function):
-    """w^T @ dy (a convolution's input-gradient contraction, cuBLAS); its
-    weight-side VJP is the long-n contraction dy @ g^T (_WGrad)."""
-
-    @staticmethod
-    def forward(ctx, w, dy):
-        ctx.save_for_backward(w, dy)
-        return torch.bmm(w.transpose(1, 2), dy)
-
-    @staticmethod
-    def backward(ctx, g):
-        w, dy = ctx.saved_tensors
-        gw = _WGrad.apply(dy, g) if ctx.needs_input_grad[0] else None
-        gdy = torch.bmm(w, g) if ctx.needs_input_grad[1] else None
-        return gw, gdy
+    @torch.autograd.function.once_differentiable
+    def backward(ctx, ggw, ggc, ggb):
+        dy, w, cols = ctx.saved_tensors
+        d_dy = d_w = d_cols = None
+        if ctx.needs_input_grad[0]:
+            bias = ggb.unsqueeze(-1) if ggb is not None else None
+            pairs = ([(ggw, cols)] if ggw is not None else []) + ([(w, ggc)] if ggc is not None else [])
+            for a, b in pairs:
+                if d_dy is None:
+                    d_dy = torch.baddbmm(bias, a, b) if bias is not None else torch.bmm(a, b)
+                else:
+                    d_dy.baddbmm_(a, b)
+            if d_dy is None:
+                d_dy = bias.expand(dy.shape).contiguous() if bias is not None else None
+        if ctx.needs_input_grad[1] and ggc is not None:
+            d_w = _wgrad_fwd(dy, ggc)
+        if ctx.needs_input_grad[2] and ggw is not None:
+            d_cols = torch.bmm(ggw.transpose(1, 2), dy)
+        return d_dy, d_w, d_cols, None, None, None
 
 
 class _TaskConvGemm(torch.autograd.Function):
     """bias + w @ cols for the task-batched convolution (cuBLAS batched
-    SGEMM); backward: weight gradient through _WGrad (split-K), input
-    gradient through _DCols, both differentiable for second order."""
+    SGEMM); backward: one _ConvBwd node (weight gradient through the
+    split-K kernel or cuBLAS, input gradient, bias gradient), differentiable
+    once for the second-order meta-gradient."""
 
     @staticmethod
     def forward(ctx, w, cols, bias):
@@ -344,10 +356,8 @@ class _TaskConvGemm(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dy):
         w, cols = ctx.saved_tensors
-        gw = _WGrad.apply(dy, cols) if ctx.needs_input_grad[0] else None
-        gc = _DCols.apply(w, dy) if ctx.needs_input_grad[1] else None
-        gb = dy.sum(-1) if ctx.needs_input_grad[2] else None
-        return gw, gc, gb
+        nw, nc, nb = ctx.needs_input_grad
+        return _ConvBwd.apply(dy.contiguous(), w, cols, nw, nc, nb)
 
 
 def _conv3x3_tasks_fused(h, w, b):

@@ -30,7 +30,7 @@ def main():
     inner = maml.FusedSgdInner(maml.sizes_of(maml.CONV4_SHAPES), dev, cfg)
     outer = maml.FusedAdamOuter(phi.numel(), dev, cfg.outer_lr)
     shard = maml.GraphedShard(range(cfg.tasks), cfg, inner, dev, batched=args.impl == "batched",
-                              streams=8)
+                              streams=1 if args.impl == "batched" else 8)
     for i in range(3):
         phi, _, _ = maml.outer_step(phi, i, cfg, inner, outer, shard=shard)
     torch.cuda.synchronize()
