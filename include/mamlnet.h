@@ -118,7 +118,9 @@ int net_gemm_nt(int64_t T, int64_t M, int64_t P, int64_t N, const float* A, cons
  * has stride 1. splits > 1 splits k into ranges whose partial tiles go to
  * `workspace` (net_tc_gemm_workspace_bytes) and are summed in order by a
  * second kernel; then D must be contiguous (ldD == M, bD == M*N) and bias
- * NULL. Requires T <= 65535. */
+ * NULL. Requires T <= 65535. Diagnostics only: the environment variable
+ * NET_TC_DBG (read once) skips stages for timing ablations (1 = no MMA,
+ * 2 = no split, 4 = no copies; results are then wrong by design). */
 size_t net_tc_gemm_workspace_bytes(int64_t T, int64_t M, int64_t N, int64_t K, int64_t splits);
 int net_tc_gemm(int64_t T, int64_t M, int64_t N, int64_t K, const float* A, int64_t sAm,
                 int64_t sAk, int64_t bA, const float* B, int64_t sBn, int64_t sBk, int64_t bB,

@@ -890,10 +890,11 @@ int net_tc_gemm(int64_t T, int64_t M, int64_t N, int64_t K, const float* A, int6
   a.kchunk = (int)kchunk;
   a.mtiles = (int)mt;
   a.splits = (int)S;
-  {
-    const char* d = getenv("NET_TC_DBG");  // diagnostics only: see tcg::Args::dbg
-    a.dbg = d ? atoi(d) : 0;
-  }
+  static const int dbg = [] {  // diagnostics only (stage ablation): see tcg::Args::dbg
+    const char* d = getenv("NET_TC_DBG");
+    return d ? atoi(d) : 0;
+  }();
+  a.dbg = dbg;
   if (mt * nt * S * T > 0x7FFFFFFF) return fail("net_tc_gemm: too many tiles");
   a.ntiles = (int)(mt * nt * S * T);
   cudaStream_t st = (cudaStream_t)stream;
@@ -926,14 +927,14 @@ int net_tc_gemm(int64_t T, int64_t M, int64_t N, int64_t K, const float* A, int6
       tcg::tc3_gemm_kernel<true, false, true, false>,   tcg::tc3_gemm_kernel<true, false, true, true>,
       tcg::tc3_gemm_kernel<true, true, false, false>,   tcg::tc3_gemm_kernel<true, true, false, true>,
       tcg::tc3_gemm_kernel<true, true, true, false>,    tcg::tc3_gemm_kernel<true, true, true, true>};
-  static bool attr[16] = {};
+  static std::atomic<bool> attr[16];  // cudaFuncSetAttribute done (idempotent)
   const int which = (a_mn ? 8 : 0) + (b_mn ? 4 : 0) + (va ? 2 : 0) + (vb ? 1 : 0);
   const KFn kern = table[which];
   if (!attr[which]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              tcg::SMEM_BYTES) != cudaSuccess)
       return fail("net_tc_gemm: cannot set shared-memory size");
-    attr[which] = true;
+    attr[which].store(true);
   }
   kern<<<grid, tcg::THREADS, tcg::SMEM_BYTES, st>>>(a);
   int rc = launched();
