@@ -12,7 +12,7 @@
 //   u1 = ((w >> 41) + .5) 2^-23,  u2 = ((w & 0x7FFFFF) + .5) 2^-23,
 //   z_2k = sqrt(-2 ln u1) cos(2 pi u2), z_2k+1 = sqrt(-2 ln u1) sin(2 pi u2)
 // (SplitMix64 finaliser `mix`; one draw per Box-Muller pair). u1, u2 are
-// exact in fp32; log/sqrt/sincospi are the accurate fp32 functions.
+// exact in fp32; log and sin/cos use the MUFU approximations (es_pair).
 #pragma once
 #include <stdint.h>
 
@@ -37,11 +37,14 @@ __device__ __forceinline__ void es_pair(uint64_t key, int64_t k, float& z0, floa
   const uint64_t w = es_mix(key + (uint64_t)k);
   const float u1 = ((float)(uint32_t)(w >> 41) + 0.5f) * (1.0f / 8388608.0f);
   const float u2 = ((float)(uint32_t)(w & 0x7FFFFFull) + 0.5f) * (1.0f / 8388608.0f);
-  const float r = sqrtf(-2.0f * logf(u1));
-  float sn, cs;
-  sincospif(2.0f * u2, &sn, &cs);
-  z0 = r * cs;
-  z1 = r * sn;
+  // MUFU fast paths (the kernel is ALU-bound otherwise: 67% of HBM with the
+  // accurate functions): lg2.approx for the log (rel. error ~2^-22),
+  // sin/cos.approx on a = 2 pi (u2 - 1/2) in (-pi, pi) (abs. error ~2^-21),
+  // with sin(2 pi u2) = -sin(a), cos(2 pi u2) = -cos(a) exactly.
+  const float r = sqrtf(-2.0f * 0.69314718055994531f * __log2f(u1));
+  const float a = 6.28318530717958648f * (u2 - 0.5f);
+  z0 = -r * __cosf(a);
+  z1 = -r * __sinf(a);
 }
 
 __device__ __forceinline__ float es_normal(uint64_t key, int64_t j) {
