@@ -56,7 +56,7 @@
 extern "C" {
 #endif
 
-#define DIFFOPT_ABI_VERSION 3
+#define DIFFOPT_ABI_VERSION 4
 
 typedef enum {
   OPT_OK = 0,
@@ -328,6 +328,32 @@ int opt_cg_update(int64_t n, float* x, float* r, const float* p, const float* Ap
                   void* workspace, size_t workspace_bytes, void* stream);
 int opt_cg_direction(int64_t n, float* p, const float* r, const double* state, void* stream);
 int opt_neumann_step(int64_t n, float* v, const float* Av, float* x, double alpha, void* stream);
+
+/* ------------------------------------- sharded step over peer memory
+ * SURVEY §8(f) NEXT-2, element-sharded (ZeRO-1) Adam for W ranks of one
+ * node, with the reduce-scatter, the fused step and the all-gather in ONE
+ * kernel over peer memory (NVLink / NVSwitch loads and stores through
+ * CUDA-IPC-mapped pointers) instead of two collectives around a local step.
+ * Rank r owns elements [lo, lo + n_shard) of the flat tree. For each owned
+ * element e:
+ *   g      = grad_scale * sum_{w = 0..world-1} g_peers[w][e]   (fixed order)
+ *   (u, m', v') = Adam_step(g, mu[e - lo], nu[e - lo])          (as opt_adam_fwd)
+ *   theta' = params[e] + u, written to params_peers[w][e] for every w
+ * mu / nu (fp32, the shard only) are updated in place. g_peers[w] /
+ * params_peers[w] are device pointers valid in this process (the peer's
+ * buffer mapped by CUDA IPC, or local memory); params is this rank's copy
+ * (== params_peers[rank]). The caller orders the call: every peer's
+ * gradient complete before, every peer's writes complete after (e.g. a
+ * stream sync + process-group barrier on both sides). 1 <= world <=
+ * OPT_MAX_PEERS; pointers 16-byte aligned; lo % 4 == 0. */
+#define OPT_MAX_PEERS 8
+typedef struct {
+  const float* g[OPT_MAX_PEERS];
+  float* params[OPT_MAX_PEERS];
+} opt_peers;
+int opt_adam_fwd_peers(int world, const opt_peers* peers, int64_t lo, int64_t n_shard,
+                       int64_t step, const opt_adam_hp* hp, double grad_scale, float* mu,
+                       float* nu, const float* params, void* stream);
 
 /* -------------------------------------------------------------- misc */
 const char* opt_status_string(int status);

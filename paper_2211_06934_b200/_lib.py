@@ -486,3 +486,32 @@ def opt_cg_direction(n, p, r, state, stream=None):
 def opt_neumann_step(n, v, Av, x, alpha, stream=None):
     _check(lib.opt_neumann_step(int(n), _ptr(v), _ptr(Av), _ptr(x), float(alpha),
                                 _stream(stream)))
+
+
+# ------------------------- sharded Adam step over peer memory (NEXT-2, fused)
+OPT_MAX_PEERS = 8
+
+
+class opt_peers(ctypes.Structure):
+    _fields_ = [("g", ctypes.c_void_p * OPT_MAX_PEERS),
+                ("params", ctypes.c_void_p * OPT_MAX_PEERS)]
+
+
+lib.opt_adam_fwd_peers.argtypes = [ctypes.c_int, ctypes.POINTER(opt_peers), _i64, _i64, _i64,
+                                   ctypes.POINTER(opt_adam_hp), ctypes.c_double, _P, _P, _P, _P]
+lib.opt_adam_fwd_peers.restype = ctypes.c_int
+EXPORTS += ["opt_adam_fwd_peers"]
+
+
+def opt_adam_fwd_peers(world, g_peers, params_peers, lo, n_shard, step, hp, grad_scale, mu, nu,
+                       params, stream=None):
+    """g_peers / params_peers: per-rank tensors (or device pointers) valid in
+    this process (CUDA-IPC mapped for remote ranks)."""
+    pr = opt_peers()
+    for w in range(min(int(world), OPT_MAX_PEERS, len(g_peers))):  # the C side validates world
+        pr.g[w] = _ptr(g_peers[w])
+        pr.params[w] = _ptr(params_peers[w])
+    h = _hp(opt_adam_hp, hp)
+    _check(lib.opt_adam_fwd_peers(int(world), ctypes.byref(pr), int(lo), int(n_shard), int(step),
+                                  ctypes.byref(h), float(grad_scale), _ptr(mu), _ptr(nu),
+                                  _ptr(params), _stream(stream)))

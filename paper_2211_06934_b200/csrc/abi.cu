@@ -1113,6 +1113,84 @@ int opt_quadratic_rev(int64_t numel, const float* a, const float* g_bar, float* 
 }  // extern "C"
 
 // ------------------------------------------- zero-order ES (NEXT-3, es.cuh)
+
+// ------------------------------------------ sharded Adam step over peer memory
+namespace dopt {
+struct PeerArgs {
+  const float* g[OPT_MAX_PEERS];
+  float* p[OPT_MAX_PEERS];
+};
+
+// One pass over the shard: W peer gradient loads (summed in rank order, so
+// every rank computes bit-identical sums), the Adam step on the local state,
+// and W peer parameter stores: reduce-scatter + step + all-gather fused.
+__global__ void __launch_bounds__(256) adam_peers_kernel(int world, PeerArgs pa, int64_t lo,
+                                                         int64_t nvec, int64_t tail, float scale,
+                                                         AdamFwd<float> op, float* __restrict__ mu,
+                                                         float* __restrict__ nu,
+                                                         const float* __restrict__ params) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec + tail; v += stride) {
+    const bool vec = v < nvec;
+    const int64_t i0 = vec ? 4 * v : 4 * nvec + (v - nvec);  // shard index
+    const int nl = vec ? 4 : 1;
+    float g[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int w = 0; w < world; ++w) {
+      if (vec) {
+        const float4 x = __ldcv(reinterpret_cast<const float4*>(pa.g[w] + lo + i0));
+        g[0] += x.x, g[1] += x.y, g[2] += x.z, g[3] += x.w;
+      } else {
+        g[0] += __ldcv(pa.g[w] + lo + i0);
+      }
+    }
+    float m[4], vv[4], th[4], out[4];
+    for (int k = 0; k < nl; ++k) {
+      m[k] = mu[i0 + k], vv[k] = nu[i0 + k], th[k] = params[lo + i0 + k];
+      float u, m1, v1;
+      op.apply(g[k] * scale, m[k], vv[k], u, m1, v1);
+      mu[i0 + k] = m1, nu[i0 + k] = v1;
+      out[k] = th[k] + u;
+    }
+    for (int w = 0; w < world; ++w) {
+      if (vec)
+        __stcg(reinterpret_cast<float4*>(pa.p[w] + lo + i0), make_float4(out[0], out[1], out[2], out[3]));
+      else
+        __stcg(pa.p[w] + lo + i0, out[0]);
+    }
+  }
+}
+}  // namespace dopt
+
+extern "C" int opt_adam_fwd_peers(int world, const opt_peers* peers, int64_t lo, int64_t n_shard,
+                                  int64_t step, const opt_adam_hp* hp, double grad_scale,
+                                  float* mu, float* nu, const float* params, void* stream) {
+  using namespace dopt;
+  g_err.clear();
+  TRY(check_adam(step, hp));
+  if (world < 1 || world > OPT_MAX_PEERS) return fail(OPT_EINVAL, "world = %d", world);
+  if (!peers) return fail(OPT_EINVAL, "peers is NULL");
+  if (lo < 0 || n_shard < 0) return fail(OPT_EINVAL, "bad shard range");
+  if (lo % 4) return fail(OPT_EALIGN, "lo = %lld is not a multiple of 4", (long long)lo);
+  if (!(grad_scale == grad_scale)) return fail(OPT_EINVAL, "grad_scale is NaN");
+  if (n_shard == 0) return OPT_OK;
+  if (!mu || !nu || !params) return fail(OPT_EINVAL, "mu / nu / params is NULL");
+  TRY(check_align({mu, nu, params}));
+  PeerArgs pa{};
+  for (int w = 0; w < world; ++w) {
+    if (!peers->g[w] || !peers->params[w]) return fail(OPT_EINVAL, "peer %d pointer is NULL", w);
+    TRY(check_align({peers->g[w], peers->params[w]}));
+    pa.g[w] = peers->g[w], pa.p[w] = peers->params[w];
+  }
+  AdamFwd<float> op;
+  fill_adam_fwd(op, step, hp);
+  const int64_t nvec = n_shard / 4, tail = n_shard - 4 * nvec;
+  int64_t blocks = (nvec + tail + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  adam_peers_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      world, pa, lo, nvec, tail, (float)grad_scale, op, mu, nu, params);
+  return launched(static_cast<cudaStream_t>(stream));
+}
+
 #include "es.cuh"
 
 extern "C" {

@@ -63,3 +63,64 @@ class ShardedAdam:
         else:
             params.copy_(self.p_out)
         return params
+
+
+class PeerShardedAdam:
+    """ZeRO-1 Adam with the reduce-scatter, the fused step and the all-gather
+    in ONE kernel over peer memory (opt_adam_fwd_peers): every rank maps its
+    peers' gradient and parameter buffers with CUDA IPC once (handles
+    exchanged through the process group), then each step rank r reads the
+    W gradient slices of its shard over NVLink, steps its m, v, and stores
+    the new parameter slice into all W parameter copies. Ordering across
+    ranks is a stream sync + process-group barrier before the kernel (every
+    gradient complete) and after it (every peer's stores complete).
+
+    grads / params: this rank's full (n_pad) buffers, allocated here so
+    they can be shared: write gradients into ``self.grads`` and read the
+    parameters from ``self.params``."""
+
+    def __init__(self, n, world, rank, device, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, group=None,
+                 average=True):
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        if world > L.OPT_MAX_PEERS:
+            raise ValueError(f"world {world} > OPT_MAX_PEERS {L.OPT_MAX_PEERS}")
+        self.n, self.world, self.rank, self.dev = int(n), int(world), int(rank), device
+        self.shard = shard_size(n, world)
+        self.n_pad = self.shard * world
+        self.hp = (lr, b1, b2, eps, 0.0)
+        self.scale = 1.0 / world if average else 1.0
+        self.grads = torch.zeros(self.n_pad, device=device)
+        self.params = torch.zeros(self.n_pad, device=device)
+        self.m = torch.zeros(self.shard, device=device)
+        self.v = torch.zeros(self.shard, device=device)
+        self.t = 0
+        self.group = group
+        mine = (reduce_tensor(self.grads), reduce_tensor(self.params))
+        handles = [None] * world
+        if world > 1:
+            dist.all_gather_object(handles, mine, group=group)
+        else:
+            handles = [mine]
+        self.g_peers, self.p_peers = [], []
+        for w, (hg, hp_) in enumerate(handles):
+            if w == rank:
+                self.g_peers.append(self.grads)
+                self.p_peers.append(self.params)
+            else:  # peer's buffers mapped into this process (kept alive here)
+                self.g_peers.append(hg[0](*hg[1]))
+                self.p_peers.append(hp_[0](*hp_[1]))
+
+    def _barrier(self):
+        torch.cuda.synchronize(self.dev)
+        if self.world > 1:
+            dist.barrier(group=self.group)
+
+    def step(self):
+        """One synchronous sharded step on self.grads -> self.params (all ranks)."""
+        self.t += 1
+        self._barrier()  # every rank's gradient is complete
+        L.opt_adam_fwd_peers(self.world, self.g_peers, self.p_peers, self.rank * self.shard,
+                             self.shard, self.t, self.hp, self.scale, self.m, self.v, self.params)
+        self._barrier()  # every rank's stores into every parameter copy are complete
+        return self.params

@@ -1,0 +1,153 @@
+"""GPU tests of the fused peer-memory sharded Adam step (opt_adam_fwd_peers,
+SURVEY §8(f) NEXT-2): reduce-scatter + step + all-gather in one kernel.
+
+* W virtual ranks in one process (W buffers on one device, the W calls in
+  sequence): every parameter copy is bitwise identical to the others and
+  equals the fused single-GPU Adam step (opt_adam_fwd with apply) on the
+  averaged gradient to fp32 rounding (two kernels may contract the same
+  expressions into FMAs differently), for W = 1, 2, 3, 8, ragged sizes.
+* Two real processes on one GPU: the buffers of the other process are mapped
+  by CUDA IPC (handles exchanged over a gloo process group) exactly as on a
+  multi-GPU node; three steps match the virtual-rank run bitwise."""
+import os
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+HP = (1e-2, 0.9, 0.999, 1e-8, 0.0)
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2211_06934_b200 import _lib
+
+    return _lib
+
+
+def virtual(L, grads, p0, steps):
+    """The W ranks' calls in sequence in one process (same kernel as the
+    multi-process run): returns rank 0's parameter copy."""
+    from paper_2211_06934_b200.sharded import shard_size
+
+    W = len(grads[0])
+    shard = p0.numel() // W
+    copies = [p0.clone() for _ in range(W)]
+    state = [(torch.zeros(shard, device=DEV), torch.zeros(shard, device=DEV)) for _ in range(W)]
+    for t in range(steps):
+        for r in range(W):
+            L.opt_adam_fwd_peers(W, grads[t], copies, r * shard, shard, t + 1, HP, 1.0 / W,
+                                 state[r][0], state[r][1], copies[r])
+    torch.cuda.synchronize()
+    return copies[0]
+
+
+def reference(L, grads, params, steps):
+    """Fused single-GPU Adam (opt_adam_fwd with apply) on the averaged gradient."""
+    W = len(grads[0])
+    n = params.numel()
+    tree = L.Tree(numel=n, device=DEV)
+    m, v, p = torch.zeros(n, device=DEV), torch.zeros(n, device=DEV), params.clone()
+    for t in range(steps):
+        g = grads[t][0].clone()
+        for w in range(1, W):
+            g = g + grads[t][w]
+        g = g * (1.0 / W)
+        L.opt_adam_fwd(tree, t + 1, HP, 0, 1, g, m, v, None, m, v, p, p)
+    return p
+
+
+@pytest.mark.parametrize("W,n", [(1, 1000), (2, 4096), (3, 10001), (8, 2 ** 18 + 7)])
+def test_virtual_ranks_equal_single_gpu_step(L, W, n):
+    from paper_2211_06934_b200.sharded import shard_size
+
+    shard = shard_size(n, W)
+    n_pad = shard * W
+    gen = torch.Generator(device=DEV).manual_seed(W)
+    p0 = torch.zeros(n_pad, device=DEV)
+    p0[:n] = torch.randn(n, device=DEV, generator=gen)
+    steps = 3
+    grads = [[torch.zeros(n_pad, device=DEV) for _ in range(W)] for _ in range(steps)]
+    for t in range(steps):
+        for w in range(W):
+            grads[t][w][:n] = torch.randn(n, device=DEV, generator=gen)
+    copies = [p0.clone() for _ in range(W)]
+    state = [(torch.zeros(shard, device=DEV), torch.zeros(shard, device=DEV)) for _ in range(W)]
+    for t in range(steps):
+        for r in range(W):  # each "rank" in turn: disjoint shards
+            L.opt_adam_fwd_peers(W, grads[t], copies, r * shard, shard, t + 1, HP, 1.0 / W,
+                                 state[r][0], state[r][1], copies[r])
+        torch.cuda.synchronize()
+    ref = reference(L, grads, p0, steps)
+    for w in range(W):
+        assert torch.equal(copies[w], copies[0]), f"copy {w} differs from copy 0"
+    torch.testing.assert_close(copies[0], ref, rtol=1e-6, atol=1e-6)
+
+
+def test_bad_arguments_rejected(L):
+    z = torch.zeros(16, device=DEV)
+    with pytest.raises(L.DiffoptError):
+        L.opt_adam_fwd_peers(0, [], [], 0, 16, 1, HP, 1.0, z, z, z)
+    with pytest.raises(L.DiffoptError):
+        L.opt_adam_fwd_peers(1, [z], [z], 2, 8, 1, HP, 1.0, z, z, z)  # lo not a multiple of 4
+    with pytest.raises(L.DiffoptError):
+        L.opt_adam_fwd_peers(9, [z] * 9, [z] * 9, 0, 16, 1, HP, 1.0, z, z, z)
+
+
+def _worker(rank, world, init_file, n, steps, out_dir):
+    import torch.distributed as dist
+
+    from paper_2211_06934_b200.sharded import PeerShardedAdam
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"file://{init_file}", rank=rank,
+                            world_size=world)
+    opt = PeerShardedAdam(n, world, rank, torch.device(DEV), lr=HP[0])
+    gen = torch.Generator(device=DEV).manual_seed(100)
+    opt.params[:n] = torch.randn(n, device=DEV, generator=gen)
+    for t in range(steps):
+        g = torch.Generator(device=DEV).manual_seed(1000 * t + rank)
+        opt.grads[:n] = torch.randn(n, device=DEV, generator=g)
+        opt.step()
+    np.save(os.path.join(out_dir, f"p{rank}.npy"), opt.params.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_processes_cuda_ipc(L):
+    import torch.multiprocessing as mp
+
+    from paper_2211_06934_b200.sharded import shard_size
+
+    n, world, steps = 50_003, 2, 3
+    with tempfile.TemporaryDirectory() as d:
+        ctx = mp.get_context("spawn")
+        procs = [ctx.Process(target=_worker, args=(r, world, os.path.join(d, "init"), n, steps, d))
+                 for r in range(world)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(timeout=240)
+        assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+        outs = [np.load(os.path.join(d, f"p{r}.npy")) for r in range(world)]
+    shard = shard_size(n, world)
+    n_pad = shard * world
+    p0 = torch.zeros(n_pad, device=DEV)
+    p0[:n] = torch.randn(n, device=DEV, generator=torch.Generator(device=DEV).manual_seed(100))
+    grads = []
+    for t in range(steps):
+        row = []
+        for r in range(world):
+            g = torch.zeros(n_pad, device=DEV)
+            g[:n] = torch.randn(n, device=DEV,
+                                generator=torch.Generator(device=DEV).manual_seed(1000 * t + r))
+            row.append(g)
+        grads.append(row)
+    ref = virtual(L, grads, p0, steps).cpu().numpy()
+    for r in range(world):
+        assert np.array_equal(outs[r], ref), f"rank {r}"
