@@ -369,6 +369,9 @@ def main():
                     help="MAML task-batched network form (maml.conv4_forward_tasks)")
     ap.add_argument("--maml-streams", type=int, default=8,
                     help="MAML (--maml-impl streams): parallel task branches in the graph")
+    ap.add_argument("--maml-outer", default="adam", choices=["adam", "peer"],
+                    help="MAML outer step: NCCL all-reduce + replicated fused Adam, or the "
+                         "all-reduce fused into a sharded Adam over peer memory")
     ap.add_argument("--maml-groups", type=int, default=1,
                     help="MAML (batched): task groups run as concurrent graph branches")
     ap.add_argument("--size", type=int, default=1 << 24)
@@ -588,7 +591,10 @@ def measure_maml(args, dev, rank, world, steps=None):
     cfg = maml.MamlConfig(tasks=args.tasks, net=args.maml_net)
     phi = maml.init_params(0, dev)
     inner = maml.FusedSgdInner(maml.sizes_of(maml.CONV4_SHAPES), dev, cfg)
-    outer = maml.FusedAdamOuter(phi.numel(), dev, cfg.outer_lr)
+    if args.maml_outer == "peer":  # all-reduce fused into the outer step (peer memory)
+        outer = maml.PeerAdamOuter(phi.numel(), world, rank, dev, cfg.outer_lr, cfg.tasks)
+    else:
+        outer = maml.FusedAdamOuter(phi.numel(), dev, cfg.outer_lr)
     state = {"phi": phi}
     torch.backends.cudnn.benchmark = True
     torch.backends.cudnn.allow_tf32 = False   # fp32 convolutions (dtype f32)
@@ -616,7 +622,10 @@ def measure_maml(args, dev, rank, world, steps=None):
            "ms_per_step": round(ms / steps, 3), "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded 5-way tasks)",
            "config": {"workload": "C4 MAML 4-conv64, 5-way 5-shot 15-query, 5 inner SGD-mom steps",
-                      "tasks": cfg.tasks, "parallelism": f"task-sharded x{world}, NCCL all-reduce",
+                      "tasks": cfg.tasks,
+                      "parallelism": (f"task-sharded x{world}, " + (
+                          "all-reduce fused into the outer step (peer memory)"
+                          if args.maml_outer == "peer" else "NCCL all-reduce")),
                       "cuda_graph": shard is not None,
                       "shard_impl": ("eager per-task" if shard is None else
                                      f"task-batched graph ({cfg.net}), {shard.nstreams} "

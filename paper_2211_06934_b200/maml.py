@@ -619,6 +619,32 @@ class GraphedShard:
         return self.mg, self.loss
 
 
+class PeerAdamOuter:
+    """Outer Adam with the meta-gradient all-reduce FUSED into the step
+    (sharded.PeerShardedAdam / opt_adam_fwd_peers): rank r sums the W ranks'
+    local meta-gradient sums for its 1/W shard of phi straight from their
+    memory (CUDA IPC; NVLink on a multi-GPU node), applies Adam with the
+    1/tasks scaling, and stores the new phi slice into every rank's copy.
+    Replaces FusedAdamOuter + the NCCL all-reduce of the meta-gradient; the
+    scalar query loss is still all-reduced (4 bytes)."""
+
+    fused_allreduce = True
+
+    def __init__(self, n, world, rank, device, lr, tasks, group=None):
+        from .sharded import PeerShardedAdam
+
+        self.n = int(n)
+        self.opt = PeerShardedAdam(n, world, rank, device, lr=lr, group=group,
+                                   grad_scale=1.0 / tasks)
+
+    def step_from_local(self, phi, mg_local):
+        self.opt.params[:self.n].copy_(phi)  # replicas are identical; keeps phi's storage
+        self.opt.grads[:self.n].copy_(mg_local)
+        self.opt.step()
+        phi.copy_(self.opt.params[:self.n])
+        return phi
+
+
 def outer_step(phi, outer_step_idx, cfg: MamlConfig, inner, outer, world=1, rank=0, group=None,
                shard=None):
     """One synchronous meta-update over the cfg.tasks-task meta-batch.
@@ -628,6 +654,12 @@ def outer_step(phi, outer_step_idx, cfg: MamlConfig, inner, outer, world=1, rank
     ids = task_range(world, rank, cfg.tasks)
     run = shard if shard is not None else meta_grad_tasks
     mg, loss = run(phi, ids, outer_step_idx, cfg, inner)
+    if getattr(outer, "fused_allreduce", False):
+        loss = loss.reshape(1).clone()
+        if world > 1:
+            dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=group)
+        phi = outer.step_from_local(phi, mg)
+        return phi, loss[0] / cfg.tasks, None
     buf = torch.cat([mg, loss.reshape(1)])
     if world > 1:
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)  # the one exchange step

@@ -80,7 +80,7 @@ class PeerShardedAdam:
     parameters from ``self.params``."""
 
     def __init__(self, n, world, rank, device, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, group=None,
-                 average=True):
+                 average=True, grad_scale=None):
         from torch.multiprocessing.reductions import reduce_tensor
 
         if world > L.OPT_MAX_PEERS:
@@ -89,7 +89,7 @@ class PeerShardedAdam:
         self.shard = shard_size(n, world)
         self.n_pad = self.shard * world
         self.hp = (lr, b1, b2, eps, 0.0)
-        self.scale = 1.0 / world if average else 1.0
+        self.scale = grad_scale if grad_scale is not None else (1.0 / world if average else 1.0)
         self.grads = torch.zeros(self.n_pad, device=device)
         self.params = torch.zeros(self.n_pad, device=device)
         self.m = torch.zeros(self.shard, device=device)

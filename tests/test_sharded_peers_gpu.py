@@ -151,3 +151,79 @@ def test_two_processes_cuda_ipc(L):
     ref = virtual(L, grads, p0, steps).cpu().numpy()
     for r in range(world):
         assert np.array_equal(outs[r], ref), f"rank {r}"
+
+
+def _maml_worker(rank, world, init_file, out_dir):
+    import torch.distributed as dist
+
+    from paper_2211_06934_b200 import maml
+
+    torch.cuda.set_device(0)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    dist.init_process_group("gloo", init_method=f"file://{init_file}", rank=rank,
+                            world_size=world)
+    cfg = maml.MamlConfig(tasks=4, inner_steps=2)
+    phi = maml.init_params(0, DEV)
+    inner = maml.FusedSgdInner(maml.sizes_of(maml.CONV4_SHAPES), DEV, cfg)
+    outer = maml.PeerAdamOuter(phi.numel(), world, rank, torch.device(DEV), cfg.outer_lr,
+                               cfg.tasks)
+    losses, phis = [], []
+    for step in range(2):
+        phi, loss, _ = maml.outer_step(phi, step, cfg, inner, outer, world, rank)
+        losses.append(float(loss))
+        phis.append(phi.cpu().numpy())
+    np.save(os.path.join(out_dir, f"phi{rank}.npy"), np.stack(phis))
+    np.save(os.path.join(out_dir, f"loss{rank}.npy"), np.array(losses))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_maml_outer_step_with_fused_peer_allreduce(L):
+    """Two ranks x 2 tasks with the meta-gradient all-reduce fused into the
+    outer Adam step (maml.PeerAdamOuter) == one process computing the same
+    two local sums, adding them in rank order and taking the fused
+    single-GPU Adam step. Step 1 starts from identical inputs: updates agree
+    to fp32 rounding. Step 2 starts from phis that differ by that rounding,
+    and Adam maps near-zero meta-gradient entries to +-lr-sized updates, so
+    there only the replicas' identity and the losses are held tight."""
+    import torch.multiprocessing as mp
+
+    from paper_2211_06934_b200 import maml
+
+    world = 2
+    with tempfile.TemporaryDirectory() as d:
+        ctx = mp.get_context("spawn")
+        procs = [ctx.Process(target=_maml_worker, args=(r, world, os.path.join(d, "init"), d))
+                 for r in range(world)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(timeout=300)
+        assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+        phis = [np.load(os.path.join(d, f"phi{r}.npy")) for r in range(world)]
+        losses = [np.load(os.path.join(d, f"loss{r}.npy")) for r in range(world)]
+    assert np.array_equal(phis[0], phis[1])  # replicas identical
+    assert np.array_equal(losses[0], losses[1])
+    # reference in one process with the same summation: the two ranks' local
+    # meta-gradient sums (same kernels, same tasks), added in rank order,
+    # scaled by 1/tasks, then the fused single-GPU Adam step with apply
+    torch.backends.cuda.matmul.allow_tf32 = False
+    cfg = maml.MamlConfig(tasks=4, inner_steps=2)
+    phi = maml.init_params(0, DEV)
+    inner = maml.FusedSgdInner(maml.sizes_of(maml.CONV4_SHAPES), DEV, cfg)
+    tree = L.Tree(numel=phi.numel(), device=DEV)
+    m, v = torch.zeros_like(phi), torch.zeros_like(phi)
+    ref_losses, refs = [], []
+    for step in range(2):
+        parts = [maml.meta_grad_tasks(phi, maml.task_range(world, r, cfg.tasks), step, cfg, inner)
+                 for r in range(world)]
+        g = (parts[0][0] + parts[1][0]) * (1.0 / cfg.tasks)
+        ref_losses.append(float((parts[0][1] + parts[1][1]) / cfg.tasks))
+        L.opt_adam_fwd(tree, step + 1, (cfg.outer_lr, 0.9, 0.999, 1e-8, 0.0), 0, 1, g, m, v, None,
+                       m, v, phi, phi)
+        refs.append(phi.cpu().numpy())
+    phi0 = maml.init_params(0, "cpu").numpy()
+    upd, ref_upd = phis[0][0] - phi0, refs[0] - phi0
+    assert np.abs(upd - ref_upd).max() <= 1e-5 * np.abs(ref_upd).max() + 1e-8
+    np.testing.assert_allclose(losses[0], ref_losses, rtol=1e-5)
+    assert np.all(np.isfinite(phis[0][1]))
