@@ -211,7 +211,7 @@ __device__ __forceinline__ void cluster_sum(double (&v)[K], double* sm, double* 
   for (int k = 0; k < K; ++k) v[k] = sm[32 * K + k];
 }
 
-__global__ void bnpool_fwd_kernel(int B, int H, int W, const float* __restrict__ x,
+__global__ void __launch_bounds__(256, 6) bnpool_fwd_kernel(int B, int H, int W, const float* __restrict__ x,
                                   const float* __restrict__ gamma, const float* __restrict__ beta,
                                   double eps, float* __restrict__ out, uint8_t* __restrict__ code,
                                   float* __restrict__ mean_out, float* __restrict__ rstd_out) {
@@ -258,7 +258,7 @@ __global__ void bnpool_fwd_kernel(int B, int H, int W, const float* __restrict__
   }
 }
 
-__global__ void bnpool_bwd_kernel(int B, int H, int W, const float* __restrict__ dp,
+__global__ void __launch_bounds__(256, 6) bnpool_bwd_kernel(int B, int H, int W, const float* __restrict__ dp,
                                   const uint8_t* __restrict__ code, const float* __restrict__ x,
                                   const float* __restrict__ gamma, const float* __restrict__ mean,
                                   const float* __restrict__ rstd, float* __restrict__ dx,
@@ -277,8 +277,8 @@ __global__ void bnpool_bwd_kernel(int B, int H, int W, const float* __restrict__
   double v[2] = {0.0, 0.0};
   for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
     const uint8_t c = cg[p];
+    const float d = dpg[p];  // unconditional: only the x gather depends on the code
     if (c != kOff) {
-      const float d = dpg[p];
       const float xh = (xg[q.elem0(p) + q.off(c)] - m) * r;
       v[0] += (double)d;
       v[1] += (double)d * (double)xh;
@@ -295,7 +295,7 @@ __global__ void bnpool_bwd_kernel(int B, int H, int W, const float* __restrict__
   for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
     const int e0 = q.elem0(p);
     const uint8_t c = cg[p];
-    const float d = c != kOff ? dpg[p] : 0.f;
+    const float dl = dpg[p], d = c != kOff ? dl : 0.f;  // unconditional load
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int e = e0 + q.off(k);
@@ -311,7 +311,7 @@ __global__ void bnpool_bwd_kernel(int B, int H, int W, const float* __restrict__
   }
 }
 
-__global__ void bnpool_bwd2_kernel(int B, int H, int W, const float* __restrict__ gdx,
+__global__ void __launch_bounds__(256, 6) bnpool_bwd2_kernel(int B, int H, int W, const float* __restrict__ gdx,
                                    const float* __restrict__ gdgamma, const float* __restrict__ gdbeta,
                                    const float* __restrict__ dp, const uint8_t* __restrict__ code,
                                    const float* __restrict__ x, const float* __restrict__ gamma,
@@ -340,13 +340,14 @@ __global__ void bnpool_bwd2_kernel(int B, int H, int W, const float* __restrict_
     for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
       const int e0 = q.elem0(p);
       const uint8_t c = cg[p];
+      const float dl = dpg[p];  // unconditional: no code -> load dependence
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int e = e0 + q.off(k);
         const float t = gg[e];
         v[0] += (double)t;
         v[1] += (double)t * (double)((xg[e] - m) * r);
-        if (c == k) v[2] += (double)dpg[p] * (double)t;
+        if (c == k) v[2] += (double)dl * (double)t;
       }
     }
     for (int j = ls.lo + threadIdx.x; j < ls.hi; j += blockDim.x) {
@@ -375,7 +376,7 @@ __global__ void bnpool_bwd2_kernel(int B, int H, int W, const float* __restrict_
   for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
     const int e0 = q.elem0(p);
     const uint8_t c = cg[p];
-    const float d = c != kOff ? dpg[p] : 0.f;
+    const float dl = dpg[p], d = c != kOff ? dl : 0.f;  // unconditional load
     float o = 0.f;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
