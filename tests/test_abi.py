@@ -171,3 +171,25 @@ def test_rmsprop_cm_validation(L):
     rc = L.lib.opt_rmsprop_cm_fwd(ctypes.byref(t.c), ctypes.byref(h), ctypes.byref(ext), 0, 0,
                                   P + 4, P, P, P, P, P, P, P, P, P, 0)
     assert rc == L.OPT_EALIGN
+
+
+def test_peer_sharded_step_validation(L):
+    """opt_adam_fwd_peers rejects bad arguments before any CUDA call."""
+    h = L.opt_adam_hp(1e-3, 0.9, 0.999, 1e-8, 0.0)
+    P = 0x10000
+
+    def call(world, lo=0, n=16, g_null=False, step=1, align_bad=False):
+        pr = L.opt_peers()
+        for w in range(min(world, L.OPT_MAX_PEERS)):
+            pr.g[w] = None if g_null else P + (4 if align_bad else 0)
+            pr.params[w] = P
+        return L.lib.opt_adam_fwd_peers(world, ctypes.byref(pr), lo, n, step, ctypes.byref(h),
+                                        1.0, P, P, P, 0)
+
+    assert call(0) == L.OPT_EINVAL
+    assert call(L.OPT_MAX_PEERS + 1) == L.OPT_EINVAL
+    assert call(2, lo=2) == L.OPT_EALIGN
+    assert call(2, g_null=True) == L.OPT_EINVAL
+    assert call(2, align_bad=True) == L.OPT_EALIGN
+    assert call(2, step=0) == L.OPT_EINVAL
+    assert call(2, n=0) == L.OPT_OK  # empty shard: nothing launched
