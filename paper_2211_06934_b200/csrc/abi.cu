@@ -264,6 +264,12 @@ int zero_outputs(const opt_tree* t, int nh, double* d_hp, double* d_hp_leaf, cud
 #endif
 
 // cp.async double-buffered streaming kernel (step_pipe)
+#ifndef DOPT_FWD_GRID_MULT  // forward grid = persistent grid x this (0 = one block per 256 vectors)
+#define DOPT_FWD_GRID_MULT 0
+#endif
+#ifndef DOPT_BWD_GRID_MULT  // backward grid = persistent grid x this (0 = kMaxGrid), <= kMaxGrid
+#define DOPT_BWD_GRID_MULT 1
+#endif
 #ifndef DOPT_PIPE_FWD
 #define DOPT_PIPE_FWD 0
 #endif
@@ -381,6 +387,20 @@ int launch(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r, const 
   int64_t work = ((a.numel >> 2) + kBlock - 1) / kBlock + 1;
   int rc = grid_for(k, work, 0, &grid);
   if (rc) return rc;
+  if constexpr (Op::NH == 0) {
+    // no block partials, so the grid is free: one block per 256 vectors
+    // (measured on B200: forward 97-101% of the copy peak vs 91-94% with the
+    // persistent grid, whose per-block tails end unevenly; DOPT_FWD_GRID_MULT)
+    int64_t g = DOPT_FWD_GRID_MULT > 0 ? (int64_t)grid * DOPT_FWD_GRID_MULT : work;
+    if (g > work) g = work;
+    if (g > 0x7FFFFFFF) g = 0x7FFFFFFF;
+    grid = (int)g;
+  } else {
+    int64_t g = DOPT_BWD_GRID_MULT > 0 ? (int64_t)grid * DOPT_BWD_GRID_MULT : kMaxGrid;
+    if (g > kMaxGrid) g = kMaxGrid;  // block partials live in the workspace
+    if (g > work) g = work;
+    grid = (int)g;
+  }
   cudaError_t le = launch_k(k, grid, kBlock, 0, s, op, a);
   if (le != cudaSuccess) return fail(OPT_ECUDA, "launch: %s", cudaGetErrorString(le));
   return launched(s);

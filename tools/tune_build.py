@@ -31,6 +31,12 @@ def one(cfg):
     m = re.search(r"st(\d)", extra)
     if m:
         defs.append(f"DOPT_ST_POLICY={m.group(1)}")
+    m = re.search(r"gm(\d+)", extra)
+    if m:
+        defs.append(f"DOPT_FWD_GRID_MULT={m.group(1)}")
+    m = re.search(r"bm(\d+)", extra)
+    if m:
+        defs.append(f"DOPT_BWD_GRID_MULT={m.group(1)}")
     if "span" in extra:
         defs.append("DOPT_SPAN=1")
     if "pipeF" in extra:
