@@ -37,6 +37,8 @@ def one(cfg):
     m = re.search(r"bm(\d+)", extra)
     if m:
         defs.append(f"DOPT_BWD_GRID_MULT={m.group(1)}")
+    if "wp" in extra:
+        defs.append("DOPT_WARP_PARTIALS=1")
     if "span" in extra:
         defs.append("DOPT_SPAN=1")
     if "pipeF" in extra:
