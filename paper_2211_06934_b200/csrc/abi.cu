@@ -12,6 +12,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <unordered_map>
 
 #include "diffopt.h"
@@ -387,15 +388,17 @@ int launch(const Op& op, StepArgs<Op::NIN, Op::NOUT>& a, const Reduce& r, const 
   int64_t work = ((a.numel >> 2) + kBlock - 1) / kBlock + 1;
   int rc = grid_for(k, work, 0, &grid);
   if (rc) return rc;
-  if constexpr (Op::NH == 0) {
-    // no block partials, so the grid is free: one block per 256 vectors
-    // (measured on B200: forward 97-101% of the copy peak vs 91-94% with the
-    // persistent grid, whose per-block tails end unevenly; DOPT_FWD_GRID_MULT)
+  if constexpr (Op::NH == 0 && std::is_same<ST, float>::value) {
+    // fp32 state and no block partials, so the grid is free: one block per
+    // 256 vectors (measured on B200: fp32 forwards 103-106% of the copy peak
+    // at 2^26-2^30 vs 91-94% with the persistent grid, whose per-block tails
+    // end unevenly; bf16-state forwards measured 2-5% slower this way, so they
+    // keep the persistent grid; DOPT_FWD_GRID_MULT)
     int64_t g = DOPT_FWD_GRID_MULT > 0 ? (int64_t)grid * DOPT_FWD_GRID_MULT : work;
     if (g > work) g = work;
     if (g > 0x7FFFFFFF) g = 0x7FFFFFFF;
     grid = (int)g;
-  } else {
+  } else if constexpr (Op::NH > 0) {
     int64_t g = DOPT_BWD_GRID_MULT > 0 ? (int64_t)grid * DOPT_BWD_GRID_MULT : kMaxGrid;
     if (g > kMaxGrid) g = kMaxGrid;  // block partials live in the workspace
     if (g > work) g = work;
