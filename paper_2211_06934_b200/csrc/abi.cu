@@ -1240,8 +1240,8 @@ int opt_es_perturb(int64_t numel, int64_t n_samples, int64_t sample0, int antith
   if (groups > n_samples) groups = n_samples;
   const int64_t spg = (n_samples + groups - 1) / groups;
   const int64_t work = nvec * ((n_samples + spg - 1) / spg);
-  int64_t grid = (work + 255) / 256;
-  if (grid > (int64_t)sms * 8) grid = (int64_t)sms * 8;
+  int64_t grid = (work + 255) / 256;  // one work item per thread (no persistent cap: as
+  if (grid > 0x7FFFFFFF) grid = 0x7FFFFFFF;  // for the forward step kernels, blocks end evenly)
   if (grid < 1) grid = 1;
   const size_t smem = sizeof(uint64_t) * (size_t)n_samples;
   static const cudaError_t attr = cudaFuncSetAttribute(
@@ -1270,7 +1270,10 @@ int opt_es_grad(int64_t numel, int64_t n_samples, int antithetic, double sigma, 
   const bool split = nvec < (int64_t)sms * 512 && n_samples >= 64;  // small tree, many samples
   const int64_t threads = split ? nvec * 32 : nvec;
   int64_t grid = (threads + 255) / 256;
-  if (grid > (int64_t)sms * 8) grid = (int64_t)sms * 8;
+  // every block stages the samples' keys and weights: with few samples a
+  // full grid (blocks end evenly) is cheap; with many, stay persistent
+  if (n_samples > 256 && grid > (int64_t)sms * 8) grid = (int64_t)sms * 8;
+  if (grid > 0x7FFFFFFF) grid = 0x7FFFFFFF;
   if (grid < 1) grid = 1;
   const size_t smem = (sizeof(uint64_t) + sizeof(float)) * (size_t)n_samples;
   const int max_smem = (int)((sizeof(uint64_t) + sizeof(float)) * kEsMaxSamples);
