@@ -1084,7 +1084,13 @@ __global__ void __launch_bounds__(kBlock) quad_rev_kernel(int64_t n, const float
 
 template <class K>
 int glue_launch(K kernel, int64_t n, cudaStream_t s, int* grid) {
-  return grid_for(kernel, ((n >> 2) + kBlock - 1) / kBlock + 1, 0, grid);
+  // elementwise, no partials: one block per 256 vectors (blocks end evenly;
+  // see the forward step kernels)
+  (void)kernel;
+  (void)s;
+  const int64_t g = ((n >> 2) + kBlock - 1) / kBlock + 1;
+  *grid = (int)(g < 0x7FFFFFFF ? g : 0x7FFFFFFF);
+  return OPT_OK;
 }
 
 }  // namespace
@@ -1370,7 +1376,7 @@ int opt_neumann_step(int64_t n, float* v, const float* Av, float* x, double alph
   if (!v || !Av || !x) return fail(OPT_EINVAL, "NULL array");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int grid = 0;
-  TRY(grid_for(neumann_kernel, ((n >> 2) + kBlock - 1) / kBlock + 1, 0, &grid));
+  TRY(glue_launch(neumann_kernel, n, s, &grid));
   neumann_kernel<<<grid, kBlock, 0, s>>>(n, v, Av, x, (float)alpha);
   return launched(s);
 }
