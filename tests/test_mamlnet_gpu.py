@@ -262,3 +262,33 @@ def test_tc_gemm_split_k(maml, splits):
     ref = torch.bmm(B.double(), A.double().transpose(1, 2))
     assert float((D.double() - ref).abs().max()) <= 1e-5 * K ** 0.5
     assert torch.equal(D, _tc(maml, A, B, splits=splits))  # fixed order: reproducible
+
+
+def test_tc_gemm_network_path_meta_gradient(maml):
+    """Experimental tcgen05 3xTF32 convolutions (maml.USE_TC, engaged at
+    >= 16 tasks and >= 4096 positions): the second-order meta-gradient of a
+    16-task batch stays as close to float64 as the SIMT path's."""
+    import torch.nn.functional as F  # noqa: F401
+
+    T = 16
+    cfg = maml.MamlConfig(tasks=T, inner_steps=2)
+    phi = maml.init_params(0, DEV)
+    data = [maml.task_data(1, t, DEV) for t in range(T)]
+
+    def torch_inner(g, b, theta):
+        b1 = g if b is None else cfg.inner_momentum * b + g
+        return theta - cfg.inner_lr * b1, b1
+
+    d64 = [[a.double() if a.is_floating_point() else a for a in d] for d in data]
+    mg64, _ = maml.meta_grad_data(phi.double(), d64, maml.MamlConfig(tasks=T, inner_steps=2,
+                                                                      net="gemm"), torch_inner)
+    errs = {}
+    old = maml.USE_TC
+    try:
+        for tc in (False, True):
+            maml.USE_TC = tc
+            mg, _ = maml.meta_grad_batched(phi, data, cfg, maml.TaskBatchInner(T, DEV, cfg))
+            errs[tc] = float((mg.double() - mg64).norm() / mg64.norm())
+    finally:
+        maml.USE_TC = old
+    assert errs[True] < max(3 * errs[False], 2e-5), errs
