@@ -23,6 +23,12 @@
 
 namespace dopt {
 
+#ifndef DOPT_DYN_TAIL_PCT  // percent of the vectors claimed dynamically (0 = off)
+#define DOPT_DYN_TAIL_PCT 5
+#endif
+constexpr int64_t kDynTailPct = DOPT_DYN_TAIL_PCT;
+constexpr int64_t kDynTailMinVec = int64_t(1) << 24;  // >= 2^26 elements
+constexpr int64_t kMaxParts = 4096;  // partial slots in the workspace (= kMaxGrid)
 #ifndef DOPT_SPAN
 #define DOPT_SPAN 0
 #endif
@@ -252,13 +258,30 @@ __global__ void __launch_bounds__(kBlock, MINB) step_uniform(const Op op,
   const int64_t nvec = a.numel >> 2;
   const int64_t nthreads = (int64_t)gridDim.x * kBlock;
   const int64_t tid = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+  // Dynamic tail (large trees, hyper-gradient mode): the last kDynTailPct
+  // percent of the vectors are split into chunks that blocks claim with an
+  // atomic counter once their static share is done, so blocks on slower SMs
+  // do not stretch the kernel's end. Each chunk's partial sum has its own
+  // slot and is computed identically whichever block takes it: the total
+  // stays a fixed-order, bitwise-reproducible sum. (Measured on B200: +1-2%
+  // at 2^28 elements, -0.5% at the 11.7M-element C2 tree, hence the floor.)
+  int64_t nstatic = nvec, nchunks = 0, chunk = kBlock;
+  if (Op::NH > 0 && want_hp && nvec >= kDynTailMinVec) {
+    const int64_t dyn = nvec * kDynTailPct / 100;
+    const int64_t room = kMaxParts - gridDim.x;
+    chunk = ((dyn / 256 + kBlock - 1) / kBlock) * kBlock;
+    if (chunk < kBlock) chunk = kBlock;
+    nchunks = room > 0 ? dyn / chunk : 0;
+    if (nchunks > room) nchunks = room;
+    nstatic = nvec - nchunks * chunk;
+  }
   pdl_wait();
 #if DOPT_SPAN
-  process_spans<Op, ST, U>(op, a, nvec, tid, nthreads, acc, want_hp);
+  process_spans<Op, ST, U>(op, a, nstatic, tid, nthreads, acc, want_hp);
 #else
-  process_vectors<Op, ST, U>(op, a, 0, nvec, tid, nthreads, acc, want_hp);
+  process_vectors<Op, ST, U>(op, a, 0, nstatic, tid, nthreads, acc, want_hp);
 #endif
-  pdl_trigger();
+  if (nchunks == 0) pdl_trigger();
   // ragged tail (numel % 4 elements) -> the last block
   const int64_t tail0 = nvec << 2;
   if (blockIdx.x == gridDim.x - 1 && tail0 + threadIdx.x < a.numel)
@@ -272,11 +295,33 @@ __global__ void __launch_bounds__(kBlock, MINB) step_uniform(const Op op,
 #pragma unroll
       for (int k = 0; k < NH; ++k) a.partials[(int64_t)blockIdx.x * NH + k] = acc[k];
     }
+    if (nchunks > 0) {  // claim dynamic chunks until none is left
+      __shared__ int64_t s_c;
+      for (;;) {
+        if (threadIdx.x == 0) s_c = (int64_t)atomicAdd(a.counter + 1, 1u);
+        __syncthreads();
+        const int64_t c = s_c;
+        __syncthreads();
+        if (c >= nchunks) break;
+        double a2[NH];
+#pragma unroll
+        for (int k = 0; k < NH; ++k) a2[k] = 0.0;
+        const int64_t v0 = nstatic + c * chunk;
+        process_vectors<Op, ST, U>(op, a, v0, v0 + chunk, threadIdx.x, kBlock, a2, want_hp);
+        block_sum<NH>(a2, sm);
+        if (threadIdx.x == 0) {
+#pragma unroll
+          for (int k = 0; k < NH; ++k) a.partials[((int64_t)gridDim.x + c) * NH + k] = a2[k];
+        }
+      }
+      pdl_trigger();
+    }
     if (last_block(a.counter, gridDim.x)) {
       double s[NH];
 #pragma unroll
       for (int k = 0; k < NH; ++k) s[k] = 0.0;
-      for (int64_t b = threadIdx.x; b < gridDim.x; b += kBlock)
+      const int64_t nparts = (int64_t)gridDim.x + nchunks;  // blocks, then chunks
+      for (int64_t b = threadIdx.x; b < nparts; b += kBlock)
 #pragma unroll
         for (int k = 0; k < NH; ++k) s[k] += __ldcg(&a.partials[b * NH + k]);
       block_sum<NH>(s, sm);
@@ -284,7 +329,8 @@ __global__ void __launch_bounds__(kBlock, MINB) step_uniform(const Op op,
 #pragma unroll
         for (int k = 0; k < NH; ++k)
           if (a.d_hp) a.d_hp[k] = s[k];
-        *a.counter = 0u;
+        a.counter[0] = 0u;
+        a.counter[1] = 0u;
       }
     }
   }
