@@ -345,12 +345,15 @@ class _ConvBwd(torch.autograd.Function):
     elementwise adds over the dy-sized tensor."""
 
     @staticmethod
-    def forward(ctx, dy, w, cols, need_w, need_cols, need_b):
+    def forward(ctx, dy, w, cols, need_w, need_cols, need_b, bias_zero=False):
         ctx.save_for_backward(dy, w, cols)
         ctx.set_materialize_grads(False)  # unused outputs: no GEMMs on zero cotangents
+        ctx.bias_zero = bias_zero
         gw = _wgrad_fwd(dy, cols) if need_w else None
         gc = torch.bmm(w.transpose(1, 2), dy) if need_cols else None
-        gb = dy.sum(-1) if need_b else None
+        gb = None
+        if need_b:  # identically zero when a batch norm follows (see _conv3x3_tasks_fused)
+            gb = dy.new_zeros(dy.shape[:2]) if bias_zero else dy.sum(-1)
         return gw, gc, gb
 
     @staticmethod
@@ -359,7 +362,8 @@ class _ConvBwd(torch.autograd.Function):
         dy, w, cols = ctx.saved_tensors
         d_dy = d_w = d_cols = None
         if ctx.needs_input_grad[0]:
-            bias = ggb.unsqueeze(-1) if ggb is not None else None
+            # a constant-zero gb contributes nothing to dy's cotangent
+            bias = ggb.unsqueeze(-1) if (ggb is not None and not ctx.bias_zero) else None
             pairs = ([(ggw, cols)] if ggw is not None else []) + ([(w, ggc)] if ggc is not None else [])
             for a, b in pairs:
                 if d_dy is None:
@@ -372,7 +376,7 @@ class _ConvBwd(torch.autograd.Function):
             d_w = _wgrad_fwd(dy, ggc)
         if ctx.needs_input_grad[2] and ggw is not None:
             d_cols = torch.bmm(ggw.transpose(1, 2), dy)
-        return d_dy, d_w, d_cols, None, None, None
+        return d_dy, d_w, d_cols, None, None, None, None
 
 
 class _TaskConvGemm(torch.autograd.Function):
@@ -382,22 +386,29 @@ class _TaskConvGemm(torch.autograd.Function):
     once for the second-order meta-gradient."""
 
     @staticmethod
-    def forward(ctx, w, cols, bias):
+    def forward(ctx, w, cols, bias, bias_zero=False):
         ctx.save_for_backward(w, cols)
+        ctx.bias_zero = bias_zero
         return _conv_fwd(w, cols, bias)
 
     @staticmethod
     def backward(ctx, dy):
         w, cols = ctx.saved_tensors
-        nw, nc, nb = ctx.needs_input_grad
-        return _ConvBwd.apply(dy.contiguous(), w, cols, nw, nc, nb)
+        nw, nc, nb = ctx.needs_input_grad[:3]
+        gw, gc, gb = _ConvBwd.apply(dy.contiguous(), w, cols, nw, nc, nb, ctx.bias_zero)
+        return gw, gc, gb, None
 
 
-def _conv3x3_tasks_fused(h, w, b):
+def _conv3x3_tasks_fused(h, w, b, bn_follows=False):
     """_conv3x3_tasks with libmamlnet.so im2col/col2im and split-K weight
-    gradients."""
+    gradients. bn_follows: a training-mode batch norm over (task, channel)
+    groups consumes the output, so the gradient reaching the conv output
+    sums to zero over every group (BN removes the group mean: sum dx =
+    gamma*r*(sum dy - n*A - Bm*sum xh) = 0) and the bias gradient is
+    identically zero; it is returned as exact zeros (no reduction kernel,
+    and no rounding noise where the exact value is 0)."""
     T, Cin, B, H, W = h.shape
-    out = _TaskConvGemm.apply(w.reshape(T, w.shape[1], Cin * 9), _Im2ColK.apply(h), b)
+    out = _TaskConvGemm.apply(w.reshape(T, w.shape[1], Cin * 9), _Im2ColK.apply(h), b, bn_follows)
     return out.view(T, -1, B, H, W)
 
 
@@ -502,7 +513,7 @@ def conv4_forward_tasks(params, x, T, net="cudnn"):
         h = x.permute(1, 0, 2, 3).unsqueeze(1).contiguous()  # [T, 1, B, 28, 28]
         for blk in range(4):
             w, b, gam, bet = params[4 * blk: 4 * blk + 4]
-            h = _BnPool.apply(_conv3x3_tasks_fused(h, w, b), gam, bet)
+            h = _BnPool.apply(_conv3x3_tasks_fused(h, w, b, bn_follows=True), gam, bet)
         h = h.reshape(T, 64, -1).transpose(1, 2)  # [T, B, 64]
     elif net == "gemm":
         h = x.permute(1, 0, 2, 3).unsqueeze(1)  # [T, 1, B, 28, 28]
