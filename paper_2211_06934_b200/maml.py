@@ -330,9 +330,12 @@ def _conv_fwd(w, cols, bias):
     T, Co, K = w.shape
     n = cols.shape[2]
     if _tc_ok(T, n):  # D(m = n_sp, n = co) = sum_k cols[k][m] w[co][k] (+ bias[co])
-        w, cols, bias = w.contiguous(), cols.contiguous(), bias.contiguous()
+        w, cols = w.contiguous(), cols.contiguous()
+        bias = bias.contiguous() if bias is not None else None
         out = cols.new_empty(T, Co, n)
         return _tc_call(T, n, Co, K, cols, 1, n, K * n, w, K, 1, Co * K, out, n, Co * n, bias)
+    if bias is None:
+        return torch.bmm(w, cols)
     return torch.baddbmm(bias.unsqueeze(-1), w, cols)
 
 
@@ -345,15 +348,12 @@ class _ConvBwd(torch.autograd.Function):
     elementwise adds over the dy-sized tensor."""
 
     @staticmethod
-    def forward(ctx, dy, w, cols, need_w, need_cols, need_b, bias_zero=False):
+    def forward(ctx, dy, w, cols, need_w, need_cols, need_b):
         ctx.save_for_backward(dy, w, cols)
         ctx.set_materialize_grads(False)  # unused outputs: no GEMMs on zero cotangents
-        ctx.bias_zero = bias_zero
         gw = _wgrad_fwd(dy, cols) if need_w else None
         gc = torch.bmm(w.transpose(1, 2), dy) if need_cols else None
-        gb = None
-        if need_b:  # identically zero when a batch norm follows (see _conv3x3_tasks_fused)
-            gb = dy.new_zeros(dy.shape[:2]) if bias_zero else dy.sum(-1)
+        gb = dy.sum(-1) if need_b else None
         return gw, gc, gb
 
     @staticmethod
@@ -362,8 +362,7 @@ class _ConvBwd(torch.autograd.Function):
         dy, w, cols = ctx.saved_tensors
         d_dy = d_w = d_cols = None
         if ctx.needs_input_grad[0]:
-            # a constant-zero gb contributes nothing to dy's cotangent
-            bias = ggb.unsqueeze(-1) if (ggb is not None and not ctx.bias_zero) else None
+            bias = ggb.unsqueeze(-1) if ggb is not None else None
             pairs = ([(ggw, cols)] if ggw is not None else []) + ([(w, ggc)] if ggc is not None else [])
             for a, b in pairs:
                 if d_dy is None:
@@ -376,7 +375,7 @@ class _ConvBwd(torch.autograd.Function):
             d_w = _wgrad_fwd(dy, ggc)
         if ctx.needs_input_grad[2] and ggw is not None:
             d_cols = torch.bmm(ggw.transpose(1, 2), dy)
-        return d_dy, d_w, d_cols, None, None, None, None
+        return d_dy, d_w, d_cols, None, None, None
 
 
 class _TaskConvGemm(torch.autograd.Function):
@@ -386,29 +385,31 @@ class _TaskConvGemm(torch.autograd.Function):
     once for the second-order meta-gradient."""
 
     @staticmethod
-    def forward(ctx, w, cols, bias, bias_zero=False):
+    def forward(ctx, w, cols, bias):
         ctx.save_for_backward(w, cols)
-        ctx.bias_zero = bias_zero
         return _conv_fwd(w, cols, bias)
 
     @staticmethod
     def backward(ctx, dy):
         w, cols = ctx.saved_tensors
         nw, nc, nb = ctx.needs_input_grad[:3]
-        gw, gc, gb = _ConvBwd.apply(dy.contiguous(), w, cols, nw, nc, nb, ctx.bias_zero)
-        return gw, gc, gb, None
+        return _ConvBwd.apply(dy.contiguous(), w, cols, nw, nc, nb)
 
 
 def _conv3x3_tasks_fused(h, w, b, bn_follows=False):
     """_conv3x3_tasks with libmamlnet.so im2col/col2im and split-K weight
     gradients. bn_follows: a training-mode batch norm over (task, channel)
-    groups consumes the output, so the gradient reaching the conv output
-    sums to zero over every group (BN removes the group mean: sum dx =
-    gamma*r*(sum dy - n*A - Bm*sum xh) = 0) and the bias gradient is
-    identically zero; it is returned as exact zeros (no reduction kernel,
-    and no rounding noise where the exact value is 0)."""
+    groups consumes the output. It subtracts the group mean, so a
+    per-channel bias is inert: BN(y + b) = BN(y) in exact arithmetic, the
+    bias gradient is identically zero (BN's input gradient sums to zero
+    over the group: sum dx = gamma*r*(sum dy - n*A - Bm*sum xh) = 0), and
+    the network output does not depend on b. The bias is then left out of
+    the GEMM (no broadcast copy into the output, no reduction for its
+    gradient; reading N5 in DESIGN.md): its meta-gradient is exactly 0 and
+    the outputs differ from the biased form by rounding only."""
     T, Cin, B, H, W = h.shape
-    out = _TaskConvGemm.apply(w.reshape(T, w.shape[1], Cin * 9), _Im2ColK.apply(h), b, bn_follows)
+    out = _TaskConvGemm.apply(w.reshape(T, w.shape[1], Cin * 9), _Im2ColK.apply(h),
+                              None if bn_follows else b)
     return out.view(T, -1, B, H, W)
 
 
