@@ -259,6 +259,17 @@ def test_maml_meta_gradient_fp32_accuracy(pkg, batched, net):
     err = float((mg.double() - mg64).norm() / mg64.norm())
     assert err < 2e-4, err
     assert float(loss) == pytest.approx(float(loss64), rel=1e-5)
+    # reading N5: the conv biases feed batch norms, so their meta-gradient is
+    # 0 (float64: rounding-sized); the task-batched fused network leaves
+    # them out and returns exact zeros
+    offs = [0]
+    for shp in maml.CONV4_SHAPES:
+        offs.append(offs[-1] + int(torch.Size(shp).numel()))
+    for leaf in (1, 5, 9, 13):
+        blk64 = mg64[offs[leaf]:offs[leaf + 1]]
+        assert float(blk64.abs().max()) <= 1e-9 * float(mg64.norm())
+        if batched and net == "fused":
+            assert not mg[offs[leaf]:offs[leaf + 1]].any()
 
 
 @pytest.mark.parametrize("net", ["gemm", "fused"])

@@ -158,6 +158,35 @@ def test_second_derivative_wrt_beta_is_zero():
     assert gb is None or float(gb.abs().max()) < 1e-10
 
 
+def test_conv_bias_before_batch_norm_is_inert():
+    """Reading N5: the fused network leaves the conv bias out
+    because a training-mode batch norm follows. In float64 with PyTorch's
+    own conv2d and batch_norm: the block's output with and without a
+    per-channel bias agrees to rounding, and the first and second
+    derivatives w.r.t. the bias vanish (BN's input gradient sums to zero
+    over every channel group)."""
+    g = torch.Generator().manual_seed(11)
+    x = torch.randn(6, 3, 10, 10, generator=g, dtype=torch.float64)
+    w = torch.randn(4, 3, 3, 3, generator=g, dtype=torch.float64, requires_grad=True)
+    b = (3 * torch.randn(4, generator=g, dtype=torch.float64)).requires_grad_(True)
+    gam = (torch.rand(4, generator=g, dtype=torch.float64) + 0.5).requires_grad_(True)
+    bet = torch.randn(4, generator=g, dtype=torch.float64, requires_grad=True)
+
+    def net(bias):
+        y = F.conv2d(x, w, bias, padding=1)
+        z = F.batch_norm(y, None, None, gam, bet, training=True, eps=EPS)
+        return F.relu(F.max_pool2d(z, 2))
+
+    out_b, out_0 = net(b), net(None)
+    torch.testing.assert_close(out_b, out_0, rtol=0, atol=1e-12)
+    dp = torch.randn(out_b.shape, generator=g, dtype=torch.float64)
+    gw, gb = torch.autograd.grad(out_b, (w, b), dp, create_graph=True)
+    assert float(gb.abs().max()) < 1e-11 * float(dp.abs().sum())
+    (ggb,) = torch.autograd.grad((gw * torch.randn(gw.shape, generator=g, dtype=torch.float64))
+                                 .sum(), (b,), allow_unused=True)
+    assert ggb is None or float(ggb.abs().max()) < 1e-9
+
+
 # ------------------------------------------------------------- the library
 def declared():
     src = open(os.path.join(ROOT, "include", "mamlnet.h")).read()
