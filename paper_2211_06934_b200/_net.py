@@ -13,7 +13,8 @@ import os
 from ._lib import _ptr, _stream
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmamlnet.so")
+# MAMLNET_LIB: load another build of the same ABI (A/B kernel experiments, tools/)
+LIB_PATH = os.environ.get("MAMLNET_LIB") or os.path.join(HERE, "libmamlnet.so")
 NET_OK = 0
 
 EXPORTS = ["net_im2col3x3", "net_col2im3x3", "net_bnpool_fwd", "net_bnpool_bwd",

@@ -108,7 +108,10 @@ def test_bnpool_second_derivative_partial_cotangents(maml):
 
 
 @pytest.mark.parametrize("geo", [(2, 1, 5, 28, 28), (2, 64, 5, 14, 14), (3, 4, 2, 7, 7),
-                                 (2, 64, 3, 3, 3), (1, 2, 1, 1, 5)])
+                                 (2, 64, 3, 3, 3), (1, 2, 1, 1, 5),
+                                 # n % 4 == 0 (float4 im2col) with 4-runs crossing rows and
+                                 # images: HW = 15, and H = 1 (the row index wraps at once)
+                                 (2, 3, 4, 3, 5), (1, 2, 4, 1, 3)])
 def test_im2col_col2im(maml, geo):
     gen = torch.Generator(device=DEV).manual_seed(6)
     h = torch.randn(geo, device=DEV, generator=gen)
