@@ -732,10 +732,21 @@ constexpr int kSmemCap = 64 * 1024;  // per-CTA slice budget (>= 3 CTAs per SM)
 
 // CTAs per group (cluster size): enough groups-x-slices to give every SM
 // ~8 CTAs, each slice >= 1024 elements; portable cluster sizes 1, 2, 4, 8.
+// Also split groups larger than kSliceCap elements (the 28x28 layer's
+// 19,600 at 25 images) so 32-task grids end in a finer last wave: 2 CTAs
+// per group measured 128 vs 137 us (backward), 172 vs 182 us (second
+// derivative); smaller slices lose more to the cluster reduction
+// (profiles/r01f_bn_slice_sweep.txt). NET_BN_SLICE overrides (0 = off).
+constexpr int64_t kSliceCap = 16384;
 int cluster_for(int64_t G, int64_t n) {
+  static const int64_t slice_cap = [] {
+    const char* e = getenv("NET_BN_SLICE");
+    return e ? (int64_t)atoll(e) : kSliceCap;
+  }();
   const int64_t want = 148 * 8;
   int kc = 1;
-  while (kc < 8 && G * kc < want && n / (2 * kc) >= 1024) kc *= 2;
+  while (kc < 8 && ((G * kc < want && n / (2 * kc) >= 1024) || (slice_cap > 0 && n / kc > slice_cap)))
+    kc *= 2;
   return kc;
 }
 
