@@ -295,3 +295,33 @@ def test_tc_gemm_network_path_meta_gradient(maml):
     finally:
         maml.USE_TC = old
     assert errs[True] < max(3 * errs[False], 2e-5), errs
+
+
+@pytest.mark.parametrize("geo,second_order", [((32, 64, 25, 28, 28), True),
+                                              ((32, 64, 75, 28, 28), False)])
+def test_bnpool_full_size_32_tasks(maml, geo, second_order):
+    """The 28x28 layer at the bench's 32 tasks (2048 groups of 19,600 /
+    58,800 elements: groups above 16K elements are split over 2 / 4-CTA
+    clusters, the finer-last-wave plan): forward, VJP and (support size)
+    VJP-of-VJP against the float64 composition, computed on the GPU."""
+    gen = torch.Generator(device=DEV).manual_seed(8)
+    T, C, B, H, W = geo
+    x = torch.randn(geo, device=DEV, generator=gen, dtype=torch.float64) * 2 + 0.5
+    gamma = torch.rand(T, C, device=DEV, generator=gen, dtype=torch.float64) + 0.5
+    beta = torch.randn(T, C, device=DEV, generator=gen, dtype=torch.float64) * 0.3
+    dp = torch.randn(T, C, B, H // 2, W // 2, device=DEV, generator=gen, dtype=torch.float64)
+    gdx = torch.randn(geo, device=DEV, generator=gen, dtype=torch.float64)
+
+    def run(fn, dt):
+        xx, gg, bb, dd = (t.to(dt).requires_grad_(True) for t in (x, gamma, beta, dp))
+        out = fn(xx, gg, bb)
+        dx, dg, db = torch.autograd.grad(out, (xx, gg, bb), dd, create_graph=second_order)
+        res = [out.detach(), dx.detach(), dg.detach(), db.detach()]
+        if second_order:
+            res += list(torch.autograd.grad((dx * gdx.to(dt)).sum(), (dd, xx, gg)))
+        return res
+
+    got = run(maml._BnPool.apply, torch.float32)
+    ref = run(ref_block, torch.float64)
+    for a, b in zip(got, ref):
+        close(a, b, tol=5e-5)
