@@ -345,12 +345,20 @@ class _ConvBwd(torch.autograd.Function):
     by the second-order meta-gradient) writes the cotangent of dy with two
     accumulating GEMMs, d_dy = gb_bar + gw_bar cols + w gcols_bar, instead of
     three autograd nodes whose contributions are summed by separate
-    elementwise adds over the dy-sized tensor."""
+    elementwise adds over the dy-sized tensor.
+
+    cols enters as a plain (detached) tensor and h, the image cols was
+    built from, as the differentiable input: the cotangent gw_bar reaches
+    h as col2im(gw_bar^T dy), so autograd adds it to the conv's other
+    contribution (col2im of w^T dy_meta through the im2col node) on h, 9x
+    smaller than cols, instead of summing the two 9x-expanded cols
+    cotangents (col2im is linear: the same sum, one add of |h| elements)."""
 
     @staticmethod
-    def forward(ctx, dy, w, cols, need_w, need_cols, need_b):
+    def forward(ctx, dy, w, cols, h, need_w, need_cols, need_b, hshape):
         ctx.save_for_backward(dy, w, cols)
         ctx.set_materialize_grads(False)  # unused outputs: no GEMMs on zero cotangents
+        ctx.hshape = hshape
         gw = _wgrad_fwd(dy, cols) if need_w else None
         gc = torch.bmm(w.transpose(1, 2), dy) if need_cols else None
         gb = dy.sum(-1) if need_b else None
@@ -360,7 +368,7 @@ class _ConvBwd(torch.autograd.Function):
     @torch.autograd.function.once_differentiable
     def backward(ctx, ggw, ggc, ggb):
         dy, w, cols = ctx.saved_tensors
-        d_dy = d_w = d_cols = None
+        d_dy = d_w = d_h = None
         if ctx.needs_input_grad[0]:
             bias = ggb.unsqueeze(-1) if ggb is not None else None
             pairs = ([(ggw, cols)] if ggw is not None else []) + ([(w, ggc)] if ggc is not None else [])
@@ -373,27 +381,31 @@ class _ConvBwd(torch.autograd.Function):
                 d_dy = bias.expand(dy.shape).contiguous() if bias is not None else None
         if ctx.needs_input_grad[1] and ggc is not None:
             d_w = _wgrad_fwd(dy, ggc)
-        if ctx.needs_input_grad[2] and ggw is not None:
-            d_cols = torch.bmm(ggw.transpose(1, 2), dy)
-        return d_dy, d_w, d_cols, None, None, None
+        if ctx.needs_input_grad[3] and ggw is not None:
+            d_h = _Col2ImK.apply(torch.bmm(ggw.transpose(1, 2), dy), ctx.hshape)
+        return d_dy, d_w, None, d_h, None, None, None, None
 
 
 class _TaskConvGemm(torch.autograd.Function):
     """bias + w @ cols for the task-batched convolution (cuBLAS batched
     SGEMM); backward: one _ConvBwd node (weight gradient through the
     split-K kernel or cuBLAS, input gradient, bias gradient), differentiable
-    once for the second-order meta-gradient."""
+    once for the second-order meta-gradient. h: the image cols = im2col(h)
+    was built from (not read here; handed to _ConvBwd as its differentiable
+    image input)."""
 
     @staticmethod
-    def forward(ctx, w, cols, bias):
-        ctx.save_for_backward(w, cols)
+    def forward(ctx, w, cols, bias, h):
+        ctx.save_for_backward(w, cols, h)
         return _conv_fwd(w, cols, bias)
 
     @staticmethod
     def backward(ctx, dy):
-        w, cols = ctx.saved_tensors
+        w, cols, h = ctx.saved_tensors
         nw, nc, nb = ctx.needs_input_grad[:3]
-        return _ConvBwd.apply(dy.contiguous(), w, cols, nw, nc, nb)
+        gw, gc, gb = _ConvBwd.apply(dy.contiguous(), w, cols.detach(), h, nw, nc, nb,
+                                    tuple(h.shape))
+        return gw, gc, gb, None
 
 
 def _conv3x3_tasks_fused(h, w, b, bn_follows=False):
@@ -409,7 +421,7 @@ def _conv3x3_tasks_fused(h, w, b, bn_follows=False):
     the outputs differ from the biased form by rounding only."""
     T, Cin, B, H, W = h.shape
     out = _TaskConvGemm.apply(w.reshape(T, w.shape[1], Cin * 9), _Im2ColK.apply(h),
-                              None if bn_follows else b)
+                              None if bn_follows else b, h)
     return out.view(T, -1, B, H, W)
 
 
