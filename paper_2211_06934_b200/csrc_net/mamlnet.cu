@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(256, 6) bnpool_fwd_kernel(int B, int H, int W,
   }
 }
 
-__global__ void __launch_bounds__(256, 6) bnpool_bwd_kernel(int B, int H, int W, const float* __restrict__ dp,
+__global__ void __launch_bounds__(256, 8) bnpool_bwd_kernel(int B, int H, int W, const float* __restrict__ dp,
                                   const uint8_t* __restrict__ code, const float* __restrict__ x,
                                   const float* __restrict__ gamma, const float* __restrict__ mean,
                                   const float* __restrict__ rstd, float* __restrict__ dx,
