@@ -163,7 +163,10 @@ def test_fused_network_forward_equals_gemm_form(maml):
 
 @pytest.mark.parametrize("shape", [(4, 64, 576, 14700), (32, 64, 576, 4900), (3, 64, 9, 58800),
                                    (2, 5, 7, 33), (1, 64, 576, 1), (2, 70, 130, 1000),
-                                   (4, 64, 576, 225)])
+                                   (4, 64, 576, 225),
+                                   # 64 x 9 (first conv layer's weight gradient): many splits,
+                                   # one split (straight to C), ragged n
+                                   (32, 64, 9, 19600), (1, 64, 9, 100), (2, 64, 9, 33)])
 def test_gemm_nt_against_float64(maml, shape):
     """net_gemm_nt (split-K fp32) vs the float64 product; ragged tiles,
     N not a multiple of the k-chunk, several split counts; deterministic."""
