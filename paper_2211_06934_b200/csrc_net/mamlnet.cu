@@ -344,7 +344,12 @@ __global__ void __launch_bounds__(256, 8) bnpool_bwd_kernel(int B, int H, int W,
   }
 }
 
-__global__ void __launch_bounds__(256, 6) bnpool_bwd2_kernel(int B, int H, int W, const float* __restrict__ gdx,
+// MINB: 8 resident blocks for per-CTA slices of 2K-8K elements, else 6 (8 is
+// faster on the 4.9K-element slices -- 14x14 at 32 tasks, 28x28 at 4 --
+// slower on the 28x28 layer's 9.8K slices at 32 tasks and on the 7x7
+// layer's 1.2K: profiles/r01f_bn_minblocks_sweep.txt, r01f_bn_bwd2_minb.txt)
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) bnpool_bwd2_kernel(int B, int H, int W, const float* __restrict__ gdx,
                                    const float* __restrict__ gdgamma, const float* __restrict__ gdbeta,
                                    const float* __restrict__ dp, const uint8_t* __restrict__ code,
                                    const float* __restrict__ x, const float* __restrict__ gamma,
@@ -867,9 +872,12 @@ int net_bnpool_bwd2(int64_t G, int64_t B, int64_t H, int64_t W, const float* gdx
   if (!dp || !code || !x || !gamma || !mean || !rstd || !dgamma || !dbeta || !g_dp || !g_x ||
       !g_gamma)
     return fail("net_bnpool_bwd2: NULL pointer");
-  return launch_group_kernel(bnpool_bwd2_kernel, G, B * H * W, (cudaStream_t)stream, (int)B,
-                             (int)H, (int)W, gdx, gdgamma, gdbeta, dp, code, x, gamma, mean, rstd,
-                             dgamma, dbeta, g_dp, g_x, g_gamma);
+  const int kc = cluster_for(G, B * H * W);
+  const int64_t slice = B * H * W / kc;
+  auto* kernel = slice > 2048 && slice <= 8192 ? bnpool_bwd2_kernel<8> : bnpool_bwd2_kernel<6>;
+  return launch_clustered(kernel, G, kc, 0, (cudaStream_t)stream, (int)B, (int)H, (int)W, gdx,
+                          gdgamma, gdbeta, dp, code, x, gamma, mean, rstd, dgamma, dbeta, g_dp, g_x,
+                          g_gamma);
 }
 
 size_t net_gemm_nt_workspace_bytes(int64_t T, int64_t M, int64_t P, int64_t N) {
