@@ -297,15 +297,17 @@ def sweep_forward_complex(kind, a, theta0, phi, K, hp, nesterov=False):
 def _mag_lib():
     L = lib()
     P, i64, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
-    L.oracle_adam_mag.argtypes = [i64, i64, P, I, P, P, P, P, P, P, P, P]
-    L.oracle_rmsprop_mag.argtypes = [i64, P, I, P, P, P, P, P, P]
-    L.oracle_sgd_mag.argtypes = [i64, P, I, P, P, P, P, P, P]
+    L.oracle_adam_mag.argtypes = [i64, i64, P, I, P, P, P, P, P, P, P, P, P]
+    L.oracle_rmsprop_mag.argtypes = [i64, P, I, P, P, P, P, P, P, P]
+    L.oracle_sgd_mag.argtypes = [i64, P, I, P, P, P, P, P, P, P]
+    L.oracle_ex_mag.argtypes = [I, i64, i64, P, P, P, i64, P, I] + [P] * 10
     return L
 
 
 def adam_mag(g, m, v, du, dm1, dv1, t, lr, b1, b2, eps, eps_root=0.0, state_bf16=False):
     """Magnitude twins (fp32 error scales, reading Z10) of u, m', v', dg, dm,
-    dv and of the four hyper-gradient sums (Sigma of per-element scales)."""
+    dv, of the four hyper-gradient terms per element ('h', 4 x n) and of
+    their sums ('dhp', Sigma of the per-element scales)."""
     g = _f32(g)
     n = g.size
     m, v = _state(m, state_bf16), _state(v, state_bf16)
@@ -313,10 +315,11 @@ def adam_mag(g, m, v, du, dm1, dv1, t, lr, b1, b2, eps, eps_root=0.0, state_bf16
     hp = _hp([lr, b1, b2, eps, eps_root])
     out = np.empty(6 * n)
     hs = np.zeros(4)
+    he = np.empty(4 * n)
     _mag_lib().oracle_adam_mag(n, int(t), _p(hp), int(state_bf16), _p(g), _p(m), _p(v), _p(du),
-                               _p(dm1), _p(dv1), _p(out), _p(hs))
+                               _p(dm1), _p(dv1), _p(out), _p(hs), _p(he))
     o = out.reshape(6, n)
-    return dict(u=o[0], m1=o[1], v1=o[2], dg=o[3], dm=o[4], dv=o[5], dhp=hs)
+    return dict(u=o[0], m1=o[1], v1=o[2], dg=o[3], dm=o[4], dv=o[5], dhp=hs, h=he.reshape(4, n))
 
 
 def rmsprop_mag(g, v, du, dv1, lr, alpha, eps, state_bf16=False):
@@ -327,10 +330,11 @@ def rmsprop_mag(g, v, du, dv1, lr, alpha, eps, state_bf16=False):
     hp = _hp([lr, alpha, eps])
     out = np.empty(4 * n)
     hs = np.zeros(3)
+    he = np.empty(3 * n)
     _mag_lib().oracle_rmsprop_mag(n, _p(hp), int(state_bf16), _p(g), _p(v), _p(du), _p(dv1),
-                                  _p(out), _p(hs))
+                                  _p(out), _p(hs), _p(he))
     o = out.reshape(4, n)
-    return dict(u=o[0], v1=o[1], dg=o[2], dv=o[3], dhp=hs)
+    return dict(u=o[0], v1=o[1], dg=o[2], dv=o[3], dhp=hs, h=he.reshape(3, n))
 
 
 def sgd_mag(g, b, du, db1, lr, momentum, nesterov=False, state_bf16=False):
@@ -341,10 +345,11 @@ def sgd_mag(g, b, du, db1, lr, momentum, nesterov=False, state_bf16=False):
     hp = _hp([lr, momentum, 1.0 if nesterov else 0.0])
     out = np.empty(4 * n)
     hs = np.zeros(2)
+    he = np.empty(2 * n)
     _mag_lib().oracle_sgd_mag(n, _p(hp), int(state_bf16), _p(g), _p(b), _p(du), _p(db1), _p(out),
-                              _p(hs))
+                              _p(hs), _p(he))
     o = out.reshape(4, n)
-    return dict(u=o[0], b1=o[1], dg=o[2], db=o[3], dhp=hs)
+    return dict(u=o[0], b1=o[1], dg=o[2], db=o[3], dhp=hs, h=he.reshape(2, n))
 
 
 # ------------------------------------------- optimizer variants (NEXT-1)
@@ -545,7 +550,7 @@ def _cm_lib():
     P, i64, I, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
     L.oracle_rmsprop_cm_fwd.argtypes = [i64, P, P, P, i64, P, I, I] + [P] * 9
     L.oracle_rmsprop_cm_vjp.argtypes = [i64, P, P, P, i64, P, I, I] + [P] * 17
-    L.oracle_rmsprop_cm_mag.argtypes = [i64, P, P, P, i64, P, I] + [P] * 11
+    L.oracle_rmsprop_cm_mag.argtypes = [i64, P, P, P, i64, P, I] + [P] * 12
     L.oracle_rmsprop_cm_fwd_cplx.argtypes = [i64, P, P, I, D, D, I] + [P] * 20
     L._cm_ready = True
     return L
@@ -604,15 +609,17 @@ def rmsprop_cm_mag(g, v, a, b, theta, du, dv1, da1, db1, lr, alpha, eps, momentu
     lrl, nl, off = _leaf_args(lr_leaf, offsets)
     out = np.empty(9 * n)
     hs = np.zeros(5)
+    he = np.empty(5 * n)
     _cm_lib().oracle_rmsprop_cm_mag(n, _p(_cm_hp(lr, alpha, eps, momentum, centered)),
                                     _p(_ext(weight_decay, False, maximize)), _p(lrl), nl,
                                     _p(off), int(state_bf16), _p(g), _p(v), _p(a), _p(b),
                                     _p(theta), _p(du), _p(dv1), _p(da1), _p(db1), _p(out),
-                                    _p(hs))
+                                    _p(hs), _p(he))
     o = out.reshape(9, n)
     keys = ("u", "v1", "a1", "b1", "dg", "dv", "da", "db", "dtheta")
     r = {k: o[i] for i, k in enumerate(keys)}
     r["dhp"] = hs
+    r["h"] = he.reshape(5, n)
     return r
 
 
@@ -635,47 +642,40 @@ def rmsprop_cm_fwd_complex(g, v, a, b, theta, hp, lr_elem, centered=False, weigh
 
 def ex_mag(kind, g, state, theta, du, ds1, dv1=None, t=1, hp=(), weight_decay=0.0,
            decoupled=False, maximize=False, lr_leaf=None, offsets=None, state_bf16=False):
-    """Magnitude twins (Z10) of the variant outputs: the base twins evaluated
-    at |g~| <= |g| + wd |theta| (the rounding scale of the decayed gradient)
-    with each element's lr, plus the weight-decay terms. ``state`` is
-    (m, v) for adam, the single state array otherwise. Returns arrays keyed
-    like the base twins plus 'dtheta', 'dwd' and 'extra_lr' (per element)."""
-    g64 = _f32(g).astype(np.float64)
-    th = np.abs(_f32(theta).astype(np.float64))
-    n = g64.size
-    if lr_leaf is not None:
-        lr_e = np.repeat(np.asarray(lr_leaf, np.float64), np.diff(np.asarray(offsets)))
+    """Magnitude twins (Z10) of the variant outputs (oracle.hpp ``ex_mag``):
+    the base twins at the decayed gradient (its value in denominators, the
+    magnitude |g| + wd |theta| in numerators) with each element's lr, plus
+    the weight-decay terms. ``state`` is (m, v) for adam, the single state
+    array otherwise; ``hp`` the base hyper-parameters. Returns the output
+    twins keyed like the base twins plus 'dtheta', the hyper twins per
+    element ('h', nh x n: adam lr, b1, b2, eps, wd; rmsprop lr, alpha, eps,
+    wd; sgd lr, mu, wd) and their sums ('dhp')."""
+    g, theta = _f32(g), _f32(theta)
+    n = g.size
+    k = {"adam": 0, "rmsprop": 1, "sgd": 2}[kind]
+    s0, s1 = (state if kind == "adam" else (state, None))
+    s0, s1 = _state(s0, state_bf16), _state(s1, state_bf16)
+    du, ds1_, dv1_ = _f32(du), _f32(ds1), _f32(dv1)
+    if kind == "adam":
+        hv = _hp(list(hp) + [0.0] * (5 - len(hp)))
     else:
-        lr_e = np.full(n, float(hp[0]))
-    gmag = np.abs(g64) + weight_decay * th
-    sub = lambda a, sel: None if a is None else np.asarray(a)[sel]
-    base = {}
-    for lr in np.unique(lr_e):
-        sel = lr_e == lr
-        if kind == "adam":
-            b = adam_mag(gmag[sel], sub(state[0], sel), sub(state[1], sel), du[sel], sub(ds1, sel),
-                         sub(dv1, sel), t, lr, *hp[1:], state_bf16=state_bf16)
-        elif kind == "rmsprop":
-            b = rmsprop_mag(gmag[sel], sub(state, sel), du[sel], sub(ds1, sel), lr, *hp[1:],
-                            state_bf16=state_bf16)
-        else:
-            b = sgd_mag(gmag[sel], sub(state, sel), du[sel], sub(ds1, sel), lr, *hp[1:],
-                        state_bf16=state_bf16)
-        for k, val in b.items():
-            if k != "dhp":
-                base.setdefault(k, np.zeros(n))[sel] = val
-    adu = np.abs(_f32(du).astype(np.float64))
-    out = dict(base)
-    if kind == "adam" and decoupled:
-        out["u"] = base["u"] + np.abs(lr_e) * weight_decay * th
-        out["dtheta"] = np.abs(lr_e) * weight_decay * adu
-        out["dwd"] = adu * np.abs(lr_e) * th
-        out["extra_lr"] = adu * weight_decay * th
-    else:
-        out["dtheta"] = weight_decay * base["dg"]
-        out["dwd"] = base["dg"] * th
-        out["extra_lr"] = np.zeros(n)
-    return out
+        hv = _hp([hp[0], hp[1], float(hp[2]) if len(hp) > 2 else 0.0, 0.0, 0.0])
+    lrl, nl, off = _leaf_args(lr_leaf, offsets)
+    nh = (5, 4, 3)[k]
+    out = np.empty(7 * n)
+    hs = np.zeros(5)
+    he = np.empty(nh * n)
+    _mag_lib().oracle_ex_mag(k, n, int(t), _p(hv), _p(_ext(weight_decay, decoupled, maximize)),
+                             _p(lrl), nl, _p(off), int(state_bf16), _p(g), _p(s0), _p(s1),
+                             _p(theta), _p(du), _p(ds1_), _p(dv1_), _p(out), _p(hs), _p(he))
+    o = out.reshape(7, n)
+    names = {"adam": ("u", "m1", "v1", "dg", "dm", "dv"), "rmsprop": ("u", "v1", None, "dg", "dv", None),
+             "sgd": ("u", "b1", None, "dg", "db", None)}[kind]
+    r = {nm: o[i] for i, nm in enumerate(names) if nm is not None}
+    r["dtheta"] = o[6]
+    r["h"] = he.reshape(nh, n)
+    r["dhp"] = hs[:nh]
+    return r
 
 
 # ------------------------------------------------ zero-order ES (NEXT-3)

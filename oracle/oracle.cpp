@@ -578,7 +578,7 @@ extern "C" {
 
 void oracle_adam_mag(int64_t n, int64_t t, const double* hp, int bf, const float* g,
                      const void* m, const void* v, const float* du, const float* dm1,
-                     const float* dv1, double* out, double* hsum) {
+                     const float* dv1, double* out, double* hsum, double* h_elem) {
   const AdamHP<double> h = adam_hp<double>(hp);
   long double hs[4] = {0, 0, 0, 0};
   for (int64_t i = 0; i < n; ++i) {
@@ -587,12 +587,15 @@ void oracle_adam_mag(int64_t n, int64_t t, const double* hp, int bf, const float
     const double o[6] = {r.u, r.m1, r.v1, r.dg, r.dm, r.dv};
     for (int k = 0; k < 6; ++k) out[k * n + i] = o[k];
     for (int k = 0; k < 4; ++k) hs[k] += r.h[k];
+    if (h_elem)
+      for (int k = 0; k < 4; ++k) h_elem[k * n + i] = r.h[k];
   }
   for (int k = 0; k < 4; ++k) hsum[k] = (double)hs[k];
 }
 
 void oracle_rmsprop_mag(int64_t n, const double* hp, int bf, const float* g, const void* v,
-                        const float* du, const float* dv1, double* out, double* hsum) {
+                        const float* du, const float* dv1, double* out, double* hsum,
+                        double* h_elem) {
   const RmsHP<double> h = rms_hp<double>(hp);
   long double hs[3] = {0, 0, 0};
   for (int64_t i = 0; i < n; ++i) {
@@ -600,12 +603,15 @@ void oracle_rmsprop_mag(int64_t n, const double* hp, int bf, const float* g, con
     const double o[4] = {r.u, r.v1, r.dg, r.dv};
     for (int k = 0; k < 4; ++k) out[k * n + i] = o[k];
     for (int k = 0; k < 3; ++k) hs[k] += r.h[k];
+    if (h_elem)
+      for (int k = 0; k < 3; ++k) h_elem[k * n + i] = r.h[k];
   }
   for (int k = 0; k < 3; ++k) hsum[k] = (double)hs[k];
 }
 
 void oracle_sgd_mag(int64_t n, const double* hp, int bf, const float* g, const void* b,
-                    const float* du, const float* db1, double* out, double* hsum) {
+                    const float* du, const float* db1, double* out, double* hsum,
+                    double* h_elem) {
   const SgdHP<double> h = sgd_hp<double>(hp);
   long double hs[2] = {0, 0};
   for (int64_t i = 0; i < n; ++i) {
@@ -613,6 +619,8 @@ void oracle_sgd_mag(int64_t n, const double* hp, int bf, const float* g, const v
     const double o[4] = {r.u, r.b1, r.dg, r.db};
     for (int k = 0; k < 4; ++k) out[k * n + i] = o[k];
     for (int k = 0; k < 2; ++k) hs[k] += r.h[k];
+    if (h_elem)
+      for (int k = 0; k < 2; ++k) h_elem[k * n + i] = r.h[k];
   }
   for (int k = 0; k < 2; ++k) hsum[k] = (double)hs[k];
 }
@@ -977,7 +985,7 @@ void oracle_rmsprop_cm_mag(int64_t n, const double* hp, const double* ext,
                            const double* lr_leaf, int64_t nl, const int64_t* off, int bf,
                            const float* g, const void* v, const void* a, const void* b,
                            const float* th, const float* du, const float* dv1, const float* da1,
-                           const float* db1, double* out, double* hsum) {
+                           const float* db1, double* out, double* hsum, double* h_elem) {
   oracle::ExHP<double> x = ex_hp<double>(ext);
   x.decoupled = 0;
   long double hs[5] = {0, 0, 0, 0, 0};
@@ -990,8 +998,40 @@ void oracle_rmsprop_cm_mag(int64_t n, const double* hp, const double* ext,
     const double o[9] = {r.u, r.v1, r.a1, r.b1, r.dg, r.dv, r.da, r.db, r.dtheta};
     for (int k = 0; k < 9; ++k) out[k * n + i] = o[k];
     for (int k = 0; k < 5; ++k) hs[k] += r.h[k];
+    if (h_elem)
+      for (int k = 0; k < 5; ++k) h_elem[k * n + i] = r.h[k];
   });
   for (int k = 0; k < 5; ++k) hsum[k] = (double)hs[k];
+}
+
+// Magnitude twins of the *_ex variants (oracle::ex_mag): kind 0 adam
+// (hp = lr, b1, b2, eps, eps_root), 1 rmsprop (lr, alpha, eps), 2 sgd (lr,
+// mu, nesterov). out[k*n + i] for k = u, s0', s1', dg, ds0, ds1, dtheta;
+// hsum / h_elem[k*n + i] for the hyper slots (adam: lr, b1, b2, eps, wd;
+// rmsprop: lr, alpha, eps, wd; sgd: lr, mu, wd).
+void oracle_ex_mag(int kind, int64_t n, int64_t t, const double* hp, const double* ext,
+                   const double* lr_leaf, int64_t nl, const int64_t* off, int bf, const float* g,
+                   const void* s0, const void* s1, const float* th, const float* du,
+                   const float* ds0, const float* ds1, double* out, double* hsum,
+                   double* h_elem) {
+  const oracle::ExHP<double> x = ex_hp<double>(ext);
+  const int nh = kind == 0 ? 5 : kind == 1 ? 4 : 3;
+  long double hs[5] = {0, 0, 0, 0, 0};
+  per_leaf_elements(n, nl, off, [&](int64_t i, int64_t l) {
+    double hh[5];
+    for (int k = 0; k < 5; ++k) hh[k] = k < (kind == 0 ? 5 : 3) ? hp[k] : 0.0;
+    if (lr_leaf) hh[0] = lr_leaf[l];
+    auto r = oracle::ex_mag(kind, f32_in(g, i), state_in(s0, bf, i), state_in(s1, bf, i),
+                            f32_in(th, i), f32_in(du, i), f32_in(ds0, i), f32_in(ds1, i), hh, x,
+                            t);
+    const double o[7] = {r.u, r.s0, r.s1, r.dg, r.ds0, r.ds1, r.dtheta};
+    for (int k = 0; k < 7; ++k) out[k * n + i] = o[k];
+    for (int k = 0; k < nh; ++k) {
+      hs[k] += r.h[k];
+      if (h_elem) h_elem[k * n + i] = r.h[k];
+    }
+  });
+  for (int k = 0; k < nh; ++k) hsum[k] = (double)hs[k];
 }
 
 // Complex forward (complex-step pins); per-ELEMENT lr; hp_re/hp_im[4] =

@@ -255,22 +255,31 @@ struct AdamMag {
   double u, m1, v1, dg, dm, dv, h[4];
 };
 
-inline AdamMag adam_mag(double g, double m, double v, double du, double dm1, double dv1,
-                        const AdamHP<double>& h, int64_t t) {
+// gt is the gradient value fed to the moments (denominators keep their
+// values, so s and d use it); agt is its magnitude twin: |g| for the plain
+// step, |g| + wd |theta| when L2 weight decay forms gt = +-g + wd theta
+// (that sum's conditioning is charged like m' = b1 m + (1-b1) g in the
+// numerators and, through the Lipschitz factor below, in the denominators).
+inline AdamMag adam_mag2(double gt, double agt, double m, double v, double du, double dm1,
+                         double dv1, const AdamHP<double>& h, int64_t t) {
   const double b1 = h.b1, b2 = h.b2, lr = std::fabs(h.lr), eps = h.eps;
   const double bc1 = 1.0 - ipow(b1, t), bc2 = 1.0 - ipow(b2, t);
   const double A = (1 - b1) / bc1, C = (1 - b2) / bc2;
   const double P = b1 * m / bc1, Q = b2 * v / bc2 + h.eps_root;
-  const double s = std::sqrt(C * g * g + Q), d = s + eps;
-  const double rd = d == 0 ? 0 : 1 / d, rs = s == 0 ? 0 : 1 / s;
-  const double ag = std::fabs(g), adu = std::fabs(du);
+  const double s = std::sqrt(C * gt * gt + Q), d = s + eps;
+  // s is sqrt(C)-Lipschitz in gt; a cancelling gt (agt > |gt|) is known to
+  // the kernel only within its rounding, so 1/d and 1/s carry the factor
+  // 1 + sqrt(C) (agt - |gt|) / d (or / s); exactly 1 for the plain step.
+  const double ex = std::sqrt(C) * (agt - std::fabs(gt));
+  const double rd = d == 0 ? 0 : (1 + ex / d) / d, rs = s == 0 ? 0 : (1 + ex / s) / s;
+  const double ag = agt, g2 = agt * agt, adu = std::fabs(du);
   const double mh = A * ag + std::fabs(P);
   AdamMag r;
   r.m1 = b1 * std::fabs(m) + (1 - b1) * ag;
-  r.v1 = b2 * std::fabs(v) + (1 - b2) * g * g;
+  r.v1 = b2 * std::fabs(v) + (1 - b2) * g2;
   r.u = lr * mh * rd;
   r.dg = (1 - b1) * std::fabs(dm1) + 2 * (1 - b2) * ag * std::fabs(dv1) +
-         adu * lr * rd * rd * (A * eps + (A * std::fabs(Q) + std::fabs(P * C * g)) * rs);
+         adu * lr * rd * rd * (A * eps + (A * std::fabs(Q) + std::fabs(P * C) * ag) * rs);
   r.dm = b1 * (std::fabs(dm1) + adu * lr * rd / bc1);
   const double w = 0.5 * lr * mh * rd * rd * rs;
   r.dv = b2 * (std::fabs(dv1) + adu * w / bc2);
@@ -282,50 +291,61 @@ inline AdamMag adam_mag(double g, double m, double v, double du, double dm1, dou
   const double K4 = (1 - p2 - tt * ipow(b2, t - 1) * (1 - b2)) / (bc2 * bc2);
   r.h[0] = adu * mh * rd;
   r.h[1] = std::fabs(dm1) * (std::fabs(m) + ag) +
-           adu * lr * rd * (std::fabs(m * K1) + std::fabs(g * K2));
-  r.h[2] = std::fabs(dv1) * (std::fabs(v) + g * g) +
-           adu * w * (std::fabs(v * K3) + std::fabs(g * g * K4));
+           adu * lr * rd * (std::fabs(m * K1) + ag * std::fabs(K2));
+  r.h[2] = std::fabs(dv1) * (std::fabs(v) + g2) +
+           adu * w * (std::fabs(v * K3) + g2 * std::fabs(K4));
   r.h[3] = adu * lr * mh * rd * rd;
   return r;
+}
+
+inline AdamMag adam_mag(double g, double m, double v, double du, double dm1, double dv1,
+                        const AdamHP<double>& h, int64_t t) {
+  return adam_mag2(g, std::fabs(g), m, v, du, dm1, dv1, h, t);
 }
 
 struct RmsMag {
   double u, v1, dg, dv, h[3];
 };
 
-inline RmsMag rmsprop_mag(double g, double v, double du, double dv1, const RmsHP<double>& h) {
+inline RmsMag rmsprop_mag2(double gt, double agt, double v, double du, double dv1,
+                           const RmsHP<double>& h) {
   const double a = h.alpha, lr = std::fabs(h.lr), eps = h.eps;
-  const double s = std::sqrt(a * v + (1 - a) * g * g), d = s + eps;
-  const double rd = d == 0 ? 0 : 1 / d, rs = s == 0 ? 0 : 1 / s;
-  const double ag = std::fabs(g), adu = std::fabs(du);
+  const double s = std::sqrt(a * v + (1 - a) * gt * gt), d = s + eps;
+  const double ex = std::sqrt(1 - a) * (agt - std::fabs(gt));  // as adam_mag2
+  const double rd = d == 0 ? 0 : (1 + ex / d) / d, rs = s == 0 ? 0 : (1 + ex / s) / s;
+  const double ag = agt, adu = std::fabs(du);
   RmsMag r;
-  r.v1 = a * std::fabs(v) + (1 - a) * g * g;
+  r.v1 = a * std::fabs(v) + (1 - a) * ag * ag;
   r.u = lr * ag * rd;
   r.dg = 2 * (1 - a) * ag * std::fabs(dv1) + adu * lr * rd * rd * (eps + a * std::fabs(v) * rs);
   const double w = 0.5 * lr * ag * rd * rd * rs;
   r.dv = a * (std::fabs(dv1) + adu * w);
   r.h[0] = adu * ag * rd;
-  r.h[1] = (std::fabs(dv1) + adu * w) * (std::fabs(v) + g * g);
+  r.h[1] = (std::fabs(dv1) + adu * w) * (std::fabs(v) + ag * ag);
   r.h[2] = adu * lr * ag * rd * rd;
   return r;
+}
+
+inline RmsMag rmsprop_mag(double g, double v, double du, double dv1, const RmsHP<double>& h) {
+  return rmsprop_mag2(g, std::fabs(g), v, du, dv1, h);
 }
 
 struct SgdMag {
   double u, b1, dg, db, h[2];
 };
 
-inline SgdMag sgd_mag(double g, double b, double du, double db1, const SgdHP<double>& h) {
+inline SgdMag sgd_mag2(double agt, double b, double du, double db1, const SgdHP<double>& h) {
   const double mu = h.mu, lr = std::fabs(h.lr);
-  const double ab1 = mu * std::fabs(b) + std::fabs(g);
+  const double ab1 = mu * std::fabs(b) + agt;
   const double adu = std::fabs(du), adb = std::fabs(db1);
   SgdMag r;
   r.b1 = ab1;
   if (h.nesterov) {
     const double B = adb + lr * mu * adu;
-    r.u = lr * (std::fabs(g) + mu * ab1);
+    r.u = lr * (agt + mu * ab1);
     r.dg = B + lr * adu;
     r.db = mu * B;
-    r.h[0] = adu * (std::fabs(g) + mu * ab1);
+    r.h[0] = adu * (agt + mu * ab1);
     r.h[1] = B * std::fabs(b) + adu * lr * ab1;
   } else {
     const double B = adb + lr * adu;
@@ -336,6 +356,10 @@ inline SgdMag sgd_mag(double g, double b, double du, double db1, const SgdHP<dou
     r.h[1] = B * std::fabs(b);
   }
   return r;
+}
+
+inline SgdMag sgd_mag(double g, double b, double du, double db1, const SgdHP<double>& h) {
+  return sgd_mag2(std::fabs(g), b, du, db1, h);
 }
 
 }  // namespace oracle
@@ -450,6 +474,60 @@ SgdVjpEx<T> sgd_vjp_ex(T g, T b, T theta, T du, T db1_out, const SgdHP<T>& h, co
   SgdVjp<T> c = sgd_vjp<T>(gt, b, du, db1_out, h);
   SgdVjpEx<T> r{x.maximize ? -c.dg : c.dg, c.db, c.dg * x.wd, c.dlr, c.dmu, c.dg * theta};
   return r;
+}
+
+
+// Magnitude twin (Z10) of the variants: the base twins at the gradient fed
+// to the moments, gt = (maximize ? -g : g) + wd theta (L2 decay; AdamW keeps
+// gt = +-g), with the magnitude |g| + wd |theta| in every numerator (the
+// conditioning of that sum, charged like m') and gt's value in every
+// denominator; plus the weight-decay terms over |.|. kind 0 adam (hp = lr,
+// b1, b2, eps, eps_root), 1 rmsprop (lr, alpha, eps), 2 sgd (lr, mu,
+// nesterov); s0/s1 = the state (m, v) / v / b and its cotangents. h[] =
+// (lr, b1, b2, eps, wd) / (lr, alpha, eps, wd) / (lr, mu, wd).
+struct ExMag {
+  double u, s0, s1, dg, ds0, ds1, dtheta, h[5];
+};
+
+inline ExMag ex_mag(int kind, double g, double s0, double s1, double theta, double du,
+                    double ds0, double ds1, const double* hp, const ExHP<double>& x, int64_t t) {
+  const double gm = x.maximize ? -g : g, ath = std::fabs(theta), adu = std::fabs(du);
+  const double lr = std::fabs(hp[0]);
+  const bool l2 = !(kind == 0 && x.decoupled);
+  const double gt = l2 ? gm + x.wd * theta : gm;
+  const double agt = l2 ? std::fabs(g) + x.wd * ath : std::fabs(g);
+  ExMag o{};
+  double dgmag = 0;
+  int nb = 0;  // number of base hyper slots (the wd slot follows them)
+  if (kind == 0) {
+    const AdamHP<double> h{hp[0], hp[1], hp[2], hp[3], hp[4]};
+    const AdamMag b = adam_mag2(gt, agt, s0, s1, du, ds0, ds1, h, t);
+    o.u = b.u, o.s0 = b.m1, o.s1 = b.v1, o.dg = b.dg, o.ds0 = b.dm, o.ds1 = b.dv;
+    for (int k = 0; k < 4; ++k) o.h[k] = b.h[k];
+    dgmag = b.dg, nb = 4;
+  } else if (kind == 1) {
+    const RmsHP<double> h{hp[0], hp[1], hp[2]};
+    const RmsMag b = rmsprop_mag2(gt, agt, s0, du, ds0, h);
+    o.u = b.u, o.s0 = b.v1, o.dg = b.dg, o.ds0 = b.dv;
+    for (int k = 0; k < 3; ++k) o.h[k] = b.h[k];
+    dgmag = b.dg, nb = 3;
+  } else {
+    const SgdHP<double> h{hp[0], hp[1], hp[2] != 0.0 ? 1 : 0};
+    const SgdMag b = sgd_mag2(agt, s0, du, ds0, h);
+    o.u = b.u, o.s0 = b.b1, o.dg = b.dg, o.ds0 = b.db;
+    for (int k = 0; k < 2; ++k) o.h[k] = b.h[k];
+    dgmag = b.dg, nb = 2;
+  }
+  if (l2) {  // gt = gm + wd theta: d/dwd = dgt theta, d/dtheta = dgt wd
+    o.h[nb] = dgmag * ath;
+    o.dtheta = x.wd * dgmag;
+  } else {   // AdamW: u += -lr wd theta
+    o.u += lr * x.wd * ath;
+    o.h[0] += adu * x.wd * ath;
+    o.h[nb] = adu * lr * ath;
+    o.dtheta = adu * lr * x.wd;
+  }
+  return o;
 }
 
 }  // namespace oracle
@@ -572,7 +650,10 @@ inline RmsCmMag rmsprop_cm_mag(double g, double v, double a, double b, double th
   const double a1 = h.centered ? al * a + om * gt : a;
   const double q = h.centered ? v1 - a1 * a1 : v1;
   const double r = q > 0 ? std::sqrt(q) : 0.0, d = r + eps;
-  const double rd = d == 0 ? 0 : 1 / d, rs = r == 0 ? 0 : 1 / r;
+  // r is L-Lipschitz in gt (L = sqrt(alpha (1-alpha)) centred, sqrt(1-alpha)
+  // otherwise): the conditioning of a cancelling gt, as adam_mag2
+  const double ex = std::sqrt(h.centered ? al * om : om) * (agt - std::fabs(gt));
+  const double rd = d == 0 ? 0 : (1 + ex / d) / d, rs = r == 0 ? 0 : (1 + ex / r) / r;
   RmsCmMag o;
   o.v1 = al * std::fabs(v) + om * agt * agt;
   o.a1 = h.centered ? al * std::fabs(a) + om * agt : std::fabs(a);

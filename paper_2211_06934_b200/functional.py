@@ -78,6 +78,49 @@ def _contig(t):
     return None if t is None else t.contiguous()
 
 
+def _cot(t):
+    """A cotangent as a contiguous float32 buffer. Autograd hands the VJP of a
+    bfloat16 state output a bfloat16 cotangent; the C ABI reads every
+    cotangent as float (diffopt.h), so it is widened here (exactly)."""
+    if t is None:
+        return None
+    if t.dtype != torch.float32:
+        t = t.float()
+    return t.contiguous()
+
+
+def _check_args(cfg, g, states=(), f32=(), lr_leaf=None):
+    """Validate what the kernels assume before raw pointers leave Python:
+    float32 CUDA buffers of exactly tree.numel elements on one device
+    (state may be bfloat16), lr_leaf float32 with one entry per leaf."""
+    n = cfg.tree.numel
+    if not isinstance(g, torch.Tensor) or not g.is_cuda:
+        raise TypeError("the gradient must be a CUDA tensor (there is no CPU path)")
+    if g.dtype != torch.float32:
+        raise TypeError(f"the gradient must be float32, got {g.dtype}")
+    if g.numel() != n:
+        raise ValueError(f"the gradient has {g.numel()} elements, the tree {n}")
+    d = cfg.tree.d_offsets
+    if d is not None and d.device != g.device:
+        raise ValueError(f"the tree's offsets live on {d.device}, the gradient on {g.device}")
+    for kind, ts in (("state", states), ("buffer", f32)):
+        for t in ts:
+            if t is None:
+                continue
+            if t.device != g.device:
+                raise ValueError(f"a {kind} tensor is on {t.device}, the gradient on {g.device}")
+            ok = (torch.float32, torch.bfloat16) if kind == "state" else (torch.float32,)
+            if t.dtype not in ok:
+                raise TypeError(f"a {kind} tensor has dtype {t.dtype}; allowed: {ok}")
+            if t.numel() != n:
+                raise ValueError(f"a {kind} tensor has {t.numel()} elements, the tree {n}")
+    if lr_leaf is not None:
+        if lr_leaf.device != g.device or lr_leaf.dtype != torch.float32:
+            raise TypeError("lr_leaf must be a float32 tensor on the gradient's device")
+        if lr_leaf.numel() != cfg.tree.n_leaves:
+            raise ValueError("lr_leaf must have one entry per leaf")
+
+
 @dataclass
 class StepConfig:
     tree: L.Tree
@@ -92,6 +135,12 @@ class AdamStep(torch.autograd.Function):
     @staticmethod
     def forward(ctx, g, mu, nu, params, lr, b1, b2, eps, step, eps_root, cfg):
         g, mu, nu, params = _contig(g), _contig(mu), _contig(nu), _contig(params)
+        _check_args(cfg, g, (mu, nu), (params,))
+        with torch.cuda.device(g.device):
+            return AdamStep._fwd(ctx, g, mu, nu, params, lr, b1, b2, eps, step, eps_root, cfg)
+
+    @staticmethod
+    def _fwd(ctx, g, mu, nu, params, lr, b1, b2, eps, step, eps_root, cfg):
         sd = cfg.state_dtype if cfg.state_dtype is not None else _sd(mu, nu)
         hp = (_f(lr), _f(b1), _f(b2), _f(eps), float(eps_root))
         out = torch.empty_like(g)
@@ -108,6 +157,11 @@ class AdamStep(torch.autograd.Function):
     @once_differentiable
     def backward(ctx, d_out, d_mu1, d_nu1):
         g, mu, nu = ctx.saved_tensors
+        with torch.cuda.device(g.device):
+            return AdamStep._bwd(ctx, g, mu, nu, d_out, d_mu1, d_nu1)
+
+    @staticmethod
+    def _bwd(ctx, g, mu, nu, d_out, d_mu1, d_nu1):
         hp, step, sd, cfg, fused, hps, mu_none, nu_none = ctx.meta
         want_hp = any(_needs(x) for x in hps)
         d_g = torch.empty_like(g)
@@ -115,8 +169,8 @@ class AdamStep(torch.autograd.Function):
         d_nu = None if nu_none or not ctx.needs_input_grad[2] else torch.empty_like(g)
         d_hp = torch.empty(4, dtype=torch.float64, device=g.device) if want_hp else None
         ws = _workspace(cfg.tree, g.device) if want_hp else None
-        L.opt_adam_bwd(cfg.tree, step, hp, sd, cfg.compute, g, mu, nu, _contig(d_out),
-                       _contig(d_mu1), _contig(d_nu1), d_g, d_mu, d_nu, d_hp, None, ws)
+        L.opt_adam_bwd(cfg.tree, step, hp, sd, cfg.compute, g, mu, nu, _cot(d_out),
+                       _cot(d_mu1), _cot(d_nu1), d_g, d_mu, d_nu, d_hp, None, ws)
         d_params = d_out if fused else None
         hg = [None] * 4 if d_hp is None else [_hp_grad(x, d_hp[k]) for k, x in enumerate(hps)]
         return (d_g, d_mu, d_nu, d_params, *hg, None, None, None)
@@ -129,6 +183,12 @@ class RmsPropStep(torch.autograd.Function):
     @staticmethod
     def forward(ctx, g, nu, params, lr, alpha, eps, cfg):
         g, nu, params = _contig(g), _contig(nu), _contig(params)
+        _check_args(cfg, g, (nu,), (params,))
+        with torch.cuda.device(g.device):
+            return RmsPropStep._fwd(ctx, g, nu, params, lr, alpha, eps, cfg)
+
+    @staticmethod
+    def _fwd(ctx, g, nu, params, lr, alpha, eps, cfg):
         sd = cfg.state_dtype if cfg.state_dtype is not None else _sd(nu)
         hp = (_f(lr), _f(alpha), _f(eps))
         out = torch.empty_like(g)
@@ -144,13 +204,18 @@ class RmsPropStep(torch.autograd.Function):
     @once_differentiable
     def backward(ctx, d_out, d_nu1):
         g, nu = ctx.saved_tensors
+        with torch.cuda.device(g.device):
+            return RmsPropStep._bwd(ctx, g, nu, d_out, d_nu1)
+
+    @staticmethod
+    def _bwd(ctx, g, nu, d_out, d_nu1):
         hp, sd, cfg, fused, hps, nu_none = ctx.meta
         want_hp = any(_needs(x) for x in hps)
         d_g = torch.empty_like(g)
         d_nu = None if nu_none or not ctx.needs_input_grad[1] else torch.empty_like(g)
         d_hp = torch.empty(3, dtype=torch.float64, device=g.device) if want_hp else None
         ws = _workspace(cfg.tree, g.device) if want_hp else None
-        L.opt_rmsprop_bwd(cfg.tree, hp, sd, cfg.compute, g, nu, _contig(d_out), _contig(d_nu1),
+        L.opt_rmsprop_bwd(cfg.tree, hp, sd, cfg.compute, g, nu, _cot(d_out), _cot(d_nu1),
                           d_g, d_nu, d_hp, None, ws)
         hg = [None] * 3 if d_hp is None else [_hp_grad(x, d_hp[k]) for k, x in enumerate(hps)]
         return (d_g, d_nu, d_out if fused else None, *hg, None)
@@ -163,6 +228,12 @@ class SgdStep(torch.autograd.Function):
     @staticmethod
     def forward(ctx, g, mom, params, lr, momentum, nesterov, cfg):
         g, mom, params = _contig(g), _contig(mom), _contig(params)
+        _check_args(cfg, g, (mom,), (params,))
+        with torch.cuda.device(g.device):
+            return SgdStep._fwd(ctx, g, mom, params, lr, momentum, nesterov, cfg)
+
+    @staticmethod
+    def _fwd(ctx, g, mom, params, lr, momentum, nesterov, cfg):
         sd = cfg.state_dtype if cfg.state_dtype is not None else _sd(mom)
         hp = (_f(lr), _f(momentum), bool(nesterov))
         out = torch.empty_like(g)
@@ -181,6 +252,11 @@ class SgdStep(torch.autograd.Function):
     @once_differentiable
     def backward(ctx, d_out, d_mom1):
         g, mom = ctx.saved_tensors
+        with torch.cuda.device(g.device):
+            return SgdStep._bwd(ctx, g, mom, d_out, d_mom1)
+
+    @staticmethod
+    def _bwd(ctx, g, mom, d_out, d_mom1):
         hp, sd, cfg, fused, hps, mom_none = ctx.meta
         want_hp = any(_needs(x) for x in hps)
         if d_mom1 is not None and d_mom1.numel() == 0:
@@ -189,7 +265,7 @@ class SgdStep(torch.autograd.Function):
         d_mom = None if mom_none or not ctx.needs_input_grad[1] else torch.empty_like(g)
         d_hp = torch.empty(2, dtype=torch.float64, device=g.device) if want_hp else None
         ws = _workspace(cfg.tree, g.device) if want_hp else None
-        L.opt_sgd_bwd(cfg.tree, hp, sd, cfg.compute, g, mom, _contig(d_out), _contig(d_mom1),
+        L.opt_sgd_bwd(cfg.tree, hp, sd, cfg.compute, g, mom, _cot(d_out), _cot(d_mom1),
                       d_g, d_mom, d_hp, None, ws)
         hg = [None] * 2 if d_hp is None else [_hp_grad(x, d_hp[k]) for k, x in enumerate(hps)]
         return (d_g, d_mom, d_out if fused else None, *hg, None, None)
@@ -212,6 +288,14 @@ class StepEx(torch.autograd.Function):
     def forward(ctx, g, s0, s1, params, lr, wd, lr_leaf, hps, kind, step, opts, cfg):
         decoupled, maximize, nesterov, eps_root, fused = opts
         g, s0, s1, params = _contig(g), _contig(s0), _contig(s1), _contig(params)
+        _check_args(cfg, g, (s0, s1), (params,), None if lr_leaf is None else lr_leaf)
+        with torch.cuda.device(g.device):
+            return StepEx._fwd(ctx, g, s0, s1, params, lr, wd, lr_leaf, hps, kind, step, opts,
+                               cfg)
+
+    @staticmethod
+    def _fwd(ctx, g, s0, s1, params, lr, wd, lr_leaf, hps, kind, step, opts, cfg):
+        decoupled, maximize, nesterov, eps_root, fused = opts
         sd = cfg.state_dtype if cfg.state_dtype is not None else _sd(s0, s1)
         ext = L._ext(_f(wd), decoupled, maximize, None if lr_leaf is None else lr_leaf.detach())
         out = torch.empty_like(g)
@@ -239,6 +323,11 @@ class StepEx(torch.autograd.Function):
     @once_differentiable
     def backward(ctx, d_out, d_n0, d_n1):
         g, s0, s1, params, lr_leaf = ctx.saved_tensors
+        with torch.cuda.device(g.device):
+            return StepEx._bwd(ctx, g, s0, s1, params, lr_leaf, d_out, d_n0, d_n1)
+
+    @staticmethod
+    def _bwd(ctx, g, s0, s1, params, lr_leaf, d_out, d_n0, d_n1):
         kind, hp, ext, sd, cfg, fused, hyp, step = ctx.meta
         nh = _EX_NH[kind]
         want_leaf = lr_leaf is not None and lr_leaf.requires_grad
@@ -250,19 +339,20 @@ class StepEx(torch.autograd.Function):
         d_hp = torch.empty(nh, dtype=torch.float64, device=g.device) if want_hp else None
         d_leaf = (torch.empty(cfg.tree.n_leaves * nh, dtype=torch.float64, device=g.device)
                   if want_leaf else None)
-        ws = _workspace(cfg.tree, g.device, per_leaf=want_leaf) if want_hp else None
-        d_out = _contig(d_out)
+        # the library sums per leaf whenever lr_leaf is given (even a fixed one)
+        ws = _workspace(cfg.tree, g.device, per_leaf=lr_leaf is not None) if want_hp else None
+        d_out = _cot(d_out)
         if d_n1 is not None and d_n1.numel() == 0:
             d_n1 = None
         if kind == "adam":
             L.opt_adam_bwd_ex(cfg.tree, step, hp, ext, sd, cfg.compute, g, s0, s1, params, d_out,
-                              _contig(d_n0), _contig(d_n1), d_g, d_s0, d_s1, d_p, d_hp, d_leaf, ws)
+                              _cot(d_n0), _cot(d_n1), d_g, d_s0, d_s1, d_p, d_hp, d_leaf, ws)
         elif kind == "rmsprop":
             L.opt_rmsprop_bwd_ex(cfg.tree, hp, ext, sd, cfg.compute, g, s0, params, d_out,
-                                 _contig(d_n0), d_g, d_s0, d_p, d_hp, d_leaf, ws)
+                                 _cot(d_n0), d_g, d_s0, d_p, d_hp, d_leaf, ws)
         else:
             L.opt_sgd_bwd_ex(cfg.tree, hp, ext, sd, cfg.compute, g, s0, params, d_out,
-                             _contig(d_n0), d_g, d_s0, d_p, d_hp, d_leaf, ws)
+                             _cot(d_n0), d_g, d_s0, d_p, d_hp, d_leaf, ws)
         if d_p is not None and fused:
             d_p = d_p + d_out  # identity of the fused apply_updates
         lr, *rest = hyp
@@ -285,8 +375,15 @@ class RmsCmStep(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, g, nu, gavg, buf, params, lr, alpha, eps, mom, wd, lr_leaf, opts, cfg):
-        centered, maximize, fused = opts
         g, nu, gavg, buf, params = (_contig(x) for x in (g, nu, gavg, buf, params))
+        _check_args(cfg, g, (nu, gavg, buf), (params,), lr_leaf)
+        with torch.cuda.device(g.device):
+            return RmsCmStep._fwd(ctx, g, nu, gavg, buf, params, lr, alpha, eps, mom, wd,
+                                  lr_leaf, opts, cfg)
+
+    @staticmethod
+    def _fwd(ctx, g, nu, gavg, buf, params, lr, alpha, eps, mom, wd, lr_leaf, opts, cfg):
+        centered, maximize, fused = opts
         sd = cfg.state_dtype if cfg.state_dtype is not None else _sd(nu, gavg, buf)
         ext = L._ext(_f(wd), False, maximize, None if lr_leaf is None else lr_leaf.detach())
         hp = (_f(lr), _f(alpha), _f(eps), _f(mom), bool(centered))
@@ -304,6 +401,12 @@ class RmsCmStep(torch.autograd.Function):
     @once_differentiable
     def backward(ctx, d_out, d_nu1, d_gavg1, d_buf1):
         g, nu, gavg, buf, params, lr_leaf = ctx.saved_tensors
+        with torch.cuda.device(g.device):
+            return RmsCmStep._bwd(ctx, g, nu, gavg, buf, params, lr_leaf, d_out, d_nu1, d_gavg1,
+                                  d_buf1)
+
+    @staticmethod
+    def _bwd(ctx, g, nu, gavg, buf, params, lr_leaf, d_out, d_nu1, d_gavg1, d_buf1):
         hp, ext, sd, cfg, fused, centered, hyp = ctx.meta
         want_leaf = lr_leaf is not None and lr_leaf.requires_grad
         want_hp = want_leaf or any(_needs(x) for x in hyp)
@@ -315,11 +418,11 @@ class RmsCmStep(torch.autograd.Function):
         d_hp = torch.empty(5, dtype=torch.float64, device=g.device) if want_hp else None
         d_leaf = (torch.empty(cfg.tree.n_leaves * 5, dtype=torch.float64, device=g.device)
                   if want_leaf else None)
-        ws = _workspace(cfg.tree, g.device, per_leaf=want_leaf) if want_hp else None
+        ws = _workspace(cfg.tree, g.device, per_leaf=lr_leaf is not None) if want_hp else None
         if d_gavg1 is not None and d_gavg1.numel() == 0:
             d_gavg1 = None
         L.opt_rmsprop_cm_bwd(cfg.tree, hp, ext, sd, cfg.compute, g, nu, gavg, buf, params,
-                             _contig(d_out), _contig(d_nu1), _contig(d_gavg1), _contig(d_buf1),
+                             _cot(d_out), _cot(d_nu1), _cot(d_gavg1), _cot(d_buf1),
                              d_g, d_nu, d_gavg, d_buf, d_p, d_hp, d_leaf, ws)
         if d_p is not None and fused:
             d_p = d_p + d_out  # identity of the fused apply_updates
@@ -334,8 +437,13 @@ class ApplyUpdates(torch.autograd.Function):
     @staticmethod
     def forward(ctx, params, updates):
         p, u = params.contiguous(), updates.contiguous()
+        if not (p.is_cuda and u.is_cuda) or p.device != u.device:
+            raise TypeError("apply_updates needs params and updates on one CUDA device")
+        if p.dtype != torch.float32 or u.dtype != torch.float32:
+            raise TypeError("apply_updates needs float32 params and updates")
         out = torch.empty_like(p)
-        L.opt_apply_updates(p.numel(), p, u, out)
+        with torch.cuda.device(p.device):
+            L.opt_apply_updates(p.numel(), p, u, out)
         return out
 
     @staticmethod
@@ -401,13 +509,12 @@ class GradientTransformation:
             # in-place update would destroy the state the VJP needs
             raise RuntimeError("inplace=True is not allowed with a differentiable update")
         layout = state.layout
-        flat = grads if isinstance(grads, torch.Tensor) and grads.dim() == 1 \
-            and len(layout.sizes) == 1 else layout.flatten(grads)
+        flat = grads if _is_flat(grads, layout) else layout.flatten(grads)
         cfg = StepConfig(layout.tree, self.compute, self.state_dtype)
         t = state.step + 1
         flat_p = None
         if params is not None:
-            flat_p = params if isinstance(params, torch.Tensor) else layout.flatten(params)
+            flat_p = params if _is_flat(params, layout) else layout.flatten(params)
         if self.kind == "rmsprop_cm":
             return self._update_cm(flat, state, flat_p, cfg, t, inplace, differentiable)
         if self.ext is not None:
@@ -480,6 +587,20 @@ class GradientTransformation:
                 if old is not None and new is not None:
                     old.copy_(new)
         return out, OptState(t, slots, state.layout)
+
+
+def _is_flat(x, layout):
+    """A 1-D tensor of tree.numel elements is already the flat buffer (e.g. the
+    gradient autograd returns for a flat parameter buffer); a single tensor of
+    another shape is the one leaf of a one-leaf tree; sequences are leaves."""
+    if not isinstance(x, torch.Tensor):
+        return False
+    if x.dim() == 1 and x.numel() == layout.tree.numel:
+        return True
+    if len(layout.sizes) == 1:
+        return True  # flatten() of one tensor would iterate its first dimension
+    raise ValueError(f"a single tensor of shape {tuple(x.shape)} is not the flat buffer of a "
+                     f"{len(layout.sizes)}-leaf tree ({layout.tree.numel} elements)")
 
 
 def _any_requires_grad(grads, state):

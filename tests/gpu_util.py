@@ -61,3 +61,25 @@ def assert_sum_close(name, x, ref, ref_abs, rtol=1e-5, atol=1e-6):
     ok = np.abs(x - ref) <= atol + rtol * ref_abs
     if not ok.all():
         raise AssertionError(f"{name}: got {x.tolist()} want {ref.tolist()} (Sigma|t| {ref_abs.tolist()})")
+
+
+def leaf_scale(h, offsets):
+    """Per-leaf error scale of per-leaf hyper-gradient sums: the per-element
+    hyper twins h (nh x n, oracle *_mag()['h'], each >= |term| -- pinned in
+    tests/test_oracle.py) summed over each leaf's elements -> (n_leaves, nh).
+    A leaf is held to its OWN Sigma |term| scale (reading Z10), never the
+    whole tree's."""
+    h = np.asarray(h, np.float64)
+    off = np.asarray(offsets, np.int64)
+    return np.stack([h[:, lo:hi].sum(1) for lo, hi in zip(off[:-1], off[1:])])
+
+
+def assert_leaf_sums_close(name, got, ref, scale, rtol=1e-5, atol=1e-6):
+    """Per-leaf sums: |got - ref| <= atol + rtol * (that leaf's scale)."""
+    got, ref, scale = (np.asarray(a, np.float64) for a in (got, ref, scale))
+    bad = ~(np.abs(got - ref) <= atol + rtol * scale)
+    if bad.any():
+        i = np.argwhere(bad)[:5]
+        raise AssertionError(f"{name}: {int(bad.sum())} per-leaf sums outside tol; (leaf, k) "
+                             f"{i.tolist()} got {got[bad][:5].tolist()} want "
+                             f"{ref[bad][:5].tolist()} scale {scale[bad][:5].tolist()}")

@@ -513,3 +513,159 @@ def test_sharded_adam_fused_local_step(pkg):
         opt.step(p, g)
         L.opt_adam_fwd(tree, t, (1e-2, 0.9, 0.999, 1e-8, 0.0), 0, 0, g, m, v, None, m, v, ref, ref)
     assert torch.equal(p, ref)
+
+
+# ------------------------------------------- functional API input handling
+@pytest.mark.parametrize("kind", ["adam", "rmsprop", "sgd", "rmsprop_cm", "adamw"])
+def test_bf16_state_autograd_cotangents_are_widened(pkg, kind):
+    """bfloat16 state through the autograd Functions: the
+    cotangent autograd hands a bf16 state output is bf16; the Function must
+    widen it to float32 before the C call (diffopt.h reads cotangents as
+    float). Checked bitwise against a direct C-ABI call with the widened
+    cotangents, plus a 2-step Listing-1 meta-gradient within bf16 rounding
+    of the fp32-state run."""
+    torch.manual_seed(3)
+    n = 4097
+    tree = pkg.Tree(numel=n, device=DEV)
+    cfg = pkg.functional.StepConfig(tree)
+    g = torch.randn(n, device=DEV) * 1e-2
+    s0 = (torch.rand(n, device=DEV) * 1e-4).to(torch.bfloat16).requires_grad_(True)
+    s1 = (torch.rand(n, device=DEV) * 1e-4).to(torch.bfloat16).requires_grad_(True)
+    du, dn0, dn1 = (torch.randn(n, device=DEV) for _ in range(3))
+    gg = g.clone().requires_grad_(True)
+    L = pkg._lib
+    if kind == "adam":
+        hp = (1e-2, 0.9, 0.999, 1e-8, 0.0)
+        u, a, b = pkg.AdamStep.apply(gg, s0, s1, None, *hp[:4], 3, 0.0, cfg)
+        loss = (u * du).sum() + (a.float() * dn0).sum() + (b.float() * dn1).sum()
+        got = torch.autograd.grad(loss, [gg, s0, s1])
+        ref = [torch.empty(n, device=DEV) for _ in range(3)]
+        L.opt_adam_bwd(tree, 3, hp, L.OPT_BF16, L.OPT_COMPUTE_DEFAULT, g, s0.detach(),
+                       s1.detach(), du, dn0.bfloat16().float(), dn1.bfloat16().float(), *ref)
+    elif kind == "rmsprop":
+        hp = (1e-2, 0.99, 1e-8)
+        u, a = pkg.RmsPropStep.apply(gg, s0, None, *hp, cfg)
+        loss = (u * du).sum() + (a.float() * dn0).sum()
+        got = torch.autograd.grad(loss, [gg, s0])
+        ref = [torch.empty(n, device=DEV) for _ in range(2)]
+        L.opt_rmsprop_bwd(tree, hp, L.OPT_BF16, L.OPT_COMPUTE_DEFAULT, g, s0.detach(), du,
+                          dn0.bfloat16().float(), *ref)
+    elif kind == "sgd":
+        hp = (1e-1, 0.9, True)
+        u, a = pkg.SgdStep.apply(gg, s0, None, *hp, cfg)
+        loss = (u * du).sum() + (a.float() * dn0).sum()
+        got = torch.autograd.grad(loss, [gg, s0])
+        ref = [torch.empty(n, device=DEV) for _ in range(2)]
+        L.opt_sgd_bwd(tree, hp, L.OPT_BF16, L.OPT_COMPUTE_DEFAULT, g, s0.detach(), du,
+                      dn0.bfloat16().float(), *ref)
+    elif kind == "rmsprop_cm":
+        hp = (1e-2, 0.9, 1e-3, 0.5, True)
+        ext = L._ext()
+        gavg = (torch.randn(n, device=DEV) * 1e-3).to(torch.bfloat16).requires_grad_(True)
+        u, a, c, b = pkg.functional.RmsCmStep.apply(gg, s0, gavg, s1, None, *hp[:4], 0.0, None,
+                                                    (True, False, False), cfg)
+        loss = ((u * du).sum() + (a.float() * dn0).sum() + (c.float() * dn1).sum()
+                + (b.float() * du).sum())
+        got = torch.autograd.grad(loss, [gg, s0, gavg, s1])
+        ref = [torch.empty(n, device=DEV) for _ in range(4)]
+        L.opt_rmsprop_cm_bwd(tree, hp, ext, L.OPT_BF16, L.OPT_COMPUTE_DEFAULT, g, s0.detach(),
+                             gavg.detach(), s1.detach(), None, du, dn0.bfloat16().float(),
+                             dn1.bfloat16().float(), du.bfloat16().float(), *ref, None)
+    else:  # adamw through the _ex path
+        hp = (1e-2, 0.9, 0.999, 1e-8, 0.0)
+        p = torch.randn(n, device=DEV)
+        u, a, b = pkg.functional.StepEx.apply(gg, s0, s1, p, hp[0], 0.1, None, hp[1:4], "adam",
+                                              3, (True, False, False, 0.0, False), cfg)
+        loss = (u * du).sum() + (a.float() * dn0).sum() + (b.float() * dn1).sum()
+        got = torch.autograd.grad(loss, [gg, s0, s1])
+        ref = [torch.empty(n, device=DEV) for _ in range(3)]
+        ext = L._ext(0.1, True, False, None)
+        L.opt_adam_bwd_ex(tree, 3, hp, ext, L.OPT_BF16, L.OPT_COMPUTE_DEFAULT, g, s0.detach(),
+                          s1.detach(), p, du, dn0.bfloat16().float(), dn1.bfloat16().float(),
+                          *ref, None)
+    torch.cuda.synchronize()
+    assert torch.equal(got[0], ref[0]), "gradient cotangent"
+    for x, y in zip(got[1:], ref[1:]):
+        # the gradient of a bf16 leaf is bf16: autograd rounds the fp32 VJP
+        assert x.dtype == torch.bfloat16
+        assert torch.equal(x, y.bfloat16())
+
+
+@pytest.mark.parametrize("make", ["adam", "rmsprop", "sgd"])
+def test_listing1_bf16_state_meta_gradient(pkg, make):
+    """Two Listing-1 steps with bf16 optimizer state: the meta-gradient is
+    within bf16 rounding (1e-2, reading Z9) of the fp32-state run."""
+    torch.manual_seed(4)
+    shapes = [(33, 7), (129,), (4, 4, 4)]
+    p0 = [torch.randn(s, device=DEV) for s in shapes]
+    tgt = [torch.randn(s, device=DEV) for s in shapes]
+
+    def run(sd):
+        meta = torch.tensor(1.5, device=DEV, requires_grad=True)
+        params = [p.clone().requires_grad_(True) for p in p0]
+        opt = {"adam": lambda: pkg.adam(lr=0.05, state_dtype=sd),
+               "rmsprop": lambda: pkg.rmsprop(lr=0.01, state_dtype=sd),
+               "sgd": lambda: pkg.sgd(lr=0.05, momentum=0.9, state_dtype=sd)}[make]()
+        layout = pkg.FlatTree.of(params)
+        flat = layout.flatten(params)
+        state = opt.init(params)
+        for _ in range(2):
+            ps = layout.views(flat)
+            # meta shifts the target (a loss scale would cancel in Adam/RMSProp)
+            inner = sum(((p - meta * t) ** 2).sum() for p, t in zip(ps, tgt))
+            (g,) = torch.autograd.grad(inner, flat, create_graph=True)
+            upd, state = opt.update(g, state)
+            flat = pkg.apply_updates(flat, upd)
+        outer = (flat.double() ** 2).sum()
+        (gm,) = torch.autograd.grad(outer, meta)
+        assert all(s is None or s.dtype == (torch.bfloat16 if sd == pkg._lib.OPT_BF16
+                                            else torch.float32) for s in state.slots)
+        return float(outer), float(gm)
+
+    o32, g32 = run(pkg._lib.OPT_F32)
+    o16, g16 = run(pkg._lib.OPT_BF16)
+    assert np.isfinite(g16)
+    assert o16 == pytest.approx(o32, rel=1e-2)
+    assert abs(g32) > 1e-2
+    assert g16 == pytest.approx(g32, rel=1e-2)
+
+
+def test_update_accepts_flat_gradient_of_multi_leaf_tree(pkg):
+    """update() with the 1-D flat gradient autograd returns for a flat
+    parameter buffer of a many-leaf tree takes it as the flat buffer (no
+    per-element flatten); equals the leaf-list path bitwise."""
+    import time
+    sizes = [300_000, 7, 200_000, 1]
+    params = [torch.randn(s, device=DEV) for s in sizes]
+    opt = pkg.adam(lr=1e-2)
+    layout = pkg.FlatTree.of(params)
+    flat_g = torch.randn(sum(sizes), device=DEV)
+    st = opt.init(params)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    u1, _ = opt.update(flat_g, st)
+    torch.cuda.synchronize()
+    assert time.perf_counter() - t0 < 1.0
+    u2, _ = opt.update(layout.views(flat_g), st)
+    assert torch.equal(u1, u2)
+
+
+def test_fixed_lr_leaf_with_learnable_weight_decay_large_tree(pkg):
+    """A fixed (non-learnable) lr_leaf plus a learnable weight decay on a
+    >1M-element tree: the library sums per leaf whenever lr_leaf is given,
+    so the Function must size the per-leaf workspace."""
+    sizes = [1_500_000, 300_001, 17]
+    tree = pkg.Tree.from_sizes(sizes, device=DEV)
+    cfg = pkg.functional.StepConfig(tree)
+    n = tree.numel
+    g = (torch.randn(n, device=DEV) * 1e-2).requires_grad_(True)
+    p = torch.randn(n, device=DEV)
+    lr_leaf = torch.tensor([1e-2, 2e-2, 3e-2], device=DEV)
+    wd = torch.tensor(0.1, dtype=torch.float64, requires_grad=True)
+    u, a, b = pkg.functional.StepEx.apply(g, None, None, p, 1e-2, wd, lr_leaf, (0.9, 0.999, 1e-8),
+                                          "adam", 1, (True, False, False, 0.0, False), cfg)
+    (gwd,) = torch.autograd.grad(u.sum(), [wd])
+    # AdamW: u = -lr_l (g / (|g| + eps) + wd p) at t = 1, so du/dwd = -lr_l p
+    lrs = torch.repeat_interleave(lr_leaf.double(), torch.tensor(sizes, device=DEV))
+    want = float(-(lrs * p.double()).sum())
+    assert float(gwd) == pytest.approx(want, rel=1e-5, abs=1e-3)

@@ -945,3 +945,285 @@ def test_neumann_series_closed_forms(orc):
         x = orc.neumann_dense(2 * np.eye(3), b, K, 0.25)
         np.testing.assert_allclose(x, b / 2 * (1 - 0.5 ** (K + 1)), rtol=1e-14)
     assert np.max(np.abs(orc.neumann_dense(2 * np.eye(3), b, 20, 0.25) - b / 2)) < 1e-5
+
+
+# ------------------- tolerance twins: bounds, teeth, looseness (Z10, r2)
+def _per_elem_terms(fn, n):
+    """Per-element hyper-gradient terms from an oracle VJP: every element its
+    own leaf (offsets 0..n), so dhp_leaf[i] is element i's term."""
+    return fn(np.arange(n + 1, dtype=np.int64))["dhp_leaf"].T
+
+
+def _assert_bounds(name, val, mag):
+    val, mag = np.abs(np.asarray(val, np.float64)), np.asarray(mag, np.float64)
+    bad = ~(val <= mag * (1 + 1e-9) + 1e-300)
+    assert not bad.any(), (name, np.flatnonzero(bad)[:5], val[bad][:5], mag[bad][:5])
+
+
+def test_base_hyper_twins_bound_each_term(orc):
+    """Per-element hyper twins (the 'h' arrays the per-leaf bars sum) bound
+    every element's hyper-gradient term, not only the sums."""
+    x = synth.state_tree(72, [2000, 33])
+    g, m, v, du, dm1, dv1 = (x[k] for k in ("g", "m", "v", "du", "dm1", "dv1"))
+    n = g.size
+    for t in (1, 10):
+        hp = (0.5, 0.9, 0.999, 1e-8)
+        mag = orc.adam_mag(g, m, v, du, dm1, dv1, t, *hp)
+        terms = _per_elem_terms(lambda o: orc.adam_vjp(g, m, v, du, dm1, dv1, t, *hp, prec=1,
+                                                       offsets=o), n)
+        _assert_bounds("adam h", terms, mag["h"])
+        np.testing.assert_allclose(mag["h"].sum(1), mag["dhp"], rtol=1e-12)
+    mr = orc.rmsprop_mag(g, v, du, dv1, 0.3, 0.99, 1e-8)
+    tr = _per_elem_terms(lambda o: orc.rmsprop_vjp(g, v, du, dv1, 0.3, 0.99, 1e-8, prec=1,
+                                                   offsets=o), n)
+    _assert_bounds("rmsprop h", tr, mr["h"])
+    for nest in (False, True):
+        ms = orc.sgd_mag(g, m, du, dm1, 0.1, 0.9, nest)
+        ts = _per_elem_terms(lambda o: orc.sgd_vjp(g, m, du, dm1, 0.1, 0.9, nest, prec=1,
+                                                   offsets=o), n)
+        _assert_bounds("sgd h", ts, ms["h"])
+
+
+def _ex_case(seed=73):
+    leaves = [1500, 1, 400, 7]
+    x = synth.state_tree(seed, leaves)
+    th = synth.normal(seed, synth.S_THETA0, sum(leaves)).astype(np.float32)
+    off = synth.offsets_of(leaves)
+    lr_leaf = np.array([0.5, 2e-2, 1.0, 3e-3])
+    return x, th, off, lr_leaf
+
+
+@pytest.mark.parametrize("kind", ["adam", "adamw", "rmsprop", "sgd", "sgd_nesterov"])
+@pytest.mark.parametrize("maximize", [False, True])
+def test_ex_twins_bound_the_values(orc, kind, maximize):
+    """ex_mag (the NEXT-1 variants' tolerance) bounds |value| of every output
+    and of every element's hyper-gradient term (weight decay, maximize,
+    per-leaf lr), at t = 1 and t = 10."""
+    x, th, off, lrl = _ex_case()
+    n = x["g"].size
+    wd = 0.05
+    kw = dict(weight_decay=wd, maximize=maximize, lr_leaf=lrl, offsets=off)
+    for t in (1, 10):
+        if kind in ("adam", "adamw"):
+            hp = (0.5, 0.9, 0.999, 1e-8, 0.0)
+            dec = kind == "adamw"
+            u, m1, v1 = orc.adam_fwd_ex(x["g"], x["m"], x["v"], th, t, *hp, decoupled=dec,
+                                        prec=1, **kw)
+            r = orc.adam_vjp_ex(x["g"], x["m"], x["v"], th, x["du"], x["dm1"], x["dv1"], t, *hp,
+                                decoupled=dec, prec=1, **kw)
+            mag = orc.ex_mag("adam", x["g"], (x["m"], x["v"]), th, x["du"], x["dm1"], x["dv1"],
+                             t, hp, decoupled=dec, **kw)
+            vals = dict(u=u, m1=m1, v1=v1, dg=r["dg"], dm=r["dm"], dv=r["dv"],
+                        dtheta=r["dtheta"])
+            terms = _per_elem_terms(lambda o: orc.adam_vjp_ex(
+                x["g"], x["m"], x["v"], th, x["du"], x["dm1"], x["dv1"], t, *hp, decoupled=dec,
+                prec=1, weight_decay=wd, maximize=maximize,
+                lr_leaf=np.repeat(lrl, np.diff(off)), offsets=o), n)
+        elif kind == "rmsprop":
+            hp = (0.3, 0.95, 1e-8)
+            u, v1 = orc.rmsprop_fwd_ex(x["g"], x["v"], th, *hp, prec=1, **kw)
+            r = orc.rmsprop_vjp_ex(x["g"], x["v"], th, x["du"], x["dv1"], *hp, prec=1, **kw)
+            mag = orc.ex_mag("rmsprop", x["g"], x["v"], th, x["du"], x["dv1"], hp=hp, **kw)
+            vals = dict(u=u, v1=v1, dg=r["dg"], dv=r["dv"], dtheta=r["dtheta"])
+            terms = _per_elem_terms(lambda o: orc.rmsprop_vjp_ex(
+                x["g"], x["v"], th, x["du"], x["dv1"], *hp, prec=1, weight_decay=wd,
+                maximize=maximize, lr_leaf=np.repeat(lrl, np.diff(off)), offsets=o), n)
+        else:
+            hp = (0.1, 0.9, kind == "sgd_nesterov")
+            u, b1 = orc.sgd_fwd_ex(x["g"], x["m"], th, *hp, prec=1, **kw)
+            r = orc.sgd_vjp_ex(x["g"], x["m"], th, x["du"], x["dm1"], *hp, prec=1, **kw)
+            mag = orc.ex_mag("sgd", x["g"], x["m"], th, x["du"], x["dm1"], hp=hp, **kw)
+            vals = dict(u=u, b1=b1, dg=r["dg"], db=r["db"], dtheta=r["dtheta"])
+            terms = _per_elem_terms(lambda o: orc.sgd_vjp_ex(
+                x["g"], x["m"], th, x["du"], x["dm1"], *hp, prec=1, weight_decay=wd,
+                maximize=maximize, lr_leaf=np.repeat(lrl, np.diff(off)), offsets=o), n)
+        for k, val in vals.items():
+            _assert_bounds(f"{kind} {k} t={t}", val, mag[k])
+        _assert_bounds(f"{kind} h t={t}", terms, mag["h"])
+        _assert_bounds(f"{kind} dhp t={t}", r["dhp"], mag["dhp"])
+
+
+@pytest.mark.parametrize("centered", [False, True])
+@pytest.mark.parametrize("momentum", [0.0, 0.9])
+def test_rmsprop_cm_twins_bound_the_values(orc, centered, momentum):
+    """rmsprop_cm_mag bounds |value| of every output and element term."""
+    leaves = [900, 1, 300]
+    x = synth.rms_cm_tree(74, leaves)
+    off = synth.offsets_of(leaves)
+    lrl = np.array([0.3, 1e-2, 1.0])
+    n = x["g"].size
+    hp = (0.3, 0.9, 1e-6, momentum, centered)
+    kw = dict(weight_decay=0.05, maximize=False)
+    args = (x["g"], x["v"], x["a"], x["b"], x["theta"])
+    cots = (x["du"], x["dv1"], x["da1"], x["db1"])
+    u, v1, a1, b1 = orc.rmsprop_cm_fwd(*args, *hp[:4], centered=centered, prec=1, lr_leaf=lrl,
+                                       offsets=off, **kw)
+    r = orc.rmsprop_cm_vjp(*args, *cots, *hp[:4], centered=centered, prec=1, lr_leaf=lrl,
+                           offsets=off, **kw)
+    mag = orc.rmsprop_cm_mag(*args, *cots, *hp[:4], centered=centered, lr_leaf=lrl, offsets=off,
+                             **kw)
+    vals = dict(u=u, v1=v1, b1=b1, dg=r["dg"], dv=r["dv"], db=r["db"], dtheta=r["dtheta"])
+    if centered:
+        vals.update(a1=a1, da=r["da"])
+    for k, val in vals.items():
+        _assert_bounds(f"cm {k}", val, mag[k])
+    terms = _per_elem_terms(lambda o: orc.rmsprop_cm_vjp(
+        *args, *cots, *hp[:4], centered=centered, prec=1, lr_leaf=np.repeat(lrl, np.diff(off)),
+        offsets=o, **kw), n)
+    _assert_bounds("cm h", terms, mag["h"])
+
+
+def test_ex_mag_has_teeth(orc):
+    """The variants' fp32 bar is passed by an fp32 evaluation of the reduced
+    form and failed by an fp32 evaluation of the textbook chain rule, with
+    L2 weight decay folded into the gradient (Adam, t = 1, zero state)."""
+    rng = np.random.default_rng(5)
+    n = 1 << 15
+    g = (1e-2 * rng.standard_normal(n)).astype(np.float32)
+    th = rng.standard_normal(n).astype(np.float32)
+    du = rng.standard_normal(n).astype(np.float32)
+    wd = 1e-3
+    hp = (1.0, 0.9, 0.999, 1e-8, 0.0)
+    r = orc.adam_vjp_ex(g, None, None, th, du, None, None, 1, *hp, weight_decay=wd, prec=1)
+    mag = orc.ex_mag("adam", g, (None, None), th, du, None, None, 1, hp, weight_decay=wd)
+    gt = (g + np.float32(wd) * th).astype(np.float32)
+    ok = lambda y: np.abs(y.astype(np.float64) - r["dg"]) <= 1e-6 + 1e-5 * np.maximum(
+        mag["dg"], np.abs(r["dg"]))
+    assert ok(_f32_adam_dg(gt, du, *hp[:4], reduced=True)).mean() == 1.0
+    assert ok(_f32_adam_dg(gt, du, *hp[:4], reduced=False)).mean() < 0.5
+
+
+def test_rmsprop_cm_mag_has_teeth(orc):
+    """Centred RMSProp (zero state, no momentum): the fp32 reduced form
+    dg = -du lr eps / d^2 passes the bar, the fp32 textbook chain rule
+    (-lr/d + lr g/d^2 * dq/dg / (2r), which cancels down to it) fails."""
+    rng = np.random.default_rng(6)
+    n = 1 << 15
+    f = np.float32
+    g = (1e-2 * rng.standard_normal(n)).astype(f)
+    du = rng.standard_normal(n).astype(f)
+    z = np.zeros(n, f)
+    lr, al, eps = 1.0, 0.9, 1e-8
+    r = orc.rmsprop_cm_vjp(g, None, None, None, z, du, None, None, None, lr, al, eps,
+                           centered=True, prec=1)
+    mag = orc.rmsprop_cm_mag(g, None, None, None, z, du, None, None, None, lr, al, eps,
+                             centered=True)
+    om = f(1) - f(al)
+    v1, a1 = om * g * g, om * g
+    q = v1 - a1 * a1
+    rr = np.sqrt(q)
+    d = rr + f(eps)
+    reduced = -du * f(lr) * f(eps) / (d * d)
+    dd = du * f(lr) * g / (d * d)
+    dq = np.where(rr == 0, f(0), dd / (f(2) * np.where(rr == 0, f(1), rr)))
+    textbook = du * (-f(lr) / d) + dq * (f(2) * om * g) + (-f(2) * a1 * dq) * om
+    ok = lambda y: np.abs(y.astype(np.float64) - r["dg"]) <= 1e-6 + 1e-5 * np.maximum(
+        mag["dg"], np.abs(r["dg"]))
+    assert ok(reduced).mean() == 1.0
+    assert ok(textbook).mean() < 0.5
+
+
+def _rho(s, a):
+    """Cancellation ratio |sum| / sum|terms| of a sum node (1 where 0/0)."""
+    s, a = np.abs(s), np.asarray(a)
+    return np.where(a > 0, s / np.where(a > 0, a, 1.0), 1.0)
+
+
+def _check_loose(name, mag, ref, bound):
+    """mag / |ref| <= bound wherever ref != 0 and the bound is finite."""
+    ref = np.abs(ref)
+    sel = (ref > 0) & np.isfinite(bound)
+    ratio = mag[sel] / ref[sel]
+    bad = ratio > bound[sel] * (1 + 1e-6) + 1e-9
+    assert not bad.any(), (name, ratio[bad][:5], bound[sel][bad][:5])
+    return float(np.mean(ratio > 10)), float(np.mean(bound[sel] > 10))
+
+
+def test_adam_twin_looseness_is_input_cancellation(orc):
+    """Looseness pin: on the C2 recipe at lr = 1, t = 10 the twin
+    may exceed |ref| only by the cancellation of the sums of the REDUCED
+    form. With rho = |sum| / sum|terms| of each sum node (m' = b1 m + (1-b1)
+    g, the reduced dg bracket A eps + (A Q - P C g)/s, dg's top-level three
+    terms, dm's and dv's two terms), mag / |ref| <= prod 1/rho exactly
+    (mag is the tree over |.|), so every element with mag > 10 |ref| shows a
+    cancellation in one of those sums; no other looseness is allowed."""
+    idx = synth.uniform(0x1005E, 1, 1 << 16) * sum(synth.RESNET18_LEAVES)
+    x = synth.state_tree(0xC2, synth.RESNET18_LEAVES, index=idx.astype(np.int64))
+    t, lr, b1, b2, eps = 10, 1.0, 0.9, 0.999, 1e-8
+    g, m, v, du, dm1, dv1 = (x[k].astype(np.float64) for k in ("g", "m", "v", "du", "dm1", "dv1"))
+    u, m1, v1 = orc.adam_fwd(x["g"], x["m"], x["v"], t, lr, b1, b2, eps, prec=1)
+    r = orc.adam_vjp(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], t, lr, b1, b2, eps,
+                     prec=1)
+    mag = orc.adam_mag(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], t, lr, b1, b2, eps)
+    bc1, bc2 = 1 - b1 ** t, 1 - b2 ** t
+    A, C = (1 - b1) / bc1, (1 - b2) / bc2
+    P, Q = b1 * m / bc1, b2 * v / bc2
+    mh = A * g + P
+    s = np.sqrt(C * g * g + Q)
+    d = s + eps
+    rs = np.where(s > 0, 1 / np.where(s > 0, s, 1), 0)
+    rho_m = _rho(mh, A * np.abs(g) + np.abs(P))
+    br = A * eps + (A * Q - P * C * g) * rs
+    rho_in = _rho(br, A * eps + (A * Q + np.abs(P * C * g)) * rs)
+    T = [(1 - b1) * dm1, 2 * (1 - b2) * g * dv1, -du * lr * br / d ** 2]
+    rho_top = _rho(sum(T), sum(np.abs(x) for x in T))
+    y = du * lr / (bc1 * d)
+    rho_dm = _rho(dm1 - y, np.abs(dm1) + np.abs(y))
+    w = du * lr * mh * rs / (2 * bc2 * d ** 2)
+    rho_dv = _rho(dv1 + w, np.abs(dv1) + np.abs(w))
+    inv = lambda *rh: 1.0 / np.prod(rh, axis=0)
+    stats = {}
+    stats["u"] = _check_loose("u", mag["u"], u, inv(rho_m))
+    stats["m1"] = _check_loose("m1", mag["m1"], m1, inv(rho_m))
+    stats["v1"] = _check_loose("v1", mag["v1"], v1, np.ones_like(v1))
+    stats["dg"] = _check_loose("dg", mag["dg"], r["dg"], inv(rho_in, rho_top))
+    stats["dm"] = _check_loose("dm", mag["dm"], r["dm"], inv(rho_dm))
+    stats["dv"] = _check_loose("dv", mag["dv"], r["dv"], inv(rho_dv, rho_m))
+    # the reading's premise on this recipe: looseness happens, and is rare
+    assert stats["dv"][0] > 0 and all(f < 0.2 for f, _ in stats.values())
+
+
+def test_rmsprop_twin_looseness_is_input_cancellation(orc):
+    """The same pin for RMSProp: u and v' are cancellation-free (ratio 1);
+    dg and dv only by their top-level sums."""
+    x = synth.state_tree(0xC2, None, n=1 << 16)
+    lr, al, eps = 1.0, 0.99, 1e-8
+    g, v, du, dv1 = (x[k].astype(np.float64) for k in ("g", "v", "du", "dv1"))
+    u, v1 = orc.rmsprop_fwd(x["g"], x["v"], lr, al, eps, prec=1)
+    r = orc.rmsprop_vjp(x["g"], x["v"], x["du"], x["dv1"], lr, al, eps, prec=1)
+    mag = orc.rmsprop_mag(x["g"], x["v"], x["du"], x["dv1"], lr, al, eps)
+    s = np.sqrt(al * v + (1 - al) * g * g)
+    d = s + eps
+    rs = np.where(s > 0, 1 / np.where(s > 0, s, 1), 0)
+    T = [2 * (1 - al) * g * dv1, -du * lr * (eps + al * v * rs) / d ** 2]
+    rho_top = _rho(sum(T), sum(np.abs(t) for t in T))
+    w = du * lr * g * rs / (2 * d ** 2)
+    rho_dv = _rho(dv1 + w, np.abs(dv1) + np.abs(w))
+    _check_loose("u", mag["u"], u, np.ones_like(u))
+    _check_loose("v1", mag["v1"], v1, np.ones_like(v1))
+    _check_loose("dg", mag["dg"], r["dg"], 1 / rho_top)
+    _check_loose("dv", mag["dv"], r["dv"], 1 / rho_dv)
+
+
+def test_ex_twin_looseness_adds_only_the_decay_sum(orc):
+    """Adam with L2 decay: beyond the base step's sums, the twin may exceed
+    |ref| only through gt = g + wd theta: rho_gt in the numerators (squared
+    in v') and the Lipschitz factor f_d = 1 + sqrt(C) (|g| + wd |theta| -
+    |gt|) / d on 1/d (oracle.hpp adam_mag2)."""
+    x, th, off, _ = _ex_case(75)
+    t, hp, wd = 10, (1.0, 0.9, 0.999, 1e-8, 0.0), 0.05
+    u, m1, v1 = orc.adam_fwd_ex(x["g"], x["m"], x["v"], th, t, *hp, weight_decay=wd, prec=1)
+    mag = orc.ex_mag("adam", x["g"], (x["m"], x["v"]), th, x["du"], x["dm1"], x["dv1"], t, hp,
+                     weight_decay=wd)
+    g, m, thd = x["g"].astype(np.float64), x["m"].astype(np.float64), th.astype(np.float64)
+    gt = g + wd * thd
+    rho_gt = _rho(gt, np.abs(g) + wd * np.abs(thd))
+    b1 = hp[1]
+    rho_m = _rho(b1 * m + (1 - b1) * gt, b1 * np.abs(m) + (1 - b1) * np.abs(gt))
+    bc1, bc2 = 1 - b1 ** t, 1 - hp[2] ** t
+    C = (1 - hp[2]) / bc2
+    s = np.sqrt(C * gt * gt + hp[2] * x["v"].astype(np.float64) / bc2)
+    f_d = 1 + np.sqrt(C) * (np.abs(g) + wd * np.abs(thd) - np.abs(gt)) / (s + hp[3])
+    _check_loose("u", mag["u"], u, f_d / (rho_m * rho_gt))
+    _check_loose("m1", mag["m1"], m1, 1 / (rho_m * rho_gt))
+    _check_loose("v1", mag["v1"], v1, 1 / rho_gt ** 2)

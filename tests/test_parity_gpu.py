@@ -8,8 +8,8 @@ import torch
 
 import oracle
 import synth
-from gpu_util import (DEV, assert_close, assert_sum_close, dev_f32, dev_state, host,
-                      state_host_bits)
+from gpu_util import (DEV, assert_close, assert_leaf_sums_close, assert_sum_close, dev_f32,
+                      dev_state, host, leaf_scale, state_host_bits)
 
 pytestmark = pytest.mark.gpu
 
@@ -89,8 +89,8 @@ def test_adam_fwd_bwd(L, case, lr, bf16, ct):
     assert_sum_close("dhp", host(dhp), r["dhp"], hs)
     assert np.allclose(host(dhl).reshape(-1, 4).sum(0), host(dhp), rtol=1e-12,
                        atol=1e-12 * hs.max())
-    np.testing.assert_allclose(host(dhl).reshape(-1, 4), r["dhp_leaf"], rtol=1e-5,
-                               atol=1e-6 + 1e-5 * hs.max())
+    assert_leaf_sums_close("dhp_leaf", host(dhl).reshape(-1, 4), r["dhp_leaf"],
+                           leaf_scale(mag["h"], tree.h_offsets))
     # global-only reduction path gives the same sums
     dhp2 = torch.empty(4, dtype=torch.float64, device=DEV)
     L.opt_adam_bwd(tree, t, hp, sd, ct, g, m, v, du, dm1, dv1, None, None, None, dhp2, None, ws)
@@ -129,8 +129,8 @@ def test_rmsprop_fwd_bwd(L, bf16, ct):
     check("dv", host(dv), r["dv"], mag["dv"], ct)
     hs = np.maximum(r["dhp_abs"], mag["dhp"])
     assert_sum_close("dhp", host(dhp), r["dhp"], hs)
-    np.testing.assert_allclose(host(dhl).reshape(-1, 3), r["dhp_leaf"], rtol=1e-5,
-                               atol=1e-6 + 1e-5 * hs.max())
+    assert_leaf_sums_close("dhp_leaf", host(dhl).reshape(-1, 3), r["dhp_leaf"],
+                           leaf_scale(mag["h"], tree.h_offsets))
 
 
 @pytest.mark.parametrize("nesterov", [False, True])
@@ -321,7 +321,7 @@ def test_many_leaves_per_leaf_sums(L, n_leaves):
     check("dg", host(dg), r["dg"], mag["dg"], 1)
     got = host(dhl).reshape(-1, 4)
     hs = np.maximum(r["dhp_abs"], mag["dhp"])
-    np.testing.assert_allclose(got, r["dhp_leaf"], rtol=1e-5, atol=1e-6 + 1e-5 * hs.max())
+    assert_leaf_sums_close("dhp_leaf", got, r["dhp_leaf"], leaf_scale(mag["h"], off))
     assert np.all(got[7] == 0) and np.all(got[-1] == 0)
     assert_sum_close("dhp", host(dhp), r["dhp"], hs)
 
@@ -348,7 +348,7 @@ def test_per_leaf_sums_large_leaves(L):
         check(k, host(out), r[k], mag[k], 1)
     got = host(dhl).reshape(-1, 4)
     hs = np.maximum(r["dhp_abs"], mag["dhp"])
-    np.testing.assert_allclose(got, r["dhp_leaf"], rtol=1e-5, atol=1e-6 + 1e-5 * hs.max())
+    assert_leaf_sums_close("dhp_leaf", got, r["dhp_leaf"], leaf_scale(mag["h"], off))
     assert np.all(got[3] == 0)
     assert_sum_close("dhp", host(dhp), r["dhp"], hs)
 
