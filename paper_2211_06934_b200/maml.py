@@ -703,9 +703,11 @@ class PeerAdamOuter:
 
 
 def outer_step(phi, outer_step_idx, cfg: MamlConfig, inner, outer, world=1, rank=0, group=None,
-               shard=None):
+               shard=None, allreduce_events=None):
     """One synchronous meta-update over the cfg.tasks-task meta-batch.
-    ``shard`` (optional) replaces meta_grad_tasks, e.g. a GraphedShard."""
+    ``shard`` (optional) replaces meta_grad_tasks, e.g. a GraphedShard.
+    ``allreduce_events`` (optional list) receives a (start, end) CUDA event
+    pair recorded around the exchange step on the current stream."""
     import torch.distributed as dist
 
     ids = task_range(world, rank, cfg.tasks)
@@ -718,8 +720,14 @@ def outer_step(phi, outer_step_idx, cfg: MamlConfig, inner, outer, world=1, rank
         phi = outer.step_from_local(phi, mg)
         return phi, loss[0] / cfg.tasks, None
     buf = torch.cat([mg, loss.reshape(1)])
+    if allreduce_events is not None:
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record()
     if world > 1:
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)  # the one exchange step
+    if allreduce_events is not None:
+        ev[1].record()
+        allreduce_events.append(ev)
     buf.mul_(1.0 / cfg.tasks)
     mg, loss = buf[:-1].contiguous(), buf[-1]
     phi = outer(phi, mg)
