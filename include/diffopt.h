@@ -242,6 +242,16 @@ int opt_sgd_bwd_ex(const opt_tree* tree, const opt_sgd_hp* hp, const opt_ext* ex
                    float* d_g, float* d_mom, float* d_params, double* d_hp, double* d_hp_leaf,
                    void* workspace, size_t workspace_bytes, void* stream);
 
+/* ----------------------------------------- combining partial hyper sums
+ * out[c] = sum over r = 0 .. rows-1 (in that order) of in[r * cols + c]:
+ * the hyper-gradient sums of a step split into several calls (e.g. the
+ * chunks of a host-streamed step, offload.py) combined on the device in a
+ * fixed order (row a5; bitwise reproducible). in: device fp64 [rows][cols]
+ * row-major (caller-owned); out: device fp64 [cols], written (not
+ * accumulated); rows = 0 writes zeros. OPT_EINVAL on negative sizes or a
+ * NULL pointer that is needed. */
+int opt_sum_rows(int64_t rows, int64_t cols, const double* in, double* out, void* stream);
+
 /* ------------------------------------------- apply_updates (row a8)
  * out = params + updates (out may alias params). Its VJP is the identity. */
 int opt_apply_updates(int64_t numel, const float* params, const float* updates,

@@ -237,6 +237,16 @@ def opt_apply_updates(numel, params, updates, out, stream=None):
                                  _stream(stream)))
 
 
+lib.opt_sum_rows.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                             ctypes.c_void_p]
+lib.opt_sum_rows.restype = ctypes.c_int
+EXPORTS.append("opt_sum_rows")
+
+
+def opt_sum_rows(rows, cols, inp, out, stream=None):
+    _check(lib.opt_sum_rows(int(rows), int(cols), _ptr(inp), _ptr(out), _stream(stream)))
+
+
 def opt_quadratic_grad(numel, a, theta, phi, g, stream=None):
     _check(lib.opt_quadratic_grad(int(numel), _ptr(a), _ptr(theta), _ptr(phi), _ptr(g),
                                   _stream(stream)))

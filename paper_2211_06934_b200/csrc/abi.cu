@@ -1111,6 +1111,39 @@ int opt_apply_updates(int64_t numel, const float* params, const float* updates, 
   return launched(s);
 }
 
+// Fixed-order column sums of a row-major fp64 matrix: one warp per column,
+// lane l sums rows l, l+32, ... in order, then a fixed xor-shuffle tree.
+__global__ void __launch_bounds__(kBlock) sum_rows_kernel(int64_t rows, int64_t cols,
+                                                          const double* __restrict__ in,
+                                                          double* __restrict__ out) {
+  const int64_t c = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= cols) return;
+  double s = 0.0;
+  for (int64_t r = lane; r < rows; r += 32) s += in[r * cols + c];
+  s = warp_sum(s);
+  if (lane == 0) out[c] = s;
+}
+
+int opt_sum_rows(int64_t rows, int64_t cols, const double* in, double* out, void* stream) {
+  g_err.clear();
+  if (rows < 0 || cols < 0) return fail(OPT_EINVAL, "rows = %lld, cols = %lld",
+                                        (long long)rows, (long long)cols);
+  if (cols == 0) return OPT_OK;
+  if (!out) return fail(OPT_EINVAL, "out is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (rows == 0) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double) * cols, s);
+    if (e != cudaSuccess) return fail(OPT_ECUDA, "memset: %s", cudaGetErrorString(e));
+    return OPT_OK;
+  }
+  if (!in) return fail(OPT_EINVAL, "in is NULL");
+  const int64_t grid = (cols + kWarps - 1) / kWarps;
+  if (grid > 0x7FFFFFFF) return fail(OPT_EINVAL, "too many columns");
+  sum_rows_kernel<<<(int)grid, kBlock, 0, s>>>(rows, cols, in, out);
+  return launched(s);
+}
+
 int opt_quadratic_grad(int64_t numel, const float* a, const float* theta, const float* phi,
                        float* g, void* stream) {
   g_err.clear();

@@ -5,7 +5,8 @@ run chunk by chunk with three streams: host->device copies of chunk c+1,
 the fused forward + backward kernels of chunk c (libdiffopt.so, the same
 C-ABI calls as the device-resident path) and device->host copies of chunk
 c-1 overlap, so the PCIe link in both directions is the only bound. The
-per-chunk hyper-gradient sums are combined in chunk order (deterministic).
+per-chunk hyper-gradient sums are combined in chunk order on the device
+(opt_sum_rows; deterministic).
 This is the end-to-end path bench.py reports as "e2e".
 """
 from __future__ import annotations
@@ -47,7 +48,8 @@ class HostStreamedAdam:
         self.buf = [{k: torch.empty(per, device=device) for k in IN_KEYS + OUT_KEYS}
                     for _ in range(nb)]
         self.dhp = torch.empty(len(self.bounds), 4, dtype=torch.float64, device=device)
-        self.h_dhp = torch.empty(len(self.bounds), 4, dtype=torch.float64).pin_memory()
+        self.dhp_total = torch.empty(4, dtype=torch.float64, device=device)
+        self.h_dhp = torch.empty(4, dtype=torch.float64).pin_memory()
         self.s_h2d = torch.cuda.Stream(device)
         self.s_cmp = torch.cuda.Stream(device)
         self.s_d2h = torch.cuda.Stream(device)
@@ -56,7 +58,7 @@ class HostStreamedAdam:
         return 4 * self.n * len(IN_KEYS)
 
     def bytes_d2h(self):
-        return 4 * self.n * len(OUT_KEYS) + self.dhp.numel() * 8
+        return 4 * self.n * len(OUT_KEYS) + self.h_dhp.numel() * 8
 
     def run(self, host_in, host_out, step, hp):
         """host_in / host_out: dicts of pinned fp32 CPU tensors of n elements.
@@ -95,18 +97,11 @@ class HostStreamedAdam:
                 e = torch.cuda.Event()
                 e.record(self.s_d2h)
                 d2h_done.append(e)
+        with torch.cuda.stream(self.s_cmp):  # chunk-ordered sum on the device (row a5)
+            L.opt_sum_rows(len(self.bounds), 4, self.dhp, self.dhp_total, stream=self.s_cmp)
         with torch.cuda.stream(self.s_d2h):
             self.s_d2h.wait_stream(self.s_cmp)
-            self.h_dhp.copy_(self.dhp, non_blocking=True)
+            self.h_dhp.copy_(self.dhp_total, non_blocking=True)
         for s in (self.s_h2d, self.s_cmp, self.s_d2h):
             cur.wait_stream(s)
-        return self.h_dhp  # valid after the current stream reaches this point
-
-    @staticmethod
-    def combine(h_dhp):
-        """Chunk-ordered sum of the per-chunk hyper-gradient sums."""
-        out = [0.0] * 4
-        for row in h_dhp.tolist():
-            for k in range(4):
-                out[k] += row[k]
-        return out
+        return self.h_dhp  # (lr, b1, b2, eps) sums; valid once the current stream gets here

@@ -491,8 +491,36 @@ def test_host_streamed_step_equals_device_step(pkg):
     for k in OUT_KEYS:
         assert torch.equal(h_out[k], o[k].cpu()), k
     ref = oracle.adam_vjp(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], 4, *hp)
-    np.testing.assert_allclose(HostStreamedAdam.combine(h_dhp), host(dhp), rtol=1e-9,
+    np.testing.assert_allclose(h_dhp.numpy(), host(dhp), rtol=1e-9,
                                atol=1e-12 * ref["dhp_abs"].max())
+    # the chunk rows are summed on the device in chunk order (opt_sum_rows)
+    rows = hs.dhp.cpu().numpy()
+    want = np.zeros(4)
+    for r in rows:
+        want += r
+    np.testing.assert_array_equal(h_dhp.numpy(), want)
+
+
+def test_sum_rows_fixed_order(pkg):
+    """opt_sum_rows: column sums in row order, bitwise equal to a sequential
+    fp64 sum of the same rows; rows = 0 writes zeros."""
+    L = pkg._lib
+    rng = np.random.default_rng(3)
+    for rows, cols in ((1, 4), (7, 4), (33, 5), (1000, 3), (65, 70)):
+        x = rng.standard_normal((rows, cols)) * 10.0 ** rng.integers(-8, 8, (rows, cols))
+        out = torch.empty(cols, dtype=torch.float64, device=DEV)
+        L.opt_sum_rows(rows, cols, torch.from_numpy(x).to(DEV), out)
+        # lane l sums rows l, l+32, ... then a xor tree: compare to the same order in numpy
+        lanes = np.zeros((32, cols))
+        for r in range(rows):
+            lanes[r % 32] += x[r]
+        for o in (16, 8, 4, 2, 1):
+            lanes = lanes + lanes[np.arange(32) ^ o]
+        np.testing.assert_array_equal(host(out), lanes[0])
+        np.testing.assert_allclose(host(out), x.sum(0), rtol=1e-12, atol=1e-12 * np.abs(x).sum())
+    out = torch.full((3,), 5.0, dtype=torch.float64, device=DEV)
+    L.opt_sum_rows(0, 3, None, out)
+    assert torch.all(out == 0)
 
 
 def test_sharded_adam_fused_local_step(pkg):
