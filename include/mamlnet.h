@@ -107,26 +107,6 @@ size_t net_gemm_nt_workspace_bytes(int64_t T, int64_t M, int64_t P, int64_t N);
 int net_gemm_nt(int64_t T, int64_t M, int64_t P, int64_t N, const float* A, const float* B,
                 float* C, void* workspace, size_t workspace_bytes, void* stream);
 
-/* Batched fp32-accurate GEMM on the tensor cores (tcgen05 kind::tf32,
- * 3xTF32 split: hi*hi + hi*lo + lo*hi with hi = rna_tf32(x),
- * lo = rna_tf32(x - hi), fp32 accumulation in TMEM; ~2^-21 relative per
- * product, i.e. SGEMM accuracy):
- *   D[t](m, n) = sum_k A[t](m, k) * B[t](n, k) (+ bias[t*N + n])
- * A(m, k) at A + t*bA + m*sAm + k*sAk; B(n, k) at B + t*bB + n*sBn + k*sBk;
- * D(m, n) at D + t*bD + m + n*ldD (m is the contiguous output axis). Any
- * strides are valid; loads are coalesced along whichever of (m, k) / (n, k)
- * has stride 1. splits > 1 splits k into ranges whose partial tiles go to
- * `workspace` (net_tc_gemm_workspace_bytes) and are summed in order by a
- * second kernel; then D must be contiguous (ldD == M, bD == M*N) and bias
- * NULL. Requires T <= 65535. Diagnostics only: the environment variable
- * NET_TC_DBG (read once) skips stages for timing ablations (1 = no MMA,
- * 2 = no split, 4 = no copies; results are then wrong by design). */
-size_t net_tc_gemm_workspace_bytes(int64_t T, int64_t M, int64_t N, int64_t K, int64_t splits);
-int net_tc_gemm(int64_t T, int64_t M, int64_t N, int64_t K, const float* A, int64_t sAm,
-                int64_t sAk, int64_t bA, const float* B, int64_t sBn, int64_t sBk, int64_t bB,
-                float* D, int64_t ldD, int64_t bD, const float* bias, int64_t splits,
-                void* workspace, size_t workspace_bytes, void* stream);
-
 const char* net_last_error(void);
 int net_abi_version(void);
 int64_t net_launch_count(void);

@@ -19,7 +19,7 @@ NET_OK = 0
 
 EXPORTS = ["net_im2col3x3", "net_col2im3x3", "net_bnpool_fwd", "net_bnpool_bwd",
            "net_bnpool_bwd2", "net_gemm_nt_workspace_bytes", "net_gemm_nt",
-           "net_tc_gemm_workspace_bytes", "net_tc_gemm", "net_last_error",
+           "net_last_error",
            "net_abi_version", "net_launch_count"]
 
 
@@ -37,11 +37,7 @@ def _load():
     L.net_gemm_nt_workspace_bytes.argtypes = [i64] * 4
     L.net_gemm_nt_workspace_bytes.restype = ctypes.c_size_t
     L.net_gemm_nt.argtypes = [i64] * 4 + [P, P, P, P, ctypes.c_size_t, P]
-    L.net_tc_gemm_workspace_bytes.argtypes = [i64] * 5
-    L.net_tc_gemm_workspace_bytes.restype = ctypes.c_size_t
-    L.net_tc_gemm.argtypes = ([i64] * 4 + [P, i64, i64, i64, P, i64, i64, i64, P, i64, i64, P, i64,
-                               P, ctypes.c_size_t, P])
-    for n in ("net_tc_gemm", "net_gemm_nt", "net_im2col3x3", "net_col2im3x3", "net_bnpool_fwd", "net_bnpool_bwd",
+    for n in ("net_gemm_nt", "net_im2col3x3", "net_col2im3x3", "net_bnpool_fwd", "net_bnpool_bwd",
               "net_bnpool_bwd2", "net_abi_version"):
         getattr(L, n).restype = ctypes.c_int
     L.net_last_error.restype = ctypes.c_char_p
@@ -91,17 +87,6 @@ def net_gemm_nt(T, M, P, N, A, B, C, workspace=None, stream=None):
     wb = 0 if workspace is None else workspace.numel() * workspace.element_size()
     _check(lib.net_gemm_nt(T, M, P, N, _ptr(A), _ptr(B), _ptr(C), _ptr(workspace), wb,
                            _stream(stream)))
-
-
-def net_tc_gemm_workspace_bytes(T, M, N, K, splits):
-    return int(lib.net_tc_gemm_workspace_bytes(T, M, N, K, splits))
-
-
-def net_tc_gemm(T, M, N, K, A, sAm, sAk, bA, B, sBn, sBk, bB, D, ldD, bD, bias=None, splits=1,
-                workspace=None, stream=None):
-    wb = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    _check(lib.net_tc_gemm(T, M, N, K, _ptr(A), sAm, sAk, bA, _ptr(B), sBn, sBk, bB, _ptr(D), ldD,
-                           bD, _ptr(bias), splits, _ptr(workspace), wb, _stream(stream)))
 
 
 def net_abi_version():

@@ -20,7 +20,6 @@
 #include <string>
 
 #include "mamlnet.h"
-#include "tc_gemm.cuh"
 
 namespace {
 
@@ -920,96 +919,6 @@ int net_gemm_nt(int64_t T, int64_t M, int64_t P, int64_t N, const float* A, cons
   if (blocks > 1024) blocks = 1024;
   gemm_nt_reduce<<<dim3((unsigned)blocks, (unsigned)T), 256, 0, st>>>(MP, q.S, out, C);
   return launched();
-}
-
-int net_tc_gemm(int64_t T, int64_t M, int64_t N, int64_t K, const float* A, int64_t sAm,
-                int64_t sAk, int64_t bA, const float* B, int64_t sBn, int64_t sBk, int64_t bB,
-                float* D, int64_t ldD, int64_t bD, const float* bias, int64_t splits,
-                void* workspace, size_t workspace_bytes, void* stream) {
-  if (T < 0 || M < 0 || N < 0 || K < 0 || T > 65535 || splits < 1 || splits > 65535)
-    return fail("net_tc_gemm: bad sizes");
-  if (T == 0 || M == 0 || N == 0) return NET_OK;
-  if (!A || !B || !D) return fail("net_tc_gemm: NULL operand");
-  // staging order follows the contiguous axis (coalesced loads); any strides are correct
-  const bool a_mn = sAm == 1 && sAk != 1, b_mn = sBn == 1 && sBk != 1;
-  const int64_t mt = (M + tcg::BM - 1) / tcg::BM, nt = (N + tcg::BN - 1) / tcg::BN;
-  if (mt * nt > 0x7FFFFFFF) return fail("net_tc_gemm: too many tiles");
-  int64_t S = splits;
-  int64_t kchunk = (K + S - 1) / S;
-  kchunk = (kchunk + tcg::BK - 1) / tcg::BK * tcg::BK;
-  if (kchunk < tcg::BK) kchunk = tcg::BK;
-  S = K > 0 ? (K + kchunk - 1) / kchunk : 1;
-  tcg::Args a;
-  a.M = (int)M, a.N = (int)N, a.K = (int)K;
-  a.A = A, a.sAm = sAm, a.sAk = sAk, a.bA = bA;
-  a.B = B, a.sBn = sBn, a.sBk = sBk, a.bB = bB;
-  a.bias = bias;
-  a.kchunk = (int)kchunk;
-  a.mtiles = (int)mt;
-  a.splits = (int)S;
-  static const int dbg = [] {  // diagnostics only (stage ablation): see tcg::Args::dbg
-    const char* d = getenv("NET_TC_DBG");
-    return d ? atoi(d) : 0;
-  }();
-  a.dbg = dbg;
-  if (mt * nt * S * T > 0x7FFFFFFF) return fail("net_tc_gemm: too many tiles");
-  a.ntiles = (int)(mt * nt * S * T);
-  cudaStream_t st = (cudaStream_t)stream;
-  if (S > 1) {
-    if (bias) return fail("net_tc_gemm: bias with split-K");
-    if (ldD != M || bD != M * N) return fail("net_tc_gemm: split-K needs D contiguous [T][N][M]");
-    const size_t need = (size_t)T * S * M * N * sizeof(float);
-    if (!workspace || workspace_bytes < need) return fail("net_tc_gemm: workspace too small");
-    a.D = (float*)workspace, a.ldD = M, a.bD = S * M * N, a.sS = M * N;
-  } else {
-    a.D = D, a.ldD = ldD, a.bD = bD, a.sS = 0;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  dim3 grid((unsigned)(a.ntiles < sms ? a.ntiles : sms));  // persistent: one CTA per SM
-  // 16-byte async copies when the contiguous axis is 16-byte aligned everywhere
-  auto al16 = [](const float* p, int64_t other, int64_t batch) {
-    return ((uintptr_t)p & 15) == 0 && other % 4 == 0 && batch % 4 == 0;
-  };
-  const bool va = a_mn ? al16(A, sAk, bA) : (sAk == 1 && al16(A, sAm, bA));
-  const bool vb = b_mn ? al16(B, sBk, bB) : (sBk == 1 && al16(B, sBn, bB));
-  using KFn = void (*)(const tcg::Args);
-  static const KFn table[16] = {
-      tcg::tc3_gemm_kernel<false, false, false, false>, tcg::tc3_gemm_kernel<false, false, false, true>,
-      tcg::tc3_gemm_kernel<false, false, true, false>,  tcg::tc3_gemm_kernel<false, false, true, true>,
-      tcg::tc3_gemm_kernel<false, true, false, false>,  tcg::tc3_gemm_kernel<false, true, false, true>,
-      tcg::tc3_gemm_kernel<false, true, true, false>,   tcg::tc3_gemm_kernel<false, true, true, true>,
-      tcg::tc3_gemm_kernel<true, false, false, false>,  tcg::tc3_gemm_kernel<true, false, false, true>,
-      tcg::tc3_gemm_kernel<true, false, true, false>,   tcg::tc3_gemm_kernel<true, false, true, true>,
-      tcg::tc3_gemm_kernel<true, true, false, false>,   tcg::tc3_gemm_kernel<true, true, false, true>,
-      tcg::tc3_gemm_kernel<true, true, true, false>,    tcg::tc3_gemm_kernel<true, true, true, true>};
-  static std::atomic<bool> attr[16];  // cudaFuncSetAttribute done (idempotent)
-  const int which = (a_mn ? 8 : 0) + (b_mn ? 4 : 0) + (va ? 2 : 0) + (vb ? 1 : 0);
-  const KFn kern = table[which];
-  if (!attr[which]) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tcg::SMEM_BYTES) != cudaSuccess)
-      return fail("net_tc_gemm: cannot set shared-memory size");
-    attr[which].store(true);
-  }
-  kern<<<grid, tcg::THREADS, tcg::SMEM_BYTES, st>>>(a);
-  int rc = launched();
-  if (rc != NET_OK || S == 1) return rc;
-  const int64_t MP = M * N;
-  int64_t blocks = (MP + 255) / 256;
-  if (blocks > 1024) blocks = 1024;
-  gemm_nt_reduce<<<dim3((unsigned)blocks, (unsigned)T), 256, 0, st>>>(MP, (int)S, a.D, D);
-  return launched();
-}
-
-size_t net_tc_gemm_workspace_bytes(int64_t T, int64_t M, int64_t N, int64_t K, int64_t splits) {
-  if (T <= 0 || M <= 0 || N <= 0 || K <= 0 || splits <= 1) return 0;
-  int64_t kchunk = (K + splits - 1) / splits;
-  kchunk = (kchunk + tcg::BK - 1) / tcg::BK * tcg::BK;
-  if (kchunk < tcg::BK) kchunk = tcg::BK;
-  const int64_t S = (K + kchunk - 1) / kchunk;
-  return S > 1 ? (size_t)T * S * M * N * sizeof(float) : 0;
 }
 
 const char* net_last_error(void) { return g_err.c_str(); }

@@ -20,7 +20,6 @@ not the method; the optimizer step and its VJP run in libdiffopt.so.
 """
 from __future__ import annotations
 
-import os
 from dataclasses import dataclass
 
 import torch
@@ -296,30 +295,10 @@ def _wgrad_uses_split_k(T, M, P):
     return P <= 16 or T * ((M + 63) // 64) * ((P + 63) // 64) < 148
 
 
-USE_TC = os.environ.get("MAML_TC", "0") == "1"  # experimental: tcgen05 3xTF32 GEMMs
-
-
-def _tc_ok(T, n):
-    return USE_TC and T >= 16 and n >= 4096
-
-
-def _tc_call(T, M, Nn, K, A, sAm, sAk, bA, B, sBn, sBk, bB, D, ldD, bD, bias=None, splits=1):
-    from . import _net as N
-
-    wb = N.net_tc_gemm_workspace_bytes(T, M, Nn, K, splits)
-    ws = D.new_empty((wb + 3) // 4) if wb else None
-    N.net_tc_gemm(T, M, Nn, K, A, sAm, sAk, bA, B, sBn, sBk, bB, D, ldD, bD, bias, splits, ws)
-    return D
-
-
 def _wgrad_fwd(a, b):
     """a @ b^T, long contraction: split-K kernel or cuBLAS by shape."""
     T, M, n = a.shape
     P = b.shape[1]
-    if _tc_ok(T, n) and P > 16:  # D(m = p, n = co) = sum_n b[p][n] a[co][n]
-        a, b = a.contiguous(), b.contiguous()
-        out = a.new_empty(T, M, P)
-        return _tc_call(T, P, M, n, b, n, 1, P * n, a, n, 1, M * n, out, P, M * P, splits=8)
     if _wgrad_uses_split_k(T, M, P):
         return _gemm_nt(a, b)
     return torch.bmm(a, b.transpose(1, 2))
@@ -327,13 +306,6 @@ def _wgrad_fwd(a, b):
 
 def _conv_fwd(w, cols, bias):
     """bias + w @ cols (w [T, Co, K], cols [T, K, n])."""
-    T, Co, K = w.shape
-    n = cols.shape[2]
-    if _tc_ok(T, n):  # D(m = n_sp, n = co) = sum_k cols[k][m] w[co][k] (+ bias[co])
-        w, cols = w.contiguous(), cols.contiguous()
-        bias = bias.contiguous() if bias is not None else None
-        out = cols.new_empty(T, Co, n)
-        return _tc_call(T, n, Co, K, cols, 1, n, K * n, w, K, 1, Co * K, out, n, Co * n, bias)
     if bias is None:
         return torch.bmm(w, cols)
     return torch.baddbmm(bias.unsqueeze(-1), w, cols)

@@ -213,93 +213,6 @@ def test_task_conv_second_order(maml):
         close(a, r, tol=1e-4)
 
 
-def _tc(maml, A, B, bias=None, splits=1):
-    """net_tc_gemm on logical A [T, M, K], B [T, N, K] (any strides) -> D [T, N, M]
-    (m contiguous), i.e. D[t, n, m] = sum_k A[t, m, k] B[t, n, k] (+ bias[t, n])."""
-    from paper_2211_06934_b200 import _net as N
-
-    T, M, K = A.shape
-    Nn = B.shape[1]
-    D = torch.empty(T, Nn, M, device=DEV)
-    wb = N.net_tc_gemm_workspace_bytes(T, M, Nn, K, splits)
-    ws = torch.empty((wb + 3) // 4, device=DEV) if wb else None
-    N.net_tc_gemm(T, M, Nn, K, A, A.stride(1), A.stride(2), A.stride(0), B, B.stride(1),
-                  B.stride(2), B.stride(0), D, M, M * Nn, bias, splits, ws)
-    return D
-
-
-@pytest.mark.parametrize("layout", ["fwd", "dcols", "wgrad"])
-@pytest.mark.parametrize("shape", [(2, 300, 64, 576), (3, 130, 70, 33), (1, 128, 64, 32),
-                                   (2, 4900, 64, 576), (2, 1, 1, 1), (2, 200, 9, 9)])
-def test_tc_gemm_3xtf32_against_float64(maml, layout, shape):
-    """tcgen05 3xTF32 GEMM in the three operand layouts the convolutions use
-    (A m-contiguous / k-contiguous, B n- / k-contiguous), ragged tiles,
-    against the float64 product: fp32-GEMM accuracy (~K * 2^-22 of the
-    |a||b| scale), far below single-pass TF32 (2^-11)."""
-    T, M, Nn, K = shape
-    gen = torch.Generator(device=DEV).manual_seed(12)
-    if layout == "fwd":      # A(m, k) = cols[k][m]; B(n, k) = W[n][k]
-        A = torch.randn(T, K, M, device=DEV, generator=gen).transpose(1, 2)
-        B = torch.randn(T, Nn, K, device=DEV, generator=gen)
-    elif layout == "dcols":  # A(m, k) = dY[k][m]; B(n, k) = W[k][n]
-        A = torch.randn(T, K, M, device=DEV, generator=gen).transpose(1, 2)
-        B = torch.randn(T, K, Nn, device=DEV, generator=gen).transpose(1, 2)
-    else:                    # A(m, k) = cols[m][k]; B(n, k) = dY[n][k]
-        A = torch.randn(T, M, K, device=DEV, generator=gen)
-        B = torch.randn(T, Nn, K, device=DEV, generator=gen)
-    bias = torch.randn(T, Nn, device=DEV, generator=gen) if layout == "fwd" else None
-    D = _tc(maml, A, B, bias)
-    ref = torch.bmm(B.double(), A.double().transpose(1, 2))
-    if bias is not None:
-        ref = ref + bias.double()[:, :, None]
-    err = float((D.double() - ref).abs().max())
-    assert err <= 1e-5 * K ** 0.5 + 1e-6, err
-    tf32_err = 2.0 ** -11 * K ** 0.5  # what one TF32 pass would miss by
-    assert err < tf32_err / 20 or K < 4
-
-
-@pytest.mark.parametrize("splits", [2, 5])
-def test_tc_gemm_split_k(maml, splits):
-    T, M, Nn, K = 3, 576, 64, 4900
-    gen = torch.Generator(device=DEV).manual_seed(13)
-    A = torch.randn(T, M, K, device=DEV, generator=gen)
-    B = torch.randn(T, Nn, K, device=DEV, generator=gen)
-    D = _tc(maml, A, B, splits=splits)
-    ref = torch.bmm(B.double(), A.double().transpose(1, 2))
-    assert float((D.double() - ref).abs().max()) <= 1e-5 * K ** 0.5
-    assert torch.equal(D, _tc(maml, A, B, splits=splits))  # fixed order: reproducible
-
-
-def test_tc_gemm_network_path_meta_gradient(maml):
-    """Experimental tcgen05 3xTF32 convolutions (maml.USE_TC, engaged at
-    >= 16 tasks and >= 4096 positions): the second-order meta-gradient of a
-    16-task batch stays as close to float64 as the SIMT path's."""
-    import torch.nn.functional as F  # noqa: F401
-
-    T = 16
-    cfg = maml.MamlConfig(tasks=T, inner_steps=2)
-    phi = maml.init_params(0, DEV)
-    data = [maml.task_data(1, t, DEV) for t in range(T)]
-
-    def torch_inner(g, b, theta):
-        b1 = g if b is None else cfg.inner_momentum * b + g
-        return theta - cfg.inner_lr * b1, b1
-
-    d64 = [[a.double() if a.is_floating_point() else a for a in d] for d in data]
-    mg64, _ = maml.meta_grad_data(phi.double(), d64, maml.MamlConfig(tasks=T, inner_steps=2,
-                                                                      net="gemm"), torch_inner)
-    errs = {}
-    old = maml.USE_TC
-    try:
-        for tc in (False, True):
-            maml.USE_TC = tc
-            mg, _ = maml.meta_grad_batched(phi, data, cfg, maml.TaskBatchInner(T, DEV, cfg))
-            errs[tc] = float((mg.double() - mg64).norm() / mg64.norm())
-    finally:
-        maml.USE_TC = old
-    assert errs[True] < max(3 * errs[False], 2e-5), errs
-
-
 @pytest.mark.parametrize("geo,second_order", [((32, 64, 25, 28, 28), True),
                                               ((32, 64, 75, 28, 28), False)])
 def test_bnpool_full_size_32_tasks(maml, geo, second_order):
