@@ -206,7 +206,7 @@ def N():
 
 def test_header_symbols_exported(N):
     syms = declared()
-    assert len(syms) == 12
+    assert len(syms) == 10
     assert set(syms) == set(N.EXPORTS)
     for s in syms:
         assert hasattr(N.lib, s)
