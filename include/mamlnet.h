@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define MAMLNET_ABI_VERSION 1
+#define MAMLNET_ABI_VERSION 2
 #define NET_OK 0
 #define NET_EINVAL 1
 #define NET_ECUDA 3
@@ -106,6 +106,76 @@ int net_bnpool_bwd2(int64_t G, int64_t B, int64_t H, int64_t W, const float* gdx
 size_t net_gemm_nt_workspace_bytes(int64_t T, int64_t M, int64_t P, int64_t N);
 int net_gemm_nt(int64_t T, int64_t M, int64_t P, int64_t N, const float* A, const float* B,
                 float* C, void* workspace, size_t workspace_bytes, void* stream);
+
+/* As net_gemm_nt with a second operand pair and an accumulate flag:
+ *   C[t] (+)= A[t].B[t]^T + A2[t].B2[t]^T
+ * (A2, B2 both NULL = one pair; accumulate != 0 adds into C's contents).
+ * Both pairs' n-ranges are one launch, then one fixed-order reduce over all
+ * partials (bitwise reproducible). Workspace:
+ * net_gemm_nt2_workspace_bytes(T, M, P, N, npairs, accumulate). Used for the
+ * tangent of a convolution weight gradient, d(dy.cols^T) = dyd.cols^T +
+ * dy.colsd^T, accumulated into a parameter cotangent. */
+size_t net_gemm_nt2_workspace_bytes(int64_t T, int64_t M, int64_t P, int64_t N, int npairs,
+                                    int accumulate);
+int net_gemm_nt2(int64_t T, int64_t M, int64_t P, int64_t N, const float* A, const float* B,
+                 const float* A2, const float* B2, float* C, int accumulate, void* workspace,
+                 size_t workspace_bytes, void* stream);
+
+/* ---- forward-mode derivatives (Hessian-vector products of the inner loss,
+ * forward-over-reverse; the hand-scheduled MAML step) ---- */
+
+/* JVP of net_bnpool_fwd at (x, gamma, beta) along (xd, gd, bd) (gd, bd
+ * nullable = 0), with the forward's code/mean/rstd (routing is piecewise
+ * constant: held fixed). Per group, with r = rstd, xh = (x - mean)*r:
+ *   a = mean(xd), b = mean(xh*xd)                 -> s1[g] = a, s2[g] = b
+ *   xhd = r*(xd - a - xh*b)                       (tangent of xh)
+ *   outd[p] = gd*xh + gamma*xhd + bd at the window maximum of an active
+ *             window p, 0 for inactive windows. */
+int net_bnpool_jvp(int64_t G, int64_t B, int64_t H, int64_t W, const float* x, const float* xd,
+                   const float* gamma, const float* gd, const float* bd, const uint8_t* code,
+                   const float* mean, const float* rstd, float* outd, float* s1, float* s2,
+                   void* stream);
+
+/* JVP of net_bnpool_bwd at (dp, x, gamma) along (dpd, xd, gd) (gd nullable),
+ * given the backward's dgamma/dbeta and s1/s2 of net_bnpool_jvp for the same
+ * xd. dy / dyd = dp / dpd routed to the window maxima. With A = dbeta/n,
+ * Bm = dgamma/n, D = dy - A - xh*Bm (so dx = gamma*r*D) and xhd as above:
+ *   dbetad  = sum dyd                   (ADDED to dbd_acc[g]; nullable)
+ *   dgammad = sum (dyd*xh + dy*xhd)     (ADDED to dgd_acc[g]; nullable)
+ *   Dd  = dyd - dbetad/n - xhd*Bm - xh*dgammad/n
+ *   dxd = (gd*r - gamma*r^2*b)*D + gamma*r*Dd     (r' = -r^2*b) */
+int net_bnpool_bwd_jvp(int64_t G, int64_t B, int64_t H, int64_t W, const float* dp,
+                       const float* dpd, const uint8_t* code, const float* x, const float* xd,
+                       const float* gamma, const float* gd, const float* mean, const float* rstd,
+                       const float* dgamma, const float* dbeta, const float* s1, const float* s2,
+                       float* dxd, float* dgd_acc, float* dbd_acc, void* stream);
+
+/* Classifier head of T tasks, forward and backward in one launch (one CTA
+ * per task): feat[t][b][c] = h4[t][c][b] (the [T, C, B] pooled map),
+ * logits = feat.Wfc[t]^T + bfc[t] (Wfc [T, J, C], bfc [T, J]),
+ * loss[t] = mean over b of cross_entropy(logits[b], labels[t][b]) (int64),
+ * prob = softmax(logits) [T, B, J] (saved for the JVP), dl = (prob -
+ * onehot)/B, dW[t] = dl^T.feat, db[t] = sum_b dl, dh4[t][c][b] =
+ * (dl.Wfc)[b][c] (all written). */
+int net_fc_xent(int64_t T, int64_t B, int64_t C, int64_t J, const float* h4, const float* Wfc,
+                const float* bfc, const int64_t* labels, float* loss, float* prob, float* dW,
+                float* db, float* dh4, void* stream);
+
+/* JVP of net_fc_xent's (dW, db, dh4) along (h4d, Wd, bd) (each nullable = 0):
+ *   ld = featd.Wfc^T + feat.Wd^T + bd;  dld = prob*(ld - sum_j prob*ld)/B
+ *   dWd_acc[t] += dld^T.feat + dl^T.featd;  dbd_acc[t] += sum_b dld
+ *   dh4d[t][c][b] = (dld.Wfc + dl.Wd)[b][c]  (written). */
+int net_fc_xent_jvp(int64_t T, int64_t B, int64_t C, int64_t J, const float* h4, const float* h4d,
+                    const float* Wfc, const float* Wd, const float* bd, const int64_t* labels,
+                    const float* prob, float* dWd_acc, float* dbd_acc, float* dh4d,
+                    void* stream);
+
+/* Fold the task axis of a leaf-major T-task buffer: with per-task leaf
+ * offsets off[0..n_leaves] (host and device copies, off[0] = 0, monotone),
+ *   out[off[l] + i] = sum over t = 0..T-1 (in order) of in[T*off[l] + t*size_l + i].
+ * (theta_0 of every task is phi, so phi's cotangent is this sum.) */
+int net_task_sum(int64_t T, int64_t n_leaves, const int64_t* h_offsets, const int64_t* d_offsets,
+                 const float* in, float* out, void* stream);
 
 const char* net_last_error(void);
 int net_abi_version(void);

@@ -560,18 +560,21 @@ __global__ void __launch_bounds__(GTHREADS) gemm_nt_partial(int M, int P, int N,
                                                             const float* __restrict__ B,
                                                             float* __restrict__ out,
                                                             int64_t out_t_stride,
-                                                            int64_t out_s_stride) {
+                                                            int64_t out_s_stride, int S1,
+                                                            const float* __restrict__ A2,
+                                                            const float* __restrict__ B2) {
   constexpr int GP = 16 * TP;
   constexpr int AG = GM / 16, BG = GP / 16;  // 4-row groups per warp
   __shared__ __align__(16) float As[2][GK][GM + GPAD];
   __shared__ __align__(16) float Bs[2][GK][GP + GPAD];
-  const int t = blockIdx.z, s = blockIdx.y;
+  // splits [0, S1) contract (A, B), splits [S1, 2 S1) the second pair (A2, B2)
+  const int t = blockIdx.z, s = blockIdx.y, second = s >= S1, sl = second ? s - S1 : s;
   const int mt = blockIdx.x / ptiles, pt = blockIdx.x - mt * ptiles;
   const int m0 = mt * GM, p0 = pt * GP;
   const int nch = (N + GK - 1) / GK;
-  const int c0 = s * cps, c1 = min(nch, c0 + cps);
-  const float* At = A + (int64_t)t * M * N;
-  const float* Bt = B + (int64_t)t * P * N;
+  const int c0 = sl * cps, c1 = min(nch, c0 + cps);
+  const float* At = (second ? A2 : A) + (int64_t)t * M * N;
+  const float* Bt = (second ? B2 : B) + (int64_t)t * P * N;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // p: tx*TP.., m: ty*8..
   float4 ra[AG], rb[BG];
@@ -649,16 +652,16 @@ __global__ void __launch_bounds__(GTHREADS) gemm_nt_partial(int M, int P, int N,
   }
 }
 
-// C[t][e] = sum over s (in order) of part[t][s][e], e < M*P
+// C[t][e] (+)= sum over s (in order) of part[t][s][e], e < M*P
 __global__ void gemm_nt_reduce(int64_t MP, int S, const float* __restrict__ part,
-                               float* __restrict__ C) {
+                               float* __restrict__ C, int accumulate) {
   const int64_t t = blockIdx.y;
   const float* pt = part + t * S * MP;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < MP;
        e += (int64_t)gridDim.x * blockDim.x) {
     float acc = 0.f;
     for (int s = 0; s < S; ++s) acc += pt[(int64_t)s * MP + e];
-    C[t * MP + e] = acc;
+    C[t * MP + e] = accumulate ? C[t * MP + e] + acc : acc;
   }
 }
 
@@ -806,6 +809,298 @@ int launch_group_kernel(void (*kernel)(KArgs...), int64_t G, int64_t n, cudaStre
   return launch_clustered(kernel, G, cluster_for(G, n), 0, st, args...);
 }
 
+// ------------------------------------------- forward-mode (JVP) kernels
+// The hand-scheduled second-order MAML step (maml.ExplicitMaml) gets the
+// Hessian-vector products of the inner loss by forward-over-reverse
+// differentiation: tangents (ẋ, γ̇, β̇) ride along the forward pass and the
+// backward pass. Formulas: include/mamlnet.h (net_bnpool_jvp,
+// net_bnpool_bwd_jvp); derivation DESIGN.md §8.2.
+
+// JVP of bnpool_fwd at (x, gamma, beta) along (xd, gd, bd): one CTA cluster
+// per group; pass 1 the group sums S1 = sum xd, S2 = sum xh*xd (fp64),
+// pass 2 the pooled tangent at each active window's maximum.
+__global__ void __launch_bounds__(256, 8) bnpool_jvp_kernel(
+    int B, int H, int W, const float* __restrict__ x, const float* __restrict__ xd,
+    const float* __restrict__ gamma, const float* __restrict__ gd, const float* __restrict__ bd,
+    const uint8_t* __restrict__ code, const float* __restrict__ mean,
+    const float* __restrict__ rstd, float* __restrict__ outd, float* __restrict__ s1,
+    float* __restrict__ s2) {
+  __shared__ double sm[32 * 2 + 2];
+  __shared__ double part[2];
+  const Geo q(B, H, W);
+  const int kc = (int)cooperative_groups::this_cluster().num_blocks();
+  const int rank = (int)cooperative_groups::this_cluster().block_rank();
+  const int64_t g = blockIdx.x / kc;
+  const Slice es(q.n, rank, kc), ps(q.np, rank, kc);
+  const float* xg = x + g * q.n;
+  const float* xdg = xd + g * q.n;
+  const float m = mean[g], r = rstd[g];
+  double v[2] = {0.0, 0.0};
+  for (int i = es.lo + threadIdx.x; i < es.hi; i += blockDim.x) {
+    const float t = xdg[i];
+    v[0] += (double)t;
+    v[1] += (double)t * (double)((xg[i] - m) * r);
+  }
+  cluster_sum<2>(v, sm, part);
+  const float a = (float)(v[0] / q.n), b = (float)(v[1] / q.n);
+  if (threadIdx.x == 0 && rank == 0) {
+    s1[g] = a;
+    s2[g] = b;
+  }
+  const float ga = gamma[g], gdd = gd ? gd[g] : 0.f, bdd = bd ? bd[g] : 0.f;
+  const uint8_t* cg = code + g * q.np;
+  float* og = outd + g * q.np;
+  for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
+    const uint8_t c = cg[p];
+    float o = 0.f;
+    if (c != kOff) {
+      const int e = q.elem0(p) + q.off(c);
+      const float xh = (xg[e] - m) * r;
+      const float xhd = r * (xdg[e] - a - xh * b);
+      o = gdd * xh + ga * xhd + bdd;
+    }
+    og[p] = o;
+  }
+}
+
+// JVP of bnpool_bwd at (dp, x, gamma) along (dpd, xd, gd), with S1/n, S2/n
+// from bnpool_jvp of the same xd. Pass 1 (pooled): P1 = sum dyd,
+// P2 = sum dyd*xh, P3 = sum dy*xhd; pass 2 (every element) the tangent of dx.
+// dgd/dbd are ACCUMULATED (+=).
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) bnpool_bwd_jvp_kernel(
+    int B, int H, int W, const float* __restrict__ dp, const float* __restrict__ dpd,
+    const uint8_t* __restrict__ code, const float* __restrict__ x, const float* __restrict__ xd,
+    const float* __restrict__ gamma, const float* __restrict__ gd, const float* __restrict__ mean,
+    const float* __restrict__ rstd, const float* __restrict__ dgamma,
+    const float* __restrict__ dbeta, const float* __restrict__ s1, const float* __restrict__ s2,
+    float* __restrict__ dxd, float* __restrict__ dgd_acc, float* __restrict__ dbd_acc) {
+  __shared__ double sm[32 * 3 + 3];
+  __shared__ double part[3];
+  const Geo q(B, H, W);
+  const int kc = (int)cooperative_groups::this_cluster().num_blocks();
+  const int rank = (int)cooperative_groups::this_cluster().block_rank();
+  const int64_t g = blockIdx.x / kc;
+  const Slice ps(q.np, rank, kc);
+  const float* xg = x + g * q.n;
+  const float* xdg = xd + g * q.n;
+  const float* dpg = dp + g * q.np;
+  const float* dpdg = dpd + g * q.np;
+  const uint8_t* cg = code + g * q.np;
+  const float m = mean[g], r = rstd[g], a = s1[g], b = s2[g];
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
+    const uint8_t c = cg[p];
+    const float d = dpg[p], dd = dpdg[p];  // unconditional: only the x gathers depend on the code
+    if (c != kOff) {
+      const int e = q.elem0(p) + q.off(c);
+      const float xh = (xg[e] - m) * r;
+      const float xhd = r * (xdg[e] - a - xh * b);
+      v[0] += (double)dd;
+      v[1] += (double)dd * (double)xh;
+      v[2] += (double)d * (double)xhd;
+    }
+  }
+  cluster_sum<3>(v, sm, part);
+  const double nd = (double)q.n;
+  if (threadIdx.x == 0 && rank == 0) {
+    if (dbd_acc) dbd_acc[g] += (float)v[0];
+    if (dgd_acc) dgd_acc[g] += (float)(v[1] + v[2]);
+  }
+  const float ga = gamma[g], gdd = gd ? gd[g] : 0.f;
+  const float A = (float)((double)dbeta[g] / nd), Bm = (float)((double)dgamma[g] / nd);
+  const float Ad = (float)(v[0] / nd), Bmd = (float)((v[1] + v[2]) / nd);
+  // dxd = c1*D + c2*Dd, D = dy - A - xh*Bm, Dd = dyd - Ad - xhd*Bm - xh*Bmd
+  const float c1 = gdd * r - ga * r * r * b, c2 = ga * r;
+  float* og = dxd + g * q.n;
+  for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
+    const int e0 = q.elem0(p);
+    const uint8_t c = cg[p];
+    const float dl = dpg[p], ddl = dpdg[p];
+    const float d = c != kOff ? dl : 0.f, dd = c != kOff ? ddl : 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = e0 + q.off(k);
+      const float xh = (xg[e] - m) * r;
+      const float xhd = r * (xdg[e] - a - xh * b);
+      const float D = (c == k ? d : 0.f) - A - xh * Bm;
+      const float Dd = (c == k ? dd : 0.f) - Ad - xhd * Bm - xh * Bmd;
+      og[e] = c1 * D + c2 * Dd;
+    }
+  }
+  const Slice ls(q.nl, rank, kc);
+  for (int j = ls.lo + threadIdx.x; j < ls.hi; j += blockDim.x) {
+    const int e = q.left(j);
+    const float xh = (xg[e] - m) * r;
+    const float xhd = r * (xdg[e] - a - xh * b);
+    og[e] = c1 * (-A - xh * Bm) + c2 * (-Ad - xhd * Bm - xh * Bmd);
+  }
+}
+
+// ------------------------------------------- classifier head (fc + cross entropy)
+// One CTA per task: feat[b][c] = h4[t][c][b] (the 1x1 pooled map), logits =
+// feat.Wfc^T + bfc, per-task mean cross entropy over its B images, and the
+// whole backward of that loss. Shared memory: feat [C][B] (+ tangent),
+// W [J][C] (+ tangent), probabilities and dlogits [B][J].
+constexpr int kHeadThreads = 256;
+
+__device__ __forceinline__ float block_sum_f(float v, float* red) {
+  // fixed-order block sum (warp xor tree, then warp totals in order)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  float s = 0.f;
+  for (int w = 0; w < nw; ++w) s += red[w];
+  return s;
+}
+
+__global__ void __launch_bounds__(kHeadThreads) fc_xent_kernel(
+    int B, int C, int J, float inv_b, const float* __restrict__ h4, const float* __restrict__ Wfc,
+    const float* __restrict__ bfc, const int64_t* __restrict__ labels, float* __restrict__ loss,
+    float* __restrict__ prob, float* __restrict__ dW, float* __restrict__ db,
+    float* __restrict__ dh4) {
+  extern __shared__ float hs[];
+  float* f = hs;              // [C][B]
+  float* w = f + C * B;       // [J][C]
+  float* pr = w + J * C;      // [B][J] probabilities, then dlogits
+  __shared__ float red[32];
+  const int64_t t = blockIdx.x;
+  const float* ht = h4 + t * C * B;
+  for (int i = threadIdx.x; i < C * B; i += blockDim.x) f[i] = ht[i];
+  for (int i = threadIdx.x; i < J * C; i += blockDim.x) w[i] = Wfc[t * J * C + i];
+  __syncthreads();
+  for (int o = threadIdx.x; o < B * J; o += blockDim.x) {
+    const int b = o / J, j = o - b * J;
+    float z = bfc[t * J + j];
+    for (int c = 0; c < C; ++c) z = fmaf(f[c * B + b], w[j * C + c], z);
+    pr[o] = z;
+  }
+  __syncthreads();
+  float lsum = 0.f;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    float* z = pr + b * J;
+    float mx = z[0];
+    for (int j = 1; j < J; ++j) mx = fmaxf(mx, z[j]);
+    float se = 0.f;
+    for (int j = 0; j < J; ++j) se += expf(z[j] - mx);
+    const int y = (int)labels[t * B + b];
+    lsum += logf(se) + mx - z[y];
+    const float ise = 1.f / se;
+    for (int j = 0; j < J; ++j) {
+      const float p = expf(z[j] - mx) * ise;
+      prob[(t * B + b) * J + j] = p;
+      z[j] = (p - (j == y ? 1.f : 0.f)) * inv_b;  // dlogits
+    }
+  }
+  lsum = block_sum_f(lsum, red);
+  if (threadIdx.x == 0) loss[t] = lsum * inv_b;
+  __syncthreads();
+  for (int o = threadIdx.x; o < J * C; o += blockDim.x) {
+    const int j = o / C, c = o - j * C;
+    float s = 0.f;
+    for (int b = 0; b < B; ++b) s = fmaf(pr[b * J + j], f[c * B + b], s);
+    dW[t * J * C + o] = s;
+  }
+  for (int j = threadIdx.x; j < J; j += blockDim.x) {
+    float s = 0.f;
+    for (int b = 0; b < B; ++b) s += pr[b * J + j];
+    db[t * J + j] = s;
+  }
+  for (int o = threadIdx.x; o < C * B; o += blockDim.x) {
+    const int c = o / B, b = o - c * B;
+    float s = 0.f;
+    for (int j = 0; j < J; ++j) s = fmaf(pr[b * J + j], w[j * C + c], s);
+    dh4[t * C * B + o] = s;
+  }
+}
+
+// JVP of fc_xent's gradient outputs along (h4d, Wd, bd); dWd/dbd accumulated.
+__global__ void __launch_bounds__(kHeadThreads) fc_xent_jvp_kernel(
+    int B, int C, int J, float inv_b, const float* __restrict__ h4, const float* __restrict__ h4d,
+    const float* __restrict__ Wfc, const float* __restrict__ Wd, const float* __restrict__ bd,
+    const int64_t* __restrict__ labels, const float* __restrict__ prob,
+    float* __restrict__ dWd_acc, float* __restrict__ dbd_acc, float* __restrict__ dh4d) {
+  extern __shared__ float hs[];
+  float* f = hs;              // [C][B]
+  float* fd = f + C * B;      // [C][B]
+  float* w = fd + C * B;      // [J][C]
+  float* wd = w + J * C;      // [J][C]
+  float* dl = wd + J * C;     // [B][J] dlogits
+  float* dld = dl + B * J;    // [B][J] their tangent
+  const int64_t t = blockIdx.x;
+  for (int i = threadIdx.x; i < C * B; i += blockDim.x) {
+    f[i] = h4[t * C * B + i];
+    fd[i] = h4d ? h4d[t * C * B + i] : 0.f;
+  }
+  for (int i = threadIdx.x; i < J * C; i += blockDim.x) {
+    w[i] = Wfc[t * J * C + i];
+    wd[i] = Wd ? Wd[t * J * C + i] : 0.f;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < B * J; o += blockDim.x) {  // logit tangents
+    const int b = o / J, j = o - b * J;
+    float z = bd ? bd[t * J + j] : 0.f;
+    for (int c = 0; c < C; ++c) z = fmaf(fd[c * B + b], w[j * C + c], fmaf(f[c * B + b], wd[j * C + c], z));
+    dld[o] = z;
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {  // softmax Jacobian
+    const float* p = prob + (t * B + b) * J;
+    const int y = (int)labels[t * B + b];
+    float sp = 0.f;
+    for (int j = 0; j < J; ++j) sp = fmaf(p[j], dld[b * J + j], sp);
+    for (int j = 0; j < J; ++j) {
+      dld[b * J + j] = p[j] * (dld[b * J + j] - sp) * inv_b;
+      dl[b * J + j] = (p[j] - (j == y ? 1.f : 0.f)) * inv_b;
+    }
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < J * C; o += blockDim.x) {
+    const int j = o / C, c = o - j * C;
+    float s = 0.f;
+    for (int b = 0; b < B; ++b)
+      s = fmaf(dld[b * J + j], f[c * B + b], fmaf(dl[b * J + j], fd[c * B + b], s));
+    if (dWd_acc) dWd_acc[t * J * C + o] += s;
+  }
+  for (int j = threadIdx.x; j < J; j += blockDim.x) {
+    float s = 0.f;
+    for (int b = 0; b < B; ++b) s += dld[b * J + j];
+    if (dbd_acc) dbd_acc[t * J + j] += s;
+  }
+  for (int o = threadIdx.x; o < C * B; o += blockDim.x) {
+    const int c = o / B, b = o - c * B;
+    float s = 0.f;
+    for (int j = 0; j < J; ++j)
+      s = fmaf(dld[b * J + j], w[j * C + c], fmaf(dl[b * J + j], wd[j * C + c], s));
+    dh4d[t * C * B + o] = s;
+  }
+}
+
+// ------------------------------------------- sum over the task axis
+// out[off[l] + i] = sum over t (in order) of in[T*off[l] + t*size_l + i]:
+// the leaf-major [leaf][T][size] buffer of T tasks' parameter cotangents
+// folded into one tree (theta_0 = phi broadcast -> its cotangent).
+__global__ void task_sum_kernel(int64_t T, int64_t nl, const int64_t* __restrict__ off,
+                                const float* __restrict__ in, float* __restrict__ out) {
+  const int64_t n = off[nl];
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = nl - 1;  // last leaf l with off[l] <= o
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (off[mid] <= o) lo = mid; else hi = mid - 1;
+    }
+    const int64_t size = off[lo + 1] - off[lo], i = o - off[lo];
+    const float* src = in + T * off[lo] + i;
+    float s = 0.f;
+    for (int64_t t = 0; t < T; ++t) s += src[t * size];
+    out[o] = s;
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -879,45 +1174,168 @@ int net_bnpool_bwd2(int64_t G, int64_t B, int64_t H, int64_t W, const float* gdx
                           g_gamma);
 }
 
+// C (+)= A.B^T (+ A2.B2^T): one partial launch over npairs x S n-ranges, then
+// the fixed-order reduce (skipped only for one pair, S = 1, no accumulate).
+static size_t gemm_nt_need(int64_t T, int64_t M, int64_t P, int64_t N, int npairs, int accumulate) {
+  if (T <= 0 || M <= 0 || P <= 0 || N <= 0) return 0;
+  SplitPlan q = split_plan(T * npairs, M, P, N);
+  if (npairs == 1 && q.S == 1 && !accumulate) return 0;
+  return (size_t)T * npairs * q.S * M * P * sizeof(float);
+}
+
+static int gemm_nt_run(const char* who, int64_t T, int64_t M, int64_t P, int64_t N,
+                       const float* A, const float* B, const float* A2, const float* B2,
+                       float* C, int accumulate, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  static thread_local std::string msg;
+  auto bad = [&](const char* what) {
+    msg = std::string(who) + ": " + what;
+    return fail(msg.c_str());
+  };
+  if (T < 0 || M < 0 || P < 0 || N < 0 || T > 65535 || M > (1 << 20) || P > (1 << 20) ||
+      N > ((int64_t)1 << 31) - 64 || M * N > ((int64_t)1 << 40))
+    return bad("bad sizes");
+  if (T == 0 || M == 0 || P == 0) return NET_OK;
+  if (!C) return bad("NULL C");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (N == 0) {
+    if (accumulate) return NET_OK;
+    if (cudaMemsetAsync(C, 0, (size_t)T * M * P * sizeof(float), st) != cudaSuccess)
+      return bad("memset failed");
+    return NET_OK;
+  }
+  if (!A || !B) return bad("NULL operand");
+  if ((A2 == nullptr) != (B2 == nullptr)) return bad("A2 and B2 must both be given or both NULL");
+  const int npairs = A2 ? 2 : 1;
+  SplitPlan q = split_plan(T * npairs, M, P, N);
+  const size_t need = gemm_nt_need(T, M, P, N, npairs, accumulate);
+  if (need && (!workspace || workspace_bytes < need))
+    return bad("workspace too small (see the *_workspace_bytes function)");
+  const int slots = npairs * q.S;
+  dim3 grid((unsigned)(q.mtiles * q.ptiles), (unsigned)slots, (unsigned)T);
+  float* out = need ? (float*)workspace : C;
+  const int64_t MP = M * P;
+  if (q.tp == 4)
+    gemm_nt_partial<4><<<grid, GTHREADS, 0, st>>>((int)M, (int)P, (int)N, q.ptiles, q.cps, A, B,
+                                                   out, slots * MP, MP, q.S, A2, B2);
+  else
+    gemm_nt_partial<1><<<grid, GTHREADS, 0, st>>>((int)M, (int)P, (int)N, q.ptiles, q.cps, A, B,
+                                                   out, slots * MP, MP, q.S, A2, B2);
+  int rc = launched();
+  if (rc != NET_OK || !need) return rc;
+  int64_t blocks = (MP + 255) / 256;
+  if (blocks > 1024) blocks = 1024;
+  gemm_nt_reduce<<<dim3((unsigned)blocks, (unsigned)T), 256, 0, st>>>(MP, slots, out, C,
+                                                                       accumulate);
+  return launched();
+}
+
 size_t net_gemm_nt_workspace_bytes(int64_t T, int64_t M, int64_t P, int64_t N) {
-  if (T < 0 || M < 0 || P < 0 || N < 0) return 0;
-  if (T == 0 || M == 0 || P == 0 || N == 0) return 0;
-  SplitPlan q = split_plan(T, M, P, N);
-  return q.S > 1 ? (size_t)T * q.S * M * P * sizeof(float) : 0;
+  return gemm_nt_need(T, M, P, N, 1, 0);
 }
 
 int net_gemm_nt(int64_t T, int64_t M, int64_t P, int64_t N, const float* A, const float* B,
                 float* C, void* workspace, size_t workspace_bytes, void* stream) {
-  if (T < 0 || M < 0 || P < 0 || N < 0 || T > 65535 || M > (1 << 20) || P > (1 << 20) ||
-      N > ((int64_t)1 << 31) - 64 || M * N > ((int64_t)1 << 40))
-    return fail("net_gemm_nt: bad sizes");
-  if (T == 0 || M == 0 || P == 0) return NET_OK;
-  if (!C) return fail("net_gemm_nt: NULL C");
-  cudaStream_t st = (cudaStream_t)stream;
-  if (N == 0) {
-    if (cudaMemsetAsync(C, 0, (size_t)T * M * P * sizeof(float), st) != cudaSuccess)
-      return fail("net_gemm_nt: memset failed");
-    return NET_OK;
-  }
-  if (!A || !B) return fail("net_gemm_nt: NULL operand");
-  SplitPlan q = split_plan(T, M, P, N);
-  const size_t need = q.S > 1 ? (size_t)T * q.S * M * P * sizeof(float) : 0;
-  if (need && (!workspace || workspace_bytes < need))
-    return fail("net_gemm_nt: workspace too small (net_gemm_nt_workspace_bytes)");
-  dim3 grid((unsigned)(q.mtiles * q.ptiles), (unsigned)q.S, (unsigned)T);
-  float* out = q.S > 1 ? (float*)workspace : C;
-  const int64_t MP = M * P;
-  if (q.tp == 4)
-    gemm_nt_partial<4><<<grid, GTHREADS, 0, st>>>((int)M, (int)P, (int)N, q.ptiles, q.cps, A, B,
-                                                   out, q.S * MP, MP);
-  else
-    gemm_nt_partial<1><<<grid, GTHREADS, 0, st>>>((int)M, (int)P, (int)N, q.ptiles, q.cps, A, B,
-                                                   out, q.S * MP, MP);
-  int rc = launched();
-  if (rc != NET_OK || q.S == 1) return rc;
-  int64_t blocks = (MP + 255) / 256;
-  if (blocks > 1024) blocks = 1024;
-  gemm_nt_reduce<<<dim3((unsigned)blocks, (unsigned)T), 256, 0, st>>>(MP, q.S, out, C);
+  return gemm_nt_run("net_gemm_nt", T, M, P, N, A, B, nullptr, nullptr, C, 0, workspace,
+                     workspace_bytes, stream);
+}
+
+size_t net_gemm_nt2_workspace_bytes(int64_t T, int64_t M, int64_t P, int64_t N, int npairs,
+                                    int accumulate) {
+  if (npairs != 1 && npairs != 2) return 0;
+  return gemm_nt_need(T, M, P, N, npairs, accumulate != 0);
+}
+
+int net_gemm_nt2(int64_t T, int64_t M, int64_t P, int64_t N, const float* A, const float* B,
+                 const float* A2, const float* B2, float* C, int accumulate, void* workspace,
+                 size_t workspace_bytes, void* stream) {
+  return gemm_nt_run("net_gemm_nt2", T, M, P, N, A, B, A2, B2, C, accumulate != 0, workspace,
+                     workspace_bytes, stream);
+}
+
+int net_bnpool_jvp(int64_t G, int64_t B, int64_t H, int64_t W, const float* x, const float* xd,
+                   const float* gamma, const float* gd, const float* bd, const uint8_t* code,
+                   const float* mean, const float* rstd, float* outd, float* s1, float* s2,
+                   void* stream) {
+  if (!geo_ok(G, B, H, W, true)) return fail("net_bnpool_jvp: bad geometry");
+  if (G == 0) return NET_OK;
+  if (!x || !xd || !gamma || !code || !mean || !rstd || !outd || !s1 || !s2)
+    return fail("net_bnpool_jvp: NULL pointer");
+  return launch_group_kernel(bnpool_jvp_kernel, G, B * H * W, (cudaStream_t)stream, (int)B,
+                             (int)H, (int)W, x, xd, gamma, gd, bd, code, mean, rstd, outd, s1, s2);
+}
+
+int net_bnpool_bwd_jvp(int64_t G, int64_t B, int64_t H, int64_t W, const float* dp,
+                       const float* dpd, const uint8_t* code, const float* x, const float* xd,
+                       const float* gamma, const float* gd, const float* mean, const float* rstd,
+                       const float* dgamma, const float* dbeta, const float* s1, const float* s2,
+                       float* dxd, float* dgd_acc, float* dbd_acc, void* stream) {
+  if (!geo_ok(G, B, H, W, true)) return fail("net_bnpool_bwd_jvp: bad geometry");
+  if (G == 0) return NET_OK;
+  if (!dp || !dpd || !code || !x || !xd || !gamma || !mean || !rstd || !dgamma || !dbeta || !s1 ||
+      !s2 || !dxd)
+    return fail("net_bnpool_bwd_jvp: NULL pointer");
+  const int kc = cluster_for(G, B * H * W);
+  const int64_t slice = B * H * W / kc;
+  auto* kernel = slice > 2048 && slice <= 8192 ? bnpool_bwd_jvp_kernel<8> : bnpool_bwd_jvp_kernel<6>;
+  return launch_clustered(kernel, G, kc, 0, (cudaStream_t)stream, (int)B, (int)H, (int)W, dp, dpd,
+                          code, x, xd, gamma, gd, mean, rstd, dgamma, dbeta, s1, s2, dxd, dgd_acc,
+                          dbd_acc);
+}
+
+static int head_smem(const void* kernel, size_t bytes) {
+  if (bytes > 227 * 1024) return fail("head: B*C too large for shared memory");
+  if (bytes > 48 * 1024 &&
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+          cudaSuccess)
+    return fail("head: cannot raise the dynamic shared-memory limit");
+  return NET_OK;
+}
+
+int net_fc_xent(int64_t T, int64_t B, int64_t C, int64_t J, const float* h4, const float* Wfc,
+                const float* bfc, const int64_t* labels, float* loss, float* prob, float* dW,
+                float* db, float* dh4, void* stream) {
+  if (T < 0 || B < 1 || C < 1 || J < 1 || T > 65535 || B * C > (1 << 24) || J > 1024)
+    return fail("net_fc_xent: bad sizes");
+  if (T == 0) return NET_OK;
+  if (!h4 || !Wfc || !bfc || !labels || !loss || !prob || !dW || !db || !dh4)
+    return fail("net_fc_xent: NULL pointer");
+  const size_t bytes = (size_t)(C * B + J * C + B * J) * sizeof(float);
+  if (int rc = head_smem((const void*)fc_xent_kernel, bytes)) return rc;
+  fc_xent_kernel<<<(unsigned)T, kHeadThreads, bytes, (cudaStream_t)stream>>>(
+      (int)B, (int)C, (int)J, 1.0f / (float)B, h4, Wfc, bfc, labels, loss, prob, dW, db, dh4);
+  return launched();
+}
+
+int net_fc_xent_jvp(int64_t T, int64_t B, int64_t C, int64_t J, const float* h4, const float* h4d,
+                    const float* Wfc, const float* Wd, const float* bd, const int64_t* labels,
+                    const float* prob, float* dWd_acc, float* dbd_acc, float* dh4d,
+                    void* stream) {
+  if (T < 0 || B < 1 || C < 1 || J < 1 || T > 65535 || B * C > (1 << 24) || J > 1024)
+    return fail("net_fc_xent_jvp: bad sizes");
+  if (T == 0) return NET_OK;
+  if (!h4 || !Wfc || !labels || !prob || !dh4d) return fail("net_fc_xent_jvp: NULL pointer");
+  const size_t bytes = (size_t)(2 * C * B + 2 * J * C + 2 * B * J) * sizeof(float);
+  if (int rc = head_smem((const void*)fc_xent_jvp_kernel, bytes)) return rc;
+  fc_xent_jvp_kernel<<<(unsigned)T, kHeadThreads, bytes, (cudaStream_t)stream>>>(
+      (int)B, (int)C, (int)J, 1.0f / (float)B, h4, h4d, Wfc, Wd, bd, labels, prob, dWd_acc,
+      dbd_acc, dh4d);
+  return launched();
+}
+
+int net_task_sum(int64_t T, int64_t n_leaves, const int64_t* h_offsets, const int64_t* d_offsets,
+                 const float* in, float* out, void* stream) {
+  if (T < 0 || n_leaves < 1 || !h_offsets || !d_offsets) return fail("net_task_sum: bad arguments");
+  if (h_offsets[0] != 0) return fail("net_task_sum: offsets[0] must be 0");
+  for (int64_t l = 0; l < n_leaves; ++l)
+    if (h_offsets[l + 1] < h_offsets[l]) return fail("net_task_sum: offsets must be monotone");
+  const int64_t n = h_offsets[n_leaves];
+  if (n == 0) return NET_OK;
+  if (!in || !out) return fail("net_task_sum: NULL pointer");
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  task_sum_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(T, n_leaves, d_offsets, in,
+                                                                    out);
   return launched();
 }
 

@@ -1,0 +1,293 @@
+"""Hand-scheduled second-order MAML meta-gradient.
+
+The autograd form (maml.meta_grad_batched, create_graph=True) records the
+network's backward as a graph and differentiates it again, which costs ~890
+kernels per 4-task outer step, a quarter of them PyTorch adds, copies and
+reductions that sum cotangents autograd could not fuse. Here the whole
+meta-gradient is an explicit schedule of libmamlnet.so / libdiffopt.so /
+cuBLAS calls (~370 per outer step at any task count), captured in one CUDA
+graph by ExplicitShard:
+
+Inner loop (MAML; 5 SGD-momentum steps, the optimizer of row a7):
+    for k = 0..K-1:  g_k = grad L_s(theta_k)        (forward + backward, saved)
+                     b_{k+1} = mu b_k + g_k;  theta_{k+1} = theta_k - lr b_{k+1}
+                     (ONE fused opt_sgd_fwd launch with apply, all T tasks)
+Outer reverse sweep (row a9's recurrence with the SGD VJP of row a7):
+    theta_bar_K = grad L_q(theta_K);  b_bar_K = 0
+    for k = K-1..0:  (v, b_bar_k) = opt_sgd_bwd(u_bar = theta_bar_{k+1}, b_bar_{k+1})
+                     theta_bar_k = theta_bar_{k+1} + H_k v     (H_k = Hessian of L_s at theta_k)
+    phi_bar = sum over tasks of theta_bar_0           (theta_0 = phi for every task)
+
+The Hessian-vector product is forward-over-reverse: the tangent v of theta
+rides through the saved forward pass and the saved backward pass (Pearlmutter's
+R-operator), every tangent computed once and every sum landing in a GEMM
+accumulator or a kernel's `+=` epilogue, so there is no cotangent glue:
+    conv:      Ry = RW.cols + W.Rcols;   R(dW) = Rdy.cols^T + dy.Rcols^T (+= theta_bar)
+               R(dcols) = RW^T.dy + W^T.Rdy;   Rdh = col2im(R dcols)
+    norm/pool: net_bnpool_jvp / net_bnpool_bwd_jvp (include/mamlnet.h)
+    head:      net_fc_xent_jvp
+Conv biases feed training-mode batch norms and are inert (reading N5): their
+gradients, tangents and meta-gradients are exactly zero and never touched.
+
+Layout: the T tasks' parameters are one leaf-major flat buffer (leaf l is a
+[T, size_l] block; conv weight l is [T, 64, Cin*9], the im2col row order),
+activations task-major [T, C, B, H, W] (maml.conv4_forward_tasks' "fused"
+form). Every intermediate of the K inner steps is kept (about 1 GB per step
+at 32 tasks): nothing is recomputed in the reverse sweep.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import _net as N
+from .maml import (BN_EPS, CONV4_SHAPES, HW, WAYS, MamlConfig, _wgrad_uses_split_k, sizes_of,
+                   task_data)
+
+C = 64                      # channels of every conv block
+LAYER_H = (28, 14, 7, 3)    # input spatial size of conv block l (3x3, padding 1)
+LAYER_CIN = (1, 64, 64, 64)
+
+
+class _Acts:
+    """Saved forward/backward intermediates of one gradient evaluation."""
+
+    def __init__(self, T, B, dev, with_cols=True):
+        self.B = B
+        self.cols = [None] * 4      # cols[0] is the image's (shared, set by the caller)
+        self.y, self.code, self.mean, self.rstd, self.h, self.dh, self.dy = ([None] * 4 for _ in
+                                                                               range(7))
+        for l, H in enumerate(LAYER_H):
+            n = B * H * H
+            if l > 0 and with_cols:
+                self.cols[l] = torch.empty(T, LAYER_CIN[l] * 9, n, device=dev)
+            self.y[l] = torch.empty(T, C, n, device=dev)
+            self.dy[l] = torch.empty(T, C, n, device=dev)
+            H2 = H // 2
+            self.h[l] = torch.empty(T, C, B * H2 * H2, device=dev)
+            self.dh[l] = torch.empty(T, C, B * H2 * H2, device=dev)
+            self.code[l] = torch.empty(T, C, B * H2 * H2, dtype=torch.uint8, device=dev)
+            self.mean[l] = torch.empty(T * C, device=dev)
+            self.rstd[l] = torch.empty(T * C, device=dev)
+        self.prob = torch.empty(T, B, WAYS, device=dev)
+        self.loss = torch.empty(T, device=dev)
+
+
+class ExplicitMaml:
+    """Meta-gradient of T tasks through K inner SGD-momentum steps, run as
+    an explicit kernel schedule (module docstring). Buffers are allocated
+    once for (T, n_support, n_query); meta_grad() only launches work on the
+    current stream (graph-capturable)."""
+
+    def __init__(self, T, cfg: MamlConfig, device, n_support=WAYS * 5, n_query=WAYS * 15):
+        if cfg.nesterov:
+            raise NotImplementedError("ExplicitMaml: plain SGD momentum only (the C4 recipe)")
+        dev = torch.device(device)
+        self.T, self.cfg, self.dev = int(T), cfg, dev
+        self.K = int(cfg.inner_steps)
+        sizes = sizes_of(CONV4_SHAPES)
+        self.n = sum(sizes)
+        self.off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        self.h_off = torch.from_numpy(self.off.copy())          # host copy (net_task_sum)
+        self.d_off = self.h_off.to(dev)
+        self.tree = L.Tree(numel=self.T * self.n, device=dev)
+        self.hp = (cfg.inner_lr, cfg.inner_momentum, False)
+        Tn = self.T * self.n
+        # theta_0..theta_K, b_1..b_K, g_0..g_{K-1}; conv-bias slices of g stay 0
+        self.theta = [torch.empty(Tn, device=dev) for _ in range(self.K + 1)]
+        self.b = [None] + [torch.empty(Tn, device=dev) for _ in range(self.K)]
+        self.g = [torch.zeros(Tn, device=dev) for _ in range(self.K)]
+        self.theta_bar = torch.zeros(Tn, device=dev)
+        self.b_bar = torch.empty(Tn, device=dev)
+        self.v = torch.empty(Tn, device=dev)
+        self.mg = torch.empty(self.n, device=dev)
+        # theta_0 = phi broadcast to every task: one gather
+        idx = [self.off[l] + np.tile(np.arange(sizes[l]), self.T) for l in range(len(sizes))]
+        self.bcast = torch.from_numpy(np.concatenate(idx)).to(dev)
+        # saved intermediates: one set per inner step (support), one for the query
+        self.Bs, self.Bq = int(n_support), int(n_query)
+        self.acts = [_Acts(self.T, self.Bs, dev) for _ in range(self.K)]
+        self.acts_q = _Acts(self.T, self.Bq, dev)
+        self.cols1_s = torch.empty(self.T, 9, self.Bs * HW * HW, device=dev)
+        self.cols1_q = torch.empty(self.T, 9, self.Bq * HW * HW, device=dev)
+        # tangent scratch (reused by every HVP) and the input-gradient scratch
+        self.tan = _Acts(self.T, self.Bs, dev)
+        self.s1 = [torch.empty(self.T * C, device=dev) for _ in range(4)]
+        self.s2 = [torch.empty(self.T * C, device=dev) for _ in range(4)]
+        nmax = max(self.Bs, self.Bq) * LAYER_H[1] ** 2
+        self.dcols = torch.empty(self.T * C * 9 * nmax, device=dev)
+        self.labels_s = torch.empty(self.T, self.Bs, dtype=torch.int64, device=dev)
+        self.labels_q = torch.empty(self.T, self.Bq, dtype=torch.int64, device=dev)
+        self.xs = torch.empty(self.T, 1, self.Bs, HW, HW, device=dev)
+        self.xq = torch.empty(self.T, 1, self.Bq, HW, HW, device=dev)
+        # split-K workspace: the largest of every weight-gradient call
+        need = 0
+        for B in (self.Bs, self.Bq):
+            for l, H in enumerate(LAYER_H):
+                for npairs in (1, 2):
+                    for acc in (0, 1):
+                        need = max(need, N.net_gemm_nt2_workspace_bytes(
+                            self.T, C, LAYER_CIN[l] * 9, B * H * H, npairs, acc))
+        self.ws = torch.empty(max(1, (need + 3) // 4), device=dev)
+
+    # ----------------------------------------------------------- views
+    def leaf(self, buf, l):
+        """Leaf l of a leaf-major T-task buffer as [T, *shape]."""
+        a, b = self.T * int(self.off[l]), self.T * int(self.off[l + 1])
+        return buf[a:b].view(self.T, *CONV4_SHAPES[l])
+
+    def _w(self, buf, l):    # conv weight of block l as [T, 64, Cin*9]
+        return self.leaf(buf, 4 * l).reshape(self.T, C, LAYER_CIN[l] * 9)
+
+    def _gamma(self, buf, l):
+        return self.leaf(buf, 4 * l + 2)
+
+    def _beta(self, buf, l):
+        return self.leaf(buf, 4 * l + 3)
+
+    # ------------------------------------------------------ contractions
+    def _wgrad(self, dy, cols, out, dy2=None, cols2=None, accumulate=False):
+        """out (+)= dy.cols^T (+ dy2.cols2^T): the weight-gradient shape."""
+        T, M, n = dy.shape
+        P = cols.shape[1]
+        if _wgrad_uses_split_k(T, M, P):
+            N.net_gemm_nt2(T, M, P, n, dy, cols, dy2, cols2, out, accumulate, self.ws)
+            return
+        if accumulate:
+            out.baddbmm_(dy, cols.transpose(1, 2))
+        else:
+            torch.bmm(dy, cols.transpose(1, 2), out=out)
+        if dy2 is not None:
+            out.baddbmm_(dy2, cols2.transpose(1, 2))
+
+    def _dcols(self, l, n):
+        return self.dcols[:self.T * LAYER_CIN[l] * 9 * n].view(self.T, LAYER_CIN[l] * 9, n)
+
+    # ----------------------------------------------------------- gradient
+    def _grad(self, theta, cols1, labels, A: _Acts, g):
+        """Forward + backward of the T tasks' losses at theta; saves A,
+        writes the gradient into g (conv-bias slices untouched) and the
+        per-task losses into A.loss."""
+        T, B = self.T, A.B
+        A.cols[0] = cols1
+        for l, H in enumerate(LAYER_H):
+            if l > 0:
+                N.net_im2col3x3(T * C, B, H, H, A.h[l - 1], A.cols[l])
+            torch.bmm(self._w(theta, l), A.cols[l], out=A.y[l])
+            N.net_bnpool_fwd(T * C, B, H, H, A.y[l], self._gamma(theta, l), self._beta(theta, l),
+                             BN_EPS, A.h[l], A.code[l], A.mean[l], A.rstd[l])
+        N.net_fc_xent(T, B, C, WAYS, A.h[3], self.leaf(theta, 16), self.leaf(theta, 17), labels,
+                      A.loss, A.prob, self.leaf(g, 16), self.leaf(g, 17), A.dh[3])
+        for l in range(3, -1, -1):
+            H = LAYER_H[l]
+            N.net_bnpool_bwd(T * C, B, H, H, A.dh[l], A.code[l], A.y[l], self._gamma(theta, l),
+                             A.mean[l], A.rstd[l], A.dy[l], self._gamma(g, l), self._beta(g, l))
+            self._wgrad(A.dy[l], A.cols[l], self._w(g, l))
+            if l > 0:
+                dc = self._dcols(l, B * H * H)
+                torch.bmm(self._w(theta, l).transpose(1, 2), A.dy[l], out=dc)
+                N.net_col2im3x3(T * C, B, LAYER_H[l - 1] // 2, LAYER_H[l - 1] // 2, dc, A.dh[l - 1])
+
+    # ------------------------------------------------------ Hessian-vector
+    def _hvp(self, theta, g, A: _Acts, v, acc):
+        """acc += H(theta) v for the support loss whose gradient pass saved A
+        and g (forward-over-reverse; module docstring)."""
+        T, B, R = self.T, A.B, self.tan
+        for l, H in enumerate(LAYER_H):        # forward tangents
+            torch.bmm(self._w(v, l), A.cols[l], out=R.y[l])
+            if l > 0:
+                N.net_im2col3x3(T * C, B, H, H, R.h[l - 1], R.cols[l])
+                R.y[l].baddbmm_(self._w(theta, l), R.cols[l])
+            N.net_bnpool_jvp(T * C, B, H, H, A.y[l], R.y[l], self._gamma(theta, l),
+                             self._gamma(v, l), self._beta(v, l), A.code[l], A.mean[l],
+                             A.rstd[l], R.h[l], self.s1[l], self.s2[l])
+        N.net_fc_xent_jvp(T, B, C, WAYS, A.h[3], R.h[3], self.leaf(theta, 16), self.leaf(v, 16),
+                          self.leaf(v, 17), self.labels_s, A.prob, self.leaf(acc, 16),
+                          self.leaf(acc, 17), R.dh[3])
+        for l in range(3, -1, -1):             # backward tangents
+            H = LAYER_H[l]
+            N.net_bnpool_bwd_jvp(T * C, B, H, H, A.dh[l], R.dh[l], A.code[l], A.y[l], R.y[l],
+                                 self._gamma(theta, l), self._gamma(v, l), A.mean[l], A.rstd[l],
+                                 self._gamma(g, l), self._beta(g, l), self.s1[l], self.s2[l],
+                                 R.dy[l], self._gamma(acc, l), self._beta(acc, l))
+            if l == 0:
+                self._wgrad(R.dy[0], A.cols[0], self._w(acc, 0), accumulate=True)
+                continue
+            self._wgrad(R.dy[l], A.cols[l], self._w(acc, l), A.dy[l], R.cols[l], accumulate=True)
+            dc = self._dcols(l, B * H * H)
+            torch.bmm(self._w(v, l).transpose(1, 2), A.dy[l], out=dc)
+            dc.baddbmm_(self._w(theta, l).transpose(1, 2), R.dy[l])
+            N.net_col2im3x3(T * C, B, LAYER_H[l - 1] // 2, LAYER_H[l - 1] // 2, dc, R.dh[l - 1])
+
+    # -------------------------------------------------------- meta-gradient
+    def meta_grad(self, phi):
+        """Sum over the T tasks of d L_query(theta_K(phi)) / d phi, and the
+        summed query loss, for the task data in self.xs/labels_s/xq/labels_q
+        (written by load()). Returns views of internal buffers."""
+        T, K = self.T, self.K
+        torch.index_select(phi, 0, self.bcast, out=self.theta[0])
+        N.net_im2col3x3(T, self.Bs, HW, HW, self.xs, self.cols1_s)
+        N.net_im2col3x3(T, self.Bq, HW, HW, self.xq, self.cols1_q)
+        for k in range(K):
+            self._grad(self.theta[k], self.cols1_s, self.labels_s, self.acts[k], self.g[k])
+            L.opt_sgd_fwd(self.tree, self.hp, L.OPT_F32, L.OPT_COMPUTE_DEFAULT, self.g[k],
+                          self.b[k], None, self.b[k + 1], self.theta[k], self.theta[k + 1])
+        self._grad(self.theta[K], self.cols1_q, self.labels_q, self.acts_q, self.theta_bar)
+        for k in range(K - 1, -1, -1):
+            L.opt_sgd_bwd(self.tree, self.hp, L.OPT_F32, L.OPT_COMPUTE_DEFAULT, self.g[k],
+                          self.b[k], self.theta_bar, self.b_bar if k < K - 1 else None, self.v,
+                          self.b_bar if k > 0 else None)
+            self._hvp(self.theta[k], self.g[k], self.acts[k], self.v, self.theta_bar)
+        N.net_task_sum(T, len(CONV4_SHAPES), self.h_off, self.d_off, self.theta_bar, self.mg)
+        return self.mg, self.acts_q.loss.sum()
+
+    def load(self, data):
+        """Copy T tasks' (xs, ys, xq, yq) into the static input buffers."""
+        assert len(data) == self.T
+        for t, (xs, ys, xq, yq) in enumerate(data):
+            self.xs[t, 0].copy_(xs.view(self.Bs, HW, HW))
+            self.xq[t, 0].copy_(xq.view(self.Bq, HW, HW))
+            self.labels_s[t].copy_(ys)
+            self.labels_q[t].copy_(yq)
+
+
+def meta_grad_explicit(phi, data, cfg: MamlConfig, engine: ExplicitMaml | None = None):
+    """maml.meta_grad_batched's result through the explicit schedule."""
+    eng = engine or ExplicitMaml(len(data), cfg, phi.device)
+    eng.load(data)
+    mg, loss = eng.meta_grad(phi.detach().contiguous())
+    return mg.clone(), loss.clone()
+
+
+class ExplicitShard:
+    """One rank's task shard as ONE CUDA graph of the explicit schedule
+    (the maml.GraphedShard interface: call it like maml.meta_grad_tasks).
+    Per outer step only phi and the task data are copied in."""
+
+    batched = True
+    nstreams = 1
+
+    def __init__(self, task_ids, cfg: MamlConfig, device, warmup=2):
+        self.ids, self.cfg = list(task_ids), cfg
+        self.eng = ExplicitMaml(len(self.ids), cfg, device)
+        self.phi = torch.zeros(self.eng.n, device=device)
+        self.eng.load([task_data(0, t, device, cfg.seed) for t in self.ids])
+        side = torch.cuda.Stream(device)
+        side.wait_stream(torch.cuda.current_stream(device))
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                self.eng.meta_grad(self.phi)
+        torch.cuda.current_stream(device).wait_stream(side)
+        n0 = L.opt_launch_count() + N.net_launch_count()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.mg, self.loss = self.eng.meta_grad(self.phi)
+        self.launches_per_replay = L.opt_launch_count() + N.net_launch_count() - n0
+
+    def __call__(self, phi, task_ids, outer_step, cfg, inner=None):
+        assert list(task_ids) == self.ids
+        self.phi.copy_(phi)
+        self.eng.load([task_data(outer_step, t, phi.device, cfg.seed) for t in self.ids])
+        self.graph.replay()
+        return self.mg, self.loss
