@@ -418,8 +418,10 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="MAML without CUDA-graph capture")
     ap.add_argument("--no-fuse-glue", action="store_true",
                     help="C3: separate inner-loss glue kernels (NEXT-2 fusion off)")
-    ap.add_argument("--maml-impl", default="batched", choices=["batched", "streams"],
-                    help="MAML shard: one task-batched network, or per-task graph branches")
+    ap.add_argument("--maml-impl", default="batched", choices=["explicit", "batched", "streams"],
+                    help="MAML shard: the hand-scheduled forward-over-reverse step "
+                         "(maml_explicit), the autograd task-batched network, or per-task "
+                         "graph branches")
     ap.add_argument("--maml-net", default="fused", choices=["gemm", "cudnn", "fused"],
                     help="MAML task-batched network form (maml.conv4_forward_tasks)")
     ap.add_argument("--maml-streams", type=int, default=8,
@@ -906,7 +908,11 @@ def measure_maml(args, dev, rank, world, steps=None):
     torch.backends.cudnn.allow_tf32 = False   # fp32 convolutions (dtype f32)
     torch.backends.cuda.matmul.allow_tf32 = False
     shard = None
-    if not args.no_graph:
+    if args.maml_impl == "explicit":
+        from paper_2211_06934_b200 import maml_explicit
+
+        shard = maml_explicit.ExplicitShard(maml.task_range(world, rank, cfg.tasks), cfg, dev)
+    elif not args.no_graph:
         shard = maml.GraphedShard(maml.task_range(world, rank, cfg.tasks), cfg, inner, dev,
                                   streams=(args.maml_groups if args.maml_impl == "batched"
                                            else args.maml_streams),
@@ -937,6 +943,8 @@ def measure_maml(args, dev, rank, world, steps=None):
                           if args.maml_outer == "peer" else "NCCL all-reduce")),
                       "cuda_graph": shard is not None,
                       "shard_impl": ("eager per-task" if shard is None else
+                                     "hand-scheduled forward-over-reverse graph (explicit)"
+                                     if args.maml_impl == "explicit" else
                                      f"task-batched graph ({cfg.net}), {shard.nstreams} "
                                      "concurrent group(s)" if shard.batched else
                                      f"graph, {shard.nstreams} task branches")},

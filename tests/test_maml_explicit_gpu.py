@@ -1,0 +1,305 @@
+"""GPU tests of the hand-scheduled second-order MAML step (row a10,
+paper_2211_06934_b200/maml_explicit.py) and the forward-mode kernels it
+adds to libmamlnet.so (include/mamlnet.h, ABI v2).
+
+Kernel checks compare the fp32 kernels with float64 forward-mode AD
+(torch.func.jvp / forward-over-reverse) of the PyTorch composition; the
+header formulas are pinned the same way on CPU (tests/test_mamlnet_math.py).
+The meta-gradient checks compare the whole schedule with an INDEPENDENT
+float64 MAML written in this file from torch.nn.functional ops and
+torch.autograd.grad(create_graph=True) -- no code of the product's network,
+inner step or driver -- per task, and with the product's autograd path."""
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+EPS = 1e-5
+
+
+@pytest.fixture(scope="module")
+def mx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    from paper_2211_06934_b200 import maml_explicit as m
+
+    return m
+
+
+def close(got, ref, tol=2e-5):
+    """fp32 kernel vs float64 reference: |d| <= tol * (|ref| + max|ref|/10)."""
+    got, ref = got.double().cpu(), ref.double().cpu()
+    scale = float(ref.abs().max()) + 1e-30
+    bad = (got - ref).abs() > tol * (ref.abs() + 0.1 * scale)
+    assert not bool(bad.any()), (f"{int(bad.sum())}/{ref.numel()} off; max abs err "
+                                 f"{float((got - ref).abs().max()):.3e}, scale {scale:.3e}")
+
+
+def ref_block(x, gamma, beta):
+    """relu(max_pool2d(batch_norm(x))), per-(task, channel) statistics, on
+    [T, C, B, H, W] (float64 PyTorch ops)."""
+    T, C, B, H, W = x.shape
+    z = F.batch_norm(x.reshape(1, T * C, -1), None, None, gamma.reshape(-1), beta.reshape(-1),
+                     training=True, eps=EPS)
+    p = F.max_pool2d(z.reshape(T * C * B, 1, H, W), 2)
+    return F.relu(p).reshape(T, C, B, H // 2, W // 2)
+
+
+GEOS = [(2, 64, 5, 28, 28), (2, 64, 25, 14, 14), (2, 64, 5, 7, 7), (4, 64, 25, 3, 3),
+        (3, 5, 7, 9, 6), (1, 3, 2, 2, 2), (2, 3, 25, 28, 28), (1, 2, 75, 14, 14)]
+
+
+def _block_case(geo, seed):
+    gen = torch.Generator().manual_seed(seed)
+    T, C, B, H, W = geo
+    r = lambda *s: torch.randn(*s, generator=gen, dtype=torch.float64)
+    x = r(*geo) * 2 + 0.5
+    gamma = torch.rand(T, C, generator=gen, dtype=torch.float64) + 0.5
+    beta = r(T, C) * 0.3
+    dp = r(T, C, B, H // 2, W // 2)
+    return x, gamma, beta, dp, r(*geo), r(T, C), r(T, C), r(T, C, B, H // 2, W // 2)
+
+
+def _fwd_gpu(N, x, gamma, beta):
+    T, C, B, H, W = x.shape
+    xf, gf, bf = (t.float().to(DEV).contiguous() for t in (x, gamma, beta))
+    out = torch.empty(T, C, B, H // 2, W // 2, device=DEV)
+    code = torch.empty(out.shape, dtype=torch.uint8, device=DEV)
+    mean, rstd = torch.empty(T * C, device=DEV), torch.empty(T * C, device=DEV)
+    N.net_bnpool_fwd(T * C, B, H, W, xf, gf, bf, EPS, out, code, mean, rstd)
+    return xf, gf, bf, code, mean, rstd
+
+
+@pytest.mark.parametrize("geo", GEOS)
+def test_bnpool_jvp_and_bwd_jvp_against_forward_mode_ad(mx, geo):
+    from torch.func import jvp, vjp
+
+    from paper_2211_06934_b200 import _net as N
+
+    x, gamma, beta, dp, xd, gd, bd, dpd = _block_case(geo, 21)
+    T, C, B, H, W = geo
+    _, ref_outd = jvp(ref_block, (x, gamma, beta), (xd, gd, bd))
+
+    def bwd(dp_, x_, g_):
+        return vjp(lambda a, c, b_: ref_block(a, c, b_), x_, g_, beta)[1](dp_)
+
+    _, (rdxd, rdgd, rdbd) = jvp(bwd, (dp, x, gamma), (dpd, xd, gd))
+    xf, gf, bf, code, mean, rstd = _fwd_gpu(N, x, gamma, beta)
+    xdf, gdf, bdf, dpf, dpdf = (t.float().to(DEV).contiguous() for t in (xd, gd, bd, dp, dpd))
+    outd = torch.empty(T, C, B, H // 2, W // 2, device=DEV)
+    s1, s2 = torch.empty(T * C, device=DEV), torch.empty(T * C, device=DEV)
+    N.net_bnpool_jvp(T * C, B, H, W, xf, xdf, gf, gdf, bdf, code, mean, rstd, outd, s1, s2)
+    close(outd, ref_outd)
+    # the backward's own outputs (dgamma, dbeta) are inputs of its JVP
+    dx = torch.empty_like(xf)
+    dg, db = torch.empty(T * C, device=DEV), torch.empty(T * C, device=DEV)
+    N.net_bnpool_bwd(T * C, B, H, W, dpf, code, xf, gf, mean, rstd, dx, dg, db)
+    dxd = torch.empty_like(xf)
+    base_g, base_b = torch.randn(T * C, device=DEV), torch.randn(T * C, device=DEV)
+    acc_g, acc_b = base_g.clone(), base_b.clone()  # accumulated into (+=)
+    N.net_bnpool_bwd_jvp(T * C, B, H, W, dpf, dpdf, code, xf, xdf, gf, gdf, mean, rstd, dg, db,
+                         s1, s2, dxd, acc_g, acc_b)
+    close(dxd, rdxd, tol=5e-5)
+    close(acc_g - base_g, rdgd.reshape(-1), tol=5e-5)
+    close(acc_b - base_b, rdbd.reshape(-1), tol=5e-5)
+
+
+@pytest.mark.parametrize("T,B", [(3, 25), (2, 75), (5, 1)])
+def test_fc_xent_and_jvp_against_float64(mx, T, B):
+    from torch.func import grad, jvp
+
+    from paper_2211_06934_b200 import _net as N
+
+    C, J = 64, 5
+    gen = torch.Generator().manual_seed(22)
+    r = lambda *s: torch.randn(*s, generator=gen, dtype=torch.float64)
+    h4, W, b, h4d, Wd, bd = r(T, C, B), r(T, J, C) * 0.3, r(T, J), r(T, C, B), r(T, J, C), r(T, J)
+    y = torch.randint(0, J, (T, B), generator=gen)
+
+    def loss_fn(hh, WW, bb):
+        logits = hh.transpose(1, 2) @ WW.transpose(1, 2) + bb[:, None, :]
+        return F.cross_entropy(logits.reshape(-1, J), y.reshape(-1), reduction="none") \
+            .view(T, B).mean(1)
+
+    rl = loss_fn(h4, W, b)
+    rg = grad(lambda *a: loss_fn(*a).sum(), argnums=(0, 1, 2))(h4, W, b)
+    _, rt = jvp(grad(lambda *a: loss_fn(*a).sum(), argnums=(0, 1, 2)), (h4, W, b), (h4d, Wd, bd))
+    g = lambda t: t.float().to(DEV).contiguous()
+    yd = y.to(DEV)
+    loss, prob = torch.empty(T, device=DEV), torch.empty(T, B, J, device=DEV)
+    dW, db, dh4 = torch.empty(T, J, C, device=DEV), torch.empty(T, J, device=DEV), torch.empty(
+        T, C, B, device=DEV)
+    N.net_fc_xent(T, B, C, J, g(h4), g(W), g(b), yd, loss, prob, dW, db, dh4)
+    close(loss, rl)
+    close(dh4, rg[0])
+    close(dW, rg[1])
+    close(db, rg[2])
+    aW, ab = torch.ones(T, J, C, device=DEV), torch.ones(T, J, device=DEV)
+    dh4d = torch.empty(T, C, B, device=DEV)
+    N.net_fc_xent_jvp(T, B, C, J, g(h4), g(h4d), g(W), g(Wd), g(bd), yd, prob, aW, ab, dh4d)
+    close(dh4d, rt[0])
+    close(aW - 1, rt[1], tol=5e-5)
+    close(ab - 1, rt[2], tol=5e-5)
+
+
+@pytest.mark.parametrize("T,M,P,N_", [(2, 64, 9, 19600), (4, 64, 576, 4900), (3, 64, 576, 225),
+                                      (1, 5, 7, 33), (2, 64, 576, 0)])
+@pytest.mark.parametrize("pairs,acc", [(1, False), (1, True), (2, False), (2, True)])
+def test_gemm_nt2_pairs_and_accumulate(mx, T, M, P, N_, pairs, acc):
+    from paper_2211_06934_b200 import _net as N
+
+    gen = torch.Generator(device=DEV).manual_seed(23)
+    A, B = (torch.randn(T, M, N_, device=DEV, generator=gen),
+            torch.randn(T, P, N_, device=DEV, generator=gen))
+    A2, B2 = (torch.randn(T, M, N_, device=DEV, generator=gen),
+              torch.randn(T, P, N_, device=DEV, generator=gen)) if pairs == 2 else (None, None)
+    C0 = torch.randn(T, M, P, device=DEV, generator=gen)
+    Cm = C0.clone()
+    wb = N.net_gemm_nt2_workspace_bytes(T, M, P, N_, pairs, acc)
+    ws = torch.empty((wb + 3) // 4, device=DEV) if wb else None
+    N.net_gemm_nt2(T, M, P, N_, A, B, A2, B2, Cm, acc, ws)
+    ref = (C0.double() if acc else 0) + A.double() @ B.double().transpose(1, 2)
+    if pairs == 2:
+        ref = ref + A2.double() @ B2.double().transpose(1, 2)
+    err = float((Cm.double() - ref).abs().max()) if N_ or acc else float(Cm.abs().max())
+    assert err <= 1e-5 * max(N_, 1) ** 0.5 + 1e-5
+    Cr = C0.clone()
+    N.net_gemm_nt2(T, M, P, N_, A, B, A2, B2, Cr, acc, ws)
+    assert torch.equal(Cr, Cm)  # fixed-order reduce: bitwise reproducible
+
+
+def test_task_sum_is_the_broadcast_adjoint(mx):
+    from paper_2211_06934_b200 import _net as N
+
+    e = mx.ExplicitMaml(3, mx.MamlConfig(tasks=3, inner_steps=1), DEV)
+    x = torch.randn(3 * e.n, device=DEV)
+    out = torch.empty(e.n, device=DEV)
+    N.net_task_sum(3, len(mx.CONV4_SHAPES), e.h_off, e.d_off, x, out)
+    ref = torch.zeros(e.n, dtype=torch.float64, device=DEV)
+    ref.index_add_(0, e.bcast, x.double())       # adjoint of the theta_0 gather
+    assert float((out.double() - ref).abs().max()) <= 1e-6 * float(ref.abs().max())
+
+
+# ------------------------------------------------ independent float64 MAML
+def ref_conv4(params, x):
+    """4 x [conv3x3 -> batch norm (batch statistics) -> ReLU -> 2x2 max-pool],
+    fc -> 5 ways, torch.nn.functional only (reading Z16). params: 18 tensors."""
+    h = x
+    for blk in range(4):
+        w, b, gam, bet = params[4 * blk: 4 * blk + 4]
+        h = F.conv2d(h, w, b, padding=1)
+        h = F.batch_norm(h, None, None, gam, bet, training=True, eps=EPS)
+        h = F.max_pool2d(F.relu(h), 2)
+    return F.linear(h.flatten(1), params[16], params[17])
+
+
+def ref_meta_grad(phi_leaves, xs, ys, xq, yq, steps, lr, mom):
+    """float64 second-order MAML meta-gradient of ONE task: `steps` SGD
+    momentum steps b' = mom*b + g, theta' = theta - lr*b' (b_0 = 0) on the
+    support loss with create_graph=True, then d L_query / d phi."""
+    phi = [p.detach().clone().requires_grad_(True) for p in phi_leaves]
+    theta, buf = phi, None
+    for _ in range(steps):
+        loss = F.cross_entropy(ref_conv4(theta, xs), ys)
+        grads = torch.autograd.grad(loss, theta, create_graph=True)
+        buf = list(grads) if buf is None else [mom * b + g for b, g in zip(buf, grads)]
+        theta = [t - lr * b for t, b in zip(theta, buf)]
+    qloss = F.cross_entropy(ref_conv4(theta, xq), yq)
+    return torch.cat([g.reshape(-1) for g in torch.autograd.grad(qloss, phi)]), float(qloss)
+
+
+def _phi_leaves(mx, phi):
+    sizes = mx.sizes_of(mx.CONV4_SHAPES)
+    return [p.view(s) for p, s in zip(torch.split(phi, sizes), mx.CONV4_SHAPES)]
+
+
+def test_explicit_per_task_vs_independent_float64(mx):
+    """Per task, 3 inner steps, 8 (step, task) pairs: relative error of the
+    explicit schedule's meta-gradient vs the independent float64 MAML. fp32
+    rounding gives ~1e-6..1e-5; a ReLU/argmax decision within rounding
+    distance (a 'decision flip') can move one pair by 1e-4+,
+    so the median must be < 1e-5 and at least 6 of 8 < 1e-4."""
+    from paper_2211_06934_b200 import maml
+
+    cfg = maml.MamlConfig(tasks=1, inner_steps=3)
+    eng = mx.ExplicitMaml(1, cfg, DEV)
+    phi = maml.init_params(0, DEV)
+    leaves64 = _phi_leaves(mx, phi.double())
+    errs, lerrs = [], []
+    for step, task in [(0, 0), (0, 1), (1, 2), (1, 3), (3, 0), (3, 2), (4, 0), (4, 3)]:
+        d = maml.task_data(step, task, DEV)
+        mg, loss = mx.meta_grad_explicit(phi, [d], cfg, eng)
+        xs, ys, xq, yq = d
+        ref, rloss = ref_meta_grad(leaves64, xs.double(), ys, xq.double(), yq, 3,
+                                   cfg.inner_lr, cfg.inner_momentum)
+        errs.append(float((mg.double() - ref).norm() / ref.norm()))
+        lerrs.append(abs(float(loss) - rloss) / abs(rloss))
+    s = sorted(errs)
+    assert s[3] < 1e-5 and s[5] < 1e-4, errs
+    assert max(lerrs) < 1e-5, lerrs
+
+
+def test_explicit_task_batch_vs_independent_float64(mx):
+    """4 tasks in one batch, all 5 inner steps (the C4 recipe): the summed
+    meta-gradient and loss vs the sum of the independent float64 per-task
+    references; conv-bias meta-gradients are exactly zero (reading N5)."""
+    from paper_2211_06934_b200 import maml
+
+    T = 4
+    cfg = maml.MamlConfig(tasks=T, inner_steps=5)
+    phi = maml.init_params(0, DEV)
+    data = [maml.task_data(2, t, DEV) for t in range(T)]
+    mg, loss = mx.meta_grad_explicit(phi, data, cfg)
+    leaves64 = _phi_leaves(mx, phi.double())
+    ref = torch.zeros(phi.numel(), dtype=torch.float64, device=DEV)
+    rl = 0.0
+    for xs, ys, xq, yq in data:
+        r, l = ref_meta_grad(leaves64, xs.double(), ys, xq.double(), yq, 5, cfg.inner_lr,
+                             cfg.inner_momentum)
+        ref += r
+        rl += l
+    assert float((mg.double() - ref).norm() / ref.norm()) < 1e-4
+    assert abs(float(loss) - rl) <= 1e-5 * abs(rl)
+    sizes = mx.sizes_of(mx.CONV4_SHAPES)
+    offs = [0]
+    for s in sizes:
+        offs.append(offs[-1] + s)
+    for leaf in (1, 5, 9, 13):
+        assert not mg[offs[leaf]:offs[leaf + 1]].any()
+
+
+def test_explicit_equals_autograd_path(mx):
+    """The explicit schedule and the product's autograd (create_graph) path
+    compute the same meta-gradient up to fp32 rounding (8 tasks, 2 steps)."""
+    from paper_2211_06934_b200 import maml
+
+    T = 8
+    cfg = maml.MamlConfig(tasks=T, inner_steps=2)
+    phi = maml.init_params(0, DEV)
+    data = [maml.task_data(1, t, DEV) for t in range(T)]
+    mg_e, loss_e = mx.meta_grad_explicit(phi, data, cfg)
+    mg_a, loss_a = maml.meta_grad_batched(phi, data, cfg, maml.TaskBatchInner(T, DEV, cfg))
+    assert float((mg_e - mg_a).norm() / mg_a.norm()) < 1e-4
+    assert float(loss_e) == pytest.approx(float(loss_a), rel=1e-5)
+
+
+def test_explicit_shard_graph_replay(mx):
+    """The CUDA-graph shard replays the eager schedule bit for bit on fresh
+    task data, and the schedule is a few hundred library launches."""
+    from paper_2211_06934_b200 import maml
+
+    cfg = maml.MamlConfig(tasks=4)
+    shard = mx.ExplicitShard(range(4), cfg, DEV)
+    assert 0 < shard.launches_per_replay <= 400, shard.launches_per_replay
+    phi = maml.init_params(0, DEV)
+    eng = mx.ExplicitMaml(4, cfg, DEV)
+    for step in (0, 3):
+        mg_g, loss_g = shard(phi, range(4), step, cfg)
+        mg_e, loss_e = mx.meta_grad_explicit(phi, [maml.task_data(step, t, DEV)
+                                                   for t in range(4)], cfg, eng)
+        assert torch.equal(mg_g, mg_e)
+        assert torch.equal(loss_g, loss_e)
+        phi = phi - 1e-3 * mg_e
