@@ -426,6 +426,8 @@ def main():
                     help="MAML task-batched network form (maml.conv4_forward_tasks)")
     ap.add_argument("--maml-streams", type=int, default=8,
                     help="MAML (--maml-impl streams): parallel task branches in the graph")
+    ap.add_argument("--maml-serial", action="store_true",
+                    help="MAML (--maml-impl explicit): no side stream (A/B of the concurrency)")
     ap.add_argument("--maml-outer", default="adam", choices=["adam", "peer"],
                     help="MAML outer step: NCCL all-reduce + replicated fused Adam, or the "
                          "all-reduce fused into a sharded Adam over peer memory")
@@ -911,7 +913,8 @@ def measure_maml(args, dev, rank, world, steps=None):
     if args.maml_impl == "explicit":
         from paper_2211_06934_b200 import maml_explicit
 
-        shard = maml_explicit.ExplicitShard(maml.task_range(world, rank, cfg.tasks), cfg, dev)
+        shard = maml_explicit.ExplicitShard(maml.task_range(world, rank, cfg.tasks), cfg, dev,
+                                            concurrent=not args.maml_serial)
     elif not args.no_graph:
         shard = maml.GraphedShard(maml.task_range(world, rank, cfg.tasks), cfg, inner, dev,
                                   streams=(args.maml_groups if args.maml_impl == "batched"

@@ -19,7 +19,7 @@ NET_OK = 0
 
 EXPORTS = ["net_im2col3x3", "net_col2im3x3", "net_bnpool_fwd", "net_bnpool_bwd",
            "net_bnpool_bwd2", "net_gemm_nt_workspace_bytes", "net_gemm_nt",
-           "net_gemm_nt2_workspace_bytes", "net_gemm_nt2", "net_bnpool_jvp",
+           "net_gemm_nt2_workspace_bytes", "net_gemm_nt2",  "net_bnpool_jvp",
            "net_bnpool_bwd_jvp", "net_fc_xent", "net_fc_xent_jvp", "net_task_sum",
            "net_last_error",
            "net_abi_version", "net_launch_count"]

@@ -684,7 +684,7 @@ int resident_slots(int tp) {  // CTAs of gemm_nt_partial<tp> resident on the dev
   return cached[tp];
 }
 
-SplitPlan split_plan(int64_t T, int64_t M, int64_t P, int64_t N) {
+SplitPlan split_plan(int64_t T, int64_t M, int64_t P, int64_t N, int64_t min_chunks = 8) {
   SplitPlan q;
   q.tp = P <= 16 ? 1 : 4;
   const int GP = 16 * q.tp;
@@ -693,7 +693,7 @@ SplitPlan split_plan(int64_t T, int64_t M, int64_t P, int64_t N) {
   const int64_t nch = (N + GK - 1) / GK;
   const int64_t tiles = T * q.mtiles * q.ptiles;
   const int64_t slots = resident_slots(q.tp);
-  int64_t most = nch / 8;  // each split walks >= 8 chunks (256 of n)
+  int64_t most = nch / min_chunks;  // each split walks >= min_chunks chunks (default 256 of n)
   if (most < 1) most = 1;
   if (most > 4096) most = 4096;
   // fewest splits whose CTA count fills the resident slots' waves to >= 90%
@@ -819,7 +819,7 @@ int launch_group_kernel(void (*kernel)(KArgs...), int64_t G, int64_t n, cudaStre
 // JVP of bnpool_fwd at (x, gamma, beta) along (xd, gd, bd): one CTA cluster
 // per group; pass 1 the group sums S1 = sum xd, S2 = sum xh*xd (fp64),
 // pass 2 the pooled tangent at each active window's maximum.
-__global__ void __launch_bounds__(256, 8) bnpool_jvp_kernel(
+__global__ void __launch_bounds__(256, 6) bnpool_jvp_kernel(
     int B, int H, int W, const float* __restrict__ x, const float* __restrict__ xd,
     const float* __restrict__ gamma, const float* __restrict__ gd, const float* __restrict__ bd,
     const uint8_t* __restrict__ code, const float* __restrict__ mean,
@@ -1277,8 +1277,8 @@ int net_bnpool_bwd_jvp(int64_t G, int64_t B, int64_t H, int64_t W, const float* 
     return fail("net_bnpool_bwd_jvp: NULL pointer");
   const int kc = cluster_for(G, B * H * W);
   const int64_t slice = B * H * W / kc;
-  auto* kernel = slice > 2048 && slice <= 8192 ? bnpool_bwd_jvp_kernel<8> : bnpool_bwd_jvp_kernel<6>;
-  return launch_clustered(kernel, G, kc, 0, (cudaStream_t)stream, (int)B, (int)H, (int)W, dp, dpd,
+  (void)slice;  // <8> compiles spill-free (<6> spills 48 bytes): one variant for every slice
+  return launch_clustered(bnpool_bwd_jvp_kernel<8>, G, kc, 0, (cudaStream_t)stream, (int)B, (int)H, (int)W, dp, dpd,
                           code, x, xd, gamma, gd, mean, rstd, dgamma, dbeta, s1, s2, dxd, dgd_acc,
                           dbd_acc);
 }

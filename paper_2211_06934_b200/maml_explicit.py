@@ -37,13 +37,14 @@ at 32 tasks): nothing is recomputed in the reverse sweep.
 """
 from __future__ import annotations
 
+import contextlib
+
 import numpy as np
 import torch
 
 from . import _lib as L
 from . import _net as N
-from .maml import (BN_EPS, CONV4_SHAPES, HW, WAYS, MamlConfig, _wgrad_uses_split_k, sizes_of,
-                   task_data)
+from .maml import BN_EPS, CONV4_SHAPES, HW, WAYS, MamlConfig, _wgrad_uses_split_k, sizes_of
 
 C = 64                      # channels of every conv block
 LAYER_H = (28, 14, 7, 3)    # input spatial size of conv block l (3x3, padding 1)
@@ -80,7 +81,8 @@ class ExplicitMaml:
     once for (T, n_support, n_query); meta_grad() only launches work on the
     current stream (graph-capturable)."""
 
-    def __init__(self, T, cfg: MamlConfig, device, n_support=WAYS * 5, n_query=WAYS * 15):
+    def __init__(self, T, cfg: MamlConfig, device, n_support=WAYS * 5, n_query=WAYS * 15,
+                 concurrent=True):
         if cfg.nesterov:
             raise NotImplementedError("ExplicitMaml: plain SGD momentum only (the C4 recipe)")
         dev = torch.device(device)
@@ -117,6 +119,12 @@ class ExplicitMaml:
         self.s2 = [torch.empty(self.T * C, device=dev) for _ in range(4)]
         nmax = max(self.Bs, self.Bq) * LAYER_H[1] ** 2
         self.dcols = torch.empty(self.T * C * 9 * nmax, device=dev)
+        self.rdc = [None] + [torch.empty(self.T, C * 9, self.Bs * H * H, device=dev)
+                             for H in LAYER_H[1:]]
+        # off-chain work (weight gradients, the tangent terms that need only v)
+        # runs on a side stream that forks from and joins the current one
+        self.concurrent = bool(concurrent)
+        self.side = torch.cuda.Stream(dev) if self.concurrent else None
         self.labels_s = torch.empty(self.T, self.Bs, dtype=torch.int64, device=dev)
         self.labels_q = torch.empty(self.T, self.Bq, dtype=torch.int64, device=dev)
         self.xs = torch.empty(self.T, 1, self.Bs, HW, HW, device=dev)
@@ -164,11 +172,30 @@ class ExplicitMaml:
     def _dcols(self, l, n):
         return self.dcols[:self.T * LAYER_CIN[l] * 9 * n].view(self.T, LAYER_CIN[l] * 9, n)
 
+    # ------------------------------------------------------------ streams
+    def _fork(self):
+        """Side stream waits for everything enqueued so far on the current one."""
+        if self.concurrent:
+            self.side.wait_stream(torch.cuda.current_stream(self.dev))
+
+    def _on_side(self):
+        return torch.cuda.stream(self.side) if self.concurrent else contextlib.nullcontext()
+
+    def _mark(self):
+        e = torch.cuda.Event()
+        e.record(torch.cuda.current_stream(self.dev))
+        return e
+
+    def _join(self):
+        if self.concurrent:
+            torch.cuda.current_stream(self.dev).wait_stream(self.side)
+
     # ----------------------------------------------------------- gradient
     def _grad(self, theta, cols1, labels, A: _Acts, g):
         """Forward + backward of the T tasks' losses at theta; saves A,
         writes the gradient into g (conv-bias slices untouched) and the
-        per-task losses into A.loss."""
+        per-task losses into A.loss. The weight gradients (off the
+        backward's dependency chain) run on the side stream."""
         T, B = self.T, A.B
         A.cols[0] = cols1
         for l, H in enumerate(LAYER_H):
@@ -183,21 +210,38 @@ class ExplicitMaml:
             H = LAYER_H[l]
             N.net_bnpool_bwd(T * C, B, H, H, A.dh[l], A.code[l], A.y[l], self._gamma(theta, l),
                              A.mean[l], A.rstd[l], A.dy[l], self._gamma(g, l), self._beta(g, l))
-            self._wgrad(A.dy[l], A.cols[l], self._w(g, l))
+            self._fork()
+            with self._on_side():
+                self._wgrad(A.dy[l], A.cols[l], self._w(g, l))
             if l > 0:
                 dc = self._dcols(l, B * H * H)
                 torch.bmm(self._w(theta, l).transpose(1, 2), A.dy[l], out=dc)
                 N.net_col2im3x3(T * C, B, LAYER_H[l - 1] // 2, LAYER_H[l - 1] // 2, dc, A.dh[l - 1])
+        self._join()
 
     # ------------------------------------------------------ Hessian-vector
     def _hvp(self, theta, g, A: _Acts, v, acc):
         """acc += H(theta) v for the support loss whose gradient pass saved A
-        and g (forward-over-reverse; module docstring)."""
+        and g (forward-over-reverse; module docstring). The dependency chain
+        (tangents through the layers and back) stays on the current stream;
+        the terms that need only v and saved values (RW.cols, RW^T.dy) and
+        the weight-gradient tangents go to the side stream."""
         T, B, R = self.T, A.B, self.tan
+        cur = torch.cuda.current_stream(self.dev)
+        self._fork()
+        ey, edc = [None] * 4, [None] * 4
+        with self._on_side():
+            for l in range(4):
+                torch.bmm(self._w(v, l), A.cols[l], out=R.y[l])
+                ey[l] = self._mark()
+            for l in range(3, 0, -1):
+                torch.bmm(self._w(v, l).transpose(1, 2), A.dy[l], out=self.rdc[l])
+                edc[l] = self._mark()
         for l, H in enumerate(LAYER_H):        # forward tangents
-            torch.bmm(self._w(v, l), A.cols[l], out=R.y[l])
             if l > 0:
                 N.net_im2col3x3(T * C, B, H, H, R.h[l - 1], R.cols[l])
+            cur.wait_event(ey[l])
+            if l > 0:
                 R.y[l].baddbmm_(self._w(theta, l), R.cols[l])
             N.net_bnpool_jvp(T * C, B, H, H, A.y[l], R.y[l], self._gamma(theta, l),
                              self._gamma(v, l), self._beta(v, l), A.code[l], A.mean[l],
@@ -211,14 +255,20 @@ class ExplicitMaml:
                                  self._gamma(theta, l), self._gamma(v, l), A.mean[l], A.rstd[l],
                                  self._gamma(g, l), self._beta(g, l), self.s1[l], self.s2[l],
                                  R.dy[l], self._gamma(acc, l), self._beta(acc, l))
-            if l == 0:
-                self._wgrad(R.dy[0], A.cols[0], self._w(acc, 0), accumulate=True)
-                continue
-            self._wgrad(R.dy[l], A.cols[l], self._w(acc, l), A.dy[l], R.cols[l], accumulate=True)
-            dc = self._dcols(l, B * H * H)
-            torch.bmm(self._w(v, l).transpose(1, 2), A.dy[l], out=dc)
-            dc.baddbmm_(self._w(theta, l).transpose(1, 2), R.dy[l])
-            N.net_col2im3x3(T * C, B, LAYER_H[l - 1] // 2, LAYER_H[l - 1] // 2, dc, R.dh[l - 1])
+            self._fork()
+            with self._on_side():
+                if l == 0:
+                    self._wgrad(R.dy[0], A.cols[0], self._w(acc, 0), accumulate=True)
+                else:
+                    self._wgrad(R.dy[l], A.cols[l], self._w(acc, l), A.dy[l], R.cols[l],
+                                accumulate=True)
+            if l > 0:
+                cur.wait_event(edc[l])
+                dc = self.rdc[l]
+                dc.baddbmm_(self._w(theta, l).transpose(1, 2), R.dy[l])
+                N.net_col2im3x3(T * C, B, LAYER_H[l - 1] // 2, LAYER_H[l - 1] // 2, dc,
+                                R.dh[l - 1])
+        self._join()
 
     # -------------------------------------------------------- meta-gradient
     def meta_grad(self, phi):
@@ -252,6 +302,32 @@ class ExplicitMaml:
             self.labels_q[t].copy_(yq)
 
 
+    def load_seeded(self, outer_step, task_ids, seed=0):
+        """maml.task_data(outer_step, t, seed) for every task, drawn straight
+        into the static buffers (the same generator draws in the same order,
+        so bitwise the same data, without the per-task temporaries and
+        copies). Labels are the fixed class-major ones."""
+        from .maml import QUERIES, SHOTS, task_seed
+
+        assert len(task_ids) == self.T and self.Bs == WAYS * SHOTS and self.Bq == WAYS * QUERIES
+        if not getattr(self, "_labels_set", False):
+            ar = torch.arange(WAYS, device=self.dev)
+            self.labels_s.copy_(ar.repeat_interleave(SHOTS).expand(self.T, -1))
+            self.labels_q.copy_(ar.repeat_interleave(QUERIES).expand(self.T, -1))
+            self._labels_set = True
+        if not hasattr(self, "_proto"):
+            self._proto = torch.empty(WAYS, 1, HW, HW, device=self.dev)
+        for t, tid in enumerate(task_ids):
+            gen = torch.Generator(device=self.dev).manual_seed(task_seed(outer_step, tid, seed))
+            xs = self.xs[t, 0].view(self.Bs, 1, HW, HW)
+            xq = self.xq[t, 0].view(self.Bq, 1, HW, HW)
+            torch.randn(xs.shape, generator=gen, device=self.dev, out=xs)
+            torch.randn(xq.shape, generator=gen, device=self.dev, out=xq)
+            torch.randn(self._proto.shape, generator=gen, device=self.dev, out=self._proto)
+            xs.view(WAYS, SHOTS, HW, HW).add_(self._proto.view(WAYS, 1, HW, HW))
+            xq.view(WAYS, QUERIES, HW, HW).add_(self._proto.view(WAYS, 1, HW, HW))
+
+
 def meta_grad_explicit(phi, data, cfg: MamlConfig, engine: ExplicitMaml | None = None):
     """maml.meta_grad_batched's result through the explicit schedule."""
     eng = engine or ExplicitMaml(len(data), cfg, phi.device)
@@ -268,11 +344,11 @@ class ExplicitShard:
     batched = True
     nstreams = 1
 
-    def __init__(self, task_ids, cfg: MamlConfig, device, warmup=2):
+    def __init__(self, task_ids, cfg: MamlConfig, device, warmup=2, concurrent=True):
         self.ids, self.cfg = list(task_ids), cfg
-        self.eng = ExplicitMaml(len(self.ids), cfg, device)
+        self.eng = ExplicitMaml(len(self.ids), cfg, device, concurrent=concurrent)
         self.phi = torch.zeros(self.eng.n, device=device)
-        self.eng.load([task_data(0, t, device, cfg.seed) for t in self.ids])
+        self.eng.load_seeded(0, self.ids, cfg.seed)
         side = torch.cuda.Stream(device)
         side.wait_stream(torch.cuda.current_stream(device))
         with torch.cuda.stream(side):
@@ -288,6 +364,6 @@ class ExplicitShard:
     def __call__(self, phi, task_ids, outer_step, cfg, inner=None):
         assert list(task_ids) == self.ids
         self.phi.copy_(phi)
-        self.eng.load([task_data(outer_step, t, phi.device, cfg.seed) for t in self.ids])
+        self.eng.load_seeded(outer_step, self.ids, cfg.seed)
         self.graph.replay()
         return self.mg, self.loss

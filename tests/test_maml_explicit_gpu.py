@@ -303,3 +303,24 @@ def test_explicit_shard_graph_replay(mx):
         assert torch.equal(mg_g, mg_e)
         assert torch.equal(loss_g, loss_e)
         phi = phi - 1e-3 * mg_e
+
+
+def test_seeded_load_and_serial_schedule_are_bitwise_equal(mx):
+    """load_seeded draws maml.task_data's values into the static buffers
+    bit for bit, and the side-stream schedule computes exactly what the
+    single-stream one does (same kernels on the same inputs)."""
+    from paper_2211_06934_b200 import maml
+
+    T = 3
+    cfg = maml.MamlConfig(tasks=T, inner_steps=2)
+    phi = maml.init_params(0, DEV)
+    a = mx.ExplicitMaml(T, cfg, DEV)
+    b = mx.ExplicitMaml(T, cfg, DEV, concurrent=False)
+    a.load_seeded(7, [4, 9, 2])
+    b.load([maml.task_data(7, t, DEV) for t in (4, 9, 2)])
+    for x, y in ((a.xs, b.xs), (a.xq, b.xq), (a.labels_s, b.labels_s), (a.labels_q, b.labels_q)):
+        assert torch.equal(x, y)
+    mga, la = a.meta_grad(phi)
+    mgb, lb = b.meta_grad(phi)
+    torch.cuda.synchronize()
+    assert torch.equal(mga, mgb) and torch.equal(la, lb)
