@@ -418,7 +418,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="MAML without CUDA-graph capture")
     ap.add_argument("--no-fuse-glue", action="store_true",
                     help="C3: separate inner-loss glue kernels (NEXT-2 fusion off)")
-    ap.add_argument("--maml-impl", default="batched", choices=["explicit", "batched", "streams"],
+    ap.add_argument("--maml-impl", default="explicit", choices=["explicit", "batched", "streams"],
                     help="MAML shard: the hand-scheduled forward-over-reverse step "
                          "(maml_explicit), the autograd task-batched network, or per-task "
                          "graph branches")
@@ -431,8 +431,9 @@ def main():
     ap.add_argument("--maml-outer", default="adam", choices=["adam", "peer"],
                     help="MAML outer step: NCCL all-reduce + replicated fused Adam, or the "
                          "all-reduce fused into a sharded Adam over peer memory")
-    ap.add_argument("--maml-groups", type=int, default=1,
-                    help="MAML (batched): task groups run as concurrent graph branches")
+    ap.add_argument("--maml-groups", type=int, default=None,
+                    help="MAML: task groups run as concurrent graph branches (default: explicit "
+                         "-> one group per task when a rank has <= 4 tasks, else 1; batched -> 1)")
     ap.add_argument("--size", type=int, default=1 << 24)
     ap.add_argument("--bf16", action="store_true", help="bf16 optimizer state")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -910,11 +911,15 @@ def measure_maml(args, dev, rank, world, steps=None):
     torch.backends.cudnn.allow_tf32 = False   # fp32 convolutions (dtype f32)
     torch.backends.cuda.matmul.allow_tf32 = False
     shard = None
+    my_tasks = len(maml.task_range(world, rank, cfg.tasks))
+    if args.maml_groups is None:  # measured: parallel single-task chains win at <= 4 tasks
+        args.maml_groups = my_tasks if (args.maml_impl == "explicit" and my_tasks <= 4) else 1
     if args.maml_impl == "explicit":
         from paper_2211_06934_b200 import maml_explicit
 
         shard = maml_explicit.ExplicitShard(maml.task_range(world, rank, cfg.tasks), cfg, dev,
-                                            concurrent=not args.maml_serial)
+                                            concurrent=not args.maml_serial,
+                                            groups=args.maml_groups)
     elif not args.no_graph:
         shard = maml.GraphedShard(maml.task_range(world, rank, cfg.tasks), cfg, inner, dev,
                                   streams=(args.maml_groups if args.maml_impl == "batched"
@@ -946,7 +951,8 @@ def measure_maml(args, dev, rank, world, steps=None):
                           if args.maml_outer == "peer" else "NCCL all-reduce")),
                       "cuda_graph": shard is not None,
                       "shard_impl": ("eager per-task" if shard is None else
-                                     "hand-scheduled forward-over-reverse graph (explicit)"
+                                     f"hand-scheduled forward-over-reverse graph (explicit), "
+                                     f"{shard.nstreams} task group(s)"
                                      if args.maml_impl == "explicit" else
                                      f"task-batched graph ({cfg.net}), {shard.nstreams} "
                                      "concurrent group(s)" if shard.batched else

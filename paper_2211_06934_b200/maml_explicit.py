@@ -339,31 +339,62 @@ def meta_grad_explicit(phi, data, cfg: MamlConfig, engine: ExplicitMaml | None =
 class ExplicitShard:
     """One rank's task shard as ONE CUDA graph of the explicit schedule
     (the maml.GraphedShard interface: call it like maml.meta_grad_tasks).
-    Per outer step only phi and the task data are copied in."""
+    Per outer step only phi and the task data are copied in.
+
+    groups = G > 1 splits the shard into G contiguous task groups, each its
+    own ExplicitMaml on its own pair of streams, captured as parallel
+    branches of the graph: at a few tasks per GPU most kernels are
+    latency-bound, so two independent chains overlap where one cannot. The
+    group meta-gradients are summed in group order after the join."""
 
     batched = True
-    nstreams = 1
 
-    def __init__(self, task_ids, cfg: MamlConfig, device, warmup=2, concurrent=True):
+    def __init__(self, task_ids, cfg: MamlConfig, device, warmup=2, concurrent=True, groups=1):
         self.ids, self.cfg = list(task_ids), cfg
-        self.eng = ExplicitMaml(len(self.ids), cfg, device, concurrent=concurrent)
-        self.phi = torch.zeros(self.eng.n, device=device)
-        self.eng.load_seeded(0, self.ids, cfg.seed)
+        n, G = len(self.ids), max(1, min(int(groups), len(self.ids)))
+        cuts = [n * i // G for i in range(G + 1)]
+        self.groups = [self.ids[cuts[i]:cuts[i + 1]] for i in range(G)]
+        self.nstreams = G
+        self.engs = [ExplicitMaml(len(g), cfg, device, concurrent=concurrent) for g in self.groups]
+        self.streams = [torch.cuda.Stream(device) for _ in self.groups]
+        self.phi = torch.zeros(self.engs[0].n, device=device)
+        self._load(0)
         side = torch.cuda.Stream(device)
         side.wait_stream(torch.cuda.current_stream(device))
         with torch.cuda.stream(side):
             for _ in range(warmup):
-                self.eng.meta_grad(self.phi)
+                self._body()
         torch.cuda.current_stream(device).wait_stream(side)
         n0 = L.opt_launch_count() + N.net_launch_count()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            self.mg, self.loss = self.eng.meta_grad(self.phi)
+            self.mg, self.loss = self._body()
         self.launches_per_replay = L.opt_launch_count() + N.net_launch_count() - n0
+
+    def _load(self, outer_step):
+        for eng, ids in zip(self.engs, self.groups):
+            eng.load_seeded(outer_step, ids, self.cfg.seed)
+
+    def _body(self):
+        if len(self.engs) == 1:
+            return self.engs[0].meta_grad(self.phi)
+        cur = torch.cuda.current_stream()
+        parts = []
+        for eng, st in zip(self.engs, self.streams):
+            st.wait_stream(cur)
+            with torch.cuda.stream(st):
+                parts.append(eng.meta_grad(self.phi))
+        for st in self.streams:
+            cur.wait_stream(st)
+        mg, loss = parts[0][0].clone(), parts[0][1].clone()
+        for m, l in parts[1:]:  # group order
+            mg += m
+            loss += l
+        return mg, loss
 
     def __call__(self, phi, task_ids, outer_step, cfg, inner=None):
         assert list(task_ids) == self.ids
         self.phi.copy_(phi)
-        self.eng.load_seeded(outer_step, self.ids, cfg.seed)
+        self._load(outer_step)
         self.graph.replay()
         return self.mg, self.loss
