@@ -56,7 +56,7 @@
 extern "C" {
 #endif
 
-#define DIFFOPT_ABI_VERSION 4
+#define DIFFOPT_ABI_VERSION 5
 
 typedef enum {
   OPT_OK = 0,
@@ -364,6 +364,26 @@ typedef struct {
 int opt_adam_fwd_peers(int world, const opt_peers* peers, int64_t lo, int64_t n_shard,
                        int64_t step, const opt_adam_hp* hp, double grad_scale, float* mu,
                        float* nu, const float* params, void* stream);
+
+/* Device-side barrier for opt_adam_fwd_peers (replaces a host stream sync
+ * + process-group barrier on each side of the step). flags->f[w] is peer
+ * w's flag array of 2 * OPT_MAX_PEERS uint64 (zero-initialised once, mapped
+ * into this process by CUDA IPC for remote ranks; f[rank] is this rank's
+ * own). One launch on `stream` (one warp): after a system-scope fence, it
+ * writes `epoch` into slot `slot` (0 = gradients ready, 1 = parameter
+ * stores done) of every peer's array at index slot * OPT_MAX_PEERS + rank,
+ * then waits until every peer has written `epoch` (or more) into this
+ * rank's array. Epochs increase by step (>= 1); the arrays are never
+ * reset. The stream does not advance past the wait, so the order is:
+ *   gradient -> signal_wait(0, t) -> opt_adam_fwd_peers -> signal_wait(1, t)
+ * with no host round trip. A wait longer than timeout_s stops waiting and
+ * sets *status (device int) to 1: the step's result is then undefined and
+ * the caller should report it (no hang). */
+typedef struct {
+  uint64_t* f[OPT_MAX_PEERS];
+} opt_peer_flags;
+int opt_peer_signal_wait(int world, int rank, int slot, const opt_peer_flags* flags,
+                         uint64_t epoch, double timeout_s, int* status, void* stream);
 
 /* -------------------------------------------------------------- misc */
 const char* opt_status_string(int status);

@@ -513,6 +513,29 @@ lib.opt_adam_fwd_peers.restype = ctypes.c_int
 EXPORTS += ["opt_adam_fwd_peers"]
 
 
+class opt_peer_flags(ctypes.Structure):
+    _fields_ = [("f", ctypes.c_void_p * OPT_MAX_PEERS)]
+
+
+lib.opt_peer_signal_wait.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.POINTER(opt_peer_flags), ctypes.c_uint64,
+                                     ctypes.c_double, _P, _P]
+lib.opt_peer_signal_wait.restype = ctypes.c_int
+EXPORTS += ["opt_peer_signal_wait"]
+PEER_READY, PEER_DONE = 0, 1
+
+
+def opt_peer_signal_wait(world, rank, slot, flag_peers, epoch, status, timeout_s=20.0,
+                         stream=None):
+    """flag_peers: per-rank int64 device tensors of 2*OPT_MAX_PEERS (IPC-mapped
+    for remote ranks); status: a device int32 tensor (set to 1 on timeout)."""
+    fl = opt_peer_flags()
+    for w in range(min(int(world), OPT_MAX_PEERS, len(flag_peers))):
+        fl.f[w] = _ptr(flag_peers[w])
+    _check(lib.opt_peer_signal_wait(int(world), int(rank), int(slot), ctypes.byref(fl),
+                                    int(epoch), float(timeout_s), _ptr(status), _stream(stream)))
+
+
 def opt_adam_fwd_peers(world, g_peers, params_peers, lo, n_shard, step, hp, grad_scale, mu, nu,
                        params, stream=None):
     """g_peers / params_peers: per-rank tensors (or device pointers) valid in

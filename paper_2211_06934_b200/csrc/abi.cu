@@ -1253,6 +1253,80 @@ extern "C" int opt_adam_fwd_peers(int world, const opt_peers* peers, int64_t lo,
   return launched(static_cast<cudaStream_t>(stream));
 }
 
+// ------------------------------------------ device-side peer barrier (flags)
+namespace dopt {
+struct PeerFlags {
+  unsigned long long* f[OPT_MAX_PEERS];
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// One warp: lane w < world publishes `epoch` into rank `rank`'s slot of
+// peer w's flag array (after a system-scope fence, so every write this
+// rank's stream issued before -- its gradient, or its parameter stores into
+// every peer -- is visible first), then lane w spins (acquire loads, backed
+// off) until peer w's slot in this rank's own array reaches `epoch`. A wait
+// longer than timeout_ns writes 1 to *status and gives up (no hang).
+__global__ void peer_signal_wait_kernel(int world, int rank, int slot, PeerFlags pf,
+                                        unsigned long long epoch, unsigned long long timeout_ns,
+                                        int* status) {
+  const int w = threadIdx.x;
+  __threadfence_system();
+  __syncwarp();
+  if (w < world) st_release_sys(pf.f[w] + (int64_t)slot * OPT_MAX_PEERS + rank, epoch);
+  if (w < world) {
+    const unsigned long long* mine = pf.f[rank] + (int64_t)slot * OPT_MAX_PEERS + w;
+    const unsigned long long t0 = globaltimer();
+    unsigned ns = 32;
+    while (ld_acquire_sys(mine) < epoch) {
+      if (globaltimer() - t0 > timeout_ns) {
+        atomicExch(status, 1);
+        break;
+      }
+      __nanosleep(ns);
+      if (ns < 1024) ns <<= 1;
+    }
+  }
+  __syncwarp();
+  __threadfence_system();
+}
+}  // namespace dopt
+
+extern "C" int opt_peer_signal_wait(int world, int rank, int slot, const opt_peer_flags* flags,
+                                    uint64_t epoch, double timeout_s, int* status, void* stream) {
+  using namespace dopt;
+  g_err.clear();
+  if (world < 1 || world > OPT_MAX_PEERS) return fail(OPT_EINVAL, "world = %d", world);
+  if (rank < 0 || rank >= world) return fail(OPT_EINVAL, "rank = %d", rank);
+  if (slot < 0 || slot > 1) return fail(OPT_EINVAL, "slot = %d (0 = ready, 1 = done)", slot);
+  if (!flags || !status) return fail(OPT_EINVAL, "flags / status is NULL");
+  if (epoch == 0) return fail(OPT_EINVAL, "epoch must be >= 1 (flags start at 0)");
+  if (!(timeout_s > 0.0)) return fail(OPT_EINVAL, "timeout must be > 0");
+  PeerFlags pf{};
+  for (int w = 0; w < world; ++w) {
+    if (!flags->f[w]) return fail(OPT_EINVAL, "flags of peer %d is NULL", w);
+    if ((uintptr_t)flags->f[w] & 7) return fail(OPT_EALIGN, "flags of peer %d not 8-byte aligned", w);
+    pf.f[w] = reinterpret_cast<unsigned long long*>(flags->f[w]);
+  }
+  const double ns = timeout_s * 1e9;
+  peer_signal_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      world, rank, slot, pf, (unsigned long long)epoch,
+      ns > 1.8e19 ? 18000000000000000000ull : (unsigned long long)ns, status);
+  return launched(static_cast<cudaStream_t>(stream));
+}
+
 #include "es.cuh"
 
 extern "C" {

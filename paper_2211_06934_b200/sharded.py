@@ -68,19 +68,22 @@ class ShardedAdam:
 class PeerShardedAdam:
     """ZeRO-1 Adam with the reduce-scatter, the fused step and the all-gather
     in ONE kernel over peer memory (opt_adam_fwd_peers): every rank maps its
-    peers' gradient and parameter buffers with CUDA IPC once (handles
+    peers' gradient, parameter and flag buffers with CUDA IPC once (handles
     exchanged through the process group), then each step rank r reads the
     W gradient slices of its shard over NVLink, steps its m, v, and stores
-    the new parameter slice into all W parameter copies. Ordering across
-    ranks is a stream sync + process-group barrier before the kernel (every
-    gradient complete) and after it (every peer's stores complete).
+    the new parameter slice into all W parameter copies. Cross-rank ordering
+    is on the device, with no host round trip: a one-warp signal/wait launch
+    (opt_peer_signal_wait) before the step ("my gradient of step t is
+    written"; wait for every peer's) and after it ("my stores of step t
+    are done"; wait for every peer's), epochs in peer-mapped flag arrays.
+    step() only enqueues work on the current stream.
 
     grads / params: this rank's full (n_pad) buffers, allocated here so
     they can be shared: write gradients into ``self.grads`` and read the
-    parameters from ``self.params``."""
+    parameters from ``self.params`` (stream-ordered after step())."""
 
     def __init__(self, n, world, rank, device, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, group=None,
-                 average=True, grad_scale=None):
+                 average=True, grad_scale=None, timeout_s=20.0):
         from torch.multiprocessing.reductions import reduce_tensor
 
         if world > L.OPT_MAX_PEERS:
@@ -90,37 +93,48 @@ class PeerShardedAdam:
         self.n_pad = self.shard * world
         self.hp = (lr, b1, b2, eps, 0.0)
         self.scale = grad_scale if grad_scale is not None else (1.0 / world if average else 1.0)
+        self.timeout_s = float(timeout_s)
         self.grads = torch.zeros(self.n_pad, device=device)
         self.params = torch.zeros(self.n_pad, device=device)
+        self.flags = torch.zeros(2 * L.OPT_MAX_PEERS, dtype=torch.int64, device=device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=device)
         self.m = torch.zeros(self.shard, device=device)
         self.v = torch.zeros(self.shard, device=device)
         self.t = 0
         self.group = group
-        mine = (reduce_tensor(self.grads), reduce_tensor(self.params))
+        torch.cuda.synchronize(device)  # zeroed flags visible before any peer maps them
+        mine = (reduce_tensor(self.grads), reduce_tensor(self.params), reduce_tensor(self.flags))
         handles = [None] * world
         if world > 1:
             dist.all_gather_object(handles, mine, group=group)
         else:
             handles = [mine]
-        self.g_peers, self.p_peers = [], []
-        for w, (hg, hp_) in enumerate(handles):
+        self.g_peers, self.p_peers, self.f_peers = [], [], []
+        for w, hs in enumerate(handles):
             if w == rank:
-                self.g_peers.append(self.grads)
-                self.p_peers.append(self.params)
+                bufs = (self.grads, self.params, self.flags)
             else:  # peer's buffers mapped into this process (kept alive here)
-                self.g_peers.append(hg[0](*hg[1]))
-                self.p_peers.append(hp_[0](*hp_[1]))
-
-    def _barrier(self):
-        torch.cuda.synchronize(self.dev)
-        if self.world > 1:
-            dist.barrier(group=self.group)
+                bufs = tuple(h[0](*h[1]) for h in hs)
+            self.g_peers.append(bufs[0])
+            self.p_peers.append(bufs[1])
+            self.f_peers.append(bufs[2])
+        if world > 1:  # every rank has mapped every peer before the first signal
+            dist.barrier(group=group)
 
     def step(self):
-        """One synchronous sharded step on self.grads -> self.params (all ranks)."""
+        """Enqueue one synchronous sharded step on self.grads -> self.params
+        (all ranks) on the current stream."""
         self.t += 1
-        self._barrier()  # every rank's gradient is complete
+        L.opt_peer_signal_wait(self.world, self.rank, L.PEER_READY, self.f_peers, self.t,
+                               self.status, self.timeout_s)
         L.opt_adam_fwd_peers(self.world, self.g_peers, self.p_peers, self.rank * self.shard,
                              self.shard, self.t, self.hp, self.scale, self.m, self.v, self.params)
-        self._barrier()  # every rank's stores into every parameter copy are complete
+        L.opt_peer_signal_wait(self.world, self.rank, L.PEER_DONE, self.f_peers, self.t,
+                               self.status, self.timeout_s)
         return self.params
+
+    def check(self):
+        """Raise if a device-side wait timed out (synchronises)."""
+        if int(self.status.item()):
+            raise RuntimeError("PeerShardedAdam: a peer did not signal within "
+                               f"{self.timeout_s} s (device-side barrier timed out)")

@@ -89,6 +89,59 @@ def test_virtual_ranks_equal_single_gpu_step(L, W, n):
     torch.testing.assert_close(copies[0], ref, rtol=1e-6, atol=1e-6)
 
 
+@pytest.mark.parametrize("W", [2, 3, 8])
+def test_device_flags_virtual_ranks_on_streams(L, W):
+    """The device-side barrier (opt_peer_signal_wait) with W virtual ranks in
+    one process, each on its own stream and never synchronised by the host:
+    ready-wait, fused step, done-wait per rank per step. Ranks that run ahead
+    block on the device until the others signal; the result is bitwise the
+    serialised run's, and no wait times out."""
+    from paper_2211_06934_b200.sharded import shard_size
+
+    n, steps = 30_011, 3
+    shard = shard_size(n, W)
+    n_pad = shard * W
+    gen = torch.Generator(device=DEV).manual_seed(40 + W)
+    p0 = torch.zeros(n_pad, device=DEV)
+    p0[:n] = torch.randn(n, device=DEV, generator=gen)
+    grads = [[torch.zeros(n_pad, device=DEV) for _ in range(W)] for _ in range(steps)]
+    for t in range(steps):
+        for w in range(W):
+            grads[t][w][:n] = torch.randn(n, device=DEV, generator=gen)
+    ref = virtual(L, grads, p0, steps)
+    copies = [p0.clone() for _ in range(W)]
+    gbuf = [torch.zeros(n_pad, device=DEV) for _ in range(W)]
+    flags = [torch.zeros(2 * L.OPT_MAX_PEERS, dtype=torch.int64, device=DEV) for _ in range(W)]
+    status = torch.zeros(1, dtype=torch.int32, device=DEV)
+    state = [(torch.zeros(shard, device=DEV), torch.zeros(shard, device=DEV)) for _ in range(W)]
+    streams = [torch.cuda.Stream(DEV) for _ in range(W)]
+    torch.cuda.synchronize()
+    for t in range(steps):
+        for r in reversed(range(W)):  # enqueue the last rank first: it must wait on the device
+            with torch.cuda.stream(streams[r]):
+                gbuf[r].copy_(grads[t][r])  # "my gradient of step t"
+                L.opt_peer_signal_wait(W, r, L.PEER_READY, flags, t + 1, status, 20.0)
+                L.opt_adam_fwd_peers(W, gbuf, copies, r * shard, shard, t + 1, HP, 1.0 / W,
+                                     state[r][0], state[r][1], copies[r])
+                L.opt_peer_signal_wait(W, r, L.PEER_DONE, flags, t + 1, status, 20.0)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0
+    for w in range(W):
+        assert torch.equal(copies[w], ref), f"copy {w}"
+    assert all(int(f[:W].min()) == steps and int(f[8:8 + W].min()) == steps for f in flags)
+
+
+def test_device_flags_timeout_is_reported_not_hung(L):
+    """A peer that never signals: the wait gives up after timeout_s and sets
+    the status word instead of hanging the stream."""
+    flags = [torch.zeros(2 * L.OPT_MAX_PEERS, dtype=torch.int64, device=DEV) for _ in range(2)]
+    status = torch.zeros(1, dtype=torch.int32, device=DEV)
+    L.opt_peer_signal_wait(2, 0, L.PEER_READY, flags, 1, status, 0.05)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 1
+    assert int(flags[1][0]) == 1 and int(flags[0][0]) == 1  # rank 0 did publish its epoch
+
+
 def test_bad_arguments_rejected(L):
     z = torch.zeros(16, device=DEV)
     with pytest.raises(L.DiffoptError):
@@ -113,7 +166,8 @@ def _worker(rank, world, init_file, n, steps, out_dir):
     for t in range(steps):
         g = torch.Generator(device=DEV).manual_seed(1000 * t + rank)
         opt.grads[:n] = torch.randn(n, device=DEV, generator=g)
-        opt.step()
+        opt.step()  # enqueues only: device-side signal/wait, no host sync
+    opt.check()
     np.save(os.path.join(out_dir, f"p{rank}.npy"), opt.params.cpu().numpy())
     dist.barrier()
     dist.destroy_process_group()
