@@ -233,8 +233,12 @@ def time_ours(args, workload_inputs, dev, rank, world):
         torch.cuda.synchronize()
         return a.elapsed_time(b) / args.steps
 
-    fwd_ms = [loop_ms(W.fwd)]
-    bwd_ms = [loop_ms(W.bwd)]
+    # 5 alternating repetitions, median reported (one 20-launch sample is
+    # ~1.4 ms and a transient clock dip can move it by 10%+)
+    fwd_ms, bwd_ms = [], []
+    for _ in range(5):
+        fwd_ms.append(loop_ms(W.fwd))
+        bwd_ms.append(loop_ms(W.bwd))
     clocks = sampler.stop()
     if world > 1:
         tt = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -487,8 +491,8 @@ def main():
     per_rank_bytes = W.bytes_fwd + W.bytes_bwd
     value = world * per_rank_bytes * args.steps / (r["ms"] * 1e-3) / 1e9
     peak, peak_src = peaks()
-    bwd_avg = statistics.mean(r["bwd_ms"])
-    fwd_avg = statistics.mean(r["fwd_ms"])
+    bwd_avg = statistics.median(r["bwd_ms"])
+    fwd_avg = statistics.median(r["fwd_ms"])
     achieved = W.bytes_bwd / (bwd_avg * 1e-3) / 1e9
     compute_name = {"default": "f32", "f32": "f32", "f64": "f64"}[args.compute]
     from paper_2211_06934_b200 import _lib as L
@@ -525,7 +529,8 @@ def main():
                      "alg_bytes_per_launch": W.bytes_bwd,
                      "share_of_step": round(bwd_avg / (fwd_avg + bwd_avg), 3),
                      "how": "avg duration of K back-to-back opt_adam_bwd launches (CUDA "
-                            "events on the launching stream around the loop)"},
+                            "events on the launching stream around the loop), median of 5 "
+                            "repetitions"},
         "libdiffopt_abi": L.opt_abi_version(),
     }
     if not args.no_maml:  # second half of the BASELINE metric: C4 tasks/s at this N
