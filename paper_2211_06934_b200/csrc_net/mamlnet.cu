@@ -944,6 +944,28 @@ __global__ void __launch_bounds__(256, MINB) bnpool_bwd_jvp_kernel(
 // W [J][C] (+ tangent), probabilities and dlogits [B][J].
 constexpr int kHeadThreads = 256;
 
+// smem[0..count) = src[0..count) with 16-byte loads when both are aligned
+// (all loads issued before the stores: one latency, not one per element).
+__device__ __forceinline__ void stage(float* __restrict__ dst, const float* __restrict__ src,
+                                      int count) {
+  if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
+    const int c4 = count >> 2;
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    int i = threadIdx.x;
+    for (; i + 3 * (int)blockDim.x < c4; i += 4 * blockDim.x) {
+      const float4 a = __ldg(s4 + i), b = __ldg(s4 + i + blockDim.x),
+                   c = __ldg(s4 + i + 2 * blockDim.x), d = __ldg(s4 + i + 3 * blockDim.x);
+      d4[i] = a, d4[i + blockDim.x] = b, d4[i + 2 * blockDim.x] = c, d4[i + 3 * blockDim.x] = d;
+    }
+    for (; i < c4; i += blockDim.x) d4[i] = __ldg(s4 + i);
+    for (int j = (c4 << 2) + threadIdx.x; j < count; j += blockDim.x) dst[j] = __ldg(src + j);
+  } else {
+#pragma unroll 4
+    for (int j = threadIdx.x; j < count; j += blockDim.x) dst[j] = __ldg(src + j);
+  }
+}
+
 __device__ __forceinline__ float block_sum_f(float v, float* red) {
   // fixed-order block sum (warp xor tree, then warp totals in order)
 #pragma unroll
@@ -969,8 +991,8 @@ __global__ void __launch_bounds__(kHeadThreads) fc_xent_kernel(
   __shared__ float red[32];
   const int64_t t = blockIdx.x;
   const float* ht = h4 + t * C * B;
-  for (int i = threadIdx.x; i < C * B; i += blockDim.x) f[i] = ht[i];
-  for (int i = threadIdx.x; i < J * C; i += blockDim.x) w[i] = Wfc[t * J * C + i];
+  stage(f, ht, C * B);
+  stage(w, Wfc + t * J * C, J * C);
   __syncthreads();
   for (int o = threadIdx.x; o < B * J; o += blockDim.x) {
     const int b = o / J, j = o - b * J;
@@ -1031,14 +1053,16 @@ __global__ void __launch_bounds__(kHeadThreads) fc_xent_jvp_kernel(
   float* dl = wd + J * C;     // [B][J] dlogits
   float* dld = dl + B * J;    // [B][J] their tangent
   const int64_t t = blockIdx.x;
-  for (int i = threadIdx.x; i < C * B; i += blockDim.x) {
-    f[i] = h4[t * C * B + i];
-    fd[i] = h4d ? h4d[t * C * B + i] : 0.f;
-  }
-  for (int i = threadIdx.x; i < J * C; i += blockDim.x) {
-    w[i] = Wfc[t * J * C + i];
-    wd[i] = Wd ? Wd[t * J * C + i] : 0.f;
-  }
+  stage(f, h4 + t * C * B, C * B);
+  if (h4d)
+    stage(fd, h4d + t * C * B, C * B);
+  else
+    for (int i = threadIdx.x; i < C * B; i += blockDim.x) fd[i] = 0.f;
+  stage(w, Wfc + t * J * C, J * C);
+  if (Wd)
+    stage(wd, Wd + t * J * C, J * C);
+  else
+    for (int i = threadIdx.x; i < J * C; i += blockDim.x) wd[i] = 0.f;
   __syncthreads();
   for (int o = threadIdx.x; o < B * J; o += blockDim.x) {  // logit tangents
     const int b = o / J, j = o - b * J;

@@ -20,12 +20,13 @@ def main():
     ap.add_argument("--tasks", type=int, default=4)
     ap.add_argument("--timeline", default=None)
     ap.add_argument("--top", type=int, default=30)
+    ap.add_argument("--groups", type=int, default=1)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.backends.cuda.matmul.allow_tf32 = False
     cfg = maml.MamlConfig(tasks=args.tasks)
     phi = maml.init_params(0, dev)
-    shard = maml_explicit.ExplicitShard(range(cfg.tasks), cfg, dev)
+    shard = maml_explicit.ExplicitShard(range(cfg.tasks), cfg, dev, groups=args.groups)
     for i in range(3):
         shard(phi, range(cfg.tasks), i, cfg)
     torch.cuda.synchronize()
