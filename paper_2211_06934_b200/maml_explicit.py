@@ -356,7 +356,12 @@ class ExplicitShard:
         self.groups = [self.ids[cuts[i]:cuts[i + 1]] for i in range(G)]
         self.nstreams = G
         self.engs = [ExplicitMaml(len(g), cfg, device, concurrent=concurrent) for g in self.groups]
-        self.streams = [torch.cuda.Stream(device) for _ in self.groups]
+        # with several groups, the dependency chains run on high-priority
+        # streams so the side streams' off-chain work fills in behind them
+        # (graph nodes keep the priority; measured: 4 tasks 5.53 -> 5.44 ms;
+        # one chain of 32 tasks is 1.5% slower this way, so not there)
+        self.streams = [torch.cuda.Stream(device, priority=-1 if G > 1 else 0)
+                        for _ in self.groups]
         self.phi = torch.zeros(self.engs[0].n, device=device)
         self._load(0)
         side = torch.cuda.Stream(device)
