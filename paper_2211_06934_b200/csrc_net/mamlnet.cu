@@ -738,7 +738,7 @@ constexpr int kBnThreads = 256;
 constexpr int kSmemCap = 64 * 1024;  // per-CTA slice budget (>= 3 CTAs per SM)
 
 // CTAs per group (cluster size): enough groups-x-slices to give every SM
-// ~8 CTAs, each slice >= 1024 elements; portable cluster sizes 1, 2, 4, 8.
+// ~8 CTAs, each slice >= 4096 elements; portable cluster sizes 1, 2, 4, 8.
 // Also split groups larger than kSliceCap elements (the 28x28 layer's
 // 19,600 at 25 images) so 32-task grids end in a finer last wave: 2 CTAs
 // per group measured 128 vs 137 us (backward), 172 vs 182 us (second
@@ -750,9 +750,19 @@ int cluster_for(int64_t G, int64_t n) {
     const char* e = getenv("NET_BN_SLICE");
     return e ? (int64_t)atoll(e) : kSliceCap;
   }();
+  // smallest per-CTA slice when splitting only to fill the GPU: below ~4K
+  // elements the cluster reduction and per-CTA fixed costs outweigh the
+  // extra CTAs (measured, explicit MAML step at 4 tasks: 1024 -> 5.46 ms,
+  // 2048 -> 5.32, 4096 -> 5.23, no fill splitting -> 5.28; 32 tasks, whose
+  // splits come from the slice cap, unchanged: profiles/r02x_bn_min_slice.txt)
+  static const int64_t min_slice = [] {
+    const char* e = getenv("NET_BN_MIN_SLICE");
+    return e ? (int64_t)atoll(e) : (int64_t)4096;
+  }();
   const int64_t want = 148 * 8;
   int kc = 1;
-  while (kc < 8 && ((G * kc < want && n / (2 * kc) >= 1024) || (slice_cap > 0 && n / kc > slice_cap)))
+  while (kc < 8 && ((G * kc < want && n / (2 * kc) >= min_slice) ||
+                    (slice_cap > 0 && n / kc > slice_cap)))
     kc *= 2;
   return kc;
 }
