@@ -898,6 +898,13 @@ def run_maml(args, dev, rank, world):
         print(json.dumps(out), flush=True)
 
 
+def maml_explicit_groups(tasks):
+    """Task groups (concurrent graph chains) for the explicit MAML shard."""
+    if tasks <= 8:
+        return min(tasks, 4)
+    return 2 if tasks <= 16 else 1
+
+
 def measure_maml(args, dev, rank, world, steps=None):
     import torch
 
@@ -917,8 +924,9 @@ def measure_maml(args, dev, rank, world, steps=None):
     torch.backends.cuda.matmul.allow_tf32 = False
     shard = None
     my_tasks = len(maml.task_range(world, rank, cfg.tasks))
-    if args.maml_groups is None:  # measured: parallel single-task chains win at <= 4 tasks
-        args.maml_groups = my_tasks if (args.maml_impl == "explicit" and my_tasks <= 4) else 1
+    if args.maml_groups is None:  # measured (profiles/r02aa_*, r02ab_*): concurrent
+        # task-group chains win at <= 16 tasks per rank: 4 -> 4 chains, 8 -> 4, 16 -> 2, 32 -> 1
+        args.maml_groups = (maml_explicit_groups(my_tasks) if args.maml_impl == "explicit" else 1)
     if args.maml_impl == "explicit":
         from paper_2211_06934_b200 import maml_explicit
 
