@@ -898,13 +898,6 @@ def run_maml(args, dev, rank, world):
         print(json.dumps(out), flush=True)
 
 
-def maml_explicit_groups(tasks):
-    """Task groups (concurrent graph chains) for the explicit MAML shard."""
-    if tasks <= 8:
-        return min(tasks, 4)
-    return 2 if tasks <= 16 else 1
-
-
 def measure_maml(args, dev, rank, world, steps=None):
     import torch
 
@@ -926,7 +919,9 @@ def measure_maml(args, dev, rank, world, steps=None):
     my_tasks = len(maml.task_range(world, rank, cfg.tasks))
     if args.maml_groups is None:  # measured (profiles/r02aa_*, r02ab_*): concurrent
         # task-group chains win at <= 16 tasks per rank: 4 -> 4 chains, 8 -> 4, 16 -> 2, 32 -> 1
-        args.maml_groups = (maml_explicit_groups(my_tasks) if args.maml_impl == "explicit" else 1)
+        from paper_2211_06934_b200.maml_explicit import default_groups
+
+        args.maml_groups = default_groups(my_tasks) if args.maml_impl == "explicit" else 1
     if args.maml_impl == "explicit":
         from paper_2211_06934_b200 import maml_explicit
 

@@ -336,6 +336,15 @@ def meta_grad_explicit(phi, data, cfg: MamlConfig, engine: ExplicitMaml | None =
     return mg.clone(), loss.clone()
 
 
+def default_groups(tasks):
+    """Task groups (concurrent graph chains) for a shard of `tasks` tasks,
+    from the measured sweep on one B200 (profiles/r02ab_task_groups.txt):
+    <= 8 tasks -> up to 4 chains, <= 16 -> 2, more -> 1."""
+    if tasks <= 8:
+        return max(1, min(tasks, 4))
+    return 2 if tasks <= 16 else 1
+
+
 class ExplicitShard:
     """One rank's task shard as ONE CUDA graph of the explicit schedule
     (the maml.GraphedShard interface: call it like maml.meta_grad_tasks).
@@ -349,8 +358,10 @@ class ExplicitShard:
 
     batched = True
 
-    def __init__(self, task_ids, cfg: MamlConfig, device, warmup=2, concurrent=True, groups=1):
+    def __init__(self, task_ids, cfg: MamlConfig, device, warmup=2, concurrent=True, groups=None):
         self.ids, self.cfg = list(task_ids), cfg
+        if groups is None:
+            groups = default_groups(len(self.ids))
         n, G = len(self.ids), max(1, min(int(groups), len(self.ids)))
         cuts = [n * i // G for i in range(G + 1)]
         self.groups = [self.ids[cuts[i]:cuts[i + 1]] for i in range(G)]
