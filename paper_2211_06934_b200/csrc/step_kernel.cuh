@@ -237,6 +237,15 @@ __device__ __forceinline__ bool last_block(unsigned int* counter, unsigned int n
   return s_last;
 }
 
+#ifndef DOPT_TAIL_PROBE  // diagnostics build: timestamps of the reduction tail in the workspace
+#define DOPT_TAIL_PROBE 0   // (tools/tail_probe.py; profiles/r02ad_*)
+#endif
+__device__ __forceinline__ unsigned long long probe_gt() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // PDL hooks (no-ops unless the launch used programmatic serialization).
 __device__ __forceinline__ void pdl_wait() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -276,12 +285,20 @@ __global__ void __launch_bounds__(kBlock, MINB) step_uniform(const Op op,
     nstatic = nvec - nchunks * chunk;
   }
   pdl_wait();
+#if DOPT_TAIL_PROBE
+  if (threadIdx.x == 0 && a.partials) a.partials[8192 + blockIdx.x] = (double)probe_gt();
+#endif
 #if DOPT_SPAN
   process_spans<Op, ST, U>(op, a, nstatic, tid, nthreads, acc, want_hp);
 #else
   process_vectors<Op, ST, U>(op, a, 0, nstatic, tid, nthreads, acc, want_hp);
 #endif
   if (nchunks == 0) pdl_trigger();
+#if DOPT_TAIL_PROBE
+  __syncthreads();
+  if (threadIdx.x == 0 && a.partials) a.partials[12288 + blockIdx.x] = (double)probe_gt();
+  long long c0 = clock64();
+#endif
   // ragged tail (numel % 4 elements) -> the last block
   const int64_t tail0 = nvec << 2;
   if (blockIdx.x == gridDim.x - 1 && tail0 + threadIdx.x < a.numel)
@@ -316,7 +333,14 @@ __global__ void __launch_bounds__(kBlock, MINB) step_uniform(const Op op,
       }
       pdl_trigger();
     }
-    if (last_block(a.counter, gridDim.x)) {
+#if DOPT_TAIL_PROBE
+    long long c1 = clock64();
+#endif
+    const bool is_last = last_block(a.counter, gridDim.x);
+#if DOPT_TAIL_PROBE
+    long long c2 = clock64();
+#endif
+    if (is_last) {
       double s[NH];
 #pragma unroll
       for (int k = 0; k < NH; ++k) s[k] = 0.0;
@@ -324,6 +348,9 @@ __global__ void __launch_bounds__(kBlock, MINB) step_uniform(const Op op,
       for (int64_t b = threadIdx.x; b < nparts; b += kBlock)
 #pragma unroll
         for (int k = 0; k < NH; ++k) s[k] += __ldcg(&a.partials[b * NH + k]);
+#if DOPT_TAIL_PROBE
+      long long c3 = clock64();
+#endif
       block_sum<NH>(s, sm);
       if (threadIdx.x == 0) {
 #pragma unroll
@@ -331,6 +358,15 @@ __global__ void __launch_bounds__(kBlock, MINB) step_uniform(const Op op,
           if (a.d_hp) a.d_hp[k] = s[k];
         a.counter[0] = 0u;
         a.counter[1] = 0u;
+#if DOPT_TAIL_PROBE  // uniform-mode workspace slots beyond 4 x 4096 are free
+        const long long c4 = clock64();
+        a.partials[16384 + 0] = (double)(c1 - c0);  // block sum + partial store
+        a.partials[16384 + 1] = (double)(c2 - c1);  // arrival ticket
+        a.partials[16384 + 2] = (double)(c3 - c2);  // partial loads
+        a.partials[16384 + 3] = (double)(c4 - c3);  // final block sum + store
+        a.partials[16384 + 4] = (double)probe_gt();
+        a.partials[16384 + 5] = (double)blockIdx.x;
+#endif
       }
     }
   }
