@@ -47,3 +47,12 @@ def test_reference_arm_prints_once_from_rank_0():
     d = _line(r.stdout)
     assert d["impl"] == "reference" and d["n_gpus"] == 2
     assert d["cpu_baseline"]["kind"] == "oracle"
+
+
+def test_explicit_maml_default_groups_policy():
+    """Task groups per shard size for the explicit MAML step (measured sweep,
+    profiles/r02ab_task_groups.txt): the 1/2/4/8-GPU shards of 32 tasks."""
+    from paper_2211_06934_b200.maml_explicit import default_groups
+
+    assert [default_groups(t) for t in (32, 16, 8, 4, 2, 1)] == [1, 2, 4, 4, 2, 1]
+    assert default_groups(0) == 1
