@@ -956,7 +956,8 @@ def measure_maml(args, dev, rank, world, steps=None):
                       "tasks": cfg.tasks,
                       "parallelism": (f"task-sharded x{world}, " + (
                           "all-reduce fused into the outer step (peer memory)"
-                          if args.maml_outer == "peer" else "NCCL all-reduce")),
+                          if args.maml_outer == "peer" else
+                          f"{'NCCL' if args.dist_backend == 'nccl' else 'gloo'} all-reduce")),
                       "cuda_graph": shard is not None,
                       "shard_impl": ("eager per-task" if shard is None else
                                      f"hand-scheduled forward-over-reverse graph (explicit), "
