@@ -86,6 +86,10 @@ class ExplicitMaml:
         if cfg.nesterov:
             raise NotImplementedError("ExplicitMaml: plain SGD momentum only (the C4 recipe)")
         dev = torch.device(device)
+        if dev.type != "cuda":
+            raise ValueError("ExplicitMaml runs on a CUDA device (libmamlnet.so / libdiffopt.so)")
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
         self.T, self.cfg, self.dev = int(T), cfg, dev
         self.K = int(cfg.inner_steps)
         sizes = sizes_of(CONV4_SHAPES)
@@ -276,7 +280,10 @@ class ExplicitMaml:
         summed query loss, for the task data in self.xs/labels_s/xq/labels_q
         (written by load()). Returns views of internal buffers."""
         T, K = self.T, self.K
-        torch.index_select(phi, 0, self.bcast, out=self.theta[0])
+        if phi.dtype != torch.float32 or phi.device != self.dev or phi.numel() != self.n:
+            raise ValueError(f"ExplicitMaml.meta_grad: phi must be float32 on {self.dev} with "
+                             f"{self.n} elements (got {phi.dtype}, {phi.device}, {phi.numel()})")
+        torch.index_select(phi.reshape(-1), 0, self.bcast, out=self.theta[0])
         N.net_im2col3x3(T, self.Bs, HW, HW, self.xs, self.cols1_s)
         N.net_im2col3x3(T, self.Bq, HW, HW, self.xq, self.cols1_q)
         for k in range(K):
@@ -294,7 +301,8 @@ class ExplicitMaml:
 
     def load(self, data):
         """Copy T tasks' (xs, ys, xq, yq) into the static input buffers."""
-        assert len(data) == self.T
+        if len(data) != self.T:
+            raise ValueError(f"ExplicitMaml.load: {len(data)} tasks for an engine of {self.T}")
         for t, (xs, ys, xq, yq) in enumerate(data):
             self.xs[t, 0].copy_(xs.view(self.Bs, HW, HW))
             self.xq[t, 0].copy_(xq.view(self.Bq, HW, HW))
