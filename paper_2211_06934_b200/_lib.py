@@ -197,6 +197,46 @@ def opt_adam_bwd(tree, step, hp, state_dtype, compute, g, mu, nu, d_updates, d_m
                             _ptr(d_hp), _ptr(d_hp_leaf), wp, wb, _stream(stream)))
 
 
+class Prepared:
+    """A C-ABI call with every argument already marshalled (tensor pointers,
+    hyper-parameter struct, tree, workspace, stream resolved once): calling
+    it costs one ctypes call, for launch-bound small trees (C1) called in a
+    loop on fixed buffers. `step` stays a per-call argument (Adam's bias
+    correction); everything else, including the stream, is fixed at
+    preparation time, so the buffers must outlive the object."""
+
+    __slots__ = ("fn", "head", "tail", "keep")
+
+    def __init__(self, fn, head, tail, keep):
+        self.fn, self.head, self.tail, self.keep = fn, head, tail, keep
+
+    def __call__(self, step):
+        rc = self.fn(*self.head, int(step), *self.tail)
+        if rc != OPT_OK:
+            _check(rc)
+
+
+def prepare_adam_fwd(tree, hp, state_dtype, compute, g, mu, nu, updates, mu_out, nu_out,
+                     params=None, params_out=None, stream=None):
+    """opt_adam_fwd pre-marshalled: returns f with f(step) == opt_adam_fwd(tree, step, ...)."""
+    h = _hp(opt_adam_hp, hp)
+    tail = (ctypes.byref(h), int(state_dtype), int(compute), _ptr(g), _ptr(mu), _ptr(nu),
+            _ptr(updates), _ptr(mu_out), _ptr(nu_out), _ptr(params), _ptr(params_out),
+            _stream(stream))
+    return Prepared(lib.opt_adam_fwd, (ctypes.byref(tree.c),), tail, (tree, h))
+
+
+def prepare_adam_bwd(tree, hp, state_dtype, compute, g, mu, nu, d_updates, d_mu_out, d_nu_out,
+                     d_g, d_mu, d_nu, d_hp=None, d_hp_leaf=None, workspace=None, stream=None):
+    """opt_adam_bwd pre-marshalled: returns f with f(step) == opt_adam_bwd(tree, step, ...)."""
+    h = _hp(opt_adam_hp, hp)
+    wp, wb = _ws(workspace)
+    tail = (ctypes.byref(h), int(state_dtype), int(compute), _ptr(g), _ptr(mu), _ptr(nu),
+            _ptr(d_updates), _ptr(d_mu_out), _ptr(d_nu_out), _ptr(d_g), _ptr(d_mu), _ptr(d_nu),
+            _ptr(d_hp), _ptr(d_hp_leaf), wp, wb, _stream(stream))
+    return Prepared(lib.opt_adam_bwd, (ctypes.byref(tree.c),), tail, (tree, h, workspace))
+
+
 def opt_rmsprop_fwd(tree, hp, state_dtype, compute, g, nu, updates, nu_out, params=None,
                     params_out=None, stream=None):
     h = _hp(opt_rmsprop_hp, hp)

@@ -534,3 +534,33 @@ def test_adam_beyond_int32_elements_sampled(L):
                            t, *hp)
     assert_sum_close("dhp(last piece)", host(parts[-1]), full["dhp"],
                      np.maximum(full["dhp_abs"], fmag["dhp"]))
+
+
+def test_prepared_calls_equal_marshalled_calls(L):
+    """_lib.prepare_adam_fwd/bwd (arguments marshalled once, step per call)
+    give bitwise the outputs of the per-call wrappers, at two step counts
+    and with state and hyper-gradients."""
+    leaves = [5, 4096, 300, 3]
+    x = synth.state_tree(0x7E, leaves)
+    tree = L.Tree(offsets=synth.offsets_of(leaves), device=DEV)
+    hp = (1e-2, 0.9, 0.999, 1e-8, 0.0)
+    up = lambda a: torch.from_numpy(a).to(DEV)
+    g, m, v, du, dm1, dv1 = (up(x[k]) for k in ("g", "m", "v", "du", "dm1", "dv1"))
+    outs = {k: [torch.empty_like(g) for _ in range(2)] for k in ("u", "m1", "v1", "dg", "dm", "dv")}
+    dhp = [torch.empty(4, dtype=torch.float64, device=DEV) for _ in range(2)]
+    ws = tree.workspace(DEV)
+    pf = L.prepare_adam_fwd(tree, hp, 0, 0, g, m, v, outs["u"][1], outs["m1"][1], outs["v1"][1])
+    pb = L.prepare_adam_bwd(tree, hp, 0, 0, g, m, v, du, dm1, dv1, outs["dg"][1], outs["dm"][1],
+                            outs["dv"][1], dhp[1], None, ws)
+    for t in (1, 7):
+        L.opt_adam_fwd(tree, t, hp, 0, 0, g, m, v, outs["u"][0], outs["m1"][0], outs["v1"][0])
+        L.opt_adam_bwd(tree, t, hp, 0, 0, g, m, v, du, dm1, dv1, outs["dg"][0], outs["dm"][0],
+                       outs["dv"][0], dhp[0], None, ws)
+        pf(t)
+        pb(t)
+        torch.cuda.synchronize()
+        for k, (a, b) in outs.items():
+            assert torch.equal(a, b), (t, k)
+        assert torch.equal(dhp[0], dhp[1])
+    with pytest.raises(L.DiffoptError):
+        pf(0)  # step >= 1 is still validated per call
