@@ -310,11 +310,12 @@ class ExplicitMaml:
             self.labels_q[t].copy_(yq)
 
 
-    def load_seeded(self, outer_step, task_ids, seed=0):
+    def load_seeded(self, outer_step, task_ids, seed=0, xs_out=None, xq_out=None):
         """maml.task_data(outer_step, t, seed) for every task, drawn straight
-        into the static buffers (the same generator draws in the same order,
-        so bitwise the same data, without the per-task temporaries and
-        copies). Labels are the fixed class-major ones."""
+        into the static buffers (or xs_out / xq_out of the same shapes; the
+        same generator draws in the same order, so bitwise the same data,
+        without the per-task temporaries and copies). Labels are the fixed
+        class-major ones."""
         from .maml import QUERIES, SHOTS, task_seed
 
         assert len(task_ids) == self.T and self.Bs == WAYS * SHOTS and self.Bq == WAYS * QUERIES
@@ -325,15 +326,18 @@ class ExplicitMaml:
             self._labels_set = True
         if not hasattr(self, "_proto"):
             self._proto = torch.empty(WAYS, 1, HW, HW, device=self.dev)
+        XS = self.xs if xs_out is None else xs_out
+        XQ = self.xq if xq_out is None else xq_out
+        proto = torch.empty(WAYS, 1, HW, HW, device=self.dev) if xs_out is not None else self._proto
         for t, tid in enumerate(task_ids):
             gen = torch.Generator(device=self.dev).manual_seed(task_seed(outer_step, tid, seed))
-            xs = self.xs[t, 0].view(self.Bs, 1, HW, HW)
-            xq = self.xq[t, 0].view(self.Bq, 1, HW, HW)
+            xs = XS[t, 0].view(self.Bs, 1, HW, HW)
+            xq = XQ[t, 0].view(self.Bq, 1, HW, HW)
             torch.randn(xs.shape, generator=gen, device=self.dev, out=xs)
             torch.randn(xq.shape, generator=gen, device=self.dev, out=xq)
-            torch.randn(self._proto.shape, generator=gen, device=self.dev, out=self._proto)
-            xs.view(WAYS, SHOTS, HW, HW).add_(self._proto.view(WAYS, 1, HW, HW))
-            xq.view(WAYS, QUERIES, HW, HW).add_(self._proto.view(WAYS, 1, HW, HW))
+            torch.randn(proto.shape, generator=gen, device=self.dev, out=proto)
+            xs.view(WAYS, SHOTS, HW, HW).add_(proto.view(WAYS, 1, HW, HW))
+            xq.view(WAYS, QUERIES, HW, HW).add_(proto.view(WAYS, 1, HW, HW))
 
 
 def meta_grad_explicit(phi, data, cfg: MamlConfig, engine: ExplicitMaml | None = None):
@@ -394,6 +398,21 @@ class ExplicitShard:
         with torch.cuda.graph(self.graph):
             self.mg, self.loss = self._body()
         self.launches_per_replay = L.opt_launch_count() + N.net_launch_count() - n0
+        # next step's task data, drawn on a side stream while this step's
+        # graph replays (input pipelining; bitwise the same draws)
+        self.stage = [(torch.empty_like(e.xs), torch.empty_like(e.xq)) for e in self.engs]
+        self.pf_stream = torch.cuda.Stream(device)
+        self.pf_step, self.pf_done, self.copied = None, None, None
+
+    def _prefetch(self, outer_step):
+        if self.copied is not None:
+            self.pf_stream.wait_event(self.copied)  # the stage buffers were consumed
+        with torch.cuda.stream(self.pf_stream):
+            for eng, ids, (sx, sq) in zip(self.engs, self.groups, self.stage):
+                eng.load_seeded(outer_step, ids, self.cfg.seed, sx, sq)
+            self.pf_done = torch.cuda.Event()
+            self.pf_done.record(self.pf_stream)
+        self.pf_step = outer_step
 
     def _load(self, outer_step):
         for eng, ids in zip(self.engs, self.groups):
@@ -418,7 +437,17 @@ class ExplicitShard:
 
     def __call__(self, phi, task_ids, outer_step, cfg, inner=None):
         assert list(task_ids) == self.ids
+        cur = torch.cuda.current_stream(self.phi.device)
+        if self.pf_step == outer_step:  # drawn during the previous replay
+            cur.wait_event(self.pf_done)
+            for eng, (sx, sq) in zip(self.engs, self.stage):
+                eng.xs.copy_(sx)
+                eng.xq.copy_(sq)
+        else:
+            self._load(outer_step)
+        self.copied = torch.cuda.Event()
+        self.copied.record(cur)
         self.phi.copy_(phi)
-        self._load(outer_step)
         self.graph.replay()
+        self._prefetch(outer_step + 1)  # the outer loop's next step
         return self.mg, self.loss

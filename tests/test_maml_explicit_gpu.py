@@ -371,7 +371,7 @@ def test_explicit_shard_graph_replay(mx, groups):
     phi = maml.init_params(0, DEV)
     cuts = [4 * i // groups for i in range(groups + 1)]
     engs = [mx.ExplicitMaml(cuts[i + 1] - cuts[i], cfg, DEV) for i in range(groups)]
-    for step in (0, 3):
+    for step in (0, 3, 4, 5):  # 4 and 5: inputs prefetched during the previous replay
         mg_g, loss_g = shard(phi, range(4), step, cfg)
         mg_e = loss_e = None
         for i, e in enumerate(engs):
