@@ -290,7 +290,8 @@ __global__ void __launch_bounds__(256, 6) bnpool_fwd_kernel(int B, int H, int W,
   }
 }
 
-__global__ void __launch_bounds__(256, 8) bnpool_bwd_kernel(int B, int H, int W, const float* __restrict__ dp,
+template <bool EVEN>  // W even: each window's two rows as float2 pairs (8-byte aligned)
+__global__ void __launch_bounds__(256, EVEN ? 6 : 8) bnpool_bwd_kernel(int B, int H, int W, const float* __restrict__ dp,
                                   const uint8_t* __restrict__ code, const float* __restrict__ x,
                                   const float* __restrict__ gamma, const float* __restrict__ mean,
                                   const float* __restrict__ rstd, float* __restrict__ dx,
@@ -328,11 +329,22 @@ __global__ void __launch_bounds__(256, 8) bnpool_bwd_kernel(int B, int H, int W,
     const int e0 = q.elem0(p);
     const uint8_t c = cg[p];
     const float dl = dpg[p], d = c != kOff ? dl : 0.f;  // unconditional load
+    if constexpr (EVEN) {
+      const float2 t = *reinterpret_cast<const float2*>(xg + e0);
+      const float2 u = *reinterpret_cast<const float2*>(xg + e0 + W);
+      const float xv[4] = {t.x, t.y, u.x, u.y};
+      float o[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int e = e0 + q.off(k);
-      const float xh = (xg[e] - m) * r;
-      dxg[e] = c0 * ((c == k ? d : 0.f) - A - xh * Bm);
+      for (int k = 0; k < 4; ++k) o[k] = c0 * ((c == k ? d : 0.f) - A - (xv[k] - m) * r * Bm);
+      *reinterpret_cast<float2*>(dxg + e0) = make_float2(o[0], o[1]);
+      *reinterpret_cast<float2*>(dxg + e0 + W) = make_float2(o[2], o[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int e = e0 + q.off(k);
+        const float xh = (xg[e] - m) * r;
+        dxg[e] = c0 * ((c == k ? d : 0.f) - A - xh * Bm);
+      }
     }
   }
   // ... and over the elements outside every window (dy = 0)
@@ -877,7 +889,7 @@ __global__ void __launch_bounds__(256, 6) bnpool_jvp_kernel(
 // from bnpool_jvp of the same xd. Pass 1 (pooled): P1 = sum dyd,
 // P2 = sum dyd*xh, P3 = sum dy*xhd; pass 2 (every element) the tangent of dx.
 // dgd/dbd are ACCUMULATED (+=).
-template <int MINB>
+template <int MINB, bool EVEN>  // EVEN: W even, window rows as float2 pairs
 __global__ void __launch_bounds__(256, MINB) bnpool_bwd_jvp_kernel(
     int B, int H, int W, const float* __restrict__ dp, const float* __restrict__ dpd,
     const uint8_t* __restrict__ code, const float* __restrict__ x, const float* __restrict__ xd,
@@ -928,14 +940,33 @@ __global__ void __launch_bounds__(256, MINB) bnpool_bwd_jvp_kernel(
     const uint8_t c = cg[p];
     const float dl = dpg[p], ddl = dpdg[p];
     const float d = c != kOff ? dl : 0.f, dd = c != kOff ? ddl : 0.f;
+    if constexpr (EVEN) {
+      const float2 t0 = *reinterpret_cast<const float2*>(xg + e0);
+      const float2 t1 = *reinterpret_cast<const float2*>(xg + e0 + W);
+      const float2 u0 = *reinterpret_cast<const float2*>(xdg + e0);
+      const float2 u1 = *reinterpret_cast<const float2*>(xdg + e0 + W);
+      const float xv[4] = {t0.x, t0.y, t1.x, t1.y}, xdv[4] = {u0.x, u0.y, u1.x, u1.y};
+      float o[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int e = e0 + q.off(k);
-      const float xh = (xg[e] - m) * r;
-      const float xhd = r * (xdg[e] - a - xh * b);
-      const float D = (c == k ? d : 0.f) - A - xh * Bm;
-      const float Dd = (c == k ? dd : 0.f) - Ad - xhd * Bm - xh * Bmd;
-      og[e] = c1 * D + c2 * Dd;
+      for (int k = 0; k < 4; ++k) {
+        const float xh = (xv[k] - m) * r;
+        const float xhd = r * (xdv[k] - a - xh * b);
+        const float D = (c == k ? d : 0.f) - A - xh * Bm;
+        const float Dd = (c == k ? dd : 0.f) - Ad - xhd * Bm - xh * Bmd;
+        o[k] = c1 * D + c2 * Dd;
+      }
+      *reinterpret_cast<float2*>(og + e0) = make_float2(o[0], o[1]);
+      *reinterpret_cast<float2*>(og + e0 + W) = make_float2(o[2], o[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int e = e0 + q.off(k);
+        const float xh = (xg[e] - m) * r;
+        const float xhd = r * (xdg[e] - a - xh * b);
+        const float D = (c == k ? d : 0.f) - A - xh * Bm;
+        const float Dd = (c == k ? dd : 0.f) - Ad - xhd * Bm - xh * Bmd;
+        og[e] = c1 * D + c2 * Dd;
+      }
     }
   }
   const Slice ls(q.nl, rank, kc);
@@ -1186,8 +1217,10 @@ int net_bnpool_bwd(int64_t G, int64_t B, int64_t H, int64_t W, const float* dp,
   if (G == 0) return NET_OK;
   if (!dp || !code || !x || !gamma || !mean || !rstd || !dx || !dgamma || !dbeta)
     return fail("net_bnpool_bwd: NULL pointer");
-  return launch_group_kernel(bnpool_bwd_kernel, G, B * H * W, (cudaStream_t)stream, (int)B,
-                             (int)H, (int)W, dp, code, x, gamma, mean, rstd, dx, dgamma, dbeta);
+  const bool even = (W % 2 == 0) && ((uintptr_t)x & 7) == 0 && ((uintptr_t)dx & 7) == 0;
+  return launch_group_kernel(even ? bnpool_bwd_kernel<true> : bnpool_bwd_kernel<false>, G,
+                             B * H * W, (cudaStream_t)stream, (int)B, (int)H, (int)W, dp, code, x,
+                             gamma, mean, rstd, dx, dgamma, dbeta);
 }
 
 int net_bnpool_bwd2(int64_t G, int64_t B, int64_t H, int64_t W, const float* gdx,
@@ -1312,7 +1345,9 @@ int net_bnpool_bwd_jvp(int64_t G, int64_t B, int64_t H, int64_t W, const float* 
   const int kc = cluster_for(G, B * H * W);
   const int64_t slice = B * H * W / kc;
   (void)slice;  // <8> compiles spill-free (<6> spills 48 bytes): one variant for every slice
-  return launch_clustered(bnpool_bwd_jvp_kernel<8>, G, kc, 0, (cudaStream_t)stream, (int)B, (int)H, (int)W, dp, dpd,
+  const bool even = (W % 2 == 0) && (((uintptr_t)x | (uintptr_t)xd | (uintptr_t)dxd) & 7) == 0;
+  return launch_clustered(even ? bnpool_bwd_jvp_kernel<8, true> : bnpool_bwd_jvp_kernel<8, false>,
+                          G, kc, 0, (cudaStream_t)stream, (int)B, (int)H, (int)W, dp, dpd,
                           code, x, xd, gamma, gd, mean, rstd, dgamma, dbeta, s1, s2, dxd, dgd_acc,
                           dbd_acc);
 }
