@@ -11,10 +11,13 @@ graph by ExplicitShard:
 Inner loop (MAML; 5 SGD-momentum steps, the optimizer of row a7):
     for k = 0..K-1:  g_k = grad L_s(theta_k)        (forward + backward, saved)
                      b_{k+1} = mu b_k + g_k;  theta_{k+1} = theta_k - lr b_{k+1}
+                     (Nesterov: theta_{k+1} = theta_k - lr (g_k + mu b_{k+1}))
                      (ONE fused opt_sgd_fwd launch with apply, all T tasks)
 Outer reverse sweep (row a9's recurrence with the SGD VJP of row a7):
     theta_bar_K = grad L_q(theta_K);  b_bar_K = 0
     for k = K-1..0:  (v, b_bar_k) = opt_sgd_bwd(u_bar = theta_bar_{k+1}, b_bar_{k+1})
+                     (plain: v = b_bar' - lr u_bar; Nesterov: v = -lr u_bar + B,
+                      B = b_bar' - lr mu u_bar; b_bar_k = mu v or mu B)
                      theta_bar_k = theta_bar_{k+1} + H_k v     (H_k = Hessian of L_s at theta_k)
     phi_bar = sum over tasks of theta_bar_0           (theta_0 = phi for every task)
 
@@ -83,8 +86,6 @@ class ExplicitMaml:
 
     def __init__(self, T, cfg: MamlConfig, device, n_support=WAYS * 5, n_query=WAYS * 15,
                  concurrent=True):
-        if cfg.nesterov:
-            raise NotImplementedError("ExplicitMaml: plain SGD momentum only (the C4 recipe)")
         dev = torch.device(device)
         if dev.type != "cuda":
             raise ValueError("ExplicitMaml runs on a CUDA device (libmamlnet.so / libdiffopt.so)")
@@ -98,7 +99,9 @@ class ExplicitMaml:
         self.h_off = torch.from_numpy(self.off.copy())          # host copy (net_task_sum)
         self.d_off = self.h_off.to(dev)
         self.tree = L.Tree(numel=self.T * self.n, device=dev)
-        self.hp = (cfg.inner_lr, cfg.inner_momentum, False)
+        # plain or Nesterov momentum: opt_sgd_fwd / opt_sgd_bwd carry the
+        # difference (u = -lr b' or -lr (g + mu b'); the VJP gives v = g_bar)
+        self.hp = (cfg.inner_lr, cfg.inner_momentum, bool(cfg.nesterov))
         Tn = self.T * self.n
         # theta_0..theta_K, b_1..b_K, g_0..g_{K-1}; conv-bias slices of g stay 0
         self.theta = [torch.empty(Tn, device=dev) for _ in range(self.K + 1)]

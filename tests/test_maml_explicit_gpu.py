@@ -216,7 +216,7 @@ def ref_codes(params, x):
     return out
 
 
-def ref_meta_grad(phi_leaves, xs, ys, xq, yq, steps, lr, mom, codes=None):
+def ref_meta_grad(phi_leaves, xs, ys, xq, yq, steps, lr, mom, codes=None, nesterov=False):
     """float64 second-order MAML meta-gradient of ONE task: `steps` SGD
     momentum steps b' = mom*b + g, theta' = theta - lr*b' (b_0 = 0) on the
     support loss with create_graph=True, then d L_query / d phi. codes (a
@@ -230,7 +230,8 @@ def ref_meta_grad(phi_leaves, xs, ys, xq, yq, steps, lr, mom, codes=None):
         loss = F.cross_entropy(ref_conv4(theta, xs), ys)
         grads = torch.autograd.grad(loss, theta, create_graph=True)
         buf = list(grads) if buf is None else [mom * b + g for b, g in zip(buf, grads)]
-        theta = [t - lr * b for t, b in zip(theta, buf)]
+        step = [g + mom * b for g, b in zip(grads, buf)] if nesterov else buf
+        theta = [t - lr * st for t, st in zip(theta, step)]
     if codes is not None:
         codes.append(ref_codes([t.detach() for t in theta], xq))
     qloss = F.cross_entropy(ref_conv4(theta, xq), yq)
@@ -272,7 +273,8 @@ def _flip_aware_check(eng, data, phi, K, strict=2e-5, min_clean=None):
     for t, (xs, ys, xq, yq) in enumerate(data):
         codes = []
         ref, rloss = ref_meta_grad(leaves64, xs.double(), ys, xq.double(), yq, K,
-                                   eng.cfg.inner_lr, eng.cfg.inner_momentum, codes)
+                                   eng.cfg.inner_lr, eng.cfg.inner_momentum, codes,
+                                   eng.cfg.nesterov)
         same = all(torch.equal(a.reshape(-1), b.reshape(-1)) for ca, cb in
                    zip(_engine_codes(eng, t), codes) for a, b in zip(ca, cb))
         if not same:
@@ -291,6 +293,24 @@ def eng_mod():
     from paper_2211_06934_b200 import maml_explicit
 
     return maml_explicit
+
+
+def test_explicit_nesterov_vs_independent_float64(mx):
+    """The explicit schedule with Nesterov inner momentum (opt_sgd_fwd/bwd
+    carry it) vs the independent float64 MAML with Nesterov steps, per task,
+    strict where the routing decisions match."""
+    from paper_2211_06934_b200 import maml
+
+    cfg = maml.MamlConfig(tasks=1, inner_steps=2, nesterov=True)
+    eng = mx.ExplicitMaml(1, cfg, DEV)
+    phi = maml.init_params(0, DEV)
+    clean = 0
+    for step, task in [(0, 0), (1, 2), (3, 1), (4, 3), (2, 0), (5, 1), (6, 2), (7, 3)]:
+        d = maml.task_data(step, task, DEV)
+        mx.meta_grad_explicit(phi, [d], cfg, eng)
+        errs, _ = _flip_aware_check(eng, [d], phi, 2)
+        clean += len(errs)
+    assert clean >= 2, clean
 
 
 def test_explicit_per_task_vs_independent_float64(mx):

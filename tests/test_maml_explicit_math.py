@@ -47,7 +47,7 @@ def ref_net(params, x):
     return F.linear(h.flatten(1), params[16], params[17])
 
 
-def ref_meta_grad(phi, xs, ys, xq, yq, K, lr, mom):
+def ref_meta_grad(phi, xs, ys, xq, yq, K, lr, mom, nesterov=False):
     """Autograd (create_graph) second-order MAML meta-gradient."""
     phi = [p.clone().requires_grad_(True) for p in phi]
     theta, buf = phi, None
@@ -55,7 +55,8 @@ def ref_meta_grad(phi, xs, ys, xq, yq, K, lr, mom):
         grads = torch.autograd.grad(F.cross_entropy(ref_net(theta, xs), ys), theta,
                                     create_graph=True)
         buf = list(grads) if buf is None else [mom * b + g for b, g in zip(buf, grads)]
-        theta = [t - lr * b for t, b in zip(theta, buf)]
+        step = [g + mom * b for g, b in zip(grads, buf)] if nesterov else buf
+        theta = [t - lr * st for t, st in zip(theta, step)]
     return [g.detach() for g in torch.autograd.grad(F.cross_entropy(ref_net(theta, xq), yq), phi)]
 
 
@@ -131,7 +132,7 @@ def hvp(theta, S, grad, v, labels, drop=()):
     return out
 
 
-def explicit_meta_grad(phi, xs, ys, xq, yq, K, lr, mom, drop=()):
+def explicit_meta_grad(phi, xs, ys, xq, yq, K, lr, mom, drop=(), nesterov=False):
     thetas, grads, saved, bufs = [list(phi)], [], [], [None]
     for _ in range(K):
         g, S, _ = grad_pass(thetas[-1], xs, ys)
@@ -139,20 +140,29 @@ def explicit_meta_grad(phi, xs, ys, xq, yq, K, lr, mom, drop=()):
         saved.append(S)
         b = g if bufs[-1] is None else [mom * bb + gg for bb, gg in zip(bufs[-1], g)]
         bufs.append(b)
-        thetas.append([t - lr * bb for t, bb in zip(thetas[-1], b)])
+        step = [gg + mom * bb for gg, bb in zip(g, b)] if nesterov else b
+        thetas.append([t - lr * st for t, st in zip(thetas[-1], step)])
     theta_bar, _, _ = grad_pass(thetas[-1], xq, yq)
     b_bar = None
     for k in range(K - 1, -1, -1):
-        v = [(0 if b_bar is None else bb) - lr * tb for bb, tb in
-             zip(b_bar or theta_bar, theta_bar)]                  # opt_sgd_bwd: ḡ = b̄' − lr ū
-        b_bar = [(0.0 if "momentum" in drop else mom) * vv for vv in v]   # b̄ = μ ḡ
+        if nesterov:  # opt_sgd_bwd, Nesterov: B = b̄' − lr μ ū, ḡ = −lr ū + B, b̄ = μ B
+            Bv = [(0 if b_bar is None else bb) - lr * mom * tb for bb, tb in
+                  zip(b_bar or theta_bar, theta_bar)]
+            v = [-lr * tb + bv for tb, bv in zip(theta_bar, Bv)]
+            b_bar = [mom * bv for bv in Bv]
+        else:
+            v = [(0 if b_bar is None else bb) - lr * tb for bb, tb in
+                 zip(b_bar or theta_bar, theta_bar)]              # opt_sgd_bwd: ḡ = b̄' − lr ū
+            b_bar = [(0.0 if "momentum" in drop else mom) * vv for vv in v]   # b̄ = μ ḡ
         hv = hvp(thetas[k], saved[k], grads[k], v, ys, drop)
         theta_bar = [tb + h for tb, h in zip(theta_bar, hv)]
     return theta_bar
 
 
-@pytest.mark.parametrize("K,mom,seed", [(1, 0.9, 0), (3, 0.9, 1), (3, 0.0, 2), (5, 0.5, 3)])
-def test_explicit_schedule_equals_autograd_maml(K, mom, seed):
+@pytest.mark.parametrize("K,mom,seed,nesterov", [(1, 0.9, 0, False), (3, 0.9, 1, False),
+                                                 (3, 0.0, 2, False), (5, 0.5, 3, False),
+                                                 (3, 0.9, 4, True), (2, 0.5, 5, True)])
+def test_explicit_schedule_equals_autograd_maml(K, mom, seed, nesterov):
     gen = torch.Generator().manual_seed(seed)
     phi = make_params(gen)
     Bs, Bq = 2 * WAYS, 3 * WAYS
@@ -161,8 +171,8 @@ def test_explicit_schedule_equals_autograd_maml(K, mom, seed):
     ys = torch.arange(WAYS).repeat_interleave(2)
     yq = torch.arange(WAYS).repeat_interleave(3)
     lr = 0.1
-    ref = ref_meta_grad(phi, xs, ys, xq, yq, K, lr, mom)
-    got = explicit_meta_grad(phi, xs, ys, xq, yq, K, lr, mom)
+    ref = ref_meta_grad(phi, xs, ys, xq, yq, K, lr, mom, nesterov)
+    got = explicit_meta_grad(phi, xs, ys, xq, yq, K, lr, mom, nesterov=nesterov)
     scale = max(float(r.abs().max()) for r in ref)
     for i, (a, r) in enumerate(zip(got, ref)):
         if i < 16 and i % 4 == 1:  # conv bias: inert (N5), exactly 0 in the schedule
