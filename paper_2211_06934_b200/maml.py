@@ -90,6 +90,13 @@ class MamlConfig:
     outer_lr: float = 1e-3
     seed: int = 0
     net: str = "fused"  # network form (conv4_forward_tasks)
+    # inner optimizer of the explicit step (maml_explicit): "sgd" (momentum /
+    # Nesterov, the C4 recipe) or "adam" (differentiable Adam inner loop,
+    # MetaAdam-style; inner_lr is its lr)
+    inner_opt: str = "sgd"
+    adam_b1: float = 0.9
+    adam_b2: float = 0.999
+    adam_eps: float = 1e-8
 
 
 class FusedSgdInner:

@@ -102,10 +102,19 @@ class ExplicitMaml:
         # plain or Nesterov momentum: opt_sgd_fwd / opt_sgd_bwd carry the
         # difference (u = -lr b' or -lr (g + mu b'); the VJP gives v = g_bar)
         self.hp = (cfg.inner_lr, cfg.inner_momentum, bool(cfg.nesterov))
+        if cfg.inner_opt not in ("sgd", "adam"):
+            raise ValueError(f"inner_opt {cfg.inner_opt!r}: 'sgd' or 'adam'")
+        self.adam = cfg.inner_opt == "adam"
+        self.hp_adam = (cfg.inner_lr, cfg.adam_b1, cfg.adam_b2, cfg.adam_eps, 0.0)
         Tn = self.T * self.n
         # theta_0..theta_K, b_1..b_K, g_0..g_{K-1}; conv-bias slices of g stay 0
         self.theta = [torch.empty(Tn, device=dev) for _ in range(self.K + 1)]
         self.b = [None] + [torch.empty(Tn, device=dev) for _ in range(self.K)]
+        if self.adam:  # Adam inner loop: m, v per step (step 0: zero state = NULL)
+            self.mu = [None] + [torch.empty(Tn, device=dev) for _ in range(self.K)]
+            self.nu = [None] + [torch.empty(Tn, device=dev) for _ in range(self.K)]
+            self.mu_bar = torch.empty(Tn, device=dev)
+            self.nu_bar = torch.empty(Tn, device=dev)
         self.g = [torch.zeros(Tn, device=dev) for _ in range(self.K)]
         self.theta_bar = torch.zeros(Tn, device=dev)
         self.b_bar = torch.empty(Tn, device=dev)
@@ -289,15 +298,28 @@ class ExplicitMaml:
         torch.index_select(phi.reshape(-1), 0, self.bcast, out=self.theta[0])
         N.net_im2col3x3(T, self.Bs, HW, HW, self.xs, self.cols1_s)
         N.net_im2col3x3(T, self.Bq, HW, HW, self.xq, self.cols1_q)
+        F32, CD = L.OPT_F32, L.OPT_COMPUTE_DEFAULT
         for k in range(K):
             self._grad(self.theta[k], self.cols1_s, self.labels_s, self.acts[k], self.g[k])
-            L.opt_sgd_fwd(self.tree, self.hp, L.OPT_F32, L.OPT_COMPUTE_DEFAULT, self.g[k],
-                          self.b[k], None, self.b[k + 1], self.theta[k], self.theta[k + 1])
+            if self.adam:  # (u, m', v') = Adam_t(g, m, v), t = k + 1; theta' = theta + u
+                L.opt_adam_fwd(self.tree, k + 1, self.hp_adam, F32, CD, self.g[k], self.mu[k],
+                               self.nu[k], None, self.mu[k + 1], self.nu[k + 1], self.theta[k],
+                               self.theta[k + 1])
+            else:
+                L.opt_sgd_fwd(self.tree, self.hp, F32, CD, self.g[k], self.b[k], None,
+                              self.b[k + 1], self.theta[k], self.theta[k + 1])
         self._grad(self.theta[K], self.cols1_q, self.labels_q, self.acts_q, self.theta_bar)
         for k in range(K - 1, -1, -1):
-            L.opt_sgd_bwd(self.tree, self.hp, L.OPT_F32, L.OPT_COMPUTE_DEFAULT, self.g[k],
-                          self.b[k], self.theta_bar, self.b_bar if k < K - 1 else None, self.v,
-                          self.b_bar if k > 0 else None)
+            if self.adam:  # Adam VJP (row a4): v = g_bar; m_bar, v_bar carried backwards
+                last, first = k == K - 1, k == 0
+                L.opt_adam_bwd(self.tree, k + 1, self.hp_adam, F32, CD, self.g[k], self.mu[k],
+                               self.nu[k], self.theta_bar, None if last else self.mu_bar,
+                               None if last else self.nu_bar, self.v,
+                               None if first else self.mu_bar, None if first else self.nu_bar)
+            else:
+                L.opt_sgd_bwd(self.tree, self.hp, F32, CD, self.g[k], self.b[k], self.theta_bar,
+                              self.b_bar if k < K - 1 else None, self.v,
+                              self.b_bar if k > 0 else None)
             self._hvp(self.theta[k], self.g[k], self.acts[k], self.v, self.theta_bar)
         N.net_task_sum(T, len(CONV4_SHAPES), self.h_off, self.d_off, self.theta_bar, self.mg)
         return self.mg, self.acts_q.loss.sum()

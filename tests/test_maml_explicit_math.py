@@ -197,3 +197,104 @@ def test_dropping_a_term_is_detected(term):
     err = max(float((a - r).abs().max()) for a, r in zip(got, ref))
     scale = max(float(r.abs().max()) for r in ref)
     assert err > 1e-5 * scale, (term, err, scale)
+
+
+# ------------------------------------------------ Adam inner loop (inner_opt="adam")
+B1, B2, AEPS = 0.9, 0.999, 1e-8
+
+
+def adam_step(g, m, v, t, lr):
+    """One Adam step (bias-corrected, eps outside the sqrt: reading Z1)."""
+    m1 = B1 * m + (1 - B1) * g
+    v1 = B2 * v + (1 - B2) * g * g
+    u = -lr * (m1 / (1 - B1 ** t)) / (torch.sqrt(v1 / (1 - B2 ** t)) + AEPS)
+    return u, m1, v1
+
+
+BIAS = [4 * b + 1 for b in range(BLOCKS)]  # conv biases: inert (N5), held constant here
+
+
+def ref_net_nb(params, x):
+    """ref_net without the (inert) conv biases: with an Adam inner loop their
+    exactly-zero gradients would put sqrt(0)'s infinite slope (times 0) into
+    autograd's second derivative -- the 0/0 the library resolves by reading Z6."""
+    return ref_net([None if i in BIAS else p for i, p in enumerate(params)], x)
+
+
+def ref_meta_grad_adam(phi, xs, ys, xq, yq, K, lr):
+    phi = [p.clone().requires_grad_(i not in BIAS) for i, p in enumerate(phi)]
+    theta = phi
+    m = [torch.zeros_like(p) for p in phi]
+    v = [torch.zeros_like(p) for p in phi]
+    live = [i for i in range(len(phi)) if i not in BIAS]
+    for k in range(K):
+        gl = torch.autograd.grad(F.cross_entropy(ref_net_nb(theta, xs), ys),
+                                 [theta[i] for i in live], create_graph=True)
+        grads = [torch.zeros_like(p) for p in phi]
+        for i, g in zip(live, gl):
+            grads[i] = g
+        outs = [adam_step(g, mm, vv, k + 1, lr) if i in live else (torch.zeros_like(g), mm, vv)
+                for i, (g, mm, vv) in enumerate(zip(grads, m, v))]
+        theta = [t + o[0] for t, o in zip(theta, outs)]
+        m, v = [o[1] for o in outs], [o[2] for o in outs]
+    gq = torch.autograd.grad(F.cross_entropy(ref_net_nb(theta, xq), yq), [phi[i] for i in live])
+    out = [torch.zeros_like(p) for p in phi]
+    for i, g in zip(live, gq):
+        out[i] = g.detach()
+    return out
+
+
+def explicit_meta_grad_adam(phi, xs, ys, xq, yq, K, lr):
+    """The explicit schedule with an Adam inner loop: forward steps with saved
+    (g, m, v); reverse: the Adam VJP (here torch.func.vjp of adam_step, an
+    independent derivation from the kernels) then θ̄ += H_k ḡ."""
+    from torch.func import vjp
+
+    thetas, grads, saved = [list(phi)], [], []
+    ms, vs = [[torch.zeros_like(p) for p in phi]], [[torch.zeros_like(p) for p in phi]]
+    for k in range(K):
+        g, S, _ = grad_pass(thetas[-1], xs, ys)
+        grads.append(g)
+        saved.append(S)
+        outs = [adam_step(gg, mm, vv, k + 1, lr) for gg, mm, vv in zip(g, ms[-1], vs[-1])]
+        thetas.append([t + o[0] for t, o in zip(thetas[-1], outs)])
+        ms.append([o[1] for o in outs])
+        vs.append([o[2] for o in outs])
+    theta_bar, _, _ = grad_pass(thetas[-1], xq, yq)
+    m_bar = [torch.zeros_like(p) for p in phi]
+    v_bar = [torch.zeros_like(p) for p in phi]
+    for k in range(K - 1, -1, -1):
+        gb, mb, vb = [], [], []
+        for i in range(len(phi)):
+            if i in BIAS:  # exact-zero gradient and state: the Z6 convention gives 0
+                gb.append(torch.zeros_like(phi[i]))
+                mb.append(torch.zeros_like(phi[i]))
+                vb.append(torch.zeros_like(phi[i]))
+                continue
+            _, f = vjp(lambda g_, m_, v_: adam_step(g_, m_, v_, k + 1, lr),
+                       grads[k][i], ms[k][i], vs[k][i])
+            a, b, c = f((theta_bar[i], m_bar[i], v_bar[i]))
+            gb.append(a)
+            mb.append(b)
+            vb.append(c)
+        m_bar, v_bar = mb, vb
+        hv = hvp(thetas[k], saved[k], grads[k], gb, ys)
+        theta_bar = [tb + h for tb, h in zip(theta_bar, hv)]
+    return theta_bar
+
+
+@pytest.mark.parametrize("K,seed", [(1, 10), (3, 11)])
+def test_explicit_schedule_adam_inner_equals_autograd_maml(K, seed):
+    gen = torch.Generator().manual_seed(seed)
+    phi = make_params(gen)
+    xs = torch.randn(2 * WAYS, 1, HW, HW, generator=gen, dtype=torch.float64)
+    xq = torch.randn(3 * WAYS, 1, HW, HW, generator=gen, dtype=torch.float64)
+    ys = torch.arange(WAYS).repeat_interleave(2)
+    yq = torch.arange(WAYS).repeat_interleave(3)
+    ref = ref_meta_grad_adam(phi, xs, ys, xq, yq, K, 0.01)
+    got = explicit_meta_grad_adam(phi, xs, ys, xq, yq, K, 0.01)
+    scale = max(float(r.abs().max()) for r in ref)
+    for i, (a, r) in enumerate(zip(got, ref)):
+        if i < 16 and i % 4 == 1:  # conv bias: inert
+            continue
+        torch.testing.assert_close(a, r, rtol=1e-7, atol=1e-10 * scale, msg=f"leaf {i}")
