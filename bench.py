@@ -430,6 +430,8 @@ def main():
                     help="MAML task-batched network form (maml.conv4_forward_tasks)")
     ap.add_argument("--maml-streams", type=int, default=8,
                     help="MAML (--maml-impl streams): parallel task branches in the graph")
+    ap.add_argument("--maml-inner", default="sgd", choices=["sgd", "adam"],
+                    help="MAML inner optimizer (explicit step): SGD momentum (C4) or Adam")
     ap.add_argument("--maml-serial", action="store_true",
                     help="MAML (--maml-impl explicit): no side stream (A/B of the concurrency)")
     ap.add_argument("--maml-outer", default="adam", choices=["adam", "peer"],
@@ -943,7 +945,8 @@ def measure_maml(args, dev, rank, world, steps=None):
     from paper_2211_06934_b200 import _lib as L
     from paper_2211_06934_b200 import maml
 
-    cfg = maml.MamlConfig(tasks=args.tasks, net=args.maml_net)
+    cfg = maml.MamlConfig(tasks=args.tasks, net=args.maml_net, inner_opt=args.maml_inner,
+                          inner_lr=0.1 if args.maml_inner == "sgd" else 0.01)
     phi = maml.init_params(0, dev)
     inner = maml.FusedSgdInner(maml.sizes_of(maml.CONV4_SHAPES), dev, cfg)
     if args.maml_outer == "peer":  # all-reduce fused into the outer step (peer memory)
@@ -991,7 +994,8 @@ def measure_maml(args, dev, rank, world, steps=None):
            "n_gpus": world, "steps": steps, "warmup": args.warmup,
            "ms_per_step": round(ms / steps, 3), "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded 5-way tasks)",
-           "config": {"workload": "C4 MAML 4-conv64, 5-way 5-shot 15-query, 5 inner SGD-mom steps",
+           "config": {"workload": ("C4 MAML 4-conv64, 5-way 5-shot 15-query, 5 inner "
+                                   + ("SGD-mom" if cfg.inner_opt == "sgd" else "Adam") + " steps"),
                       "tasks": cfg.tasks,
                       "parallelism": (f"task-sharded x{world}, " + (
                           "all-reduce fused into the outer step (peer memory)"
