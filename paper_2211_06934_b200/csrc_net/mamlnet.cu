@@ -858,7 +858,22 @@ __global__ void __launch_bounds__(256, 6) bnpool_jvp_kernel(
   const float* xdg = xd + g * q.n;
   const float m = mean[g], r = rstd[g];
   double v[2] = {0.0, 0.0};
-  for (int i = es.lo + threadIdx.x; i < es.hi; i += blockDim.x) {
+  // 16-byte loads over the 4-aligned middle of the slice, scalar ends
+  const bool al = (((uintptr_t)xg | (uintptr_t)xdg) & 15) == 0;
+  int va = al ? min((es.lo + 3) & ~3, es.hi) : es.hi, vb = al ? max(es.hi & ~3, va) : es.hi;
+  for (int i4 = (va >> 2) + threadIdx.x; i4 < (vb >> 2); i4 += blockDim.x) {
+    const float4 t = reinterpret_cast<const float4*>(xdg)[i4];
+    const float4 x4 = reinterpret_cast<const float4*>(xg)[i4];
+    v[0] += (double)t.x + (double)t.y + (double)t.z + (double)t.w;
+    v[1] += (double)t.x * (double)((x4.x - m) * r) + (double)t.y * (double)((x4.y - m) * r) +
+            (double)t.z * (double)((x4.z - m) * r) + (double)t.w * (double)((x4.w - m) * r);
+  }
+  for (int i = es.lo + threadIdx.x; i < va; i += blockDim.x) {
+    const float t = xdg[i];
+    v[0] += (double)t;
+    v[1] += (double)t * (double)((xg[i] - m) * r);
+  }
+  for (int i = vb + threadIdx.x; i < es.hi; i += blockDim.x) {
     const float t = xdg[i];
     v[0] += (double)t;
     v[1] += (double)t * (double)((xg[i] - m) * r);
