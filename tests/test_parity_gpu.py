@@ -442,14 +442,17 @@ def test_c2_full_size_sampled_rmsprop_sgd(L, kind, bf16):
     s1 = torch.empty(n, dtype=torch.bfloat16 if bf16 else torch.float32, device=DEV)
     dg, ds = torch.empty_like(g), torch.empty_like(g)
     sd = 1 if bf16 else 0
+    ws = tree.workspace(DEV)
     if kind == "rmsprop":
         hp = (1e-2, 0.99, 1e-8)
+        dhp = torch.empty(3, dtype=torch.float64, device=DEV)
         L.opt_rmsprop_fwd(tree, hp, sd, 0, g, st, u, s1)
-        L.opt_rmsprop_bwd(tree, hp, sd, 0, g, st, du, ds1, dg, ds)
+        L.opt_rmsprop_bwd(tree, hp, sd, 0, g, st, du, ds1, dg, ds, dhp, None, ws)
     else:
         hp = (0.1, 0.9, True)
+        dhp = torch.empty(2, dtype=torch.float64, device=DEV)
         L.opt_sgd_fwd(tree, hp, sd, 0, g, st, u, s1)
-        L.opt_sgd_bwd(tree, hp, sd, 0, g, st, du, ds1, dg, ds)
+        L.opt_sgd_bwd(tree, hp, sd, 0, g, st, du, ds1, dg, ds, dhp, None, ws)
     idx = np.sort(np.random.default_rng(1).choice(n, 1 << 16, replace=False))
     sg, sst = x["g"][idx], st_h[idx]
     sdu = x["du"][idx]
@@ -471,6 +474,17 @@ def test_c2_full_size_sampled_rmsprop_sgd(L, kind, bf16):
         assert_close("state'", oracle.bf16_to_f64(s1h), rs1, rtol=1e-2, atol=0)
     else:
         check("state'", s1h, rs1, mag["v1" if kind == "rmsprop" else "b1"], 1)
+    # global hyper-gradient sums over all 11.7M elements vs the full oracle
+    # sum (bar: the oracle's per-element magnitude twin summed, as for Adam)
+    oracle.set_num_threads(0)
+    if kind == "rmsprop":
+        full = oracle.rmsprop_vjp(x["g"], st_h, x["du"], x["dv1"], *hp, state_bf16=bf16)
+        fmag = oracle.rmsprop_mag(x["g"], st_h, x["du"], x["dv1"], *hp, state_bf16=bf16)
+    else:
+        full = oracle.sgd_vjp(x["g"], st_h, x["du"], x["dm1"], *hp, state_bf16=bf16)
+        fmag = oracle.sgd_mag(x["g"], st_h, x["du"], x["dm1"], *hp, state_bf16=bf16)
+    oracle.set_num_threads(1)
+    assert_sum_close("dhp", host(dhp), full["dhp"], np.maximum(full["dhp_abs"], fmag["dhp"]))
 
 
 # ------------------------------------------------- beyond 32-bit indexing
