@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define MAMLNET_ABI_VERSION 2
+#define MAMLNET_ABI_VERSION 3
 #define NET_OK 0
 #define NET_EINVAL 1
 #define NET_ECUDA 3
@@ -67,6 +67,16 @@ int net_col2im3x3(int64_t G, int64_t B, int64_t H, int64_t W, const float* cols,
 int net_bnpool_fwd(int64_t G, int64_t B, int64_t H, int64_t W, const float* x,
                    const float* gamma, const float* beta, double eps, float* out, uint8_t* code,
                    float* mean, float* rstd, void* stream);
+
+/* net_bnpool_fwd that also writes the next convolution's input columns:
+ * cols [G, 9, B, H/2, W/2] = net_im2col3x3 of `out` (ABI v3; one launch
+ * instead of two on the forward chain). Only positions whose source lies
+ * inside the pooled map are written; the caller keeps the others (the
+ * padding taps) zero, e.g. by zero-filling the buffer once. cols must not
+ * be NULL. */
+int net_bnpool_fwd_cols(int64_t G, int64_t B, int64_t H, int64_t W, const float* x,
+                        const float* gamma, const float* beta, double eps, float* out,
+                        uint8_t* code, float* mean, float* rstd, float* cols, void* stream);
 
 /* VJP of net_bnpool_fwd. dy = the pooled cotangent dp routed to each window's
  * maximum (zero elsewhere and for inactive windows);
@@ -135,6 +145,14 @@ int net_bnpool_jvp(int64_t G, int64_t B, int64_t H, int64_t W, const float* x, c
                    const float* gamma, const float* gd, const float* bd, const uint8_t* code,
                    const float* mean, const float* rstd, float* outd, float* s1, float* s2,
                    void* stream);
+
+/* net_bnpool_jvp that also writes cols = net_im2col3x3 of `outd` (the next
+ * convolution's tangent columns), with net_bnpool_fwd_cols' convention:
+ * padding taps are not written (kept zero by the caller). ABI v3. */
+int net_bnpool_jvp_cols(int64_t G, int64_t B, int64_t H, int64_t W, const float* x,
+                        const float* xd, const float* gamma, const float* gd, const float* bd,
+                        const uint8_t* code, const float* mean, const float* rstd, float* outd,
+                        float* s1, float* s2, float* cols, void* stream);
 
 /* JVP of net_bnpool_bwd at (dp, x, gamma) along (dpd, xd, gd) (gd nullable),
  * given the backward's dgamma/dbeta and s1/s2 of net_bnpool_jvp for the same

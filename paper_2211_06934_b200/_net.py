@@ -20,7 +20,7 @@ NET_OK = 0
 EXPORTS = ["net_im2col3x3", "net_col2im3x3", "net_bnpool_fwd", "net_bnpool_bwd",
            "net_bnpool_bwd2", "net_gemm_nt_workspace_bytes", "net_gemm_nt",
            "net_gemm_nt2_workspace_bytes", "net_gemm_nt2",  "net_bnpool_jvp",
-           "net_bnpool_bwd_jvp", "net_fc_xent", "net_fc_xent_jvp", "net_task_sum",
+           "net_bnpool_bwd_jvp", "net_bnpool_fwd_cols", "net_bnpool_jvp_cols", "net_fc_xent", "net_fc_xent_jvp", "net_task_sum",
            "net_last_error",
            "net_abi_version", "net_launch_count"]
 
@@ -34,6 +34,8 @@ def _load():
     L.net_im2col3x3.argtypes = [i64] * 4 + [P, P, P]
     L.net_col2im3x3.argtypes = [i64] * 4 + [P, P, P]
     L.net_bnpool_fwd.argtypes = [i64] * 4 + [P, P, P, D] + [P] * 4 + [P]
+    L.net_bnpool_fwd_cols.argtypes = [i64] * 4 + [P, P, P, D] + [P] * 5 + [P]
+    L.net_bnpool_jvp_cols.argtypes = [i64] * 4 + [P] * 12 + [P]
     L.net_bnpool_bwd.argtypes = [i64] * 4 + [P] * 9 + [P]
     L.net_bnpool_bwd2.argtypes = [i64] * 4 + [P] * 14 + [P]
     L.net_gemm_nt_workspace_bytes.argtypes = [i64] * 4
@@ -48,9 +50,9 @@ def _load():
     L.net_fc_xent.argtypes = [i64] * 4 + [P] * 9 + [P]
     L.net_fc_xent_jvp.argtypes = [i64] * 4 + [P] * 10 + [P]
     L.net_task_sum.argtypes = [i64, i64, P, P, P, P, P]
-    for n in ("net_gemm_nt2", "net_bnpool_jvp", "net_bnpool_bwd_jvp", "net_fc_xent",
+    for n in ("net_gemm_nt2", "net_bnpool_jvp", "net_bnpool_bwd_jvp", "net_bnpool_fwd_cols", "net_bnpool_jvp_cols", "net_fc_xent",
               "net_fc_xent_jvp", "net_task_sum", "net_gemm_nt", "net_im2col3x3", "net_col2im3x3", "net_bnpool_fwd", "net_bnpool_bwd",
-              "net_bnpool_bwd2", "net_abi_version"):
+              "net_bnpool_bwd2", "net_abi_version", "net_bnpool_fwd_cols", "net_bnpool_jvp_cols"):
         getattr(L, n).restype = ctypes.c_int
     L.net_last_error.restype = ctypes.c_char_p
     L.net_launch_count.restype = i64
@@ -76,6 +78,13 @@ def net_col2im3x3(G, B, H, W, cols, dh, stream=None):
 def net_bnpool_fwd(G, B, H, W, x, gamma, beta, eps, out, code, mean, rstd, stream=None):
     _check(lib.net_bnpool_fwd(G, B, H, W, _ptr(x), _ptr(gamma), _ptr(beta), float(eps), _ptr(out),
                               _ptr(code), _ptr(mean), _ptr(rstd), _stream(stream)))
+
+
+def net_bnpool_fwd_cols(G, B, H, W, x, gamma, beta, eps, out, code, mean, rstd, cols,
+                        stream=None):
+    _check(lib.net_bnpool_fwd_cols(G, B, H, W, _ptr(x), _ptr(gamma), _ptr(beta), float(eps),
+                                   _ptr(out), _ptr(code), _ptr(mean), _ptr(rstd), _ptr(cols),
+                                   _stream(stream)))
 
 
 def net_bnpool_bwd(G, B, H, W, dp, code, x, gamma, mean, rstd, dx, dgamma, dbeta, stream=None):
@@ -115,6 +124,13 @@ def net_bnpool_jvp(G, B, H, W, x, xd, gamma, gd, bd, code, mean, rstd, outd, s1,
     _check(lib.net_bnpool_jvp(G, B, H, W, _ptr(x), _ptr(xd), _ptr(gamma), _ptr(gd), _ptr(bd),
                               _ptr(code), _ptr(mean), _ptr(rstd), _ptr(outd), _ptr(s1), _ptr(s2),
                               _stream(stream)))
+
+
+def net_bnpool_jvp_cols(G, B, H, W, x, xd, gamma, gd, bd, code, mean, rstd, outd, s1, s2, cols,
+                        stream=None):
+    _check(lib.net_bnpool_jvp_cols(G, B, H, W, _ptr(x), _ptr(xd), _ptr(gamma), _ptr(gd),
+                                   _ptr(bd), _ptr(code), _ptr(mean), _ptr(rstd), _ptr(outd),
+                                   _ptr(s1), _ptr(s2), _ptr(cols), _stream(stream)))
 
 
 def net_bnpool_bwd_jvp(G, B, H, W, dp, dpd, code, x, xd, gamma, gd, mean, rstd, dgamma, dbeta,

@@ -30,6 +30,7 @@ int fail(const char* msg) {
   g_err = msg;
   return NET_EINVAL;
 }
+int fail(const std::string& msg) { return fail(msg.c_str()); }
 
 int launched() {
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -117,6 +118,25 @@ struct Geo {  // one group's geometry
     return b * HW + 2 * y2 * W + 2 * x2;
   }
   __device__ __forceinline__ int off(int k) const { return (k >> 1) * W + (k & 1); }
+  // Pooled value o at pooled index p written into the 3x3 / padding-1 im2col
+  // of the pooled map (cols9 = this group's [9, B, H2, W2] block): tap (i, j)
+  // of output position (y2-i+1, x2-j+1) reads source (y2, x2). Positions
+  // whose source lies outside the map are not written (kept zero by the caller).
+  __device__ __forceinline__ void scatter_cols(float* __restrict__ cols9, int p, float o) const {
+    const int b = (int)dP2.div(p), r = p - b * P2, y2 = (int)dW2.div(r), x2 = r - y2 * W2;
+    float* base = cols9 + b * P2;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int y = y2 - i + 1;
+      if ((unsigned)y >= (unsigned)H2) continue;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int x = x2 - j + 1;
+        if ((unsigned)x >= (unsigned)W2) continue;
+        __stcs(base + (int64_t)(3 * i + j) * np + y * W2 + x, o);
+      }
+    }
+  }
   // j-th element outside every window (odd last column, then odd last row)
   __device__ __forceinline__ int left(int j) const {
     const int b = (int)dL.div(j), r = j - b * L;
@@ -246,7 +266,8 @@ __device__ __forceinline__ void cluster_sum(double (&v)[K], double* sm, double* 
 __global__ void __launch_bounds__(256, 6) bnpool_fwd_kernel(int B, int H, int W, const float* __restrict__ x,
                                   const float* __restrict__ gamma, const float* __restrict__ beta,
                                   double eps, float* __restrict__ out, uint8_t* __restrict__ code,
-                                  float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+                                  float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                  float* __restrict__ cols) {
   __shared__ double sm[32 * 2 + 2];
   __shared__ double part[2];
   const Geo q(B, H, W);
@@ -274,6 +295,7 @@ __global__ void __launch_bounds__(256, 6) bnpool_fwd_kernel(int B, int H, int W,
   const float s = ga * r;  // z = s*(x - m) + be
   float* og = out + g * q.np;
   uint8_t* cg = code + g * q.np;
+  float* c9 = cols ? cols + g * 9 * (int64_t)q.np : nullptr;
   for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
     const int e0 = q.elem0(p);
     float best = s * (xg[e0] - m) + be;
@@ -287,6 +309,7 @@ __global__ void __launch_bounds__(256, 6) bnpool_fwd_kernel(int B, int H, int W,
     const bool on = best > 0.f;
     og[p] = on ? best : 0.f;
     cg[p] = on ? (uint8_t)kb : kOff;
+    if (c9) q.scatter_cols(c9, p, on ? best : 0.f);
   }
 }
 
@@ -500,7 +523,8 @@ struct ImgSlice {
 __global__ void bnpool_fwd_smem(int B, int H, int W, const float* __restrict__ x,
                                 const float* __restrict__ gamma, const float* __restrict__ beta,
                                 double eps, float* __restrict__ out, uint8_t* __restrict__ code,
-                                float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+                                float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                float* __restrict__ cols) {
   extern __shared__ float xs[];
   __shared__ double sm[32 * 2 + 2];
   __shared__ double part[2];
@@ -532,6 +556,7 @@ __global__ void bnpool_fwd_smem(int B, int H, int W, const float* __restrict__ x
   const float s = ga * r;
   float* og = out + g * q.np;
   uint8_t* cg = code + g * q.np;
+  float* c9 = cols ? cols + g * 9 * (int64_t)q.np : nullptr;
   for (int p = is.b0 * q.P2 + threadIdx.x; p < is.b1 * q.P2; p += blockDim.x) {
     const int e = q.elem0(p) - e0;
     const float x0 = xs[e], x1 = xs[e + 1], x2 = xs[e + W], x3 = xs[e + W + 1];
@@ -546,6 +571,7 @@ __global__ void bnpool_fwd_smem(int B, int H, int W, const float* __restrict__ x
     const bool on = best > 0.f;
     og[p] = on ? best : 0.f;
     cg[p] = on ? (uint8_t)kb : kOff;
+    if (c9) q.scatter_cols(c9, p, on ? best : 0.f);
   }
 }
 
@@ -846,7 +872,7 @@ __global__ void __launch_bounds__(256, 6) bnpool_jvp_kernel(
     const float* __restrict__ gamma, const float* __restrict__ gd, const float* __restrict__ bd,
     const uint8_t* __restrict__ code, const float* __restrict__ mean,
     const float* __restrict__ rstd, float* __restrict__ outd, float* __restrict__ s1,
-    float* __restrict__ s2) {
+    float* __restrict__ s2, float* __restrict__ cols) {
   __shared__ double sm[32 * 2 + 2];
   __shared__ double part[2];
   const Geo q(B, H, W);
@@ -887,6 +913,7 @@ __global__ void __launch_bounds__(256, 6) bnpool_jvp_kernel(
   const float ga = gamma[g], gdd = gd ? gd[g] : 0.f, bdd = bd ? bd[g] : 0.f;
   const uint8_t* cg = code + g * q.np;
   float* og = outd + g * q.np;
+  float* c9 = cols ? cols + g * 9 * (int64_t)q.np : nullptr;
   for (int p = ps.lo + threadIdx.x; p < ps.hi; p += blockDim.x) {
     const uint8_t c = cg[p];
     float o = 0.f;
@@ -897,6 +924,7 @@ __global__ void __launch_bounds__(256, 6) bnpool_jvp_kernel(
       o = gdd * xh + ga * xhd + bdd;
     }
     og[p] = o;
+    if (c9) q.scatter_cols(c9, p, o);
   }
 }
 
@@ -1209,20 +1237,36 @@ int net_col2im3x3(int64_t G, int64_t B, int64_t H, int64_t W, const float* cols,
   return launched();
 }
 
-int net_bnpool_fwd(int64_t G, int64_t B, int64_t H, int64_t W, const float* x,
-                   const float* gamma, const float* beta, double eps, float* out, uint8_t* code,
-                   float* mean, float* rstd, void* stream) {
-  if (!geo_ok(G, B, H, W, true)) return fail("net_bnpool_fwd: bad geometry");
-  if (!(eps >= 0.0)) return fail("net_bnpool_fwd: eps must be >= 0");
+static int bnpool_fwd_run(const char* who, int64_t G, int64_t B, int64_t H, int64_t W,
+                          const float* x, const float* gamma, const float* beta, double eps,
+                          float* out, uint8_t* code, float* mean, float* rstd, float* cols,
+                          void* stream) {
+  if (!geo_ok(G, B, H, W, true)) return fail(std::string(who) + ": bad geometry");
+  if (!(eps >= 0.0)) return fail(std::string(who) + ": eps must be >= 0");
   if (G == 0) return NET_OK;
   if (!x || !gamma || !beta || !out || !code || !mean || !rstd)
-    return fail("net_bnpool_fwd: NULL pointer");
+    return fail(std::string(who) + ": NULL pointer");
   size_t sb = 0;
   if (const int kc = ((uintptr_t)x & 15) ? 0 : smem_cluster(G, B, H * W, 1, &sb))
     return launch_clustered(bnpool_fwd_smem, G, kc, sb, (cudaStream_t)stream, (int)B, (int)H,
-                            (int)W, x, gamma, beta, eps, out, code, mean, rstd);
+                            (int)W, x, gamma, beta, eps, out, code, mean, rstd, cols);
   return launch_group_kernel(bnpool_fwd_kernel, G, B * H * W, (cudaStream_t)stream, (int)B,
-                             (int)H, (int)W, x, gamma, beta, eps, out, code, mean, rstd);
+                             (int)H, (int)W, x, gamma, beta, eps, out, code, mean, rstd, cols);
+}
+
+int net_bnpool_fwd(int64_t G, int64_t B, int64_t H, int64_t W, const float* x,
+                   const float* gamma, const float* beta, double eps, float* out, uint8_t* code,
+                   float* mean, float* rstd, void* stream) {
+  return bnpool_fwd_run("net_bnpool_fwd", G, B, H, W, x, gamma, beta, eps, out, code, mean, rstd,
+                        nullptr, stream);
+}
+
+int net_bnpool_fwd_cols(int64_t G, int64_t B, int64_t H, int64_t W, const float* x,
+                        const float* gamma, const float* beta, double eps, float* out,
+                        uint8_t* code, float* mean, float* rstd, float* cols, void* stream) {
+  if (!cols && G > 0) return fail("net_bnpool_fwd_cols: NULL cols");
+  return bnpool_fwd_run("net_bnpool_fwd_cols", G, B, H, W, x, gamma, beta, eps, out, code, mean,
+                        rstd, cols, stream);
 }
 
 int net_bnpool_bwd(int64_t G, int64_t B, int64_t H, int64_t W, const float* dp,
@@ -1335,16 +1379,35 @@ int net_gemm_nt2(int64_t T, int64_t M, int64_t P, int64_t N, const float* A, con
                      workspace_bytes, stream);
 }
 
+static int bnpool_jvp_run(const char* who, int64_t G, int64_t B, int64_t H, int64_t W,
+                          const float* x, const float* xd, const float* gamma, const float* gd,
+                          const float* bd, const uint8_t* code, const float* mean,
+                          const float* rstd, float* outd, float* s1, float* s2, float* cols,
+                          void* stream) {
+  if (!geo_ok(G, B, H, W, true)) return fail(std::string(who) + ": bad geometry");
+  if (G == 0) return NET_OK;
+  if (!x || !xd || !gamma || !code || !mean || !rstd || !outd || !s1 || !s2)
+    return fail(std::string(who) + ": NULL pointer");
+  return launch_group_kernel(bnpool_jvp_kernel, G, B * H * W, (cudaStream_t)stream, (int)B,
+                             (int)H, (int)W, x, xd, gamma, gd, bd, code, mean, rstd, outd, s1, s2,
+                             cols);
+}
+
 int net_bnpool_jvp(int64_t G, int64_t B, int64_t H, int64_t W, const float* x, const float* xd,
                    const float* gamma, const float* gd, const float* bd, const uint8_t* code,
                    const float* mean, const float* rstd, float* outd, float* s1, float* s2,
                    void* stream) {
-  if (!geo_ok(G, B, H, W, true)) return fail("net_bnpool_jvp: bad geometry");
-  if (G == 0) return NET_OK;
-  if (!x || !xd || !gamma || !code || !mean || !rstd || !outd || !s1 || !s2)
-    return fail("net_bnpool_jvp: NULL pointer");
-  return launch_group_kernel(bnpool_jvp_kernel, G, B * H * W, (cudaStream_t)stream, (int)B,
-                             (int)H, (int)W, x, xd, gamma, gd, bd, code, mean, rstd, outd, s1, s2);
+  return bnpool_jvp_run("net_bnpool_jvp", G, B, H, W, x, xd, gamma, gd, bd, code, mean, rstd,
+                        outd, s1, s2, nullptr, stream);
+}
+
+int net_bnpool_jvp_cols(int64_t G, int64_t B, int64_t H, int64_t W, const float* x,
+                        const float* xd, const float* gamma, const float* gd, const float* bd,
+                        const uint8_t* code, const float* mean, const float* rstd, float* outd,
+                        float* s1, float* s2, float* cols, void* stream) {
+  if (!cols && G > 0) return fail("net_bnpool_jvp_cols: NULL cols");
+  return bnpool_jvp_run("net_bnpool_jvp_cols", G, B, H, W, x, xd, gamma, gd, bd, code, mean, rstd,
+                        outd, s1, s2, cols, stream);
 }
 
 int net_bnpool_bwd_jvp(int64_t G, int64_t B, int64_t H, int64_t W, const float* dp,

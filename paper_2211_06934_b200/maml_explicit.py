@@ -64,8 +64,8 @@ class _Acts:
                                                                                range(7))
         for l, H in enumerate(LAYER_H):
             n = B * H * H
-            if l > 0 and with_cols:
-                self.cols[l] = torch.empty(T, LAYER_CIN[l] * 9, n, device=dev)
+            if l > 0 and with_cols:  # zeroed once: fused producers never write the padding taps
+                self.cols[l] = torch.zeros(T, LAYER_CIN[l] * 9, n, device=dev)
             self.y[l] = torch.empty(T, C, n, device=dev)
             self.dy[l] = torch.empty(T, C, n, device=dev)
             H2 = H // 2
@@ -93,6 +93,12 @@ class ExplicitMaml:
             dev = torch.device("cuda", torch.cuda.current_device())
         self.T, self.cfg, self.dev = int(T), cfg, dev
         self.K = int(cfg.inner_steps)
+        # next-layer im2col fused into the norm/pool producers (forward and
+        # tangent) for chains of <= 8 tasks: one launch fewer per layer on the
+        # dependency chain (4 tasks 5.10 -> 4.99 ms, 8: 8.42 -> 8.24, 16 equal);
+        # a 32-task chain keeps the separate float4 im2col (26.6 vs 26.9 ms)
+        # (profiles/r02bf_fused_cols.txt)
+        self.fuse_cols = self.T <= 8
         sizes = sizes_of(CONV4_SHAPES)
         self.n = sum(sizes)
         self.off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
@@ -215,11 +221,15 @@ class ExplicitMaml:
         T, B = self.T, A.B
         A.cols[0] = cols1
         for l, H in enumerate(LAYER_H):
-            if l > 0:
-                N.net_im2col3x3(T * C, B, H, H, A.h[l - 1], A.cols[l])
             torch.bmm(self._w(theta, l), A.cols[l], out=A.y[l])
-            N.net_bnpool_fwd(T * C, B, H, H, A.y[l], self._gamma(theta, l), self._beta(theta, l),
-                             BN_EPS, A.h[l], A.code[l], A.mean[l], A.rstd[l])
+            args = (T * C, B, H, H, A.y[l], self._gamma(theta, l), self._beta(theta, l), BN_EPS,
+                    A.h[l], A.code[l], A.mean[l], A.rstd[l])
+            if l < 3 and self.fuse_cols:  # the next layer's columns from the same launch
+                N.net_bnpool_fwd_cols(*args, A.cols[l + 1])
+            else:
+                N.net_bnpool_fwd(*args)
+                if l < 3:
+                    N.net_im2col3x3(T * C, B, H // 2, H // 2, A.h[l], A.cols[l + 1])
         N.net_fc_xent(T, B, C, WAYS, A.h[3], self.leaf(theta, 16), self.leaf(theta, 17), labels,
                       A.loss, A.prob, self.leaf(g, 16), self.leaf(g, 17), A.dh[3])
         for l in range(3, -1, -1):
@@ -254,14 +264,18 @@ class ExplicitMaml:
                 torch.bmm(self._w(v, l).transpose(1, 2), A.dy[l], out=self.rdc[l])
                 edc[l] = self._mark()
         for l, H in enumerate(LAYER_H):        # forward tangents
-            if l > 0:
-                N.net_im2col3x3(T * C, B, H, H, R.h[l - 1], R.cols[l])
             cur.wait_event(ey[l])
             if l > 0:
                 R.y[l].baddbmm_(self._w(theta, l), R.cols[l])
-            N.net_bnpool_jvp(T * C, B, H, H, A.y[l], R.y[l], self._gamma(theta, l),
-                             self._gamma(v, l), self._beta(v, l), A.code[l], A.mean[l],
-                             A.rstd[l], R.h[l], self.s1[l], self.s2[l])
+            args = (T * C, B, H, H, A.y[l], R.y[l], self._gamma(theta, l), self._gamma(v, l),
+                    self._beta(v, l), A.code[l], A.mean[l], A.rstd[l], R.h[l], self.s1[l],
+                    self.s2[l])
+            if l < 3 and self.fuse_cols:  # tangent columns of the next layer, same launch
+                N.net_bnpool_jvp_cols(*args, R.cols[l + 1])
+            else:
+                N.net_bnpool_jvp(*args)
+                if l < 3:
+                    N.net_im2col3x3(T * C, B, H // 2, H // 2, R.h[l], R.cols[l + 1])
         N.net_fc_xent_jvp(T, B, C, WAYS, A.h[3], R.h[3], self.leaf(theta, 16), self.leaf(v, 16),
                           self.leaf(v, 17), self.labels_s, A.prob, self.leaf(acc, 16),
                           self.leaf(acc, 17), R.dh[3])

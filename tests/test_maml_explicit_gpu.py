@@ -500,3 +500,52 @@ def test_seeded_load_and_serial_schedule_are_bitwise_equal(mx):
     mgb, lb = b.meta_grad(phi)
     torch.cuda.synchronize()
     assert torch.equal(mga, mgb) and torch.equal(la, lb)
+    # next-layer columns fused into the norm/pool launches (chains of <= 8
+    # tasks) or written by a separate im2col: the same values, bitwise
+    assert a.fuse_cols
+    c = mx.ExplicitMaml(T, cfg, DEV)
+    c.fuse_cols = False
+    c.load_seeded(7, [4, 9, 2])
+    mgc, lc = c.meta_grad(phi)
+    torch.cuda.synchronize()
+    assert torch.equal(mga, mgc) and torch.equal(la, lc)
+
+
+@pytest.mark.parametrize("geo", [(2, 64, 25, 28, 28), (1, 64, 75, 14, 14), (2, 64, 5, 7, 7),
+                                 (3, 5, 7, 9, 6), (1, 3, 2, 2, 2), (1, 2, 64, 64, 64)])
+def test_bnpool_fused_columns_equal_separate_im2col(mx, geo):
+    """net_bnpool_fwd_cols / net_bnpool_jvp_cols (ABI v3): the pooled output
+    and tangent are bitwise those of net_bnpool_fwd / net_bnpool_jvp, and the
+    fused columns are bitwise net_im2col3x3 of them (a gather of the same
+    values) -- the padding taps stay as the caller left them (zero)."""
+    from paper_2211_06934_b200 import _net as N
+
+    x, gamma, beta, dp, xd, gd, bd, dpd = _block_case(geo, 33)
+    T, C, B, H, W = geo
+    H2, W2 = H // 2, W // 2
+    xf, gf, bf, code, mean, rstd = _fwd_gpu(N, x, gamma, beta)
+    out = torch.empty(T, C, B, H2, W2, device=DEV)
+    code2 = torch.empty(out.shape, dtype=torch.uint8, device=DEV)
+    mean2, rstd2 = torch.empty(T * C, device=DEV), torch.empty(T * C, device=DEV)
+    cols = torch.zeros(T * C, 9, B, H2, W2, device=DEV)
+    N.net_bnpool_fwd_cols(T * C, B, H, W, xf, gf, bf, EPS, out, code2, mean2, rstd2, cols)
+    ref_out = torch.empty_like(out)
+    N.net_bnpool_fwd(T * C, B, H, W, xf, gf, bf, EPS, ref_out, code, mean, rstd)
+    assert torch.equal(out, ref_out) and torch.equal(code2, code)
+    assert torch.equal(mean2, mean) and torch.equal(rstd2, rstd)
+    ref_cols = torch.full_like(cols, float("nan"))
+    N.net_im2col3x3(T * C, B, H2, W2, ref_out, ref_cols)
+    assert torch.equal(cols, ref_cols)
+    # tangent
+    xdf, gdf, bdf = (t.float().to(DEV).contiguous() for t in (xd, gd, bd))
+    outd, ref_outd = torch.empty_like(out), torch.empty_like(out)
+    s1, s2, r1, r2 = (torch.empty(T * C, device=DEV) for _ in range(4))
+    tcols = torch.zeros_like(cols)
+    N.net_bnpool_jvp_cols(T * C, B, H, W, xf, xdf, gf, gdf, bdf, code, mean, rstd, outd, s1, s2,
+                          tcols)
+    N.net_bnpool_jvp(T * C, B, H, W, xf, xdf, gf, gdf, bdf, code, mean, rstd, ref_outd, r1, r2)
+    assert torch.equal(outd, ref_outd) and torch.equal(s1, r1) and torch.equal(s2, r2)
+    N.net_im2col3x3(T * C, B, H2, W2, ref_outd, ref_cols)
+    assert torch.equal(tcols, ref_cols)
+    with pytest.raises(RuntimeError):
+        N.net_bnpool_fwd_cols(T * C, B, H, W, xf, gf, bf, EPS, out, code2, mean2, rstd2, None)

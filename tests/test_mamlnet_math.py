@@ -380,11 +380,11 @@ def N():
 
 def test_header_symbols_exported(N):
     syms = declared()
-    assert len(syms) == 17
+    assert len(syms) == 19
     assert set(syms) == set(N.EXPORTS)
     for s in syms:
         assert hasattr(N.lib, s)
-    assert N.net_abi_version() == 2
+    assert N.net_abi_version() == 3
 
 
 def test_bad_geometry_rejected_before_launch(N):
