@@ -223,6 +223,42 @@ __device__ __forceinline__ void block_sum(double* acc, double (*sm)[kWarps]) {
   __syncthreads();
 }
 
+// This thread's share of the final sum over nparts partial rows (rows
+// threadIdx.x, +kBlock, +2 kBlock, ... added in that order): four rows' loads
+// are issued before any add, so the last block waits for one L2 round trip
+// per four rows instead of one per row (same order, same bits).
+template <int NH>
+__device__ __forceinline__ void sum_partials(const double* __restrict__ part, int64_t nparts,
+                                             double* s) {
+  int64_t b = threadIdx.x;
+  for (; b + 3 * kBlock < nparts; b += 4 * kBlock) {
+    double t[4][NH];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int k = 0; k < NH; ++k) t[u][k] = __ldcg(&part[(b + u * kBlock) * NH + k]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int k = 0; k < NH; ++k) s[k] += t[u][k];
+  }
+  double t[3][NH];
+  int r = 0;
+#pragma unroll
+  for (int u = 0; u < 3; ++u)
+    if (b + u * kBlock < nparts) {
+#pragma unroll
+      for (int k = 0; k < NH; ++k) t[u][k] = __ldcg(&part[(b + u * kBlock) * NH + k]);
+      r = u + 1;
+    }
+#pragma unroll
+  for (int u = 0; u < 3; ++u)
+    if (u < r) {
+#pragma unroll
+      for (int k = 0; k < NH; ++k) s[k] += t[u][k];
+    }
+}
+
 // Arrival ticket: returns true in every thread of the last block to finish.
 __device__ __forceinline__ bool last_block(unsigned int* counter, unsigned int nblocks) {
   __shared__ bool s_last;
@@ -345,9 +381,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_uniform(const Op op,
 #pragma unroll
       for (int k = 0; k < NH; ++k) s[k] = 0.0;
       const int64_t nparts = (int64_t)gridDim.x + nchunks;  // blocks, then chunks
-      for (int64_t b = threadIdx.x; b < nparts; b += kBlock)
-#pragma unroll
-        for (int k = 0; k < NH; ++k) s[k] += __ldcg(&a.partials[b * NH + k]);
+      sum_partials<NH>(a.partials, nparts, s);
 #if DOPT_TAIL_PROBE
       long long c3 = clock64();
 #endif
@@ -461,9 +495,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_pipe(const Op op,
       double s[NH];
 #pragma unroll
       for (int k = 0; k < NH; ++k) s[k] = 0.0;
-      for (int64_t b = threadIdx.x; b < gridDim.x; b += kBlock)
-#pragma unroll
-        for (int k = 0; k < NH; ++k) s[k] += __ldcg(&a.partials[b * NH + k]);
+      sum_partials<NH>(a.partials, gridDim.x, s);
       block_sum<NH>(s, sm);
       if (threadIdx.x == 0) {
 #pragma unroll
