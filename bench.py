@@ -301,14 +301,17 @@ def time_e2e(args, W, dev):
     ms_serial = timed(serial)
     out = {"serial_ms_per_step": round(ms_serial, 4)}
     if W.sd == 0 and W.n >= 1 << 16 and len(ins) == 6:
-        hs = HostStreamedAdam(W.n, dev, chunks=8, compute=W.compute)
-        hin = {k: h_in[k] for k in IN_KEYS}
-        hout = {k: h_out[k] for k in OUT_KEYS}
+        chunks = int(os.environ.get("E2E_CHUNKS", "12"))
+        hs = HostStreamedAdam(W.n, dev, chunks=chunks, compute=W.compute)
+        hin, hout = HostStreamedAdam.alloc_host(W.n)  # rows of one pinned buffer per direction
+        for k in IN_KEYS:
+            hin[k].copy_(h_in[k])
         ms = timed(lambda: hs.run(hin, hout, STEP_T, HP))
         h2d, d2h = hs.bytes_h2d(), hs.bytes_d2h()
-        how = ("paper_2211_06934_b200.offload.HostStreamedAdam: pinned host inputs/outputs, "
-               "8 chunks, H2D / opt_adam_fwd+bwd / D2H overlapped on 3 streams; all copies "
-               "inside the timed region")
+        how = ("paper_2211_06934_b200.offload.HostStreamedAdam: pinned host inputs/outputs "
+               f"(rows of one buffer per direction), {chunks} chunks, one strided H2D / "
+               "opt_adam_fwd+bwd / one strided D2H per chunk overlapped on 3 streams; all "
+               "copies inside the timed region")
     else:
         ms = ms_serial
         h2d = sum(h_in[k].numel() * h_in[k].element_size() for k in ins)

@@ -287,6 +287,18 @@ def opt_sum_rows(rows, cols, inp, out, stream=None):
     _check(lib.opt_sum_rows(int(rows), int(cols), _ptr(inp), _ptr(out), _stream(stream)))
 
 
+lib.opt_copy_rows.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t,
+                              ctypes.c_size_t, ctypes.c_size_t, ctypes.c_void_p]
+lib.opt_copy_rows.restype = ctypes.c_int
+EXPORTS.append("opt_copy_rows")
+
+
+def opt_copy_rows(dst, dpitch, src, spitch, width_bytes, rows, stream=None):
+    """dst / src: raw addresses (int) or tensors (their data_ptr())."""
+    _check(lib.opt_copy_rows(_ptr(dst), int(dpitch), _ptr(src), int(spitch), int(width_bytes),
+                             int(rows), _stream(stream)))
+
+
 def opt_quadratic_grad(numel, a, theta, phi, g, stream=None):
     _check(lib.opt_quadratic_grad(int(numel), _ptr(a), _ptr(theta), _ptr(phi), _ptr(g),
                                   _stream(stream)))

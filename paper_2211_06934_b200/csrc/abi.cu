@@ -1144,6 +1144,20 @@ int opt_sum_rows(int64_t rows, int64_t cols, const double* in, double* out, void
   return launched(s);
 }
 
+int opt_copy_rows(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width_bytes,
+                  size_t rows, void* stream) {
+  g_err.clear();
+  if (rows == 0 || width_bytes == 0) return OPT_OK;
+  if (!dst || !src) return fail(OPT_EINVAL, "NULL pointer");
+  if (rows > 1 && (width_bytes > dpitch || width_bytes > spitch))
+    return fail(OPT_EINVAL, "width %zu exceeds a pitch (%zu, %zu)", width_bytes, dpitch, spitch);
+  if (rows == 1) dpitch = spitch = width_bytes;
+  cudaError_t e = cudaMemcpy2DAsync(dst, dpitch, src, spitch, width_bytes, rows, cudaMemcpyDefault,
+                                    static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(OPT_ECUDA, "cudaMemcpy2DAsync: %s", cudaGetErrorString(e));
+  return OPT_OK;
+}
+
 int opt_quadratic_grad(int64_t numel, const float* a, const float* theta, const float* phi,
                        float* g, void* stream) {
   g_err.clear();

@@ -113,6 +113,12 @@ def test_rmsprop_sgd_validation(L):
                              None, None, 0) == L.OPT_EINVAL
     assert L.lib.opt_apply_updates(-1, None, None, None, 0) == L.OPT_EINVAL
     assert L.lib.opt_quadratic_grad(8, 0x104, 0x100, 0x100, 0x100, 0) == L.OPT_EALIGN
+    # opt_copy_rows (ABI v6 plumbing): host-side validation, nothing enqueued
+    assert L.lib.opt_copy_rows(None, 64, 0x100, 64, 32, 2, 0) == L.OPT_EINVAL
+    assert L.lib.opt_copy_rows(0x100, 16, 0x200, 64, 32, 2, 0) == L.OPT_EINVAL  # width > dpitch
+    assert L.lib.opt_copy_rows(None, 0, None, 0, 0, 5, 0) == L.OPT_OK  # empty rows
+    assert L.lib.opt_copy_rows(None, 0, None, 0, 64, 0, 0) == L.OPT_OK  # no rows
+    assert L.opt_abi_version() == 6
 
 
 def test_status_strings(L):

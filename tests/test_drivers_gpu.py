@@ -465,10 +465,14 @@ def test_functional_centered_momentum_rmsprop_meta_gradients(pkg):
         torch.testing.assert_close(x, y, rtol=5e-4, atol=1e-5, msg=name)
 
 
-def test_host_streamed_step_equals_device_step(pkg):
+@pytest.mark.parametrize("packed", [False, True])
+def test_host_streamed_step_equals_device_step(pkg, packed):
     """offload.HostStreamedAdam (pinned host arrays, chunked H2D / kernels /
     D2H on three streams) gives the device-resident step's outputs bitwise
-    per element, and the chunk-ordered hyper-gradient sum to rounding."""
+    per element, and the chunk-ordered hyper-gradient sum to rounding --
+    with six separate host arrays per direction, and with the arrays as rows
+    of one buffer (alloc_host(): one opt_copy_rows DMA per chunk and
+    direction)."""
     from paper_2211_06934_b200.offload import HostStreamedAdam, IN_KEYS, OUT_KEYS
 
     leaves = [70000, 4096, 333, 120000]
@@ -476,9 +480,17 @@ def test_host_streamed_step_equals_device_step(pkg):
     x = synth.state_tree(0xF5, leaves)
     hp = (1e-3, 0.9, 0.999, 1e-8, 0.0)
     L = pkg._lib
-    h_in = {k: torch.from_numpy(x[k]).pin_memory() for k in IN_KEYS}
-    h_out = {k: torch.empty(n).pin_memory() for k in OUT_KEYS}
+    if packed:
+        h_in, h_out = HostStreamedAdam.alloc_host(n)
+        for k in IN_KEYS:
+            h_in[k].copy_(torch.from_numpy(x[k]))
+        for k in OUT_KEYS:
+            h_out[k].fill_(float("nan"))
+    else:
+        h_in = {k: torch.from_numpy(x[k]).pin_memory() for k in IN_KEYS}
+        h_out = {k: torch.empty(n).pin_memory() for k in OUT_KEYS}
     hs = HostStreamedAdam(n, DEV, chunks=5)
+    assert (hs._rows([h_in[k] for k in IN_KEYS], n) is not None) == packed
     h_dhp = hs.run(h_in, h_out, 4, hp)
     torch.cuda.synchronize()
     d = {k: dev_f32(x[k]) for k in IN_KEYS}
@@ -499,6 +511,28 @@ def test_host_streamed_step_equals_device_step(pkg):
     for r in rows:
         want += r
     np.testing.assert_array_equal(h_dhp.numpy(), want)
+    # back-to-back calls (the next call's host->device copies may start while
+    # the previous call's results stream out): three more steps on new
+    # gradients, no synchronisation in between; the last one checked
+    # (each call gets its own host input buffers: a host array may not be
+    # rewritten while an enqueued copy still reads it)
+    ins = []
+    for rep in range(3):
+        hi = HostStreamedAdam.alloc_host(n)[0] if packed else {
+            k: torch.empty(n).pin_memory() for k in IN_KEYS}
+        for k in IN_KEYS:
+            hi[k].copy_(h_in[k])
+        hi["g"].mul_((-0.5) ** (rep + 1))
+        ins.append(hi)
+    for hi in ins:
+        hs.run(hi, h_out, 4, hp)
+    torch.cuda.synchronize()
+    d["g"].copy_(ins[-1]["g"])
+    L.opt_adam_fwd(tree, 4, hp, 0, 0, d["g"], d["m"], d["v"], o["u"], o["m1"], o["v1"])
+    L.opt_adam_bwd(tree, 4, hp, 0, 0, d["g"], d["m"], d["v"], d["du"], d["dm1"], d["dv1"],
+                   o["dg"], o["dm"], o["dv"], dhp, None, tree.workspace(DEV))
+    for k in OUT_KEYS:
+        assert torch.equal(h_out[k], o[k].cpu()), k
 
 
 def test_sum_rows_fixed_order(pkg):

@@ -57,13 +57,14 @@ def main():
     res["bidir_floor_ms"] = nbytes / (res["bidir_gbs_each"] * 1e6)
     print(json.dumps(res), flush=True)
     g = torch.Generator(device=dev).manual_seed(0)
-    h_in = {k: torch.randn(N, device=dev, generator=g).abs().cpu().pin_memory() for k in IN_KEYS}
-    h_out = {k: torch.empty(N).pin_memory() for k in OUT_KEYS}
+    # packed host rows (one strided DMA per chunk and direction), as bench.py
+    h_in, h_out = HostStreamedAdam.alloc_host(N)
+    for k in IN_KEYS:
+        h_in[k].copy_(torch.randn(N, device=dev, generator=g).abs())
     alg = 60 * N
-    cands = [dict(chunks=c) for c in (4, 6, 8, 12)]
-    cands += [dict(ramp=r) for r in ((1, 2, 4, 4, 4, 4, 2, 1), (1, 2, 4, 8, 8, 8, 4, 2, 1),
-                                      (1, 3, 6, 6, 6, 3, 1), (1, 2, 3, 4, 4, 4, 4, 3, 2, 1),
-                                      (1, 2, 4, 8, 8, 8, 8, 4, 2, 1), (1, 4, 8, 8, 8, 4, 1))]
+    cands = [dict(chunks=c, slots=sl) for c in (8, 10, 12, 14) for sl in (2, 3, 4, 6)]
+    cands += [dict(ramp=r) for r in ((1, 2, 4, 4, 4, 4, 2, 1), (1, 2, 2, 2, 2, 2, 2, 2, 2, 1),
+                                      (1, 1, 2, 2, 2, 2, 2, 2, 2, 2, 1, 1))]
     for kw in cands:
         hs = HostStreamedAdam(N, dev, **kw)
         ms = timed(lambda: hs.run(h_in, h_out, 10, HP))
