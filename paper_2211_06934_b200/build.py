@@ -46,14 +46,15 @@ def build(force: bool = False, out: str = LIB, defines=(), verbose: bool = False
     return out
 
 
-def build_net(force: bool = False, out: str = NET_LIB, verbose: bool = False) -> str:
-    """Compile csrc_net/mamlnet.cu into ``out``."""
+def build_net(force: bool = False, out: str = NET_LIB, verbose: bool = False,
+              defines=()) -> str:
+    """Compile csrc_net/mamlnet.cu into ``out`` (defines: -D knobs for A/B builds)."""
     srcs = ([NET_SRC, os.path.join(INCLUDE, "mamlnet.h")]
             + glob.glob(os.path.join(os.path.dirname(NET_SRC), "*.cuh")))
-    if (not force and os.path.exists(out)
+    if (not force and not defines and os.path.exists(out)
             and all(os.path.getmtime(s) <= os.path.getmtime(out) for s in srcs)):
         return out
-    cmd = [NVCC] + ARCH + FLAGS + ["-I" + INCLUDE]
+    cmd = [NVCC] + ARCH + FLAGS + ["-I" + INCLUDE] + ["-D" + d for d in defines]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     cmd += ["-o", out, NET_SRC]
