@@ -387,6 +387,31 @@ def meta_grad_explicit(phi, data, cfg: MamlConfig, engine: ExplicitMaml | None =
     return mg.clone(), loss.clone()
 
 
+def _cublas_sm_target(n):
+    """cublasSetSmCountTarget on the current thread's PyTorch cuBLAS handle
+    (n = 0 restores the device's own count); returns False if the library
+    entry point is not available. A heuristics hint only: cuBLAS picks its
+    tile shape / split-K as if the GPU had n SMs."""
+    import ctypes
+    import glob
+    import os
+
+    for cand in ["libcublas.so.12"] + glob.glob(
+            os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cublas", "lib",
+                         "libcublas.so.12")):
+        try:
+            lib = ctypes.CDLL(cand)
+            fn = lib.cublasSetSmCountTarget
+            break
+        except (OSError, AttributeError):
+            continue
+    else:
+        return False
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    fn.restype = ctypes.c_int
+    return fn(ctypes.c_void_p(torch.cuda.current_blas_handle()), int(n)) == 0
+
+
 def default_groups(tasks):
     """Task groups (concurrent graph chains) for a shard of `tasks` tasks,
     from the measured sweep on one B200 (profiles/r02ab_task_groups.txt):
@@ -426,17 +451,29 @@ class ExplicitShard:
                         for _ in self.groups]
         self.phi = torch.zeros(self.engs[0].n, device=device)
         self._load(0)
-        side = torch.cuda.Stream(device)
-        side.wait_stream(torch.cuda.current_stream(device))
-        with torch.cuda.stream(side):
-            for _ in range(warmup):
-                self._body()
-        torch.cuda.current_stream(device).wait_stream(side)
-        n0 = L.opt_launch_count() + N.net_launch_count()
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
-            self.mg, self.loss = self._body()
-        self.launches_per_replay = L.opt_launch_count() + N.net_launch_count() - n0
+        # with >= 4 concurrent chains, cuBLAS sizes each product as if it had
+        # half the GPU (its kernel choices are baked into the graph; the
+        # handle is restored after capture). Measured: 4 tasks 4.99 -> 4.91 ms,
+        # 8: 8.25 -> 8.11 (a quarter of the GPU: 4.91 / 8.69)
+        # (profiles/r02bm_cublas_sm_target.txt)
+        sms = torch.cuda.get_device_properties(device).multi_processor_count
+        self.cublas_sm_target = sms // 2 if G >= 4 else 0
+        hinted = self.cublas_sm_target > 0 and _cublas_sm_target(self.cublas_sm_target)
+        try:
+            side = torch.cuda.Stream(device)
+            side.wait_stream(torch.cuda.current_stream(device))
+            with torch.cuda.stream(side):
+                for _ in range(warmup):
+                    self._body()
+            torch.cuda.current_stream(device).wait_stream(side)
+            n0 = L.opt_launch_count() + N.net_launch_count()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph):
+                self.mg, self.loss = self._body()
+            self.launches_per_replay = L.opt_launch_count() + N.net_launch_count() - n0
+        finally:
+            if hinted:
+                _cublas_sm_target(0)
         # next step's task data, drawn on a side stream while this step's
         # graph replays (input pipelining; bitwise the same draws)
         self.stage = [(torch.empty_like(e.xs), torch.empty_like(e.xq)) for e in self.engs]
