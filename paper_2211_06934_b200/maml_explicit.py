@@ -451,13 +451,13 @@ class ExplicitShard:
                         for _ in self.groups]
         self.phi = torch.zeros(self.engs[0].n, device=device)
         self._load(0)
-        # with >= 4 concurrent chains, cuBLAS sizes each product as if it had
-        # half the GPU (its kernel choices are baked into the graph; the
-        # handle is restored after capture). Measured: 4 tasks 4.99 -> 4.91 ms,
-        # 8: 8.25 -> 8.11 (a quarter of the GPU: 4.91 / 8.69)
-        # (profiles/r02bm_cublas_sm_target.txt)
+        # with concurrent chains, cuBLAS sizes each product as if it had half
+        # the GPU (its kernel choices are baked into the graph; the handle is
+        # restored after capture). Measured: 4 tasks 4.99 -> 4.91 ms, 8: 8.25
+        # -> 8.11, 16 (2 chains): 14.90 -> 14.75 (a quarter of the GPU: 4.91 /
+        # 8.69) (profiles/r02bm_cublas_sm_target.txt)
         sms = torch.cuda.get_device_properties(device).multi_processor_count
-        self.cublas_sm_target = sms // 2 if G >= 4 else 0
+        self.cublas_sm_target = sms // 2 if G >= 2 else 0
         hinted = self.cublas_sm_target > 0 and _cublas_sm_target(self.cublas_sm_target)
         try:
             side = torch.cuda.Stream(device)
