@@ -792,10 +792,13 @@ int cluster_for(int64_t G, int64_t n) {
   // elements the cluster reduction and per-CTA fixed costs outweigh the
   // extra CTAs (measured, explicit MAML step at 4 tasks: 1024 -> 5.46 ms,
   // 2048 -> 5.32, 4096 -> 5.23, no fill splitting -> 5.28; 32 tasks, whose
-  // splits come from the slice cap, unchanged: profiles/r02x_bn_min_slice.txt)
+  // splits come from the slice cap, unchanged: profiles/r02x_bn_min_slice.txt).
+  // With concurrent task chains and the cuBLAS SM hint, 8192 is as fast at
+  // 4 tasks and faster at 8 (8.09 -> 7.97 ms) and 16 (14.75 -> 14.70):
+  // profiles/r02bn_bn_min_slice_8k.txt
   static const int64_t min_slice = [] {
     const char* e = getenv("NET_BN_MIN_SLICE");
-    return e ? (int64_t)atoll(e) : (int64_t)4096;
+    return e ? (int64_t)atoll(e) : (int64_t)8192;
   }();
   const int64_t want = 148 * 8;
   int kc = 1;
