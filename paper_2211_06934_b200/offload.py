@@ -101,16 +101,20 @@ class HostStreamedAdam:
     def bytes_d2h(self):
         return 4 * self.n * len(OUT_KEYS) + self.h_dhp.numel() * 8
 
-    def run(self, host_in, host_out, step, hp):
+    def run(self, host_in, host_out, step, hp, inputs_on_host=False):
         """host_in / host_out: dicts of pinned fp32 CPU tensors of n elements.
-        Enqueues the kernels and the device->host copies ordered after the
-        current stream; the current stream waits for completion at the end.
-        The host->device copies only wait for their staging slot to be free
-        (they read host memory and write this object's slots), so the next
-        call's first chunks stream in while this call's last chunks stream
-        out: back-to-back calls keep both PCIe directions busy."""
+        Enqueues everything ordered after the current stream; the current
+        stream waits for completion at the end. host_in must not be
+        rewritten before the current stream has passed this call.
+
+        inputs_on_host=True declares that host_in was filled by the CPU (not
+        by device work still queued on the current stream): the host->device
+        copies then wait only for their staging slot, so the next call's
+        first chunks stream in while this call's last chunks stream out and
+        back-to-back calls keep both PCIe directions busy."""
         cur = torch.cuda.current_stream(self.dev)
-        for s in (self.s_cmp, self.s_d2h):
+        for s in ((self.s_cmp, self.s_d2h) if inputs_on_host else
+                  (self.s_h2d, self.s_cmp, self.s_d2h)):
             s.wait_stream(cur)
         h2d_done, cmp_done, d2h_done = [], [], []
         rin = self._rows([host_in[k] for k in IN_KEYS], self.n)

@@ -525,9 +525,24 @@ def test_host_streamed_step_equals_device_step(pkg, packed):
         hi["g"].mul_((-0.5) ** (rep + 1))
         ins.append(hi)
     for hi in ins:
-        hs.run(hi, h_out, 4, hp)
+        hs.run(hi, h_out, 4, hp, inputs_on_host=True)
     torch.cuda.synchronize()
     d["g"].copy_(ins[-1]["g"])
+    L.opt_adam_fwd(tree, 4, hp, 0, 0, d["g"], d["m"], d["v"], o["u"], o["m1"], o["v1"])
+    L.opt_adam_bwd(tree, 4, hp, 0, 0, d["g"], d["m"], d["v"], d["du"], d["dm1"], d["dv1"],
+                   o["dg"], o["dm"], o["dv"], dhp, None, tree.workspace(DEV))
+    for k in OUT_KEYS:
+        assert torch.equal(h_out[k], o[k].cpu()), k
+    # default mode: inputs written into host memory by device work still
+    # queued on the current stream (a device->host copy), then run(): the
+    # uploads must wait for it
+    hi = ins[0]
+    g_dev = torch.full((n,), 0.25, device=DEV)
+    torch.cuda._sleep(2_000_000)  # keep the stream busy so an early upload would see stale data
+    hi["g"].copy_(g_dev, non_blocking=True)
+    hs.run(hi, h_out, 4, hp)
+    torch.cuda.synchronize()
+    d["g"].fill_(0.25)
     L.opt_adam_fwd(tree, 4, hp, 0, 0, d["g"], d["m"], d["v"], o["u"], o["m1"], o["v1"])
     L.opt_adam_bwd(tree, 4, hp, 0, 0, d["g"], d["m"], d["v"], d["du"], d["dm1"], d["dv1"],
                    o["dg"], o["dm"], o["dv"], dhp, None, tree.workspace(DEV))

@@ -67,7 +67,7 @@ def main():
                                       (1, 1, 2, 2, 2, 2, 2, 2, 2, 2, 1, 1))]
     for kw in cands:
         hs = HostStreamedAdam(N, dev, **kw)
-        ms = timed(lambda: hs.run(h_in, h_out, 10, HP))
+        ms = timed(lambda: hs.run(h_in, h_out, 10, HP, inputs_on_host=True))
         print(json.dumps({**{k: list(v) if isinstance(v, tuple) else v for k, v in kw.items()},
                           "ms": round(ms, 3), "e2e_gbs": round(alg / ms / 1e6, 1)}), flush=True)
         del hs
