@@ -32,6 +32,11 @@ accumulator or a kernel's `+=` epilogue, so there is no cotangent glue:
 Conv biases feed training-mode batch norms and are inert (reading N5): their
 gradients, tangents and meta-gradients are exactly zero and never touched.
 
+Launch-count and sharing details: chains of <= 8 tasks get
+the next layer's im2col columns from the norm/pool launch itself
+(net_bnpool_fwd_cols / net_bnpool_jvp_cols); a shard of several concurrent
+chains is captured with a cuBLAS SM-count hint of half the GPU.
+
 Layout: the T tasks' parameters are one leaf-major flat buffer (leaf l is a
 [T, size_l] block; conv weight l is [T, 64, Cin*9], the im2col row order),
 activations task-major [T, C, B, H, W] (maml.conv4_forward_tasks' "fused"
