@@ -297,7 +297,7 @@ def _per_task_meta_grads(eng):
     return torch.cat(parts, 1)
 
 
-def _flip_aware_check(eng, data, phi, K, strict=2e-5, min_clean=None):
+def _flip_aware_check(eng, data, phi, K, strict=2e-5, min_clean=None, only=None):
     """Per task of an engine that has just run meta_grad on `data`: if every
     routing decision the fp32 kernels took (ReLU on/off, 2x2 argmax, every
     block, every inner step and the query pass) equals float64's, the
@@ -310,6 +310,8 @@ def _flip_aware_check(eng, data, phi, K, strict=2e-5, min_clean=None):
     per = _per_task_meta_grads(eng)
     errs, flipped = [], []
     for t, (xs, ys, xq, yq) in enumerate(data):
+        if only is not None and t not in only:
+            continue
         codes = []
         if eng.cfg.inner_opt == "adam":
             ref, rloss = ref_meta_grad_adam(leaves64, xs.double(), ys, xq.double(), yq, K,
@@ -437,6 +439,43 @@ def test_explicit_task_batch_vs_independent_float64(mx):
         offs.append(offs[-1] + s)
     for leaf in (1, 5, 9, 13):
         assert not mg[offs[leaf]:offs[leaf + 1]].any()
+
+
+@pytest.mark.parametrize("tasks,check", [(32, tuple(range(32))), (4, (0, 1, 2, 3))])
+def test_bench_shard_vs_independent_float64(mx, tasks, check):
+    """The shards bench.py times, as CUDA graphs with their default task
+    groups: 32 tasks (the 1-GPU C4 step: one chain, separate im2col) and 4
+    tasks (the 8-GPU shard: four single-task chains, fused next-layer
+    columns, captured under the cuBLAS SM-count hint). Seeded outer-step-0
+    data as the bench draws it; every task's meta-gradient and query loss vs
+    the independent float64 MAML (flip-aware, strict 2e-5; at least half the
+    tasks decision-clean), and the shard's meta-gradient equals the
+    fixed-order fold of the per-task slices."""
+    from paper_2211_06934_b200 import maml
+
+    cfg = maml.MamlConfig(tasks=tasks)
+    phi = maml.init_params(0, DEV)
+    shard = mx.ExplicitShard(range(tasks), cfg, DEV)
+    assert len(shard.engs) == mx.default_groups(tasks)
+    mg, loss = shard(phi, range(tasks), 0, cfg)
+    torch.cuda.synchronize()
+    data = [maml.task_data(0, t, DEV) for t in range(tasks)]
+    clean, off = 0, 0
+    for eng in shard.engs:
+        part = data[off:off + eng.T]
+        only = [t - off for t in check if off <= t < off + eng.T]
+        errs, _ = _flip_aware_check(eng, part, phi, cfg.inner_steps, only=only)
+        clean += len(errs)
+        off += eng.T
+    assert clean >= len(check) // 2, clean
+    total = None
+    for eng in shard.engs:  # group order, each group's fold in task order
+        per = _per_task_meta_grads(eng)
+        g = per[0].clone()
+        for t in range(1, eng.T):
+            g += per[t]
+        total = g if total is None else total + g
+    assert torch.equal(total, mg)
 
 
 def test_explicit_equals_autograd_path(mx):
