@@ -550,6 +550,40 @@ def test_host_streamed_step_equals_device_step(pkg, packed):
         assert torch.equal(h_out[k], o[k].cpu()), k
 
 
+def test_host_streamed_c2_bench_config(pkg):
+    """The e2e configuration bench.py times: the C2 tree (11,689,512
+    elements) through HostStreamedAdam with 12 chunks, packed host rows
+    (opt_copy_rows) and back-to-back pipelined calls: every output element
+    bitwise equal to the device-resident fused step, the chunk-ordered
+    hyper-gradient sums equal to the whole-tree launch's to rounding."""
+    from paper_2211_06934_b200.offload import HostStreamedAdam, IN_KEYS, OUT_KEYS
+
+    leaves = synth.RESNET18_LEAVES
+    n = int(sum(leaves))
+    x = synth.state_tree(0xC2, leaves)
+    hp, t = (1e-3, 0.9, 0.999, 1e-8, 0.0), 10
+    L = pkg._lib
+    h_in, h_out = HostStreamedAdam.alloc_host(n)
+    for k in IN_KEYS:
+        h_in[k].copy_(torch.from_numpy(x[k]))
+    hs = HostStreamedAdam(n, DEV, chunks=12)
+    for _ in range(3):
+        h_dhp = hs.run(h_in, h_out, t, hp, inputs_on_host=True)
+    torch.cuda.synchronize()
+    d = {k: dev_f32(x[k]) for k in IN_KEYS}
+    o = {k: torch.empty(n, device=DEV) for k in OUT_KEYS}
+    tree = L.Tree(offsets=synth.offsets_of(leaves), device=DEV)
+    dhp = torch.empty(4, dtype=torch.float64, device=DEV)
+    L.opt_adam_fwd(tree, t, hp, 0, 0, d["g"], d["m"], d["v"], o["u"], o["m1"], o["v1"])
+    L.opt_adam_bwd(tree, t, hp, 0, 0, d["g"], d["m"], d["v"], d["du"], d["dm1"], d["dv1"],
+                   o["dg"], o["dm"], o["dv"], dhp, None, tree.workspace(DEV))
+    for k in OUT_KEYS:
+        assert torch.equal(h_out[k], o[k].cpu()), k
+    full = oracle.adam_vjp(x["g"], x["m"], x["v"], x["du"], x["dm1"], x["dv1"], t, *hp)
+    np.testing.assert_allclose(h_dhp.numpy(), host(dhp), rtol=1e-9,
+                               atol=1e-12 * full["dhp_abs"].max())
+
+
 def test_sum_rows_fixed_order(pkg):
     """opt_sum_rows: column sums in row order, bitwise equal to a sequential
     fp64 sum of the same rows; rows = 0 writes zeros."""
