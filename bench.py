@@ -964,7 +964,7 @@ def measure_maml(args, dev, rank, world, steps=None):
     shard = None
     my_tasks = len(maml.task_range(world, rank, cfg.tasks))
     if args.maml_groups is None:  # measured (profiles/r02aa_*, r02ab_*): concurrent
-        # task-group chains win at <= 16 tasks per rank: 4 -> 4 chains, 8 -> 4, 16 -> 2, 32 -> 1
+        # task-group chains win at <= 16 tasks per rank: 4, 8 and 16 -> 4 chains, 32 -> 1
         from paper_2211_06934_b200.maml_explicit import default_groups
 
         args.maml_groups = default_groups(my_tasks) if args.maml_impl == "explicit" else 1

@@ -419,11 +419,13 @@ def _cublas_sm_target(n):
 
 def default_groups(tasks):
     """Task groups (concurrent graph chains) for a shard of `tasks` tasks,
-    from the measured sweep on one B200 (profiles/r02ab_task_groups.txt):
-    <= 8 tasks -> up to 4 chains, <= 16 -> 2, more -> 1."""
-    if tasks <= 8:
+    from the measured sweeps on one B200 (profiles/r02ab_task_groups.txt;
+    with the cuBLAS SM hint and 8K norm/pool slices, profiles/r02ca_*):
+    <= 16 tasks -> up to 4 chains (16 tasks: 14.47 ms vs 14.72 with 2),
+    more -> 1 (32 tasks: 26.6 ms vs 27.7-27.8 with 2 or 4)."""
+    if tasks <= 16:
         return max(1, min(tasks, 4))
-    return 2 if tasks <= 16 else 1
+    return 1
 
 
 class ExplicitShard:

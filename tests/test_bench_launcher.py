@@ -54,5 +54,5 @@ def test_explicit_maml_default_groups_policy():
     profiles/r02ab_task_groups.txt): the 1/2/4/8-GPU shards of 32 tasks."""
     from paper_2211_06934_b200.maml_explicit import default_groups
 
-    assert [default_groups(t) for t in (32, 16, 8, 4, 2, 1)] == [1, 2, 4, 4, 2, 1]
+    assert [default_groups(t) for t in (32, 16, 8, 4, 2, 1)] == [1, 4, 4, 4, 2, 1]
     assert default_groups(0) == 1
